@@ -1,0 +1,224 @@
+/*
+ * nrrs_gpu.h -- C ABI of the B200 (sm_100a) NRRS per-bounce RRS stage.
+ *
+ * One batched call per depth replaces the per-vertex and serial calls the
+ * reference makes inside trace_frame's RRS decision block
+ * (/root/reference/proj/src/wavefront.cpp:363-411, slot layout :413-425,
+ * compaction :488-497).  Every entry point names the reference interface it
+ * replaces.  Plain pointers and sizes only; no torch or CUDA types appear in the
+ * signatures (streams are passed as void*).
+ *
+ * Conventions:
+ *  - every function returns an nrrs_status; 0 = ok.  EINVAL / ESIZE mirror the
+ *    reference's fail() / std::invalid_argument cases (rrs.cpp:11-12, :37-38,
+ *    wavefront.cpp:146-147, :198-211, encodings.hpp:22-23); ECUDA wraps a CUDA
+ *    error.  nrrs_gpu_last_error() returns the message.
+ *  - "d_" pointers are device pointers, "h_" pointers host pointers.
+ *  - stream-ordered on the context's stream; one context per device per host
+ *    thread; not re-entrant.  There is no CPU fallback: without a CUDA device
+ *    nrrs_gpu_create fails with ECUDA.
+ */
+#ifndef NRRS_GPU_H
+#define NRRS_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NRRS_GPU_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define NRRS_API __attribute__((visibility("default")))
+#else
+#define NRRS_API
+#endif
+
+typedef enum {
+    NRRS_OK = 0,
+    NRRS_EINVAL = 1, /* invalid argument / value the reference rejects with fail() */
+    NRRS_ESIZE = 2,  /* size mismatch (realize_counts, set_weights block sizes) */
+    NRRS_ECUDA = 3,  /* CUDA runtime error or no device */
+    NRRS_ENCCL = 4,  /* reserved: collective failure (multi-rank driver) */
+    NRRS_ESTATE = 5  /* call order: e.g. neural strategy before set_weights */
+} nrrs_status;
+
+/* StrategyKind, rrs.hpp:72-79 (same numbering). */
+typedef enum {
+    NRRS_FIXED = 0,
+    NRRS_THROUGHPUT = 1,
+    NRRS_ADRRS_TREE = 2, /* out of scope (octree cache): EINVAL */
+    NRRS_ADRRS_NN = 3,
+    NRRS_NRRS = 4,
+    NRRS_AID_NRRS = 5
+} nrrs_strategy_kind;
+
+/* RrsVariant, networks.hpp:75 */
+typedef enum { NRRS_VARIANT_NRRS = 0, NRRS_VARIANT_AID = 1 } nrrs_variant;
+
+/* HashGridSpec, hashgrid.hpp:13-22.  features must be 2 and levels*2+16 <= 32. */
+typedef struct {
+    int32_t levels, features, base_resolution, log2_table_size;
+} nrrs_grid_spec;
+
+/* Snapshot parameter blocks as published by NeuralRrs::publish()
+ * (networks.cpp:199-204) or read from an NRRSCK01 checkpoint
+ * (networks.cpp:610-705): flat fp32 theta vectors in the reference's layout
+ * (hash grid [level][entry][feature]; MLP per layer column-major W then bias,
+ * mlp.cpp:7-32).  Host pointers; lengths are checked (ESIZE). */
+typedef struct {
+    int32_t variant;
+    nrrs_grid_spec grid;
+    const float *stat_grid; uint64_t stat_grid_len;
+    const float *stat_mlp;  uint64_t stat_mlp_len;
+    const float *rrs_grid;  uint64_t rrs_grid_len; /* empty for NRRS (networks.cpp:26-35) */
+    const float *rrs_mlp;   uint64_t rrs_mlp_len;
+} nrrs_net_weights;
+
+/* Strategy, rrs.hpp:81-92 */
+typedef struct {
+    int32_t kind;      /* nrrs_strategy_kind */
+    float fixed_value; /* Fixed only */
+} nrrs_strategy;
+
+/* Surface vertices entering the decision at one depth, SoA (the VertexRec
+ * fields the stage reads, wavefront.cpp:46-65).  Vectors are packed xyz / xy
+ * (Eigen Vec3f / Vec2f arrays).  i_pixel is film.i_acc[v.pixel]; pass NULL and
+ * set pixel + i_acc to have the stage gather it (wavefront.cpp:378). */
+typedef struct {
+    const float *p01;       /* [3n] scene-normalized position */
+    const float *wo01;      /* [2n] spherical omega_o in [0,1]^2 */
+    const float *roughness; /* [n] */
+    const float *weight;    /* [3n] path weight w (= t_x) */
+    const float *i_pixel;   /* [3n] or NULL */
+    const uint64_t *path_key; /* [n] */
+    const uint32_t *pixel;  /* [n] (only if i_pixel == NULL) */
+    const float *i_acc;     /* [3 * n_pixels] (only if i_pixel == NULL) */
+} nrrs_vertex_soa;
+
+typedef struct {
+    uint32_t depth;    /* d >= 1; depth 1 pins q = 1 (wavefront.cpp:373-375) */
+    uint32_t n_pixels; /* Npx of the normalization budget (rrs.cpp:8-24) */
+    uint32_t capacity; /* queue capacity; 0 = queue_capacity_for(n_pixels) */
+    nrrs_strategy strategy; /* Mix-Depth gate: assignment[depth-1] (wavefront.cpp:366) */
+    float gain;        /* RateControl::gain() (rrs.hpp:30); applied iff depth >= 2 && adaptive */
+    float eps_div;     /* ADRRS divisor guard (wavefront.cpp:238-243) */
+    uint64_t seed;     /* TraceConfig::seed */
+} nrrs_stage_params;
+
+/* Per-vertex and per-slot outputs (device pointers).  q_norm, q_real and slots
+ * are required; the rest may be NULL. */
+typedef struct {
+    float *q_norm;    /* [n] VertexRec::q_norm (wavefront.cpp:400) */
+    float *q_real;    /* [n] VertexRec::q_real (wavefront.cpp:401) */
+    uint32_t *slots;  /* [2 * capacity] (parent vertex j, child c) per queue slot, slot order */
+    int32_t *k;       /* [n] realized counts (rrs.cpp:35-45) */
+    uint32_t *offset; /* [n] SpawnPlan::offset (wavefront.cpp:141-154) */
+    uint8_t *decided; /* [n] VertexRec::decided */
+    float *q_orig;    /* [n] sanitized raw factor before normalization */
+    float *u;         /* [n] RrsRound uniform */
+} nrrs_stage_out;
+
+/* Scalars of one stage call (FrameReport / SpawnPlan / RateControl inputs). */
+typedef struct {
+    double f_norm;           /* normalize_factors' return value */
+    double sum_q;            /* sum of sanitized raw factors (this rank) */
+    uint64_t total;          /* realized child count S */
+    uint64_t dropped;        /* SpawnPlan::dropped (bias_drop_events) */
+    uint64_t nonfinite;      /* FrameReport::nonfinite_drops increment */
+    uint64_t box_cox_clamps; /* diag::box_cox_clamps increment (encodings.hpp:14-17) */
+    uint32_t spawned;        /* SpawnPlan::spawned = next queue size before compaction */
+    uint32_t overflow;       /* 1 iff dropped > 0: caller does rc.note_overflow() (wavefront.cpp:407-411) */
+} nrrs_stage_result;
+
+typedef struct nrrs_gpu_ctx nrrs_gpu_ctx;
+
+/* ---- context ------------------------------------------------------------ */
+NRRS_API int nrrs_gpu_abi_version(void);
+NRRS_API int nrrs_gpu_create(int device, nrrs_gpu_ctx **out);
+NRRS_API int nrrs_gpu_destroy(nrrs_gpu_ctx *ctx);
+NRRS_API const char *nrrs_gpu_last_error(const nrrs_gpu_ctx *ctx);
+NRRS_API int nrrs_gpu_set_stream(nrrs_gpu_ctx *ctx, void *cuda_stream);
+/* Preallocate per-call scratch for up to max_vertices (no allocation in the hot path after). */
+NRRS_API int nrrs_gpu_reserve(nrrs_gpu_ctx *ctx, uint64_t max_vertices, uint32_t max_capacity);
+/* Count of kernel launches issued by this context since creation (bench evidence). */
+NRRS_API uint64_t nrrs_gpu_launch_count(const nrrs_gpu_ctx *ctx);
+
+/* ---- weights: replaces reading NeuralRrs' snapshot (networks.hpp:147, networks.cpp:276-279) */
+NRRS_API int nrrs_gpu_set_weights(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w);
+
+/* ---- fused stage (1 rank): replaces wavefront.cpp:363-425 for one depth:
+ *   strategy_factor over ns vertices (:368-389), normalize_factors (:390),
+ *   gain (:391), RrsRound uniforms (:393-402), realize_counts (:403-404),
+ *   plan_spawns (:406) and the child slot layout (:421-425). Device buffers.
+ *   h_result may be NULL (fully asynchronous); otherwise the call syncs the stream. */
+NRRS_API int nrrs_gpu_rrs_stage(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *d_v, uint64_t n,
+                       const nrrs_stage_params *p, const nrrs_stage_out *d_out,
+                       nrrs_stage_result *h_result);
+
+/* Same call over HOST buffers (the reference-facing plugin path): copies the
+ * SoA to the device, runs the stage, copies every non-NULL output back.
+ * h_out->slots receives result.spawned records. */
+NRRS_API int nrrs_gpu_rrs_stage_host(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *h_v, uint64_t n,
+                            const nrrs_stage_params *p, const nrrs_stage_out *h_out,
+                            nrrs_stage_result *h_result);
+
+/* ---- tile-sharded stage (multi-rank), two phases per depth:
+ * phase 1: factors + RrsRound uniforms; writes this rank's sum of sanitized
+ *          factors (double) to d_local_sum.  The caller all-gathers it.
+ * phase 2: normalization with F = n_pixels_total / sum_r(d_rank_sums[r]) in
+ *          rank order, gain, counts, local scan and local slot records
+ *          (rank-local parent indices, clipped at p->capacity); writes the
+ *          rank's realized total to d_local_total.  The caller all-gathers the
+ *          totals; the global tail clip is then a count truncation of the
+ *          rank's records (nrrs_gpu_sharded_clip). */
+NRRS_API int nrrs_gpu_stage_factors(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *d_v, uint64_t n,
+                           const nrrs_stage_params *p, const nrrs_stage_out *d_out,
+                           double *d_local_sum);
+NRRS_API int nrrs_gpu_stage_decide(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_stage_params *p,
+                          const double *d_rank_sums, int32_t nranks,
+                          const nrrs_stage_out *d_out, uint64_t *d_local_total);
+/* Host arithmetic of the global clip: base_r = sum of totals of ranks < rank;
+ * rank keeps min(total_r, cap - min(cap, base_r)) records. */
+NRRS_API int nrrs_gpu_sharded_clip(const uint64_t *h_rank_totals, int32_t nranks, int32_t rank,
+                          uint32_t capacity, uint64_t *h_base, uint32_t *h_kept,
+                          uint32_t *h_spawned_global, uint64_t *h_dropped_global);
+
+/* ---- order-preserving compaction of filled slots (wavefront.cpp:488-497):
+ * keeps record s iff d_used[s] != 0, in slot order.  Records are
+ * record_words x 32-bit (2 for slot records, 18 for a 72-byte PathState).
+ * Writes the kept count to d_count (device) and, if h_count != NULL, to the host. */
+NRRS_API int nrrs_gpu_compact(nrrs_gpu_ctx *ctx, const void *d_in, const uint8_t *d_used, uint32_t count,
+                     uint32_t record_words, void *d_out, uint32_t *d_count, uint32_t *h_count);
+
+/* ---- granular drop-ins for the reference's free functions (device data) ---- */
+/* normalize_factors (rrs.hpp:18, rrs.cpp:8-24): in place; EINVAL on negative/non-finite (q untouched) */
+NRRS_API int nrrs_gpu_normalize_factors(nrrs_gpu_ctx *ctx, float *d_q, uint64_t n, uint64_t n_pixels,
+                               double *h_f_norm);
+/* realize_counts (rrs.hpp:45-46, rrs.cpp:35-45): EINVAL where stochastic_round throws */
+NRRS_API int nrrs_gpu_realize_counts(nrrs_gpu_ctx *ctx, const float *d_q, const float *d_u, int32_t *d_counts,
+                            uint64_t n, uint64_t *h_total);
+/* plan_spawns (wavefront.hpp:132, wavefront.cpp:141-154): EINVAL on a negative count */
+NRRS_API int nrrs_gpu_plan_spawns(nrrs_gpu_ctx *ctx, const int32_t *d_counts, uint64_t n, uint32_t capacity,
+                         uint32_t *d_offset, uint32_t *h_spawned, uint64_t *h_dropped);
+/* strategy_factor (wavefront.hpp:161-163) batched, no sanitize/normalize: d_q[j] = raw factor */
+NRRS_API int nrrs_gpu_strategy_factor(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *d_v, uint64_t n,
+                             const nrrs_strategy *s, float eps_div, float *d_q);
+/* NeuralRrs::predict_stats (networks.hpp:133) batched: d_stats[6j..6j+5] = mean(3), m2(3) */
+NRRS_API int nrrs_gpu_predict_stats(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *d_v, uint64_t n, float *d_stats);
+
+/* ---- host helpers (pure arithmetic, no device) ---- */
+NRRS_API uint32_t nrrs_queue_capacity_for(uint32_t n_pixels); /* wavefront.cpp:82-84 */
+/* RngStream(seed, seq).next_float() x n, mapped to [lo, hi): used by the host
+ * mirror to reproduce NeuralRrs' initializers (rng.hpp:33-62). */
+NRRS_API void nrrs_rng_fill(uint64_t seed, uint64_t seq, float *h_out, uint64_t n, float lo, float hi);
+/* root_path_key / child_path_key (rng.hpp:70-76) */
+NRRS_API uint64_t nrrs_root_path_key(uint32_t pixel, uint32_t frame);
+NRRS_API uint64_t nrrs_child_path_key(uint64_t parent_key, uint32_t child_index);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NRRS_GPU_H */

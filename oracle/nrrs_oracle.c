@@ -1,0 +1,619 @@
+/*
+ * nrrs_oracle.c -- CPU ORACLE (test infrastructure only; see nrrs_oracle.h).
+ *
+ * A line-by-line restatement of the reference's NRRS decision path in plain C.
+ * Build flags must keep IEEE semantics: -O2 -ffp-contract=off -fno-fast-math
+ * (the reference's Release build on x86-64 does not contract a*b+c).
+ * Citations are relative to /root/reference/proj.
+ */
+#include "nrrs_oracle.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdatomic.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ======================= rng.hpp ======================================== */
+
+/* rng.hpp:8-13 SplitMix64 finalizer */
+uint64_t orc_mix_bits(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+
+/* rng.hpp:15-17 */
+uint64_t orc_mix_bits2(uint64_t a, uint64_t b) { return orc_mix_bits(a ^ orc_mix_bits(b)); }
+
+/* rng.hpp:43-56 PCG32 step */
+uint32_t orc_rng_next_u32(orc_rng *r) {
+    const uint64_t old = r->state;
+    r->state = old * 6364136223846793005ull + r->inc;
+    const uint32_t xorshifted = (uint32_t)(((old >> 18u) ^ old) >> 27u);
+    const uint32_t rot = (uint32_t)(old >> 59u);
+    return (xorshifted >> rot) | (xorshifted << ((32u - rot) & 31u));
+}
+
+/* rng.hpp:37-41 constructor */
+void orc_rng_init(orc_rng *r, uint64_t seed, uint64_t sequence) {
+    r->inc = (sequence << 1u) | 1u;
+    r->state = 0u;
+    orc_rng_next_u32(r);
+    r->state += orc_mix_bits(seed);
+    orc_rng_next_u32(r);
+}
+
+/* rng.hpp:59-61 */
+float orc_rng_next_float(orc_rng *r) { return (float)(orc_rng_next_u32(r) >> 8) * 0x1p-24f; }
+
+/* rng.hpp:70-72 */
+uint64_t orc_child_path_key(uint64_t parent_key, uint32_t child_index) {
+    return orc_mix_bits2(parent_key, 0xc2b2ae3d27d4eb4full + child_index);
+}
+
+/* rng.hpp:74-76 */
+uint64_t orc_root_path_key(uint32_t pixel, uint32_t frame) {
+    return orc_mix_bits(((uint64_t)frame << 32) | pixel);
+}
+
+/* rng.hpp:78-82 */
+void orc_path_stream(orc_rng *r, uint64_t seed, uint64_t path_key, uint32_t depth, uint64_t purpose) {
+    const uint64_t seq = orc_mix_bits2(path_key, ((uint64_t)depth << 8) ^ purpose);
+    orc_rng_init(r, seed, seq);
+}
+
+/* wavefront.cpp:397-399, Draw::RrsRound = 0x55 (rng.hpp:27) */
+float orc_rrs_uniform(uint64_t seed, uint64_t path_key, uint32_t depth) {
+    orc_rng r;
+    orc_path_stream(&r, seed, path_key, depth, 0x55);
+    return orc_rng_next_float(&r);
+}
+
+void orc_fill_uniform(uint64_t seed, uint64_t sequence, float *out, size_t n, float lo, float hi) {
+    orc_rng r;
+    orc_rng_init(&r, seed, sequence);
+    for (size_t i = 0; i < n; ++i)
+        out[i] = lo + (hi - lo) * orc_rng_next_float(&r);
+}
+
+/* ======================= core.hpp / encodings.hpp ======================= */
+
+/* core.hpp:24-26 */
+float orc_luminance(const float c[3]) { return 0.2126f * c[0] + 0.7152f * c[1] + 0.0722f * c[2]; }
+
+static _Atomic uint64_t g_box_cox_clamps;
+uint64_t orc_box_cox_clamps(void) { return atomic_load(&g_box_cox_clamps); }
+void orc_reset_box_cox_clamps(void) { atomic_store(&g_box_cox_clamps, 0); }
+
+/* encodings.hpp:21-27 */
+int orc_stochastic_round(float q, float u) {
+    if (!(q >= 0.0f) || !isfinite(q))
+        return -1;
+    const float fl = floorf(q);
+    const float r = q - fl;
+    return (int)fl + (u < r ? 1 : 0);
+}
+
+/* encodings.hpp:31-44 */
+void orc_one_blob(float x, int bins, float *out) {
+    const float sigma = 1.0f / (float)bins;
+    const float inv_two_sigma2 = 1.0f / (2.0f * sigma * sigma);
+    float sum = 0.0f;
+    for (int i = 0; i < bins; ++i) {
+        const float c = ((float)i + 0.5f) / (float)bins;
+        const float d = x - c;
+        out[i] = expf(-d * d * inv_two_sigma2);
+        sum += out[i];
+    }
+    const float inv = 1.0f / sum;
+    for (int i = 0; i < bins; ++i)
+        out[i] *= inv;
+}
+
+/* encodings.hpp:54-62, lambda = 0.5 */
+float orc_box_cox(float x) {
+    if (x < 0.0f) {
+        atomic_fetch_add(&g_box_cox_clamps, 1);
+        x = 0.0f;
+    }
+    return (powf(x, 0.5f) - 1.0f) / 0.5f;
+}
+
+/* encodings.hpp:65-67 */
+float orc_roughness_remap(float a) { return 1.0f - expf(-a); }
+
+/* encodings.hpp:71-75 */
+float orc_softplus_mod(float x) {
+    if (x < 0.0f)
+        return log1pf(expf(x));
+    return 0.5f * x + 0.6931471805599453f;
+}
+
+/* encodings.hpp:85-88 */
+float orc_softplus_mod_inverse_pos(float y) { return 2.0f * (y - 0.6931471805599453f); }
+
+/* ======================= hashgrid.cpp ==================================== */
+
+static const uint32_t kPrimeY = 2654435761u; /* hashgrid.cpp:10-11 */
+static const uint32_t kPrimeZ = 805459861u;
+
+size_t orc_grid_param_count(const orc_grid_spec *s) {
+    return (size_t)s->levels * ((size_t)1 << s->log2_table_size) * (size_t)s->features;
+}
+
+/* hashgrid.cpp:25-28 */
+void orc_grid_init(const orc_grid_spec *s, float *theta, uint64_t seed, uint64_t seq) {
+    orc_rng r;
+    orc_rng_init(&r, seed, seq);
+    const size_t n = orc_grid_param_count(s);
+    for (size_t i = 0; i < n; ++i)
+        theta[i] = (orc_rng_next_float(&r) * 2.0f - 1.0f) * 1e-4f;
+}
+
+/* hashgrid.cpp:30-36 */
+static uint32_t grid_vertex_index(const orc_grid_spec *s, int level, uint32_t x, uint32_t y, uint32_t z) {
+    const uint64_t res = (uint64_t)(s->base_resolution << level);
+    const uint32_t table = 1u << s->log2_table_size;
+    if ((res + 1) * (res + 1) * (res + 1) <= table) { /* dense level, hashgrid.cpp:16-22 */
+        const uint32_t n = (uint32_t)res + 1;
+        return (x * n + y) * n + z;
+    }
+    return (x ^ (y * kPrimeY) ^ (z * kPrimeZ)) & (table - 1);
+}
+
+static float clamp01(float v) { return v < 0.0f ? 0.0f : (1.0f < v ? 1.0f : v); }
+
+/* hashgrid.cpp:38-82 (one point) */
+void orc_grid_encode(const orc_grid_spec *s, const float *theta, const float p01[3], float *out) {
+    const int F = s->features, L = s->levels;
+    const uint32_t stride = (1u << s->log2_table_size) * (uint32_t)F;
+    for (int l = 0; l < L; ++l) {
+        const int res = s->base_resolution << l;
+        const float fx = clamp01(p01[0]) * (float)res;
+        const float fy = clamp01(p01[1]) * (float)res;
+        const float fz = clamp01(p01[2]) * (float)res;
+        uint32_t cx = (uint32_t)fx, cy = (uint32_t)fy, cz = (uint32_t)fz;
+        if (cx > (uint32_t)(res - 1)) cx = (uint32_t)(res - 1);
+        if (cy > (uint32_t)(res - 1)) cy = (uint32_t)(res - 1);
+        if (cz > (uint32_t)(res - 1)) cz = (uint32_t)(res - 1);
+        const float tx = fx - (float)cx, ty = fy - (float)cy, tz = fz - (float)cz;
+        float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        for (int c = 0; c < 8; ++c) {
+            const uint32_t ox = (c & 1), oy = (c >> 1) & 1, oz = (c >> 2) & 1;
+            const float w = (ox ? tx : 1.0f - tx) * (oy ? ty : 1.0f - ty) * (oz ? tz : 1.0f - tz);
+            const uint32_t idx = grid_vertex_index(s, l, cx + ox, cy + oy, cz + oz);
+            const uint32_t base = (uint32_t)l * stride + idx * (uint32_t)F;
+            for (int f = 0; f < F; ++f)
+                acc[f] += w * theta[base + f];
+        }
+        for (int f = 0; f < F; ++f)
+            out[l * F + f] = acc[f];
+    }
+}
+
+/* ======================= mlp.cpp ========================================= */
+#define HID 32
+#define HLAYERS 3
+
+static int layer_in(int in, int l) { return l == 0 ? in : HID; }
+static int layer_out(int out, int l) { return l == HLAYERS ? out : HID; }
+
+/* mlp.cpp:7-16 */
+static int layer_offset(int in, int out, int layer) {
+    int off = 0;
+    for (int l = 0; l < layer; ++l)
+        off += layer_out(out, l) * layer_in(in, l) + layer_out(out, l);
+    return off;
+}
+int orc_mlp_param_count(int in, int out) { return layer_offset(in, out, HLAYERS + 1); }
+int orc_mlp_head_offset(int in, int out) { return layer_offset(in, out, HLAYERS); }
+
+/* mlp.cpp:34-44: He-uniform hidden layers (column-major W), zero head */
+void orc_mlp_init(int in, int out, float *theta, uint64_t seed, uint64_t seq) {
+    orc_rng r;
+    orc_rng_init(&r, seed, seq);
+    memset(theta, 0, sizeof(float) * (size_t)orc_mlp_param_count(in, out));
+    for (int l = 0; l < HLAYERS; ++l) {
+        const int li = layer_in(in, l), lo = layer_out(out, l);
+        const float bound = sqrtf(6.0f / (float)li);
+        float *w = theta + layer_offset(in, out, l);
+        for (int c = 0; c < li; ++c)
+            for (int rr = 0; rr < lo; ++rr)
+                w[c * lo + rr] = (orc_rng_next_float(&r) * 2.0f - 1.0f) * bound;
+    }
+}
+
+/* mlp.cpp:52-72: z = W a + b ; a = max(z, slope z) ; head linear */
+void orc_mlp_forward(int in, int out, const float *theta, const float *x, float *y) {
+    float a[64], z[64];
+    const float slope = 0.01f;
+    for (int i = 0; i < in; ++i)
+        a[i] = x[i];
+    for (int l = 0; l <= HLAYERS; ++l) {
+        const int li = layer_in(in, l), lo = layer_out(out, l);
+        const float *w = theta + layer_offset(in, out, l);
+        const float *b = w + lo * li;
+        for (int r = 0; r < lo; ++r) {
+            float s = 0.0f;
+            for (int c = 0; c < li; ++c)
+                s += w[c * lo + r] * a[c];
+            z[r] = s + b[r];
+        }
+        if (l < HLAYERS) {
+            for (int r = 0; r < lo; ++r) {
+                const float zs = z[r] * slope;
+                a[r] = z[r] < zs ? zs : z[r]; /* cwiseMax(z, z*slope) */
+            }
+        } else {
+            for (int r = 0; r < lo; ++r)
+                y[r] = z[r];
+        }
+    }
+}
+
+/* ======================= networks.cpp ==================================== */
+
+int orc_stat_input_dim(const orc_nets *n) { return n->grid.levels * n->grid.features + 16; }
+int orc_rrs_input_dim(const orc_nets *n) {
+    return n->variant == ORC_VARIANT_NRRS ? 11 : n->grid.levels * n->grid.features + 16;
+}
+
+/* Eigen Vector3f::mean(): redux x + (y + z), then / 3 */
+static float mean3(const float v[3]) { return (v[0] + (v[1] + v[2])) / 3.0f; }
+
+/* networks.cpp:131-135 */
+void orc_build_stat_tail(const float wo01[2], float roughness, float *out) {
+    orc_one_blob(wo01[0], 4, out);
+    orc_one_blob(wo01[1], 4, out + 4);
+    orc_one_blob(orc_roughness_remap(roughness), 8, out + 8);
+}
+
+/* networks.cpp:137-147 */
+void orc_build_nrrs_input(const float mean[3], const float m2[3], const float t_x[3],
+                          const float i_pixel[3], float roughness, float *out) {
+    for (int c = 0; c < 3; ++c)
+        out[c] = orc_box_cox(mean[c]);
+    for (int c = 0; c < 3; ++c)
+        out[3 + c] = orc_box_cox(m2[c]);
+    for (int c = 0; c < 3; ++c)
+        out[6 + c] = orc_box_cox(t_x[c]);
+    out[9] = orc_box_cox(mean3(i_pixel));
+    out[10] = orc_roughness_remap(roughness);
+}
+
+/* networks.cpp:149-157 */
+void orc_build_aid_tail(const float wo01[2], const float t_x[3], const float i_pixel[3],
+                        float roughness, float *out) {
+    orc_one_blob(wo01[0], 4, out);
+    orc_one_blob(wo01[1], 4, out + 4);
+    for (int c = 0; c < 3; ++c)
+        out[8 + c] = orc_box_cox(t_x[c]);
+    out[11] = orc_box_cox(mean3(i_pixel));
+    orc_one_blob(orc_roughness_remap(roughness), 4, out + 12);
+}
+
+/* networks.cpp:206-224 + 252-264: StatNet on the snapshot */
+void orc_predict_stats(const orc_nets *n, const float p01[3], const float wo01[2], float roughness,
+                       float stats[6]) {
+    float x[64];
+    const int gd = n->grid.levels * n->grid.features;
+    orc_grid_encode(&n->grid, n->stat_grid, p01, x);
+    orc_build_stat_tail(wo01, roughness, x + gd);
+    orc_mlp_forward(gd + 16, 6, n->stat_mlp, x, stats);
+}
+
+/* networks.cpp:266-281.  AID also runs StatNet and discards the result
+ * (networks.cpp:276); its only side effect is nothing (StatNet has no
+ * box_cox), so the restatement skips it. */
+float orc_predict_q(const orc_nets *n, const float p01[3], const float wo01[2], float roughness,
+                    const float t_x[3], const float i_pixel[3]) {
+    float x[64], y[8];
+    if (n->variant == ORC_VARIANT_NRRS) {
+        float st[6];
+        orc_predict_stats(n, p01, wo01, roughness, st);
+        orc_build_nrrs_input(st, st + 3, t_x, i_pixel, roughness, x);
+        orc_mlp_forward(11, 1, n->rrs_mlp, x, y);
+    } else {
+        const int gd = n->grid.levels * n->grid.features;
+        orc_grid_encode(&n->grid, n->rrs_grid, p01, x);
+        orc_build_aid_tail(wo01, t_x, i_pixel, roughness, x + gd);
+        orc_mlp_forward(gd + 16, 1, n->rrs_mlp, x, y);
+    }
+    return orc_softplus_mod(y[0]);
+}
+
+/* ======================= rrs.hpp / rrs.cpp ============================== */
+
+static float fmin_std(float a, float b) { return (b < a) ? b : a; } /* std::min(a,b) */
+
+/* rrs.hpp:56-61 */
+float orc_adrrs_factor(const float w[3], const float lo_hat[3], const float i_pixel[3], float eps_div) {
+    const float prod[3] = {w[0] * lo_hat[0], w[1] * lo_hat[1], w[2] * lo_hat[2]};
+    const float num = orc_luminance(prod);
+    const float q = num / (orc_luminance(i_pixel) + eps_div);
+    return q < 0.05f ? 0.05f : (20.0f < q ? 20.0f : q); /* std::clamp */
+}
+
+/* wavefront.cpp:186-215 (AdrrsTree is out of scope: returns NaN, sanitized to 0) */
+float orc_strategy_factor(int kind, float fixed_value, const orc_nets *nets, const float w[3],
+                          const float p01[3], const float wo01[2], float roughness,
+                          const float i_pixel[3], float eps_div) {
+    const float eps = (eps_div < 1e-8f) ? 1e-8f : eps_div; /* std::max(eps_div, 1e-8f) */
+    switch (kind) {
+    case ORC_FIXED:
+        return fixed_value;
+    case ORC_THROUGHPUT:
+        return fmin_std(1.0f, orc_luminance(w)); /* rrs.hpp:49-51 */
+    case ORC_ADRRS_NN: {
+        float st[6];
+        orc_predict_stats(nets, p01, wo01, roughness, st);
+        return orc_adrrs_factor(w, st, i_pixel, eps);
+    }
+    case ORC_NRRS:
+    case ORC_AID_NRRS:
+        return orc_predict_q(nets, p01, wo01, roughness, w, i_pixel);
+    default:
+        return NAN;
+    }
+}
+
+/* rrs.cpp:8-24 */
+double orc_normalize_factors(float *q, size_t n, uint64_t n_pixels, int *err) {
+    double sum = 0.0;
+    *err = 0;
+    for (size_t i = 0; i < n; ++i) {
+        if (!(q[i] >= 0.0f) || !isfinite(q[i])) {
+            *err = 1;
+            return 0.0;
+        }
+        sum += q[i];
+    }
+    if (sum <= 0.0)
+        return 1.0;
+    const double f_norm = (double)n_pixels / sum;
+    if (f_norm < 1.0) {
+        const float s = (float)f_norm;
+        for (size_t i = 0; i < n; ++i)
+            q[i] *= s;
+    }
+    return f_norm;
+}
+
+/* rrs.cpp:26-33 */
+double orc_bernstein_bound(double f_rate, uint64_t n_pixels) {
+    if (f_rate >= 1.0)
+        return 1.0;
+    const double gap = 1.0 - f_rate;
+    const double exponent = gap * gap * (double)n_pixels / (2.0 * f_rate + (2.0 / 3.0) * gap);
+    return exp(-exponent);
+}
+
+/* rrs.cpp:35-45 */
+uint64_t orc_realize_counts(const float *q, const float *u, int *counts, size_t n, int *err) {
+    uint64_t total = 0;
+    *err = 0;
+    for (size_t i = 0; i < n; ++i) {
+        counts[i] = orc_stochastic_round(q[i], u[i]);
+        if (counts[i] < 0) {
+            *err = 1;
+            return 0;
+        }
+        total += (uint64_t)counts[i];
+    }
+    return total;
+}
+
+/* wavefront.cpp:82-84 */
+uint32_t orc_queue_capacity_for(uint32_t n_pixels) { return n_pixels + (n_pixels + 7u) / 8u; }
+
+/* wavefront.cpp:141-154 */
+void orc_plan_spawns(const int *counts, size_t n, uint32_t capacity, uint32_t *offset,
+                     uint32_t *spawned, uint64_t *dropped, int *err) {
+    uint64_t cum = 0;
+    *err = 0;
+    for (size_t i = 0; i < n; ++i) {
+        if (counts[i] < 0) {
+            *err = 1;
+            return;
+        }
+        offset[i] = (uint32_t)(cum < capacity ? cum : capacity);
+        cum += (uint64_t)counts[i];
+    }
+    *spawned = (uint32_t)(cum < capacity ? cum : capacity);
+    *dropped = cum - *spawned;
+}
+
+/* ======================= trace_frame RRS block ========================== */
+
+typedef struct {
+    const orc_vertices *v;
+    const orc_stage_params *p;
+    const orc_nets *nets;
+    orc_stage_out *out;
+    size_t n;
+    _Atomic size_t next_block;
+    _Atomic uint64_t nonfinite;
+} factor_job;
+
+/* wavefront.cpp:368-389 body, one parallel_for_blocks block (parallel.hpp:28-63) */
+static void factor_block(factor_job *job, size_t begin, size_t end) {
+    const orc_vertices *v = job->v;
+    const orc_stage_params *p = job->p;
+    uint64_t nonfinite = 0;
+    for (size_t j = begin; j < end; ++j) {
+        float q = 0.0f;
+        int decided = 0;
+        const float *w = v->weight + 3 * j;
+        if (p->depth == 1) {
+            q = 1.0f;
+            decided = 1;
+        } else if (orc_luminance(w) > 0.0f) {
+            q = orc_strategy_factor(p->kind, p->fixed_value, job->nets, w, v->p01 + 3 * j,
+                                    v->wo01 + 2 * j, v->roughness[j], v->i_pixel + 3 * j, p->eps_div);
+            decided = 1;
+        }
+        if (!isfinite(q) || q < 0.0f) {
+            q = 0.0f;
+            decided = 0;
+            ++nonfinite;
+        }
+        if (job->out->decided)
+            job->out->decided[j] = (uint8_t)decided;
+        job->out->q_orig[j] = q;
+    }
+    atomic_fetch_add(&job->nonfinite, nonfinite);
+}
+
+static void *factor_worker(void *arg) {
+    factor_job *job = (factor_job *)arg;
+    const size_t block = 4096; /* parallel.hpp kParallelBlock */
+    for (;;) {
+        const size_t b = atomic_fetch_add(&job->next_block, 1);
+        const size_t begin = b * block;
+        if (begin >= job->n)
+            return NULL;
+        factor_block(job, begin, begin + block < job->n ? begin + block : job->n);
+    }
+}
+
+void orc_rrs_stage(const orc_vertices *v, size_t n, const orc_stage_params *p, const orc_nets *nets,
+                   orc_stage_out *out) {
+    /* factor pass: parallel_for_blocks over ns surface vertices (wavefront.cpp:368-389) */
+    factor_job job;
+    job.v = v;
+    job.p = p;
+    job.nets = nets;
+    job.out = out;
+    job.n = n;
+    atomic_init(&job.next_block, 0);
+    atomic_init(&job.nonfinite, 0);
+    int threads = p->threads < 1 ? 1 : p->threads;
+    if (threads > 256)
+        threads = 256;
+    pthread_t pool[256];
+    int spawned_threads = 0;
+    for (int t = 1; t < threads; ++t)
+        if (pthread_create(&pool[spawned_threads], NULL, factor_worker, &job) == 0)
+            ++spawned_threads;
+    factor_worker(&job);
+    for (int t = 0; t < spawned_threads; ++t)
+        pthread_join(pool[t], NULL);
+    out->nonfinite = atomic_load(&job.nonfinite);
+
+    /* serial part: normalize (:390), gain (:391), RNG + q_real (:393-402), realize (:403-404),
+     * plan (:406) */
+    memcpy(out->q_norm, out->q_orig, n * sizeof(float));
+    double sum = 0.0;
+    for (size_t j = 0; j < n; ++j)
+        sum += out->q_norm[j];
+    out->sum_q = sum;
+    int err = 0;
+    out->f_norm = orc_normalize_factors(out->q_norm, n, p->n_pixels, &err);
+    const int adaptive = p->kind != ORC_FIXED;
+    const float gain = (p->depth >= 2 && adaptive) ? p->gain : 1.0f;
+    uint64_t total = 0;
+    for (size_t j = 0; j < n; ++j) {
+        out->q_real[j] = out->q_norm[j] * gain;
+        out->u[j] = orc_rrs_uniform(p->seed, v->path_key[j], p->depth);
+        out->k[j] = orc_stochastic_round(out->q_real[j], out->u[j]);
+        total += (uint64_t)out->k[j];
+    }
+    out->total = total;
+    orc_plan_spawns(out->k, n, p->capacity, out->offset, &out->spawned, &out->dropped, &err);
+    /* child slot layout (wavefront.cpp:421-425, :436): slot off+c <- (j, c) */
+    if (out->slots) {
+        for (size_t j = 0; j < n; ++j) {
+            const uint32_t off = out->offset[j];
+            const uint32_t rem = out->spawned - (out->spawned < off ? out->spawned : off);
+            const uint32_t kept = (uint32_t)out->k[j] < rem ? (uint32_t)out->k[j] : rem;
+            for (uint32_t c = 0; c < kept; ++c) {
+                out->slots[2 * (size_t)(off + c)] = (uint32_t)j;
+                out->slots[2 * (size_t)(off + c) + 1] = c;
+            }
+        }
+    }
+}
+
+/* wavefront.cpp:488-497 */
+uint32_t orc_compact_slots(const uint32_t *slots, const uint8_t *used, uint32_t count, uint32_t *out) {
+    uint32_t write = 0;
+    for (uint32_t s = 0; s < count; ++s) {
+        if (!used[s])
+            continue;
+        out[2 * (size_t)write] = slots[2 * (size_t)s];
+        out[2 * (size_t)write + 1] = slots[2 * (size_t)s + 1];
+        ++write;
+    }
+    return write;
+}
+
+/* ======================= synthetic inputs =============================== */
+
+/* vertex i draws from RngStream(0xC0FFEE, i) in the order of
+ * test_networks.cpp:37-51 (position, omega_o, roughness, t_x, i_pixel),
+ * each vector component drawn left to right. */
+void orc_gen_vertices(size_t n, uint32_t n_pixels, uint32_t frame, float *p01, float *wo01,
+                      float *rough, float *t_x, float *i_pixel, uint64_t *path_key,
+                      uint32_t *pixel) {
+    for (size_t i = 0; i < n; ++i) {
+        orc_rng g;
+        orc_rng_init(&g, 0xC0FFEEull, (uint64_t)i);
+        for (int c = 0; c < 3; ++c) p01[3 * i + c] = orc_rng_next_float(&g);
+        for (int c = 0; c < 2; ++c) wo01[2 * i + c] = orc_rng_next_float(&g);
+        rough[i] = orc_rng_next_float(&g);
+        for (int c = 0; c < 3; ++c) t_x[3 * i + c] = 0.2f + orc_rng_next_float(&g);
+        for (int c = 0; c < 3; ++c) i_pixel[3 * i + c] = 0.5f + orc_rng_next_float(&g);
+        const uint32_t px = (uint32_t)(i % (n_pixels ? n_pixels : 1));
+        if (pixel) pixel[i] = px;
+        path_key[i] = orc_root_path_key(px, frame);
+    }
+}
+
+/* nrrs_cli.cpp:121-125 per-index convention with acceptance.cpp:99-102's seed */
+void orc_gen_split_bound_factors(size_t n, float *q) {
+    for (size_t i = 0; i < n; ++i) {
+        orc_rng r;
+        orc_rng_init(&r, 0xACC02ull, (uint64_t)i);
+        q[i] = orc_rng_next_float(&r) * 4.0f;
+    }
+}
+
+void orc_init_nets(int variant, const orc_grid_spec *g, uint64_t seed, int randomize,
+                   float *stat_grid, float *stat_mlp, float *rrs_grid, float *rrs_mlp) {
+    const int gd = g->levels * g->features;
+    const int stat_in = gd + 16, rrs_in = variant == ORC_VARIANT_NRRS ? 11 : gd + 16;
+    /* networks.cpp:177-190 */
+    orc_grid_init(g, stat_grid, seed, 0);
+    orc_mlp_init(stat_in, 6, stat_mlp, seed, 1);
+    if (variant == ORC_VARIANT_AID)
+        orc_grid_init(g, rrs_grid, seed, 2);
+    orc_mlp_init(rrs_in, 1, rrs_mlp, seed, 3);
+    const int rrs_head = orc_mlp_head_offset(rrs_in, 1);
+    rrs_mlp[orc_mlp_param_count(rrs_in, 1) - 1] = orc_softplus_mod_inverse_pos(1.0f);
+    if (!randomize)
+        return;
+    /* benchmark randomization: heads (w, b) ~ U(-0.5, 0.5) as in
+     * test_networks.cpp:407-410, StatNet head bias 1 (mostly positive stats),
+     * RRSNet head bias softplus_inv(2) (mean q ~ 2 so F < 1), grids x 1e4
+     * (test_networks.cpp:337-339). */
+    const int stat_head = orc_mlp_head_offset(stat_in, 6), stat_n = orc_mlp_param_count(stat_in, 6);
+    orc_rng r;
+    orc_rng_init(&r, seed, 100);
+    for (int k = stat_head; k < stat_n; ++k)
+        stat_mlp[k] = (orc_rng_next_float(&r) * 2.0f - 1.0f) * 0.5f;
+    for (int k = stat_n - 6; k < stat_n; ++k)
+        stat_mlp[k] = 1.0f;
+    const int rrs_n = orc_mlp_param_count(rrs_in, 1);
+    orc_rng_init(&r, seed, 101);
+    for (int k = rrs_head; k < rrs_n; ++k)
+        rrs_mlp[k] = (orc_rng_next_float(&r) * 2.0f - 1.0f) * 0.5f;
+    rrs_mlp[rrs_n - 1] = orc_softplus_mod_inverse_pos(2.0f);
+    const size_t gn = orc_grid_param_count(g);
+    for (size_t i = 0; i < gn; ++i)
+        stat_grid[i] *= 1e4f;
+    if (variant == ORC_VARIANT_AID)
+        for (size_t i = 0; i < gn; ++i)
+            rrs_grid[i] *= 1e4f;
+}

@@ -1,0 +1,161 @@
+/*
+ * nrrs_oracle.h -- CPU ORACLE for the NRRS per-bounce RRS stage.
+ *
+ * TEST INFRASTRUCTURE ONLY.  This is a plain-C restatement of the reference's
+ * algorithm (/root/reference/proj, arXiv 2510.07868) used as the parity checker
+ * for the CUDA path.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference leg may load it.  The product library
+ * (paper_2510_07868_b200/libnrrs_gpu.so) never links or calls it.
+ *
+ * Parity pin: every function cites the reference file:line it restates.  The
+ * reference itself does not build here (Eigen3 / doctest / CLI11 are absent,
+ * SURVEY.md section 8c); rng.hpp is Eigen-free and is compiled verbatim into
+ * oracle/_ref/ to pin the RNG, and the integer decision path is pinned by the
+ * reference's own known-answer tests (tests/golden/reference_kats.json).
+ */
+#ifndef NRRS_ORACLE_H
+#define NRRS_ORACLE_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- rng.hpp:8-82 ------------------------------------------------------- */
+typedef struct { uint64_t state, inc; } orc_rng;
+uint64_t orc_mix_bits(uint64_t x);
+uint64_t orc_mix_bits2(uint64_t a, uint64_t b);
+void orc_rng_init(orc_rng *r, uint64_t seed, uint64_t sequence);
+uint32_t orc_rng_next_u32(orc_rng *r);
+float orc_rng_next_float(orc_rng *r);
+uint64_t orc_child_path_key(uint64_t parent_key, uint32_t child_index);
+uint64_t orc_root_path_key(uint32_t pixel, uint32_t frame);
+void orc_path_stream(orc_rng *r, uint64_t seed, uint64_t path_key, uint32_t depth, uint64_t purpose);
+/* u = path_stream(seed, key, depth, Draw::RrsRound).next_float()  (wavefront.cpp:397-399) */
+float orc_rrs_uniform(uint64_t seed, uint64_t path_key, uint32_t depth);
+void orc_fill_uniform(uint64_t seed, uint64_t sequence, float *out, size_t n, float lo, float hi);
+
+/* ---- encodings.hpp:21-88, core.hpp:24-26 -------------------------------- */
+float orc_luminance(const float c[3]);
+int orc_stochastic_round(float q, float u); /* returns -1 where the reference throws */
+void orc_one_blob(float x, int bins, float *out);
+float orc_box_cox(float x); /* lambda = 0.5 */
+float orc_roughness_remap(float a);
+float orc_softplus_mod(float x);
+float orc_softplus_mod_inverse_pos(float y);
+uint64_t orc_box_cox_clamps(void);
+void orc_reset_box_cox_clamps(void);
+
+/* ---- hashgrid.hpp:13-22, hashgrid.cpp:10-82 ----------------------------- */
+typedef struct {
+    int levels, features, base_resolution, log2_table_size;
+} orc_grid_spec;
+size_t orc_grid_param_count(const orc_grid_spec *s);
+void orc_grid_init(const orc_grid_spec *s, float *theta, uint64_t seed, uint64_t seq);
+void orc_grid_encode(const orc_grid_spec *s, const float *theta, const float p01[3], float *out);
+
+/* ---- mlp.hpp:12-18, mlp.cpp:7-72 (hidden 32, 3 hidden layers, leaky 0.01) */
+int orc_mlp_param_count(int in, int out);
+int orc_mlp_head_offset(int in, int out);
+void orc_mlp_init(int in, int out, float *theta, uint64_t seed, uint64_t seq);
+void orc_mlp_forward(int in, int out, const float *theta, const float *x, float *y);
+
+/* ---- networks.cpp: snapshot inference ----------------------------------- */
+enum { ORC_VARIANT_NRRS = 0, ORC_VARIANT_AID = 1 };
+typedef struct {
+    int variant;
+    orc_grid_spec grid;
+    const float *stat_grid; /* snapshot StatNet grid theta */
+    const float *stat_mlp;  /* snapshot StatNet MLP theta (in = L*F+16, out = 6) */
+    const float *rrs_grid;  /* snapshot RRS grid theta (AID only) */
+    const float *rrs_mlp;   /* snapshot RRSNet MLP theta (in = 11 or L*F+16, out = 1) */
+} orc_nets;
+int orc_stat_input_dim(const orc_nets *n);
+int orc_rrs_input_dim(const orc_nets *n);
+void orc_build_stat_tail(const float wo01[2], float roughness, float *out);
+void orc_build_nrrs_input(const float mean[3], const float m2[3], const float t_x[3],
+                          const float i_pixel[3], float roughness, float *out);
+void orc_build_aid_tail(const float wo01[2], const float t_x[3], const float i_pixel[3],
+                        float roughness, float *out);
+void orc_predict_stats(const orc_nets *n, const float p01[3], const float wo01[2], float roughness,
+                       float stats[6]);
+float orc_predict_q(const orc_nets *n, const float p01[3], const float wo01[2], float roughness,
+                    const float t_x[3], const float i_pixel[3]);
+
+/* ---- rrs.hpp / rrs.cpp --------------------------------------------------- */
+enum {
+    ORC_FIXED = 0, ORC_THROUGHPUT = 1, ORC_ADRRS_TREE = 2, ORC_ADRRS_NN = 3, ORC_NRRS = 4,
+    ORC_AID_NRRS = 5
+};
+float orc_adrrs_factor(const float w[3], const float lo_hat[3], const float i_pixel[3], float eps_div);
+float orc_strategy_factor(int kind, float fixed_value, const orc_nets *nets, const float w[3],
+                          const float p01[3], const float wo01[2], float roughness,
+                          const float i_pixel[3], float eps_div);
+/* returns F_norm; *err = 1 where the reference throws */
+double orc_normalize_factors(float *q, size_t n, uint64_t n_pixels, int *err);
+uint64_t orc_realize_counts(const float *q, const float *u, int *counts, size_t n, int *err);
+double orc_bernstein_bound(double f_rate, uint64_t n_pixels);
+uint32_t orc_queue_capacity_for(uint32_t n_pixels);
+/* plan_spawns (wavefront.cpp:141-154) */
+void orc_plan_spawns(const int *counts, size_t n, uint32_t capacity, uint32_t *offset,
+                     uint32_t *spawned, uint64_t *dropped, int *err);
+
+/* ---- the RRS decision block of trace_frame (wavefront.cpp:363-411, 413-425, 488-497) ---- */
+typedef struct {
+    const float *p01;      /* [3n] */
+    const float *wo01;     /* [2n] */
+    const float *roughness;/* [n]  */
+    const float *weight;   /* [3n] path weight w (= t_x) */
+    const float *i_pixel;  /* [3n] film.i_acc[pixel] gathered per vertex */
+    const uint64_t *path_key; /* [n] */
+} orc_vertices;
+
+typedef struct {
+    uint32_t depth, n_pixels, capacity;
+    int kind;
+    float fixed_value;
+    float gain;        /* rc.gain() evaluated by the caller; applied iff depth>=2 && adaptive */
+    float eps_div;
+    uint64_t seed;
+    int threads;       /* factor pass threads (reference: parallel_for_blocks) */
+} orc_stage_params;
+
+typedef struct {
+    float *q_orig;   /* [n] raw sanitized factor */
+    float *q_norm;   /* [n] */
+    float *q_real;   /* [n] */
+    float *u;        /* [n] */
+    int *k;          /* [n] */
+    uint32_t *offset;/* [n] */
+    uint8_t *decided;/* [n] */
+    uint32_t *slots; /* [2*capacity] (parent j, child c) in slot order */
+    double f_norm;
+    double sum_q;
+    uint64_t total;
+    uint32_t spawned;
+    uint64_t dropped;
+    uint64_t nonfinite;
+} orc_stage_out;
+
+void orc_rrs_stage(const orc_vertices *v, size_t n, const orc_stage_params *p, const orc_nets *nets,
+                   orc_stage_out *out);
+/* order-preserving compaction (wavefront.cpp:488-497) of 2-word slot records */
+uint32_t orc_compact_slots(const uint32_t *slots, const uint8_t *used, uint32_t count, uint32_t *out);
+
+/* ---- synthetic inputs (generator follows test_networks.cpp:37-51) ---- */
+void orc_gen_vertices(size_t n, uint32_t n_pixels, uint32_t frame, float *p01, float *wo01,
+                      float *rough, float *t_x, float *i_pixel, uint64_t *path_key,
+                      uint32_t *pixel);
+void orc_gen_split_bound_factors(size_t n, float *q); /* RngStream(0xACC02, i).next_float()*4 */
+/* NeuralRrs constructor init (networks.cpp:159-197) followed by the benchmark's
+ * randomization (test_networks.cpp:407-410 style heads, RRSNet head bias
+ * softplus_inv(2), grid *= 1e4). randomize = 0 gives the fresh constructor state. */
+void orc_init_nets(int variant, const orc_grid_spec *g, uint64_t seed, int randomize,
+                   float *stat_grid, float *stat_mlp, float *rrs_grid, float *rrs_mlp);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

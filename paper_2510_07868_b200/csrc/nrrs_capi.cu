@@ -1,0 +1,1010 @@
+// nrrs_capi.cu -- C ABI (include/nrrs_gpu.h) over the sm_100a kernels.
+//
+// Host responsibilities: argument validation mirroring the reference's fail()
+// cases, the Mix-Depth gate (strategy per depth -> kernel kind), packing the
+// snapshot MLP weights into the fp16 hi/lo UMMA canonical layout, scratch
+// management, and launch sequencing.  No compute happens on the host: there is
+// no CPU fallback anywhere in this library.
+#include "../../include/nrrs_gpu.h"
+#include "nrrs_internal.h"
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace nrrs;
+
+namespace {
+
+// ---- host mirrors of rng.hpp (pure arithmetic) ----
+uint64_t h_mix_bits(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+
+struct HostRng {
+    uint64_t state, inc;
+    HostRng(uint64_t seed, uint64_t seq) {
+        inc = (seq << 1u) | 1u;
+        state = 0;
+        next();
+        state += h_mix_bits(seed);
+        next();
+    }
+    uint32_t next() {
+        const uint64_t old = state;
+        state = old * 6364136223846793005ull + inc;
+        const uint32_t xs = (uint32_t)(((old >> 18u) ^ old) >> 27u);
+        const uint32_t rot = (uint32_t)(old >> 59u);
+        return (xs >> rot) | (xs << ((32u - rot) & 31u));
+    }
+    float next_float() { return (float)(next() >> 8) * 0x1p-24f; }
+};
+
+constexpr int kHidden = 32;
+
+struct PackedNet {
+    std::vector<uint8_t> bytes;
+    NetDesc desc;
+};
+
+int mlp_param_count(int in, int out) {
+    int n = 0;
+    for (int l = 0; l < 4; ++l) {
+        const int li = l == 0 ? in : kHidden, lo = l == 3 ? out : kHidden;
+        n += lo * li + lo;
+    }
+    return n;
+}
+
+// Packs one snapshot MLP theta (mlp.cpp:7-32 layout) into hi/lo fp16 canonical
+// tiles.  colmap[c] = kernel K column of reference input column c (layer 0).
+PackedNet pack_net(const float *theta, int in, int out, int k0, const std::vector<int> &colmap) {
+    PackedNet pn;
+    int off = 0;
+    for (int l = 0; l < 4; ++l) {
+        const int li = l == 0 ? in : kHidden, lo = l == 3 ? out : kHidden;
+        const int K = l == 0 ? k0 : kHidden;
+        const int N = l == 3 ? 16 : kHidden;
+        const float *W = theta + off;         // column-major lo x li
+        const float *b = theta + off + lo * li;
+        off += lo * li + lo;
+        const size_t wbytes = (size_t)N * K * 2;
+        LayerDesc &L = pn.desc.layer[l];
+        L.K = (uint16_t)K;
+        L.N = (uint16_t)N;
+        L.w_hi = (uint32_t)pn.bytes.size();
+        L.w_lo = L.w_hi + (uint32_t)wbytes;
+        L.bias = L.w_lo + (uint32_t)wbytes;
+        const size_t bias_bytes = ((size_t)N * 4 + 15) / 16 * 16;
+        pn.bytes.resize(pn.bytes.size() + 2 * wbytes + bias_bytes, 0);
+        uint8_t *hi = pn.bytes.data() + L.w_hi, *lo_p = pn.bytes.data() + L.w_lo;
+        const uint32_t sbo = (uint32_t)K * 16u;
+        for (int r = 0; r < lo; ++r) {
+            for (int c = 0; c < li; ++c) {
+                const int kc = l == 0 ? colmap[c] : c;
+                const float v = W[c * lo + r];
+                const __half h = __float2half_rn(v);
+                const __half lw = __float2half_rn(v - __half2float(h));
+                const size_t o = (size_t)(r >> 3) * sbo + (size_t)(kc >> 3) * 128 + (size_t)(r & 7) * 16 +
+                                 (size_t)(kc & 7) * 2;
+                std::memcpy(hi + o, &h, 2);
+                std::memcpy(lo_p + o, &lw, 2);
+            }
+        }
+        float *bias = reinterpret_cast<float *>(pn.bytes.data() + L.bias);
+        for (int r = 0; r < lo; ++r)
+            bias[r] = b[r];
+    }
+    return pn;
+}
+
+// Concatenates packed nets into one blob; returns offsets rebased into desc.
+void append_net(std::vector<uint8_t> &blob, const PackedNet &pn, NetDesc &desc) {
+    const uint32_t base = (uint32_t)blob.size();
+    blob.insert(blob.end(), pn.bytes.begin(), pn.bytes.end());
+    desc = pn.desc;
+    for (auto &L : desc.layer) {
+        L.w_hi += base;
+        L.w_lo += base;
+        L.bias += base;
+    }
+}
+
+template <typename T>
+cudaError_t grow(T *&ptr, uint64_t &cap, uint64_t need) {
+    if (need <= cap && ptr)
+        return cudaSuccess;
+    if (ptr)
+        cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+    const cudaError_t e = cudaMalloc(&ptr, (need ? need : 1) * sizeof(T));
+    if (e == cudaSuccess)
+        cap = need;
+    return e;
+}
+
+}  // namespace
+
+struct DeviceBlob {
+    uint8_t *ptr = nullptr;
+    uint32_t bytes = 0;
+    KernelNets nets{};
+};
+
+struct nrrs_gpu_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    uint64_t launches = 0;
+
+    // weights
+    bool has_weights = false;
+    int variant = 0;
+    nrrs_grid_spec spec{};
+    GridDev grid{};
+    float *d_stat_grid = nullptr, *d_rrs_grid = nullptr;
+    DeviceBlob blob_stat, blob_rrs, blob_both;  // ADRRS/STATS, AID, NRRS
+
+    // scratch
+    float *d_q = nullptr, *d_u = nullptr;
+    uint64_t cap_q = 0, cap_u = 0;
+    double *d_parts = nullptr;
+    uint64_t cap_parts = 0;
+    uint32_t *d_part_counts = nullptr;
+    uint64_t cap_part_counts = 0;
+    uint64_t *d_tile_state = nullptr;
+    uint64_t cap_tiles = 0;
+    uint64_t *d_ctile_state = nullptr;
+    uint64_t cap_ctiles = 0;
+    uint32_t *d_misc = nullptr;  // [0] infer counter [1] decide tile ctr [2] compact tile ctr [3] err [4] count [5] sum ctr
+    DevResult *d_res = nullptr;
+    double *d_sum = nullptr;            // [0] local sum  [1] scratch sum
+    unsigned long long *d_total = nullptr;
+    uint32_t decide_epoch = 0, compact_epoch = 0;
+
+    // host-path device staging
+    struct Staging {
+        float *p01 = nullptr, *wo01 = nullptr, *rough = nullptr, *weight = nullptr, *ipix = nullptr;
+        uint64_t *key = nullptr;
+        float *q_norm = nullptr, *q_real = nullptr, *q_orig = nullptr, *u = nullptr;
+        int32_t *k = nullptr;
+        uint32_t *offset = nullptr, *slots = nullptr;
+        uint8_t *decided = nullptr;
+        uint64_t cap = 0, cap_slots = 0;
+    } st;
+};
+
+static int fail(nrrs_gpu_ctx *ctx, int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (ctx)
+        ctx->err = buf;
+    return code;
+}
+
+#define CK(ctx, call)                                                                                    \
+    do {                                                                                                 \
+        const cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess)                                                                           \
+            return fail(ctx, NRRS_ECUDA, "%s failed: %s", #call, cudaGetErrorString(e_));                \
+    } while (0)
+
+static int ensure_scratch(nrrs_gpu_ctx *ctx, uint64_t n) {
+    CK(ctx, cudaSetDevice(ctx->device));
+    CK(ctx, grow(ctx->d_q, ctx->cap_q, n));
+    CK(ctx, grow(ctx->d_u, ctx->cap_u, n));
+    const uint64_t g = infer_max_grid(ctx->num_sms);
+    CK(ctx, grow(ctx->d_parts, ctx->cap_parts, g));
+    CK(ctx, grow(ctx->d_part_counts, ctx->cap_part_counts, 2 * g));
+    const uint64_t tiles = decide_tiles(n) + 1;
+    if (tiles > ctx->cap_tiles) {
+        CK(ctx, grow(ctx->d_tile_state, ctx->cap_tiles, tiles));
+        CK(ctx, cudaMemsetAsync(ctx->d_tile_state, 0, tiles * sizeof(uint64_t), ctx->stream));
+    }
+    return NRRS_OK;
+}
+
+static int ensure_compact_scratch(nrrs_gpu_ctx *ctx, uint64_t count, uint32_t words) {
+    const uint64_t tiles = compact_tiles(count, words) + 1;
+    if (tiles > ctx->cap_ctiles) {
+        CK(ctx, grow(ctx->d_ctile_state, ctx->cap_ctiles, tiles));
+        CK(ctx, cudaMemsetAsync(ctx->d_ctile_state, 0, tiles * sizeof(uint64_t), ctx->stream));
+    }
+    return NRRS_OK;
+}
+
+// 14-bit launch epochs; on wrap the state array is cleared once.
+static uint32_t next_epoch(nrrs_gpu_ctx *ctx, uint32_t &epoch, uint64_t *state, uint64_t cap) {
+    epoch = (epoch + 1) & 0x3FFFu;
+    if (epoch == 0) {
+        cudaMemsetAsync(state, 0, cap * sizeof(uint64_t), ctx->stream);
+        epoch = 1;
+    }
+    return epoch;
+}
+
+extern "C" {
+
+int nrrs_gpu_abi_version(void) { return NRRS_GPU_ABI_VERSION; }
+
+uint32_t nrrs_queue_capacity_for(uint32_t n_pixels) { return n_pixels + (n_pixels + 7u) / 8u; }
+
+uint64_t nrrs_root_path_key(uint32_t pixel, uint32_t frame) {
+    return h_mix_bits(((uint64_t)frame << 32) | pixel);
+}
+
+uint64_t nrrs_child_path_key(uint64_t parent_key, uint32_t child_index) {
+    return h_mix_bits(parent_key ^ h_mix_bits(0xc2b2ae3d27d4eb4full + child_index));
+}
+
+void nrrs_rng_fill(uint64_t seed, uint64_t seq, float *h_out, uint64_t n, float lo, float hi) {
+    HostRng r(seed, seq);
+    for (uint64_t i = 0; i < n; ++i)
+        h_out[i] = lo + (hi - lo) * r.next_float();
+}
+
+int nrrs_gpu_create(int device, nrrs_gpu_ctx **out) {
+    if (!out)
+        return NRRS_EINVAL;
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count <= 0)
+        return NRRS_ECUDA;
+    if (device < 0 || device >= count)
+        return NRRS_EINVAL;
+    if (cudaSetDevice(device) != cudaSuccess)
+        return NRRS_ECUDA;
+    int major = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+    if (major != 10)
+        return NRRS_ECUDA;  // sm_100a binary only
+    auto *ctx = new nrrs_gpu_ctx();
+    ctx->device = device;
+    cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (cudaMalloc(&ctx->d_misc, 16 * sizeof(uint32_t)) != cudaSuccess ||
+        cudaMalloc(&ctx->d_res, sizeof(DevResult)) != cudaSuccess ||
+        cudaMalloc(&ctx->d_sum, 4 * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&ctx->d_total, 4 * sizeof(unsigned long long)) != cudaSuccess) {
+        delete ctx;
+        return NRRS_ECUDA;
+    }
+    cudaMemset(ctx->d_misc, 0, 16 * sizeof(uint32_t));
+    cudaMemset(ctx->d_res, 0, sizeof(DevResult));
+    cudaMemset(ctx->d_sum, 0, 4 * sizeof(double));
+    *out = ctx;
+    return NRRS_OK;
+}
+
+int nrrs_gpu_destroy(nrrs_gpu_ctx *ctx) {
+    if (!ctx)
+        return NRRS_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    void *ptrs[] = {ctx->d_stat_grid, ctx->d_rrs_grid, ctx->blob_stat.ptr, ctx->blob_rrs.ptr, ctx->blob_both.ptr,
+                    ctx->d_q, ctx->d_u, ctx->d_parts, ctx->d_part_counts, ctx->d_tile_state, ctx->d_ctile_state,
+                    ctx->d_misc, ctx->d_res, ctx->d_sum, ctx->d_total, ctx->st.p01, ctx->st.wo01, ctx->st.rough,
+                    ctx->st.weight, ctx->st.ipix, ctx->st.key, ctx->st.q_norm, ctx->st.q_real, ctx->st.q_orig,
+                    ctx->st.u, ctx->st.k, ctx->st.offset, ctx->st.slots, ctx->st.decided};
+    for (void *p : ptrs)
+        if (p)
+            cudaFree(p);
+    delete ctx;
+    return NRRS_OK;
+}
+
+const char *nrrs_gpu_last_error(const nrrs_gpu_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int nrrs_gpu_set_stream(nrrs_gpu_ctx *ctx, void *stream) {
+    if (!ctx)
+        return NRRS_EINVAL;
+    ctx->stream = reinterpret_cast<cudaStream_t>(stream);
+    return NRRS_OK;
+}
+
+uint64_t nrrs_gpu_launch_count(const nrrs_gpu_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+int nrrs_gpu_reserve(nrrs_gpu_ctx *ctx, uint64_t max_vertices, uint32_t max_capacity) {
+    if (!ctx)
+        return NRRS_EINVAL;
+    int rc = ensure_scratch(ctx, max_vertices);
+    if (rc)
+        return rc;
+    rc = ensure_compact_scratch(ctx, max_capacity, 2);
+    if (rc)
+        return rc;
+    return ensure_compact_scratch(ctx, max_capacity, 18);
+}
+
+int nrrs_gpu_set_weights(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w) {
+    if (!ctx || !w)
+        return NRRS_EINVAL;
+    const nrrs_grid_spec g = w->grid;
+    if (w->variant != NRRS_VARIANT_NRRS && w->variant != NRRS_VARIANT_AID)
+        return fail(ctx, NRRS_EINVAL, "set_weights: unknown variant %d", w->variant);
+    if (g.features != 2 || g.levels < 1 || g.levels > 8 || g.base_resolution < 1 || g.log2_table_size < 1 ||
+        g.log2_table_size > 24)
+        return fail(ctx, NRRS_EINVAL,
+                    "set_weights: grid spec (levels=%d features=%d base=%d log2T=%d) unsupported: the sm_100a "
+                    "kernel needs features == 2 and 1 <= levels <= 8",
+                    g.levels, g.features, g.base_resolution, g.log2_table_size);
+    if ((int64_t)g.base_resolution << (g.levels - 1) > (1 << 30))
+        return fail(ctx, NRRS_EINVAL, "set_weights: grid resolution overflow");
+    const uint64_t T = 1ull << g.log2_table_size;
+    const uint64_t grid_len = (uint64_t)g.levels * T * 2;
+    const int gd = g.levels * 2;
+    const int stat_in = gd + 16;
+    const int rrs_in = w->variant == NRRS_VARIANT_NRRS ? 11 : gd + 16;
+    if (w->stat_grid_len != grid_len || !w->stat_grid)
+        return fail(ctx, NRRS_ESIZE, "set_weights: stat grid has %llu params, expected %llu",
+                    (unsigned long long)w->stat_grid_len, (unsigned long long)grid_len);
+    if (w->stat_mlp_len != (uint64_t)mlp_param_count(stat_in, 6) || !w->stat_mlp)
+        return fail(ctx, NRRS_ESIZE, "set_weights: stat mlp has %llu params, expected %d",
+                    (unsigned long long)w->stat_mlp_len, mlp_param_count(stat_in, 6));
+    const uint64_t rrs_grid_len = w->variant == NRRS_VARIANT_AID ? grid_len : 0;
+    if (w->rrs_grid_len != rrs_grid_len || (rrs_grid_len && !w->rrs_grid))
+        return fail(ctx, NRRS_ESIZE, "set_weights: rrs grid has %llu params, expected %llu",
+                    (unsigned long long)w->rrs_grid_len, (unsigned long long)rrs_grid_len);
+    if (w->rrs_mlp_len != (uint64_t)mlp_param_count(rrs_in, 1) || !w->rrs_mlp)
+        return fail(ctx, NRRS_ESIZE, "set_weights: rrs mlp has %llu params, expected %d",
+                    (unsigned long long)w->rrs_mlp_len, mlp_param_count(rrs_in, 1));
+
+    CK(ctx, cudaSetDevice(ctx->device));
+    // layer-0 column maps: grid features -> [0, 2L), tail -> [16, 32)
+    std::vector<int> grid_map(stat_in);
+    for (int c = 0; c < stat_in; ++c)
+        grid_map[c] = c < gd ? c : 16 + (c - gd);
+    std::vector<int> id11(11);
+    for (int c = 0; c < 11; ++c)
+        id11[c] = c;
+    const PackedNet stat = pack_net(w->stat_mlp, stat_in, 6, 32, grid_map);
+    const PackedNet rrs = w->variant == NRRS_VARIANT_NRRS ? pack_net(w->rrs_mlp, 11, 1, 16, id11)
+                                                          : pack_net(w->rrs_mlp, rrs_in, 1, 32, grid_map);
+    auto upload_blob = [&](DeviceBlob &b, bool with_stat, bool with_rrs) -> int {
+        std::vector<uint8_t> bytes;
+        KernelNets nets{};
+        if (with_stat)
+            append_net(bytes, stat, nets.stat);
+        if (with_rrs)
+            append_net(bytes, rrs, nets.rrs);
+        if (b.ptr)
+            cudaFree(b.ptr);
+        b.ptr = nullptr;
+        CK(ctx, cudaMalloc(&b.ptr, bytes.size()));
+        CK(ctx, cudaMemcpy(b.ptr, bytes.data(), bytes.size(), cudaMemcpyHostToDevice));
+        b.bytes = (uint32_t)bytes.size();
+        b.nets = nets;
+        return NRRS_OK;
+    };
+    int rc = upload_blob(ctx->blob_stat, true, false);
+    if (!rc)
+        rc = upload_blob(ctx->blob_rrs, false, true);
+    if (!rc)
+        rc = upload_blob(ctx->blob_both, true, true);
+    if (rc)
+        return rc;
+    auto upload_grid = [&](float *&dst, const float *src, uint64_t len) -> int {
+        if (dst)
+            cudaFree(dst);
+        dst = nullptr;
+        if (!len)
+            return NRRS_OK;
+        CK(ctx, cudaMalloc(&dst, len * sizeof(float)));
+        CK(ctx, cudaMemcpy(dst, src, len * sizeof(float), cudaMemcpyHostToDevice));
+        return NRRS_OK;
+    };
+    rc = upload_grid(ctx->d_stat_grid, w->stat_grid, grid_len);
+    if (!rc)
+        rc = upload_grid(ctx->d_rrs_grid, w->rrs_grid, rrs_grid_len);
+    if (rc)
+        return rc;
+    ctx->variant = w->variant;
+    ctx->spec = g;
+    ctx->grid.levels = g.levels;
+    ctx->grid.base_resolution = g.base_resolution;
+    ctx->grid.table_size = (uint32_t)T;
+    ctx->grid.dense_mask = 0;
+    for (int l = 0; l < g.levels; ++l) {
+        const uint64_t res = (uint64_t)g.base_resolution << l;
+        if ((res + 1) * (res + 1) * (res + 1) <= T)
+            ctx->grid.dense_mask |= 1u << l;
+    }
+    ctx->has_weights = true;
+    return NRRS_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// shared launch helpers
+// ---------------------------------------------------------------------------
+// Maps (depth, strategy) to a kernel kind -- the Mix-Depth gate
+// (wavefront.cpp:366, :373-375; strategy_factor switch :192-214).  Neural
+// kinds follow the nets' variant exactly like NeuralRrs::predict_q.
+static int select_kind(nrrs_gpu_ctx *ctx, uint32_t depth, const nrrs_strategy &s, int *kind, int *heur) {
+    *heur = 0;
+    if (depth == 1) {
+        *kind = kKindHeuristic;
+        return NRRS_OK;
+    }
+    switch (s.kind) {
+    case NRRS_FIXED:
+        *kind = kKindHeuristic;
+        *heur = 0;
+        return NRRS_OK;
+    case NRRS_THROUGHPUT:
+        *kind = kKindHeuristic;
+        *heur = 1;
+        return NRRS_OK;
+    case NRRS_ADRRS_TREE:
+        return fail(ctx, NRRS_EINVAL, "strategy_factor: adrrs-tree needs an octree cache (not part of the GPU stage)");
+    case NRRS_ADRRS_NN:
+        if (!ctx->has_weights)
+            return fail(ctx, NRRS_ESTATE, "strategy_factor: adrrs-nn needs networks");
+        *kind = kKindAdrrs;
+        return NRRS_OK;
+    case NRRS_NRRS:
+    case NRRS_AID_NRRS:
+        if (!ctx->has_weights)
+            return fail(ctx, NRRS_ESTATE, "strategy_factor: neural RRS needs networks");
+        *kind = ctx->variant == NRRS_VARIANT_NRRS ? kKindNrrs : kKindAid;
+        return NRRS_OK;
+    default:
+        return fail(ctx, NRRS_EINVAL, "strategy_factor: unknown strategy kind %d", s.kind);
+    }
+}
+
+static void fill_infer_common(nrrs_gpu_ctx *ctx, int kind, InferParams &ip) {
+    ip.stat_grid = reinterpret_cast<const float2 *>(ctx->d_stat_grid);
+    ip.rrs_grid = reinterpret_cast<const float2 *>(ctx->d_rrs_grid);
+    ip.grid = ctx->grid;
+    const DeviceBlob *b = nullptr;
+    if (kind == kKindNrrs)
+        b = &ctx->blob_both;
+    else if (kind == kKindAid)
+        b = &ctx->blob_rrs;
+    else if (kind == kKindAdrrs || kind == kKindStats)
+        b = &ctx->blob_stat;
+    if (b) {
+        ip.blob = b->ptr;
+        ip.blob_bytes = b->bytes;
+        ip.nets = b->nets;
+    }
+}
+
+static int check_soa(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, int kind) {
+    if (!v || !v->p01 || !v->weight || !v->path_key)
+        return fail(ctx, NRRS_EINVAL, "vertex SoA: p01, weight and path_key are required");
+    if (kind != kKindHeuristic) {
+        if (!v->wo01 || !v->roughness)
+            return fail(ctx, NRRS_EINVAL, "vertex SoA: wo01 and roughness are required for neural strategies");
+        if (kind != kKindStats && !v->i_pixel && (!v->pixel || !v->i_acc))
+            return fail(ctx, NRRS_EINVAL, "vertex SoA: i_pixel or (pixel, i_acc) is required");
+    }
+    return NRRS_OK;
+}
+
+static int run_factors(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, const nrrs_stage_params *p,
+                       float *q_out, float *u_out, uint8_t *decided_out, double *sum_out) {
+    int kind = 0, heur = 0;
+    int rc = select_kind(ctx, p->depth, p->strategy, &kind, &heur);
+    if (rc)
+        return rc;
+    rc = check_soa(ctx, v, kind);
+    if (rc)
+        return rc;
+    InferParams ip{};
+    ip.p01 = v->p01;
+    ip.wo01 = v->wo01;
+    ip.roughness = v->roughness;
+    ip.weight = v->weight;
+    ip.i_pixel = v->i_pixel;
+    ip.path_key = v->path_key;
+    ip.pixel = v->pixel;
+    ip.i_acc = v->i_acc;
+    ip.n = n;
+    ip.depth = p->depth;
+    ip.gate = 1;
+    ip.heur_kind = heur;
+    ip.fixed_value = p->strategy.fixed_value;
+    ip.eps = p->eps_div < 1e-8f ? 1e-8f : p->eps_div;  // std::max(eps_div, 1e-8f) (wavefront.cpp:191)
+    ip.mixed_seed = h_mix_bits(p->seed);
+    fill_infer_common(ctx, kind, ip);
+    ip.q_out = q_out;
+    ip.u_out = u_out;
+    ip.decided_out = decided_out;
+    ip.parts = ctx->d_parts;
+    ip.part_counts = ctx->d_part_counts;
+    ip.counter = ctx->d_misc + 0;
+    ip.sum_out = sum_out;
+    ip.res = ctx->d_res;
+    uint32_t grid = 0;
+    CK(ctx, launch_infer(kind, ip, ctx->num_sms, ctx->stream, &grid));
+    ctx->launches += 1;
+    return NRRS_OK;
+}
+
+static int run_decide(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_stage_params *p, const float *q, const float *u,
+                      const double *rank_sums, int nranks, uint64_t n_pixels, uint32_t capacity,
+                      const nrrs_stage_out *o, unsigned long long *total_out, DevResult *res) {
+    if (!std::isfinite(p->gain) || p->gain < 0.0f)
+        return fail(ctx, NRRS_EINVAL, "stage: gain must be finite and >= 0 (got %g)", (double)p->gain);
+    const bool adaptive = p->strategy.kind != NRRS_FIXED;
+    DecideParams dp{};
+    dp.q = q;
+    dp.u = u;
+    dp.n = n;
+    dp.rank_sums = rank_sums;
+    dp.nranks = nranks;
+    dp.n_pixels = n_pixels;
+    dp.gain = (p->depth >= 2 && adaptive) ? p->gain : 1.0f;  // wavefront.cpp:391
+    dp.capacity = capacity;
+    dp.q_norm = o->q_norm;
+    dp.q_real = o->q_real;
+    dp.k_out = o->k;
+    dp.offset = o->offset;
+    dp.slots = o->slots;
+    dp.tile_state = ctx->d_tile_state;
+    dp.tile_counter = ctx->d_misc + 1;
+    dp.num_tiles = decide_tiles(n);
+    dp.epoch = next_epoch(ctx, ctx->decide_epoch, ctx->d_tile_state, ctx->cap_tiles);
+    dp.err_flag = ctx->d_misc + 3;
+    dp.total_out = total_out;
+    dp.res = res;
+    CK(ctx, launch_decide(0, dp, ctx->stream));
+    ctx->launches += 1;
+    return NRRS_OK;
+}
+
+static int check_out(nrrs_gpu_ctx *ctx, const nrrs_stage_out *o, uint64_t n) {
+    if (!o)
+        return fail(ctx, NRRS_EINVAL, "stage out: null");
+    if (n == 0)
+        return NRRS_OK;
+    if (!o->q_norm || !o->q_real || !o->slots)
+        return fail(ctx, NRRS_EINVAL, "stage out: q_norm, q_real and slots are required");
+    if ((reinterpret_cast<uintptr_t>(o->q_norm) | reinterpret_cast<uintptr_t>(o->q_real)) & 15u)
+        return fail(ctx, NRRS_EINVAL, "stage out: q_norm / q_real must be 16-byte aligned");
+    return NRRS_OK;
+}
+
+static int fetch_result(nrrs_gpu_ctx *ctx, nrrs_stage_result *h) {
+    DevResult r{};
+    CK(ctx, cudaMemcpyAsync(&r, ctx->d_res, sizeof r, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(ctx, cudaStreamSynchronize(ctx->stream));
+    h->f_norm = r.f_norm;
+    h->sum_q = r.sum_q;
+    h->total = r.total;
+    h->dropped = r.dropped;
+    h->nonfinite = r.nonfinite;
+    h->box_cox_clamps = r.box_cox_clamps;
+    h->spawned = r.spawned;
+    h->overflow = r.overflow;
+    return NRRS_OK;
+}
+
+static int resolve_capacity(nrrs_gpu_ctx *ctx, const nrrs_stage_params *p, uint32_t *cap) {
+    if (!p)
+        return fail(ctx, NRRS_EINVAL, "stage: null params");
+    if (p->depth < 1)
+        return fail(ctx, NRRS_EINVAL, "trace_frame: depth must be at least 1");
+    if (p->n_pixels == 0)
+        return fail(ctx, NRRS_EINVAL, "trace_frame: film has no pixels");
+    *cap = p->capacity ? p->capacity : nrrs_queue_capacity_for(p->n_pixels);
+    if (*cap < p->n_pixels)
+        return fail(ctx, NRRS_EINVAL, "trace_frame: queue capacity below the pixel count");
+    return NRRS_OK;
+}
+
+extern "C" {
+
+int nrrs_gpu_rrs_stage(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, const nrrs_stage_params *p,
+                       const nrrs_stage_out *o, nrrs_stage_result *h_result) {
+    if (!ctx)
+        return NRRS_EINVAL;
+    uint32_t cap = 0;
+    int rc = resolve_capacity(ctx, p, &cap);
+    if (rc)
+        return rc;
+    rc = check_out(ctx, o, n);
+    if (rc)
+        return rc;
+    if (n > 0xFFFFFFFFull)
+        return fail(ctx, NRRS_EINVAL, "stage: more than 2^32 vertices");
+    if (n == 0) {
+        DevResult r{};
+        r.f_norm = 1.0;  // all-zero (empty) input passes through with F = 1 (rrs.cpp:15-16)
+        CK(ctx, cudaMemcpyAsync(ctx->d_res, &r, sizeof r, cudaMemcpyHostToDevice, ctx->stream));
+        if (h_result)
+            return fetch_result(ctx, h_result);
+        return NRRS_OK;
+    }
+    rc = ensure_scratch(ctx, n);
+    if (rc)
+        return rc;
+    float *q = o->q_orig ? o->q_orig : ctx->d_q;
+    float *u = o->u ? o->u : ctx->d_u;
+    if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(u)) & 15u)
+        return fail(ctx, NRRS_EINVAL, "stage out: q_orig / u must be 16-byte aligned");
+    rc = run_factors(ctx, v, n, p, q, u, o->decided, ctx->d_sum);
+    if (rc)
+        return rc;
+    rc = run_decide(ctx, n, p, q, u, ctx->d_sum, 1, p->n_pixels, cap, o, ctx->d_total, ctx->d_res);
+    if (rc)
+        return rc;
+    if (h_result)
+        return fetch_result(ctx, h_result);
+    return NRRS_OK;
+}
+
+int nrrs_gpu_stage_factors(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, const nrrs_stage_params *p,
+                           const nrrs_stage_out *o, double *d_local_sum) {
+    if (!ctx || !d_local_sum)
+        return NRRS_EINVAL;
+    uint32_t cap = 0;
+    int rc = resolve_capacity(ctx, p, &cap);
+    if (rc)
+        return rc;
+    if (n == 0) {
+        CK(ctx, cudaMemsetAsync(d_local_sum, 0, sizeof(double), ctx->stream));
+        return NRRS_OK;
+    }
+    rc = ensure_scratch(ctx, n);
+    if (rc)
+        return rc;
+    float *q = o && o->q_orig ? o->q_orig : ctx->d_q;
+    float *u = o && o->u ? o->u : ctx->d_u;
+    return run_factors(ctx, v, n, p, q, u, o ? o->decided : nullptr, d_local_sum);
+}
+
+int nrrs_gpu_stage_decide(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_stage_params *p, const double *d_rank_sums,
+                          int32_t nranks, const nrrs_stage_out *o, uint64_t *d_local_total) {
+    if (!ctx || !d_rank_sums || nranks < 1 || !d_local_total)
+        return NRRS_EINVAL;
+    uint32_t cap = 0;
+    int rc = resolve_capacity(ctx, p, &cap);
+    if (rc)
+        return rc;
+    rc = check_out(ctx, o, n);
+    if (rc)
+        return rc;
+    if (n == 0) {
+        CK(ctx, cudaMemsetAsync(d_local_total, 0, sizeof(uint64_t), ctx->stream));
+        return NRRS_OK;
+    }
+    rc = ensure_scratch(ctx, n);
+    if (rc)
+        return rc;
+    const float *q = o->q_orig ? o->q_orig : ctx->d_q;
+    const float *u = o->u ? o->u : ctx->d_u;
+    // n_pixels here is the GLOBAL budget (sum over ranks); capacity clips the
+    // rank-local records, the global clip is applied by the caller.
+    return run_decide(ctx, n, p, q, u, d_rank_sums, nranks, p->n_pixels, cap, o,
+                      reinterpret_cast<unsigned long long *>(d_local_total), ctx->d_res);
+}
+
+int nrrs_gpu_sharded_clip(const uint64_t *totals, int32_t nranks, int32_t rank, uint32_t capacity,
+                          uint64_t *h_base, uint32_t *h_kept, uint32_t *h_spawned_global,
+                          uint64_t *h_dropped_global) {
+    if (!totals || nranks < 1 || rank < 0 || rank >= nranks)
+        return NRRS_EINVAL;
+    uint64_t base = 0, all = 0;
+    for (int r = 0; r < nranks; ++r) {
+        if (r < rank)
+            base += totals[r];
+        all += totals[r];
+    }
+    const uint64_t cap = capacity;
+    const uint64_t room = cap - (base < cap ? base : cap);
+    const uint64_t kept = totals[rank] < room ? totals[rank] : room;
+    const uint64_t spawned = all < cap ? all : cap;
+    if (h_base)
+        *h_base = base;
+    if (h_kept)
+        *h_kept = (uint32_t)kept;
+    if (h_spawned_global)
+        *h_spawned_global = (uint32_t)spawned;
+    if (h_dropped_global)
+        *h_dropped_global = all - spawned;
+    return NRRS_OK;
+}
+
+int nrrs_gpu_compact(nrrs_gpu_ctx *ctx, const void *d_in, const uint8_t *d_used, uint32_t count,
+                     uint32_t record_words, void *d_out, uint32_t *d_count, uint32_t *h_count) {
+    if (!ctx || (count && (!d_in || !d_used || !d_out)))
+        return NRRS_EINVAL;
+    if (record_words != 2 && record_words != 18)
+        return fail(ctx, NRRS_EINVAL, "compact: record_words must be 2 (slot) or 18 (PathState)");
+    uint32_t *cnt = d_count ? d_count : ctx->d_misc + 4;
+    if (count == 0) {
+        CK(ctx, cudaMemsetAsync(cnt, 0, sizeof(uint32_t), ctx->stream));
+    } else {
+        int rc = ensure_compact_scratch(ctx, count, record_words);
+        if (rc)
+            return rc;
+        CompactParams cp{};
+        cp.in = d_in;
+        cp.used = d_used;
+        cp.count = count;
+        cp.out = d_out;
+        cp.count_out = cnt;
+        cp.tile_state = ctx->d_ctile_state;
+        cp.tile_counter = ctx->d_misc + 2;
+        cp.num_tiles = compact_tiles(count, record_words);
+        cp.epoch = next_epoch(ctx, ctx->compact_epoch, ctx->d_ctile_state, ctx->cap_ctiles);
+        CK(ctx, launch_compact(record_words, cp, ctx->stream));
+        ctx->launches += 1;
+    }
+    if (h_count) {
+        CK(ctx, cudaMemcpyAsync(h_count, cnt, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+    return NRRS_OK;
+}
+
+int nrrs_gpu_normalize_factors(nrrs_gpu_ctx *ctx, float *d_q, uint64_t n, uint64_t n_pixels, double *h_f_norm) {
+    if (!ctx || (n && !d_q))
+        return NRRS_EINVAL;
+    if (n == 0) {
+        if (h_f_norm)
+            *h_f_norm = 1.0;
+        return NRRS_OK;
+    }
+    int rc = ensure_scratch(ctx, 1);
+    if (rc)
+        return rc;
+    CK(ctx, cudaMemsetAsync(ctx->d_misc + 3, 0, sizeof(uint32_t), ctx->stream));
+    uint64_t grid = (n + 255) / 256;
+    const uint64_t gmax = infer_max_grid(ctx->num_sms);
+    if (grid > gmax)
+        grid = gmax;
+    CK(ctx, launch_sum_check(d_q, n, ctx->d_parts, ctx->d_misc + 5, ctx->d_misc + 3, ctx->d_sum + 1,
+                             (uint32_t)grid, ctx->stream));
+    CK(ctx, launch_scale(d_q, n, ctx->d_sum + 1, n_pixels, ctx->d_misc + 3, ctx->d_sum + 2, ctx->num_sms,
+                         ctx->stream));
+    ctx->launches += 2;
+    uint32_t err = 0;
+    double f = 1.0;
+    CK(ctx, cudaMemcpyAsync(&err, ctx->d_misc + 3, sizeof err, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(ctx, cudaMemcpyAsync(&f, ctx->d_sum + 2, sizeof f, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(ctx, cudaStreamSynchronize(ctx->stream));
+    if (err)
+        return fail(ctx, NRRS_EINVAL, "normalize_factors: factors must be finite and >= 0");
+    if (h_f_norm)
+        *h_f_norm = f;
+    return NRRS_OK;
+}
+
+int nrrs_gpu_realize_counts(nrrs_gpu_ctx *ctx, const float *d_q, const float *d_u, int32_t *d_counts, uint64_t n,
+                            uint64_t *h_total) {
+    if (!ctx || (n && (!d_q || !d_u || !d_counts)))
+        return NRRS_EINVAL;
+    CK(ctx, cudaMemsetAsync(ctx->d_misc + 3, 0, sizeof(uint32_t), ctx->stream));
+    CK(ctx, cudaMemsetAsync(ctx->d_total + 1, 0, sizeof(unsigned long long), ctx->stream));
+    if (n) {
+        CK(ctx, launch_realize(d_q, d_u, d_counts, n, ctx->d_misc + 3, ctx->d_total + 1, ctx->num_sms, ctx->stream));
+        ctx->launches += 1;
+    }
+    uint32_t err = 0;
+    unsigned long long total = 0;
+    CK(ctx, cudaMemcpyAsync(&err, ctx->d_misc + 3, sizeof err, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(ctx, cudaMemcpyAsync(&total, ctx->d_total + 1, sizeof total, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(ctx, cudaStreamSynchronize(ctx->stream));
+    if (err)
+        return fail(ctx, NRRS_EINVAL, "stochastic_round: q must be finite and >= 0");
+    if (h_total)
+        *h_total = total;
+    return NRRS_OK;
+}
+
+int nrrs_gpu_plan_spawns(nrrs_gpu_ctx *ctx, const int32_t *d_counts, uint64_t n, uint32_t capacity,
+                         uint32_t *d_offset, uint32_t *h_spawned, uint64_t *h_dropped) {
+    if (!ctx || (n && (!d_counts || !d_offset)))
+        return NRRS_EINVAL;
+    if (n == 0) {
+        if (h_spawned)
+            *h_spawned = 0;
+        if (h_dropped)
+            *h_dropped = 0;
+        return NRRS_OK;
+    }
+    int rc = ensure_scratch(ctx, n);
+    if (rc)
+        return rc;
+    CK(ctx, cudaMemsetAsync(ctx->d_misc + 3, 0, sizeof(uint32_t), ctx->stream));
+    DecideParams dp{};
+    dp.counts_in = d_counts;
+    dp.n = n;
+    dp.capacity = capacity;
+    dp.offset = d_offset;
+    dp.tile_state = ctx->d_tile_state;
+    dp.tile_counter = ctx->d_misc + 1;
+    dp.num_tiles = decide_tiles(n);
+    dp.epoch = next_epoch(ctx, ctx->decide_epoch, ctx->d_tile_state, ctx->cap_tiles);
+    dp.err_flag = ctx->d_misc + 3;
+    dp.total_out = ctx->d_total + 2;
+    CK(ctx, launch_decide(1, dp, ctx->stream));
+    ctx->launches += 1;
+    uint32_t err = 0;
+    unsigned long long total = 0;
+    CK(ctx, cudaMemcpyAsync(&err, ctx->d_misc + 3, sizeof err, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(ctx, cudaMemcpyAsync(&total, ctx->d_total + 2, sizeof total, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(ctx, cudaStreamSynchronize(ctx->stream));
+    if (err)
+        return fail(ctx, NRRS_EINVAL, "plan_spawns: negative count");
+    const uint64_t spawned = total < capacity ? total : capacity;
+    if (h_spawned)
+        *h_spawned = (uint32_t)spawned;
+    if (h_dropped)
+        *h_dropped = total - spawned;
+    return NRRS_OK;
+}
+
+int nrrs_gpu_strategy_factor(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, const nrrs_strategy *s,
+                             float eps_div, float *d_q) {
+    if (!ctx || !s || (n && !d_q))
+        return NRRS_EINVAL;
+    int kind = 0, heur = 0;
+    int rc = select_kind(ctx, 2, *s, &kind, &heur);  // depth >= 2: no depth pin in strategy_factor
+    if (rc)
+        return rc;
+    if (n == 0)
+        return NRRS_OK;
+    rc = check_soa(ctx, v, kind);
+    if (rc)
+        return rc;
+    InferParams ip{};
+    ip.p01 = v->p01;
+    ip.wo01 = v->wo01;
+    ip.roughness = v->roughness;
+    ip.weight = v->weight;
+    ip.i_pixel = v->i_pixel;
+    ip.path_key = v->path_key;
+    ip.pixel = v->pixel;
+    ip.i_acc = v->i_acc;
+    ip.n = n;
+    ip.depth = 2;
+    ip.gate = 0;
+    ip.heur_kind = heur;
+    ip.fixed_value = s->fixed_value;
+    ip.eps = eps_div < 1e-8f ? 1e-8f : eps_div;
+    fill_infer_common(ctx, kind, ip);
+    ip.q_out = d_q;
+    uint32_t grid = 0;
+    CK(ctx, launch_infer(kind, ip, ctx->num_sms, ctx->stream, &grid));
+    ctx->launches += 1;
+    return NRRS_OK;
+}
+
+int nrrs_gpu_predict_stats(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, float *d_stats) {
+    if (!ctx || (n && !d_stats))
+        return NRRS_EINVAL;
+    if (!ctx->has_weights)
+        return fail(ctx, NRRS_ESTATE, "predict_stats: set_weights first");
+    if (n == 0)
+        return NRRS_OK;
+    int rc = check_soa(ctx, v, kKindStats);
+    if (rc)
+        return rc;
+    InferParams ip{};
+    ip.p01 = v->p01;
+    ip.wo01 = v->wo01;
+    ip.roughness = v->roughness;
+    ip.weight = v->weight;
+    ip.path_key = v->path_key;
+    ip.n = n;
+    ip.depth = 2;
+    ip.gate = 0;
+    fill_infer_common(ctx, kKindStats, ip);
+    ip.stats_out = d_stats;
+    uint32_t grid = 0;
+    CK(ctx, launch_infer(kKindStats, ip, ctx->num_sms, ctx->stream, &grid));
+    ctx->launches += 1;
+    return NRRS_OK;
+}
+
+// ---- host-buffer entry: H2D, stage, D2H ----
+int nrrs_gpu_rrs_stage_host(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *h, uint64_t n, const nrrs_stage_params *p,
+                            const nrrs_stage_out *ho, nrrs_stage_result *h_result) {
+    if (!ctx || !h || !ho || !ho->q_norm || !ho->q_real || !ho->slots)
+        return NRRS_EINVAL;
+    uint32_t cap = 0;
+    int rc = resolve_capacity(ctx, p, &cap);
+    if (rc)
+        return rc;
+    CK(ctx, cudaSetDevice(ctx->device));
+    auto &s = ctx->st;
+    if (n > s.cap) {
+        float **fp[] = {&s.p01, &s.wo01, &s.rough, &s.weight, &s.ipix, &s.q_norm, &s.q_real, &s.q_orig, &s.u};
+        const int mult[] = {3, 2, 1, 3, 3, 1, 1, 1, 1};
+        for (int i = 0; i < 9; ++i) {
+            if (*fp[i])
+                cudaFree(*fp[i]);
+            *fp[i] = nullptr;
+            CK(ctx, cudaMalloc(fp[i], n * mult[i] * sizeof(float)));
+        }
+        if (s.key) cudaFree(s.key);
+        if (s.k) cudaFree(s.k);
+        if (s.offset) cudaFree(s.offset);
+        if (s.decided) cudaFree(s.decided);
+        CK(ctx, cudaMalloc(&s.key, n * sizeof(uint64_t)));
+        CK(ctx, cudaMalloc(&s.k, n * sizeof(int32_t)));
+        CK(ctx, cudaMalloc(&s.offset, n * sizeof(uint32_t)));
+        CK(ctx, cudaMalloc(&s.decided, n));
+        s.cap = n;
+    }
+    if (cap > s.cap_slots) {
+        if (s.slots) cudaFree(s.slots);
+        CK(ctx, cudaMalloc(&s.slots, (size_t)cap * 2 * sizeof(uint32_t)));
+        s.cap_slots = cap;
+    }
+    auto h2d = [&](void *dst, const void *src, size_t bytes) -> int {
+        if (src && bytes)
+            CK(ctx, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        return NRRS_OK;
+    };
+    if (!h->i_pixel)
+        return fail(ctx, NRRS_EINVAL, "stage_host: pass i_pixel (gathered per vertex)");
+    rc = h2d(s.p01, h->p01, n * 12);
+    if (!rc) rc = h2d(s.wo01, h->wo01, n * 8);
+    if (!rc) rc = h2d(s.rough, h->roughness, n * 4);
+    if (!rc) rc = h2d(s.weight, h->weight, n * 12);
+    if (!rc) rc = h2d(s.ipix, h->i_pixel, n * 12);
+    if (!rc) rc = h2d(s.key, h->path_key, n * 8);
+    if (rc)
+        return rc;
+    nrrs_vertex_soa dv{};
+    dv.p01 = s.p01;
+    dv.wo01 = h->wo01 ? s.wo01 : nullptr;
+    dv.roughness = h->roughness ? s.rough : nullptr;
+    dv.weight = s.weight;
+    dv.i_pixel = s.ipix;
+    dv.path_key = s.key;
+    nrrs_stage_out dout{};
+    dout.q_norm = s.q_norm;
+    dout.q_real = s.q_real;
+    dout.slots = s.slots;
+    dout.k = ho->k ? s.k : nullptr;
+    dout.offset = ho->offset ? s.offset : nullptr;
+    dout.decided = ho->decided ? s.decided : nullptr;
+    dout.q_orig = s.q_orig;
+    dout.u = s.u;
+    nrrs_stage_result r{};
+    rc = nrrs_gpu_rrs_stage(ctx, &dv, n, p, &dout, &r);  // syncs (needs spawned for the slot copy)
+    if (rc)
+        return rc;
+    auto d2h = [&](void *dst, const void *src, size_t bytes) -> int {
+        if (dst && bytes)
+            CK(ctx, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        return NRRS_OK;
+    };
+    rc = d2h(ho->q_norm, s.q_norm, n * 4);
+    if (!rc) rc = d2h(ho->q_real, s.q_real, n * 4);
+    if (!rc) rc = d2h(ho->slots, s.slots, (size_t)r.spawned * 8);
+    if (!rc) rc = d2h(ho->k, s.k, n * 4);
+    if (!rc) rc = d2h(ho->offset, s.offset, n * 4);
+    if (!rc) rc = d2h(ho->decided, s.decided, n);
+    if (!rc) rc = d2h(ho->q_orig, s.q_orig, n * 4);
+    if (!rc) rc = d2h(ho->u, s.u, n * 4);
+    if (rc)
+        return rc;
+    CK(ctx, cudaStreamSynchronize(ctx->stream));
+    if (h_result)
+        *h_result = r;
+    return NRRS_OK;
+}
+
+}  // extern "C"

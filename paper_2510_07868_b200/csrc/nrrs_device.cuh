@@ -1,0 +1,277 @@
+// nrrs_device.cuh -- device building blocks of the sm_100a NRRS stage.
+//
+// Bit-exactness contract: every expression that feeds an
+// integer decision (luminance gate, normalization scale, gain, stochastic
+// rounding) uses explicit round-to-nearest intrinsics so nvcc cannot contract
+// it into an FMA; the network chain (tolerance 1e-3) may contract freely.
+#pragma once
+
+#include <cstdint>
+#include <cuda_fp16.h>
+
+namespace nrrs {
+
+// ---------------------------------------------------------------------------
+// Counter-based RNG: SplitMix64 keyed PCG32 (reference rng.hpp:8-82).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t mix_bits(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+
+__device__ __forceinline__ uint32_t pcg_output(uint64_t old) {
+    const uint32_t xs = (uint32_t)(((old >> 18u) ^ old) >> 27u);
+    const uint32_t rot = (uint32_t)(old >> 59u);
+    return __funnelshift_r(xs, xs, rot);  // rotate right
+}
+
+// path_stream(seed, key, depth, Draw::RrsRound).next_float()  (wavefront.cpp:397-399).
+// The stream constructor advances twice (rng.hpp:37-41); the third output is u.
+__device__ __forceinline__ float rrs_uniform(uint64_t mixed_seed, uint64_t key, uint32_t depth) {
+    constexpr uint64_t kMul = 6364136223846793005ull;
+    const uint64_t seq = mix_bits(key ^ mix_bits(((uint64_t)depth << 8) ^ 0x55ull));
+    const uint64_t inc = (seq << 1u) | 1u;
+    uint64_t state = inc;            // 0 * kMul + inc
+    state = state + mixed_seed;      // m_state += mix_bits(seed)
+    state = state * kMul + inc;      // second constructor step
+    const uint32_t out = pcg_output(state);
+    return __fmul_rn((float)(out >> 8), 0x1p-24f);
+}
+
+// ---------------------------------------------------------------------------
+// Encodings (encodings.hpp:21-88, core.hpp:24-26)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float luminance(float x, float y, float z) {
+    return __fadd_rn(__fadd_rn(__fmul_rn(0.2126f, x), __fmul_rn(0.7152f, y)), __fmul_rn(0.0722f, z));
+}
+
+__device__ __forceinline__ float clamp01(float v) { return v < 0.0f ? 0.0f : (1.0f < v ? 1.0f : v); }
+
+template <int BINS>
+__device__ __forceinline__ void one_blob(float x, float *out) {
+    constexpr float sigma = 1.0f / (float)BINS;
+    constexpr float inv_two_sigma2 = 1.0f / (2.0f * sigma * sigma);
+    float sum = 0.0f;
+#pragma unroll
+    for (int i = 0; i < BINS; ++i) {
+        const float c = ((float)i + 0.5f) / (float)BINS;
+        const float d = x - c;
+        out[i] = expf(-d * d * inv_two_sigma2);
+        sum += out[i];
+    }
+    const float inv = 1.0f / sum;
+#pragma unroll
+    for (int i = 0; i < BINS; ++i)
+        out[i] *= inv;
+}
+
+// box_cox with lambda = 0.5; negative inputs clamp to 0 and are counted.
+__device__ __forceinline__ float box_cox(float x, uint32_t &clamps) {
+    if (x < 0.0f) {
+        ++clamps;
+        x = 0.0f;
+    }
+    return (sqrtf(x) - 1.0f) * 2.0f;
+}
+
+__device__ __forceinline__ float roughness_remap(float a) { return 1.0f - expf(-a); }
+
+__device__ __forceinline__ float softplus_mod(float x) {
+    if (x < 0.0f)
+        return log1pf(expf(x));
+    return 0.5f * x + 0.6931471805599453f;
+}
+
+__device__ __forceinline__ float mean3(float x, float y, float z) { return (x + (y + z)) / 3.0f; }
+
+// stochastic_round (encodings.hpp:21-27) on a sanitized q >= 0.
+__device__ __forceinline__ uint32_t stochastic_round(float q, float u) {
+    const float fl = floorf(q);
+    const float r = __fsub_rn(q, fl);
+    return (uint32_t)fl + (u < r ? 1u : 0u);
+}
+
+// ---------------------------------------------------------------------------
+// tcgen05 / TMEM / mbarrier wrappers (inline PTX, sm_100a)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done = 0;
+    const uint32_t addr = smem_u32(bar);
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(addr), "r"(parity)
+            : "memory");
+    }
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// Warp-wide: allocate `ncols` TMEM columns, base address written to *dst (smem).
+__device__ __forceinline__ void tmem_alloc(uint32_t *dst, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+
+// UMMA shared-memory matrix descriptor, K-major, SWIZZLE_NONE canonical layout
+// ((8,m),(8 elems,k)) : 8x16B core matrices; lbo = byte stride between the two
+// 16-byte K chunks of one K16 slice, sbo = byte stride between 8-row groups.
+__device__ __forceinline__ uint64_t make_smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;  // version = 1 (sm_100)
+    // base_offset = 0, lbo_mode = 0, layout_type = 0 (SWIZZLE_NONE)
+    return d;
+}
+
+// Instruction descriptor: kind::f16, A = B = F16, D = F32, both K-major, M = 128.
+__host__ __device__ constexpr uint32_t make_idesc_f16(uint32_t n) {
+    return (1u << 4)              // c_format = F32
+           | (0u << 7)            // a_format = F16
+           | (0u << 10)           // b_format = F16
+           | ((n >> 3) << 17)     // N >> 3
+           | ((128u >> 4) << 24); // M >> 4
+}
+
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+        v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+          "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+        v[i] = __uint_as_float(r[i]);
+}
+
+// ---------------------------------------------------------------------------
+// Decoupled look-back tile state: [63:62] flag (1 = aggregate, 2 = inclusive
+// prefix), [61:48] launch epoch, [47:0] value.  Entries written by an earlier
+// launch carry another epoch and read as "not yet published", so the state
+// array never needs a memset between launches (the host clears it only when
+// the 14-bit epoch wraps).
+// ---------------------------------------------------------------------------
+constexpr uint64_t kFlagAgg = 1ull << 62;
+constexpr uint64_t kFlagPrefix = 2ull << 62;
+constexpr uint64_t kValueMask = (1ull << 48) - 1;
+
+__device__ __forceinline__ void st_release_u64(uint64_t *p, uint64_t v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Single-thread look-back: returns the exclusive prefix of `tile` and publishes
+// its inclusive prefix.  Tiles are claimed in launch order (dynamic tile id),
+// so predecessors always make progress.
+__device__ __forceinline__ uint64_t lookback_exclusive(uint64_t *state, uint32_t tile, uint64_t aggregate,
+                                                       uint32_t epoch) {
+    const uint64_t tag = (uint64_t)(epoch & 0x3FFFu) << 48;
+    if (tile == 0) {
+        st_release_u64(&state[0], kFlagPrefix | tag | aggregate);
+        return 0;
+    }
+    st_release_u64(&state[tile], kFlagAgg | tag | aggregate);
+    uint64_t excl = 0;
+    int32_t t = (int32_t)tile - 1;
+    while (t >= 0) {
+        uint64_t s;
+        do {
+            s = ld_acquire_u64(&state[t]);
+        } while ((s >> 62) == 0 || ((s >> 48) & 0x3FFFu) != (epoch & 0x3FFFu));
+        excl += s & kValueMask;
+        if ((s >> 62) == 2)
+            break;
+        --t;
+    }
+    st_release_u64(&state[tile], kFlagPrefix | tag | (excl + aggregate));
+    return excl;
+}
+
+// Claims the next tile in launch order; the CTA that claims the last tile
+// resets the counter for the next launch (no claims can follow it).
+__device__ __forceinline__ uint32_t claim_tile(uint32_t *counter, uint32_t num_tiles) {
+    const uint32_t t = atomicAdd(counter, 1u);
+    if (t == num_tiles - 1)
+        atomicExch(counter, 0u);
+    return t;
+}
+
+}  // namespace nrrs

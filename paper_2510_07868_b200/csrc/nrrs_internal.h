@@ -1,0 +1,130 @@
+// nrrs_internal.h -- kernel parameter blocks shared by nrrs_kernels.cu and the
+// C ABI layer (nrrs_capi.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace nrrs {
+
+// infer_kernel template kinds
+enum : int {
+    kKindHeuristic = 0,  // Fixed / Throughput / depth-1 pin (no MMA)
+    kKindAdrrs = 1,      // ADRRS-NN: StatNet -> adrrs_factor
+    kKindNrrs = 2,       // NRRS: StatNet -> build_nrrs_input -> RRSNet
+    kKindAid = 3,        // AID-NRRS: own grid + tail -> RRSNet
+    kKindStats = 4       // predict_stats batch (StatNet outputs only)
+};
+
+// One MLP layer inside the smem weight blob (byte offsets from the blob start).
+// W_hi / W_lo are the fp16 split of W in the UMMA K-major canonical layout
+// (N rows x K cols, 8x16B core matrices, LBO = 128 B, SBO = K*16 B).
+struct LayerDesc {
+    uint32_t w_hi, w_lo, bias;  // bias: N fp32 (padded with zeros)
+    uint16_t K, N;              // K in {16, 32}, N in {16, 32}
+};
+
+struct NetDesc {
+    LayerDesc layer[4];
+};
+
+struct KernelNets {
+    NetDesc stat, rrs;
+};
+
+struct GridDev {
+    int32_t levels;
+    int32_t base_resolution;
+    uint32_t table_size;
+    uint32_t dense_mask;  // bit l: level l is dense ((res+1)^3 <= T, hashgrid.hpp / hashgrid.cpp:16-22)
+};
+
+// Device-side scalar results of one stage call (mirrors nrrs_stage_result).
+struct DevResult {
+    double f_norm;
+    double sum_q;
+    unsigned long long total;
+    unsigned long long dropped;
+    unsigned long long nonfinite;
+    unsigned long long box_cox_clamps;
+    uint32_t spawned;
+    uint32_t overflow;
+};
+
+struct InferParams {
+    const float *p01, *wo01, *roughness, *weight, *i_pixel;
+    const uint64_t *path_key;
+    const uint32_t *pixel;
+    const float *i_acc;
+    uint64_t n;
+    uint32_t depth;
+    int32_t gate;       // 1: stage semantics (depth pin, lum gate, sanitize); 0: raw factor
+    int32_t heur_kind;  // 0 fixed, 1 throughput
+    float fixed_value;
+    float eps;          // max(eps_div, 1e-8)
+    uint64_t mixed_seed;  // mix_bits(seed)
+    const float2 *stat_grid, *rrs_grid;
+    GridDev grid;
+    const uint8_t *blob;
+    uint32_t blob_bytes;
+    KernelNets nets;
+    float *q_out, *u_out;
+    uint8_t *decided_out;
+    float *stats_out;
+    double *parts;     // [grid] per-CTA partial sums
+    uint32_t *part_counts; // [2*grid] per-CTA nonfinite / box_cox clamp counts
+    uint32_t *counter; // last-CTA-done counter (self-resetting)
+    double *sum_out;   // local sum of q
+    DevResult *res;
+};
+
+struct DecideParams {
+    const float *q, *u;
+    const int32_t *counts_in;
+    uint64_t n;
+    const double *rank_sums;
+    int32_t nranks;
+    uint64_t n_pixels;
+    float gain;
+    uint32_t capacity;
+    uint32_t parent_base;
+    float *q_norm, *q_real;
+    int32_t *k_out;
+    uint32_t *offset;
+    uint32_t *slots;
+    uint64_t *tile_state;
+    uint32_t *tile_counter;
+    uint32_t num_tiles;
+    uint32_t epoch;
+    uint32_t *err_flag;
+    unsigned long long *total_out;
+    DevResult *res;
+};
+
+struct CompactParams {
+    const void *in;
+    const uint8_t *used;
+    uint64_t count;
+    void *out;
+    uint32_t *count_out;
+    uint64_t *tile_state;
+    uint32_t *tile_counter;
+    uint32_t num_tiles;
+    uint32_t epoch;
+};
+
+size_t infer_smem_bytes(int kind, const InferParams &p);
+cudaError_t launch_infer(int kind, const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out);
+uint32_t infer_max_grid(int num_sms);
+uint32_t decide_tiles(uint64_t n);
+cudaError_t launch_decide(int src, const DecideParams &p, cudaStream_t stream);
+uint32_t compact_tiles(uint64_t count, uint32_t words);
+cudaError_t launch_compact(uint32_t words, const CompactParams &p, cudaStream_t stream);
+cudaError_t launch_sum_check(const float *q, uint64_t n, double *parts, uint32_t *counter, uint32_t *err,
+                             double *sum_out, uint32_t grid, cudaStream_t stream);
+cudaError_t launch_scale(float *q, uint64_t n, const double *sum, uint64_t n_pixels, const uint32_t *err,
+                         double *f_out, int num_sms, cudaStream_t stream);
+cudaError_t launch_realize(const float *q, const float *u, int32_t *counts, uint64_t n, uint32_t *err,
+                           unsigned long long *total, int num_sms, cudaStream_t stream);
+
+}  // namespace nrrs

@@ -1,0 +1,850 @@
+// nrrs_kernels.cu -- sm_100a kernels of the NRRS per-bounce RRS stage.
+//
+//   K-A infer_kernel<KIND>   strategy factor per vertex (hash grid + tcgen05 MLP
+//                            chain for the neural kinds), sanitize, RrsRound
+//                            uniform, deterministic per-CTA double partial sums
+//                            of q; the last CTA reduces them in fixed order.
+//   K-B decide_kernel<SRC>   normalization (F from the rank sums), gain,
+//                            stochastic rounding, single-pass decoupled
+//                            look-back scan (u64), capacity clip, coalesced
+//                            (parent, child) slot emission.
+//   K-C compact_kernel<W,I>  order-preserving stream compaction of W-word
+//                            records by a used mask, staged through smem.
+//
+// Reference: /root/reference/proj/src/wavefront.cpp:363-425 (+ :488-497),
+// networks.cpp:131-281, hashgrid.cpp:38-82, mlp.cpp:52-72, rrs.cpp:8-45.
+#include "nrrs_device.cuh"
+#include "nrrs_internal.h"
+
+#include <cuda_runtime.h>
+
+namespace nrrs {
+
+// ===========================================================================
+// K-A: factor inference
+// ===========================================================================
+constexpr int kTileM = 128;          // vertices per MMA tile (UMMA M)
+constexpr int kAChunkStride = 128;   // bytes between 16-byte K chunks (LBO)
+constexpr int kASbo = 512;           // bytes between 8-row groups (K = 32 -> 4 chunks)
+constexpr int kABytes = kTileM * 32 * 2;
+
+struct InferSmemHeader {
+    uint64_t mbar;
+    uint32_t tmem_base;
+    uint32_t is_last;
+    double warp_sums[4];
+    uint32_t warp_cnt[4];
+    uint32_t warp_bc[4];
+};
+
+// Writes one 32-wide (kchunks*8 used) fp32 row as fp16 hi/lo into the K-major
+// canonical A tiles (3-term split: x = hi + lo).
+__device__ __forceinline__ void write_a_row(uint8_t *a_hi, uint8_t *a_lo, int row, const float *x,
+                                            int kchunks) {
+    const int base = (row >> 3) * kASbo + (row & 7) * 16;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        if (c >= kchunks)
+            break;
+        uint32_t h[4], l[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float v0 = x[c * 8 + 2 * e], v1 = x[c * 8 + 2 * e + 1];
+            const __half h0 = __float2half_rn(v0), h1 = __float2half_rn(v1);
+            const __half l0 = __float2half_rn(v0 - __half2float(h0));
+            const __half l1 = __float2half_rn(v1 - __half2float(h1));
+            h[e] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+            l[e] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+        }
+        *reinterpret_cast<uint4 *>(a_hi + base + c * kAChunkStride) = make_uint4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<uint4 *>(a_lo + base + c * kAChunkStride) = make_uint4(l[0], l[1], l[2], l[3]);
+    }
+}
+
+// Barrier + one MMA layer (3-term split) + wait for the accumulator.
+__device__ __forceinline__ void mma_layer(const uint8_t *smem_w, const LayerDesc &L, const uint8_t *a_hi,
+                                          const uint8_t *a_lo, uint32_t tmem_d, uint64_t *bar,
+                                          uint32_t &phase) {
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        tc_fence_after();
+        const uint32_t idesc = make_idesc_f16(L.N);
+        const uint32_t a_hi_s = smem_u32(a_hi), a_lo_s = smem_u32(a_lo);
+        const uint32_t w_hi_s = smem_u32(smem_w + L.w_hi), w_lo_s = smem_u32(smem_w + L.w_lo);
+        const uint32_t w_sbo = (uint32_t)L.K * 16u;
+        for (uint32_t s = 0; s < (uint32_t)L.K / 16u; ++s) {
+            const uint64_t ah = make_smem_desc(a_hi_s + s * 256u, kAChunkStride, kASbo);
+            const uint64_t al = make_smem_desc(a_lo_s + s * 256u, kAChunkStride, kASbo);
+            const uint64_t wh = make_smem_desc(w_hi_s + s * 256u, kAChunkStride, w_sbo);
+            const uint64_t wl = make_smem_desc(w_lo_s + s * 256u, kAChunkStride, w_sbo);
+            mma_f16(tmem_d, ah, wh, idesc, s > 0 ? 1u : 0u);
+            mma_f16(tmem_d, al, wh, idesc, 1u);
+            mma_f16(tmem_d, ah, wl, idesc, 1u);
+        }
+        mma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    tc_fence_after();
+}
+
+// Runs a 3-hidden-layer MLP (mlp.cpp:52-72) for this thread's row. The input
+// row must already be in a_hi/a_lo.  Head outputs (N = 16 columns) land in y.
+__device__ __forceinline__ void run_mlp(const uint8_t *smem_w, const NetDesc &net, uint8_t *a_hi, uint8_t *a_lo,
+                                        uint32_t tmem_base, uint32_t tmem_row, uint64_t *bar, uint32_t &phase,
+                                        float (&y)[16]) {
+    const int row = threadIdx.x;
+#pragma unroll 1
+    for (int l = 0; l < 3; ++l) {
+        const LayerDesc &L = net.layer[l];
+        mma_layer(smem_w, L, a_hi, a_lo, tmem_base, bar, phase);
+        float acc[32];
+        tmem_ld32(tmem_row, acc);
+        const float *b = reinterpret_cast<const float *>(smem_w + L.bias);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            const float z = acc[i] + b[i];
+            const float zs = z * 0.01f;
+            acc[i] = z < zs ? zs : z;  // cwiseMax(z, slope * z)
+        }
+        write_a_row(a_hi, a_lo, row, acc, 4);
+    }
+    const LayerDesc &H = net.layer[3];
+    mma_layer(smem_w, H, a_hi, a_lo, tmem_base, bar, phase);
+    tmem_ld16(tmem_row, y);
+    const float *b = reinterpret_cast<const float *>(smem_w + H.bias);
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+        y[i] += b[i];
+}
+
+// HashGrid::encode for one point (hashgrid.cpp:38-82), F = 2, L <= 8.
+__device__ __forceinline__ void grid_encode(const float2 *__restrict__ theta, const GridDev &g, float px,
+                                            float py, float pz, float *out) {
+    const float cpx = clamp01(px), cpy = clamp01(py), cpz = clamp01(pz);
+#pragma unroll
+    for (int l = 0; l < 8; ++l) {
+        if (l >= g.levels) {
+            out[2 * l] = 0.0f;
+            out[2 * l + 1] = 0.0f;
+            continue;
+        }
+        const uint32_t res = (uint32_t)g.base_resolution << l;
+        const float resf = (float)res;
+        const float fx = cpx * resf, fy = cpy * resf, fz = cpz * resf;
+        const uint32_t cx = min((uint32_t)fx, res - 1u);
+        const uint32_t cy = min((uint32_t)fy, res - 1u);
+        const uint32_t cz = min((uint32_t)fz, res - 1u);
+        const float tx = fx - (float)cx, ty = fy - (float)cy, tz = fz - (float)cz;
+        const bool dense = (g.dense_mask >> l) & 1u;
+        const float2 *lvl = theta + (size_t)l * g.table_size;
+        uint32_t idx[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const uint32_t x = cx + (c & 1), y = cy + ((c >> 1) & 1), z = cz + ((c >> 2) & 1);
+            if (dense) {
+                const uint32_t nn = res + 1u;
+                idx[c] = (x * nn + y) * nn + z;
+            } else {
+                idx[c] = (x ^ (y * 2654435761u) ^ (z * 805459861u)) & (g.table_size - 1u);
+            }
+        }
+        float2 v[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+            v[c] = __ldg(lvl + idx[c]);
+        float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const float w = ((c & 1) ? tx : 1.0f - tx) * (((c >> 1) & 1) ? ty : 1.0f - ty) *
+                            (((c >> 2) & 1) ? tz : 1.0f - tz);
+            a0 += w * v[c].x;
+            a1 += w * v[c].y;
+        }
+        out[2 * l] = a0;
+        out[2 * l + 1] = a1;
+    }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kTileM, 4) infer_kernel(InferParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    constexpr bool kNeural = KIND != kKindHeuristic;
+    uint8_t *a_hi = smem_raw;
+    uint8_t *a_lo = smem_raw + kABytes;
+    uint8_t *smem_w = smem_raw + 2 * kABytes;
+    InferSmemHeader *hdr = reinterpret_cast<InferSmemHeader *>(kNeural ? smem_w + p.blob_bytes : smem_raw);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    uint32_t phase = 0;
+    uint32_t tmem_base = 0, tmem_row = 0;
+    if constexpr (kNeural) {
+        // weights: global blob -> smem (16-byte vector copies)
+        const uint4 *src = reinterpret_cast<const uint4 *>(p.blob);
+        uint4 *dst = reinterpret_cast<uint4 *>(smem_w);
+        for (uint32_t i = tid; i < p.blob_bytes / 16u; i += kTileM)
+            dst[i] = __ldg(src + i);
+        if (tid == 0) {
+            mbar_init(&hdr->mbar, 1);
+            fence_barrier_init();
+        }
+        if (warp == 0)
+            tmem_alloc(&hdr->tmem_base, 32);
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+        tmem_base = hdr->tmem_base;
+        tmem_row = tmem_base + ((uint32_t)(warp * 32) << 16);
+    }
+
+    const uint64_t n = p.n;
+    const uint64_t num_tiles = (n + kTileM - 1) / kTileM;
+    const uint64_t t_begin = num_tiles * blockIdx.x / gridDim.x;
+    const uint64_t t_end = num_tiles * (blockIdx.x + 1) / gridDim.x;
+    double cta_sum = 0.0;
+    uint32_t cta_nonfinite = 0, cta_bc = 0;
+
+    for (uint64_t tile = t_begin; tile < t_end; ++tile) {
+        const uint64_t j = tile * kTileM + tid;
+        const bool valid = j < n;
+        float px = 0, py = 0, pz = 0, wox = 0, woy = 0, rough = 0, wx = 0, wy = 0, wz = 0, ipx = 0, ipy = 0, ipz = 0;
+        uint64_t key = 0;
+        if (valid) {
+            px = __ldg(p.p01 + 3 * j); py = __ldg(p.p01 + 3 * j + 1); pz = __ldg(p.p01 + 3 * j + 2);
+            wx = __ldg(p.weight + 3 * j); wy = __ldg(p.weight + 3 * j + 1); wz = __ldg(p.weight + 3 * j + 2);
+            key = __ldg(p.path_key + j);
+            if (KIND != kKindHeuristic) {
+                wox = __ldg(p.wo01 + 2 * j); woy = __ldg(p.wo01 + 2 * j + 1);
+                rough = __ldg(p.roughness + j);
+            }
+            if (KIND == kKindNrrs || KIND == kKindAid || KIND == kKindAdrrs) {
+                if (p.i_pixel) {
+                    ipx = __ldg(p.i_pixel + 3 * j); ipy = __ldg(p.i_pixel + 3 * j + 1); ipz = __ldg(p.i_pixel + 3 * j + 2);
+                } else {
+                    const uint64_t px_idx = __ldg(p.pixel + j);
+                    ipx = __ldg(p.i_acc + 3 * px_idx); ipy = __ldg(p.i_acc + 3 * px_idx + 1);
+                    ipz = __ldg(p.i_acc + 3 * px_idx + 2);
+                }
+            }
+        }
+        const float lum_w = luminance(wx, wy, wz);
+        // Mix-Depth gate + zero-throughput skip (wavefront.cpp:373-380)
+        const bool depth1 = p.depth == 1u;
+        const bool active = valid && (p.gate ? (!depth1 && lum_w > 0.0f) : true);
+        float q = 0.0f;
+        uint32_t bc = 0;
+
+        if constexpr (KIND == kKindHeuristic) {
+            if (p.heur_kind == 0)
+                q = p.fixed_value;                              // Fixed (wavefront.cpp:193-194)
+            else
+                q = (lum_w < 1.0f) ? lum_w : 1.0f;              // std::min(1, lum) (rrs.hpp:49-51)
+        } else {
+            float x[32];
+            float y[16];
+            if (KIND == kKindAid) {
+                grid_encode(p.rrs_grid, p.grid, px, py, pz, x);
+            } else {
+                grid_encode(p.stat_grid, p.grid, px, py, pz, x);
+            }
+            // kernel K layout (host packs W columns to match): grid features of
+            // levels 0..7 in [0,16) (zero past L), the 16-wide tail in [16,32)
+            // (networks.cpp:131-135 / :149-157).
+            float *tail = x + 16;
+            if (KIND == kKindAid) {
+                one_blob<4>(wox, tail);
+                one_blob<4>(woy, tail + 4);
+                tail[8] = box_cox(wx, bc);
+                tail[9] = box_cox(wy, bc);
+                tail[10] = box_cox(wz, bc);
+                tail[11] = box_cox(mean3(ipx, ipy, ipz), bc);
+                one_blob<4>(roughness_remap(rough), tail + 12);
+            } else {
+                one_blob<4>(wox, tail);
+                one_blob<4>(woy, tail + 4);
+                one_blob<8>(roughness_remap(rough), tail + 8);
+            }
+            if (!active) {
+#pragma unroll
+                for (int s = 0; s < 32; ++s)
+                    x[s] = 0.0f;
+            }
+            write_a_row(a_hi, a_lo, tid, x, 4);
+            if (KIND == kKindAid) {
+                run_mlp(smem_w, p.nets.rrs, a_hi, a_lo, tmem_base, tmem_row, &hdr->mbar, phase, y);
+                q = softplus_mod(y[0]);
+            } else {
+                run_mlp(smem_w, p.nets.stat, a_hi, a_lo, tmem_base, tmem_row, &hdr->mbar, phase, y);
+                if (KIND == kKindStats) {
+                    if (valid) {
+#pragma unroll
+                        for (int i = 0; i < 6; ++i)
+                            p.stats_out[6 * j + i] = y[i];
+                    }
+                } else if (KIND == kKindAdrrs) {
+                    // adrrs_factor (rrs.hpp:56-61) with eps = max(eps_div, 1e-8)
+                    const float num = luminance(wx * y[0], wy * y[1], wz * y[2]);
+                    const float qq = num / (luminance(ipx, ipy, ipz) + p.eps);
+                    q = qq < 0.05f ? 0.05f : (20.0f < qq ? 20.0f : qq);
+                } else {  // NRRS: stats -> build_nrrs_input (networks.cpp:137-147) -> RRSNet
+                    float xin[16];
+                    uint32_t bc2 = 0;
+#pragma unroll
+                    for (int c = 0; c < 6; ++c)
+                        xin[c] = box_cox(y[c], bc2);
+                    xin[6] = box_cox(wx, bc2);
+                    xin[7] = box_cox(wy, bc2);
+                    xin[8] = box_cox(wz, bc2);
+                    xin[9] = box_cox(mean3(ipx, ipy, ipz), bc2);
+                    xin[10] = roughness_remap(rough);
+#pragma unroll
+                    for (int c = 11; c < 16; ++c)
+                        xin[c] = 0.0f;
+                    if (!active) {
+#pragma unroll
+                        for (int c = 0; c < 16; ++c)
+                            xin[c] = 0.0f;
+                        bc2 = 0;
+                    }
+                    bc += bc2;
+                    write_a_row(a_hi, a_lo, tid, xin, 2);
+                    run_mlp(smem_w, p.nets.rrs, a_hi, a_lo, tmem_base, tmem_row, &hdr->mbar, phase, y);
+                    q = softplus_mod(y[0]);
+                }
+            }
+        }
+        if (!active)
+            bc = 0;
+
+        if constexpr (KIND != kKindStats) {
+            uint32_t decided = active ? 1u : 0u;
+            uint32_t nonfinite = 0;
+            if (p.gate) {
+                if (valid && depth1)
+                    q = 1.0f;  // depth-1 pin (wavefront.cpp:373-375)
+                if (!active && !depth1)
+                    q = 0.0f;
+                decided = valid && (depth1 || active) ? 1u : 0u;
+                if (valid && (!isfinite(q) || q < 0.0f)) {  // sanitize (wavefront.cpp:381-385)
+                    q = 0.0f;
+                    decided = 0;
+                    nonfinite = 1;
+                }
+            }
+            if (!valid)
+                q = 0.0f;
+            if (valid) {
+                p.q_out[j] = q;
+                if (p.u_out)
+                    p.u_out[j] = rrs_uniform(p.mixed_seed, key, p.depth);
+                if (p.decided_out)
+                    p.decided_out[j] = (uint8_t)decided;
+            }
+            // deterministic tile sum: butterfly per warp, then warps in order
+            double s = (double)q;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+                s += __shfl_xor_sync(0xffffffffu, s, o);
+            uint32_t nf = __reduce_add_sync(0xffffffffu, nonfinite);
+            uint32_t bcs = __reduce_add_sync(0xffffffffu, bc);
+            if (lane == 0) {
+                hdr->warp_sums[warp] = s;
+                hdr->warp_cnt[warp] = nf;
+                hdr->warp_bc[warp] = bcs;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                cta_sum += ((hdr->warp_sums[0] + hdr->warp_sums[1]) + hdr->warp_sums[2]) + hdr->warp_sums[3];
+                cta_nonfinite += hdr->warp_cnt[0] + hdr->warp_cnt[1] + hdr->warp_cnt[2] + hdr->warp_cnt[3];
+                cta_bc += hdr->warp_bc[0] + hdr->warp_bc[1] + hdr->warp_bc[2] + hdr->warp_bc[3];
+            }
+            __syncthreads();
+        }
+    }
+
+    if constexpr (kNeural) {
+        tc_fence_before();
+        __syncthreads();
+        if (warp == 0)
+            tmem_dealloc(hdr->tmem_base, 32);
+    }
+    if constexpr (KIND == kKindStats)
+        return;
+    if (p.parts == nullptr)
+        return;
+    // ---- last-CTA-done reduction of the per-CTA partial sums in CTA order ----
+    if (tid == 0) {
+        p.parts[blockIdx.x] = cta_sum;
+        p.part_counts[2 * blockIdx.x] = cta_nonfinite;
+        p.part_counts[2 * blockIdx.x + 1] = cta_bc;
+        __threadfence();
+        const uint32_t prev = atomicAdd(p.counter, 1u);
+        hdr->is_last = (prev == gridDim.x - 1) ? 1u : 0u;
+    }
+    __syncthreads();
+    if (!hdr->is_last)
+        return;
+    __threadfence();
+    double s = 0.0;
+    uint32_t nf = 0, bcs = 0;
+    for (uint32_t b = tid; b < gridDim.x; b += kTileM) {
+        s += __ldcg(p.parts + b);
+        nf += __ldcg(p.part_counts + 2 * b);
+        bcs += __ldcg(p.part_counts + 2 * b + 1);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+    nf = __reduce_add_sync(0xffffffffu, nf);
+    bcs = __reduce_add_sync(0xffffffffu, bcs);
+    if (lane == 0) {
+        hdr->warp_sums[warp] = s;
+        hdr->warp_cnt[warp] = nf;
+        hdr->warp_bc[warp] = bcs;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const double total = ((hdr->warp_sums[0] + hdr->warp_sums[1]) + hdr->warp_sums[2]) + hdr->warp_sums[3];
+        *p.sum_out = total;
+        p.res->sum_q = total;
+        p.res->nonfinite = hdr->warp_cnt[0] + hdr->warp_cnt[1] + hdr->warp_cnt[2] + hdr->warp_cnt[3];
+        p.res->box_cox_clamps = hdr->warp_bc[0] + hdr->warp_bc[1] + hdr->warp_bc[2] + hdr->warp_bc[3];
+        *p.counter = 0;  // self-cleaning for the next launch
+    }
+}
+
+// ===========================================================================
+// K-B: normalize + realize + scan + slot emission
+// ===========================================================================
+constexpr int kDecThreads = 256;
+constexpr int kDecItems = 8;
+constexpr int kDecTile = kDecThreads * kDecItems;
+
+struct DecideSmem {
+    uint32_t incl[kDecTile];
+    uint32_t warp_tot[kDecThreads / 32];
+    uint64_t prefix;
+    uint32_t tile;
+};
+
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t *warp_tot, uint32_t &total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o)
+            inc += t;
+    }
+    if (lane == 31)
+        warp_tot[warp] = inc;
+    __syncthreads();
+    uint32_t before = 0, all = 0;
+#pragma unroll
+    for (int w = 0; w < kDecThreads / 32; ++w) {
+        const uint32_t t = warp_tot[w];
+        if (w < warp)
+            before += t;
+        all += t;
+    }
+    total = all;
+    return before + inc - v;
+}
+
+template <int SRC>  // 0: counts from (q, u) with normalization; 1: counts given (plan_spawns)
+__global__ void __launch_bounds__(kDecThreads) decide_kernel(DecideParams p) {
+    __shared__ DecideSmem sm;
+    const int tid = threadIdx.x;
+    if (tid == 0)
+        sm.tile = claim_tile(p.tile_counter, p.num_tiles);
+    __syncthreads();
+    const uint32_t tile = sm.tile;
+    const uint64_t base = (uint64_t)tile * kDecTile;
+    const uint64_t first = base + (uint64_t)tid * kDecItems;
+
+    // F from the rank sums in rank order (rrs.cpp:8-24 with the tile-sharded
+    // global budget)
+    bool apply = false;
+    float scale = 1.0f;
+    if (SRC == 0) {
+        double sum = 0.0;
+        for (int r = 0; r < p.nranks; ++r)
+            sum += p.rank_sums[r];
+        if (sum > 0.0) {
+            const double f = __ddiv_rn((double)p.n_pixels, sum);
+            if (f < 1.0) {
+                apply = true;
+                scale = __double2float_rn(f);
+            }
+            if (tile == 0 && tid == 0 && p.res)
+                p.res->f_norm = f;
+        } else if (tile == 0 && tid == 0 && p.res) {
+            p.res->f_norm = 1.0;
+        }
+    }
+
+    uint32_t k[kDecItems];
+    uint32_t bad = 0;
+    if (SRC == 0) {
+        float q[kDecItems], u[kDecItems];
+        const bool full = first + kDecItems <= p.n;
+        if (full) {
+            const float4 *q4 = reinterpret_cast<const float4 *>(p.q + first);
+            const float4 *u4 = reinterpret_cast<const float4 *>(p.u + first);
+            const float4 qa = __ldcs(q4), qb = __ldcs(q4 + 1), ua = __ldcs(u4), ub = __ldcs(u4 + 1);
+            q[0] = qa.x; q[1] = qa.y; q[2] = qa.z; q[3] = qa.w; q[4] = qb.x; q[5] = qb.y; q[6] = qb.z; q[7] = qb.w;
+            u[0] = ua.x; u[1] = ua.y; u[2] = ua.z; u[3] = ua.w; u[4] = ub.x; u[5] = ub.y; u[6] = ub.z; u[7] = ub.w;
+        } else {
+#pragma unroll
+            for (int i = 0; i < kDecItems; ++i) {
+                const bool ok = first + i < p.n;
+                q[i] = ok ? p.q[first + i] : 0.0f;
+                u[i] = ok ? p.u[first + i] : 0.0f;
+            }
+        }
+        float qn[kDecItems], qr[kDecItems];
+#pragma unroll
+        for (int i = 0; i < kDecItems; ++i) {
+            qn[i] = apply ? __fmul_rn(q[i], scale) : q[i];  // q *= float(F)  (rrs.cpp:18-21)
+            qr[i] = __fmul_rn(qn[i], p.gain);               // q_real = q * gain (wavefront.cpp:396)
+            k[i] = stochastic_round(qr[i], u[i]);
+        }
+        if (full) {
+            float4 *o1 = reinterpret_cast<float4 *>(p.q_norm + first);
+            float4 *o2 = reinterpret_cast<float4 *>(p.q_real + first);
+            __stcs(o1, make_float4(qn[0], qn[1], qn[2], qn[3]));
+            __stcs(o1 + 1, make_float4(qn[4], qn[5], qn[6], qn[7]));
+            __stcs(o2, make_float4(qr[0], qr[1], qr[2], qr[3]));
+            __stcs(o2 + 1, make_float4(qr[4], qr[5], qr[6], qr[7]));
+        } else {
+#pragma unroll
+            for (int i = 0; i < kDecItems; ++i)
+                if (first + i < p.n) {
+                    p.q_norm[first + i] = qn[i];
+                    p.q_real[first + i] = qr[i];
+                }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < kDecItems; ++i) {
+            const int32_t c = first + i < p.n ? p.counts_in[first + i] : 0;
+            if (c < 0)
+                bad = 1;
+            k[i] = c < 0 ? 0u : (uint32_t)c;
+        }
+    }
+    if (bad)
+        atomicOr(p.err_flag, 1u);
+
+    uint32_t tsum = 0;
+#pragma unroll
+    for (int i = 0; i < kDecItems; ++i)
+        tsum += k[i];
+    uint32_t agg = 0;
+    const uint32_t texcl = block_exclusive_scan(tsum, sm.warp_tot, agg);
+    {
+        uint32_t run = texcl;
+#pragma unroll
+        for (int i = 0; i < kDecItems; ++i) {
+            run += k[i];
+            sm.incl[tid * kDecItems + i] = run;
+        }
+    }
+    if (tid == 0)
+        sm.prefix = lookback_exclusive(p.tile_state, tile, agg, p.epoch);
+    __syncthreads();
+    const uint64_t P = sm.prefix;
+    const uint64_t cap = p.capacity;
+
+    if (p.offset || p.k_out) {
+        uint64_t cum = P + texcl;
+#pragma unroll
+        for (int i = 0; i < kDecItems; ++i) {
+            if (first + i < p.n) {
+                if (p.offset)
+                    p.offset[first + i] = (uint32_t)(cum < cap ? cum : cap);  // min(cum, capacity)
+                if (p.k_out)
+                    p.k_out[first + i] = (int32_t)k[i];
+            }
+            cum += k[i];
+        }
+    }
+
+    // slot records: slot s in [min(P,cap), min(P+agg,cap)) -> (parent j, child c)
+    // (kept = min(k, cap - min(cum, cap)), wavefront.cpp:421-425, :436)
+    if (p.slots && P < cap) {
+        const uint64_t s_end64 = P + agg < cap ? P + agg : cap;
+        const uint32_t s_count = (uint32_t)(s_end64 - P);
+        uint2 *slots = reinterpret_cast<uint2 *>(p.slots);
+        for (uint32_t local = tid; local < s_count; local += kDecThreads) {
+            // first item whose inclusive prefix exceeds `local`
+            uint32_t lo = 0, hi = kDecTile;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (sm.incl[mid] > local)
+                    hi = mid;
+                else
+                    lo = mid + 1;
+            }
+            const uint32_t before = lo ? sm.incl[lo - 1] : 0u;
+            __stcs(slots + P + local, make_uint2((uint32_t)(base + lo) + p.parent_base, local - before));
+        }
+    }
+
+    if (tile == p.num_tiles - 1 && tid == 0) {
+        const uint64_t total = P + agg;
+        if (p.total_out)
+            *p.total_out = total;
+        if (p.res) {
+            const uint64_t spawned = total < cap ? total : cap;
+            p.res->total = total;
+            p.res->spawned = (uint32_t)spawned;
+            p.res->dropped = total - spawned;
+            p.res->overflow = total > spawned ? 1u : 0u;
+        }
+    }
+}
+
+// ===========================================================================
+// K-C: stable compaction of W-word records
+// ===========================================================================
+template <int W, int IPT>
+__global__ void __launch_bounds__(kDecThreads) compact_kernel(CompactParams p) {
+    constexpr int kTile = kDecThreads * IPT;
+    __shared__ uint32_t stage[kTile * W];
+    __shared__ uint32_t warp_tot[kDecThreads / 32];
+    __shared__ uint64_t prefix_s;
+    __shared__ uint32_t tile_s;
+    const int tid = threadIdx.x;
+    if (tid == 0)
+        tile_s = claim_tile(p.tile_counter, p.num_tiles);
+    __syncthreads();
+    const uint32_t tile = tile_s;
+    const uint64_t base = (uint64_t)tile * kTile;
+    const uint64_t first = base + (uint64_t)tid * IPT;
+    uint32_t keep[IPT];
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+        keep[i] = (first + i < p.count && p.used[first + i]) ? 1u : 0u;
+        cnt += keep[i];
+    }
+    uint32_t agg = 0;
+    const uint32_t excl = block_exclusive_scan(cnt, warp_tot, agg);
+    if (tid == 0)
+        prefix_s = lookback_exclusive(p.tile_state, tile, agg, p.epoch);
+    const uint32_t *in = reinterpret_cast<const uint32_t *>(p.in);
+    uint32_t pos = excl;
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+        if (keep[i]) {
+#pragma unroll
+            for (int w = 0; w < W; ++w)
+                stage[pos * W + w] = __ldcs(in + (first + i) * W + w);
+            ++pos;
+        }
+    }
+    __syncthreads();
+    const uint64_t P = prefix_s;
+    uint32_t *out = reinterpret_cast<uint32_t *>(p.out) + P * W;
+    for (uint32_t w = tid; w < agg * W; w += kDecThreads)
+        __stcs(out + w, stage[w]);
+    if (tile == p.num_tiles - 1 && tid == 0)
+        *p.count_out = (uint32_t)(P + agg);
+}
+
+// ===========================================================================
+// granular helpers: normalize_factors / realize_counts
+// ===========================================================================
+__global__ void __launch_bounds__(256) sum_check_kernel(const float *q, uint64_t n, double *parts,
+                                                        uint32_t *counter, uint32_t *err, double *sum_out) {
+    __shared__ double ws[8];
+    __shared__ uint32_t is_last;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t begin = n * blockIdx.x / gridDim.x, end = n * (blockIdx.x + 1) / gridDim.x;
+    double s = 0.0;
+    uint32_t bad = 0;
+    for (uint64_t i = begin + tid; i < end; i += 256) {
+        const float v = q[i];
+        if (!(v >= 0.0f) || !isfinite(v))
+            bad = 1;
+        s += (double)v;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (__any_sync(0xffffffffu, bad) && lane == 0)
+        atomicOr(err, 1u);
+    if (lane == 0)
+        ws[warp] = s;
+    __syncthreads();
+    if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w)
+            t += ws[w];
+        parts[blockIdx.x] = t;
+        __threadfence();
+        is_last = atomicAdd(counter, 1u) == gridDim.x - 1 ? 1u : 0u;
+    }
+    __syncthreads();
+    if (!is_last)
+        return;
+    __threadfence();
+    double t = 0.0;
+    for (uint32_t b = tid; b < gridDim.x; b += 256)
+        t += __ldcg(parts + b);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0)
+        ws[warp] = t;
+    __syncthreads();
+    if (tid == 0) {
+        double tot = 0.0;
+        for (int w = 0; w < 8; ++w)
+            tot += ws[w];
+        *sum_out = tot;
+        *counter = 0;
+    }
+}
+
+__global__ void scale_kernel(float *q, uint64_t n, const double *sum, uint64_t n_pixels, const uint32_t *err,
+                             double *f_out) {
+    if (*err)
+        return;
+    const double s = *sum;
+    if (!(s > 0.0)) {
+        if (blockIdx.x == 0 && threadIdx.x == 0)
+            *f_out = 1.0;
+        return;
+    }
+    const double f = __ddiv_rn((double)n_pixels, s);
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        *f_out = f;
+    if (!(f < 1.0))
+        return;
+    const float sc = __double2float_rn(f);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        q[i] = __fmul_rn(q[i], sc);
+}
+
+__global__ void realize_kernel(const float *q, const float *u, int32_t *counts, uint64_t n, uint32_t *err,
+                               unsigned long long *total) {
+    uint64_t local = 0;
+    uint32_t bad = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const float v = q[i];
+        if (!(v >= 0.0f) || !isfinite(v)) {
+            bad = 1;
+            counts[i] = 0;
+            continue;
+        }
+        const uint32_t k = stochastic_round(v, u[i]);
+        counts[i] = (int32_t)k;
+        local += k;
+    }
+    if (bad)
+        atomicOr(err, 1u);
+    if (local)
+        atomicAdd(total, (unsigned long long)local);
+}
+
+// ===========================================================================
+// launch wrappers (called from the C ABI layer)
+// ===========================================================================
+template <int KIND>
+static int infer_occupancy(size_t smem) {
+    int nb = 0;
+    cudaFuncSetAttribute(infer_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, infer_kernel<KIND>, kTileM, smem);
+    return nb < 1 ? 1 : nb;
+}
+
+size_t infer_smem_bytes(int kind, const InferParams &p) {
+    if (kind == kKindHeuristic)
+        return sizeof(InferSmemHeader) + 64;
+    return 2 * kABytes + p.blob_bytes + sizeof(InferSmemHeader) + 64;
+}
+
+cudaError_t launch_infer(int kind, const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out) {
+    const uint64_t tiles = (p.n + kTileM - 1) / kTileM;
+    const size_t smem = infer_smem_bytes(kind, p);
+    int occ = 1;
+    switch (kind) {
+    case kKindHeuristic: occ = infer_occupancy<kKindHeuristic>(smem); break;
+    case kKindAdrrs: occ = infer_occupancy<kKindAdrrs>(smem); break;
+    case kKindNrrs: occ = infer_occupancy<kKindNrrs>(smem); break;
+    case kKindAid: occ = infer_occupancy<kKindAid>(smem); break;
+    case kKindStats: occ = infer_occupancy<kKindStats>(smem); break;
+    }
+    if (kind != kKindHeuristic && occ > 4)
+        occ = 4;  // <= 4 x 32 TMEM columns per SM leaves room for other tenants
+    uint64_t grid = (uint64_t)num_sms * (uint64_t)occ;
+    if (grid > tiles)
+        grid = tiles;
+    if (grid < 1)
+        grid = 1;
+    *grid_out = (uint32_t)grid;
+    switch (kind) {
+    case kKindHeuristic: infer_kernel<kKindHeuristic><<<(uint32_t)grid, kTileM, smem, stream>>>(p); break;
+    case kKindAdrrs: infer_kernel<kKindAdrrs><<<(uint32_t)grid, kTileM, smem, stream>>>(p); break;
+    case kKindNrrs: infer_kernel<kKindNrrs><<<(uint32_t)grid, kTileM, smem, stream>>>(p); break;
+    case kKindAid: infer_kernel<kKindAid><<<(uint32_t)grid, kTileM, smem, stream>>>(p); break;
+    case kKindStats: infer_kernel<kKindStats><<<(uint32_t)grid, kTileM, smem, stream>>>(p); break;
+    default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+uint32_t infer_max_grid(int num_sms) { return (uint32_t)num_sms * 16u; }
+
+uint32_t decide_tiles(uint64_t n) { return (uint32_t)((n + kDecTile - 1) / kDecTile); }
+
+cudaError_t launch_decide(int src, const DecideParams &p, cudaStream_t stream) {
+    if (p.num_tiles == 0)
+        return cudaSuccess;
+    if (src == 0)
+        decide_kernel<0><<<p.num_tiles, kDecThreads, 0, stream>>>(p);
+    else
+        decide_kernel<1><<<p.num_tiles, kDecThreads, 0, stream>>>(p);
+    return cudaGetLastError();
+}
+
+uint32_t compact_tiles(uint64_t count, uint32_t words) {
+    const uint32_t tile = words == 2 ? kDecThreads * 8 : kDecThreads * 1;
+    return (uint32_t)((count + tile - 1) / tile);
+}
+
+cudaError_t launch_compact(uint32_t words, const CompactParams &p, cudaStream_t stream) {
+    if (p.num_tiles == 0)
+        return cudaSuccess;
+    if (words == 2)
+        compact_kernel<2, 8><<<p.num_tiles, kDecThreads, 0, stream>>>(p);
+    else if (words == 18)
+        compact_kernel<18, 1><<<p.num_tiles, kDecThreads, 0, stream>>>(p);
+    else
+        return cudaErrorInvalidValue;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sum_check(const float *q, uint64_t n, double *parts, uint32_t *counter, uint32_t *err,
+                             double *sum_out, uint32_t grid, cudaStream_t stream) {
+    sum_check_kernel<<<grid, 256, 0, stream>>>(q, n, parts, counter, err, sum_out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scale(float *q, uint64_t n, const double *sum, uint64_t n_pixels, const uint32_t *err,
+                         double *f_out, int num_sms, cudaStream_t stream) {
+    scale_kernel<<<num_sms * 4, 256, 0, stream>>>(q, n, sum, n_pixels, err, f_out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_realize(const float *q, const float *u, int32_t *counts, uint64_t n, uint32_t *err,
+                           unsigned long long *total, int num_sms, cudaStream_t stream) {
+    realize_kernel<<<num_sms * 4, 256, 0, stream>>>(q, u, counts, n, err, total);
+    return cudaGetLastError();
+}
+
+}  // namespace nrrs

@@ -1,0 +1,267 @@
+"""The per-bounce RRS stage on the GPU -- the drop-in for trace_frame's RRS
+decision block (wavefront.cpp:363-425, compaction :488-497).
+
+`RrsStage` owns one nrrs_gpu_ctx (one CUDA device, the current torch stream)
+and mirrors the reference's call sequence for one depth:
+
+    strat = assignment[depth-1]                      # Mix-Depth gate (:366)
+    q     = strategy_factor(...) per vertex          # (:368-389)
+    F     = normalize_factors(q, n_pixels)           # (:390)
+    gain  = rc.gain() if depth >= 2 and adaptive     # (:391)
+    k     = realize_counts(q*gain, u)                # (:393-404)
+    plan  = plan_spawns(k, capacity)                 # (:406)
+    if plan.dropped: rc.note_overflow()              # (:407-411)
+    slots = (parent j, child c) per queue slot       # (:421-425)
+
+All arrays are torch CUDA tensors; the host only sequences launches.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+from typing import Dict, Optional
+
+import numpy as np
+import torch
+
+from . import _capi
+from .networks import NeuralRrs
+from .rrs import RateControl, Strategy, StrategyKind, queue_capacity_for
+
+VERTEX_FIELDS = ("p01", "wo01", "roughness", "weight", "i_pixel", "path_key")
+FIELD_SHAPES = {"p01": 3, "wo01": 2, "roughness": 1, "weight": 3, "i_pixel": 3, "path_key": 1}
+
+
+@dataclasses.dataclass
+class StageResult:
+    """Scalars of one stage call (SpawnPlan + FrameReport increments)."""
+    f_norm: float
+    sum_q: float
+    total: int
+    spawned: int
+    dropped: int
+    nonfinite: int
+    box_cox_clamps: int
+    overflow: bool
+
+    @classmethod
+    def from_c(cls, r: _capi.StageResultC) -> "StageResult":
+        return cls(r.f_norm, r.sum_q, r.total, r.spawned, r.dropped, r.nonfinite, r.box_cox_clamps,
+                   bool(r.overflow))
+
+
+@dataclasses.dataclass
+class StageOutputs:
+    q_norm: torch.Tensor
+    q_real: torch.Tensor
+    slots: torch.Tensor          # [capacity, 2] int32 view of (parent, child) uint32
+    k: Optional[torch.Tensor] = None
+    offset: Optional[torch.Tensor] = None
+    decided: Optional[torch.Tensor] = None
+    q_orig: Optional[torch.Tensor] = None
+    u: Optional[torch.Tensor] = None
+
+    def c(self) -> _capi.StageOut:
+        def p(t):
+            return t.data_ptr() if t is not None else None
+        return _capi.StageOut(p(self.q_norm), p(self.q_real), p(self.slots), p(self.k), p(self.offset),
+                              p(self.decided), p(self.q_orig), p(self.u))
+
+
+def vertex_soa(v: Dict[str, torch.Tensor]) -> _capi.VertexSoA:
+    """nrrs_vertex_soa from a dict of contiguous CUDA tensors (float32; path_key int64/uint64)."""
+    def p(name):
+        t = v.get(name)
+        if t is None:
+            return None
+        if not t.is_contiguous():
+            raise RuntimeError(f"vertex field {name} must be contiguous")
+        return t.data_ptr()
+    return _capi.VertexSoA(p("p01"), p("wo01"), p("roughness"), p("weight"), p("i_pixel"), p("path_key"),
+                           p("pixel"), p("i_acc"))
+
+
+class GpuContext:
+    """One nrrs_gpu_ctx bound to a CUDA device."""
+
+    def __init__(self, device: int = 0):
+        if not torch.cuda.is_available():
+            raise RuntimeError("nrrs: a CUDA (sm_100a) device is required; there is no CPU path")
+        self.lib = _capi.lib()
+        self.device = device
+        h = C.c_void_p()
+        rc = self.lib.nrrs_gpu_create(device, C.byref(h))
+        if rc != 0:
+            raise _capi.NrrsError(rc, f"nrrs_gpu_create(device={device}) failed (sm_100 device required)")
+        self.handle = h
+
+    def bind_stream(self, stream: Optional[torch.cuda.Stream] = None) -> None:
+        s = stream or torch.cuda.current_stream(self.device)
+        _capi.check(self.handle, self.lib.nrrs_gpu_set_stream(self.handle, C.c_void_p(s.cuda_stream)))
+
+    def launch_count(self) -> int:
+        return int(self.lib.nrrs_gpu_launch_count(self.handle))
+
+    def close(self) -> None:
+        if self.handle:
+            self.lib.nrrs_gpu_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_DEFAULT: Dict[int, GpuContext] = {}
+
+
+def default_context(device: Optional[int] = None) -> GpuContext:
+    dev = torch.cuda.current_device() if device is None else device
+    if dev not in _DEFAULT:
+        _DEFAULT[dev] = GpuContext(dev)
+    ctx = _DEFAULT[dev]
+    ctx.bind_stream()
+    return ctx
+
+
+class RrsStage:
+    """Drop-in RRS decision stage for one film (n_pixels) on one GPU."""
+
+    def __init__(self, n_pixels: int, nets: Optional[NeuralRrs] = None, capacity: int = 0, seed: int = 0,
+                 device: int = 0):
+        self.ctx = GpuContext(device)
+        self.ctx.bind_stream()
+        self.n_pixels = int(n_pixels)
+        self.capacity = int(capacity) if capacity else queue_capacity_for(self.n_pixels)
+        if self.capacity < self.n_pixels:
+            raise RuntimeError("trace_frame: queue capacity below the pixel count")
+        self.seed = int(seed)
+        self.device = torch.device("cuda", device)
+        self.nets = None
+        if nets is not None:
+            self.set_weights(nets)
+
+    @property
+    def handle(self):
+        return self.ctx.handle
+
+    def set_weights(self, nets: NeuralRrs) -> None:
+        """Uploads the published snapshot (NeuralRrs::publish, networks.cpp:199-204)."""
+        w = nets.weights_c()
+        _capi.check(self.handle, self.ctx.lib.nrrs_gpu_set_weights(self.handle, C.byref(w)))
+        self.nets = nets
+
+    def reserve(self, max_vertices: int) -> None:
+        _capi.check(self.handle, self.ctx.lib.nrrs_gpu_reserve(self.handle, int(max_vertices), self.capacity))
+
+    def alloc_outputs(self, n: int, full: bool = False) -> StageOutputs:
+        dev = self.device
+        o = StageOutputs(q_norm=torch.empty(n, dtype=torch.float32, device=dev),
+                         q_real=torch.empty(n, dtype=torch.float32, device=dev),
+                         slots=torch.empty((self.capacity, 2), dtype=torch.int32, device=dev))
+        if full:
+            o.k = torch.empty(n, dtype=torch.int32, device=dev)
+            o.offset = torch.empty(n, dtype=torch.int32, device=dev)
+            o.decided = torch.empty(n, dtype=torch.uint8, device=dev)
+            o.q_orig = torch.empty(n, dtype=torch.float32, device=dev)
+            o.u = torch.empty(n, dtype=torch.float32, device=dev)
+        return o
+
+    def params(self, depth: int, strategy: Strategy, gain: float, eps_div: float = 0.0,
+               n_pixels: Optional[int] = None) -> _capi.StageParams:
+        return _capi.StageParams(int(depth), int(n_pixels if n_pixels is not None else self.n_pixels),
+                                 self.capacity, strategy.c(), float(gain), float(eps_div), self.seed)
+
+    def run(self, vertices: Dict[str, torch.Tensor], depth: int, strategy: Strategy,
+            rc: Optional[RateControl] = None, eps_div: float = 0.0, out: Optional[StageOutputs] = None,
+            sync: bool = True, full: bool = False):
+        """One depth of the decision block.  With sync=True returns (outputs, StageResult)
+        and applies rc.note_overflow() on a dropped tail like wavefront.cpp:407-411."""
+        self.ctx.bind_stream()
+        n = int(vertices["p01"].shape[0]) if vertices["p01"].dim() == 2 else vertices["p01"].numel() // 3
+        if out is None:
+            out = self.alloc_outputs(n, full=full)
+        gain = rc.gain() if rc is not None else 1.0
+        p = self.params(depth, strategy, gain, eps_div)
+        soa = vertex_soa(vertices)
+        oc = out.c()
+        if sync:
+            r = _capi.StageResultC()
+            _capi.check(self.handle, self.ctx.lib.nrrs_gpu_rrs_stage(self.handle, C.byref(soa), n, C.byref(p),
+                                                                     C.byref(oc), C.byref(r)))
+            res = StageResult.from_c(r)
+            if rc is not None and res.dropped > 0:
+                rc.note_overflow()
+            return out, res
+        _capi.check(self.handle, self.ctx.lib.nrrs_gpu_rrs_stage(self.handle, C.byref(soa), n, C.byref(p),
+                                                                 C.byref(oc), None))
+        return out, None
+
+    def run_host(self, vertices: Dict[str, np.ndarray], depth: int, strategy: Strategy,
+                 rc: Optional[RateControl] = None, eps_div: float = 0.0,
+                 out: Optional[Dict[str, np.ndarray]] = None):
+        """Reference-facing plugin path over HOST numpy buffers (H2D + stage + D2H)."""
+        n = int(vertices["roughness"].shape[0]) if "roughness" in vertices else vertices["p01"].size // 3
+        if out is None:
+            out = {"q_norm": np.empty(n, np.float32), "q_real": np.empty(n, np.float32),
+                   "slots": np.empty((self.capacity, 2), np.uint32)}
+        gain = rc.gain() if rc is not None else 1.0
+        p = self.params(depth, strategy, gain, eps_div)
+
+        def hp(name, src):
+            a = src.get(name)
+            return a.ctypes.data if a is not None else None
+        soa = _capi.VertexSoA(hp("p01", vertices), hp("wo01", vertices), hp("roughness", vertices),
+                              hp("weight", vertices), hp("i_pixel", vertices), hp("path_key", vertices), None, None)
+        oc = _capi.StageOut(hp("q_norm", out), hp("q_real", out), hp("slots", out), hp("k", out), hp("offset", out),
+                            hp("decided", out), hp("q_orig", out), hp("u", out))
+        r = _capi.StageResultC()
+        _capi.check(self.handle, self.ctx.lib.nrrs_gpu_rrs_stage_host(self.handle, C.byref(soa), n, C.byref(p),
+                                                                      C.byref(oc), C.byref(r)))
+        res = StageResult.from_c(r)
+        if rc is not None and res.dropped > 0:
+            rc.note_overflow()
+        return out, res
+
+    def compact(self, records: torch.Tensor, used: torch.Tensor, count: int, out: torch.Tensor,
+                d_count: Optional[torch.Tensor] = None, sync: bool = True) -> Optional[int]:
+        """Order-preserving compaction of filled slots (wavefront.cpp:488-497).
+        records: [>=count, W] int32 (W = 2 slot records or 18 = 72-byte PathState)."""
+        words = int(records.shape[1])
+        hc = C.c_uint32(0)
+        _capi.check(self.handle, self.ctx.lib.nrrs_gpu_compact(
+            self.handle, records.data_ptr(), used.data_ptr(), int(count), words, out.data_ptr(),
+            d_count.data_ptr() if d_count is not None else None, C.byref(hc) if sync else None))
+        return hc.value if sync else None
+
+    def strategy_factor(self, vertices: Dict[str, torch.Tensor], strategy: Strategy, eps_div: float = 0.0):
+        """Batched strategy_factor (wavefront.cpp:186-215) without sanitize/normalize."""
+        n = vertices["p01"].numel() // 3
+        q = torch.empty(n, dtype=torch.float32, device=self.device)
+        soa = vertex_soa(vertices)
+        s = strategy.c()
+        _capi.check(self.handle, self.ctx.lib.nrrs_gpu_strategy_factor(self.handle, C.byref(soa), n, C.byref(s),
+                                                                       float(eps_div), q.data_ptr()))
+        return q
+
+    def predict_stats(self, vertices: Dict[str, torch.Tensor]) -> torch.Tensor:
+        """Batched NeuralRrs::predict_stats (networks.cpp:252-264): [n, 6] = mean(3), m2(3)."""
+        n = vertices["p01"].numel() // 3
+        st = torch.empty((n, 6), dtype=torch.float32, device=self.device)
+        soa = vertex_soa(vertices)
+        _capi.check(self.handle, self.ctx.lib.nrrs_gpu_predict_stats(self.handle, C.byref(soa), n, st.data_ptr()))
+        return st
+
+    def close(self) -> None:
+        self.ctx.close()
+
+
+def strategy_for_depth(assignment, depth: int) -> Strategy:
+    """Mix-Depth gate: entry d-1 governs depth d (wavefront.cpp:366)."""
+    return assignment[depth - 1]
+
+
+__all__ = ["RrsStage", "StageResult", "StageOutputs", "GpuContext", "default_context", "vertex_soa",
+           "strategy_for_depth", "StrategyKind"]

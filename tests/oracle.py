@@ -1,0 +1,230 @@
+"""ctypes wrapper of oracle/liborc.so -- the CPU CHECKER (test infrastructure only).
+
+Imported by tests/, __graft_entry__.smoke() and bench.py's CPU-baseline legs,
+never by the product package.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import pathlib
+import subprocess
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parents[1]
+ORACLE_DIR = ROOT / "oracle"
+LIB = ORACLE_DIR / "liborc.so"
+
+FIXED, THROUGHPUT, ADRRS_TREE, ADRRS_NN, NRRS, AID_NRRS = range(6)
+VARIANT_NRRS, VARIANT_AID = 0, 1
+
+
+class GridSpec(C.Structure):
+    _fields_ = [("levels", C.c_int), ("features", C.c_int), ("base_resolution", C.c_int),
+                ("log2_table_size", C.c_int)]
+
+
+class Nets(C.Structure):
+    _fields_ = [("variant", C.c_int), ("grid", GridSpec), ("stat_grid", C.c_void_p), ("stat_mlp", C.c_void_p),
+                ("rrs_grid", C.c_void_p), ("rrs_mlp", C.c_void_p)]
+
+
+class Vertices(C.Structure):
+    _fields_ = [("p01", C.c_void_p), ("wo01", C.c_void_p), ("roughness", C.c_void_p), ("weight", C.c_void_p),
+                ("i_pixel", C.c_void_p), ("path_key", C.c_void_p)]
+
+
+class StageParams(C.Structure):
+    _fields_ = [("depth", C.c_uint32), ("n_pixels", C.c_uint32), ("capacity", C.c_uint32), ("kind", C.c_int),
+                ("fixed_value", C.c_float), ("gain", C.c_float), ("eps_div", C.c_float), ("seed", C.c_uint64),
+                ("threads", C.c_int)]
+
+
+class StageOut(C.Structure):
+    _fields_ = [("q_orig", C.c_void_p), ("q_norm", C.c_void_p), ("q_real", C.c_void_p), ("u", C.c_void_p),
+                ("k", C.c_void_p), ("offset", C.c_void_p), ("decided", C.c_void_p), ("slots", C.c_void_p),
+                ("f_norm", C.c_double), ("sum_q", C.c_double), ("total", C.c_uint64), ("spawned", C.c_uint32),
+                ("dropped", C.c_uint64), ("nonfinite", C.c_uint64)]
+
+
+_lib = None
+
+
+def build() -> None:
+    subprocess.run(["make", "-s", "-C", str(ORACLE_DIR), "liborc.so"], check=True)
+    if pathlib.Path("/root/reference/proj/include/nrrs/rng.hpp").exists():
+        subprocess.run(["make", "-s", "-C", str(ORACLE_DIR), "ref"], check=True)
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        src = ORACLE_DIR / "nrrs_oracle.c"
+        if not LIB.exists() or LIB.stat().st_mtime < src.stat().st_mtime:
+            build()
+        L = C.CDLL(str(LIB))
+        f, d, u32, u64, i, p = C.c_float, C.c_double, C.c_uint32, C.c_uint64, C.c_int, C.c_void_p
+        sig = {
+            "orc_mix_bits": (u64, [u64]), "orc_mix_bits2": (u64, [u64, u64]),
+            "orc_rng_init": (None, [p, u64, u64]), "orc_rng_next_u32": (u32, [p]), "orc_rng_next_float": (f, [p]),
+            "orc_child_path_key": (u64, [u64, u32]), "orc_root_path_key": (u64, [u32, u32]),
+            "orc_rrs_uniform": (f, [u64, u64, u32]), "orc_luminance": (f, [p]),
+            "orc_stochastic_round": (i, [f, f]), "orc_one_blob": (None, [f, i, p]), "orc_box_cox": (f, [f]),
+            "orc_roughness_remap": (f, [f]), "orc_softplus_mod": (f, [f]),
+            "orc_softplus_mod_inverse_pos": (f, [f]), "orc_box_cox_clamps": (u64, []),
+            "orc_reset_box_cox_clamps": (None, []),
+            "orc_grid_param_count": (C.c_size_t, [p]), "orc_grid_encode": (None, [p, p, p, p]),
+            "orc_mlp_param_count": (i, [i, i]), "orc_mlp_head_offset": (i, [i, i]),
+            "orc_mlp_forward": (None, [i, i, p, p, p]),
+            "orc_build_stat_tail": (None, [p, f, p]), "orc_build_nrrs_input": (None, [p, p, p, p, f, p]),
+            "orc_build_aid_tail": (None, [p, p, p, f, p]),
+            "orc_predict_stats": (None, [p, p, p, f, p]), "orc_predict_q": (f, [p, p, p, f, p, p]),
+            "orc_adrrs_factor": (f, [p, p, p, f]),
+            "orc_strategy_factor": (f, [i, f, p, p, p, p, f, p, f]),
+            "orc_normalize_factors": (d, [p, C.c_size_t, u64, p]),
+            "orc_realize_counts": (u64, [p, p, p, C.c_size_t, p]), "orc_bernstein_bound": (d, [d, u64]),
+            "orc_queue_capacity_for": (u32, [u32]), "orc_plan_spawns": (None, [p, C.c_size_t, u32, p, p, p, p]),
+            "orc_rrs_stage": (None, [p, C.c_size_t, p, p, p]),
+            "orc_compact_slots": (u32, [p, p, u32, p]),
+            "orc_gen_vertices": (None, [C.c_size_t, u32, u32, p, p, p, p, p, p, p]),
+            "orc_gen_split_bound_factors": (None, [C.c_size_t, p]),
+            "orc_init_nets": (None, [i, p, u64, i, p, p, p, p]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def ptr(a: np.ndarray | None):
+    return None if a is None else a.ctypes.data
+
+
+# ---------------------------------------------------------------------------
+class OracleNets:
+    """Snapshot weights held by the oracle (orc_init_nets)."""
+
+    def __init__(self, variant: int, levels=8, features=2, base=16, log2t=15, seed=1, randomize=True,
+                 arrays=None):
+        self.variant = variant
+        self.spec = GridSpec(levels, features, base, log2t)
+        gn = levels * (1 << log2t) * features
+        gd = levels * features
+        self.stat_in = gd + 16
+        self.rrs_in = 11 if variant == VARIANT_NRRS else gd + 16
+        L = lib()
+        if arrays is not None:
+            self.stat_grid, self.stat_mlp, self.rrs_grid, self.rrs_mlp = [np.ascontiguousarray(a, np.float32)
+                                                                          for a in arrays]
+        else:
+            self.stat_grid = np.zeros(gn, np.float32)
+            self.stat_mlp = np.zeros(L.orc_mlp_param_count(self.stat_in, 6), np.float32)
+            self.rrs_grid = np.zeros(gn if variant == VARIANT_AID else 0, np.float32)
+            self.rrs_mlp = np.zeros(L.orc_mlp_param_count(self.rrs_in, 1), np.float32)
+            L.orc_init_nets(variant, C.byref(self.spec), seed, int(randomize), ptr(self.stat_grid),
+                            ptr(self.stat_mlp), ptr(self.rrs_grid) if self.rrs_grid.size else None,
+                            ptr(self.rrs_mlp))
+        self.c = Nets(variant, self.spec, ptr(self.stat_grid), ptr(self.stat_mlp),
+                      ptr(self.rrs_grid) if self.rrs_grid.size else None, ptr(self.rrs_mlp))
+
+
+def gen_vertices(n: int, n_pixels: int | None = None, frame: int = 0) -> dict:
+    """SURVEY.md 8d synthetic vertex batch (RngStream(0xC0FFEE, i) per vertex)."""
+    n_pixels = n if n_pixels is None else n_pixels
+    v = {"p01": np.empty((n, 3), np.float32), "wo01": np.empty((n, 2), np.float32),
+         "roughness": np.empty(n, np.float32), "weight": np.empty((n, 3), np.float32),
+         "i_pixel": np.empty((n, 3), np.float32), "path_key": np.empty(n, np.uint64),
+         "pixel": np.empty(n, np.uint32)}
+    lib().orc_gen_vertices(n, n_pixels, frame, ptr(v["p01"]), ptr(v["wo01"]), ptr(v["roughness"]),
+                           ptr(v["weight"]), ptr(v["i_pixel"]), ptr(v["path_key"]), ptr(v["pixel"]))
+    return v
+
+
+def split_bound_factors(n: int) -> np.ndarray:
+    q = np.empty(n, np.float32)
+    lib().orc_gen_split_bound_factors(n, ptr(q))
+    return q
+
+
+def rrs_stage(v: dict, depth: int, n_pixels: int, capacity: int, kind: int, nets: OracleNets | None = None,
+              fixed_value: float = 1.0, gain: float = 0.85, eps_div: float = 0.0, seed: int = 0,
+              threads: int = 1) -> dict:
+    """The reference's RRS decision block (wavefront.cpp:363-425) restated in C."""
+    n = int(v["roughness"].shape[0])
+    vc = Vertices(ptr(v["p01"]), ptr(v["wo01"]), ptr(v["roughness"]), ptr(v["weight"]), ptr(v["i_pixel"]),
+                  ptr(v["path_key"]))
+    p = StageParams(depth, n_pixels, capacity, kind, fixed_value, gain, eps_div, seed, threads)
+    out = {"q_orig": np.zeros(n, np.float32), "q_norm": np.zeros(n, np.float32), "q_real": np.zeros(n, np.float32),
+           "u": np.zeros(n, np.float32), "k": np.zeros(n, np.int32), "offset": np.zeros(n, np.uint32),
+           "decided": np.zeros(n, np.uint8), "slots": np.zeros((max(capacity, 1), 2), np.uint32)}
+    o = StageOut(*(ptr(out[k]) for k in ("q_orig", "q_norm", "q_real", "u", "k", "offset", "decided", "slots")))
+    lib().orc_rrs_stage(C.byref(vc), n, C.byref(p), C.byref(nets.c) if nets is not None else None, C.byref(o))
+    out.update(f_norm=o.f_norm, sum_q=o.sum_q, total=o.total, spawned=o.spawned, dropped=o.dropped,
+               nonfinite=o.nonfinite)
+    return out
+
+
+def normalize_factors(q: np.ndarray, n_pixels: int):
+    err = C.c_int(0)
+    f = lib().orc_normalize_factors(ptr(q), q.size, n_pixels, C.byref(err))
+    if err.value:
+        raise RuntimeError("normalize_factors: factors must be finite and >= 0")
+    return f
+
+
+def plan_spawns(counts: np.ndarray, capacity: int):
+    counts = np.ascontiguousarray(counts, np.int32)
+    off = np.zeros(counts.size, np.uint32)
+    sp, dr, err = C.c_uint32(0), C.c_uint64(0), C.c_int(0)
+    lib().orc_plan_spawns(ptr(counts), counts.size, capacity, ptr(off), C.byref(sp), C.byref(dr), C.byref(err))
+    if err.value:
+        raise RuntimeError("plan_spawns: negative count")
+    return off, sp.value, dr.value
+
+
+def compact_slots(slots: np.ndarray, used: np.ndarray, count: int) -> np.ndarray:
+    out = np.zeros((max(count, 1), 2), np.uint32)
+    w = lib().orc_compact_slots(ptr(np.ascontiguousarray(slots, np.uint32)), ptr(np.ascontiguousarray(used, np.uint8)),
+                                count, ptr(out))
+    return out[:w]
+
+
+def predict_q(nets: OracleNets, v: dict) -> np.ndarray:
+    n = int(v["roughness"].shape[0])
+    q = np.empty(n, np.float32)
+    L = lib()
+    for i in range(n):
+        q[i] = L.orc_predict_q(C.byref(nets.c), ptr(v["p01"][i]), ptr(v["wo01"][i]), float(v["roughness"][i]),
+                               ptr(v["weight"][i]), ptr(v["i_pixel"][i]))
+    return q
+
+
+def strategy_factors(kind: int, v: dict, nets: OracleNets | None, eps_div: float, fixed_value: float = 1.0):
+    n = int(v["roughness"].shape[0])
+    q = np.empty(n, np.float32)
+    L = lib()
+    for i in range(n):
+        q[i] = L.orc_strategy_factor(kind, fixed_value, C.byref(nets.c) if nets else None, ptr(v["weight"][i]),
+                                     ptr(v["p01"][i]), ptr(v["wo01"][i]), float(v["roughness"][i]),
+                                     ptr(v["i_pixel"][i]), eps_div)
+    return q
+
+
+def predict_stats(nets: OracleNets, v: dict) -> np.ndarray:
+    n = int(v["roughness"].shape[0])
+    st = np.empty((n, 6), np.float32)
+    L = lib()
+    for i in range(n):
+        L.orc_predict_stats(C.byref(nets.c), ptr(v["p01"][i]), ptr(v["wo01"][i]), float(v["roughness"][i]),
+                            ptr(st[i]))
+    return st
+
+
+def threads_available() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
