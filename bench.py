@@ -1,0 +1,399 @@
+#!/usr/bin/env python
+"""Benchmark of the NRRS per-bounce RRS stage (BASELINE.json metric: path vertices/s
+through RRSNet + normalized RRS + compaction).
+
+Workload (N=1): BASELINE.json configs[2] shape -- AID-NRRS, one 1920x1080 film,
+one decision depth (depth 2) over 2,073,600 synthetic surface vertices
+(SURVEY.md 8d generator), random-init RRSNet (NeuralRrsConfig{AID, seed 1} +
+benchmark head randomization), gain f_rate*alpha = 0.85, capacity
+queue_capacity_for(Npx).  A step = K-A factors (hash grid + tcgen05 MLP) ->
+K-B normalize/realize/scan/slot emission -> K-C order-preserving compaction of
+the slot records by a synthetic BSDF-validity mask (~10% invalid).
+N>1 (torchrun): each rank owns a 2,073,600-vertex band of an N-band film,
+global normalization and capacity clip over NCCL (weak scaling; N=8 is the
+16.6M-vertex configs[4] batch).
+
+--impl reference: the reference's CPU implementation of the same path (the C
+oracle port: parallel factor pass + serial normalize/realize/plan/slots), all
+host threads, bounded samples.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "path vertices/sec (RRSNet+normalized RRS+compaction) at 1/2/4/8 B200"
+N_LOCAL = 1920 * 1080
+ALG_BYTES_INFER = 56 + 8   # K-A: reads p01 12, wo01 8, rough 4, t_x 12, i_pixel 12, key 8; writes q_orig 4 + u 4
+STAGE_READ, STAGE_WRITE = 56, 8  # SURVEY.md 8d per-vertex compulsory bytes (+ 8 B per spawned slot record)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--variant", default="aid", choices=["aid", "nrrs"])
+    ap.add_argument("--n", type=int, default=N_LOCAL)
+    ap.add_argument("--no-extra", action="store_true", help="skip the per-strategy side measurements")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_json(path):
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+def cpu_baseline(variant: str, n_sample: int = N_LOCAL):
+    """Oracle port of the reference path on this host's cores (rank 0, N=1 only)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle as orc  # CPU checker / baseline only
+    threads = orc.threads_available()
+    v = orc.gen_vertices(n_sample)
+    var = orc.VARIANT_AID if variant == "aid" else orc.VARIANT_NRRS
+    kind = orc.AID_NRRS if variant == "aid" else orc.NRRS
+    nets = orc.OracleNets(var, seed=1, randomize=True)
+    cap = orc.lib().orc_queue_capacity_for(n_sample)
+    best = float("inf")
+    for _ in range(2):
+        t0 = time.perf_counter()
+        orc.rrs_stage(v, 2, n_sample, cap, kind, nets, gain=0.85, seed=0, threads=threads)
+        best = min(best, time.perf_counter() - t0)
+    return {"value": n_sample / best, "unit": "vertices/s", "cores": threads, "kind": "port",
+            "sample": f"{n_sample} synthetic vertices, {variant}-nrrs, depth 2, best of 2 "
+                      f"(factor pass over {threads} threads + serial normalize/realize/plan/slots)"}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo", init_method="env://")
+        if rank != 0:
+            dist.barrier()
+            dist.destroy_process_group()
+            return
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle as orc
+    threads = orc.threads_available()
+    var = orc.VARIANT_AID if args.variant == "aid" else orc.VARIANT_NRRS
+    kind = orc.AID_NRRS if args.variant == "aid" else orc.NRRS
+    nets = orc.OracleNets(var, seed=1, randomize=True)
+    sample = args.n
+    v = orc.gen_vertices(sample)
+    cap = orc.lib().orc_queue_capacity_for(sample)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        orc.rrs_stage(v, 2, sample, cap, kind, nets, gain=0.85, seed=i, threads=threads)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    value = sample / statistics.mean(times)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "vertices/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{args.variant}-nrrs stage, 1920x1080 synthetic vertices at depth 2 "
+                                   f"(full batch each step)",
+                       "n_pixels": args.n, "strategy": f"{args.variant}-nrrs", "depth": 2},
+            "cpu_baseline": {"value": value, "unit": "vertices/s", "cores": threads, "kind": "port",
+                             "sample": f"the full {sample}-vertex batch per step; the reference does not build here "
+                                       "(Eigen absent): C restatement of the reference path"},
+            "e2e": {"value": value, "unit": "vertices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_07868_b200 import (NeuralRrs, NeuralRrsConfig, RateControl, RrsStage, RrsVariant, Strategy,
+                                       StrategyKind, queue_capacity_for)
+    from paper_2510_07868_b200 import _capi, synthetic
+    from paper_2510_07868_b200.sharded import ShardedRrsStage
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    n = args.n
+    npx = n * world
+    cap = queue_capacity_for(npx)
+    variant = RrsVariant.Aid if args.variant == "aid" else RrsVariant.Nrrs
+    strategy = Strategy(StrategyKind.AidNrrs if args.variant == "aid" else StrategyKind.Nrrs)
+    nets = NeuralRrs(NeuralRrsConfig(variant=variant, seed=1)).randomize_for_benchmark()
+
+    # inputs resident in HBM before timing
+    hv = synthetic.gen_vertices(n, n_pixels=npx, first=rank * n)
+    dv = {k: torch.from_numpy(a.view(np.int64) if a.dtype == np.uint64 else a).to(dev)
+          for k, a in hv.items() if k != "pixel"}
+    if world > 1:
+        sh = ShardedRrsStage(npx, nets, device=local)
+        stage = sh.stage
+    else:
+        sh = None
+        stage = RrsStage(npx, nets, device=local)
+    stage.reserve(n)
+    out = stage.alloc_outputs(n)
+    out.q_orig = torch.empty(n, dtype=torch.float32, device=dev)
+    out.u = torch.empty(n, dtype=torch.float32, device=dev)
+    slot_cap = stage.capacity
+    slot_idx = torch.arange(slot_cap, dtype=torch.int64, device=dev)
+    # synthetic BSDF validity per slot (~10% invalid samples), fixed hash of the slot index
+    used = (((slot_idx * 2654435761) >> 7) % 10 != 0).to(torch.uint8)
+    compacted = torch.empty((slot_cap, 2), dtype=torch.int32, device=dev)
+    d_count = torch.zeros(1, dtype=torch.int32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    lib = _capi.lib()
+    import ctypes as C
+    rc = RateControl()
+    local_sum = torch.zeros(1, dtype=torch.float64, device=dev)
+    local_total = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def step(ev):
+        stream = torch.cuda.current_stream()
+        ev[0].record(stream)
+        gain = rc.gain()
+        p = stage.params(2, strategy, gain, 0.0, n_pixels=npx)
+        from paper_2510_07868_b200.stage import vertex_soa
+        soa = vertex_soa(dv)
+        oc = out.c()
+        _capi.check(stage.handle, lib.nrrs_gpu_stage_factors(stage.handle, C.byref(soa), n, C.byref(p),
+                                                             C.byref(oc), local_sum.data_ptr()))
+        ev[1].record(stream)
+        if sh is None:
+            _capi.check(stage.handle, lib.nrrs_gpu_stage_decide(stage.handle, n, C.byref(p), local_sum.data_ptr(), 1,
+                                                                C.byref(oc), local_total.data_ptr()))
+            count_src = local_total
+        else:
+            sh.stage.ctx.bind_stream()
+            from paper_2510_07868_b200.sharded import sharded_depth
+            sharded_depth(local_sum, lambda rs: sh.decide(n, 2, strategy, out, rs, gain, 0.0), cap, npx, None, rc)
+            count_src = sh._total
+        ev[2].record(stream)
+        _capi.check(stage.handle, lib.nrrs_gpu_compact_dev(stage.handle, out.slots.data_ptr(), used.data_ptr(),
+                                                           count_src.data_ptr(), slot_cap, 2, compacted.data_ptr(),
+                                                           d_count.data_ptr()))
+        ev[3].record(stream)
+
+    def events():
+        return [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+
+    stage.ctx.bind_stream()
+    for _ in range(max(args.warmup, 3)):
+        flush.zero_()
+        step(events())
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = []
+    launches0 = stage.ctx.launch_count()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps (outside the events)
+            ev = events()
+            step(ev)
+            evs.append(ev)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches = stage.ctx.launch_count() - launches0
+    step_ms = [e[0].elapsed_time(e[3]) for e in evs]
+    infer_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    decide_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    compact_ms = [e[2].elapsed_time(e[3]) for e in evs]
+    total_s = sum(step_ms) / 1e3
+    t = torch.tensor([total_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_s = float(t.item())
+    value = world * n * args.steps / total_s
+    res = _capi.StageResultC()
+    spawned = int(min(int(local_total.item()), cap)) if sh is None else int(sh._total.item())
+
+    # ---- e2e: the C ABI host-buffer entry (H2D + stage + D2H every step) ----
+    e2e = None
+    if world == 1:
+        pinned = {k: torch.from_numpy(a.view(np.int64) if a.dtype == np.uint64 else a).pin_memory().numpy()
+                  for k, a in hv.items() if k != "pixel"}
+        pinned["path_key"] = pinned["path_key"].view(np.uint64)
+        hout = {"q_norm": torch.empty(n, dtype=torch.float32).pin_memory().numpy(),
+                "q_real": torch.empty(n, dtype=torch.float32).pin_memory().numpy(),
+                "slots": torch.empty((slot_cap, 2), dtype=torch.int32).pin_memory().numpy().view(np.uint32)}
+        for _ in range(3):
+            stage.run_host(pinned, 2, strategy, rc=None, out=hout)
+        torch.cuda.synchronize()
+        e_times, d2h = [], 0
+        for _ in range(max(3, args.steps // 2)):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            _, r = stage.run_host(pinned, 2, strategy, rc=None, out=hout)
+            e_times.append(time.perf_counter() - t0)
+            d2h = 8 * n + 8 * r.spawned
+        e2e = {"value": n / statistics.mean(e_times), "unit": "vertices/s", "h2d_bytes_per_step": 56 * n,
+               "d2h_bytes_per_step": d2h, "path": "nrrs_gpu_rrs_stage_host (pinned host buffers)"}
+
+    # ---- side measurements: other strategies (Mix-Depth candidates) on the same batch ----
+    extra = {}
+    if world == 1 and not args.no_extra:
+        alt_nets = NeuralRrs(NeuralRrsConfig(variant=RrsVariant.Nrrs if variant == RrsVariant.Aid
+                                             else RrsVariant.Aid, seed=1)).randomize_for_benchmark()
+        for name, strat, nn in (("nrrs" if variant == RrsVariant.Aid else "aid-nrrs",
+                                 Strategy(StrategyKind.Nrrs), alt_nets),
+                                ("adrrs-nn", Strategy(StrategyKind.AdrrsNn), nets),
+                                ("throughput", Strategy(StrategyKind.Throughput), nets),
+                                ("depth1-fixed", None, nets)):
+            stg = RrsStage(npx, nn, device=local)
+            o2 = stg.alloc_outputs(n)
+            depth = 1 if strat is None else 2
+            s2 = strat or Strategy(StrategyKind.Fixed, 1.0)
+            for _ in range(3):
+                stg.run(dv, depth, s2, rc=None, out=o2, sync=False)
+            ts = []
+            for _ in range(5):
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                stg.run(dv, depth, s2, rc=None, out=o2, sync=False)
+                b.record()
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b))
+            extra[name] = {"vertices_per_s": n / (statistics.mean(ts) / 1e3), "ms": statistics.mean(ts)}
+            stg.close()
+
+    peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}
+    hbm = peaks.get("hbm_gbs")
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    if not hbm:
+        hbm, peak_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+    infer_avg = statistics.mean(infer_ms) / 1e3
+    achieved = ALG_BYTES_INFER * n / infer_avg / 1e9
+    prof = load_json(os.path.join(ROOT, "profiles", "ncu_summary.json")) or {}
+    traffic = prof.get(f"infer_{args.variant}_dram_bytes_per_launch")
+    stage_bytes = (STAGE_READ + STAGE_WRITE) * n + 8 * spawned
+    line = {
+        "metric": METRIC, "value": value, "unit": "vertices/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": 1e3 * total_s / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"configs[2] shape: {args.variant}-nrrs stage over a 1920x1080 synthetic vertex "
+                               f"batch per GPU at depth 2 (SURVEY.md 8d), + compaction (~10% invalid slots)",
+                   "vertices_per_gpu": n, "n_pixels": npx, "capacity": cap, "strategy": f"{args.variant}-nrrs",
+                   "depth": 2, "gain": 0.85, "parallelism": f"tile-sharded dp{world}",
+                   "l2": "flushed between timed steps (256 MiB write outside the events)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": traffic, "kernel": f"infer_kernel<{'Aid' if args.variant == 'aid' else 'Nrrs'}>",
+                     "alg_bytes_per_vertex": ALG_BYTES_INFER, "peak_source": peak_src,
+                     "stage_frac": (stage_bytes / (statistics.mean(step_ms) / 1e3) / 1e9) / hbm},
+        "kernels_ms": {"infer": statistics.mean(infer_ms), "decide": statistics.mean(decide_ms),
+                       "compact": statistics.mean(compact_ms)},
+        "clocks": clk.summary(),
+        "gpu_launches": launches,
+        "spawned": spawned,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if extra:
+        line["strategies"] = extra
+    if world == 1 and rank == 0 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(args.variant)
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -193,6 +193,13 @@ NRRS_API int nrrs_gpu_sharded_clip(const uint64_t *h_rank_totals, int32_t nranks
 NRRS_API int nrrs_gpu_compact(nrrs_gpu_ctx *ctx, const void *d_in, const uint8_t *d_used, uint32_t count,
                      uint32_t record_words, void *d_out, uint32_t *d_count, uint32_t *h_count);
 
+/* Same, with the record count read on the device: count = min(*d_count_in, max_count)
+ * (e.g. the stage's realized total, so spawned = min(total, capacity) never
+ * round-trips through the host).  Launches max_count/tile CTAs. */
+NRRS_API int nrrs_gpu_compact_dev(nrrs_gpu_ctx *ctx, const void *d_in, const uint8_t *d_used,
+                                  const uint64_t *d_count_in, uint32_t max_count, uint32_t record_words,
+                                  void *d_out, uint32_t *d_count);
+
 /* ---- granular drop-ins for the reference's free functions (device data) ---- */
 /* normalize_factors (rrs.hpp:18, rrs.cpp:8-24): in place; EINVAL on negative/non-finite (q untouched) */
 NRRS_API int nrrs_gpu_normalize_factors(nrrs_gpu_ctx *ctx, float *d_q, uint64_t n, uint64_t n_pixels,

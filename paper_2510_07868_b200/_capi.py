@@ -77,6 +77,7 @@ SIGNATURES = [
                                         C.POINTER(C.c_uint64), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
                                         C.POINTER(C.c_uint64)]),
     ("nrrs_gpu_compact", C.c_int, [_P, _P, _P, C.c_uint32, C.c_uint32, _P, _P, C.POINTER(C.c_uint32)]),
+    ("nrrs_gpu_compact_dev", C.c_int, [_P, _P, _P, _P, C.c_uint32, C.c_uint32, _P, _P]),
     ("nrrs_gpu_normalize_factors", C.c_int, [_P, _P, C.c_uint64, C.c_uint64, C.POINTER(C.c_double)]),
     ("nrrs_gpu_realize_counts", C.c_int, [_P, _P, _P, _P, C.c_uint64, C.POINTER(C.c_uint64)]),
     ("nrrs_gpu_plan_spawns", C.c_int, [_P, _P, C.c_uint64, C.c_uint32, _P, C.POINTER(C.c_uint32),

@@ -755,6 +755,36 @@ int nrrs_gpu_compact(nrrs_gpu_ctx *ctx, const void *d_in, const uint8_t *d_used,
     return NRRS_OK;
 }
 
+int nrrs_gpu_compact_dev(nrrs_gpu_ctx *ctx, const void *d_in, const uint8_t *d_used, const uint64_t *d_count_in,
+                         uint32_t max_count, uint32_t record_words, void *d_out, uint32_t *d_count) {
+    if (!ctx || !d_count_in || (max_count && (!d_in || !d_used || !d_out)))
+        return NRRS_EINVAL;
+    if (record_words != 2 && record_words != 18)
+        return fail(ctx, NRRS_EINVAL, "compact: record_words must be 2 (slot) or 18 (PathState)");
+    uint32_t *cnt = d_count ? d_count : ctx->d_misc + 4;
+    if (max_count == 0) {
+        CK(ctx, cudaMemsetAsync(cnt, 0, sizeof(uint32_t), ctx->stream));
+        return NRRS_OK;
+    }
+    int rc = ensure_compact_scratch(ctx, max_count, record_words);
+    if (rc)
+        return rc;
+    CompactParams cp{};
+    cp.in = d_in;
+    cp.used = d_used;
+    cp.count = max_count;
+    cp.count_in = reinterpret_cast<const unsigned long long *>(d_count_in);
+    cp.out = d_out;
+    cp.count_out = cnt;
+    cp.tile_state = ctx->d_ctile_state;
+    cp.tile_counter = ctx->d_misc + 2;
+    cp.num_tiles = compact_tiles(max_count, record_words);
+    cp.epoch = next_epoch(ctx, ctx->compact_epoch, ctx->d_ctile_state, ctx->cap_ctiles);
+    CK(ctx, launch_compact(record_words, cp, ctx->stream));
+    ctx->launches += 1;
+    return NRRS_OK;
+}
+
 int nrrs_gpu_normalize_factors(nrrs_gpu_ctx *ctx, float *d_q, uint64_t n, uint64_t n_pixels, double *h_f_norm) {
     if (!ctx || (n && !d_q))
         return NRRS_EINVAL;

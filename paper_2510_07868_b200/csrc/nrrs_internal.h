@@ -104,7 +104,8 @@ struct DecideParams {
 struct CompactParams {
     const void *in;
     const uint8_t *used;
-    uint64_t count;
+    uint64_t count;                        // launch bound
+    const unsigned long long *count_in;    // optional device count (clamped to `count`)
     void *out;
     uint32_t *count_out;
     uint64_t *tile_state;

@@ -624,11 +624,16 @@ __global__ void __launch_bounds__(kDecThreads) compact_kernel(CompactParams p) {
     const uint32_t tile = tile_s;
     const uint64_t base = (uint64_t)tile * kTile;
     const uint64_t first = base + (uint64_t)tid * IPT;
+    uint64_t count = p.count;
+    if (p.count_in) {
+        const uint64_t c = *p.count_in;
+        count = c < count ? c : count;
+    }
     uint32_t keep[IPT];
     uint32_t cnt = 0;
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
-        keep[i] = (first + i < p.count && p.used[first + i]) ? 1u : 0u;
+        keep[i] = (first + i < count && p.used[first + i]) ? 1u : 0u;
         cnt += keep[i];
     }
     uint32_t agg = 0;

@@ -1,0 +1,130 @@
+"""Tile-sharded RRS stage across ranks.
+
+Each rank owns a contiguous band of the image (rank order == pixel order), so
+the global depth-d queue is the concatenation of the rank queues.  Per depth
+the path has exactly two real exchange steps, both 8 bytes per rank:
+
+  1. all-gather of the per-rank sum of sanitized factors (f64); every rank
+     sums them in rank order, so F_norm = Npx_total / sum is identical on all
+     ranks (normalization is global per depth, rrs.cpp:8-24; image-partition
+     local normalization is a non-goal).
+  2. all-gather of the per-rank realized totals (u64); the exclusive prefix in
+     rank order is the rank's global slot base and the capacity clip of the
+     global tail (wavefront.cpp:141-154) becomes a count truncation of the
+     rank's records.  Overflow is a global event, so RateControl stays
+     replicated.
+
+The protocol functions take the phase callables as arguments so the host logic
+is testable on CPU ranks (gloo); the product binds them to the C ABI.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+from typing import Callable, List, Optional
+
+import torch
+import torch.distributed as dist
+
+from . import _capi
+from .rrs import RateControl, Strategy
+from .stage import RrsStage, StageOutputs, vertex_soa
+
+
+@dataclasses.dataclass
+class ShardOutcome:
+    rank_sums: List[float]
+    rank_totals: List[int]
+    base: int           # global slot index of this rank's first record
+    kept: int           # records this rank keeps after the global clip
+    spawned: int        # global SpawnPlan::spawned
+    dropped: int        # global SpawnPlan::dropped
+    f_norm: float
+
+
+def global_clip(totals: List[int], rank: int, capacity: int):
+    """nrrs_gpu_sharded_clip: (base, kept, spawned_global, dropped_global)."""
+    arr = (C.c_uint64 * len(totals))(*totals)
+    base, kept, sp, dr = C.c_uint64(0), C.c_uint32(0), C.c_uint32(0), C.c_uint64(0)
+    rc = _capi.lib().nrrs_gpu_sharded_clip(arr, len(totals), rank, capacity, C.byref(base), C.byref(kept),
+                                           C.byref(sp), C.byref(dr))
+    if rc:
+        raise _capi.NrrsError(rc, "sharded_clip: invalid arguments")
+    return base.value, kept.value, sp.value, dr.value
+
+
+def f_norm_from_sums(rank_sums: List[float], n_pixels_total: int) -> float:
+    s = 0.0
+    for x in rank_sums:  # rank order
+        s += x
+    return 1.0 if s <= 0.0 else float(n_pixels_total) / s
+
+
+def sharded_depth(local_sum: torch.Tensor, decide: Callable[[torch.Tensor], torch.Tensor], capacity: int,
+                  n_pixels_total: int, group=None, rc: Optional[RateControl] = None) -> ShardOutcome:
+    """Runs the two exchanges of one depth.  local_sum: [1] float64 on the
+    collective's device; decide(rank_sums) launches phase 2 and returns the
+    rank's [1] int64 realized total."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    sums = [torch.zeros_like(local_sum) for _ in range(world)]
+    dist.all_gather(sums, local_sum, group=group)
+    rank_sums_t = torch.cat(sums)
+    local_total = decide(rank_sums_t)
+    totals = [torch.zeros_like(local_total) for _ in range(world)]
+    dist.all_gather(totals, local_total, group=group)
+    tot = [int(t.item()) for t in totals]
+    base, kept, spawned, dropped = global_clip(tot, rank, capacity)
+    if rc is not None and dropped > 0:
+        rc.note_overflow()
+    return ShardOutcome([float(x) for x in rank_sums_t.tolist()], tot, base, kept, spawned, dropped,
+                        f_norm_from_sums([float(x) for x in rank_sums_t.tolist()], n_pixels_total))
+
+
+class ShardedRrsStage:
+    """One rank of the tile-sharded stage (one GPU per process, NCCL over NVLink)."""
+
+    def __init__(self, n_pixels_total: int, nets=None, capacity: int = 0, seed: int = 0, device: int = 0,
+                 group=None):
+        self.stage = RrsStage(n_pixels_total, nets, capacity=capacity, seed=seed, device=device)
+        self.n_pixels_total = int(n_pixels_total)
+        self.capacity = self.stage.capacity
+        self.group = group
+        self.device = self.stage.device
+        self._sum = torch.zeros(1, dtype=torch.float64, device=self.device)
+        self._total = torch.zeros(1, dtype=torch.int64, device=self.device)
+
+    def factors(self, vertices, depth: int, strategy: Strategy, out: StageOutputs, eps_div: float = 0.0,
+                gain: float = 1.0) -> torch.Tensor:
+        st = self.stage
+        st.ctx.bind_stream()
+        n = vertices["p01"].numel() // 3
+        p = st.params(depth, strategy, gain, eps_div, n_pixels=self.n_pixels_total)
+        soa = vertex_soa(vertices)
+        oc = out.c()
+        _capi.check(st.handle, st.ctx.lib.nrrs_gpu_stage_factors(st.handle, C.byref(soa), n, C.byref(p),
+                                                                 C.byref(oc), self._sum.data_ptr()))
+        return self._sum
+
+    def decide(self, n: int, depth: int, strategy: Strategy, out: StageOutputs, rank_sums: torch.Tensor,
+               gain: float = 1.0, eps_div: float = 0.0) -> torch.Tensor:
+        st = self.stage
+        p = st.params(depth, strategy, gain, eps_div, n_pixels=self.n_pixels_total)
+        oc = out.c()
+        rs = rank_sums.contiguous()
+        _capi.check(st.handle, st.ctx.lib.nrrs_gpu_stage_decide(st.handle, n, C.byref(p), rs.data_ptr(),
+                                                                rs.numel(), C.byref(oc), self._total.data_ptr()))
+        return self._total
+
+    def run(self, vertices, depth: int, strategy: Strategy, rc: Optional[RateControl] = None,
+            eps_div: float = 0.0, out: Optional[StageOutputs] = None):
+        n = vertices["p01"].numel() // 3
+        out = out or self.stage.alloc_outputs(n)
+        gain = rc.gain() if rc is not None else 1.0
+        if self.stage.capacity and out.q_orig is None:
+            out.q_orig = torch.empty(n, dtype=torch.float32, device=self.device)
+            out.u = torch.empty(n, dtype=torch.float32, device=self.device)
+        local = self.factors(vertices, depth, strategy, out, eps_div, gain)
+        outcome = sharded_depth(local, lambda rs: self.decide(n, depth, strategy, out, rs, gain, eps_div),
+                                self.capacity, self.n_pixels_total, self.group, rc)
+        return out, outcome
