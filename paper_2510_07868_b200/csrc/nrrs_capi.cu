@@ -66,13 +66,18 @@ int mlp_param_count(int in, int out) {
 }
 
 // Packs one snapshot MLP theta (mlp.cpp:7-32 layout) into hi/lo fp16 canonical
-// tiles.  colmap[c] = kernel K column of reference input column c (layer 0).
+// tiles of [W | bias].  colmap[c] = kernel K column of reference input column c
+// (layer 0).  k0 = 16: the 11-input NRRS RRSNet layer, bias in column 11;
+// otherwise the data occupies K columns [0, 32) and the bias sits in column 32
+// of an extra ones slice.
 PackedNet pack_net(const float *theta, int in, int out, int k0, const std::vector<int> &colmap) {
     PackedNet pn;
     int off = 0;
     for (int l = 0; l < 4; ++l) {
         const int li = l == 0 ? in : kHidden, lo = l == 3 ? out : kHidden;
-        const int K = l == 0 ? k0 : kHidden;
+        const bool inline_bias = l == 0 && k0 == 16;
+        const int K = inline_bias ? 16 : 48;
+        const int bias_col = inline_bias ? 11 : 32;
         const int N = l == 3 ? 16 : kHidden;
         const float *W = theta + off;         // column-major lo x li
         const float *b = theta + off + lo * li;
@@ -81,28 +86,25 @@ PackedNet pack_net(const float *theta, int in, int out, int k0, const std::vecto
         LayerDesc &L = pn.desc.layer[l];
         L.K = (uint16_t)K;
         L.N = (uint16_t)N;
+        L.ones_slice = inline_bias ? 0xFFFFFFFFu : 2u;
         L.w_hi = (uint32_t)pn.bytes.size();
         L.w_lo = L.w_hi + (uint32_t)wbytes;
-        L.bias = L.w_lo + (uint32_t)wbytes;
-        const size_t bias_bytes = ((size_t)N * 4 + 15) / 16 * 16;
-        pn.bytes.resize(pn.bytes.size() + 2 * wbytes + bias_bytes, 0);
+        pn.bytes.resize(pn.bytes.size() + 2 * wbytes, 0);
         uint8_t *hi = pn.bytes.data() + L.w_hi, *lo_p = pn.bytes.data() + L.w_lo;
         const uint32_t sbo = (uint32_t)K * 16u;
+        auto put = [&](int r, int kc, float v) {
+            const __half h = __float2half_rn(v);
+            const __half lw = __float2half_rn(v - __half2float(h));
+            const size_t o = (size_t)(r >> 3) * sbo + (size_t)(kc >> 3) * 128 + (size_t)(r & 7) * 16 +
+                             (size_t)(kc & 7) * 2;
+            std::memcpy(hi + o, &h, 2);
+            std::memcpy(lo_p + o, &lw, 2);
+        };
         for (int r = 0; r < lo; ++r) {
-            for (int c = 0; c < li; ++c) {
-                const int kc = l == 0 ? colmap[c] : c;
-                const float v = W[c * lo + r];
-                const __half h = __float2half_rn(v);
-                const __half lw = __float2half_rn(v - __half2float(h));
-                const size_t o = (size_t)(r >> 3) * sbo + (size_t)(kc >> 3) * 128 + (size_t)(r & 7) * 16 +
-                                 (size_t)(kc & 7) * 2;
-                std::memcpy(hi + o, &h, 2);
-                std::memcpy(lo_p + o, &lw, 2);
-            }
+            for (int c = 0; c < li; ++c)
+                put(r, l == 0 ? colmap[c] : c, W[c * lo + r]);
+            put(r, bias_col, b[r]);
         }
-        float *bias = reinterpret_cast<float *>(pn.bytes.data() + L.bias);
-        for (int r = 0; r < lo; ++r)
-            bias[r] = b[r];
     }
     return pn;
 }
@@ -115,7 +117,6 @@ void append_net(std::vector<uint8_t> &blob, const PackedNet &pn, NetDesc &desc) 
     for (auto &L : desc.layer) {
         L.w_hi += base;
         L.w_lo += base;
-        L.bias += base;
     }
 }
 

@@ -265,6 +265,54 @@ __device__ __forceinline__ uint64_t lookback_exclusive(uint64_t *state, uint32_t
     return excl;
 }
 
+// Warp-parallel look-back (all 32 lanes of one warp call it): each round reads
+// the 32 preceding tile states at once, sums aggregates up to the nearest
+// inclusive prefix.  Returns the exclusive prefix on every lane; lane 0
+// publishes the tile's inclusive prefix.
+__device__ __forceinline__ uint64_t lookback_warp(uint64_t *state, uint32_t tile, uint64_t aggregate,
+                                                  uint32_t epoch) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t tag = (uint64_t)(epoch & 0x3FFFu) << 48;
+    if (tile == 0) {
+        if (lane == 0)
+            st_release_u64(&state[0], kFlagPrefix | tag | aggregate);
+        return 0;
+    }
+    if (lane == 0)
+        st_release_u64(&state[tile], kFlagAgg | tag | aggregate);
+    uint64_t excl = 0;
+    int64_t window_end = (int64_t)tile - 1;  // lane i inspects tile window_end - i
+    while (true) {
+        const int64_t t = window_end - (int64_t)lane;
+        uint64_t s;
+        if (t >= 0) {
+            do {
+                s = ld_acquire_u64(&state[t]);
+            } while ((s >> 62) == 0 || ((s >> 48) & 0x3FFFu) != (epoch & 0x3FFFu));
+        } else {
+            s = kFlagPrefix;  // virtual prefix 0 before tile 0
+        }
+        const uint32_t is_prefix = (uint32_t)((s >> 62) == 2);
+        const uint32_t pmask = __ballot_sync(0xffffffffu, is_prefix);
+        uint64_t v = s & kValueMask;
+        if (pmask) {
+            const uint32_t first = __ffs(pmask) - 1;  // nearest prefix
+            if (lane > first)
+                v = 0;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+            v += __shfl_xor_sync(0xffffffffu, v, o);
+        excl += v;
+        if (pmask)
+            break;
+        window_end -= 32;
+    }
+    if (lane == 0)
+        st_release_u64(&state[tile], kFlagPrefix | tag | (excl + aggregate));
+    return excl;
+}
+
 // Claims the next tile in launch order; the CTA that claims the last tile
 // resets the counter for the next launch (no claims can follow it).
 __device__ __forceinline__ uint32_t claim_tile(uint32_t *counter, uint32_t num_tiles) {

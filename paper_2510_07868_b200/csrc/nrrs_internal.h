@@ -17,11 +17,15 @@ enum : int {
 };
 
 // One MLP layer inside the smem weight blob (byte offsets from the blob start).
-// W_hi / W_lo are the fp16 split of W in the UMMA K-major canonical layout
-// (N rows x K cols, 8x16B core matrices, LBO = 128 B, SBO = K*16 B).
+// W_hi / W_lo are the fp16 split of [W | bias] in the UMMA K-major canonical
+// layout (N rows x K cols, 8x16B core matrices, LBO = 128 B, SBO = K*16 B).
+// The bias is a weight column multiplied by a constant-ones input column:
+// either a dedicated K16 slice (`ones_slice`, 2 MMA terms) or, for the 11-input
+// NRRS RRSNet layer, input column 11 of the single K16 slice.
 struct LayerDesc {
-    uint32_t w_hi, w_lo, bias;  // bias: N fp32 (padded with zeros)
-    uint16_t K, N;              // K in {16, 32}, N in {16, 32}
+    uint32_t w_hi, w_lo;
+    uint16_t K, N;        // K in {16, 48}, N in {16, 32}
+    uint32_t ones_slice;  // K16 slice index holding the ones column, or 0xFFFFFFFF
 };
 
 struct NetDesc {

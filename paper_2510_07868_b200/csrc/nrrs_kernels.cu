@@ -25,8 +25,9 @@ namespace nrrs {
 // ===========================================================================
 constexpr int kTileM = 128;          // vertices per MMA tile (UMMA M)
 constexpr int kAChunkStride = 128;   // bytes between 16-byte K chunks (LBO)
-constexpr int kASbo = 512;           // bytes between 8-row groups (K = 32 -> 4 chunks)
-constexpr int kABytes = kTileM * 32 * 2;
+constexpr int kAChunks = 6;          // K = 48: 32 data columns + a constant-ones slice (bias)
+constexpr int kASbo = kAChunks * 128;  // bytes between 8-row groups
+constexpr int kABytes = kTileM * kAChunks * 16;
 
 struct InferSmemHeader {
     uint64_t mbar;
@@ -37,8 +38,18 @@ struct InferSmemHeader {
     uint32_t warp_bc[4];
 };
 
-// Writes one 32-wide (kchunks*8 used) fp32 row as fp16 hi/lo into the K-major
-// canonical A tiles (3-term split: x = hi + lo).
+// fp32 -> fp16 hi/lo split of two values with packed conversions
+// (x = hi + lo to ~22 bits).
+__device__ __forceinline__ void split2(float v0, float v1, uint32_t &h, uint32_t &l) {
+    const __half2 hh = __float22half2_rn(make_float2(v0, v1));
+    const float2 b = __half22float2(hh);
+    const __half2 ll = __float22half2_rn(make_float2(v0 - b.x, v1 - b.y));
+    h = *reinterpret_cast<const uint32_t *>(&hh);
+    l = *reinterpret_cast<const uint32_t *>(&ll);
+}
+
+// Writes kchunks*8 fp32 values of this thread's row into the K-major canonical
+// A tiles as fp16 hi / lo.
 __device__ __forceinline__ void write_a_row(uint8_t *a_hi, uint8_t *a_lo, int row, const float *x,
                                             int kchunks) {
     const int base = (row >> 3) * kASbo + (row & 7) * 16;
@@ -48,20 +59,16 @@ __device__ __forceinline__ void write_a_row(uint8_t *a_hi, uint8_t *a_lo, int ro
             break;
         uint32_t h[4], l[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const float v0 = x[c * 8 + 2 * e], v1 = x[c * 8 + 2 * e + 1];
-            const __half h0 = __float2half_rn(v0), h1 = __float2half_rn(v1);
-            const __half l0 = __float2half_rn(v0 - __half2float(h0));
-            const __half l1 = __float2half_rn(v1 - __half2float(h1));
-            h[e] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
-            l[e] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
-        }
+        for (int e = 0; e < 4; ++e)
+            split2(x[c * 8 + 2 * e], x[c * 8 + 2 * e + 1], h[e], l[e]);
         *reinterpret_cast<uint4 *>(a_hi + base + c * kAChunkStride) = make_uint4(h[0], h[1], h[2], h[3]);
         *reinterpret_cast<uint4 *>(a_lo + base + c * kAChunkStride) = make_uint4(l[0], l[1], l[2], l[3]);
     }
 }
 
-// Barrier + one MMA layer (3-term split) + wait for the accumulator.
+// Barrier + one MMA layer + wait for the accumulator.  3-term split
+// (hi*Whi + lo*Whi + hi*Wlo) on data slices; the constant-ones slice carries
+// the bias column (1*bias_hi + 1*bias_lo).
 __device__ __forceinline__ void mma_layer(const uint8_t *smem_w, const LayerDesc &L, const uint8_t *a_hi,
                                           const uint8_t *a_lo, uint32_t tmem_d, uint64_t *bar,
                                           uint32_t &phase) {
@@ -76,12 +83,17 @@ __device__ __forceinline__ void mma_layer(const uint8_t *smem_w, const LayerDesc
         const uint32_t w_sbo = (uint32_t)L.K * 16u;
         for (uint32_t s = 0; s < (uint32_t)L.K / 16u; ++s) {
             const uint64_t ah = make_smem_desc(a_hi_s + s * 256u, kAChunkStride, kASbo);
-            const uint64_t al = make_smem_desc(a_lo_s + s * 256u, kAChunkStride, kASbo);
             const uint64_t wh = make_smem_desc(w_hi_s + s * 256u, kAChunkStride, w_sbo);
             const uint64_t wl = make_smem_desc(w_lo_s + s * 256u, kAChunkStride, w_sbo);
-            mma_f16(tmem_d, ah, wh, idesc, s > 0 ? 1u : 0u);
-            mma_f16(tmem_d, al, wh, idesc, 1u);
-            mma_f16(tmem_d, ah, wl, idesc, 1u);
+            if (s == L.ones_slice) {
+                mma_f16(tmem_d, ah, wh, idesc, 1u);
+                mma_f16(tmem_d, ah, wl, idesc, 1u);
+            } else {
+                const uint64_t al = make_smem_desc(a_lo_s + s * 256u, kAChunkStride, kASbo);
+                mma_f16(tmem_d, ah, wh, idesc, s > 0 ? 1u : 0u);
+                mma_f16(tmem_d, al, wh, idesc, 1u);
+                mma_f16(tmem_d, ah, wl, idesc, 1u);
+            }
         }
         mma_commit(bar);
     }
@@ -90,34 +102,24 @@ __device__ __forceinline__ void mma_layer(const uint8_t *smem_w, const LayerDesc
     tc_fence_after();
 }
 
-// Runs a 3-hidden-layer MLP (mlp.cpp:52-72) for this thread's row. The input
-// row must already be in a_hi/a_lo.  Head outputs (N = 16 columns) land in y.
+// 3-hidden-layer MLP (mlp.cpp:52-72) for this thread's row; the layer-0 input
+// must already be in a_hi/a_lo.  Head outputs (16 columns, bias included) -> y.
 __device__ __forceinline__ void run_mlp(const uint8_t *smem_w, const NetDesc &net, uint8_t *a_hi, uint8_t *a_lo,
                                         uint32_t tmem_base, uint32_t tmem_row, uint64_t *bar, uint32_t &phase,
                                         float (&y)[16]) {
     const int row = threadIdx.x;
 #pragma unroll 1
     for (int l = 0; l < 3; ++l) {
-        const LayerDesc &L = net.layer[l];
-        mma_layer(smem_w, L, a_hi, a_lo, tmem_base, bar, phase);
+        mma_layer(smem_w, net.layer[l], a_hi, a_lo, tmem_base, bar, phase);
         float acc[32];
         tmem_ld32(tmem_row, acc);
-        const float *b = reinterpret_cast<const float *>(smem_w + L.bias);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            const float z = acc[i] + b[i];
-            const float zs = z * 0.01f;
-            acc[i] = z < zs ? zs : z;  // cwiseMax(z, slope * z)
-        }
+        for (int i = 0; i < 32; ++i)
+            acc[i] = fmaxf(acc[i], acc[i] * 0.01f);  // leaky ReLU = cwiseMax(z, slope z)
         write_a_row(a_hi, a_lo, row, acc, 4);
     }
-    const LayerDesc &H = net.layer[3];
-    mma_layer(smem_w, H, a_hi, a_lo, tmem_base, bar, phase);
+    mma_layer(smem_w, net.layer[3], a_hi, a_lo, tmem_base, bar, phase);
     tmem_ld16(tmem_row, y);
-    const float *b = reinterpret_cast<const float *>(smem_w + H.bias);
-#pragma unroll
-    for (int i = 0; i < 16; ++i)
-        y[i] += b[i];
 }
 
 // HashGrid::encode for one point (hashgrid.cpp:38-82), F = 2, L <= 8.
@@ -138,28 +140,30 @@ __device__ __forceinline__ void grid_encode(const float2 *__restrict__ theta, co
         const uint32_t cy = min((uint32_t)fy, res - 1u);
         const uint32_t cz = min((uint32_t)fz, res - 1u);
         const float tx = fx - (float)cx, ty = fy - (float)cy, tz = fz - (float)cz;
-        const bool dense = (g.dense_mask >> l) & 1u;
         const float2 *lvl = theta + (size_t)l * g.table_size;
         uint32_t idx[8];
+        if ((g.dense_mask >> l) & 1u) {
+            const uint32_t nn = res + 1u;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-            const uint32_t x = cx + (c & 1), y = cy + ((c >> 1) & 1), z = cz + ((c >> 2) & 1);
-            if (dense) {
-                const uint32_t nn = res + 1u;
-                idx[c] = (x * nn + y) * nn + z;
-            } else {
-                idx[c] = (x ^ (y * 2654435761u) ^ (z * 805459861u)) & (g.table_size - 1u);
-            }
+            for (int c = 0; c < 8; ++c)
+                idx[c] = ((cx + (c & 1)) * nn + cy + ((c >> 1) & 1)) * nn + cz + ((c >> 2) & 1);
+        } else {
+            const uint32_t y0 = cy * 2654435761u, y1 = (cy + 1u) * 2654435761u;
+            const uint32_t z0 = cz * 805459861u, z1 = (cz + 1u) * 805459861u;
+            const uint32_t m = g.table_size - 1u;
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                idx[c] = ((cx + (c & 1)) ^ ((c & 2) ? y1 : y0) ^ ((c & 4) ? z1 : z0)) & m;
         }
         float2 v[8];
 #pragma unroll
         for (int c = 0; c < 8; ++c)
             v[c] = __ldg(lvl + idx[c]);
+        const float wx0 = 1.0f - tx, wy0 = 1.0f - ty, wz0 = 1.0f - tz;
         float a0 = 0.0f, a1 = 0.0f;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-            const float w = ((c & 1) ? tx : 1.0f - tx) * (((c >> 1) & 1) ? ty : 1.0f - ty) *
-                            (((c >> 2) & 1) ? tz : 1.0f - tz);
+            const float w = ((c & 1) ? tx : wx0) * ((c & 2) ? ty : wy0) * ((c & 4) ? tz : wz0);
             a0 += w * v[c].x;
             a1 += w * v[c].y;
         }
@@ -167,6 +171,25 @@ __device__ __forceinline__ void grid_encode(const float2 *__restrict__ theta, co
         out[2 * l + 1] = a1;
     }
 }
+
+// one_blob_encode (encodings.hpp:31-44) with the fast exp (tolerance path).
+template <int BINS>
+__device__ __forceinline__ void one_blob_fast(float x, float *out) {
+    constexpr float inv_two_sigma2 = (float)(BINS * BINS) * 0.5f;
+    float sum = 0.0f;
+#pragma unroll
+    for (int i = 0; i < BINS; ++i) {
+        const float d = x - ((float)i + 0.5f) / (float)BINS;
+        out[i] = __expf(-d * d * inv_two_sigma2);
+        sum += out[i];
+    }
+    const float inv = __fdividef(1.0f, sum);
+#pragma unroll
+    for (int i = 0; i < BINS; ++i)
+        out[i] *= inv;
+}
+
+__device__ __forceinline__ float remap_fast(float a) { return 1.0f - __expf(-a); }
 
 template <int KIND>
 __global__ void __launch_bounds__(kTileM, 4) infer_kernel(InferParams p) {
@@ -186,6 +209,16 @@ __global__ void __launch_bounds__(kTileM, 4) infer_kernel(InferParams p) {
         uint4 *dst = reinterpret_cast<uint4 *>(smem_w);
         for (uint32_t i = tid; i < p.blob_bytes / 16u; i += kTileM)
             dst[i] = __ldg(src + i);
+        // constant-ones slice of the A tiles: column 32 = 1 (hi), everything else 0
+        {
+            const int base = (tid >> 3) * kASbo + (tid & 7) * 16;
+            const uint4 one = make_uint4(0x3C00u, 0u, 0u, 0u);  // fp16 1.0 in column 32
+            const uint4 zero = make_uint4(0u, 0u, 0u, 0u);
+            *reinterpret_cast<uint4 *>(a_hi + base + 4 * kAChunkStride) = one;
+            *reinterpret_cast<uint4 *>(a_hi + base + 5 * kAChunkStride) = zero;
+            *reinterpret_cast<uint4 *>(a_lo + base + 4 * kAChunkStride) = zero;
+            *reinterpret_cast<uint4 *>(a_lo + base + 5 * kAChunkStride) = zero;
+        }
         if (tid == 0) {
             mbar_init(&hdr->mbar, 1);
             fence_barrier_init();
@@ -203,8 +236,9 @@ __global__ void __launch_bounds__(kTileM, 4) infer_kernel(InferParams p) {
     const uint64_t num_tiles = (n + kTileM - 1) / kTileM;
     const uint64_t t_begin = num_tiles * blockIdx.x / gridDim.x;
     const uint64_t t_end = num_tiles * (blockIdx.x + 1) / gridDim.x;
-    double cta_sum = 0.0;
-    uint32_t cta_nonfinite = 0, cta_bc = 0;
+    // per-thread accumulators, reduced once per CTA in a fixed order (deterministic)
+    double my_sum = 0.0;
+    uint32_t my_nonfinite = 0, my_bc = 0;
 
     for (uint64_t tile = t_begin; tile < t_end; ++tile) {
         const uint64_t j = tile * kTileM + tid;
@@ -244,27 +278,26 @@ __global__ void __launch_bounds__(kTileM, 4) infer_kernel(InferParams p) {
         } else {
             float x[32];
             float y[16];
-            if (KIND == kKindAid) {
+            if (KIND == kKindAid)
                 grid_encode(p.rrs_grid, p.grid, px, py, pz, x);
-            } else {
+            else
                 grid_encode(p.stat_grid, p.grid, px, py, pz, x);
-            }
             // kernel K layout (host packs W columns to match): grid features of
             // levels 0..7 in [0,16) (zero past L), the 16-wide tail in [16,32)
-            // (networks.cpp:131-135 / :149-157).
+            // (networks.cpp:131-135 / :149-157), bias in the ones slice.
             float *tail = x + 16;
             if (KIND == kKindAid) {
-                one_blob<4>(wox, tail);
-                one_blob<4>(woy, tail + 4);
+                one_blob_fast<4>(wox, tail);
+                one_blob_fast<4>(woy, tail + 4);
                 tail[8] = box_cox(wx, bc);
                 tail[9] = box_cox(wy, bc);
                 tail[10] = box_cox(wz, bc);
                 tail[11] = box_cox(mean3(ipx, ipy, ipz), bc);
-                one_blob<4>(roughness_remap(rough), tail + 12);
+                one_blob_fast<4>(remap_fast(rough), tail + 12);
             } else {
-                one_blob<4>(wox, tail);
-                one_blob<4>(woy, tail + 4);
-                one_blob<8>(roughness_remap(rough), tail + 8);
+                one_blob_fast<4>(wox, tail);
+                one_blob_fast<4>(woy, tail + 4);
+                one_blob_fast<8>(remap_fast(rough), tail + 8);
             }
             if (!active) {
 #pragma unroll
@@ -298,13 +331,14 @@ __global__ void __launch_bounds__(kTileM, 4) infer_kernel(InferParams p) {
                     xin[7] = box_cox(wy, bc2);
                     xin[8] = box_cox(wz, bc2);
                     xin[9] = box_cox(mean3(ipx, ipy, ipz), bc2);
-                    xin[10] = roughness_remap(rough);
+                    xin[10] = remap_fast(rough);
+                    xin[11] = 1.0f;  // bias column of the RRSNet first layer
 #pragma unroll
-                    for (int c = 11; c < 16; ++c)
+                    for (int c = 12; c < 16; ++c)
                         xin[c] = 0.0f;
                     if (!active) {
 #pragma unroll
-                        for (int c = 0; c < 16; ++c)
+                        for (int c = 0; c < 11; ++c)
                             xin[c] = 0.0f;
                         bc2 = 0;
                     }
@@ -320,7 +354,6 @@ __global__ void __launch_bounds__(kTileM, 4) infer_kernel(InferParams p) {
 
         if constexpr (KIND != kKindStats) {
             uint32_t decided = active ? 1u : 0u;
-            uint32_t nonfinite = 0;
             if (p.gate) {
                 if (valid && depth1)
                     q = 1.0f;  // depth-1 pin (wavefront.cpp:373-375)
@@ -330,37 +363,18 @@ __global__ void __launch_bounds__(kTileM, 4) infer_kernel(InferParams p) {
                 if (valid && (!isfinite(q) || q < 0.0f)) {  // sanitize (wavefront.cpp:381-385)
                     q = 0.0f;
                     decided = 0;
-                    nonfinite = 1;
+                    ++my_nonfinite;
                 }
             }
-            if (!valid)
-                q = 0.0f;
             if (valid) {
                 p.q_out[j] = q;
                 if (p.u_out)
                     p.u_out[j] = rrs_uniform(p.mixed_seed, key, p.depth);
                 if (p.decided_out)
                     p.decided_out[j] = (uint8_t)decided;
+                my_sum += (double)q;
+                my_bc += bc;
             }
-            // deterministic tile sum: butterfly per warp, then warps in order
-            double s = (double)q;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1)
-                s += __shfl_xor_sync(0xffffffffu, s, o);
-            uint32_t nf = __reduce_add_sync(0xffffffffu, nonfinite);
-            uint32_t bcs = __reduce_add_sync(0xffffffffu, bc);
-            if (lane == 0) {
-                hdr->warp_sums[warp] = s;
-                hdr->warp_cnt[warp] = nf;
-                hdr->warp_bc[warp] = bcs;
-            }
-            __syncthreads();
-            if (tid == 0) {
-                cta_sum += ((hdr->warp_sums[0] + hdr->warp_sums[1]) + hdr->warp_sums[2]) + hdr->warp_sums[3];
-                cta_nonfinite += hdr->warp_cnt[0] + hdr->warp_cnt[1] + hdr->warp_cnt[2] + hdr->warp_cnt[3];
-                cta_bc += hdr->warp_bc[0] + hdr->warp_bc[1] + hdr->warp_bc[2] + hdr->warp_bc[3];
-            }
-            __syncthreads();
         }
     }
 
@@ -374,11 +388,25 @@ __global__ void __launch_bounds__(kTileM, 4) infer_kernel(InferParams p) {
         return;
     if (p.parts == nullptr)
         return;
-    // ---- last-CTA-done reduction of the per-CTA partial sums in CTA order ----
+    // ---- CTA sum in a fixed tree, then last-CTA-done reduction in CTA order ----
+    {
+        double s = my_sum;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+            s += __shfl_xor_sync(0xffffffffu, s, o);
+        const uint32_t nf = __reduce_add_sync(0xffffffffu, my_nonfinite);
+        const uint32_t bcs = __reduce_add_sync(0xffffffffu, my_bc);
+        if (lane == 0) {
+            hdr->warp_sums[warp] = s;
+            hdr->warp_cnt[warp] = nf;
+            hdr->warp_bc[warp] = bcs;
+        }
+        __syncthreads();
+    }
     if (tid == 0) {
-        p.parts[blockIdx.x] = cta_sum;
-        p.part_counts[2 * blockIdx.x] = cta_nonfinite;
-        p.part_counts[2 * blockIdx.x + 1] = cta_bc;
+        p.parts[blockIdx.x] = ((hdr->warp_sums[0] + hdr->warp_sums[1]) + hdr->warp_sums[2]) + hdr->warp_sums[3];
+        p.part_counts[2 * blockIdx.x] = hdr->warp_cnt[0] + hdr->warp_cnt[1] + hdr->warp_cnt[2] + hdr->warp_cnt[3];
+        p.part_counts[2 * blockIdx.x + 1] = hdr->warp_bc[0] + hdr->warp_bc[1] + hdr->warp_bc[2] + hdr->warp_bc[3];
         __threadfence();
         const uint32_t prev = atomicAdd(p.counter, 1u);
         hdr->is_last = (prev == gridDim.x - 1) ? 1u : 0u;
@@ -399,6 +427,7 @@ __global__ void __launch_bounds__(kTileM, 4) infer_kernel(InferParams p) {
         s += __shfl_xor_sync(0xffffffffu, s, o);
     nf = __reduce_add_sync(0xffffffffu, nf);
     bcs = __reduce_add_sync(0xffffffffu, bcs);
+    __syncthreads();
     if (lane == 0) {
         hdr->warp_sums[warp] = s;
         hdr->warp_cnt[warp] = nf;
@@ -552,8 +581,11 @@ __global__ void __launch_bounds__(kDecThreads) decide_kernel(DecideParams p) {
             sm.incl[tid * kDecItems + i] = run;
         }
     }
-    if (tid == 0)
-        sm.prefix = lookback_exclusive(p.tile_state, tile, agg, p.epoch);
+    if (tid < 32) {
+        const uint64_t ex = lookback_warp(p.tile_state, tile, agg, p.epoch);
+        if (tid == 0)
+            sm.prefix = ex;
+    }
     __syncthreads();
     const uint64_t P = sm.prefix;
     const uint64_t cap = p.capacity;
@@ -638,8 +670,11 @@ __global__ void __launch_bounds__(kDecThreads) compact_kernel(CompactParams p) {
     }
     uint32_t agg = 0;
     const uint32_t excl = block_exclusive_scan(cnt, warp_tot, agg);
-    if (tid == 0)
-        prefix_s = lookback_exclusive(p.tile_state, tile, agg, p.epoch);
+    if (tid < 32) {
+        const uint64_t ex = lookback_warp(p.tile_state, tile, agg, p.epoch);
+        if (tid == 0)
+            prefix_s = ex;
+    }
     const uint32_t *in = reinterpret_cast<const uint32_t *>(p.in);
     uint32_t pos = excl;
 #pragma unroll
@@ -760,11 +795,25 @@ __global__ void realize_kernel(const float *q, const float *u, int32_t *counts, 
 // launch wrappers (called from the C ABI layer)
 // ===========================================================================
 template <int KIND>
-static int infer_occupancy(size_t smem) {
-    int nb = 0;
-    cudaFuncSetAttribute(infer_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, infer_kernel<KIND>, kTileM, smem);
-    return nb < 1 ? 1 : nb;
+static cudaError_t infer_occupancy(size_t smem, int *occ) {
+    cudaFuncAttributes a{};
+    cudaError_t e = cudaFuncGetAttributes(&a, infer_kernel<KIND>);
+    if (e != cudaSuccess)
+        return e;
+    if (smem > 48 * 1024) {
+        e = cudaFuncSetAttribute(infer_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess)
+            return e;
+    }
+    // registers: allocation granule 8 per thread, warp granule 256 -> per-CTA regs
+    const int regs = ((a.numRegs + 7) / 8) * 8 * kTileM;
+    const int by_regs = 65536 / (regs > 0 ? regs : 1);
+    const int by_smem = (228 * 1024) / (int)(smem + a.sharedSizeBytes + 1024);
+    int o = by_regs < by_smem ? by_regs : by_smem;
+    if (o > 8)
+        o = 8;
+    *occ = o < 1 ? 1 : o;
+    return cudaSuccess;
 }
 
 size_t infer_smem_bytes(int kind, const InferParams &p) {
@@ -777,15 +826,16 @@ cudaError_t launch_infer(int kind, const InferParams &p, int num_sms, cudaStream
     const uint64_t tiles = (p.n + kTileM - 1) / kTileM;
     const size_t smem = infer_smem_bytes(kind, p);
     int occ = 1;
+    cudaError_t e = cudaSuccess;
     switch (kind) {
-    case kKindHeuristic: occ = infer_occupancy<kKindHeuristic>(smem); break;
-    case kKindAdrrs: occ = infer_occupancy<kKindAdrrs>(smem); break;
-    case kKindNrrs: occ = infer_occupancy<kKindNrrs>(smem); break;
-    case kKindAid: occ = infer_occupancy<kKindAid>(smem); break;
-    case kKindStats: occ = infer_occupancy<kKindStats>(smem); break;
+    case kKindHeuristic: e = infer_occupancy<kKindHeuristic>(smem, &occ); break;
+    case kKindAdrrs: e = infer_occupancy<kKindAdrrs>(smem, &occ); break;
+    case kKindNrrs: e = infer_occupancy<kKindNrrs>(smem, &occ); break;
+    case kKindAid: e = infer_occupancy<kKindAid>(smem, &occ); break;
+    case kKindStats: e = infer_occupancy<kKindStats>(smem, &occ); break;
     }
-    if (kind != kKindHeuristic && occ > 4)
-        occ = 4;  // <= 4 x 32 TMEM columns per SM leaves room for other tenants
+    if (e != cudaSuccess)
+        return e;
     uint64_t grid = (uint64_t)num_sms * (uint64_t)occ;
     if (grid > tiles)
         grid = tiles;

@@ -1,0 +1,33 @@
+"""Minimal driver for ncu captures: runs the stage on a synthetic batch `reps` times.
+usage: python tools/prof_stage.py [aid|nrrs|adrrs|throughput] [n] [reps]"""
+import sys
+import os
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+from paper_2510_07868_b200 import (NeuralRrs, NeuralRrsConfig, RateControl, RrsStage, RrsVariant, Strategy,
+                                   StrategyKind, synthetic)
+
+kind = sys.argv[1] if len(sys.argv) > 1 else "aid"
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 1920 * 1080
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+variant = RrsVariant.Nrrs if kind == "nrrs" else RrsVariant.Aid
+nets = NeuralRrs(NeuralRrsConfig(variant=variant, seed=1)).randomize_for_benchmark()
+strat = {"aid": StrategyKind.AidNrrs, "nrrs": StrategyKind.Nrrs, "adrrs": StrategyKind.AdrrsNn,
+         "throughput": StrategyKind.Throughput}[kind]
+hv = synthetic.gen_vertices(n)
+dv = {k: torch.from_numpy(a.view(np.int64) if a.dtype == np.uint64 else a).cuda() for k, a in hv.items()
+      if k != "pixel"}
+st = RrsStage(n, nets)
+out = st.alloc_outputs(n)
+for _ in range(reps):
+    st.run(dv, 2, Strategy(strat), rc=RateControl(), out=out, sync=False)
+torch.cuda.synchronize()
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+a.record()
+st.run(dv, 2, Strategy(strat), rc=RateControl(), out=out, sync=False)
+b.record()
+torch.cuda.synchronize()
+print(f"{kind} n={n}: stage {a.elapsed_time(b):.3f} ms")
