@@ -22,20 +22,28 @@ namespace nrrs {
 
 // ===========================================================================
 // K-A: factor inference
+//
+// One CTA = one 128-vertex tile at a time (UMMA M = 128), 256 threads: thread
+// t owns tile row r = t & 127 and half h = t >> 7.  Half 0 encodes hash-grid
+// levels 0-3 and tail[0..7]; half 1 levels 4-7 and tail[8..15]; in every MLP
+// epilogue half h drains TMEM columns [16h, 16h+16).  Warps w and w+4 share
+// TMEM lane quarter w (tcgen05.ld lane-access rule).
 // ===========================================================================
-constexpr int kTileM = 128;          // vertices per MMA tile (UMMA M)
-constexpr int kAChunkStride = 128;   // bytes between 16-byte K chunks (LBO)
-constexpr int kAChunks = 6;          // K = 48: 32 data columns + a constant-ones slice (bias)
-constexpr int kASbo = kAChunks * 128;  // bytes between 8-row groups
-constexpr int kABytes = kTileM * kAChunks * 16;
+constexpr int kTileM = 128;           // vertices per MMA tile (UMMA M)
+constexpr int kInferThreads = 256;    // 2 threads per tile row
+constexpr int kAChunkStride = 128;    // bytes between 16-byte K chunks (LBO)
+constexpr int kASbo = 512;            // bytes between 8-row groups (K = 32 -> 4 chunks)
+constexpr int kABytes = kTileM * 32 * 2;
+constexpr int kOnesSbo = 256;         // ones slice: K = 16 -> 2 chunks per 8-row group
+constexpr int kOnesBytes = kTileM * 16 * 2;
 
 struct InferSmemHeader {
     uint64_t mbar;
     uint32_t tmem_base;
     uint32_t is_last;
-    double warp_sums[4];
-    uint32_t warp_cnt[4];
-    uint32_t warp_bc[4];
+    double warp_sums[8];
+    uint32_t warp_cnt[8];
+    uint32_t warp_bc[8];
 };
 
 // fp32 -> fp16 hi/lo split of two values with packed conversions
@@ -48,30 +56,24 @@ __device__ __forceinline__ void split2(float v0, float v1, uint32_t &h, uint32_t
     l = *reinterpret_cast<const uint32_t *>(&ll);
 }
 
-// Writes kchunks*8 fp32 values of this thread's row into the K-major canonical
-// A tiles as fp16 hi / lo.
-__device__ __forceinline__ void write_a_row(uint8_t *a_hi, uint8_t *a_lo, int row, const float *x,
-                                            int kchunks) {
-    const int base = (row >> 3) * kASbo + (row & 7) * 16;
+// 8 fp32 values -> chunk `c` (K columns 8c..8c+7) of row `row` in the K-major
+// canonical hi / lo A tiles.
+__device__ __forceinline__ void write_a_chunk(uint8_t *a_hi, uint8_t *a_lo, int row, int c, const float *x) {
+    const int off = (row >> 3) * kASbo + c * kAChunkStride + (row & 7) * 16;
+    uint32_t h[4], l[4];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        if (c >= kchunks)
-            break;
-        uint32_t h[4], l[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-            split2(x[c * 8 + 2 * e], x[c * 8 + 2 * e + 1], h[e], l[e]);
-        *reinterpret_cast<uint4 *>(a_hi + base + c * kAChunkStride) = make_uint4(h[0], h[1], h[2], h[3]);
-        *reinterpret_cast<uint4 *>(a_lo + base + c * kAChunkStride) = make_uint4(l[0], l[1], l[2], l[3]);
-    }
+    for (int e = 0; e < 4; ++e)
+        split2(x[2 * e], x[2 * e + 1], h[e], l[e]);
+    *reinterpret_cast<uint4 *>(a_hi + off) = make_uint4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<uint4 *>(a_lo + off) = make_uint4(l[0], l[1], l[2], l[3]);
 }
 
 // Barrier + one MMA layer + wait for the accumulator.  3-term split
-// (hi*Whi + lo*Whi + hi*Wlo) on data slices; the constant-ones slice carries
-// the bias column (1*bias_hi + 1*bias_lo).
+// (hi*Whi + lo*Whi + hi*Wlo) on data slices; the shared constant-ones slice
+// carries the bias column (1*bias_hi + 1*bias_lo).
 __device__ __forceinline__ void mma_layer(const uint8_t *smem_w, const LayerDesc &L, const uint8_t *a_hi,
-                                          const uint8_t *a_lo, uint32_t tmem_d, uint64_t *bar,
-                                          uint32_t &phase) {
+                                          const uint8_t *a_lo, const uint8_t *ones, uint32_t tmem_d,
+                                          uint64_t *bar, uint32_t &phase) {
     fence_proxy_async_smem();
     tc_fence_before();
     __syncthreads();
@@ -82,13 +84,14 @@ __device__ __forceinline__ void mma_layer(const uint8_t *smem_w, const LayerDesc
         const uint32_t w_hi_s = smem_u32(smem_w + L.w_hi), w_lo_s = smem_u32(smem_w + L.w_lo);
         const uint32_t w_sbo = (uint32_t)L.K * 16u;
         for (uint32_t s = 0; s < (uint32_t)L.K / 16u; ++s) {
-            const uint64_t ah = make_smem_desc(a_hi_s + s * 256u, kAChunkStride, kASbo);
             const uint64_t wh = make_smem_desc(w_hi_s + s * 256u, kAChunkStride, w_sbo);
             const uint64_t wl = make_smem_desc(w_lo_s + s * 256u, kAChunkStride, w_sbo);
             if (s == L.ones_slice) {
-                mma_f16(tmem_d, ah, wh, idesc, 1u);
-                mma_f16(tmem_d, ah, wl, idesc, 1u);
+                const uint64_t o = make_smem_desc(smem_u32(ones), kAChunkStride, kOnesSbo);
+                mma_f16(tmem_d, o, wh, idesc, 1u);
+                mma_f16(tmem_d, o, wl, idesc, 1u);
             } else {
+                const uint64_t ah = make_smem_desc(a_hi_s + s * 256u, kAChunkStride, kASbo);
                 const uint64_t al = make_smem_desc(a_lo_s + s * 256u, kAChunkStride, kASbo);
                 mma_f16(tmem_d, ah, wh, idesc, s > 0 ? 1u : 0u);
                 mma_f16(tmem_d, al, wh, idesc, 1u);
@@ -102,35 +105,35 @@ __device__ __forceinline__ void mma_layer(const uint8_t *smem_w, const LayerDesc
     tc_fence_after();
 }
 
-// 3-hidden-layer MLP (mlp.cpp:52-72) for this thread's row; the layer-0 input
-// must already be in a_hi/a_lo.  Head outputs (16 columns, bias included) -> y.
+// 3-hidden-layer MLP (mlp.cpp:52-72); the layer-0 input must be in a_hi/a_lo.
+// Head outputs (columns 0..15, bias included) land in y on half-0 threads.
 __device__ __forceinline__ void run_mlp(const uint8_t *smem_w, const NetDesc &net, uint8_t *a_hi, uint8_t *a_lo,
-                                        uint32_t tmem_base, uint32_t tmem_row, uint64_t *bar, uint32_t &phase,
-                                        float (&y)[16]) {
-    const int row = threadIdx.x;
+                                        const uint8_t *ones, uint32_t tmem_base, uint32_t tmem_row, int row,
+                                        int half, uint64_t *bar, uint32_t &phase, float (&y)[16]) {
 #pragma unroll 1
     for (int l = 0; l < 3; ++l) {
-        mma_layer(smem_w, net.layer[l], a_hi, a_lo, tmem_base, bar, phase);
-        float acc[32];
-        tmem_ld32(tmem_row, acc);
+        mma_layer(smem_w, net.layer[l], a_hi, a_lo, ones, tmem_base, bar, phase);
+        float acc[16];
+        tmem_ld16(tmem_row + 16u * (uint32_t)half, acc);
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
+        for (int i = 0; i < 16; ++i)
             acc[i] = fmaxf(acc[i], acc[i] * 0.01f);  // leaky ReLU = cwiseMax(z, slope z)
-        write_a_row(a_hi, a_lo, row, acc, 4);
+        write_a_chunk(a_hi, a_lo, row, 2 * half, acc);
+        write_a_chunk(a_hi, a_lo, row, 2 * half + 1, acc + 8);
     }
-    mma_layer(smem_w, net.layer[3], a_hi, a_lo, tmem_base, bar, phase);
-    tmem_ld16(tmem_row, y);
+    mma_layer(smem_w, net.layer[3], a_hi, a_lo, ones, tmem_base, bar, phase);
+    tmem_ld16(tmem_row, y);  // both halves load (lane-aligned), half 0 uses it
 }
 
-// HashGrid::encode for one point (hashgrid.cpp:38-82), F = 2, L <= 8.
-__device__ __forceinline__ void grid_encode(const float2 *__restrict__ theta, const GridDev &g, float px,
-                                            float py, float pz, float *out) {
-    const float cpx = clamp01(px), cpy = clamp01(py), cpz = clamp01(pz);
+// HashGrid::encode (hashgrid.cpp:38-82) for levels [l0, l0+4) of one point, F = 2.
+__device__ __forceinline__ void grid_encode4(const float2 *__restrict__ theta, const GridDev &g, int l0,
+                                             float cpx, float cpy, float cpz, float *out) {
 #pragma unroll
-    for (int l = 0; l < 8; ++l) {
+    for (int i = 0; i < 4; ++i) {
+        const int l = l0 + i;
         if (l >= g.levels) {
-            out[2 * l] = 0.0f;
-            out[2 * l + 1] = 0.0f;
+            out[2 * i] = 0.0f;
+            out[2 * i + 1] = 0.0f;
             continue;
         }
         const uint32_t res = (uint32_t)g.base_resolution << l;
@@ -167,8 +170,8 @@ __device__ __forceinline__ void grid_encode(const float2 *__restrict__ theta, co
             a0 += w * v[c].x;
             a1 += w * v[c].y;
         }
-        out[2 * l] = a0;
-        out[2 * l + 1] = a1;
+        out[2 * i] = a0;
+        out[2 * i + 1] = a1;
     }
 }
 
@@ -192,14 +195,16 @@ __device__ __forceinline__ void one_blob_fast(float x, float *out) {
 __device__ __forceinline__ float remap_fast(float a) { return 1.0f - __expf(-a); }
 
 template <int KIND>
-__global__ void __launch_bounds__(kTileM, 4) infer_kernel(InferParams p) {
+__global__ void __launch_bounds__(kInferThreads, 3) infer_kernel(InferParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     constexpr bool kNeural = KIND != kKindHeuristic;
     uint8_t *a_hi = smem_raw;
     uint8_t *a_lo = smem_raw + kABytes;
-    uint8_t *smem_w = smem_raw + 2 * kABytes;
+    uint8_t *ones = smem_raw + 2 * kABytes;
+    uint8_t *smem_w = smem_raw + 2 * kABytes + kOnesBytes;
     InferSmemHeader *hdr = reinterpret_cast<InferSmemHeader *>(kNeural ? smem_w + p.blob_bytes : smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int row = tid & (kTileM - 1), half = tid >> 7;
 
     uint32_t phase = 0;
     uint32_t tmem_base = 0, tmem_row = 0;
@@ -207,17 +212,12 @@ __global__ void __launch_bounds__(kTileM, 4) infer_kernel(InferParams p) {
         // weights: global blob -> smem (16-byte vector copies)
         const uint4 *src = reinterpret_cast<const uint4 *>(p.blob);
         uint4 *dst = reinterpret_cast<uint4 *>(smem_w);
-        for (uint32_t i = tid; i < p.blob_bytes / 16u; i += kTileM)
+        for (uint32_t i = tid; i < p.blob_bytes / 16u; i += kInferThreads)
             dst[i] = __ldg(src + i);
-        // constant-ones slice of the A tiles: column 32 = 1 (hi), everything else 0
+        // constant-ones K16 slice: column 0 = 1 (fp16), the rest 0
         {
-            const int base = (tid >> 3) * kASbo + (tid & 7) * 16;
-            const uint4 one = make_uint4(0x3C00u, 0u, 0u, 0u);  // fp16 1.0 in column 32
-            const uint4 zero = make_uint4(0u, 0u, 0u, 0u);
-            *reinterpret_cast<uint4 *>(a_hi + base + 4 * kAChunkStride) = one;
-            *reinterpret_cast<uint4 *>(a_hi + base + 5 * kAChunkStride) = zero;
-            *reinterpret_cast<uint4 *>(a_lo + base + 4 * kAChunkStride) = zero;
-            *reinterpret_cast<uint4 *>(a_lo + base + 5 * kAChunkStride) = zero;
+            const int off = (row >> 3) * kOnesSbo + half * kAChunkStride + (row & 7) * 16;
+            *reinterpret_cast<uint4 *>(ones + off) = make_uint4(half == 0 ? 0x3C00u : 0u, 0u, 0u, 0u);
         }
         if (tid == 0) {
             mbar_init(&hdr->mbar, 1);
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(kTileM, 4) infer_kernel(InferParams p) {
         __syncthreads();
         tc_fence_after();
         tmem_base = hdr->tmem_base;
-        tmem_row = tmem_base + ((uint32_t)(warp * 32) << 16);
+        tmem_row = tmem_base + ((uint32_t)((warp & 3) * 32) << 16);
     }
 
     const uint64_t n = p.n;
@@ -241,27 +241,12 @@ __global__ void __launch_bounds__(kTileM, 4) infer_kernel(InferParams p) {
     uint32_t my_nonfinite = 0, my_bc = 0;
 
     for (uint64_t tile = t_begin; tile < t_end; ++tile) {
-        const uint64_t j = tile * kTileM + tid;
+        const uint64_t j = tile * kTileM + row;
         const bool valid = j < n;
-        float px = 0, py = 0, pz = 0, wox = 0, woy = 0, rough = 0, wx = 0, wy = 0, wz = 0, ipx = 0, ipy = 0, ipz = 0;
-        uint64_t key = 0;
+        float px = 0, py = 0, pz = 0, wx = 0, wy = 0, wz = 0;
         if (valid) {
             px = __ldg(p.p01 + 3 * j); py = __ldg(p.p01 + 3 * j + 1); pz = __ldg(p.p01 + 3 * j + 2);
             wx = __ldg(p.weight + 3 * j); wy = __ldg(p.weight + 3 * j + 1); wz = __ldg(p.weight + 3 * j + 2);
-            key = __ldg(p.path_key + j);
-            if (KIND != kKindHeuristic) {
-                wox = __ldg(p.wo01 + 2 * j); woy = __ldg(p.wo01 + 2 * j + 1);
-                rough = __ldg(p.roughness + j);
-            }
-            if (KIND == kKindNrrs || KIND == kKindAid || KIND == kKindAdrrs) {
-                if (p.i_pixel) {
-                    ipx = __ldg(p.i_pixel + 3 * j); ipy = __ldg(p.i_pixel + 3 * j + 1); ipz = __ldg(p.i_pixel + 3 * j + 2);
-                } else {
-                    const uint64_t px_idx = __ldg(p.pixel + j);
-                    ipx = __ldg(p.i_acc + 3 * px_idx); ipy = __ldg(p.i_acc + 3 * px_idx + 1);
-                    ipz = __ldg(p.i_acc + 3 * px_idx + 2);
-                }
-            }
         }
         const float lum_w = luminance(wx, wy, wz);
         // Mix-Depth gate + zero-throughput skip (wavefront.cpp:373-380)
@@ -276,104 +261,127 @@ __global__ void __launch_bounds__(kTileM, 4) infer_kernel(InferParams p) {
             else
                 q = (lum_w < 1.0f) ? lum_w : 1.0f;              // std::min(1, lum) (rrs.hpp:49-51)
         } else {
-            float x[32];
+            auto load_ipix = [&](float &a, float &b, float &c) {
+                if (!valid) {
+                    a = b = c = 0.0f;
+                } else if (p.i_pixel) {
+                    a = __ldg(p.i_pixel + 3 * j); b = __ldg(p.i_pixel + 3 * j + 1); c = __ldg(p.i_pixel + 3 * j + 2);
+                } else {
+                    const uint64_t px_idx = __ldg(p.pixel + j);
+                    a = __ldg(p.i_acc + 3 * px_idx); b = __ldg(p.i_acc + 3 * px_idx + 1); c = __ldg(p.i_acc + 3 * px_idx + 2);
+                }
+            };
+            const float rough = valid ? __ldg(p.roughness + j) : 0.0f;
             float y[16];
-            if (KIND == kKindAid)
-                grid_encode(p.rrs_grid, p.grid, px, py, pz, x);
-            else
-                grid_encode(p.stat_grid, p.grid, px, py, pz, x);
-            // kernel K layout (host packs W columns to match): grid features of
-            // levels 0..7 in [0,16) (zero past L), the 16-wide tail in [16,32)
-            // (networks.cpp:131-135 / :149-157), bias in the ones slice.
-            float *tail = x + 16;
-            if (KIND == kKindAid) {
-                one_blob_fast<4>(wox, tail);
-                one_blob_fast<4>(woy, tail + 4);
-                tail[8] = box_cox(wx, bc);
-                tail[9] = box_cox(wy, bc);
-                tail[10] = box_cox(wz, bc);
-                tail[11] = box_cox(mean3(ipx, ipy, ipz), bc);
-                one_blob_fast<4>(remap_fast(rough), tail + 12);
-            } else {
-                one_blob_fast<4>(wox, tail);
-                one_blob_fast<4>(woy, tail + 4);
-                one_blob_fast<8>(remap_fast(rough), tail + 8);
-            }
-            if (!active) {
+            {
+                // layer-0 input (networks.cpp:131-135 / :149-157); kernel K layout:
+                // grid features of levels 0..7 in [0,16), the 16-wide tail in [16,32).
+                float g8[8], t8[8];
+                grid_encode4(KIND == kKindAid ? p.rrs_grid : p.stat_grid, p.grid, 4 * half, clamp01(px),
+                             clamp01(py), clamp01(pz), g8);
+                if (half == 0) {
+                    const float wox = valid ? __ldg(p.wo01 + 2 * j) : 0.0f;
+                    const float woy = valid ? __ldg(p.wo01 + 2 * j + 1) : 0.0f;
+                    one_blob_fast<4>(wox, t8);
+                    one_blob_fast<4>(woy, t8 + 4);
+                } else if (KIND == kKindAid) {
+                    float ipx, ipy, ipz;
+                    load_ipix(ipx, ipy, ipz);
+                    t8[0] = box_cox(wx, bc);
+                    t8[1] = box_cox(wy, bc);
+                    t8[2] = box_cox(wz, bc);
+                    t8[3] = box_cox(mean3(ipx, ipy, ipz), bc);
+                    one_blob_fast<4>(remap_fast(rough), t8 + 4);
+                } else {
+                    one_blob_fast<8>(remap_fast(rough), t8);
+                }
+                if (!valid) {
 #pragma unroll
-                for (int s = 0; s < 32; ++s)
-                    x[s] = 0.0f;
+                    for (int s = 0; s < 8; ++s) {
+                        g8[s] = 0.0f;
+                        t8[s] = 0.0f;
+                    }
+                }
+                write_a_chunk(a_hi, a_lo, row, half, g8);
+                write_a_chunk(a_hi, a_lo, row, 2 + half, t8);
             }
-            write_a_row(a_hi, a_lo, tid, x, 4);
             if (KIND == kKindAid) {
-                run_mlp(smem_w, p.nets.rrs, a_hi, a_lo, tmem_base, tmem_row, &hdr->mbar, phase, y);
+                run_mlp(smem_w, p.nets.rrs, a_hi, a_lo, ones, tmem_base, tmem_row, row, half, &hdr->mbar, phase, y);
                 q = softplus_mod(y[0]);
             } else {
-                run_mlp(smem_w, p.nets.stat, a_hi, a_lo, tmem_base, tmem_row, &hdr->mbar, phase, y);
+                run_mlp(smem_w, p.nets.stat, a_hi, a_lo, ones, tmem_base, tmem_row, row, half, &hdr->mbar, phase,
+                        y);
                 if (KIND == kKindStats) {
-                    if (valid) {
+                    if (valid && half == 0) {
 #pragma unroll
                         for (int i = 0; i < 6; ++i)
                             p.stats_out[6 * j + i] = y[i];
                     }
                 } else if (KIND == kKindAdrrs) {
                     // adrrs_factor (rrs.hpp:56-61) with eps = max(eps_div, 1e-8)
+                    float ipx, ipy, ipz;
+                    load_ipix(ipx, ipy, ipz);
                     const float num = luminance(wx * y[0], wy * y[1], wz * y[2]);
                     const float qq = num / (luminance(ipx, ipy, ipz) + p.eps);
                     q = qq < 0.05f ? 0.05f : (20.0f < qq ? 20.0f : qq);
                 } else {  // NRRS: stats -> build_nrrs_input (networks.cpp:137-147) -> RRSNet
-                    float xin[16];
-                    uint32_t bc2 = 0;
+                    if (half == 0) {
+                        float ipx, ipy, ipz;
+                        load_ipix(ipx, ipy, ipz);
+                        float xin[16];
 #pragma unroll
-                    for (int c = 0; c < 6; ++c)
-                        xin[c] = box_cox(y[c], bc2);
-                    xin[6] = box_cox(wx, bc2);
-                    xin[7] = box_cox(wy, bc2);
-                    xin[8] = box_cox(wz, bc2);
-                    xin[9] = box_cox(mean3(ipx, ipy, ipz), bc2);
-                    xin[10] = remap_fast(rough);
-                    xin[11] = 1.0f;  // bias column of the RRSNet first layer
+                        for (int c = 0; c < 6; ++c)
+                            xin[c] = box_cox(y[c], bc);
+                        xin[6] = box_cox(wx, bc);
+                        xin[7] = box_cox(wy, bc);
+                        xin[8] = box_cox(wz, bc);
+                        xin[9] = box_cox(mean3(ipx, ipy, ipz), bc);
+                        xin[10] = remap_fast(rough);
+                        xin[11] = 1.0f;  // bias column of the RRSNet first layer
 #pragma unroll
-                    for (int c = 12; c < 16; ++c)
-                        xin[c] = 0.0f;
-                    if (!active) {
-#pragma unroll
-                        for (int c = 0; c < 11; ++c)
+                        for (int c = 12; c < 16; ++c)
                             xin[c] = 0.0f;
-                        bc2 = 0;
+                        if (!valid) {
+#pragma unroll
+                            for (int c = 0; c < 11; ++c)
+                                xin[c] = 0.0f;
+                        }
+                        write_a_chunk(a_hi, a_lo, row, 0, xin);
+                        write_a_chunk(a_hi, a_lo, row, 1, xin + 8);
                     }
-                    bc += bc2;
-                    write_a_row(a_hi, a_lo, tid, xin, 2);
-                    run_mlp(smem_w, p.nets.rrs, a_hi, a_lo, tmem_base, tmem_row, &hdr->mbar, phase, y);
+                    run_mlp(smem_w, p.nets.rrs, a_hi, a_lo, ones, tmem_base, tmem_row, row, half, &hdr->mbar,
+                            phase, y);
                     q = softplus_mod(y[0]);
                 }
             }
         }
         if (!active)
             bc = 0;
+        my_bc += bc;
 
         if constexpr (KIND != kKindStats) {
-            uint32_t decided = active ? 1u : 0u;
-            if (p.gate) {
-                if (valid && depth1)
-                    q = 1.0f;  // depth-1 pin (wavefront.cpp:373-375)
-                if (!active && !depth1)
-                    q = 0.0f;
-                decided = valid && (depth1 || active) ? 1u : 0u;
-                if (valid && (!isfinite(q) || q < 0.0f)) {  // sanitize (wavefront.cpp:381-385)
-                    q = 0.0f;
-                    decided = 0;
-                    ++my_nonfinite;
+            if (half == 0) {
+                uint32_t decided = active ? 1u : 0u;
+                if (p.gate) {
+                    if (valid && depth1)
+                        q = 1.0f;  // depth-1 pin (wavefront.cpp:373-375)
+                    if (!active && !depth1)
+                        q = 0.0f;
+                    decided = valid && (depth1 || active) ? 1u : 0u;
+                    if (valid && (!isfinite(q) || q < 0.0f)) {  // sanitize (wavefront.cpp:381-385)
+                        q = 0.0f;
+                        decided = 0;
+                        ++my_nonfinite;
+                    }
                 }
-            }
-            if (valid) {
-                p.q_out[j] = q;
-                if (p.u_out)
-                    p.u_out[j] = rrs_uniform(p.mixed_seed, key, p.depth);
-                if (p.decided_out)
-                    p.decided_out[j] = (uint8_t)decided;
-                my_sum += (double)q;
-                my_bc += bc;
+                if (valid) {
+                    p.q_out[j] = q;
+                    if (p.u_out)
+                        p.u_out[j] = rrs_uniform(p.mixed_seed, __ldg(p.path_key + j), p.depth);
+                    if (p.decided_out)
+                        p.decided_out[j] = (uint8_t)decided;
+                    my_sum += (double)q;
+                }
             }
         }
     }
@@ -389,6 +397,7 @@ __global__ void __launch_bounds__(kTileM, 4) infer_kernel(InferParams p) {
     if (p.parts == nullptr)
         return;
     // ---- CTA sum in a fixed tree, then last-CTA-done reduction in CTA order ----
+    constexpr int kWarps = kInferThreads / 32;
     {
         double s = my_sum;
 #pragma unroll
@@ -404,9 +413,17 @@ __global__ void __launch_bounds__(kTileM, 4) infer_kernel(InferParams p) {
         __syncthreads();
     }
     if (tid == 0) {
-        p.parts[blockIdx.x] = ((hdr->warp_sums[0] + hdr->warp_sums[1]) + hdr->warp_sums[2]) + hdr->warp_sums[3];
-        p.part_counts[2 * blockIdx.x] = hdr->warp_cnt[0] + hdr->warp_cnt[1] + hdr->warp_cnt[2] + hdr->warp_cnt[3];
-        p.part_counts[2 * blockIdx.x + 1] = hdr->warp_bc[0] + hdr->warp_bc[1] + hdr->warp_bc[2] + hdr->warp_bc[3];
+        double cs = 0.0;
+        uint32_t cn = 0, cb = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            cs += hdr->warp_sums[w];
+            cn += hdr->warp_cnt[w];
+            cb += hdr->warp_bc[w];
+        }
+        p.parts[blockIdx.x] = cs;
+        p.part_counts[2 * blockIdx.x] = cn;
+        p.part_counts[2 * blockIdx.x + 1] = cb;
         __threadfence();
         const uint32_t prev = atomicAdd(p.counter, 1u);
         hdr->is_last = (prev == gridDim.x - 1) ? 1u : 0u;
@@ -417,7 +434,7 @@ __global__ void __launch_bounds__(kTileM, 4) infer_kernel(InferParams p) {
     __threadfence();
     double s = 0.0;
     uint32_t nf = 0, bcs = 0;
-    for (uint32_t b = tid; b < gridDim.x; b += kTileM) {
+    for (uint32_t b = tid; b < gridDim.x; b += kInferThreads) {
         s += __ldcg(p.parts + b);
         nf += __ldcg(p.part_counts + 2 * b);
         bcs += __ldcg(p.part_counts + 2 * b + 1);
@@ -435,11 +452,18 @@ __global__ void __launch_bounds__(kTileM, 4) infer_kernel(InferParams p) {
     }
     __syncthreads();
     if (tid == 0) {
-        const double total = ((hdr->warp_sums[0] + hdr->warp_sums[1]) + hdr->warp_sums[2]) + hdr->warp_sums[3];
+        double total = 0.0;
+        unsigned long long tn = 0, tb = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            total += hdr->warp_sums[w];
+            tn += hdr->warp_cnt[w];
+            tb += hdr->warp_bc[w];
+        }
         *p.sum_out = total;
         p.res->sum_q = total;
-        p.res->nonfinite = hdr->warp_cnt[0] + hdr->warp_cnt[1] + hdr->warp_cnt[2] + hdr->warp_cnt[3];
-        p.res->box_cox_clamps = hdr->warp_bc[0] + hdr->warp_bc[1] + hdr->warp_bc[2] + hdr->warp_bc[3];
+        p.res->nonfinite = tn;
+        p.res->box_cox_clamps = tb;
         *p.counter = 0;  // self-cleaning for the next launch
     }
 }
@@ -806,7 +830,7 @@ static cudaError_t infer_occupancy(size_t smem, int *occ) {
             return e;
     }
     // registers: allocation granule 8 per thread, warp granule 256 -> per-CTA regs
-    const int regs = ((a.numRegs + 7) / 8) * 8 * kTileM;
+    const int regs = ((a.numRegs + 7) / 8) * 8 * kInferThreads;
     const int by_regs = 65536 / (regs > 0 ? regs : 1);
     const int by_smem = (228 * 1024) / (int)(smem + a.sharedSizeBytes + 1024);
     int o = by_regs < by_smem ? by_regs : by_smem;
@@ -819,7 +843,7 @@ static cudaError_t infer_occupancy(size_t smem, int *occ) {
 size_t infer_smem_bytes(int kind, const InferParams &p) {
     if (kind == kKindHeuristic)
         return sizeof(InferSmemHeader) + 64;
-    return 2 * kABytes + p.blob_bytes + sizeof(InferSmemHeader) + 64;
+    return 2 * kABytes + kOnesBytes + p.blob_bytes + sizeof(InferSmemHeader) + 64;
 }
 
 cudaError_t launch_infer(int kind, const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out) {
@@ -843,11 +867,11 @@ cudaError_t launch_infer(int kind, const InferParams &p, int num_sms, cudaStream
         grid = 1;
     *grid_out = (uint32_t)grid;
     switch (kind) {
-    case kKindHeuristic: infer_kernel<kKindHeuristic><<<(uint32_t)grid, kTileM, smem, stream>>>(p); break;
-    case kKindAdrrs: infer_kernel<kKindAdrrs><<<(uint32_t)grid, kTileM, smem, stream>>>(p); break;
-    case kKindNrrs: infer_kernel<kKindNrrs><<<(uint32_t)grid, kTileM, smem, stream>>>(p); break;
-    case kKindAid: infer_kernel<kKindAid><<<(uint32_t)grid, kTileM, smem, stream>>>(p); break;
-    case kKindStats: infer_kernel<kKindStats><<<(uint32_t)grid, kTileM, smem, stream>>>(p); break;
+    case kKindHeuristic: infer_kernel<kKindHeuristic><<<(uint32_t)grid, kInferThreads, smem, stream>>>(p); break;
+    case kKindAdrrs: infer_kernel<kKindAdrrs><<<(uint32_t)grid, kInferThreads, smem, stream>>>(p); break;
+    case kKindNrrs: infer_kernel<kKindNrrs><<<(uint32_t)grid, kInferThreads, smem, stream>>>(p); break;
+    case kKindAid: infer_kernel<kKindAid><<<(uint32_t)grid, kInferThreads, smem, stream>>>(p); break;
+    case kKindStats: infer_kernel<kKindStats><<<(uint32_t)grid, kInferThreads, smem, stream>>>(p); break;
     default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
