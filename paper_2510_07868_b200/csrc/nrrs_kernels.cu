@@ -125,7 +125,27 @@ __device__ __forceinline__ void run_mlp(const uint8_t *smem_w, const NetDesc &ne
     tmem_ld16(tmem_row, y);  // both halves load (lane-aligned), half 0 uses it
 }
 
+// Two corners of one cell edge: e0 and e1 are entry indices.  The aligned
+// 16-byte pair holding e0 is always loaded; it also holds e1 whenever
+// e1 == e0 ^ 1 (x-adjacent corners with even x on hashed levels, z-adjacent
+// corners with even base on dense levels), otherwise e1 is fetched alone.
+__device__ __forceinline__ void gather_edge(const float2 *__restrict__ lvl, uint32_t e0, uint32_t e1, float w0,
+                                            float w1, float &a0, float &a1) {
+    const float4 pr = __ldg(reinterpret_cast<const float4 *>(lvl) + (e0 >> 1));
+    const bool odd = e0 & 1u;
+    const float v0x = odd ? pr.z : pr.x, v0y = odd ? pr.w : pr.y;
+    float v1x = odd ? pr.x : pr.z, v1y = odd ? pr.y : pr.w;
+    if (e1 != (e0 ^ 1u)) {
+        const float2 v = __ldg(lvl + e1);
+        v1x = v.x;
+        v1y = v.y;
+    }
+    a0 += w0 * v0x + w1 * v1x;
+    a1 += w0 * v0y + w1 * v1y;
+}
+
 // HashGrid::encode (hashgrid.cpp:38-82) for levels [l0, l0+4) of one point, F = 2.
+// Trilinear weight of corner (ox,oy,oz) = wx*wy*wz; entries summed per edge.
 __device__ __forceinline__ void grid_encode4(const float2 *__restrict__ theta, const GridDev &g, int l0,
                                              float cpx, float cpy, float cpz, float *out) {
 #pragma unroll
@@ -143,32 +163,31 @@ __device__ __forceinline__ void grid_encode4(const float2 *__restrict__ theta, c
         const uint32_t cy = min((uint32_t)fy, res - 1u);
         const uint32_t cz = min((uint32_t)fz, res - 1u);
         const float tx = fx - (float)cx, ty = fy - (float)cy, tz = fz - (float)cz;
+        const float wx[2] = {1.0f - tx, tx}, wy[2] = {1.0f - ty, ty}, wz[2] = {1.0f - tz, tz};
         const float2 *lvl = theta + (size_t)l * g.table_size;
-        uint32_t idx[8];
+        float a0 = 0.0f, a1 = 0.0f;
         if ((g.dense_mask >> l) & 1u) {
+            // dense index (x*n + y)*n + z: edges along z
             const uint32_t nn = res + 1u;
 #pragma unroll
-            for (int c = 0; c < 8; ++c)
-                idx[c] = ((cx + (c & 1)) * nn + cy + ((c >> 1) & 1)) * nn + cz + ((c >> 2) & 1);
+            for (int e = 0; e < 4; ++e) {
+                const uint32_t ox = e & 1, oy = e >> 1;
+                const uint32_t e0 = ((cx + ox) * nn + cy + oy) * nn + cz;
+                const float wxy = wx[ox] * wy[oy];
+                gather_edge(lvl, e0, e0 + 1u, wxy * wz[0], wxy * wz[1], a0, a1);
+            }
         } else {
-            const uint32_t y0 = cy * 2654435761u, y1 = (cy + 1u) * 2654435761u;
-            const uint32_t z0 = cz * 805459861u, z1 = (cz + 1u) * 805459861u;
+            // hashed index x ^ y*PY ^ z*PZ: edges along x
+            const uint32_t yp[2] = {cy * 2654435761u, (cy + 1u) * 2654435761u};
+            const uint32_t zp[2] = {cz * 805459861u, (cz + 1u) * 805459861u};
             const uint32_t m = g.table_size - 1u;
 #pragma unroll
-            for (int c = 0; c < 8; ++c)
-                idx[c] = ((cx + (c & 1)) ^ ((c & 2) ? y1 : y0) ^ ((c & 4) ? z1 : z0)) & m;
-        }
-        float2 v[8];
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-            v[c] = __ldg(lvl + idx[c]);
-        const float wx0 = 1.0f - tx, wy0 = 1.0f - ty, wz0 = 1.0f - tz;
-        float a0 = 0.0f, a1 = 0.0f;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-            const float w = ((c & 1) ? tx : wx0) * ((c & 2) ? ty : wy0) * ((c & 4) ? tz : wz0);
-            a0 += w * v[c].x;
-            a1 += w * v[c].y;
+            for (int e = 0; e < 4; ++e) {
+                const uint32_t oy = e & 1, oz = e >> 1;
+                const uint32_t k = yp[oy] ^ zp[oz];
+                const float wyz = wy[oy] * wz[oz];
+                gather_edge(lvl, (cx ^ k) & m, ((cx + 1u) ^ k) & m, wx[0] * wyz, wx[1] * wyz, a0, a1);
+            }
         }
         out[2 * i] = a0;
         out[2 * i + 1] = a1;
