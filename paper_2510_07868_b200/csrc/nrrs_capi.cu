@@ -364,10 +364,14 @@ int nrrs_gpu_set_weights(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w) {
                     (unsigned long long)w->rrs_mlp_len, mlp_param_count(rrs_in, 1));
 
     CK(ctx, cudaSetDevice(ctx->device));
-    // layer-0 column maps: grid features -> [0, 2L), tail -> [16, 32)
+    // layer-0 column map (kernel K layout): half h of a tile row owns K columns
+    // [16h, 16h+16) = grid features [8h, 8h+8) then tail entries [8h, 8h+8).
     std::vector<int> grid_map(stat_in);
-    for (int c = 0; c < stat_in; ++c)
-        grid_map[c] = c < gd ? c : 16 + (c - gd);
+    for (int c = 0; c < stat_in; ++c) {
+        const int f = c < gd ? c : c - gd;  // grid feature index or tail index
+        const int base = c < gd ? 0 : 8;
+        grid_map[c] = (f < 8 ? 0 : 16) + base + (f & 7);
+    }
     std::vector<int> id11(11);
     for (int c = 0; c < 11; ++c)
         id11[c] = c;

@@ -31,11 +31,8 @@ namespace nrrs {
 // ===========================================================================
 constexpr int kTileM = 128;           // vertices per MMA tile (UMMA M)
 constexpr int kInferThreads = 256;    // 2 threads per tile row
-constexpr int kAChunkStride = 128;    // bytes between 16-byte K chunks (LBO)
-constexpr int kASbo = 512;            // bytes between 8-row groups (K = 32 -> 4 chunks)
-constexpr int kABytes = kTileM * 32 * 2;
-constexpr int kOnesSbo = 256;         // ones slice: K = 16 -> 2 chunks per 8-row group
-constexpr int kOnesBytes = kTileM * 16 * 2;
+constexpr uint32_t kTmemCols = 128;   // per CTA: D [0,32) A_hi [32,48) A_lo [48,64) ones [64,72)
+constexpr uint32_t kColD = 0, kColAHi = 32, kColALo = 48, kColOnes = 64;
 
 struct InferSmemHeader {
     uint64_t mbar;
@@ -56,46 +53,42 @@ __device__ __forceinline__ void split2(float v0, float v1, uint32_t &h, uint32_t
     l = *reinterpret_cast<const uint32_t *>(&ll);
 }
 
-// 8 fp32 values -> chunk `c` (K columns 8c..8c+7) of row `row` in the K-major
-// canonical hi / lo A tiles.
-__device__ __forceinline__ void write_a_chunk(uint8_t *a_hi, uint8_t *a_lo, int row, int c, const float *x) {
-    const int off = (row >> 3) * kASbo + c * kAChunkStride + (row & 7) * 16;
-    uint32_t h[4], l[4];
+// 16 fp32 values -> K columns [16*slot, 16*slot+16) of this thread's row of the
+// A operand in TMEM (hi and lo tiles; 8 packed fp16x2 columns each).
+__device__ __forceinline__ void write_a_tmem(uint32_t tmem_row, int slot, const float *x) {
+    uint32_t h[8], l[8];
 #pragma unroll
-    for (int e = 0; e < 4; ++e)
+    for (int e = 0; e < 8; ++e)
         split2(x[2 * e], x[2 * e + 1], h[e], l[e]);
-    *reinterpret_cast<uint4 *>(a_hi + off) = make_uint4(h[0], h[1], h[2], h[3]);
-    *reinterpret_cast<uint4 *>(a_lo + off) = make_uint4(l[0], l[1], l[2], l[3]);
+    tmem_st8(tmem_row + kColAHi + 8u * (uint32_t)slot, h);
+    tmem_st8(tmem_row + kColALo + 8u * (uint32_t)slot, l);
 }
 
 // Barrier + one MMA layer + wait for the accumulator.  3-term split
-// (hi*Whi + lo*Whi + hi*Wlo) on data slices; the shared constant-ones slice
-// carries the bias column (1*bias_hi + 1*bias_lo).
-__device__ __forceinline__ void mma_layer(const uint8_t *smem_w, const LayerDesc &L, const uint8_t *a_hi,
-                                          const uint8_t *a_lo, const uint8_t *ones, uint32_t tmem_d,
+// (hi*Whi + lo*Whi + hi*Wlo) on data slices, A from TMEM; the constant-ones
+// slice carries the bias column (1*bias_hi + 1*bias_lo).
+__device__ __forceinline__ void mma_layer(const uint8_t *smem_w, const LayerDesc &L, uint32_t tmem_base,
                                           uint64_t *bar, uint32_t &phase) {
-    fence_proxy_async_smem();
+    tmem_wait_st();
     tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0) {
         tc_fence_after();
         const uint32_t idesc = make_idesc_f16(L.N);
-        const uint32_t a_hi_s = smem_u32(a_hi), a_lo_s = smem_u32(a_lo);
         const uint32_t w_hi_s = smem_u32(smem_w + L.w_hi), w_lo_s = smem_u32(smem_w + L.w_lo);
         const uint32_t w_sbo = (uint32_t)L.K * 16u;
+        const uint32_t d = tmem_base + kColD;
         for (uint32_t s = 0; s < (uint32_t)L.K / 16u; ++s) {
-            const uint64_t wh = make_smem_desc(w_hi_s + s * 256u, kAChunkStride, w_sbo);
-            const uint64_t wl = make_smem_desc(w_lo_s + s * 256u, kAChunkStride, w_sbo);
+            const uint64_t wh = make_smem_desc(w_hi_s + s * 256u, 128u, w_sbo);
+            const uint64_t wl = make_smem_desc(w_lo_s + s * 256u, 128u, w_sbo);
             if (s == L.ones_slice) {
-                const uint64_t o = make_smem_desc(smem_u32(ones), kAChunkStride, kOnesSbo);
-                mma_f16(tmem_d, o, wh, idesc, 1u);
-                mma_f16(tmem_d, o, wl, idesc, 1u);
+                mma_f16_ts(d, tmem_base + kColOnes, wh, idesc, 1u);
+                mma_f16_ts(d, tmem_base + kColOnes, wl, idesc, 1u);
             } else {
-                const uint64_t ah = make_smem_desc(a_hi_s + s * 256u, kAChunkStride, kASbo);
-                const uint64_t al = make_smem_desc(a_lo_s + s * 256u, kAChunkStride, kASbo);
-                mma_f16(tmem_d, ah, wh, idesc, s > 0 ? 1u : 0u);
-                mma_f16(tmem_d, al, wh, idesc, 1u);
-                mma_f16(tmem_d, ah, wl, idesc, 1u);
+                const uint32_t ah = tmem_base + kColAHi + 8u * s, al = tmem_base + kColALo + 8u * s;
+                mma_f16_ts(d, ah, wh, idesc, s > 0 ? 1u : 0u);
+                mma_f16_ts(d, al, wh, idesc, 1u);
+                mma_f16_ts(d, ah, wl, idesc, 1u);
             }
         }
         mma_commit(bar);
@@ -105,24 +98,23 @@ __device__ __forceinline__ void mma_layer(const uint8_t *smem_w, const LayerDesc
     tc_fence_after();
 }
 
-// 3-hidden-layer MLP (mlp.cpp:52-72); the layer-0 input must be in a_hi/a_lo.
-// Head outputs (columns 0..15, bias included) land in y on half-0 threads.
-__device__ __forceinline__ void run_mlp(const uint8_t *smem_w, const NetDesc &net, uint8_t *a_hi, uint8_t *a_lo,
-                                        const uint8_t *ones, uint32_t tmem_base, uint32_t tmem_row, int row,
-                                        int half, uint64_t *bar, uint32_t &phase, float (&y)[16]) {
+// 3-hidden-layer MLP (mlp.cpp:52-72); the layer-0 input must be in TMEM A.
+// Head outputs (columns 0..15, bias included) land in y (valid on half 0).
+__device__ __forceinline__ void run_mlp(const uint8_t *smem_w, const NetDesc &net, uint32_t tmem_base,
+                                        uint32_t tmem_row, int half, uint64_t *bar, uint32_t &phase,
+                                        float (&y)[16]) {
 #pragma unroll 1
     for (int l = 0; l < 3; ++l) {
-        mma_layer(smem_w, net.layer[l], a_hi, a_lo, ones, tmem_base, bar, phase);
+        mma_layer(smem_w, net.layer[l], tmem_base, bar, phase);
         float acc[16];
-        tmem_ld16(tmem_row + 16u * (uint32_t)half, acc);
+        tmem_ld16(tmem_row + kColD + 16u * (uint32_t)half, acc);
 #pragma unroll
         for (int i = 0; i < 16; ++i)
             acc[i] = fmaxf(acc[i], acc[i] * 0.01f);  // leaky ReLU = cwiseMax(z, slope z)
-        write_a_chunk(a_hi, a_lo, row, 2 * half, acc);
-        write_a_chunk(a_hi, a_lo, row, 2 * half + 1, acc + 8);
+        write_a_tmem(tmem_row, half, acc);
     }
-    mma_layer(smem_w, net.layer[3], a_hi, a_lo, ones, tmem_base, bar, phase);
-    tmem_ld16(tmem_row, y);  // both halves load (lane-aligned), half 0 uses it
+    mma_layer(smem_w, net.layer[3], tmem_base, bar, phase);
+    tmem_ld16(tmem_row + kColD, y);  // both halves load (warp-aligned); half 0 uses it
 }
 
 // Two corners of one cell edge: e0 and e1 are entry indices.  The aligned
@@ -217,10 +209,7 @@ template <int KIND>
 __global__ void __launch_bounds__(kInferThreads, 3) infer_kernel(InferParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     constexpr bool kNeural = KIND != kKindHeuristic;
-    uint8_t *a_hi = smem_raw;
-    uint8_t *a_lo = smem_raw + kABytes;
-    uint8_t *ones = smem_raw + 2 * kABytes;
-    uint8_t *smem_w = smem_raw + 2 * kABytes + kOnesBytes;
+    uint8_t *smem_w = smem_raw;
     InferSmemHeader *hdr = reinterpret_cast<InferSmemHeader *>(kNeural ? smem_w + p.blob_bytes : smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int row = tid & (kTileM - 1), half = tid >> 7;
@@ -233,22 +222,22 @@ __global__ void __launch_bounds__(kInferThreads, 3) infer_kernel(InferParams p) 
         uint4 *dst = reinterpret_cast<uint4 *>(smem_w);
         for (uint32_t i = tid; i < p.blob_bytes / 16u; i += kInferThreads)
             dst[i] = __ldg(src + i);
-        // constant-ones K16 slice: column 0 = 1 (fp16), the rest 0
-        {
-            const int off = (row >> 3) * kOnesSbo + half * kAChunkStride + (row & 7) * 16;
-            *reinterpret_cast<uint4 *>(ones + off) = make_uint4(half == 0 ? 0x3C00u : 0u, 0u, 0u, 0u);
-        }
         if (tid == 0) {
             mbar_init(&hdr->mbar, 1);
             fence_barrier_init();
         }
         if (warp == 0)
-            tmem_alloc(&hdr->tmem_base, 32);
+            tmem_alloc(&hdr->tmem_base, kTmemCols);
         tc_fence_before();
         __syncthreads();
         tc_fence_after();
         tmem_base = hdr->tmem_base;
         tmem_row = tmem_base + ((uint32_t)((warp & 3) * 32) << 16);
+        // constant-ones K16 A slice in TMEM: k = 0 is 1.0 (fp16), the rest 0
+        if (half == 0) {
+            const uint32_t ones[8] = {0x00003C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+            tmem_st8(tmem_row + kColOnes, ones);
+        }
     }
 
     const uint64_t n = p.n;
@@ -293,9 +282,11 @@ __global__ void __launch_bounds__(kInferThreads, 3) infer_kernel(InferParams p) 
             const float rough = valid ? __ldg(p.roughness + j) : 0.0f;
             float y[16];
             {
-                // layer-0 input (networks.cpp:131-135 / :149-157); kernel K layout:
-                // grid features of levels 0..7 in [0,16), the 16-wide tail in [16,32).
-                float g8[8], t8[8];
+                // layer-0 input (networks.cpp:131-135 / :149-157); kernel K layout
+                // (host packs W columns to match): half h owns k in [16h, 16h+16) =
+                // grid features of levels 4h..4h+3, then tail[8h .. 8h+8).
+                float in16[16];
+                float *g8 = in16, *t8 = in16 + 8;
                 grid_encode4(KIND == kKindAid ? p.rrs_grid : p.stat_grid, p.grid, 4 * half, clamp01(px),
                              clamp01(py), clamp01(pz), g8);
                 if (half == 0) {
@@ -321,15 +312,13 @@ __global__ void __launch_bounds__(kInferThreads, 3) infer_kernel(InferParams p) 
                         t8[s] = 0.0f;
                     }
                 }
-                write_a_chunk(a_hi, a_lo, row, half, g8);
-                write_a_chunk(a_hi, a_lo, row, 2 + half, t8);
+                write_a_tmem(tmem_row, half, in16);
             }
             if (KIND == kKindAid) {
-                run_mlp(smem_w, p.nets.rrs, a_hi, a_lo, ones, tmem_base, tmem_row, row, half, &hdr->mbar, phase, y);
+                run_mlp(smem_w, p.nets.rrs, tmem_base, tmem_row, half, &hdr->mbar, phase, y);
                 q = softplus_mod(y[0]);
             } else {
-                run_mlp(smem_w, p.nets.stat, a_hi, a_lo, ones, tmem_base, tmem_row, row, half, &hdr->mbar, phase,
-                        y);
+                run_mlp(smem_w, p.nets.stat, tmem_base, tmem_row, half, &hdr->mbar, phase, y);
                 if (KIND == kKindStats) {
                     if (valid && half == 0) {
 #pragma unroll
@@ -365,11 +354,9 @@ __global__ void __launch_bounds__(kInferThreads, 3) infer_kernel(InferParams p) 
                             for (int c = 0; c < 11; ++c)
                                 xin[c] = 0.0f;
                         }
-                        write_a_chunk(a_hi, a_lo, row, 0, xin);
-                        write_a_chunk(a_hi, a_lo, row, 1, xin + 8);
+                        write_a_tmem(tmem_row, 0, xin);
                     }
-                    run_mlp(smem_w, p.nets.rrs, a_hi, a_lo, ones, tmem_base, tmem_row, row, half, &hdr->mbar,
-                            phase, y);
+                    run_mlp(smem_w, p.nets.rrs, tmem_base, tmem_row, half, &hdr->mbar, phase, y);
                     q = softplus_mod(y[0]);
                 }
             }
@@ -409,7 +396,7 @@ __global__ void __launch_bounds__(kInferThreads, 3) infer_kernel(InferParams p) 
         tc_fence_before();
         __syncthreads();
         if (warp == 0)
-            tmem_dealloc(hdr->tmem_base, 32);
+            tmem_dealloc(hdr->tmem_base, kTmemCols);
     }
     if constexpr (KIND == kKindStats)
         return;
@@ -853,6 +840,8 @@ static cudaError_t infer_occupancy(size_t smem, int *occ) {
     const int by_regs = 65536 / (regs > 0 ? regs : 1);
     const int by_smem = (228 * 1024) / (int)(smem + a.sharedSizeBytes + 1024);
     int o = by_regs < by_smem ? by_regs : by_smem;
+    if (KIND != kKindHeuristic && o > (int)(512u / kTmemCols))
+        o = (int)(512u / kTmemCols);  // TMEM columns per SM
     if (o > 8)
         o = 8;
     *occ = o < 1 ? 1 : o;
@@ -862,7 +851,7 @@ static cudaError_t infer_occupancy(size_t smem, int *occ) {
 size_t infer_smem_bytes(int kind, const InferParams &p) {
     if (kind == kKindHeuristic)
         return sizeof(InferSmemHeader) + 64;
-    return 2 * kABytes + kOnesBytes + p.blob_bytes + sizeof(InferSmemHeader) + 64;
+    return p.blob_bytes + sizeof(InferSmemHeader) + 64;
 }
 
 cudaError_t launch_infer(int kind, const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out) {
