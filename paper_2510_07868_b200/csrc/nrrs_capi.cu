@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -536,6 +537,8 @@ static int run_factors(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, 
     ip.counter = ctx->d_misc + 0;
     ip.sum_out = sum_out;
     ip.res = ctx->d_res;
+    if (const char *ab = std::getenv("NRRS_DEBUG_ABLATE"))  // diagnostics only; results invalid
+        ip.ablate = (uint32_t)std::atoi(ab);
     uint32_t grid = 0;
     CK(ctx, launch_infer(kind, ip, ctx->num_sms, ctx->stream, &grid));
     ctx->launches += 1;

@@ -80,6 +80,7 @@ struct InferParams {
     uint32_t *counter; // last-CTA-done counter (self-resetting)
     double *sum_out;   // local sum of q
     DevResult *res;
+    uint32_t ablate;   // debug only (env NRRS_DEBUG_ABLATE): bit0 skip grid gathers, bit1 skip MLP
 };
 
 struct DecideParams {

@@ -287,8 +287,14 @@ __global__ void __launch_bounds__(kInferThreads, 3) infer_kernel(InferParams p) 
                 // grid features of levels 4h..4h+3, then tail[8h .. 8h+8).
                 float in16[16];
                 float *g8 = in16, *t8 = in16 + 8;
-                grid_encode4(KIND == kKindAid ? p.rrs_grid : p.stat_grid, p.grid, 4 * half, clamp01(px),
-                             clamp01(py), clamp01(pz), g8);
+                if (p.ablate & 1u) {
+#pragma unroll
+                    for (int s = 0; s < 8; ++s)
+                        g8[s] = px * (float)(s + 1) + py;
+                } else {
+                    grid_encode4(KIND == kKindAid ? p.rrs_grid : p.stat_grid, p.grid, 4 * half, clamp01(px),
+                                 clamp01(py), clamp01(pz), g8);
+                }
                 if (half == 0) {
                     const float wox = valid ? __ldg(p.wo01 + 2 * j) : 0.0f;
                     const float woy = valid ? __ldg(p.wo01 + 2 * j + 1) : 0.0f;
@@ -313,8 +319,15 @@ __global__ void __launch_bounds__(kInferThreads, 3) infer_kernel(InferParams p) 
                     }
                 }
                 write_a_tmem(tmem_row, half, in16);
+                if (p.ablate & 2u) {
+#pragma unroll
+                    for (int s = 0; s < 16; ++s)
+                        y[s] = in16[s];
+                }
             }
-            if (KIND == kKindAid) {
+            if (p.ablate & 2u) {
+                q = softplus_mod(y[0] + y[5] + y[11]);
+            } else if (KIND == kKindAid) {
                 run_mlp(smem_w, p.nets.rrs, tmem_base, tmem_row, half, &hdr->mbar, phase, y);
                 q = softplus_mod(y[0]);
             } else {
