@@ -41,8 +41,8 @@ def oracle_decide(q_orig: np.ndarray, u: np.ndarray, n_pixels: int, capacity: in
     q_real = (q * np.float32(gain)).astype(np.float32)
     k = np.zeros(q.size, np.int32)
     err = C.c_int(0)
-    total = orc.lib().orc_realize_counts(orc.ptr(q_real), orc.ptr(np.ascontiguousarray(u, np.float32)),
-                                         orc.ptr(k), q.size, C.byref(err))
+    u = np.ascontiguousarray(u, np.float32)
+    total = orc.lib().orc_realize_counts(orc.ptr(q_real), orc.ptr(u), orc.ptr(k), q.size, C.byref(err))
     assert err.value == 0
     off, spawned, dropped = orc.plan_spawns(k, capacity)
     rem = spawned - np.minimum(spawned, off.astype(np.int64))

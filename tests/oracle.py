@@ -187,8 +187,9 @@ def plan_spawns(counts: np.ndarray, capacity: int):
 
 def compact_slots(slots: np.ndarray, used: np.ndarray, count: int) -> np.ndarray:
     out = np.zeros((max(count, 1), 2), np.uint32)
-    w = lib().orc_compact_slots(ptr(np.ascontiguousarray(slots, np.uint32)), ptr(np.ascontiguousarray(used, np.uint8)),
-                                count, ptr(out))
+    slots = np.ascontiguousarray(slots, np.uint32)
+    used = np.ascontiguousarray(used, np.uint8)
+    w = lib().orc_compact_slots(ptr(slots), ptr(used), count, ptr(out))
     return out[:w]
 
 

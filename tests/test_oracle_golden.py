@@ -1,0 +1,278 @@
+"""CPU: pin the oracle against the reference's own known answers.
+
+* tests/golden/rng_kat.json -- produced by the reference's rng.hpp compiled verbatim
+  (oracle/ref_rng_kat.cpp, tests/golden/make_rng_kat.py);
+* tests/golden/reference_kats.json -- values transcribed from the reference's tests
+  (each entry cites proj/tests/<file>:<line>).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import math
+import pathlib
+
+import numpy as np
+import pytest
+
+import oracle as orc
+
+GOLDEN = pathlib.Path(__file__).parent / "golden"
+KATS = json.loads((GOLDEN / "reference_kats.json").read_text())
+RNG = json.loads((GOLDEN / "rng_kat.json").read_text())
+L = orc.lib()
+
+
+def _val(x):
+    if isinstance(x, str):
+        return {"nan": math.nan, "inf": math.inf, "log(2)": math.log(2), "log1p(exp(-1))": math.log1p(math.exp(-1)),
+                "2+log(2)": 2 + math.log(2), "1-exp(-1)": 1 - math.exp(-1), "1-exp(-2)": 1 - math.exp(-2),
+                "2*(sqrt(3)-1)": 2 * (math.sqrt(3) - 1), "exp(-1.25)": math.exp(-1.25),
+                "exp(-125)": math.exp(-125)}[x]
+    return x
+
+
+def f3(v):
+    return np.asarray(v, np.float32)
+
+
+# ---------------------------------------------------------------- RNG ------
+def test_rng_matches_reference_rng_hpp():
+    for p in RNG["pixels"]:
+        key = L.orc_root_path_key(p["pixel"], p["frame"])
+        assert f"{key:016x}" == p["key"]
+        assert np.float32(L.orc_rrs_uniform(0, key, 1)) == np.float32(p["u_seed0_d1"])
+        assert np.float32(L.orc_rrs_uniform(7, key, 2)) == np.float32(p["u_seed7_d2"])
+        assert np.float32(L.orc_rrs_uniform(0x9E3779B97F4A7C15, key, 5)) == np.float32(p["u_seedphi_d5"])
+        assert f"{L.orc_child_path_key(key, 0):016x}" == p["child0"]
+        assert f"{L.orc_child_path_key(key, 3):016x}" == p["child3"]
+    for s in RNG["streams"]:
+        r = (C.c_uint64 * 2)()
+        L.orc_rng_init(r, s["seed"], s["seq"])
+        assert [L.orc_rng_next_u32(r) for _ in range(16)] == s["u32"]
+    assert [f"{L.orc_mix_bits(x * 0x1234567):016x}" for x in range(8)] == RNG["mix_bits"]
+    r = (C.c_uint64 * 2)()
+    L.orc_rng_init(r, 3, 3)
+    assert L.orc_rng_next_u32(r) == KATS["rng_appendix_a"]["rng_3_3_first_u32"]
+
+
+def test_product_host_rng_matches_reference():
+    """The C ABI's host RNG (used to reproduce NeuralRrs initializers) == rng.hpp."""
+    from paper_2510_07868_b200 import _capi
+    lib = _capi.lib()
+    for p in RNG["pixels"][:16]:
+        key = lib.nrrs_root_path_key(p["pixel"], p["frame"])
+        assert f"{key:016x}" == p["key"]
+        assert f"{lib.nrrs_child_path_key(key, 3):016x}" == p["child3"]
+    from paper_2510_07868_b200.networks import rng_uniform
+    for s in RNG["streams"]:
+        u = rng_uniform(s["seed"], s["seq"], 16)
+        np.testing.assert_array_equal(u, (np.array(s["u32"], np.uint32) >> 8).astype(np.float32) * np.float32(2 ** -24))
+
+
+# ------------------------------------------------------- rrs core KATs ------
+def test_normalize_factors_kats():
+    for case in KATS["normalize_factors"]:
+        q = f3(case["q"]).copy()
+        assert orc.normalize_factors(q, case["n_pixels"]) == pytest.approx(case["f_norm"])
+        np.testing.assert_allclose(q, case["q_out"], rtol=1e-6)
+    for case in KATS["normalize_factors_throws"]:
+        q = f3([_val(x) for x in case["q"]]).copy()
+        with pytest.raises(RuntimeError):
+            orc.normalize_factors(q, case["n_pixels"])
+
+
+def test_normalize_budget_properties():
+    b = KATS["normalize_budget"]
+    r = (C.c_uint64 * 2)()
+    L.orc_rng_init(r, b["rng_seed"], b["rng_seq"])
+    q = np.array([L.orc_rng_next_float(r) * np.float32(b["scale"]) for _ in range(b["n"])], np.float32)
+    orc.normalize_factors(q, b["n_pixels"])
+    assert abs(q.astype(np.float64).sum() - b["n_pixels"]) / b["n_pixels"] < b["rel_tol"]
+    s = KATS["selftest_budget"]
+    q = np.empty(s["n"], np.float32)
+    for i in range(s["n"]):
+        L.orc_rng_init(r, s["rng_seed"], i)
+        q[i] = L.orc_rng_next_float(r) * np.float32(s["scale"])
+    orc.normalize_factors(q, s["n"])
+    assert abs(float(np.sum(q, dtype=np.float64)) - s["n"]) < s["abs_tol"]
+
+
+def test_uniform_factor_3_is_exactly_one():
+    k = KATS["uniform_factor_3"]
+    q = np.full(k["n"], k["q"], np.float32)
+    orc.normalize_factors(q, k["n"])
+    assert np.all(q == np.float32(k["q_norm"]))
+
+
+def test_realize_and_stochastic_round_kats():
+    for case in KATS["realize_counts"]:
+        q, u = f3(case["q"]), f3(case["u"])
+        k = np.zeros(q.size, np.int32)
+        err = C.c_int(0)
+        tot = L.orc_realize_counts(orc.ptr(q), orc.ptr(u), orc.ptr(k), q.size, C.byref(err))
+        assert err.value == 0 and tot == case["total"] and k.tolist() == case["counts"]
+    for case in KATS["stochastic_round"]:
+        assert L.orc_stochastic_round(case["q"], case["u"]) == case["k"], case["cite"]
+    for x in KATS["stochastic_round_throws"][0]["q"]:
+        assert L.orc_stochastic_round(_val(x), 0.5) == -1
+
+
+def test_rate_control_and_bernstein():
+    from paper_2510_07868_b200 import RateControl, bernstein_bound
+    k = KATS["rate_control"]
+    rc = RateControl()
+    assert rc.gain() == pytest.approx(k["gain0"])
+    for alpha in k["alpha_after"]:
+        rc.note_overflow()
+        assert rc.alpha == pytest.approx(alpha)
+    assert rc.overflow_events == 2
+    rc.enabled = False
+    assert rc.gain() == k["disabled_gain"]
+    for f, n, expect in KATS["bernstein"]["cases"]:
+        assert bernstein_bound(f, n) == pytest.approx(_val(expect), rel=1e-6)
+        assert L.orc_bernstein_bound(f, n) == pytest.approx(_val(expect), rel=1e-6)
+    assert bernstein_bound(0.7, 1000) < bernstein_bound(0.9, 1000)
+
+
+def test_queue_capacity_and_plan_spawns():
+    from paper_2510_07868_b200 import queue_capacity_for
+    for npx, cap in KATS["queue_capacity_for"]["cases"]:
+        assert L.orc_queue_capacity_for(npx) == cap
+        assert queue_capacity_for(npx) == cap
+    for case in KATS["plan_spawns"]:
+        off, sp, dr = orc.plan_spawns(np.array(case["counts"], np.int32), case["capacity"])
+        assert off.tolist() == case["offset"] and sp == case["spawned"] and dr == case["dropped"]
+    with pytest.raises(RuntimeError):
+        orc.plan_spawns(np.array([1, -1], np.int32), 4)
+
+
+# ------------------------------------------------------------ encodings -----
+def test_encoding_kats():
+    for x, y in KATS["box_cox"]["cases"]:
+        assert L.orc_box_cox(x) == pytest.approx(y)
+    before = L.orc_box_cox_clamps()
+    L.orc_box_cox(-1.0)
+    assert L.orc_box_cox_clamps() == before + 1
+    for x, y in KATS["softplus_mod"]["cases"]:
+        assert L.orc_softplus_mod(x) == pytest.approx(_val(y), rel=1e-6)
+    assert L.orc_softplus_mod(L.orc_softplus_mod_inverse_pos(1.0)) == pytest.approx(1.0)
+    for x, y in KATS["roughness_remap"]["cases"]:
+        assert L.orc_roughness_remap(x) == pytest.approx(_val(y), abs=1e-7)
+    out = np.zeros(8, np.float32)
+    for bins in (4, 8):
+        for x in (0.0, 0.1, 0.5, 0.93, 1.0):
+            L.orc_one_blob(x, bins, orc.ptr(out))
+            assert float(out[:bins].sum()) == pytest.approx(1.0, rel=1e-5)
+
+
+def test_input_builder_kats():
+    k = KATS["build_nrrs_input"]
+    out = np.zeros(11, np.float32)
+    keep = [f3(k["mean"]), f3(k["m2"]), f3(k["t_x"]), f3(k["i_pixel"])]
+    L.orc_build_nrrs_input(*(orc.ptr(a) for a in keep), k["roughness"], orc.ptr(out))
+    np.testing.assert_allclose(out, [_val(x) for x in k["expected"]], rtol=k["rel_tol"], atol=1e-7)
+    k = KATS["build_aid_tail"]
+    tail = np.zeros(16, np.float32)
+    keep = [f3(k["wo01"]), f3(k["t_x"]), f3(k["i_pixel"])]
+    L.orc_build_aid_tail(*(orc.ptr(a) for a in keep), k["roughness"], orc.ptr(tail))
+    np.testing.assert_allclose(tail[8:12], [_val(x) for x in k["expected_8_11"]], rtol=1e-5)
+    for s, n in k["blob_sums"]:
+        assert float(tail[s:s + n].sum()) == pytest.approx(1.0, rel=1e-5)
+    k = KATS["build_stat_tail"]
+    wo = f3(k["wo01"])
+    L.orc_build_stat_tail(orc.ptr(wo), k["roughness"], orc.ptr(tail))
+    for s, n in k["blob_sums"]:
+        assert float(tail[s:s + n].sum()) == pytest.approx(1.0, rel=1e-5)
+
+
+def test_heuristic_factor_kats():
+    z3, z2, o3 = f3([0, 0, 0]), f3([0, 0]), f3([1, 1, 1])
+    for w, expect in KATS["throughput_factor"]["cases"]:
+        wa = f3(w)
+        q = L.orc_strategy_factor(orc.THROUGHPUT, 1.0, None, orc.ptr(wa), orc.ptr(z3), orc.ptr(z2), 0.3,
+                                  orc.ptr(o3), 0.0)
+        assert q == pytest.approx(expect)
+    k = KATS["adrrs_factor"]
+    ip = f3(k["i_pixel"])
+    for w, lo, eps, expect in k["cases"]:
+        wa, la = f3(w), f3(lo)
+        assert L.orc_adrrs_factor(orc.ptr(wa), orc.ptr(la), orc.ptr(ip), eps) == pytest.approx(expect, rel=1e-4)
+    assert math.isfinite(L.orc_adrrs_factor(orc.ptr(o3), orc.ptr(o3), orc.ptr(z3), 1e-4))
+
+
+def test_strategy_factor_kats_fresh_nets():
+    """test_engine.cpp:567-618 with NeuralRrsConfig{seed=4} (default grid)."""
+    k = KATS["strategy_factor"]
+    keep = [f3(k["w"]), f3(k["p01"]), f3(k["wo01"]), f3(k["i_pixel"])]
+    args = (orc.ptr(keep[0]), orc.ptr(keep[1]), orc.ptr(keep[2]), k["roughness"], orc.ptr(keep[3]), k["eps_div"])
+    assert L.orc_strategy_factor(orc.FIXED, 2.5, None, *args) == k["fixed_2_5"]
+    assert L.orc_strategy_factor(orc.THROUGHPUT, 1.0, None, *args) == pytest.approx(k["throughput"])
+    for variant, kind, key in ((orc.VARIANT_NRRS, orc.NRRS, "fresh_nrrs"), (orc.VARIANT_AID, orc.AID_NRRS, "fresh_aid")):
+        nets = orc.OracleNets(variant, seed=k["net_seed"], randomize=False)
+        assert L.orc_strategy_factor(kind, 1.0, C.byref(nets.c), *args) == pytest.approx(k[key], rel=k["tol"])
+        assert L.orc_strategy_factor(orc.ADRRS_NN, 1.0, C.byref(nets.c), *args) == pytest.approx(k["fresh_adrrs_nn"])
+
+
+def test_fresh_nets_tiny_grid_unit_factor():
+    """test_networks.cpp:671-685 (tiny grid: 3 levels, base 4, T = 2^10, seed 31)."""
+    for variant in (orc.VARIANT_NRRS, orc.VARIANT_AID):
+        nets = orc.OracleNets(variant, levels=3, base=4, log2t=10, seed=31, randomize=False)
+        v = orc.gen_vertices(50)
+        np.testing.assert_allclose(orc.predict_q(nets, v), 1.0, rtol=1e-5)
+        assert np.all(orc.predict_stats(nets, v) == 0.0)
+
+
+def test_hash_grid_constant_features_and_continuity():
+    """test_networks.cpp:305-350 (2 dense levels, base 4, T = 2^12)."""
+    spec = orc.GridSpec(2, 2, 4, 12)
+    n = L.orc_grid_param_count(C.byref(spec))
+    theta = np.empty(n, np.float32)
+    stride = (1 << 12) * 2
+    theta[:stride] = 1.0
+    theta[stride:] = -0.5
+    out = np.zeros(4, np.float32)
+    rng = np.random.default_rng(11)
+    for _ in range(16):
+        p = rng.random(3).astype(np.float32)
+        L.orc_grid_encode(C.byref(spec), orc.ptr(theta), orc.ptr(p), orc.ptr(out))
+        np.testing.assert_allclose(out, [1, 1, -0.5, -0.5], rtol=1e-5)
+    theta = (rng.uniform(-1e-4, 1e-4, n) * 1e4).astype(np.float32)
+    o2 = np.zeros(4, np.float32)
+    for _ in range(50):
+        p = rng.random(3).astype(np.float32)
+        p2 = (p + np.float32(1e-6)).astype(np.float32)
+        L.orc_grid_encode(C.byref(spec), orc.ptr(theta), orc.ptr(p), orc.ptr(out))
+        L.orc_grid_encode(C.byref(spec), orc.ptr(theta), orc.ptr(p2), orc.ptr(o2))
+        assert np.max(np.abs(out - o2)) < 1e-4
+
+
+def test_stage_expected_count_equals_budget():
+    """ACCEPT-02 / test_rrs.cpp:89-111 in miniature: E[S] = Npx after normalization (4 sigma)."""
+    npx, trials = 1000, 200
+    totals, var_bound = [], 0.0
+    for t in range(trials):
+        v = orc.gen_vertices(npx, frame=t)
+        q = orc.split_bound_factors(npx)
+        rng = np.random.default_rng(t)
+        q = (q * np.float32(0.5) + rng.random(npx).astype(np.float32) * np.float32(1.5)).astype(np.float32)
+        f = orc.normalize_factors(q, npx)
+        assert f < 1.0
+        frac = q - np.floor(q)
+        var_bound += float(np.sum(frac * (1 - frac)))
+        u = np.array([L.orc_rrs_uniform(t, int(k), 2) for k in v["path_key"]], np.float32)
+        k = np.zeros(npx, np.int32)
+        err = C.c_int(0)
+        totals.append(L.orc_realize_counts(orc.ptr(q), orc.ptr(u), orc.ptr(k), npx, C.byref(err)))
+    se = math.sqrt(var_bound / trials / trials)
+    assert abs(np.mean(totals) - npx) <= 4 * se
+
+
+def test_oracle_stage_threads_invariant():
+    """test_engine.cpp:461-502: identical decisions for 1 vs 4 factor threads."""
+    nets = orc.OracleNets(orc.VARIANT_AID, levels=3, base=4, log2t=10, seed=5, randomize=True)
+    v = orc.gen_vertices(3000)
+    a = orc.rrs_stage(v, 2, 3000, 3375, orc.AID_NRRS, nets, threads=1)
+    b = orc.rrs_stage(v, 2, 3000, 3375, orc.AID_NRRS, nets, threads=4)
+    for key in ("q_orig", "q_norm", "q_real", "u", "k", "offset", "slots"):
+        np.testing.assert_array_equal(a[key], b[key])
