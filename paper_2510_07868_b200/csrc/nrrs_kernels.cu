@@ -488,6 +488,439 @@ __global__ void __launch_bounds__(kInferThreads, 3) infer_kernel(InferParams p) 
 }
 
 // ===========================================================================
+// K-A (neural kinds): warp-specialized persistent pipeline, 1 CTA per SM.
+//
+//  encoder group e (8 warps, 2 threads per tile row, half h):
+//     inputs -> hash-grid levels [4h,4h+4) + tail[8h,8h+8) -> tcgen05.st into
+//     TMEM A-slot s (hi | lo) + per-row sidecar (path key, flags, extras) in
+//     smem -> arrive full[s]
+//  MLP group g (4 warps, 1 thread per tile row, own D / A_hid / MMA mbarrier):
+//     wait full[s] -> layer chain (A from TMEM, weights in smem, 3-term split,
+//     bias via the ones slice) -> q / outputs -> arrive empty[s]
+//  Tiles are taken in order: encoder e owns local tiles i = e (mod GE), MLP
+//  group g owns i = g (mod GM), slot s = i mod S.  Gathers of tile i+1.. run
+//  while MLP groups chain tiles i, i-1.
+// ===========================================================================
+namespace ws {
+
+struct Side {        // 32 B per tile row
+    uint64_t key;
+    uint32_t flags;  // bit0 valid, bit1 active
+    float ex[5];     // NRRS: bc(t_x)x3, bc(mean I), remap(r); ADRRS: w x3, lum(I)
+};
+
+template <int GE, int GM>
+struct Cfg {
+    static constexpr int kEncThreads = GE * 256;
+    static constexpr int kMlpThreads = GM * 128;
+    static constexpr int kThreads = kEncThreads + kMlpThreads;
+    static constexpr uint32_t kColOnes = 0;                 // K16 ones slice [0, 8)
+    static constexpr uint32_t kColMlp = 32;                 // group g: D [32+64g, +32), A_hid [+32, +64)
+    static constexpr uint32_t kColSlots = 32 + 64 * GM;     // slot s: hi [c, c+16), lo [c+16, c+32)
+    static constexpr int kSlotsRaw = (512 - (int)kColSlots) / 32;
+    static constexpr int kSlots = kSlotsRaw > 8 ? 8 : kSlotsRaw;
+    static_assert(kSlots >= GE + GM, "TMEM slot ring too small");
+};
+
+struct SmemTail {
+    uint64_t full[8];
+    uint64_t empty[8];
+    uint64_t mma_bar[4];
+    uint32_t tmem_base;
+    uint32_t is_last;
+    double red_sum[32];
+    uint32_t red_nf[32];
+    uint32_t red_bc[32];
+};
+
+// One MMA layer for an MLP group: named barrier (all 128 epilogue threads done
+// with TMEM), elected issue, commit, wait.
+__device__ __forceinline__ void ws_mma(const uint8_t *smem_w, const LayerDesc &L, uint32_t tmem_base,
+                                       uint32_t col_ones, uint32_t col_a_hi, uint32_t col_a_lo, uint32_t col_d,
+                                       uint64_t *bar, uint32_t &phase, uint32_t bar_id, bool issuer) {
+    tc_fence_before();
+    named_bar_sync(bar_id, 128);
+    if (issuer) {
+        tc_fence_after();
+        const uint32_t idesc = make_idesc_f16(L.N);
+        const uint32_t w_hi_s = smem_u32(smem_w + L.w_hi), w_lo_s = smem_u32(smem_w + L.w_lo);
+        const uint32_t w_sbo = (uint32_t)L.K * 16u;
+        const uint32_t d = tmem_base + col_d;
+        for (uint32_t k = 0; k < (uint32_t)L.K / 16u; ++k) {
+            const uint64_t wh = make_smem_desc(w_hi_s + k * 256u, 128u, w_sbo);
+            const uint64_t wl = make_smem_desc(w_lo_s + k * 256u, 128u, w_sbo);
+            if (k == L.ones_slice) {
+                mma_f16_ts(d, tmem_base + col_ones, wh, idesc, 1u);
+                mma_f16_ts(d, tmem_base + col_ones, wl, idesc, 1u);
+            } else {
+                const uint32_t ah = tmem_base + col_a_hi + 8u * k, al = tmem_base + col_a_lo + 8u * k;
+                mma_f16_ts(d, ah, wh, idesc, k > 0 ? 1u : 0u);
+                mma_f16_ts(d, al, wh, idesc, 1u);
+                mma_f16_ts(d, ah, wl, idesc, 1u);
+            }
+        }
+        mma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    tc_fence_after();
+}
+
+// 32 fp32 values -> 16 hi + 16 lo packed fp16x2 TMEM columns of this thread's lane.
+__device__ __forceinline__ void ws_store_a32(uint32_t lane_base, uint32_t col_hi, const float *x) {
+#pragma unroll
+    for (int hblk = 0; hblk < 2; ++hblk) {
+        uint32_t h[8], l[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+            split2(x[16 * hblk + 2 * e], x[16 * hblk + 2 * e + 1], h[e], l[e]);
+        tmem_st8(lane_base + col_hi + 8u * hblk, h);
+        tmem_st8(lane_base + col_hi + 16u + 8u * hblk, l);
+    }
+}
+
+// MLP chain (3 hidden + head) on one group; input A at (col_in_hi, col_in_lo).
+__device__ __forceinline__ void ws_mlp(const uint8_t *smem_w, const NetDesc &net, uint32_t tmem_base,
+                                       uint32_t lane_base, uint32_t col_ones, uint32_t col_in_hi,
+                                       uint32_t col_in_lo, uint32_t col_d, uint32_t col_hid, uint64_t *bar,
+                                       uint32_t &phase, uint32_t bar_id, bool issuer, float (&y)[16]) {
+    uint32_t a_hi = col_in_hi, a_lo = col_in_lo;
+#pragma unroll 1
+    for (int l = 0; l < 3; ++l) {
+        ws_mma(smem_w, net.layer[l], tmem_base, col_ones, a_hi, a_lo, col_d, bar, phase, bar_id, issuer);
+        float acc[32];
+        tmem_ld32(lane_base + col_d, acc);
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+            acc[i] = fmaxf(acc[i], acc[i] * 0.01f);  // leaky ReLU = cwiseMax(z, slope z)
+        ws_store_a32(lane_base, col_hid, acc);
+        tmem_wait_st();
+        a_hi = col_hid;
+        a_lo = col_hid + 16u;
+    }
+    ws_mma(smem_w, net.layer[3], tmem_base, col_ones, a_hi, a_lo, col_d, bar, phase, bar_id, issuer);
+    tmem_ld16(lane_base + col_d, y);
+}
+
+}  // namespace ws
+
+template <int KIND, int GE, int GM>
+__global__ void __launch_bounds__(ws::Cfg<GE, GM>::kThreads, 1) infer_ws_kernel(InferParams p) {
+    using Cfg = ws::Cfg<GE, GM>;
+    constexpr int S = Cfg::kSlots;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem_w = smem_raw;
+    ws::Side *side = reinterpret_cast<ws::Side *>(smem_raw + ((p.blob_bytes + 127u) & ~127u));
+    ws::SmemTail *st = reinterpret_cast<ws::SmemTail *>(reinterpret_cast<uint8_t *>(side) + S * 128 * sizeof(ws::Side));
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    // ---- setup: weights -> smem, barriers, TMEM (all 512 columns), ones slice ----
+    {
+        const uint4 *src = reinterpret_cast<const uint4 *>(p.blob);
+        uint4 *dst = reinterpret_cast<uint4 *>(smem_w);
+        for (uint32_t i = tid; i < p.blob_bytes / 16u; i += Cfg::kThreads)
+            dst[i] = __ldg(src + i);
+    }
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&st->full[s], 256);
+            mbar_init(&st->empty[s], 128);
+        }
+        for (int g = 0; g < GM; ++g)
+            mbar_init(&st->mma_bar[g], 1);
+        fence_barrier_init();
+    }
+    if (warp == 0)
+        tmem_alloc(&st->tmem_base, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = st->tmem_base;
+    const uint32_t lane_base = tmem_base + ((uint32_t)((warp & 3) * 32) << 16);
+    if (tid >= Cfg::kEncThreads && tid < Cfg::kEncThreads + 128) {  // MLP group 0 writes the ones slice
+        const uint32_t ones[8] = {0x00003C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+        tmem_st8(lane_base + Cfg::kColOnes, ones);
+        tmem_wait_st();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    const uint64_t n = p.n;
+    const uint64_t num_tiles = (n + kTileM - 1) / kTileM;
+    const uint64_t t_begin = num_tiles * blockIdx.x / gridDim.x;
+    const uint64_t t_end = num_tiles * (blockIdx.x + 1) / gridDim.x;
+    const uint32_t T = (uint32_t)(t_end - t_begin);
+    double my_sum = 0.0;
+    uint32_t my_nonfinite = 0, my_bc = 0;
+    const bool depth1 = p.depth == 1u;
+
+    if (tid < Cfg::kEncThreads) {
+        // ============================== encoder ==============================
+        const int e = tid >> 8;                 // encoder group
+        const int r = tid & 127, half = (tid >> 7) & 1;
+        for (uint32_t i = (uint32_t)e; i < T; i += GE) {
+            const uint32_t s = i % S;
+            if (i >= (uint32_t)S)
+                mbar_wait(&st->empty[s], ((i / S) - 1u) & 1u);
+            const uint64_t j = (t_begin + i) * kTileM + r;
+            const bool valid = j < n;
+            float px = 0, py = 0, pz = 0, wx = 0, wy = 0, wz = 0, rough = 0;
+            if (valid) {
+                px = __ldg(p.p01 + 3 * j); py = __ldg(p.p01 + 3 * j + 1); pz = __ldg(p.p01 + 3 * j + 2);
+                wx = __ldg(p.weight + 3 * j); wy = __ldg(p.weight + 3 * j + 1); wz = __ldg(p.weight + 3 * j + 2);
+                rough = __ldg(p.roughness + j);
+            }
+            const bool active = valid && (p.gate ? (!depth1 && luminance(wx, wy, wz) > 0.0f) : true);
+            auto load_ipix = [&](float &a, float &b, float &c) {
+                a = b = c = 0.0f;
+                if (!valid)
+                    return;
+                if (p.i_pixel) {
+                    a = __ldg(p.i_pixel + 3 * j); b = __ldg(p.i_pixel + 3 * j + 1); c = __ldg(p.i_pixel + 3 * j + 2);
+                } else {
+                    const uint64_t px_idx = __ldg(p.pixel + j);
+                    a = __ldg(p.i_acc + 3 * px_idx); b = __ldg(p.i_acc + 3 * px_idx + 1); c = __ldg(p.i_acc + 3 * px_idx + 2);
+                }
+            };
+            float in16[16];
+            float *g8 = in16, *t8 = in16 + 8;
+            uint32_t bc = 0;
+            grid_encode4(KIND == kKindAid ? p.rrs_grid : p.stat_grid, p.grid, 4 * half, clamp01(px), clamp01(py),
+                         clamp01(pz), g8);
+            ws::Side sd{};
+            if (half == 0) {
+                const float wox = valid ? __ldg(p.wo01 + 2 * j) : 0.0f;
+                const float woy = valid ? __ldg(p.wo01 + 2 * j + 1) : 0.0f;
+                one_blob_fast<4>(wox, t8);
+                one_blob_fast<4>(woy, t8 + 4);
+                sd.key = valid && KIND != kKindStats ? __ldg(p.path_key + j) : 0ull;
+                sd.flags = (valid ? 1u : 0u) | (active ? 2u : 0u);
+                if (KIND == kKindNrrs) {
+                    float ipx, ipy, ipz;
+                    load_ipix(ipx, ipy, ipz);
+                    sd.ex[0] = box_cox(wx, bc);
+                    sd.ex[1] = box_cox(wy, bc);
+                    sd.ex[2] = box_cox(wz, bc);
+                    sd.ex[3] = box_cox(mean3(ipx, ipy, ipz), bc);
+                    sd.ex[4] = remap_fast(rough);
+                } else if (KIND == kKindAdrrs) {
+                    float ipx, ipy, ipz;
+                    load_ipix(ipx, ipy, ipz);
+                    sd.ex[0] = wx;
+                    sd.ex[1] = wy;
+                    sd.ex[2] = wz;
+                    sd.ex[3] = luminance(ipx, ipy, ipz);
+                }
+            } else if (KIND == kKindAid) {
+                float ipx, ipy, ipz;
+                load_ipix(ipx, ipy, ipz);
+                t8[0] = box_cox(wx, bc);
+                t8[1] = box_cox(wy, bc);
+                t8[2] = box_cox(wz, bc);
+                t8[3] = box_cox(mean3(ipx, ipy, ipz), bc);
+                one_blob_fast<4>(remap_fast(rough), t8 + 4);
+            } else {
+                one_blob_fast<8>(remap_fast(rough), t8);
+            }
+            if (!valid) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q)
+                    in16[q] = 0.0f;
+            }
+            if (active)
+                my_bc += bc;
+            const uint32_t col = Cfg::kColSlots + 32u * s;
+            uint32_t hw[8], lw[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                split2(in16[2 * q], in16[2 * q + 1], hw[q], lw[q]);
+            tmem_st8(lane_base + col + 8u * half, hw);
+            tmem_st8(lane_base + col + 16u + 8u * half, lw);
+            if (half == 0)
+                side[s * 128 + r] = sd;
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&st->full[s]);
+        }
+    } else {
+        // ================================ MLP ================================
+        const int mt = tid - Cfg::kEncThreads;
+        const int g = mt >> 7, r = mt & 127;
+        const bool issuer = (mt & 127) == 0;
+        const uint32_t col_d = Cfg::kColMlp + 64u * g, col_hid = col_d + 32u;
+        const uint32_t bar_id = 1u + (uint32_t)g;
+        uint32_t phase = 0;
+        for (uint32_t i = (uint32_t)g; i < T; i += GM) {
+            const uint32_t s = i % S;
+            mbar_wait(&st->full[s], (i / S) & 1u);
+            tc_fence_after();
+            const uint32_t col_in = Cfg::kColSlots + 32u * s;
+            float y[16];
+            float q = 0.0f;
+            const ws::Side sd = side[s * 128 + r];
+            const bool valid = sd.flags & 1u, active = (sd.flags >> 1) & 1u;
+            const uint64_t j = (t_begin + i) * kTileM + r;
+            if (KIND == kKindAid) {
+                ws::ws_mlp(smem_w, p.nets.rrs, tmem_base, lane_base, Cfg::kColOnes, col_in, col_in + 16u, col_d,
+                           col_hid, &st->mma_bar[g], phase, bar_id, issuer, y);
+                q = softplus_mod(y[0]);
+            } else {
+                ws::ws_mlp(smem_w, p.nets.stat, tmem_base, lane_base, Cfg::kColOnes, col_in, col_in + 16u, col_d,
+                           col_hid, &st->mma_bar[g], phase, bar_id, issuer, y);
+                if (KIND == kKindStats) {
+                    if (valid) {
+#pragma unroll
+                        for (int c = 0; c < 6; ++c)
+                            p.stats_out[6 * j + c] = y[c];
+                    }
+                } else if (KIND == kKindAdrrs) {
+                    const float num = luminance(sd.ex[0] * y[0], sd.ex[1] * y[1], sd.ex[2] * y[2]);
+                    const float qq = num / (sd.ex[3] + p.eps);
+                    q = qq < 0.05f ? 0.05f : (20.0f < qq ? 20.0f : qq);
+                } else {  // NRRS: stats -> build_nrrs_input (networks.cpp:137-147) -> RRSNet
+                    float xin[16];
+                    uint32_t bc = 0;
+#pragma unroll
+                    for (int c = 0; c < 6; ++c)
+                        xin[c] = box_cox(y[c], bc);
+#pragma unroll
+                    for (int c = 0; c < 5; ++c)
+                        xin[6 + c] = sd.ex[c];
+                    xin[11] = 1.0f;  // bias column of the RRSNet first layer
+#pragma unroll
+                    for (int c = 12; c < 16; ++c)
+                        xin[c] = 0.0f;
+                    if (!valid) {
+#pragma unroll
+                        for (int c = 0; c < 11; ++c)
+                            xin[c] = 0.0f;
+                    }
+                    if (active)
+                        my_bc += bc;
+                    uint32_t hw[8], lw[8];
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        split2(xin[2 * c], xin[2 * c + 1], hw[c], lw[c]);
+                    tmem_st8(lane_base + col_hid, hw);
+                    tmem_st8(lane_base + col_hid + 16u, lw);
+                    tmem_wait_st();
+                    ws::ws_mlp(smem_w, p.nets.rrs, tmem_base, lane_base, Cfg::kColOnes, col_hid, col_hid + 16u,
+                               col_d, col_hid, &st->mma_bar[g], phase, bar_id, issuer, y);
+                    q = softplus_mod(y[0]);
+                }
+            }
+            if (KIND != kKindStats) {
+                uint32_t decided = active ? 1u : 0u;
+                if (p.gate) {
+                    if (valid && depth1)
+                        q = 1.0f;
+                    if (!active && !depth1)
+                        q = 0.0f;
+                    decided = valid && (depth1 || active) ? 1u : 0u;
+                    if (valid && (!isfinite(q) || q < 0.0f)) {  // sanitize (wavefront.cpp:381-385)
+                        q = 0.0f;
+                        decided = 0;
+                        ++my_nonfinite;
+                    }
+                }
+                if (valid) {
+                    p.q_out[j] = q;
+                    if (p.u_out)
+                        p.u_out[j] = rrs_uniform(p.mixed_seed, sd.key, p.depth);
+                    if (p.decided_out)
+                        p.decided_out[j] = (uint8_t)decided;
+                    my_sum += (double)q;
+                }
+            }
+            mbar_arrive(&st->empty[s]);
+        }
+    }
+
+    // ---- teardown + deterministic CTA reduction, then last-CTA-done ----
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0)
+        tmem_dealloc(tmem_base, 512);
+    if (KIND == kKindStats || p.parts == nullptr)
+        return;
+    {
+        double sv = my_sum;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+            sv += __shfl_xor_sync(0xffffffffu, sv, o);
+        const uint32_t nf = __reduce_add_sync(0xffffffffu, my_nonfinite);
+        const uint32_t bcs = __reduce_add_sync(0xffffffffu, my_bc);
+        if (lane == 0) {
+            st->red_sum[warp] = sv;
+            st->red_nf[warp] = nf;
+            st->red_bc[warp] = bcs;
+        }
+        __syncthreads();
+    }
+    constexpr int kWarps = Cfg::kThreads / 32;
+    if (tid == 0) {
+        double cs = 0.0;
+        uint32_t cn = 0, cb = 0;
+        for (int w = 0; w < kWarps; ++w) {
+            cs += st->red_sum[w];
+            cn += st->red_nf[w];
+            cb += st->red_bc[w];
+        }
+        p.parts[blockIdx.x] = cs;
+        p.part_counts[2 * blockIdx.x] = cn;
+        p.part_counts[2 * blockIdx.x + 1] = cb;
+        __threadfence();
+        st->is_last = atomicAdd(p.counter, 1u) == gridDim.x - 1 ? 1u : 0u;
+    }
+    __syncthreads();
+    if (!st->is_last)
+        return;
+    __threadfence();
+    if (warp == 0) {
+        double sv = 0.0;
+        uint32_t nf = 0, bcs = 0;
+        for (uint32_t b = lane; b < gridDim.x; b += 32) {
+            sv += __ldcg(p.parts + b);
+            nf += __ldcg(p.part_counts + 2 * b);
+            bcs += __ldcg(p.part_counts + 2 * b + 1);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+            sv += __shfl_xor_sync(0xffffffffu, sv, o);
+        nf = __reduce_add_sync(0xffffffffu, nf);
+        bcs = __reduce_add_sync(0xffffffffu, bcs);
+        if (lane == 0) {
+            *p.sum_out = sv;
+            p.res->sum_q = sv;
+            p.res->nonfinite = nf;
+            p.res->box_cox_clamps = bcs;
+            *p.counter = 0;  // self-cleaning for the next launch
+        }
+    }
+}
+
+template <int KIND, int GE, int GM>
+static cudaError_t launch_ws(const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out) {
+    using Cfg = ws::Cfg<GE, GM>;
+    const size_t smem = ((p.blob_bytes + 127u) & ~127u) + Cfg::kSlots * 128 * sizeof(ws::Side) +
+                        sizeof(ws::SmemTail) + 64;
+    cudaError_t e = cudaFuncSetAttribute(infer_ws_kernel<KIND, GE, GM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess)
+        return e;
+    const uint64_t tiles = (p.n + kTileM - 1) / kTileM;
+    uint64_t grid = (uint64_t)num_sms;
+    if (grid > tiles)
+        grid = tiles;
+    if (grid < 1)
+        grid = 1;
+    *grid_out = (uint32_t)grid;
+    infer_ws_kernel<KIND, GE, GM><<<(uint32_t)grid, Cfg::kThreads, smem, stream>>>(p);
+    return cudaGetLastError();
+}
+
+// ===========================================================================
 // K-B: normalize + realize + scan + slot emission
 // ===========================================================================
 constexpr int kDecThreads = 256;
@@ -868,17 +1301,17 @@ size_t infer_smem_bytes(int kind, const InferParams &p) {
 }
 
 cudaError_t launch_infer(int kind, const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out) {
+    switch (kind) {
+    case kKindAdrrs: return launch_ws<kKindAdrrs, 2, 2>(p, num_sms, stream, grid_out);
+    case kKindNrrs: return launch_ws<kKindNrrs, 2, 3>(p, num_sms, stream, grid_out);
+    case kKindAid: return launch_ws<kKindAid, 2, 2>(p, num_sms, stream, grid_out);
+    case kKindStats: return launch_ws<kKindStats, 2, 2>(p, num_sms, stream, grid_out);
+    default: break;
+    }
     const uint64_t tiles = (p.n + kTileM - 1) / kTileM;
     const size_t smem = infer_smem_bytes(kind, p);
     int occ = 1;
-    cudaError_t e = cudaSuccess;
-    switch (kind) {
-    case kKindHeuristic: e = infer_occupancy<kKindHeuristic>(smem, &occ); break;
-    case kKindAdrrs: e = infer_occupancy<kKindAdrrs>(smem, &occ); break;
-    case kKindNrrs: e = infer_occupancy<kKindNrrs>(smem, &occ); break;
-    case kKindAid: e = infer_occupancy<kKindAid>(smem, &occ); break;
-    case kKindStats: e = infer_occupancy<kKindStats>(smem, &occ); break;
-    }
+    cudaError_t e = infer_occupancy<kKindHeuristic>(smem, &occ);
     if (e != cudaSuccess)
         return e;
     uint64_t grid = (uint64_t)num_sms * (uint64_t)occ;
@@ -887,14 +1320,7 @@ cudaError_t launch_infer(int kind, const InferParams &p, int num_sms, cudaStream
     if (grid < 1)
         grid = 1;
     *grid_out = (uint32_t)grid;
-    switch (kind) {
-    case kKindHeuristic: infer_kernel<kKindHeuristic><<<(uint32_t)grid, kInferThreads, smem, stream>>>(p); break;
-    case kKindAdrrs: infer_kernel<kKindAdrrs><<<(uint32_t)grid, kInferThreads, smem, stream>>>(p); break;
-    case kKindNrrs: infer_kernel<kKindNrrs><<<(uint32_t)grid, kInferThreads, smem, stream>>>(p); break;
-    case kKindAid: infer_kernel<kKindAid><<<(uint32_t)grid, kInferThreads, smem, stream>>>(p); break;
-    case kKindStats: infer_kernel<kKindStats><<<(uint32_t)grid, kInferThreads, smem, stream>>>(p); break;
-    default: return cudaErrorInvalidValue;
-    }
+    infer_kernel<kKindHeuristic><<<(uint32_t)grid, kInferThreads, smem, stream>>>(p);
     return cudaGetLastError();
 }
 
