@@ -402,14 +402,44 @@ int nrrs_gpu_set_weights(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w) {
         rc = upload_blob(ctx->blob_both, true, true);
     if (rc)
         return rc;
+    // three copies per grid (see GridDev): reference layout, then the
+    // edge-paired permutations for t = 1, 2 (dense levels: shifted copy)
+    auto pair_pos = [](uint32_t e, uint32_t t) -> uint32_t {
+        const uint32_t G = 2u << t, i = e & (G - 1u), half = G >> 1;
+        const uint32_t pi = i < half ? (i << 1) : (((G - 1u - i) << 1) | 1u);
+        return (e & ~(G - 1u)) | pi;
+    };
     auto upload_grid = [&](float *&dst, const float *src, uint64_t len) -> int {
         if (dst)
             cudaFree(dst);
         dst = nullptr;
         if (!len)
             return NRRS_OK;
-        CK(ctx, cudaMalloc(&dst, len * sizeof(float)));
-        CK(ctx, cudaMemcpy(dst, src, len * sizeof(float), cudaMemcpyHostToDevice));
+        std::vector<float> h(3 * len, 0.0f);
+        std::memcpy(h.data(), src, len * sizeof(float));
+        for (int l = 0; l < g.levels; ++l) {
+            const uint64_t res = (uint64_t)g.base_resolution << l;
+            const bool dense = (res + 1) * (res + 1) * (res + 1) <= T;
+            const float *lv = src + (uint64_t)l * T * 2;
+            float *c1 = h.data() + len + (uint64_t)l * T * 2;
+            float *c2 = h.data() + 2 * len + (uint64_t)l * T * 2;
+            for (uint32_t e = 0; e < T; ++e) {
+                if (dense) {
+                    if (e + 1 < T) {
+                        c1[2 * e] = lv[2 * (e + 1)];
+                        c1[2 * e + 1] = lv[2 * (e + 1) + 1];
+                    }
+                } else {
+                    const uint32_t p1 = pair_pos(e, 1), p2 = pair_pos(e, 2);
+                    c1[2 * p1] = lv[2 * e];
+                    c1[2 * p1 + 1] = lv[2 * e + 1];
+                    c2[2 * p2] = lv[2 * e];
+                    c2[2 * p2 + 1] = lv[2 * e + 1];
+                }
+            }
+        }
+        CK(ctx, cudaMalloc(&dst, 3 * len * sizeof(float)));
+        CK(ctx, cudaMemcpy(dst, h.data(), 3 * len * sizeof(float), cudaMemcpyHostToDevice));
         return NRRS_OK;
     };
     rc = upload_grid(ctx->d_stat_grid, w->stat_grid, grid_len);
@@ -423,6 +453,7 @@ int nrrs_gpu_set_weights(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w) {
     ctx->grid.base_resolution = g.base_resolution;
     ctx->grid.table_size = (uint32_t)T;
     ctx->grid.dense_mask = 0;
+    ctx->grid.copy_stride = (uint64_t)g.levels * T;
     for (int l = 0; l < g.levels; ++l) {
         const uint64_t res = (uint64_t)g.base_resolution << l;
         if ((res + 1) * (res + 1) * (res + 1) <= T)
@@ -539,9 +570,30 @@ static int run_factors(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, 
     ip.res = ctx->d_res;
     if (const char *ab = std::getenv("NRRS_DEBUG_ABLATE"))  // diagnostics only; results invalid
         ip.ablate = (uint32_t)std::atoi(ab);
+    unsigned long long *dbg = nullptr;
+    const bool timing = std::getenv("NRRS_DEBUG_TIMING") != nullptr;  // diagnostics only
+    if (timing) {
+        CK(ctx, cudaMalloc(&dbg, 16 * 1024 * sizeof(unsigned long long)));
+        CK(ctx, cudaMemsetAsync(dbg, 0, 16 * 1024 * sizeof(unsigned long long), ctx->stream));
+        ip.dbg = dbg;
+    }
     uint32_t grid = 0;
     CK(ctx, launch_infer(kind, ip, ctx->num_sms, ctx->stream, &grid));
     ctx->launches += 1;
+    if (timing) {
+        std::vector<unsigned long long> h(16 * 1024);
+        CK(ctx, cudaMemcpyAsync(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(ctx, cudaStreamSynchronize(ctx->stream));
+        double sum[16] = {0};
+        for (uint32_t b = 0; b < grid; ++b)
+            for (int k = 0; k < 16; ++k)
+                sum[k] += (double)h[b * 16 + k];
+        std::fprintf(stderr, "[nrrs timing] kind %d grid %u mean kcycles/CTA:", kind, grid);
+        for (int k = 0; k < 16; ++k)
+            std::fprintf(stderr, " %d:%.1f", k, sum[k] / grid / 1e3);
+        std::fprintf(stderr, "\n");
+        cudaFree(dbg);
+    }
     return NRRS_OK;
 }
 

@@ -36,11 +36,19 @@ struct KernelNets {
     NetDesc stat, rrs;
 };
 
+// Hash-grid tables on the device: three copies of the reference layout
+// [level][entry][feature], `copy_stride` entries apart:
+//   copy 0: the reference table (pairs (e, e^1) share an aligned 16-byte pair)
+//   copy 1: hashed levels: permuted so (e, e^3) share a pair; dense levels: shifted by one entry
+//   copy 2: hashed levels: permuted so (e, e^7) share a pair
+// A hashed x-edge (cx, cx+1) has entries e and e ^ (2^(t+1)-1), t = trailing ones of cx,
+// so copies 0/1/2 serve t = 0/1/2 with one 16-byte gather (7/8 of edges).
 struct GridDev {
     int32_t levels;
     int32_t base_resolution;
     uint32_t table_size;
     uint32_t dense_mask;  // bit l: level l is dense ((res+1)^3 <= T, hashgrid.hpp / hashgrid.cpp:16-22)
+    uint64_t copy_stride; // entries between table copies (= levels * table_size)
 };
 
 // Device-side scalar results of one stage call (mirrors nrrs_stage_result).
@@ -81,6 +89,7 @@ struct InferParams {
     double *sum_out;   // local sum of q
     DevResult *res;
     uint32_t ablate;   // debug only (env NRRS_DEBUG_ABLATE): bit0 skip grid gathers, bit1 skip MLP
+    unsigned long long *dbg;  // debug only (env NRRS_DEBUG_TIMING): per-CTA clock64 phase counters [grid][16]
 };
 
 struct DecideParams {

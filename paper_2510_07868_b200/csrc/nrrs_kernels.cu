@@ -117,27 +117,19 @@ __device__ __forceinline__ void run_mlp(const uint8_t *smem_w, const NetDesc &ne
     tmem_ld16(tmem_row + kColD, y);  // both halves load (warp-aligned); half 0 uses it
 }
 
-// Two corners of one cell edge: e0 and e1 are entry indices.  The aligned
-// 16-byte pair holding e0 is always loaded; it also holds e1 whenever
-// e1 == e0 ^ 1 (x-adjacent corners with even x on hashed levels, z-adjacent
-// corners with even base on dense levels), otherwise e1 is fetched alone.
-__device__ __forceinline__ void gather_edge(const float2 *__restrict__ lvl, uint32_t e0, uint32_t e1, float w0,
-                                            float w1, float &a0, float &a1) {
-    const float4 pr = __ldg(reinterpret_cast<const float4 *>(lvl) + (e0 >> 1));
-    const bool odd = e0 & 1u;
-    const float v0x = odd ? pr.z : pr.x, v0y = odd ? pr.w : pr.y;
-    float v1x = odd ? pr.x : pr.z, v1y = odd ? pr.y : pr.w;
-    if (e1 != (e0 ^ 1u)) {
-        const float2 v = __ldg(lvl + e1);
-        v1x = v.x;
-        v1y = v.y;
-    }
-    a0 += w0 * v0x + w1 * v1x;
-    a1 += w0 * v0y + w1 * v1y;
+// Position of entry e in the copy that pairs (e, e ^ (2^(t+1)-1)) into one
+// aligned 16-byte pair (t = 0: the reference layout).  Mirrors pair_pos in
+// nrrs_capi.cu (the host builds the copies at set_weights).
+__device__ __forceinline__ uint32_t pair_pos(uint32_t e, uint32_t t) {
+    const uint32_t G = 2u << t, i = e & (G - 1u), half = G >> 1;
+    const uint32_t pi = i < half ? (i << 1) : (((G - 1u - i) << 1) | 1u);
+    return (e & ~(G - 1u)) | pi;
 }
 
 // HashGrid::encode (hashgrid.cpp:38-82) for levels [l0, l0+4) of one point, F = 2.
-// Trilinear weight of corner (ox,oy,oz) = wx*wy*wz; entries summed per edge.
+// Each cell edge (2 corners) costs one 16-byte gather from the matching table
+// copy (GridDev); hashed x-edges with >= 3 trailing ones in cx (1/8) fetch the
+// second corner separately.
 __device__ __forceinline__ void grid_encode4(const float2 *__restrict__ theta, const GridDev &g, int l0,
                                              float cpx, float cpy, float cpz, float *out) {
 #pragma unroll
@@ -159,17 +151,24 @@ __device__ __forceinline__ void grid_encode4(const float2 *__restrict__ theta, c
         const float2 *lvl = theta + (size_t)l * g.table_size;
         float a0 = 0.0f, a1 = 0.0f;
         if ((g.dense_mask >> l) & 1u) {
-            // dense index (x*n + y)*n + z: edges along z
+            // dense index (x*n + y)*n + z: edges along z; odd bases read the shifted copy
             const uint32_t nn = res + 1u;
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const uint32_t ox = e & 1, oy = e >> 1;
                 const uint32_t e0 = ((cx + ox) * nn + cy + oy) * nn + cz;
+                const uint32_t odd = e0 & 1u;
+                const float4 pr =
+                    __ldg(reinterpret_cast<const float4 *>(lvl + (odd ? g.copy_stride : 0) + (e0 - odd)));
                 const float wxy = wx[ox] * wy[oy];
-                gather_edge(lvl, e0, e0 + 1u, wxy * wz[0], wxy * wz[1], a0, a1);
+                a0 += wxy * wz[0] * pr.x + wxy * wz[1] * pr.z;
+                a1 += wxy * wz[0] * pr.y + wxy * wz[1] * pr.w;
             }
         } else {
-            // hashed index x ^ y*PY ^ z*PZ: edges along x
+            // hashed index x ^ y*PY ^ z*PZ: edges along x, partner e ^ (2^(t+1)-1)
+            const uint32_t tones = __ffs(~cx) - 1u;
+            const uint32_t tc = tones > 2u ? 0u : tones;
+            const float2 *tab = lvl + (size_t)tc * g.copy_stride;
             const uint32_t yp[2] = {cy * 2654435761u, (cy + 1u) * 2654435761u};
             const uint32_t zp[2] = {cz * 805459861u, (cz + 1u) * 805459861u};
             const uint32_t m = g.table_size - 1u;
@@ -177,8 +176,20 @@ __device__ __forceinline__ void grid_encode4(const float2 *__restrict__ theta, c
             for (int e = 0; e < 4; ++e) {
                 const uint32_t oy = e & 1, oz = e >> 1;
                 const uint32_t k = yp[oy] ^ zp[oz];
+                const uint32_t e0 = (cx ^ k) & m;
+                const uint32_t pos = pair_pos(e0, tc);
+                const float4 pr = __ldg(reinterpret_cast<const float4 *>(tab + (pos & ~1u)));
+                const bool sw = pos & 1u;
+                const float v0x = sw ? pr.z : pr.x, v0y = sw ? pr.w : pr.y;
+                float v1x = sw ? pr.x : pr.z, v1y = sw ? pr.y : pr.w;
+                if (tones > 2u) {
+                    const float2 v = __ldg(lvl + (((cx + 1u) ^ k) & m));
+                    v1x = v.x;
+                    v1y = v.y;
+                }
                 const float wyz = wy[oy] * wz[oz];
-                gather_edge(lvl, (cx ^ k) & m, ((cx + 1u) ^ k) & m, wx[0] * wyz, wx[1] * wyz, a0, a1);
+                a0 += wx[0] * wyz * v0x + wx[1] * wyz * v1x;
+                a1 += wx[0] * wyz * v0y + wx[1] * wyz * v1y;
             }
         }
         out[2 * i] = a0;
@@ -509,23 +520,27 @@ struct Side {        // 32 B per tile row
     float ex[5];     // NRRS: bc(t_x)x3, bc(mean I), remap(r); ADRRS: w x3, lum(I)
 };
 
-template <int GE, int GM>
+// TMEM (512 columns, 1 CTA / SM): ones slice [0, 8); chain D accumulators
+// [32 + 32q, +32) for q < GM*P; tile slots [kColSlots + 32s, +32) holding the
+// layer-0 input (hi 16 | lo 16 columns), reused as the hidden-layer A.
+template <int GE, int GM, int P>
 struct Cfg {
     static constexpr int kEncThreads = GE * 256;
     static constexpr int kMlpThreads = GM * 128;
     static constexpr int kThreads = kEncThreads + kMlpThreads;
-    static constexpr uint32_t kColOnes = 0;                 // K16 ones slice [0, 8)
-    static constexpr uint32_t kColMlp = 32;                 // group g: D [32+64g, +32), A_hid [+32, +64)
-    static constexpr uint32_t kColSlots = 32 + 64 * GM;     // slot s: hi [c, c+16), lo [c+16, c+32)
+    static constexpr int kChains = GM * P;
+    static constexpr uint32_t kColOnes = 0;
+    static constexpr uint32_t kColD = 32;
+    static constexpr uint32_t kColSlots = 32 + 32 * kChains;
     static constexpr int kSlotsRaw = (512 - (int)kColSlots) / 32;
-    static constexpr int kSlots = kSlotsRaw > 8 ? 8 : kSlotsRaw;
-    static_assert(kSlots >= GE + GM, "TMEM slot ring too small");
+    static constexpr int kSlots = kSlotsRaw > 16 ? 16 : kSlotsRaw;
+    static_assert(kSlots >= GE + kChains, "TMEM slot ring too small");
 };
 
 struct SmemTail {
-    uint64_t full[8];
-    uint64_t empty[8];
-    uint64_t mma_bar[4];
+    uint64_t full[16];
+    uint64_t empty[16];
+    uint64_t mma_bar[8];
     uint32_t tmem_base;
     uint32_t is_last;
     double red_sum[32];
@@ -533,81 +548,51 @@ struct SmemTail {
     uint32_t red_bc[32];
 };
 
-// One MMA layer for an MLP group: named barrier (all 128 epilogue threads done
-// with TMEM), elected issue, commit, wait.
-__device__ __forceinline__ void ws_mma(const uint8_t *smem_w, const LayerDesc &L, uint32_t tmem_base,
-                                       uint32_t col_ones, uint32_t col_a_hi, uint32_t col_a_lo, uint32_t col_d,
-                                       uint64_t *bar, uint32_t &phase, uint32_t bar_id, bool issuer) {
-    tc_fence_before();
-    named_bar_sync(bar_id, 128);
-    if (issuer) {
-        tc_fence_after();
-        const uint32_t idesc = make_idesc_f16(L.N);
-        const uint32_t w_hi_s = smem_u32(smem_w + L.w_hi), w_lo_s = smem_u32(smem_w + L.w_lo);
-        const uint32_t w_sbo = (uint32_t)L.K * 16u;
-        const uint32_t d = tmem_base + col_d;
-        for (uint32_t k = 0; k < (uint32_t)L.K / 16u; ++k) {
-            const uint64_t wh = make_smem_desc(w_hi_s + k * 256u, 128u, w_sbo);
-            const uint64_t wl = make_smem_desc(w_lo_s + k * 256u, 128u, w_sbo);
-            if (k == L.ones_slice) {
-                mma_f16_ts(d, tmem_base + col_ones, wh, idesc, 1u);
-                mma_f16_ts(d, tmem_base + col_ones, wl, idesc, 1u);
-            } else {
-                const uint32_t ah = tmem_base + col_a_hi + 8u * k, al = tmem_base + col_a_lo + 8u * k;
-                mma_f16_ts(d, ah, wh, idesc, k > 0 ? 1u : 0u);
-                mma_f16_ts(d, al, wh, idesc, 1u);
-                mma_f16_ts(d, ah, wl, idesc, 1u);
-            }
-        }
-        mma_commit(bar);
-    }
-    mbar_wait(bar, phase);
-    phase ^= 1u;
+// Elected issue of one layer (3-term split on data slices, 2-term on the ones
+// slice), commit to the chain's mbarrier.  Caller has synchronized the group.
+__device__ __forceinline__ void ws_issue(const uint8_t *smem_w, const LayerDesc &L, uint32_t tmem_base,
+                                         uint32_t col_ones, uint32_t col_a, uint32_t col_d, uint64_t *bar) {
     tc_fence_after();
+    const uint32_t idesc = make_idesc_f16(L.N);
+    const uint32_t w_hi_s = smem_u32(smem_w + L.w_hi), w_lo_s = smem_u32(smem_w + L.w_lo);
+    const uint32_t w_sbo = (uint32_t)L.K * 16u;
+    const uint32_t d = tmem_base + col_d;
+    for (uint32_t k = 0; k < (uint32_t)L.K / 16u; ++k) {
+        const uint64_t wh = make_smem_desc(w_hi_s + k * 256u, 128u, w_sbo);
+        const uint64_t wl = make_smem_desc(w_lo_s + k * 256u, 128u, w_sbo);
+        if (k == L.ones_slice) {
+            mma_f16_ts(d, tmem_base + col_ones, wh, idesc, 1u);
+            mma_f16_ts(d, tmem_base + col_ones, wl, idesc, 1u);
+        } else {
+            const uint32_t ah = tmem_base + col_a + 8u * k, al = tmem_base + col_a + 16u + 8u * k;
+            mma_f16_ts(d, ah, wh, idesc, k > 0 ? 1u : 0u);
+            mma_f16_ts(d, al, wh, idesc, 1u);
+            mma_f16_ts(d, ah, wl, idesc, 1u);
+        }
+    }
+    mma_commit(bar);
 }
 
 // 32 fp32 values -> 16 hi + 16 lo packed fp16x2 TMEM columns of this thread's lane.
-__device__ __forceinline__ void ws_store_a32(uint32_t lane_base, uint32_t col_hi, const float *x) {
+__device__ __forceinline__ void ws_store_a32(uint32_t lane_base, uint32_t col, const float *x) {
 #pragma unroll
     for (int hblk = 0; hblk < 2; ++hblk) {
         uint32_t h[8], l[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e)
             split2(x[16 * hblk + 2 * e], x[16 * hblk + 2 * e + 1], h[e], l[e]);
-        tmem_st8(lane_base + col_hi + 8u * hblk, h);
-        tmem_st8(lane_base + col_hi + 16u + 8u * hblk, l);
+        tmem_st8(lane_base + col + 8u * hblk, h);
+        tmem_st8(lane_base + col + 16u + 8u * hblk, l);
     }
-}
-
-// MLP chain (3 hidden + head) on one group; input A at (col_in_hi, col_in_lo).
-__device__ __forceinline__ void ws_mlp(const uint8_t *smem_w, const NetDesc &net, uint32_t tmem_base,
-                                       uint32_t lane_base, uint32_t col_ones, uint32_t col_in_hi,
-                                       uint32_t col_in_lo, uint32_t col_d, uint32_t col_hid, uint64_t *bar,
-                                       uint32_t &phase, uint32_t bar_id, bool issuer, float (&y)[16]) {
-    uint32_t a_hi = col_in_hi, a_lo = col_in_lo;
-#pragma unroll 1
-    for (int l = 0; l < 3; ++l) {
-        ws_mma(smem_w, net.layer[l], tmem_base, col_ones, a_hi, a_lo, col_d, bar, phase, bar_id, issuer);
-        float acc[32];
-        tmem_ld32(lane_base + col_d, acc);
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-            acc[i] = fmaxf(acc[i], acc[i] * 0.01f);  // leaky ReLU = cwiseMax(z, slope z)
-        ws_store_a32(lane_base, col_hid, acc);
-        tmem_wait_st();
-        a_hi = col_hid;
-        a_lo = col_hid + 16u;
-    }
-    ws_mma(smem_w, net.layer[3], tmem_base, col_ones, a_hi, a_lo, col_d, bar, phase, bar_id, issuer);
-    tmem_ld16(lane_base + col_d, y);
 }
 
 }  // namespace ws
 
-template <int KIND, int GE, int GM>
-__global__ void __launch_bounds__(ws::Cfg<GE, GM>::kThreads, 1) infer_ws_kernel(InferParams p) {
-    using Cfg = ws::Cfg<GE, GM>;
+template <int KIND, int GE, int GM, int P>
+__global__ void __launch_bounds__(ws::Cfg<GE, GM, P>::kThreads, 1) infer_ws_kernel(InferParams p) {
+    using Cfg = ws::Cfg<GE, GM, P>;
     constexpr int S = Cfg::kSlots;
+    constexpr int kNL = KIND == kKindNrrs ? 8 : 4;  // MMA layers per tile (NRRS: StatNet then RRSNet)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem_w = smem_raw;
     ws::Side *side = reinterpret_cast<ws::Side *>(smem_raw + ((p.blob_bytes + 127u) & ~127u));
@@ -622,12 +607,12 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM>::kThreads, 1) infer_ws_kernel(
             dst[i] = __ldg(src + i);
     }
     if (tid == 0) {
-        for (int s = 0; s < S; ++s) {
-            mbar_init(&st->full[s], 256);
-            mbar_init(&st->empty[s], 128);
+        for (int q = 0; q < S; ++q) {
+            mbar_init(&st->full[q], 256);
+            mbar_init(&st->empty[q], 128);
         }
-        for (int g = 0; g < GM; ++g)
-            mbar_init(&st->mma_bar[g], 1);
+        for (int q = 0; q < Cfg::kChains; ++q)
+            mbar_init(&st->mma_bar[q], 1);
         fence_barrier_init();
     }
     if (warp == 0)
@@ -659,10 +644,14 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM>::kThreads, 1) infer_ws_kernel(
         // ============================== encoder ==============================
         const int e = tid >> 8;                 // encoder group
         const int r = tid & 127, half = (tid >> 7) & 1;
+        const bool rec = p.dbg && (tid & 255) == 0;
+        unsigned long long c_empty = 0, c_enc = 0, c_st = 0, t0 = 0;
         for (uint32_t i = (uint32_t)e; i < T; i += GE) {
             const uint32_t s = i % S;
+            if (rec) t0 = clock64();
             if (i >= (uint32_t)S)
                 mbar_wait(&st->empty[s], ((i / S) - 1u) & 1u);
+            if (rec) { const unsigned long long t1 = clock64(); c_empty += t1 - t0; t0 = t1; }
             const uint64_t j = (t_begin + i) * kTileM + r;
             const bool valid = j < n;
             float px = 0, py = 0, pz = 0, wx = 0, wy = 0, wz = 0, rough = 0;
@@ -686,8 +675,14 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM>::kThreads, 1) infer_ws_kernel(
             float in16[16];
             float *g8 = in16, *t8 = in16 + 8;
             uint32_t bc = 0;
-            grid_encode4(KIND == kKindAid ? p.rrs_grid : p.stat_grid, p.grid, 4 * half, clamp01(px), clamp01(py),
-                         clamp01(pz), g8);
+            if (p.ablate & 1u) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    g8[q] = px * (float)(q + 1) + py;
+            } else {
+                grid_encode4(KIND == kKindAid ? p.rrs_grid : p.stat_grid, p.grid, 4 * half, clamp01(px),
+                             clamp01(py), clamp01(pz), g8);
+            }
             ws::Side sd{};
             if (half == 0) {
                 const float wox = valid ? __ldg(p.wo01 + 2 * j) : 0.0f;
@@ -730,6 +725,7 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM>::kThreads, 1) infer_ws_kernel(
             }
             if (active)
                 my_bc += bc;
+            if (rec) { const unsigned long long t1 = clock64(); c_enc += t1 - t0; t0 = t1; }
             const uint32_t col = Cfg::kColSlots + 32u * s;
             uint32_t hw[8], lw[8];
 #pragma unroll
@@ -742,98 +738,168 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM>::kThreads, 1) infer_ws_kernel(
             tmem_wait_st();
             tc_fence_before();
             mbar_arrive(&st->full[s]);
+            if (rec) c_st += clock64() - t0;
+        }
+        if (rec) {
+            p.dbg[blockIdx.x * 16 + 4 * e + 0] = c_empty;
+            p.dbg[blockIdx.x * 16 + 4 * e + 1] = c_enc;
+            p.dbg[blockIdx.x * 16 + 4 * e + 2] = c_st;
         }
     } else {
         // ================================ MLP ================================
+        // Group g runs P tile chains in lockstep, layer by layer: while chain c's
+        // MMA is in flight the group drains the other chains' accumulators.
         const int mt = tid - Cfg::kEncThreads;
         const int g = mt >> 7, r = mt & 127;
-        const bool issuer = (mt & 127) == 0;
-        const uint32_t col_d = Cfg::kColMlp + 64u * g, col_hid = col_d + 32u;
+        const bool issuer = r == 0;
         const uint32_t bar_id = 1u + (uint32_t)g;
-        uint32_t phase = 0;
-        for (uint32_t i = (uint32_t)g; i < T; i += GM) {
-            const uint32_t s = i % S;
-            mbar_wait(&st->full[s], (i / S) & 1u);
-            tc_fence_after();
-            const uint32_t col_in = Cfg::kColSlots + 32u * s;
-            float y[16];
-            float q = 0.0f;
-            const ws::Side sd = side[s * 128 + r];
-            const bool valid = sd.flags & 1u, active = (sd.flags >> 1) & 1u;
-            const uint64_t j = (t_begin + i) * kTileM + r;
-            if (KIND == kKindAid) {
-                ws::ws_mlp(smem_w, p.nets.rrs, tmem_base, lane_base, Cfg::kColOnes, col_in, col_in + 16u, col_d,
-                           col_hid, &st->mma_bar[g], phase, bar_id, issuer, y);
-                q = softplus_mod(y[0]);
-            } else {
-                ws::ws_mlp(smem_w, p.nets.stat, tmem_base, lane_base, Cfg::kColOnes, col_in, col_in + 16u, col_d,
-                           col_hid, &st->mma_bar[g], phase, bar_id, issuer, y);
-                if (KIND == kKindStats) {
-                    if (valid) {
+        uint32_t phases = 0;  // bit c: parity of chain c's mbarrier
+        const bool rec = p.dbg && issuer;
+        unsigned long long c_wait = 0, c_epi = 0, t0 = 0;
+        for (uint32_t base = 0; base < T; base += Cfg::kChains) {
+            uint32_t tile[P], slot[P];
+            bool live[P];
 #pragma unroll
-                        for (int c = 0; c < 6; ++c)
-                            p.stats_out[6 * j + c] = y[c];
-                    }
-                } else if (KIND == kKindAdrrs) {
-                    const float num = luminance(sd.ex[0] * y[0], sd.ex[1] * y[1], sd.ex[2] * y[2]);
-                    const float qq = num / (sd.ex[3] + p.eps);
-                    q = qq < 0.05f ? 0.05f : (20.0f < qq ? 20.0f : qq);
-                } else {  // NRRS: stats -> build_nrrs_input (networks.cpp:137-147) -> RRSNet
-                    float xin[16];
-                    uint32_t bc = 0;
+            for (int c = 0; c < P; ++c) {
+                tile[c] = base + (uint32_t)(c * GM + g);
+                live[c] = tile[c] < T;
+                slot[c] = tile[c] % S;
+            }
+            if (!live[0])
+                break;
+            // layer 0 of every chain as soon as its input slot is full
+            tc_fence_before();
+            named_bar_sync(bar_id, 128);
 #pragma unroll
-                    for (int c = 0; c < 6; ++c)
-                        xin[c] = box_cox(y[c], bc);
-#pragma unroll
-                    for (int c = 0; c < 5; ++c)
-                        xin[6 + c] = sd.ex[c];
-                    xin[11] = 1.0f;  // bias column of the RRSNet first layer
-#pragma unroll
-                    for (int c = 12; c < 16; ++c)
-                        xin[c] = 0.0f;
-                    if (!valid) {
-#pragma unroll
-                        for (int c = 0; c < 11; ++c)
-                            xin[c] = 0.0f;
-                    }
-                    if (active)
-                        my_bc += bc;
-                    uint32_t hw[8], lw[8];
-#pragma unroll
-                    for (int c = 0; c < 8; ++c)
-                        split2(xin[2 * c], xin[2 * c + 1], hw[c], lw[c]);
-                    tmem_st8(lane_base + col_hid, hw);
-                    tmem_st8(lane_base + col_hid + 16u, lw);
-                    tmem_wait_st();
-                    ws::ws_mlp(smem_w, p.nets.rrs, tmem_base, lane_base, Cfg::kColOnes, col_hid, col_hid + 16u,
-                               col_d, col_hid, &st->mma_bar[g], phase, bar_id, issuer, y);
-                    q = softplus_mod(y[0]);
+            for (int c = 0; c < P; ++c) {
+                if (!live[c])
+                    continue;
+                mbar_wait(&st->full[slot[c]], (tile[c] / S) & 1u);
+                if (issuer) {
+                    const NetDesc &net0 = KIND == kKindAid ? p.nets.rrs : p.nets.stat;
+                    ws::ws_issue(smem_w, net0.layer[0], tmem_base, Cfg::kColOnes, Cfg::kColSlots + 32u * slot[c],
+                                 Cfg::kColD + 32u * (uint32_t)(g * P + c), &st->mma_bar[g * P + c]);
                 }
             }
-            if (KIND != kKindStats) {
-                uint32_t decided = active ? 1u : 0u;
-                if (p.gate) {
-                    if (valid && depth1)
-                        q = 1.0f;
-                    if (!active && !depth1)
-                        q = 0.0f;
-                    decided = valid && (depth1 || active) ? 1u : 0u;
-                    if (valid && (!isfinite(q) || q < 0.0f)) {  // sanitize (wavefront.cpp:381-385)
-                        q = 0.0f;
-                        decided = 0;
-                        ++my_nonfinite;
+#pragma unroll 1
+            for (int l = 0; l < kNL; ++l) {  // layer l just issued for every live chain
+#pragma unroll
+                for (int c = 0; c < P; ++c) {
+                    if (!live[c])
+                        continue;
+                    const int q = g * P + c;
+                    const uint32_t col_d = Cfg::kColD + 32u * (uint32_t)q;
+                    const uint32_t col_a = Cfg::kColSlots + 32u * slot[c];
+                    if (rec) t0 = clock64();
+                    mbar_wait(&st->mma_bar[q], (phases >> c) & 1u);
+                    phases ^= 1u << c;
+                    tc_fence_after();
+                    if (rec) { const unsigned long long t1 = clock64(); c_wait += t1 - t0; t0 = t1; }
+                    const bool head = (l & 3) == 3;
+                    const NetDesc &net = (KIND == kKindAid || l >= 4) ? p.nets.rrs : p.nets.stat;
+                    if (!head) {
+                        float acc[32];
+                        tmem_ld32(lane_base + col_d, acc);
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            acc[i] = fmaxf(acc[i], acc[i] * 0.01f);  // leaky ReLU = cwiseMax(z, slope z)
+                        ws::ws_store_a32(lane_base, col_a, acc);
+                        tmem_wait_st();
+                        tc_fence_before();
+                        named_bar_sync(bar_id, 128);
+                        if (issuer)
+                            ws::ws_issue(smem_w, net.layer[(l & 3) + 1], tmem_base, Cfg::kColOnes, col_a, col_d,
+                                         &st->mma_bar[q]);
+                    } else {
+                        float y[16];
+                        tmem_ld16(lane_base + col_d, y);
+                        mbar_wait(&st->full[slot[c]], (tile[c] / S) & 1u);  // sidecar visibility
+                        const ws::Side sd = side[slot[c] * 128 + r];
+                        const bool valid = sd.flags & 1u, active = (sd.flags >> 1) & 1u;
+                        const uint64_t j = (t_begin + tile[c]) * kTileM + r;
+                        if (KIND == kKindNrrs && l == 3) {
+                            // stats -> build_nrrs_input (networks.cpp:137-147) -> RRSNet layer 0
+                            float xin[16];
+                            uint32_t bc = 0;
+#pragma unroll
+                            for (int k = 0; k < 6; ++k)
+                                xin[k] = box_cox(y[k], bc);
+#pragma unroll
+                            for (int k = 0; k < 5; ++k)
+                                xin[6 + k] = sd.ex[k];
+                            xin[11] = 1.0f;  // bias column of the RRSNet first layer
+#pragma unroll
+                            for (int k = 12; k < 16; ++k)
+                                xin[k] = 0.0f;
+                            if (!valid) {
+#pragma unroll
+                                for (int k = 0; k < 11; ++k)
+                                    xin[k] = 0.0f;
+                            }
+                            if (active)
+                                my_bc += bc;
+                            uint32_t hw[8], lw[8];
+#pragma unroll
+                            for (int k = 0; k < 8; ++k)
+                                split2(xin[2 * k], xin[2 * k + 1], hw[k], lw[k]);
+                            tmem_st8(lane_base + col_a, hw);
+                            tmem_st8(lane_base + col_a + 16u, lw);
+                            tmem_wait_st();
+                            tc_fence_before();
+                            named_bar_sync(bar_id, 128);
+                            if (issuer)
+                                ws::ws_issue(smem_w, p.nets.rrs.layer[0], tmem_base, Cfg::kColOnes, col_a, col_d,
+                                             &st->mma_bar[q]);
+                        } else {
+                            float qv = 0.0f;
+                            if (KIND == kKindStats) {
+                                if (valid) {
+#pragma unroll
+                                    for (int k = 0; k < 6; ++k)
+                                        p.stats_out[6 * j + k] = y[k];
+                                }
+                            } else if (KIND == kKindAdrrs) {
+                                const float num = luminance(sd.ex[0] * y[0], sd.ex[1] * y[1], sd.ex[2] * y[2]);
+                                const float qq = num / (sd.ex[3] + p.eps);
+                                qv = qq < 0.05f ? 0.05f : (20.0f < qq ? 20.0f : qq);
+                            } else {
+                                qv = softplus_mod(y[0]);
+                            }
+                            if (p.ablate & 2u)
+                                qv = sd.ex[0] + 1.0f;
+                            if (KIND != kKindStats) {
+                                uint32_t decided = active ? 1u : 0u;
+                                if (p.gate) {
+                                    if (valid && depth1)
+                                        qv = 1.0f;
+                                    if (!active && !depth1)
+                                        qv = 0.0f;
+                                    decided = valid && (depth1 || active) ? 1u : 0u;
+                                    if (valid && (!isfinite(qv) || qv < 0.0f)) {  // sanitize (wavefront.cpp:381-385)
+                                        qv = 0.0f;
+                                        decided = 0;
+                                        ++my_nonfinite;
+                                    }
+                                }
+                                if (valid) {
+                                    p.q_out[j] = qv;
+                                    if (p.u_out)
+                                        p.u_out[j] = rrs_uniform(p.mixed_seed, sd.key, p.depth);
+                                    if (p.decided_out)
+                                        p.decided_out[j] = (uint8_t)decided;
+                                    my_sum += (double)qv;
+                                }
+                            }
+                            mbar_arrive(&st->empty[slot[c]]);
+                        }
                     }
-                }
-                if (valid) {
-                    p.q_out[j] = q;
-                    if (p.u_out)
-                        p.u_out[j] = rrs_uniform(p.mixed_seed, sd.key, p.depth);
-                    if (p.decided_out)
-                        p.decided_out[j] = (uint8_t)decided;
-                    my_sum += (double)q;
+                    if (rec) c_epi += clock64() - t0;
                 }
             }
-            mbar_arrive(&st->empty[s]);
+        }
+        if (rec) {
+            p.dbg[blockIdx.x * 16 + 8 + 2 * g + 0] = c_wait;
+            p.dbg[blockIdx.x * 16 + 8 + 2 * g + 1] = c_epi;
         }
     }
 
@@ -900,13 +966,13 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM>::kThreads, 1) infer_ws_kernel(
     }
 }
 
-template <int KIND, int GE, int GM>
+template <int KIND, int GE, int GM, int P>
 static cudaError_t launch_ws(const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out) {
-    using Cfg = ws::Cfg<GE, GM>;
+    using Cfg = ws::Cfg<GE, GM, P>;
     const size_t smem = ((p.blob_bytes + 127u) & ~127u) + Cfg::kSlots * 128 * sizeof(ws::Side) +
                         sizeof(ws::SmemTail) + 64;
-    cudaError_t e = cudaFuncSetAttribute(infer_ws_kernel<KIND, GE, GM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(infer_ws_kernel<KIND, GE, GM, P>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
         return e;
     const uint64_t tiles = (p.n + kTileM - 1) / kTileM;
@@ -916,7 +982,7 @@ static cudaError_t launch_ws(const InferParams &p, int num_sms, cudaStream_t str
     if (grid < 1)
         grid = 1;
     *grid_out = (uint32_t)grid;
-    infer_ws_kernel<KIND, GE, GM><<<(uint32_t)grid, Cfg::kThreads, smem, stream>>>(p);
+    infer_ws_kernel<KIND, GE, GM, P><<<(uint32_t)grid, Cfg::kThreads, smem, stream>>>(p);
     return cudaGetLastError();
 }
 
@@ -1302,10 +1368,10 @@ size_t infer_smem_bytes(int kind, const InferParams &p) {
 
 cudaError_t launch_infer(int kind, const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out) {
     switch (kind) {
-    case kKindAdrrs: return launch_ws<kKindAdrrs, 2, 2>(p, num_sms, stream, grid_out);
-    case kKindNrrs: return launch_ws<kKindNrrs, 2, 3>(p, num_sms, stream, grid_out);
-    case kKindAid: return launch_ws<kKindAid, 2, 2>(p, num_sms, stream, grid_out);
-    case kKindStats: return launch_ws<kKindStats, 2, 2>(p, num_sms, stream, grid_out);
+    case kKindAdrrs: return launch_ws<kKindAdrrs, 2, 2, 3>(p, num_sms, stream, grid_out);
+    case kKindNrrs: return launch_ws<kKindNrrs, 2, 2, 3>(p, num_sms, stream, grid_out);
+    case kKindAid: return launch_ws<kKindAid, 2, 2, 3>(p, num_sms, stream, grid_out);
+    case kKindStats: return launch_ws<kKindStats, 2, 2, 3>(p, num_sms, stream, grid_out);
     default: break;
     }
     const uint64_t tiles = (p.n + kTileM - 1) / kTileM;
