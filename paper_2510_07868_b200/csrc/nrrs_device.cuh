@@ -127,6 +127,22 @@ __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
+// try_wait with a suspend-time hint (ns): for long waits, parks the thread
+// instead of re-polling so it does not steal issue slots from working warps.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity, uint32_t hint_ns) {
+    uint32_t done = 0;
+    const uint32_t addr = smem_u32(bar);
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(addr), "r"(parity), "r"(hint_ns)
+            : "memory");
+    }
+}
+
 // Busy-poll variant (mbarrier.test_wait never suspends the thread).
 __device__ __forceinline__ void mbar_spin(uint64_t *bar, uint32_t parity) {
     uint32_t done = 0;

@@ -89,6 +89,7 @@ struct InferParams {
     double *sum_out;   // local sum of q
     DevResult *res;
     uint32_t ablate;   // debug only (env NRRS_DEBUG_ABLATE): bit0 skip grid gathers, bit1 skip MLP
+    uint32_t ws_cfg;          // pipeline variant (0 default; env NRRS_WS_CFG for tuning sweeps)
     unsigned long long *dbg;  // debug only (env NRRS_DEBUG_TIMING): per-CTA clock64 phase counters [grid][16]
 };
 

@@ -650,7 +650,7 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P>::kThreads, 1) infer_ws_kern
             const uint32_t s = i % S;
             if (rec) t0 = clock64();
             if (i >= (uint32_t)S)
-                mbar_wait(&st->empty[s], ((i / S) - 1u) & 1u);
+                mbar_wait_sleep(&st->empty[s], ((i / S) - 1u) & 1u, 1000u);
             if (rec) { const unsigned long long t1 = clock64(); c_empty += t1 - t0; t0 = t1; }
             const uint64_t j = (t_begin + i) * kTileM + r;
             const bool valid = j < n;
@@ -774,7 +774,7 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P>::kThreads, 1) infer_ws_kern
             for (int c = 0; c < P; ++c) {
                 if (!live[c])
                     continue;
-                mbar_wait(&st->full[slot[c]], (tile[c] / S) & 1u);
+                mbar_wait_sleep(&st->full[slot[c]], (tile[c] / S) & 1u, 1000u);
                 if (issuer) {
                     const NetDesc &net0 = KIND == kKindAid ? p.nets.rrs : p.nets.stat;
                     ws::ws_issue(smem_w, net0.layer[0], tmem_base, Cfg::kColOnes, Cfg::kColSlots + 32u * slot[c],
@@ -1366,12 +1366,26 @@ size_t infer_smem_bytes(int kind, const InferParams &p) {
     return p.blob_bytes + sizeof(InferSmemHeader) + 64;
 }
 
+// Pipeline shape (encoder groups GE, MLP groups GM, chains per MLP group P).
+// p.ws_cfg selects a tuned variant (0 = default); see DESIGN.md section 6.
+template <int KIND>
+static cudaError_t launch_ws_cfg(const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out) {
+    switch (p.ws_cfg) {
+    case 1: return launch_ws<KIND, 2, 2, 1>(p, num_sms, stream, grid_out);
+    case 2: return launch_ws<KIND, 2, 2, 2>(p, num_sms, stream, grid_out);
+    case 3: return launch_ws<KIND, 2, 2, 3>(p, num_sms, stream, grid_out);
+    case 4: return launch_ws<KIND, 2, 1, 3>(p, num_sms, stream, grid_out);
+    case 5: return launch_ws<KIND, 2, 3, 2>(p, num_sms, stream, grid_out);
+    default: return launch_ws<KIND, 2, 2, 1>(p, num_sms, stream, grid_out);
+    }
+}
+
 cudaError_t launch_infer(int kind, const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out) {
     switch (kind) {
-    case kKindAdrrs: return launch_ws<kKindAdrrs, 2, 2, 3>(p, num_sms, stream, grid_out);
-    case kKindNrrs: return launch_ws<kKindNrrs, 2, 2, 3>(p, num_sms, stream, grid_out);
-    case kKindAid: return launch_ws<kKindAid, 2, 2, 3>(p, num_sms, stream, grid_out);
-    case kKindStats: return launch_ws<kKindStats, 2, 2, 3>(p, num_sms, stream, grid_out);
+    case kKindAdrrs: return launch_ws_cfg<kKindAdrrs>(p, num_sms, stream, grid_out);
+    case kKindNrrs: return launch_ws_cfg<kKindNrrs>(p, num_sms, stream, grid_out);
+    case kKindAid: return launch_ws_cfg<kKindAid>(p, num_sms, stream, grid_out);
+    case kKindStats: return launch_ws_cfg<kKindStats>(p, num_sms, stream, grid_out);
     default: break;
     }
     const uint64_t tiles = (p.n + kTileM - 1) / kTileM;

@@ -23,6 +23,20 @@ __global__ void gmem_gather(const float2 *__restrict__ t, uint32_t mask, int ite
 }
 
 template <int ILP>
+__global__ void gmem_gather4(const float4 *__restrict__ t, uint32_t mask, int iters, float *out) {
+    uint32_t s = hash(blockIdx.x * blockDim.x + threadIdx.x);
+    float acc = 0.f;
+    for (int it = 0; it < iters; ++it) {
+        float4 v[ILP];
+#pragma unroll
+        for (int k = 0; k < ILP; ++k) { s = hash(s + k); v[k] = __ldg(t + (s & mask)); }
+#pragma unroll
+        for (int k = 0; k < ILP; ++k) acc += v[k].x + v[k].w;
+    }
+    if (acc == 12345.f) out[0] = acc;
+}
+
+template <int ILP>
 __global__ void smem_gather(int entries, int iters, float *out) {
     extern __shared__ float2 tab[];
     for (int i = threadIdx.x; i < entries; i += blockDim.x) tab[i] = make_float2(i, i);
@@ -47,7 +61,7 @@ int main() {
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
     const int iters = 256;
     for (int log2n : {12, 15, 18, 21}) {
-        for (int warps : {8, 16, 32}) {
+        for (int warps : {16, 64}) {
             const int blocks = sms * 2, threads = warps * 16;
             gmem_gather<8><<<blocks, threads>>>(t, (1u << log2n) - 1, iters, o);
             cudaEventRecord(a);
@@ -58,6 +72,20 @@ int main() {
             double cyc = ms * 1e-3 * clk * 1e3;  // clk in kHz
             printf("gmem table %5d KB warps/SM %2d: %.2f G gathers/s, %.2f gathers/cycle/SM\n",
                    (8 << log2n) >> 10, warps, loads / ms / 1e6, loads / cyc / sms);
+        }
+    }
+    for (int log2n : {17, 20}) {
+        for (int warps : {16, 32, 64}) {
+            const int blocks = sms * 2, threads = warps * 16;
+            gmem_gather4<8><<<blocks, threads>>>((const float4 *)t, (1u << log2n) - 1, iters, o);
+            cudaEventRecord(a);
+            gmem_gather4<8><<<blocks, threads>>>((const float4 *)t, (1u << log2n) - 1, iters, o);
+            cudaEventRecord(b); cudaEventSynchronize(b);
+            float ms; cudaEventElapsedTime(&ms, a, b);
+            double loads = (double)blocks * threads * iters * 8;
+            double cyc = ms * 1e-3 * clk * 1e3;
+            printf("gmem float4 table %5d KB warps/SM %2d: %.2f G gathers/s, %.2f gathers/cycle/SM\n",
+                   (16 << log2n) >> 10, warps, loads / ms / 1e6, loads / cyc / sms);
         }
     }
     cudaFuncSetAttribute(smem_gather<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
