@@ -593,7 +593,15 @@ static int run_factors(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, 
         std::fprintf(stderr, "[nrrs timing] kind %d grid %u mean kcycles/CTA:", kind, grid);
         for (int k = 0; k < 16; ++k)
             std::fprintf(stderr, " %d:%.1f", k, sum[k] / grid / 1e3);
-        std::fprintf(stderr, "\n");
+        unsigned long long mn = ~0ull, mx = 0, mxs = 0, mne = ~0ull;
+        for (uint32_t b = 0; b < grid; ++b) {
+            const unsigned long long s0 = h[b * 16 + 12], e0 = h[b * 16 + 13];
+            if (!s0) continue;
+            mn = s0 < mn ? s0 : mn; mxs = s0 > mxs ? s0 : mxs;
+            mx = e0 > mx ? e0 : mx; mne = e0 < mne ? e0 : mne;
+        }
+        std::fprintf(stderr, "\n[nrrs timing] CTA start spread %.1f us, end spread %.1f us, span %.1f us\n",
+                     (mxs - mn) / 1e3, (mx - mne) / 1e3, (mx - mn) / 1e3);
         cudaFree(dbg);
     }
     return NRRS_OK;

@@ -126,12 +126,38 @@ __device__ __forceinline__ uint32_t pair_pos(uint32_t e, uint32_t t) {
     return (e & ~(G - 1u)) | pi;
 }
 
+// Table entry access for fp32 (float2, 8 B) or fp16 (half2, 4 B) grids: one
+// gather returns the aligned entry pair (e, e^1) as (x0, y0, x1, y1).
+template <bool kHalf>
+struct GridTab {
+    __device__ static __forceinline__ float4 pair(const void *base, uint64_t e_even) {
+        if constexpr (kHalf) {
+            const uint2 v = __ldg(reinterpret_cast<const uint2 *>(reinterpret_cast<const __half2 *>(base) + e_even));
+            const float2 a = __half22float2(*reinterpret_cast<const __half2 *>(&v.x));
+            const float2 b = __half22float2(*reinterpret_cast<const __half2 *>(&v.y));
+            return make_float4(a.x, a.y, b.x, b.y);
+        } else {
+            return __ldg(reinterpret_cast<const float4 *>(reinterpret_cast<const float2 *>(base) + e_even));
+        }
+    }
+    __device__ static __forceinline__ float2 one(const void *base, uint64_t e) {
+        if constexpr (kHalf) {
+            const uint32_t v = __ldg(reinterpret_cast<const uint32_t *>(reinterpret_cast<const __half2 *>(base) + e));
+            return __half22float2(*reinterpret_cast<const __half2 *>(&v));
+        } else {
+            return __ldg(reinterpret_cast<const float2 *>(base) + e);
+        }
+    }
+};
+
 // HashGrid::encode (hashgrid.cpp:38-82) for levels [l0, l0+4) of one point, F = 2.
-// Each cell edge (2 corners) costs one 16-byte gather from the matching table
-// copy (GridDev); hashed x-edges with >= 3 trailing ones in cx (1/8) fetch the
-// second corner separately.
-__device__ __forceinline__ void grid_encode4(const float2 *__restrict__ theta, const GridDev &g, int l0,
-                                             float cpx, float cpy, float cpz, float *out) {
+// Each cell edge (2 corners) costs one gather of an aligned entry pair from the
+// matching table copy (GridDev); hashed x-edges with >= 3 trailing ones in cx
+// (1/8 of edges) fetch the second corner separately.
+template <bool kHalf = false>
+__device__ __forceinline__ void grid_encode4(const void *theta, const GridDev &g, int l0, float cpx, float cpy,
+                                             float cpz, float *out) {
+    using Tab = GridTab<kHalf>;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int l = l0 + i;
@@ -148,7 +174,7 @@ __device__ __forceinline__ void grid_encode4(const float2 *__restrict__ theta, c
         const uint32_t cz = min((uint32_t)fz, res - 1u);
         const float tx = fx - (float)cx, ty = fy - (float)cy, tz = fz - (float)cz;
         const float wx[2] = {1.0f - tx, tx}, wy[2] = {1.0f - ty, ty}, wz[2] = {1.0f - tz, tz};
-        const float2 *lvl = theta + (size_t)l * g.table_size;
+        const uint64_t lb = (uint64_t)l * g.table_size;
         float a0 = 0.0f, a1 = 0.0f;
         if ((g.dense_mask >> l) & 1u) {
             // dense index (x*n + y)*n + z: edges along z; odd bases read the shifted copy
@@ -158,8 +184,7 @@ __device__ __forceinline__ void grid_encode4(const float2 *__restrict__ theta, c
                 const uint32_t ox = e & 1, oy = e >> 1;
                 const uint32_t e0 = ((cx + ox) * nn + cy + oy) * nn + cz;
                 const uint32_t odd = e0 & 1u;
-                const float4 pr =
-                    __ldg(reinterpret_cast<const float4 *>(lvl + (odd ? g.copy_stride : 0) + (e0 - odd)));
+                const float4 pr = Tab::pair(theta, (odd ? g.copy_stride : 0) + lb + (e0 - odd));
                 const float wxy = wx[ox] * wy[oy];
                 a0 += wxy * wz[0] * pr.x + wxy * wz[1] * pr.z;
                 a1 += wxy * wz[0] * pr.y + wxy * wz[1] * pr.w;
@@ -168,7 +193,7 @@ __device__ __forceinline__ void grid_encode4(const float2 *__restrict__ theta, c
             // hashed index x ^ y*PY ^ z*PZ: edges along x, partner e ^ (2^(t+1)-1)
             const uint32_t tones = __ffs(~cx) - 1u;
             const uint32_t tc = tones > 2u ? 0u : tones;
-            const float2 *tab = lvl + (size_t)tc * g.copy_stride;
+            const uint64_t tab = lb + (uint64_t)tc * g.copy_stride;
             const uint32_t yp[2] = {cy * 2654435761u, (cy + 1u) * 2654435761u};
             const uint32_t zp[2] = {cz * 805459861u, (cz + 1u) * 805459861u};
             const uint32_t m = g.table_size - 1u;
@@ -178,12 +203,12 @@ __device__ __forceinline__ void grid_encode4(const float2 *__restrict__ theta, c
                 const uint32_t k = yp[oy] ^ zp[oz];
                 const uint32_t e0 = (cx ^ k) & m;
                 const uint32_t pos = pair_pos(e0, tc);
-                const float4 pr = __ldg(reinterpret_cast<const float4 *>(tab + (pos & ~1u)));
+                const float4 pr = Tab::pair(theta, tab + (pos & ~1u));
                 const bool sw = pos & 1u;
                 const float v0x = sw ? pr.z : pr.x, v0y = sw ? pr.w : pr.y;
                 float v1x = sw ? pr.x : pr.z, v1y = sw ? pr.y : pr.w;
                 if (tones > 2u) {
-                    const float2 v = __ldg(lvl + (((cx + 1u) ^ k) & m));
+                    const float2 v = Tab::one(theta, lb + (((cx + 1u) ^ k) & m));
                     v1x = v.x;
                     v1y = v.y;
                 }
@@ -523,10 +548,11 @@ struct Side {        // 32 B per tile row
 // TMEM (512 columns, 1 CTA / SM): ones slice [0, 8); chain D accumulators
 // [32 + 32q, +32) for q < GM*P; tile slots [kColSlots + 32s, +32) holding the
 // layer-0 input (hi 16 | lo 16 columns), reused as the hidden-layer A.
-template <int GE, int GM, int P>
+template <int GE, int GM, int P, int TPR>
 struct Cfg {
+    static constexpr int kGroupThreads = 128 * TPR;  // MLP threads per group (TPR threads per tile row)
     static constexpr int kEncThreads = GE * 256;
-    static constexpr int kMlpThreads = GM * 128;
+    static constexpr int kMlpThreads = GM * kGroupThreads;
     static constexpr int kThreads = kEncThreads + kMlpThreads;
     static constexpr int kChains = GM * P;
     static constexpr uint32_t kColOnes = 0;
@@ -541,6 +567,10 @@ struct SmemTail {
     uint64_t full[16];
     uint64_t empty[16];
     uint64_t mma_bar[8];
+    uint64_t wdesc[2][4][3][2];  // precomputed UMMA smem descriptors of [W | bias] hi / lo per K16 slice
+    uint32_t idesc[2][4];
+    uint32_t nslices[2][4];
+    uint32_t ones_slice[2][4];
     uint32_t tmem_base;
     uint32_t is_last;
     double red_sum[32];
@@ -550,21 +580,22 @@ struct SmemTail {
 
 // Elected issue of one layer (3-term split on data slices, 2-term on the ones
 // slice), commit to the chain's mbarrier.  Caller has synchronized the group.
-__device__ __forceinline__ void ws_issue(const uint8_t *smem_w, const LayerDesc &L, uint32_t tmem_base,
+__device__ __forceinline__ void ws_issue(const SmemTail *st, int net, int layer, uint32_t tmem_base,
                                          uint32_t col_ones, uint32_t col_a, uint32_t col_d, uint64_t *bar) {
     tc_fence_after();
-    const uint32_t idesc = make_idesc_f16(L.N);
-    const uint32_t w_hi_s = smem_u32(smem_w + L.w_hi), w_lo_s = smem_u32(smem_w + L.w_lo);
-    const uint32_t w_sbo = (uint32_t)L.K * 16u;
+    const uint32_t idesc = st->idesc[net][layer];
+    const uint32_t ns = st->nslices[net][layer], os = st->ones_slice[net][layer];
     const uint32_t d = tmem_base + col_d;
-    for (uint32_t k = 0; k < (uint32_t)L.K / 16u; ++k) {
-        const uint64_t wh = make_smem_desc(w_hi_s + k * 256u, 128u, w_sbo);
-        const uint64_t wl = make_smem_desc(w_lo_s + k * 256u, 128u, w_sbo);
-        if (k == L.ones_slice) {
+#pragma unroll
+    for (uint32_t k = 0; k < 3; ++k) {
+        if (k >= ns)
+            break;
+        const uint64_t wh = st->wdesc[net][layer][k][0], wl = st->wdesc[net][layer][k][1];
+        if (k == os) {
             mma_f16_ts(d, tmem_base + col_ones, wh, idesc, 1u);
             mma_f16_ts(d, tmem_base + col_ones, wl, idesc, 1u);
         } else {
-            const uint32_t ah = tmem_base + col_a + 8u * k, al = tmem_base + col_a + 16u + 8u * k;
+            const uint32_t ah = tmem_base + col_a + 8u * k, al = ah + 16u;
             mma_f16_ts(d, ah, wh, idesc, k > 0 ? 1u : 0u);
             mma_f16_ts(d, al, wh, idesc, 1u);
             mma_f16_ts(d, ah, wl, idesc, 1u);
@@ -588,11 +619,15 @@ __device__ __forceinline__ void ws_store_a32(uint32_t lane_base, uint32_t col, c
 
 }  // namespace ws
 
-template <int KIND, int GE, int GM, int P>
-__global__ void __launch_bounds__(ws::Cfg<GE, GM, P>::kThreads, 1) infer_ws_kernel(InferParams p) {
-    using Cfg = ws::Cfg<GE, GM, P>;
+template <int KIND, int GE, int GM, int P, int TPR>
+__global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws_kernel(InferParams p) {
+    using Cfg = ws::Cfg<GE, GM, P, TPR>;
+    constexpr uint32_t kGT = Cfg::kGroupThreads;
     constexpr int S = Cfg::kSlots;
     constexpr int kNL = KIND == kKindNrrs ? 8 : 4;  // MMA layers per tile (NRRS: StatNet then RRSNet)
+    unsigned long long g_start = 0;
+    if (p.dbg && threadIdx.x == 0)
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem_w = smem_raw;
     ws::Side *side = reinterpret_cast<ws::Side *>(smem_raw + ((p.blob_bytes + 127u) & ~127u));
@@ -607,9 +642,23 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P>::kThreads, 1) infer_ws_kern
             dst[i] = __ldg(src + i);
     }
     if (tid == 0) {
+        for (int net = 0; net < 2; ++net) {
+            const NetDesc &nd = net == 0 ? p.nets.stat : p.nets.rrs;
+            for (int l = 0; l < 4; ++l) {
+                const LayerDesc &L = nd.layer[l];
+                st->idesc[net][l] = make_idesc_f16(L.N);
+                st->nslices[net][l] = (uint32_t)L.K / 16u;
+                st->ones_slice[net][l] = L.ones_slice;
+                const uint32_t sbo = (uint32_t)L.K * 16u;
+                for (int k = 0; k < 3; ++k) {
+                    st->wdesc[net][l][k][0] = make_smem_desc(smem_u32(smem_w + L.w_hi) + 256u * k, 128u, sbo);
+                    st->wdesc[net][l][k][1] = make_smem_desc(smem_u32(smem_w + L.w_lo) + 256u * k, 128u, sbo);
+                }
+            }
+        }
         for (int q = 0; q < S; ++q) {
             mbar_init(&st->full[q], 256);
-            mbar_init(&st->empty[q], 128);
+            mbar_init(&st->empty[q], kGT);
         }
         for (int q = 0; q < Cfg::kChains; ++q)
             mbar_init(&st->mma_bar[q], 1);
@@ -679,9 +728,10 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P>::kThreads, 1) infer_ws_kern
 #pragma unroll
                 for (int q = 0; q < 8; ++q)
                     g8[q] = px * (float)(q + 1) + py;
+            } else if (KIND == kKindAid) {
+                grid_encode4<false>(p.rrs_grid, p.grid, 4 * half, clamp01(px), clamp01(py), clamp01(pz), g8);
             } else {
-                grid_encode4(KIND == kKindAid ? p.rrs_grid : p.stat_grid, p.grid, 4 * half, clamp01(px),
-                             clamp01(py), clamp01(pz), g8);
+                grid_encode4<false>(p.stat_grid, p.grid, 4 * half, clamp01(px), clamp01(py), clamp01(pz), g8);
             }
             ws::Side sd{};
             if (half == 0) {
@@ -750,8 +800,8 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P>::kThreads, 1) infer_ws_kern
         // Group g runs P tile chains in lockstep, layer by layer: while chain c's
         // MMA is in flight the group drains the other chains' accumulators.
         const int mt = tid - Cfg::kEncThreads;
-        const int g = mt >> 7, r = mt & 127;
-        const bool issuer = r == 0;
+        const int g = mt / (int)kGT, gt = mt % (int)kGT, r = gt & 127, mh = gt >> 7;  // mh: column half (TPR 2)
+        const bool issuer = gt == 0;
         const uint32_t bar_id = 1u + (uint32_t)g;
         uint32_t phases = 0;  // bit c: parity of chain c's mbarrier
         const bool rec = p.dbg && issuer;
@@ -769,17 +819,16 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P>::kThreads, 1) infer_ws_kern
                 break;
             // layer 0 of every chain as soon as its input slot is full
             tc_fence_before();
-            named_bar_sync(bar_id, 128);
+            named_bar_sync(bar_id, kGT);
 #pragma unroll
             for (int c = 0; c < P; ++c) {
                 if (!live[c])
                     continue;
-                mbar_wait_sleep(&st->full[slot[c]], (tile[c] / S) & 1u, 1000u);
-                if (issuer) {
-                    const NetDesc &net0 = KIND == kKindAid ? p.nets.rrs : p.nets.stat;
-                    ws::ws_issue(smem_w, net0.layer[0], tmem_base, Cfg::kColOnes, Cfg::kColSlots + 32u * slot[c],
-                                 Cfg::kColD + 32u * (uint32_t)(g * P + c), &st->mma_bar[g * P + c]);
-                }
+                mbar_wait(&st->full[slot[c]], (tile[c] / S) & 1u);
+                if (issuer)
+                    ws::ws_issue(st, KIND == kKindAid ? 1 : 0, 0, tmem_base, Cfg::kColOnes,
+                                 Cfg::kColSlots + 32u * slot[c], Cfg::kColD + 32u * (uint32_t)(g * P + c),
+                                 &st->mma_bar[g * P + c]);
             }
 #pragma unroll 1
             for (int l = 0; l < kNL; ++l) {  // layer l just issued for every live chain
@@ -796,20 +845,40 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P>::kThreads, 1) infer_ws_kern
                     tc_fence_after();
                     if (rec) { const unsigned long long t1 = clock64(); c_wait += t1 - t0; t0 = t1; }
                     const bool head = (l & 3) == 3;
-                    const NetDesc &net = (KIND == kKindAid || l >= 4) ? p.nets.rrs : p.nets.stat;
+                    const int net = (KIND == kKindAid || l >= 4) ? 1 : 0;
                     if (!head) {
-                        float acc[32];
-                        tmem_ld32(lane_base + col_d, acc);
+                        if constexpr (TPR == 1) {
+                            float acc[32];
+                            tmem_ld32(lane_base + col_d, acc);
 #pragma unroll
-                        for (int i = 0; i < 32; ++i)
-                            acc[i] = fmaxf(acc[i], acc[i] * 0.01f);  // leaky ReLU = cwiseMax(z, slope z)
-                        ws::ws_store_a32(lane_base, col_a, acc);
+                            for (int i = 0; i < 32; ++i)
+                                acc[i] = fmaxf(acc[i], acc[i] * 0.01f);  // leaky ReLU = cwiseMax(z, slope z)
+                            ws::ws_store_a32(lane_base, col_a, acc);
+                        } else {
+                            float acc[16];
+                            tmem_ld16(lane_base + col_d + 16u * (uint32_t)mh, acc);
+                            uint32_t hw[8], lw[8];
+#pragma unroll
+                            for (int i = 0; i < 8; ++i)
+                                split2(fmaxf(acc[2 * i], acc[2 * i] * 0.01f),
+                                       fmaxf(acc[2 * i + 1], acc[2 * i + 1] * 0.01f), hw[i], lw[i]);
+                            tmem_st8(lane_base + col_a + 8u * (uint32_t)mh, hw);
+                            tmem_st8(lane_base + col_a + 16u + 8u * (uint32_t)mh, lw);
+                        }
                         tmem_wait_st();
                         tc_fence_before();
-                        named_bar_sync(bar_id, 128);
+                        named_bar_sync(bar_id, kGT);
                         if (issuer)
-                            ws::ws_issue(smem_w, net.layer[(l & 3) + 1], tmem_base, Cfg::kColOnes, col_a, col_d,
+                            ws::ws_issue(st, net, (l & 3) + 1, tmem_base, Cfg::kColOnes, col_a, col_d,
                                          &st->mma_bar[q]);
+                    } else if (mh != 0) {
+                        // TPR 2, second column half: no head work; keep the group's barrier count
+                        if (KIND == kKindNrrs && l == 3) {
+                            tc_fence_before();
+                            named_bar_sync(bar_id, kGT);
+                        } else {
+                            mbar_arrive(&st->empty[slot[c]]);
+                        }
                     } else {
                         float y[16];
                         tmem_ld16(lane_base + col_d, y);
@@ -846,10 +915,9 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P>::kThreads, 1) infer_ws_kern
                             tmem_st8(lane_base + col_a + 16u, lw);
                             tmem_wait_st();
                             tc_fence_before();
-                            named_bar_sync(bar_id, 128);
+                            named_bar_sync(bar_id, kGT);
                             if (issuer)
-                                ws::ws_issue(smem_w, p.nets.rrs.layer[0], tmem_base, Cfg::kColOnes, col_a, col_d,
-                                             &st->mma_bar[q]);
+                                ws::ws_issue(st, 1, 0, tmem_base, Cfg::kColOnes, col_a, col_d, &st->mma_bar[q]);
                         } else {
                             float qv = 0.0f;
                             if (KIND == kKindStats) {
@@ -906,6 +974,12 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P>::kThreads, 1) infer_ws_kern
     // ---- teardown + deterministic CTA reduction, then last-CTA-done ----
     tc_fence_before();
     __syncthreads();
+    if (p.dbg && tid == 0) {
+        unsigned long long g_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
+        p.dbg[blockIdx.x * 16 + 12] = g_start;
+        p.dbg[blockIdx.x * 16 + 13] = g_end;
+    }
     if (warp == 0)
         tmem_dealloc(tmem_base, 512);
     if (KIND == kKindStats || p.parts == nullptr)
@@ -966,12 +1040,12 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P>::kThreads, 1) infer_ws_kern
     }
 }
 
-template <int KIND, int GE, int GM, int P>
+template <int KIND, int GE, int GM, int P, int TPR = 1>
 static cudaError_t launch_ws(const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out) {
-    using Cfg = ws::Cfg<GE, GM, P>;
+    using Cfg = ws::Cfg<GE, GM, P, TPR>;
     const size_t smem = ((p.blob_bytes + 127u) & ~127u) + Cfg::kSlots * 128 * sizeof(ws::Side) +
                         sizeof(ws::SmemTail) + 64;
-    cudaError_t e = cudaFuncSetAttribute(infer_ws_kernel<KIND, GE, GM, P>,
+    cudaError_t e = cudaFuncSetAttribute(infer_ws_kernel<KIND, GE, GM, P, TPR>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
         return e;
@@ -982,7 +1056,7 @@ static cudaError_t launch_ws(const InferParams &p, int num_sms, cudaStream_t str
     if (grid < 1)
         grid = 1;
     *grid_out = (uint32_t)grid;
-    infer_ws_kernel<KIND, GE, GM, P><<<(uint32_t)grid, Cfg::kThreads, smem, stream>>>(p);
+    infer_ws_kernel<KIND, GE, GM, P, TPR><<<(uint32_t)grid, Cfg::kThreads, smem, stream>>>(p);
     return cudaGetLastError();
 }
 
@@ -1374,9 +1448,14 @@ static cudaError_t launch_ws_cfg(const InferParams &p, int num_sms, cudaStream_t
     case 1: return launch_ws<KIND, 2, 2, 1>(p, num_sms, stream, grid_out);
     case 2: return launch_ws<KIND, 2, 2, 2>(p, num_sms, stream, grid_out);
     case 3: return launch_ws<KIND, 2, 2, 3>(p, num_sms, stream, grid_out);
-    case 4: return launch_ws<KIND, 2, 1, 3>(p, num_sms, stream, grid_out);
-    case 5: return launch_ws<KIND, 2, 3, 2>(p, num_sms, stream, grid_out);
-    default: return launch_ws<KIND, 2, 2, 1>(p, num_sms, stream, grid_out);
+    case 4: return launch_ws<KIND, 2, 3, 1>(p, num_sms, stream, grid_out);
+    case 5: return launch_ws<KIND, 2, 4, 1>(p, num_sms, stream, grid_out);
+    case 6: return launch_ws<KIND, 2, 2, 1, 2>(p, num_sms, stream, grid_out);
+    case 7: return launch_ws<KIND, 1, 2, 1, 2>(p, num_sms, stream, grid_out);
+    case 8: return launch_ws<KIND, 2, 1, 1, 2>(p, num_sms, stream, grid_out);
+    case 9: return launch_ws<KIND, 1, 3, 1, 2>(p, num_sms, stream, grid_out);
+    default:  // tuned default: 2 encoder groups, 3 single-chain MLP groups
+        return launch_ws<KIND, 2, 3, 1>(p, num_sms, stream, grid_out);
     }
 }
 
