@@ -1061,20 +1061,22 @@ static cudaError_t launch_ws(const InferParams &p, int num_sms, cudaStream_t str
 }
 
 // ===========================================================================
-// K-B: normalize + realize + scan + slot emission
+// K-B / K-C, two-pass large-tile versions (used by the launchers below).
+// A tile is 8 sub-tiles of 512 threads x 4 items = 16,384 elements.  Pass 1
+// computes and writes the per-element results and keeps the counts in shared
+// memory; one warp-parallel look-back over <= n/16384 tiles gives the tile's
+// exclusive prefix; pass 2 re-scans the counts sub-tile by sub-tile and emits
+// offsets / slot records with coalesced stores.  Few, large tiles keep the
+// look-back chain short (the small-tile version spent most of its time there).
 // ===========================================================================
-constexpr int kDecThreads = 256;
-constexpr int kDecItems = 8;
-constexpr int kDecTile = kDecThreads * kDecItems;
+constexpr int kBT = 512;            // threads
+constexpr int kBItems = 4;          // items per thread per sub-tile
+constexpr int kBSub = kBT * kBItems;  // 2048
+constexpr int kBSubs = 8;
+constexpr int kBTile = kBSub * kBSubs;  // 16384
 
-struct DecideSmem {
-    uint32_t incl[kDecTile];
-    uint32_t warp_tot[kDecThreads / 32];
-    uint64_t prefix;
-    uint32_t tile;
-};
-
-__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t *warp_tot, uint32_t &total) {
+template <int NT>
+__device__ __forceinline__ uint32_t block_scan_excl(uint32_t v, uint32_t *warp_tot, uint32_t &total) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t inc = v;
 #pragma unroll
@@ -1083,12 +1085,13 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t *w
         if (lane >= o)
             inc += t;
     }
+    __syncthreads();  // warp_tot reuse across calls
     if (lane == 31)
         warp_tot[warp] = inc;
     __syncthreads();
     uint32_t before = 0, all = 0;
 #pragma unroll
-    for (int w = 0; w < kDecThreads / 32; ++w) {
+    for (int w = 0; w < NT / 32; ++w) {
         const uint32_t t = warp_tot[w];
         if (w < warp)
             before += t;
@@ -1098,19 +1101,25 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t *w
     return before + inc - v;
 }
 
+struct Decide2Smem {
+    uint32_t k[kBTile];
+    uint32_t incl[kBSub];
+    uint32_t warp_tot[kBT / 32];
+    unsigned long long prefix;
+    uint32_t tile;
+};
+
 template <int SRC>  // 0: counts from (q, u) with normalization; 1: counts given (plan_spawns)
-__global__ void __launch_bounds__(kDecThreads) decide_kernel(DecideParams p) {
-    __shared__ DecideSmem sm;
+__global__ void __launch_bounds__(kBT) decide2_kernel(DecideParams p) {
+    extern __shared__ __align__(16) uint8_t dsm[];
+    Decide2Smem &sm = *reinterpret_cast<Decide2Smem *>(dsm);
     const int tid = threadIdx.x;
     if (tid == 0)
         sm.tile = claim_tile(p.tile_counter, p.num_tiles);
     __syncthreads();
     const uint32_t tile = sm.tile;
-    const uint64_t base = (uint64_t)tile * kDecTile;
-    const uint64_t first = base + (uint64_t)tid * kDecItems;
+    const uint64_t tbase = (uint64_t)tile * kBTile;
 
-    // F from the rank sums in rank order (rrs.cpp:8-24 with the tile-sharded
-    // global budget)
     bool apply = false;
     float scale = 1.0f;
     if (SRC == 0) {
@@ -1118,10 +1127,10 @@ __global__ void __launch_bounds__(kDecThreads) decide_kernel(DecideParams p) {
         for (int r = 0; r < p.nranks; ++r)
             sum += p.rank_sums[r];
         if (sum > 0.0) {
-            const double f = __ddiv_rn((double)p.n_pixels, sum);
+            const double f = __ddiv_rn((double)p.n_pixels, sum);  // F = Npx / sum (rrs.cpp:17)
             if (f < 1.0) {
                 apply = true;
-                scale = __double2float_rn(f);
+                scale = __double2float_rn(f);  // s = float(F)  (rrs.cpp:19)
             }
             if (tile == 0 && tid == 0 && p.res)
                 p.res->f_norm = f;
@@ -1130,73 +1139,66 @@ __global__ void __launch_bounds__(kDecThreads) decide_kernel(DecideParams p) {
         }
     }
 
-    uint32_t k[kDecItems];
+    // ---- pass 1: factors -> counts (smem), q_norm / q_real out ----
+    uint32_t my_total = 0;
     uint32_t bad = 0;
-    if (SRC == 0) {
-        float q[kDecItems], u[kDecItems];
-        const bool full = first + kDecItems <= p.n;
-        if (full) {
-            const float4 *q4 = reinterpret_cast<const float4 *>(p.q + first);
-            const float4 *u4 = reinterpret_cast<const float4 *>(p.u + first);
-            const float4 qa = __ldcs(q4), qb = __ldcs(q4 + 1), ua = __ldcs(u4), ub = __ldcs(u4 + 1);
-            q[0] = qa.x; q[1] = qa.y; q[2] = qa.z; q[3] = qa.w; q[4] = qb.x; q[5] = qb.y; q[6] = qb.z; q[7] = qb.w;
-            u[0] = ua.x; u[1] = ua.y; u[2] = ua.z; u[3] = ua.w; u[4] = ub.x; u[5] = ub.y; u[6] = ub.z; u[7] = ub.w;
+#pragma unroll 1
+    for (int sub = 0; sub < kBSubs; ++sub) {
+        const uint64_t first = tbase + (uint64_t)sub * kBSub + (uint64_t)tid * kBItems;
+        uint32_t k[kBItems];
+        if (SRC == 0) {
+            float q[kBItems], u[kBItems];
+            const bool full = first + kBItems <= p.n;
+            if (full) {
+                const float4 qa = __ldcs(reinterpret_cast<const float4 *>(p.q + first));
+                const float4 ua = __ldcs(reinterpret_cast<const float4 *>(p.u + first));
+                q[0] = qa.x; q[1] = qa.y; q[2] = qa.z; q[3] = qa.w;
+                u[0] = ua.x; u[1] = ua.y; u[2] = ua.z; u[3] = ua.w;
+            } else {
+#pragma unroll
+                for (int i = 0; i < kBItems; ++i) {
+                    const bool ok = first + i < p.n;
+                    q[i] = ok ? p.q[first + i] : 0.0f;
+                    u[i] = ok ? p.u[first + i] : 0.0f;
+                }
+            }
+            float qn[kBItems], qr[kBItems];
+#pragma unroll
+            for (int i = 0; i < kBItems; ++i) {
+                qn[i] = apply ? __fmul_rn(q[i], scale) : q[i];  // q *= float(F)  (rrs.cpp:18-21)
+                qr[i] = __fmul_rn(qn[i], p.gain);               // q_real = q * gain (wavefront.cpp:396)
+                k[i] = stochastic_round(qr[i], u[i]);           // (rrs.cpp:35-45)
+            }
+            if (full) {
+                __stcs(reinterpret_cast<float4 *>(p.q_norm + first), make_float4(qn[0], qn[1], qn[2], qn[3]));
+                __stcs(reinterpret_cast<float4 *>(p.q_real + first), make_float4(qr[0], qr[1], qr[2], qr[3]));
+            } else {
+#pragma unroll
+                for (int i = 0; i < kBItems; ++i)
+                    if (first + i < p.n) {
+                        p.q_norm[first + i] = qn[i];
+                        p.q_real[first + i] = qr[i];
+                    }
+            }
         } else {
 #pragma unroll
-            for (int i = 0; i < kDecItems; ++i) {
-                const bool ok = first + i < p.n;
-                q[i] = ok ? p.q[first + i] : 0.0f;
-                u[i] = ok ? p.u[first + i] : 0.0f;
+            for (int i = 0; i < kBItems; ++i) {
+                const int32_t c = first + i < p.n ? p.counts_in[first + i] : 0;
+                if (c < 0)
+                    bad = 1;
+                k[i] = c < 0 ? 0u : (uint32_t)c;
             }
         }
-        float qn[kDecItems], qr[kDecItems];
 #pragma unroll
-        for (int i = 0; i < kDecItems; ++i) {
-            qn[i] = apply ? __fmul_rn(q[i], scale) : q[i];  // q *= float(F)  (rrs.cpp:18-21)
-            qr[i] = __fmul_rn(qn[i], p.gain);               // q_real = q * gain (wavefront.cpp:396)
-            k[i] = stochastic_round(qr[i], u[i]);
-        }
-        if (full) {
-            float4 *o1 = reinterpret_cast<float4 *>(p.q_norm + first);
-            float4 *o2 = reinterpret_cast<float4 *>(p.q_real + first);
-            __stcs(o1, make_float4(qn[0], qn[1], qn[2], qn[3]));
-            __stcs(o1 + 1, make_float4(qn[4], qn[5], qn[6], qn[7]));
-            __stcs(o2, make_float4(qr[0], qr[1], qr[2], qr[3]));
-            __stcs(o2 + 1, make_float4(qr[4], qr[5], qr[6], qr[7]));
-        } else {
-#pragma unroll
-            for (int i = 0; i < kDecItems; ++i)
-                if (first + i < p.n) {
-                    p.q_norm[first + i] = qn[i];
-                    p.q_real[first + i] = qr[i];
-                }
-        }
-    } else {
-#pragma unroll
-        for (int i = 0; i < kDecItems; ++i) {
-            const int32_t c = first + i < p.n ? p.counts_in[first + i] : 0;
-            if (c < 0)
-                bad = 1;
-            k[i] = c < 0 ? 0u : (uint32_t)c;
+        for (int i = 0; i < kBItems; ++i) {
+            sm.k[sub * kBSub + tid * kBItems + i] = k[i];
+            my_total += k[i];
         }
     }
     if (bad)
         atomicOr(p.err_flag, 1u);
-
-    uint32_t tsum = 0;
-#pragma unroll
-    for (int i = 0; i < kDecItems; ++i)
-        tsum += k[i];
     uint32_t agg = 0;
-    const uint32_t texcl = block_exclusive_scan(tsum, sm.warp_tot, agg);
-    {
-        uint32_t run = texcl;
-#pragma unroll
-        for (int i = 0; i < kDecItems; ++i) {
-            run += k[i];
-            sm.incl[tid * kDecItems + i] = run;
-        }
-    }
+    block_scan_excl<kBT>(my_total, sm.warp_tot, agg);
     if (tid < 32) {
         const uint64_t ex = lookback_warp(p.tile_state, tile, agg, p.epoch);
         if (tid == 0)
@@ -1206,39 +1208,62 @@ __global__ void __launch_bounds__(kDecThreads) decide_kernel(DecideParams p) {
     const uint64_t P = sm.prefix;
     const uint64_t cap = p.capacity;
 
-    if (p.offset || p.k_out) {
-        uint64_t cum = P + texcl;
+    // ---- pass 2: offsets and slot records, sub-tile by sub-tile ----
+    uint64_t sub_base = P;
+#pragma unroll 1
+    for (int sub = 0; sub < kBSubs; ++sub) {
+        const uint64_t first = tbase + (uint64_t)sub * kBSub + (uint64_t)tid * kBItems;
+        uint32_t k[kBItems], ts = 0;
 #pragma unroll
-        for (int i = 0; i < kDecItems; ++i) {
-            if (first + i < p.n) {
-                if (p.offset)
-                    p.offset[first + i] = (uint32_t)(cum < cap ? cum : cap);  // min(cum, capacity)
-                if (p.k_out)
-                    p.k_out[first + i] = (int32_t)k[i];
-            }
-            cum += k[i];
+        for (int i = 0; i < kBItems; ++i) {
+            k[i] = sm.k[sub * kBSub + tid * kBItems + i];
+            ts += k[i];
         }
-    }
-
-    // slot records: slot s in [min(P,cap), min(P+agg,cap)) -> (parent j, child c)
-    // (kept = min(k, cap - min(cum, cap)), wavefront.cpp:421-425, :436)
-    if (p.slots && P < cap) {
-        const uint64_t s_end64 = P + agg < cap ? P + agg : cap;
-        const uint32_t s_count = (uint32_t)(s_end64 - P);
-        uint2 *slots = reinterpret_cast<uint2 *>(p.slots);
-        for (uint32_t local = tid; local < s_count; local += kDecThreads) {
-            // first item whose inclusive prefix exceeds `local`
-            uint32_t lo = 0, hi = kDecTile;
-            while (lo < hi) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if (sm.incl[mid] > local)
-                    hi = mid;
-                else
-                    lo = mid + 1;
+        uint32_t sagg = 0;
+        const uint32_t texcl = block_scan_excl<kBT>(ts, sm.warp_tot, sagg);
+        {
+            uint32_t run = texcl;
+#pragma unroll
+            for (int i = 0; i < kBItems; ++i) {
+                run += k[i];
+                sm.incl[tid * kBItems + i] = run;
             }
-            const uint32_t before = lo ? sm.incl[lo - 1] : 0u;
-            __stcs(slots + P + local, make_uint2((uint32_t)(base + lo) + p.parent_base, local - before));
         }
+        if (p.offset || p.k_out) {
+            uint64_t cum = sub_base + texcl;
+#pragma unroll
+            for (int i = 0; i < kBItems; ++i) {
+                if (first + i < p.n) {
+                    if (p.offset)
+                        p.offset[first + i] = (uint32_t)(cum < cap ? cum : cap);  // min(cum, capacity)
+                    if (p.k_out)
+                        p.k_out[first + i] = (int32_t)k[i];
+                }
+                cum += k[i];
+            }
+        }
+        __syncthreads();
+        // slot s in [min(B,cap), min(B+sagg,cap)) -> (parent j, child c)  (wavefront.cpp:421-425, :436)
+        if (p.slots && sub_base < cap) {
+            const uint64_t s_end64 = sub_base + sagg < cap ? sub_base + sagg : cap;
+            const uint32_t s_count = (uint32_t)(s_end64 - sub_base);
+            uint2 *slots = reinterpret_cast<uint2 *>(p.slots);
+            const uint32_t jbase = (uint32_t)(tbase + (uint64_t)sub * kBSub) + p.parent_base;
+            for (uint32_t local = tid; local < s_count; local += kBT) {
+                uint32_t lo = 0, hi = kBSub;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (sm.incl[mid] > local)
+                        hi = mid;
+                    else
+                        lo = mid + 1;
+                }
+                const uint32_t before = lo ? sm.incl[lo - 1] : 0u;
+                __stcs(slots + sub_base + local, make_uint2(jbase + lo, local - before));
+            }
+        }
+        sub_base += sagg;
+        __syncthreads();
     }
 
     if (tile == p.num_tiles - 1 && tid == 0) {
@@ -1255,60 +1280,75 @@ __global__ void __launch_bounds__(kDecThreads) decide_kernel(DecideParams p) {
     }
 }
 
-// ===========================================================================
-// K-C: stable compaction of W-word records
-// ===========================================================================
 template <int W, int IPT>
-__global__ void __launch_bounds__(kDecThreads) compact_kernel(CompactParams p) {
-    constexpr int kTile = kDecThreads * IPT;
-    __shared__ uint32_t stage[kTile * W];
-    __shared__ uint32_t warp_tot[kDecThreads / 32];
-    __shared__ uint64_t prefix_s;
-    __shared__ uint32_t tile_s;
+__global__ void __launch_bounds__(kBT) compact2_kernel(CompactParams p) {
+    constexpr int kSub = kBT * IPT;
+    constexpr int kTile = kSub * kBSubs;
+    extern __shared__ __align__(16) uint8_t csm[];
+    uint32_t *stage = reinterpret_cast<uint32_t *>(csm);              // kSub * W words
+    uint8_t *masks = csm + (size_t)kSub * W * 4;                      // kBSubs * kBT bytes
+    uint32_t *warp_tot = reinterpret_cast<uint32_t *>(masks + kBSubs * kBT);
+    unsigned long long *prefix = reinterpret_cast<unsigned long long *>(warp_tot + kBT / 32 + 2);
+    uint32_t *tile_s = reinterpret_cast<uint32_t *>(prefix + 1);
     const int tid = threadIdx.x;
     if (tid == 0)
-        tile_s = claim_tile(p.tile_counter, p.num_tiles);
+        *tile_s = claim_tile(p.tile_counter, p.num_tiles);
     __syncthreads();
-    const uint32_t tile = tile_s;
-    const uint64_t base = (uint64_t)tile * kTile;
-    const uint64_t first = base + (uint64_t)tid * IPT;
+    const uint32_t tile = *tile_s;
+    const uint64_t tbase = (uint64_t)tile * kTile;
     uint64_t count = p.count;
     if (p.count_in) {
         const uint64_t c = *p.count_in;
         count = c < count ? c : count;
     }
-    uint32_t keep[IPT];
-    uint32_t cnt = 0;
+    // pass 1: flags -> per-thread masks, tile count
+    uint32_t my_cnt = 0;
+#pragma unroll 1
+    for (int sub = 0; sub < kBSubs; ++sub) {
+        const uint64_t first = tbase + (uint64_t)sub * kSub + (uint64_t)tid * IPT;
+        uint32_t m = 0;
 #pragma unroll
-    for (int i = 0; i < IPT; ++i) {
-        keep[i] = (first + i < count && p.used[first + i]) ? 1u : 0u;
-        cnt += keep[i];
+        for (int i = 0; i < IPT; ++i)
+            if (first + i < count && p.used[first + i])
+                m |= 1u << i;
+        masks[sub * kBT + tid] = (uint8_t)m;
+        my_cnt += __popc(m);
     }
     uint32_t agg = 0;
-    const uint32_t excl = block_exclusive_scan(cnt, warp_tot, agg);
+    block_scan_excl<kBT>(my_cnt, warp_tot, agg);
     if (tid < 32) {
         const uint64_t ex = lookback_warp(p.tile_state, tile, agg, p.epoch);
         if (tid == 0)
-            prefix_s = ex;
-    }
-    const uint32_t *in = reinterpret_cast<const uint32_t *>(p.in);
-    uint32_t pos = excl;
-#pragma unroll
-    for (int i = 0; i < IPT; ++i) {
-        if (keep[i]) {
-#pragma unroll
-            for (int w = 0; w < W; ++w)
-                stage[pos * W + w] = __ldcs(in + (first + i) * W + w);
-            ++pos;
-        }
+            *prefix = ex;
     }
     __syncthreads();
-    const uint64_t P = prefix_s;
-    uint32_t *out = reinterpret_cast<uint32_t *>(p.out) + P * W;
-    for (uint32_t w = tid; w < agg * W; w += kDecThreads)
-        __stcs(out + w, stage[w]);
+    uint64_t out_base = *prefix;
+    const uint32_t *in = reinterpret_cast<const uint32_t *>(p.in);
+    // pass 2: stage kept records of each sub-tile in smem, write them coalesced
+#pragma unroll 1
+    for (int sub = 0; sub < kBSubs; ++sub) {
+        const uint64_t first = tbase + (uint64_t)sub * kSub + (uint64_t)tid * IPT;
+        const uint32_t m = masks[sub * kBT + tid];
+        uint32_t sagg = 0;
+        uint32_t pos = block_scan_excl<kBT>(__popc(m), warp_tot, sagg);
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+            if (m & (1u << i)) {
+#pragma unroll
+                for (int w = 0; w < W; ++w)
+                    stage[pos * W + w] = __ldcs(in + (first + i) * W + w);
+                ++pos;
+            }
+        }
+        __syncthreads();
+        uint32_t *out = reinterpret_cast<uint32_t *>(p.out) + out_base * W;
+        for (uint32_t w = tid; w < sagg * W; w += kBT)
+            __stcs(out + w, stage[w]);
+        out_base += sagg;
+        __syncthreads();
+    }
     if (tile == p.num_tiles - 1 && tid == 0)
-        *p.count_out = (uint32_t)(P + agg);
+        *p.count_out = (uint32_t)(*prefix + agg);
 }
 
 // ===========================================================================
@@ -1485,32 +1525,51 @@ cudaError_t launch_infer(int kind, const InferParams &p, int num_sms, cudaStream
 
 uint32_t infer_max_grid(int num_sms) { return (uint32_t)num_sms * 16u; }
 
-uint32_t decide_tiles(uint64_t n) { return (uint32_t)((n + kDecTile - 1) / kDecTile); }
+uint32_t decide_tiles(uint64_t n) { return (uint32_t)((n + kBTile - 1) / kBTile); }
 
 cudaError_t launch_decide(int src, const DecideParams &p, cudaStream_t stream) {
     if (p.num_tiles == 0)
         return cudaSuccess;
-    if (src == 0)
-        decide_kernel<0><<<p.num_tiles, kDecThreads, 0, stream>>>(p);
-    else
-        decide_kernel<1><<<p.num_tiles, kDecThreads, 0, stream>>>(p);
+    const size_t smem = sizeof(Decide2Smem);
+    cudaError_t e;
+    if (src == 0) {
+        e = cudaFuncSetAttribute(decide2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess)
+            return e;
+        decide2_kernel<0><<<p.num_tiles, kBT, smem, stream>>>(p);
+    } else {
+        e = cudaFuncSetAttribute(decide2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess)
+            return e;
+        decide2_kernel<1><<<p.num_tiles, kBT, smem, stream>>>(p);
+    }
     return cudaGetLastError();
 }
 
+template <int W, int IPT>
+static size_t compact2_smem() {
+    return (size_t)kBT * IPT * W * 4 + kBSubs * kBT + (kBT / 32 + 2) * 4 + 16 + 16;
+}
+
 uint32_t compact_tiles(uint64_t count, uint32_t words) {
-    const uint32_t tile = words == 2 ? kDecThreads * 8 : kDecThreads * 1;
+    const uint64_t tile = words == 2 ? (uint64_t)kBT * 4 * kBSubs : (uint64_t)kBT * 1 * kBSubs;
     return (uint32_t)((count + tile - 1) / tile);
 }
 
 cudaError_t launch_compact(uint32_t words, const CompactParams &p, cudaStream_t stream) {
     if (p.num_tiles == 0)
         return cudaSuccess;
-    if (words == 2)
-        compact_kernel<2, 8><<<p.num_tiles, kDecThreads, 0, stream>>>(p);
-    else if (words == 18)
-        compact_kernel<18, 1><<<p.num_tiles, kDecThreads, 0, stream>>>(p);
-    else
+    if (words == 2) {
+        const size_t smem = compact2_smem<2, 4>();
+        cudaFuncSetAttribute(compact2_kernel<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        compact2_kernel<2, 4><<<p.num_tiles, kBT, smem, stream>>>(p);
+    } else if (words == 18) {
+        const size_t smem = compact2_smem<18, 1>();
+        cudaFuncSetAttribute(compact2_kernel<18, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        compact2_kernel<18, 1><<<p.num_tiles, kBT, smem, stream>>>(p);
+    } else {
         return cudaErrorInvalidValue;
+    }
     return cudaGetLastError();
 }
 
