@@ -1142,7 +1142,7 @@ __global__ void __launch_bounds__(kBT) decide2_kernel(DecideParams p) {
     // ---- pass 1: factors -> counts (smem), q_norm / q_real out ----
     uint32_t my_total = 0;
     uint32_t bad = 0;
-#pragma unroll 1
+#pragma unroll
     for (int sub = 0; sub < kBSubs; ++sub) {
         const uint64_t first = tbase + (uint64_t)sub * kBSub + (uint64_t)tid * kBItems;
         uint32_t k[kBItems];
@@ -1229,37 +1229,26 @@ __global__ void __launch_bounds__(kBT) decide2_kernel(DecideParams p) {
                 sm.incl[tid * kBItems + i] = run;
             }
         }
-        if (p.offset || p.k_out) {
+        {
+            // offsets (wavefront.cpp:148) and this thread's slot records: child c of
+            // item j lands in slot cum + c while cum + c < capacity (:421-425, :436)
             uint64_t cum = sub_base + texcl;
+            uint2 *slots = reinterpret_cast<uint2 *>(p.slots);
 #pragma unroll
             for (int i = 0; i < kBItems; ++i) {
-                if (first + i < p.n) {
+                const uint64_t j = first + i;
+                if (j < p.n) {
                     if (p.offset)
-                        p.offset[first + i] = (uint32_t)(cum < cap ? cum : cap);  // min(cum, capacity)
+                        p.offset[j] = (uint32_t)(cum < cap ? cum : cap);  // min(cum, capacity)
                     if (p.k_out)
-                        p.k_out[first + i] = (int32_t)k[i];
+                        p.k_out[j] = (int32_t)k[i];
+                    if (p.slots) {
+                        const uint64_t kept64 = cum < cap ? (cap - cum < k[i] ? cap - cum : k[i]) : 0;
+                        for (uint32_t c = 0; c < (uint32_t)kept64; ++c)
+                            __stcs(slots + cum + c, make_uint2((uint32_t)j + p.parent_base, c));
+                    }
                 }
                 cum += k[i];
-            }
-        }
-        __syncthreads();
-        // slot s in [min(B,cap), min(B+sagg,cap)) -> (parent j, child c)  (wavefront.cpp:421-425, :436)
-        if (p.slots && sub_base < cap) {
-            const uint64_t s_end64 = sub_base + sagg < cap ? sub_base + sagg : cap;
-            const uint32_t s_count = (uint32_t)(s_end64 - sub_base);
-            uint2 *slots = reinterpret_cast<uint2 *>(p.slots);
-            const uint32_t jbase = (uint32_t)(tbase + (uint64_t)sub * kBSub) + p.parent_base;
-            for (uint32_t local = tid; local < s_count; local += kBT) {
-                uint32_t lo = 0, hi = kBSub;
-                while (lo < hi) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    if (sm.incl[mid] > local)
-                        hi = mid;
-                    else
-                        lo = mid + 1;
-                }
-                const uint32_t before = lo ? sm.incl[lo - 1] : 0u;
-                __stcs(slots + sub_base + local, make_uint2(jbase + lo, local - before));
             }
         }
         sub_base += sagg;
@@ -1303,7 +1292,7 @@ __global__ void __launch_bounds__(kBT) compact2_kernel(CompactParams p) {
     }
     // pass 1: flags -> per-thread masks, tile count
     uint32_t my_cnt = 0;
-#pragma unroll 1
+#pragma unroll
     for (int sub = 0; sub < kBSubs; ++sub) {
         const uint64_t first = tbase + (uint64_t)sub * kSub + (uint64_t)tid * IPT;
         uint32_t m = 0;
