@@ -34,6 +34,12 @@ sys.path.insert(0, ROOT)
 METRIC = "path vertices/sec (RRSNet+normalized RRS+compaction) at 1/2/4/8 B200"
 N_LOCAL = 1920 * 1080
 ALG_BYTES_INFER = 56 + 8   # K-A: reads p01 12, wo01 8, rough 4, t_x 12, i_pixel 12, key 8; writes q_orig 4 + u 4
+# K-A's binding resource is L2 scattered-gather throughput: hash-grid gathers per vertex
+# in 8-byte-gather equivalents (a 16-byte gather costs 1.28, measured): 7 hashed levels x (4 edge pairs x 1.28
+# + 0.5 unpaired) + dense level 0 (4 x 1.28); ceiling = 296 G/s random 8-byte gathers from a 2 MiB table
+# (profiles/r01_microbench_gather_bw.txt, tools/gather_bw.cu).
+GATHER_UNITS_PER_VERTEX = 7 * (4 * 1.28 + 0.5) + 4 * 1.28
+GATHER_CEILING_PER_S = 296e9
 STAGE_READ, STAGE_WRITE = 56, 8  # SURVEY.md 8d per-vertex compulsory bytes (+ 8 B per spawned slot record)
 
 
@@ -376,6 +382,11 @@ def main():
                      "traffic": traffic, "kernel": f"infer_kernel<{'Aid' if args.variant == 'aid' else 'Nrrs'}>",
                      "alg_bytes_per_vertex": ALG_BYTES_INFER, "peak_source": peak_src,
                      "stage_frac": (stage_bytes / (statistics.mean(step_ms) / 1e3) / 1e9) / hbm},
+        "gather_roofline": {"bound": "l2_scattered_gathers", "unit": "gathers/s (8-byte equivalents)",
+                            "achieved": GATHER_UNITS_PER_VERTEX * n / infer_avg, "peak": GATHER_CEILING_PER_S,
+                            "frac": GATHER_UNITS_PER_VERTEX * n / infer_avg / GATHER_CEILING_PER_S,
+                            "units_per_vertex": GATHER_UNITS_PER_VERTEX,
+                            "peak_source": "measured, profiles/r01_microbench_gather_bw.txt"},
         "kernels_ms": {"infer": statistics.mean(infer_ms), "decide": statistics.mean(decide_ms),
                        "compact": statistics.mean(compact_ms)},
         "clocks": clk.summary(),
