@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--variant", default="aid", choices=["aid", "nrrs"])
-    ap.add_argument("--n", type=int, default=N_LOCAL)
+    ap.add_argument("--vertices", type=int, default=N_LOCAL, help="vertices per rank")
     ap.add_argument("--no-extra", action="store_true", help="skip the per-strategy side measurements")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     return ap.parse_args()
@@ -164,7 +164,7 @@ def run_reference(args):
     var = orc.VARIANT_AID if args.variant == "aid" else orc.VARIANT_NRRS
     kind = orc.AID_NRRS if args.variant == "aid" else orc.NRRS
     nets = orc.OracleNets(var, seed=1, randomize=True)
-    sample = args.n
+    sample = args.vertices
     v = orc.gen_vertices(sample)
     cap = orc.lib().orc_queue_capacity_for(sample)
     times = []
@@ -180,7 +180,7 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{args.variant}-nrrs stage, 1920x1080 synthetic vertices at depth 2 "
                                    f"(full batch each step)",
-                       "n_pixels": args.n, "strategy": f"{args.variant}-nrrs", "depth": 2},
+                       "n_pixels": args.vertices, "strategy": f"{args.variant}-nrrs", "depth": 2},
             "cpu_baseline": {"value": value, "unit": "vertices/s", "cores": threads, "kind": "port",
                              "sample": f"the full {sample}-vertex batch per step; the reference does not build here "
                                        "(Eigen absent): C restatement of the reference path"},
@@ -207,11 +207,18 @@ def main():
     from paper_2510_07868_b200.sharded import ShardedRrsStage
 
     world, rank, local = dist_env()
+    # test-only knobs: run N ranks on one device with gloo exchanges (functional check of the N>1 path)
+    backend = os.environ.get("NRRS_BENCH_BACKEND", "nccl")
+    if os.environ.get("NRRS_BENCH_SAME_DEVICE"):
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend, init_method="env://")
     dev = torch.device("cuda", local)
-    n = args.n
+    n = args.vertices
     npx = n * world
     cap = queue_capacity_for(npx)
     variant = RrsVariant.Aid if args.variant == "aid" else RrsVariant.Nrrs
@@ -300,9 +307,9 @@ def main():
     decide_ms = [e[1].elapsed_time(e[2]) for e in evs]
     compact_ms = [e[2].elapsed_time(e[3]) for e in evs]
     total_s = sum(step_ms) / 1e3
-    t = torch.tensor([total_s], dtype=torch.float64, device=dev)
+    t = torch.tensor([total_s], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)  # max over ranks
     total_s = float(t.item())
     value = world * n * args.steps / total_s
     res = _capi.StageResultC()
@@ -318,18 +325,48 @@ def main():
                 "q_real": torch.empty(n, dtype=torch.float32).pin_memory().numpy(),
                 "slots": torch.empty((slot_cap, 2), dtype=torch.int32).pin_memory().numpy().view(np.uint32)}
         for _ in range(3):
-            stage.run_host(pinned, 2, strategy, rc=None, out=hout)
+            stage.run_host(pinned, 2, strategy, rc=RateControl(), out=hout)
         torch.cuda.synchronize()
         e_times, d2h = [], 0
         for _ in range(max(3, args.steps // 2)):
             flush.zero_()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            _, r = stage.run_host(pinned, 2, strategy, rc=None, out=hout)
+            _, r = stage.run_host(pinned, 2, strategy, rc=RateControl(), out=hout)
             e_times.append(time.perf_counter() - t0)
             d2h = 8 * n + 8 * r.spawned
         e2e = {"value": n / statistics.mean(e_times), "unit": "vertices/s", "h2d_bytes_per_step": 56 * n,
                "d2h_bytes_per_step": d2h, "path": "nrrs_gpu_rrs_stage_host (pinned host buffers)"}
+    else:
+        # N>1: each rank copies its band in from pinned host memory, runs the sharded stage (two
+        # exchanges) and reads q_norm/q_real and its kept slot records back; max over ranks.
+        pinned_t = {k: torch.from_numpy(a.view(np.int64) if a.dtype == np.uint64 else a).pin_memory()
+                    for k, a in hv.items() if k != "pixel"}
+        hq = torch.empty(n, dtype=torch.float32).pin_memory()
+        hr = torch.empty(n, dtype=torch.float32).pin_memory()
+        hs = torch.empty((slot_cap, 2), dtype=torch.int32).pin_memory()
+        e_tot, e_steps, d2h = 0.0, max(3, args.steps // 2), 0
+        for i in range(3 + e_steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            for k in dv:
+                dv[k].copy_(pinned_t[k], non_blocking=True)
+            _, oc_ = sh.run(dv, 2, strategy, rc=RateControl(), out=out)
+            hq.copy_(out.q_norm, non_blocking=True)
+            hr.copy_(out.q_real, non_blocking=True)
+            if oc_.kept:
+                hs[:oc_.kept].copy_(out.slots[:oc_.kept], non_blocking=True)
+            torch.cuda.synchronize()
+            if i >= 3:
+                e_tot += time.perf_counter() - t0
+            d2h = 8 * n + 8 * oc_.kept
+        te = torch.tensor([e_tot], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * n * e_steps / float(te.item()), "unit": "vertices/s",
+               "h2d_bytes_per_step": 56 * n, "d2h_bytes_per_step": d2h,
+               "path": "ShardedRrsStage.run per rank (pinned host buffers, per-rank bytes, max over ranks)"}
 
     # ---- side measurements: other strategies (Mix-Depth candidates) on the same batch ----
     extra = {}
@@ -379,7 +416,7 @@ def main():
                    "depth": 2, "gain": 0.85, "parallelism": f"tile-sharded dp{world}",
                    "l2": "flushed between timed steps (256 MiB write outside the events)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": traffic, "kernel": f"infer_kernel<{'Aid' if args.variant == 'aid' else 'Nrrs'}>",
+                     "traffic": traffic, "kernel": f"infer_ws_kernel<{'Aid' if args.variant == 'aid' else 'Nrrs'}> (warp-specialized, 2 encoder + 3 MLP groups)",
                      "alg_bytes_per_vertex": ALG_BYTES_INFER, "peak_source": peak_src,
                      "stage_frac": (stage_bytes / (statistics.mean(step_ms) / 1e3) / 1e9) / hbm},
         "gather_roofline": {"bound": "l2_scattered_gathers", "unit": "gathers/s (8-byte equivalents)",

@@ -67,12 +67,15 @@ def sharded_depth(local_sum: torch.Tensor, decide: Callable[[torch.Tensor], torc
     rank's [1] int64 realized total."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    sums = [torch.zeros_like(local_sum) for _ in range(world)]
-    dist.all_gather(sums, local_sum, group=group)
-    rank_sums_t = torch.cat(sums)
+    host = dist.get_backend(group) == "gloo" and local_sum.is_cuda  # gloo exchanges host copies
+    src = local_sum.cpu() if host else local_sum
+    sums = [torch.zeros_like(src) for _ in range(world)]
+    dist.all_gather(sums, src, group=group)
+    rank_sums_t = torch.cat(sums).to(local_sum.device)
     local_total = decide(rank_sums_t)
-    totals = [torch.zeros_like(local_total) for _ in range(world)]
-    dist.all_gather(totals, local_total, group=group)
+    src = local_total.cpu() if host else local_total
+    totals = [torch.zeros_like(src) for _ in range(world)]
+    dist.all_gather(totals, src, group=group)
     tot = [int(t.item()) for t in totals]
     base, kept, spawned, dropped = global_clip(tot, rank, capacity)
     if rc is not None and dropped > 0:
