@@ -336,7 +336,29 @@ def main():
             e_times.append(time.perf_counter() - t0)
             d2h = 8 * n + 8 * r.spawned
         e2e = {"value": n / statistics.mean(e_times), "unit": "vertices/s", "h2d_bytes_per_step": 56 * n,
-               "d2h_bytes_per_step": d2h, "path": "nrrs_gpu_rrs_stage_host (pinned host buffers)"}
+               "d2h_bytes_per_step": d2h, "path": "nrrs_gpu_rrs_stage_host (pinned host buffers, chunked H2D "
+                                                 "overlapped with K-A)"}
+        # the floor e2e can reach: the step's bytes over the measured pinned copy bandwidths (H2D and D2H
+        # cannot overlap inside one call -- q_norm needs the global F)
+        hb = torch.empty(56 * n, dtype=torch.uint8).pin_memory()
+        hb.fill_(1)  # touch the pages (an untouched pinned buffer copies at ~35 GB/s)
+        db = torch.empty(56 * n, dtype=torch.uint8, device=dev)
+        bw = {}
+        for name, dst, src in (("h2d", db, hb), ("d2h", hb, db)):
+            for _ in range(2):
+                dst.copy_(src, non_blocking=True)
+            a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(5):
+                dst.copy_(src, non_blocking=True)
+            z.record()
+            torch.cuda.synchronize()
+            bw[name] = 5 * 56 * n / (a.elapsed_time(z) / 1e3)
+        floor_s = 56 * n / bw["h2d"] + d2h / bw["d2h"]
+        e2e["copy_gbs"] = {k: v / 1e9 for k, v in bw.items()}
+        e2e["pcie_floor"] = n / floor_s
+        e2e["frac_of_floor"] = e2e["value"] / e2e["pcie_floor"]
+        del hb, db
     else:
         # N>1: each rank copies its band in from pinned host memory, runs the sharded stage (two
         # exchanges) and reads q_norm/q_real and its kept slot records back; max over ranks.

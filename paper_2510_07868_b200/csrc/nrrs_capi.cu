@@ -143,6 +143,9 @@ struct DeviceBlob {
     KernelNets nets{};
 };
 
+static constexpr int kMaxHostChunks = 8;
+static constexpr uint32_t kChunkSums = 8;  // d_sum[8 ..] : per-chunk sums of the host path
+
 struct nrrs_gpu_ctx {
     int device = 0;
     int num_sms = 148;
@@ -174,6 +177,11 @@ struct nrrs_gpu_ctx {
     double *d_sum = nullptr;            // [0] local sum  [1] scratch sum
     unsigned long long *d_total = nullptr;
     uint32_t decide_epoch = 0, compact_epoch = 0;
+
+    // host-path pipeline: chunked H2D on copy_stream overlapped with K-A on `stream`
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_start = nullptr;
+    cudaEvent_t ev_chunk[kMaxHostChunks] = {};
 
     // host-path device staging
     struct Staging {
@@ -279,14 +287,14 @@ int nrrs_gpu_create(int device, nrrs_gpu_ctx **out) {
     cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (cudaMalloc(&ctx->d_misc, 16 * sizeof(uint32_t)) != cudaSuccess ||
         cudaMalloc(&ctx->d_res, sizeof(DevResult)) != cudaSuccess ||
-        cudaMalloc(&ctx->d_sum, 4 * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&ctx->d_sum, (kChunkSums + kMaxHostChunks) * sizeof(double)) != cudaSuccess ||
         cudaMalloc(&ctx->d_total, 4 * sizeof(unsigned long long)) != cudaSuccess) {
         delete ctx;
         return NRRS_ECUDA;
     }
     cudaMemset(ctx->d_misc, 0, 16 * sizeof(uint32_t));
     cudaMemset(ctx->d_res, 0, sizeof(DevResult));
-    cudaMemset(ctx->d_sum, 0, 4 * sizeof(double));
+    cudaMemset(ctx->d_sum, 0, (kChunkSums + kMaxHostChunks) * sizeof(double));
     *out = ctx;
     return NRRS_OK;
 }
@@ -304,6 +312,13 @@ int nrrs_gpu_destroy(nrrs_gpu_ctx *ctx) {
     for (void *p : ptrs)
         if (p)
             cudaFree(p);
+    if (ctx->copy_stream) {
+        cudaStreamSynchronize(ctx->copy_stream);
+        cudaStreamDestroy(ctx->copy_stream);
+        cudaEventDestroy(ctx->ev_start);
+        for (cudaEvent_t e : ctx->ev_chunk)
+            cudaEventDestroy(e);
+    }
     delete ctx;
     return NRRS_OK;
 }
@@ -535,7 +550,7 @@ static int check_soa(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, int kind) {
 }
 
 static int run_factors(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, const nrrs_stage_params *p,
-                       float *q_out, float *u_out, uint8_t *decided_out, double *sum_out) {
+                       float *q_out, float *u_out, uint8_t *decided_out, double *sum_out, bool accumulate = false) {
     int kind = 0, heur = 0;
     int rc = select_kind(ctx, p->depth, p->strategy, &kind, &heur);
     if (rc)
@@ -568,6 +583,7 @@ static int run_factors(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, 
     ip.counter = ctx->d_misc + 0;
     ip.sum_out = sum_out;
     ip.res = ctx->d_res;
+    ip.accumulate = accumulate ? 1u : 0u;
     if (const char *ab = std::getenv("NRRS_DEBUG_ABLATE"))  // diagnostics only; results invalid
         ip.ablate = (uint32_t)std::atoi(ab);
     if (const char *wc = std::getenv("NRRS_WS_CFG"))  // tuning sweeps only
@@ -1051,28 +1067,10 @@ int nrrs_gpu_rrs_stage_host(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *h, uint64_
         CK(ctx, cudaMalloc(&s.slots, (size_t)cap * 2 * sizeof(uint32_t)));
         s.cap_slots = cap;
     }
-    auto h2d = [&](void *dst, const void *src, size_t bytes) -> int {
-        if (src && bytes)
-            CK(ctx, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
-        return NRRS_OK;
-    };
     if (!h->i_pixel)
         return fail(ctx, NRRS_EINVAL, "stage_host: pass i_pixel (gathered per vertex)");
-    rc = h2d(s.p01, h->p01, n * 12);
-    if (!rc) rc = h2d(s.wo01, h->wo01, n * 8);
-    if (!rc) rc = h2d(s.rough, h->roughness, n * 4);
-    if (!rc) rc = h2d(s.weight, h->weight, n * 12);
-    if (!rc) rc = h2d(s.ipix, h->i_pixel, n * 12);
-    if (!rc) rc = h2d(s.key, h->path_key, n * 8);
-    if (rc)
-        return rc;
-    nrrs_vertex_soa dv{};
-    dv.p01 = s.p01;
-    dv.wo01 = h->wo01 ? s.wo01 : nullptr;
-    dv.roughness = h->roughness ? s.rough : nullptr;
-    dv.weight = s.weight;
-    dv.i_pixel = s.ipix;
-    dv.path_key = s.key;
+    if (n > 0xFFFFFFFFull)
+        return fail(ctx, NRRS_EINVAL, "stage: more than 2^32 vertices");
     nrrs_stage_out dout{};
     dout.q_norm = s.q_norm;
     dout.q_real = s.q_real;
@@ -1083,7 +1081,67 @@ int nrrs_gpu_rrs_stage_host(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *h, uint64_
     dout.q_orig = s.q_orig;
     dout.u = s.u;
     nrrs_stage_result r{};
-    rc = nrrs_gpu_rrs_stage(ctx, &dv, n, p, &dout, &r);  // syncs (needs spawned for the slot copy)
+    if (n == 0) {
+        rc = nrrs_gpu_rrs_stage(ctx, nullptr, 0, p, &dout, &r);
+        if (!rc && h_result)
+            *h_result = r;
+        return rc;
+    }
+    rc = ensure_scratch(ctx, n);
+    if (rc)
+        return rc;
+    // Pipeline: chunk c's H2D (copy_stream) overlaps K-A of chunks < c (stream).  Each chunk's K-A
+    // writes its own sum; K-B sums them in chunk order (the rank_sums input), so the result does not
+    // depend on how chunk launches were scheduled.  Chunks are whole 128-vertex tiles.
+    if (!ctx->copy_stream) {
+        CK(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+        CK(ctx, cudaEventCreateWithFlags(&ctx->ev_start, cudaEventDisableTiming));
+        for (cudaEvent_t &e : ctx->ev_chunk)
+            CK(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const uint64_t min_chunk = 1ull << 17;
+    uint64_t nc = n < 2 * min_chunk ? 1 : (n + min_chunk - 1) / min_chunk;
+    if (nc > (uint64_t)kMaxHostChunks)
+        nc = kMaxHostChunks;
+    const uint64_t chunk = ((n + nc - 1) / nc + 127) / 128 * 128;
+    nc = (n + chunk - 1) / chunk;
+    CK(ctx, cudaEventRecord(ctx->ev_start, ctx->stream));  // staging buffers free once prior work is done
+    CK(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_start, 0));
+    double *chunk_sums = ctx->d_sum + kChunkSums;
+    for (uint64_t c = 0; c < nc; ++c) {
+        const uint64_t base = c * chunk, cn = n - base < chunk ? n - base : chunk;
+        auto h2d = [&](void *dst, const void *src, size_t elem) -> int {
+            if (src)
+                CK(ctx, cudaMemcpyAsync(static_cast<uint8_t *>(dst) + base * elem,
+                                        static_cast<const uint8_t *>(src) + base * elem, cn * elem,
+                                        cudaMemcpyHostToDevice, ctx->copy_stream));
+            return NRRS_OK;
+        };
+        rc = h2d(s.p01, h->p01, 12);
+        if (!rc) rc = h2d(s.wo01, h->wo01, 8);
+        if (!rc) rc = h2d(s.rough, h->roughness, 4);
+        if (!rc) rc = h2d(s.weight, h->weight, 12);
+        if (!rc) rc = h2d(s.ipix, h->i_pixel, 12);
+        if (!rc) rc = h2d(s.key, h->path_key, 8);
+        if (rc)
+            return rc;
+        CK(ctx, cudaEventRecord(ctx->ev_chunk[c], ctx->copy_stream));
+        CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_chunk[c], 0));
+        nrrs_vertex_soa dv{};
+        dv.p01 = h->p01 ? s.p01 + 3 * base : nullptr;
+        dv.wo01 = h->wo01 ? s.wo01 + 2 * base : nullptr;
+        dv.roughness = h->roughness ? s.rough + base : nullptr;
+        dv.weight = h->weight ? s.weight + 3 * base : nullptr;
+        dv.i_pixel = s.ipix + 3 * base;
+        dv.path_key = h->path_key ? s.key + base : nullptr;
+        rc = run_factors(ctx, &dv, cn, p, s.q_orig + base, s.u + base, dout.decided ? dout.decided + base : nullptr,
+                         chunk_sums + c, c > 0);
+        if (rc) {
+            cudaStreamSynchronize(ctx->copy_stream);
+            return rc;
+        }
+    }
+    rc = run_decide(ctx, n, p, s.q_orig, s.u, chunk_sums, (int)nc, p->n_pixels, cap, &dout, ctx->d_total, ctx->d_res);
     if (rc)
         return rc;
     auto d2h = [&](void *dst, const void *src, size_t bytes) -> int {
@@ -1091,14 +1149,16 @@ int nrrs_gpu_rrs_stage_host(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *h, uint64_
             CK(ctx, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
         return NRRS_OK;
     };
+    // per-vertex outputs go back while the host waits for the spawned count
     rc = d2h(ho->q_norm, s.q_norm, n * 4);
     if (!rc) rc = d2h(ho->q_real, s.q_real, n * 4);
-    if (!rc) rc = d2h(ho->slots, s.slots, (size_t)r.spawned * 8);
     if (!rc) rc = d2h(ho->k, s.k, n * 4);
     if (!rc) rc = d2h(ho->offset, s.offset, n * 4);
     if (!rc) rc = d2h(ho->decided, s.decided, n);
     if (!rc) rc = d2h(ho->q_orig, s.q_orig, n * 4);
     if (!rc) rc = d2h(ho->u, s.u, n * 4);
+    if (!rc) rc = fetch_result(ctx, &r);
+    if (!rc) rc = d2h(ho->slots, s.slots, (size_t)r.spawned * 8);
     if (rc)
         return rc;
     CK(ctx, cudaStreamSynchronize(ctx->stream));

@@ -516,9 +516,15 @@ __global__ void __launch_bounds__(kInferThreads, 3) infer_kernel(InferParams p) 
             tb += hdr->warp_bc[w];
         }
         *p.sum_out = total;
-        p.res->sum_q = total;
-        p.res->nonfinite = tn;
-        p.res->box_cox_clamps = tb;
+        if (p.accumulate) {
+            p.res->sum_q += total;
+            p.res->nonfinite += tn;
+            p.res->box_cox_clamps += tb;
+        } else {
+            p.res->sum_q = total;
+            p.res->nonfinite = tn;
+            p.res->box_cox_clamps = tb;
+        }
         *p.counter = 0;  // self-cleaning for the next launch
     }
 }
@@ -1032,9 +1038,15 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
         bcs = __reduce_add_sync(0xffffffffu, bcs);
         if (lane == 0) {
             *p.sum_out = sv;
-            p.res->sum_q = sv;
-            p.res->nonfinite = nf;
-            p.res->box_cox_clamps = bcs;
+            if (p.accumulate) {
+                p.res->sum_q += sv;
+                p.res->nonfinite += nf;
+                p.res->box_cox_clamps += bcs;
+            } else {
+                p.res->sum_q = sv;
+                p.res->nonfinite = nf;
+                p.res->box_cox_clamps = bcs;
+            }
             *p.counter = 0;  // self-cleaning for the next launch
         }
     }

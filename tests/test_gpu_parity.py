@@ -293,3 +293,53 @@ def test_host_buffer_path_matches_device_path(c1_vertices, nets):
     assert hres.spawned == dres.spawned and hres.total == dres.total
     np.testing.assert_array_equal(host_out["q_norm"], _np(dev_out.q_norm))
     np.testing.assert_array_equal(host_out["slots"][:hres.spawned], _np(dev_out.slots)[:dres.spawned].view(np.uint32))
+
+
+@pytest.mark.parametrize("kind", [orc.THROUGHPUT, orc.FIXED])
+def test_host_buffer_pipeline_multi_chunk_bitexact(kind):
+    """nrrs_gpu_rrs_stage_host at a ragged size that splits into several pipelined chunks
+    (H2D of chunk c overlapping K-A of earlier chunks): bit-exact against the oracle.  NaN
+    throughputs in several chunks fail the luminance gate (q = 0, not counted as non-finite,
+    wavefront.cpp:376-385)."""
+    n = 700001
+    v = orc.gen_vertices(n)
+    v["weight"] = v["weight"].copy()
+    bad = np.array([5, 140000, 300001, 699999])  # lands in chunks 0, 1, 2, last
+    v["weight"][bad, 1] = np.nan
+    cap = queue_capacity_for(n)
+    ref = orc.rrs_stage(v, 2, n, cap, kind, None, fixed_value=1.5, gain=0.85, seed=11, threads=8)
+    st = _stage(n, seed=11)
+    hv = {k: np.ascontiguousarray(a) for k, a in v.items() if k != "pixel"}
+    out = {"q_norm": np.empty(n, np.float32), "q_real": np.empty(n, np.float32),
+           "slots": np.empty((cap, 2), np.uint32), "k": np.empty(n, np.int32),
+           "offset": np.empty(n, np.uint32), "decided": np.empty(n, np.uint8),
+           "q_orig": np.empty(n, np.float32), "u": np.empty(n, np.float32)}
+    out, res = st.run_host(hv, 2, Strategy(StrategyKind(kind), 1.5), rc=RateControl(), out=out)
+    for key in ("q_orig", "q_norm", "q_real", "u", "k", "decided"):
+        np.testing.assert_array_equal(out[key].view(ref[key].dtype), ref[key], err_msg=key)
+    np.testing.assert_array_equal(out["offset"], ref["offset"])
+    assert res.nonfinite == ref["nonfinite"] == 0
+    assert not out["decided"][bad].any() if kind == orc.THROUGHPUT else True
+    assert res.spawned == ref["spawned"] and res.dropped == ref["dropped"] and res.total == ref["total"]
+    assert np.float32(res.f_norm) == np.float32(ref["f_norm"])
+    assert abs(res.sum_q - ref["sum_q"]) <= 1e-9 * abs(ref["sum_q"])
+    np.testing.assert_array_equal(out["slots"][:res.spawned], ref["slots"][:res.spawned])
+
+
+def test_host_buffer_pipeline_multi_chunk_neural(nets):
+    """Multi-chunk host path with the neural stage equals the device path's decisions; NaN
+    pixel estimates in several chunks make non-finite factors, whose per-chunk counts must add up."""
+    n = 1000003
+    v = orc.gen_vertices(n)
+    v["i_pixel"] = v["i_pixel"].copy()
+    v["i_pixel"][7::99991] = np.nan
+    st = _stage(n, nets)
+    kind = StrategyKind.AidNrrs if nets.variant == orc.VARIANT_AID else StrategyKind.Nrrs
+    dev_out, dres = st.run(to_dev(v), 2, Strategy(kind), rc=RateControl())
+    hv = {k: np.ascontiguousarray(a) for k, a in v.items() if k != "pixel"}
+    host_out, hres = st.run_host(hv, 2, Strategy(kind), rc=RateControl())
+    assert np.float32(hres.f_norm) == np.float32(dres.f_norm)
+    assert hres.spawned == dres.spawned and hres.total == dres.total
+    assert hres.nonfinite == dres.nonfinite > 0
+    np.testing.assert_array_equal(host_out["q_norm"], _np(dev_out.q_norm))
+    np.testing.assert_array_equal(host_out["slots"][:hres.spawned], _np(dev_out.slots)[:dres.spawned].view(np.uint32))
