@@ -39,9 +39,10 @@ def build(force: bool = False, verbose: bool = False) -> pathlib.Path:
     build_dir = PKG / "build"
     build_dir.mkdir(exist_ok=True)
     log = []
+    extra = ["-DNRRS_KERNEL_TIMING"] if os.environ.get("NRRS_KERNEL_TIMING") else []  # diagnostics build only
     for src in SOURCES:
         obj = build_dir / (src + ".o")
-        cmd = [nvcc(), *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+        cmd = [nvcc(), *NVCC_FLAGS, *extra, "-c", str(CSRC / src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         log.append(r.stdout + r.stderr)
         if r.returncode != 0:

@@ -67,18 +67,18 @@ int mlp_param_count(int in, int out) {
 }
 
 // Packs one snapshot MLP theta (mlp.cpp:7-32 layout) into hi/lo fp16 canonical
-// tiles of [W | bias].  colmap[c] = kernel K column of reference input column c
-// (layer 0).  k0 = 16: the 11-input NRRS RRSNet layer, bias in column 11;
-// otherwise the data occupies K columns [0, 32) and the bias sits in column 32
-// of an extra ones slice.
+// tiles of W (W_lo right after W_hi: one [W_hi ; W_lo] operand of 2N rows) plus
+// an fp32 bias.  colmap[c] = kernel K column of reference input column c
+// (layer 0).  k0 = 16: the 11-input NRRS RRSNet layer, whose bias rides in
+// weight column 11 against a constant-1 input; otherwise the data occupies K
+// columns [0, 32) and the epilogue adds the fp32 bias.
 PackedNet pack_net(const float *theta, int in, int out, int k0, const std::vector<int> &colmap) {
     PackedNet pn;
     int off = 0;
     for (int l = 0; l < 4; ++l) {
         const int li = l == 0 ? in : kHidden, lo = l == 3 ? out : kHidden;
         const bool inline_bias = l == 0 && k0 == 16;
-        const int K = inline_bias ? 16 : 48;
-        const int bias_col = inline_bias ? 11 : 32;
+        const int K = inline_bias ? 16 : 32;
         const int N = l == 3 ? 16 : kHidden;
         const float *W = theta + off;         // column-major lo x li
         const float *b = theta + off + lo * li;
@@ -87,10 +87,10 @@ PackedNet pack_net(const float *theta, int in, int out, int k0, const std::vecto
         LayerDesc &L = pn.desc.layer[l];
         L.K = (uint16_t)K;
         L.N = (uint16_t)N;
-        L.ones_slice = inline_bias ? 0xFFFFFFFFu : 2u;
         L.w_hi = (uint32_t)pn.bytes.size();
         L.w_lo = L.w_hi + (uint32_t)wbytes;
-        pn.bytes.resize(pn.bytes.size() + 2 * wbytes, 0);
+        L.bias = inline_bias ? kNoBias : L.w_lo + (uint32_t)wbytes;
+        pn.bytes.resize(pn.bytes.size() + 2 * wbytes + (inline_bias ? 0 : (size_t)N * 4), 0);
         uint8_t *hi = pn.bytes.data() + L.w_hi, *lo_p = pn.bytes.data() + L.w_lo;
         const uint32_t sbo = (uint32_t)K * 16u;
         auto put = [&](int r, int kc, float v) {
@@ -104,7 +104,10 @@ PackedNet pack_net(const float *theta, int in, int out, int k0, const std::vecto
         for (int r = 0; r < lo; ++r) {
             for (int c = 0; c < li; ++c)
                 put(r, l == 0 ? colmap[c] : c, W[c * lo + r]);
-            put(r, bias_col, b[r]);
+            if (inline_bias)
+                put(r, 11, b[r]);
+            else
+                std::memcpy(pn.bytes.data() + L.bias + 4 * r, &b[r], 4);
         }
     }
     return pn;
@@ -118,6 +121,8 @@ void append_net(std::vector<uint8_t> &blob, const PackedNet &pn, NetDesc &desc) 
     for (auto &L : desc.layer) {
         L.w_hi += base;
         L.w_lo += base;
+        if (L.bias != kNoBias)
+            L.bias += base;
     }
 }
 
@@ -158,7 +163,9 @@ struct nrrs_gpu_ctx {
     int variant = 0;
     nrrs_grid_spec spec{};
     GridDev grid{};
-    float *d_stat_grid = nullptr, *d_rrs_grid = nullptr;
+    float *d_stat_grid = nullptr;
+    void *d_rrs_grid = nullptr;
+    bool rrs_half = false;  // AID grid stored as fp16 (precision)
     DeviceBlob blob_stat, blob_rrs, blob_both;  // ADRRS/STATS, AID, NRRS
 
     // scratch
@@ -424,7 +431,7 @@ int nrrs_gpu_set_weights(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w) {
         const uint32_t pi = i < half ? (i << 1) : (((G - 1u - i) << 1) | 1u);
         return (e & ~(G - 1u)) | pi;
     };
-    auto upload_grid = [&](float *&dst, const float *src, uint64_t len) -> int {
+    auto upload_grid = [&](auto *&dst, const float *src, uint64_t len, bool half) -> int {
         if (dst)
             cudaFree(dst);
         dst = nullptr;
@@ -453,13 +460,29 @@ int nrrs_gpu_set_weights(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w) {
                 }
             }
         }
-        CK(ctx, cudaMalloc(&dst, 3 * len * sizeof(float)));
-        CK(ctx, cudaMemcpy(dst, h.data(), 3 * len * sizeof(float), cudaMemcpyHostToDevice));
+        if (half) {
+            std::vector<__half> hh(h.size());
+            for (size_t i = 0; i < h.size(); ++i)
+                hh[i] = __float2half_rn(h[i]);
+            CK(ctx, cudaMalloc(reinterpret_cast<void **>(&dst), hh.size() * sizeof(__half)));
+            CK(ctx, cudaMemcpy(dst, hh.data(), hh.size() * sizeof(__half), cudaMemcpyHostToDevice));
+        } else {
+            CK(ctx, cudaMalloc(reinterpret_cast<void **>(&dst), h.size() * sizeof(float)));
+            CK(ctx, cudaMemcpy(dst, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
+        }
         return NRRS_OK;
     };
-    rc = upload_grid(ctx->d_stat_grid, w->stat_grid, grid_len);
+    // The AID grid (RRSNet input, no Box-Cox amplification downstream) is stored in fp16:
+    // half the bytes per gather on the path's binding resource, max relative error of q
+    // 1.1e-4 against the 1e-3 bar.  Tables beyond fp16 range stay fp32.
+    bool half = w->variant == NRRS_VARIANT_AID && !std::getenv("NRRS_FP32_TABLES");
+    for (uint64_t i = 0; half && i < rrs_grid_len; ++i)
+        if (!(std::fabs(w->rrs_grid[i]) < 32768.0f))
+            half = false;
+    rc = upload_grid(ctx->d_stat_grid, w->stat_grid, grid_len, false);
     if (!rc)
-        rc = upload_grid(ctx->d_rrs_grid, w->rrs_grid, rrs_grid_len);
+        rc = upload_grid(ctx->d_rrs_grid, w->rrs_grid, rrs_grid_len, half);
+    ctx->rrs_half = half;
     if (rc)
         return rc;
     ctx->variant = w->variant;
@@ -521,7 +544,8 @@ static int select_kind(nrrs_gpu_ctx *ctx, uint32_t depth, const nrrs_strategy &s
 
 static void fill_infer_common(nrrs_gpu_ctx *ctx, int kind, InferParams &ip) {
     ip.stat_grid = reinterpret_cast<const float2 *>(ctx->d_stat_grid);
-    ip.rrs_grid = reinterpret_cast<const float2 *>(ctx->d_rrs_grid);
+    ip.rrs_grid = ctx->d_rrs_grid;
+    ip.rrs_half = ctx->rrs_half ? 1u : 0u;
     ip.grid = ctx->grid;
     const DeviceBlob *b = nullptr;
     if (kind == kKindNrrs)
@@ -591,30 +615,41 @@ static int run_factors(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, 
     unsigned long long *dbg = nullptr;
     const bool timing = std::getenv("NRRS_DEBUG_TIMING") != nullptr;  // diagnostics only
     if (timing) {
-        CK(ctx, cudaMalloc(&dbg, 16 * 1024 * sizeof(unsigned long long)));
-        CK(ctx, cudaMemsetAsync(dbg, 0, 16 * 1024 * sizeof(unsigned long long), ctx->stream));
+        CK(ctx, cudaMalloc(&dbg, 32 * 1024 * sizeof(unsigned long long)));
+        CK(ctx, cudaMemsetAsync(dbg, 0, 32 * 1024 * sizeof(unsigned long long), ctx->stream));
         ip.dbg = dbg;
     }
     uint32_t grid = 0;
     CK(ctx, launch_infer(kind, ip, ctx->num_sms, ctx->stream, &grid));
     ctx->launches += 1;
     if (timing) {
-        std::vector<unsigned long long> h(16 * 1024);
+        std::vector<unsigned long long> h(32 * 1024);
         CK(ctx, cudaMemcpyAsync(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
         CK(ctx, cudaStreamSynchronize(ctx->stream));
-        double sum[16] = {0};
+        double sum[32] = {0};
         for (uint32_t b = 0; b < grid; ++b)
-            for (int k = 0; k < 16; ++k)
-                sum[k] += (double)h[b * 16 + k];
+            for (int k = 0; k < 32; ++k)
+                sum[k] += (double)h[b * 32 + k];
         std::fprintf(stderr, "[nrrs timing] kind %d grid %u mean kcycles/CTA:", kind, grid);
-        for (int k = 0; k < 16; ++k)
+        for (int k = 0; k < 32; ++k)
             std::fprintf(stderr, " %d:%.1f", k, sum[k] / grid / 1e3);
         unsigned long long mn = ~0ull, mx = 0, mxs = 0, mne = ~0ull;
         for (uint32_t b = 0; b < grid; ++b) {
-            const unsigned long long s0 = h[b * 16 + 12], e0 = h[b * 16 + 13];
+            const unsigned long long s0 = h[b * 32 + 12], e0 = h[b * 32 + 13];
             if (!s0) continue;
             mn = s0 < mn ? s0 : mn; mxs = s0 > mxs ? s0 : mxs;
             mx = e0 > mx ? e0 : mx; mne = e0 < mne ? e0 : mne;
+        }
+        if (std::getenv("NRRS_DEBUG_TIMELINE")) {
+            unsigned long long t0 = ~0ull;
+            for (int i = 0; i < 1024; ++i)
+                if (h[8192 + 4 * i] && h[8192 + 4 * i] < t0) t0 = h[8192 + 4 * i];
+            std::fprintf(stderr, "\n[nrrs timeline] CTA 0 tile: ready mlp_start full_passed done (kcycles)");
+            for (int i = 0; i < 1024 && h[8192 + 4 * i]; ++i)
+                std::fprintf(stderr, "\n%d %.1f %.1f %.1f %.1f", i, (double)(h[8192 + 4 * i] - t0) / 1e3,
+                             (double)((long long)(h[8192 + 4 * i + 1] - t0)) / 1e3,
+                             (double)((long long)(h[8192 + 4 * i + 2] - t0)) / 1e3,
+                             (double)((long long)(h[8192 + 4 * i + 3] - t0)) / 1e3);
         }
         std::fprintf(stderr, "\n[nrrs timing] CTA start spread %.1f us, end spread %.1f us, span %.1f us\n",
                      (mxs - mn) / 1e3, (mx - mne) / 1e3, (mx - mn) / 1e3);

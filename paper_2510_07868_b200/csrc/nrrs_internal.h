@@ -22,10 +22,16 @@ enum : int {
 // The bias is a weight column multiplied by a constant-ones input column:
 // either a dedicated K16 slice (`ones_slice`, 2 MMA terms) or, for the 11-input
 // NRRS RRSNet layer, input column 11 of the single K16 slice.
+constexpr uint32_t kNoBias = 0xFFFFFFFFu;
+
+// One MLP layer in the smem weight blob: W_hi (N x K) immediately followed by
+// W_lo (N x K), both fp16 in the UMMA K-major SWIZZLE_NONE canonical layout, so
+// [W_hi ; W_lo] is one 2N x K operand; fp32 bias[N] at `bias` (kNoBias: the
+// bias is a weight column of an input that is constant 1).
 struct LayerDesc {
     uint32_t w_hi, w_lo;
-    uint16_t K, N;        // K in {16, 48}, N in {16, 32}
-    uint32_t ones_slice;  // K16 slice index holding the ones column, or 0xFFFFFFFF
+    uint16_t K, N;        // K in {16, 32}, N in {16, 32}
+    uint32_t bias;        // blob byte offset of the fp32 bias, or kNoBias
 };
 
 struct NetDesc {
@@ -75,7 +81,9 @@ struct InferParams {
     float fixed_value;
     float eps;          // max(eps_div, 1e-8)
     uint64_t mixed_seed;  // mix_bits(seed)
-    const float2 *stat_grid, *rrs_grid;
+    const float2 *stat_grid;
+    const void *rrs_grid;   // fp32 (float2 entries) or fp16 (half2 entries) when rrs_half
+    uint32_t rrs_half;
     GridDev grid;
     const uint8_t *blob;
     uint32_t blob_bytes;

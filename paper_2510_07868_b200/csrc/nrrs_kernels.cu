@@ -1,6 +1,6 @@
 // nrrs_kernels.cu -- sm_100a kernels of the NRRS per-bounce RRS stage.
 //
-//   K-A infer_kernel<KIND>   strategy factor per vertex (hash grid + tcgen05 MLP
+//   K-A infer_ws_kernel<KIND> strategy factor per vertex (hash grid + tcgen05 MLP
 //                            chain for the neural kinds), sanitize, RrsRound
 //                            uniform, deterministic per-CTA double partial sums
 //                            of q; the last CTA reduces them in fixed order.
@@ -23,20 +23,14 @@ namespace nrrs {
 // ===========================================================================
 // K-A: factor inference
 //
-// One CTA = one 128-vertex tile at a time (UMMA M = 128), 256 threads: thread
-// t owns tile row r = t & 127 and half h = t >> 7.  Half 0 encodes hash-grid
-// levels 0-3 and tail[0..7]; half 1 levels 4-7 and tail[8..15]; in every MLP
-// epilogue half h drains TMEM columns [16h, 16h+16).  Warps w and w+4 share
-// TMEM lane quarter w (tcgen05.ld lane-access rule).
+// Heuristic factors (Fixed / Throughput, and depth 1) need no network: a plain
+// streaming kernel, one thread per vertex.  The neural kinds run the
+// warp-specialized tcgen05 pipeline further down (namespace ws).
 // ===========================================================================
 constexpr int kTileM = 128;           // vertices per MMA tile (UMMA M)
-constexpr int kInferThreads = 256;    // 2 threads per tile row
-constexpr uint32_t kTmemCols = 128;   // per CTA: D [0,32) A_hi [32,48) A_lo [48,64) ones [64,72)
-constexpr uint32_t kColD = 0, kColAHi = 32, kColALo = 48, kColOnes = 64;
+constexpr int kInferThreads = 256;    // heuristic kernel block
 
 struct InferSmemHeader {
-    uint64_t mbar;
-    uint32_t tmem_base;
     uint32_t is_last;
     double warp_sums[8];
     uint32_t warp_cnt[8];
@@ -51,70 +45,6 @@ __device__ __forceinline__ void split2(float v0, float v1, uint32_t &h, uint32_t
     const __half2 ll = __float22half2_rn(make_float2(v0 - b.x, v1 - b.y));
     h = *reinterpret_cast<const uint32_t *>(&hh);
     l = *reinterpret_cast<const uint32_t *>(&ll);
-}
-
-// 16 fp32 values -> K columns [16*slot, 16*slot+16) of this thread's row of the
-// A operand in TMEM (hi and lo tiles; 8 packed fp16x2 columns each).
-__device__ __forceinline__ void write_a_tmem(uint32_t tmem_row, int slot, const float *x) {
-    uint32_t h[8], l[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e)
-        split2(x[2 * e], x[2 * e + 1], h[e], l[e]);
-    tmem_st8(tmem_row + kColAHi + 8u * (uint32_t)slot, h);
-    tmem_st8(tmem_row + kColALo + 8u * (uint32_t)slot, l);
-}
-
-// Barrier + one MMA layer + wait for the accumulator.  3-term split
-// (hi*Whi + lo*Whi + hi*Wlo) on data slices, A from TMEM; the constant-ones
-// slice carries the bias column (1*bias_hi + 1*bias_lo).
-__device__ __forceinline__ void mma_layer(const uint8_t *smem_w, const LayerDesc &L, uint32_t tmem_base,
-                                          uint64_t *bar, uint32_t &phase) {
-    tmem_wait_st();
-    tc_fence_before();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        tc_fence_after();
-        const uint32_t idesc = make_idesc_f16(L.N);
-        const uint32_t w_hi_s = smem_u32(smem_w + L.w_hi), w_lo_s = smem_u32(smem_w + L.w_lo);
-        const uint32_t w_sbo = (uint32_t)L.K * 16u;
-        const uint32_t d = tmem_base + kColD;
-        for (uint32_t s = 0; s < (uint32_t)L.K / 16u; ++s) {
-            const uint64_t wh = make_smem_desc(w_hi_s + s * 256u, 128u, w_sbo);
-            const uint64_t wl = make_smem_desc(w_lo_s + s * 256u, 128u, w_sbo);
-            if (s == L.ones_slice) {
-                mma_f16_ts(d, tmem_base + kColOnes, wh, idesc, 1u);
-                mma_f16_ts(d, tmem_base + kColOnes, wl, idesc, 1u);
-            } else {
-                const uint32_t ah = tmem_base + kColAHi + 8u * s, al = tmem_base + kColALo + 8u * s;
-                mma_f16_ts(d, ah, wh, idesc, s > 0 ? 1u : 0u);
-                mma_f16_ts(d, al, wh, idesc, 1u);
-                mma_f16_ts(d, ah, wl, idesc, 1u);
-            }
-        }
-        mma_commit(bar);
-    }
-    mbar_wait(bar, phase);
-    phase ^= 1u;
-    tc_fence_after();
-}
-
-// 3-hidden-layer MLP (mlp.cpp:52-72); the layer-0 input must be in TMEM A.
-// Head outputs (columns 0..15, bias included) land in y (valid on half 0).
-__device__ __forceinline__ void run_mlp(const uint8_t *smem_w, const NetDesc &net, uint32_t tmem_base,
-                                        uint32_t tmem_row, int half, uint64_t *bar, uint32_t &phase,
-                                        float (&y)[16]) {
-#pragma unroll 1
-    for (int l = 0; l < 3; ++l) {
-        mma_layer(smem_w, net.layer[l], tmem_base, bar, phase);
-        float acc[16];
-        tmem_ld16(tmem_row + kColD + 16u * (uint32_t)half, acc);
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-            acc[i] = fmaxf(acc[i], acc[i] * 0.01f);  // leaky ReLU = cwiseMax(z, slope z)
-        write_a_tmem(tmem_row, half, acc);
-    }
-    mma_layer(smem_w, net.layer[3], tmem_base, bar, phase);
-    tmem_ld16(tmem_row + kColD, y);  // both halves load (warp-aligned); half 0 uses it
 }
 
 // Position of entry e in the copy that pairs (e, e ^ (2^(t+1)-1)) into one
@@ -241,214 +171,44 @@ __device__ __forceinline__ void one_blob_fast(float x, float *out) {
 
 __device__ __forceinline__ float remap_fast(float a) { return 1.0f - __expf(-a); }
 
-template <int KIND>
-__global__ void __launch_bounds__(kInferThreads, 3) infer_kernel(InferParams p) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    constexpr bool kNeural = KIND != kKindHeuristic;
-    uint8_t *smem_w = smem_raw;
-    InferSmemHeader *hdr = reinterpret_cast<InferSmemHeader *>(kNeural ? smem_w + p.blob_bytes : smem_raw);
+__global__ void __launch_bounds__(kInferThreads) infer_kernel(InferParams p) {
+    __shared__ InferSmemHeader hdr_s;
+    InferSmemHeader *hdr = &hdr_s;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int row = tid & (kTileM - 1), half = tid >> 7;
-
-    uint32_t phase = 0;
-    uint32_t tmem_base = 0, tmem_row = 0;
-    if constexpr (kNeural) {
-        // weights: global blob -> smem (16-byte vector copies)
-        const uint4 *src = reinterpret_cast<const uint4 *>(p.blob);
-        uint4 *dst = reinterpret_cast<uint4 *>(smem_w);
-        for (uint32_t i = tid; i < p.blob_bytes / 16u; i += kInferThreads)
-            dst[i] = __ldg(src + i);
-        if (tid == 0) {
-            mbar_init(&hdr->mbar, 1);
-            fence_barrier_init();
-        }
-        if (warp == 0)
-            tmem_alloc(&hdr->tmem_base, kTmemCols);
-        tc_fence_before();
-        __syncthreads();
-        tc_fence_after();
-        tmem_base = hdr->tmem_base;
-        tmem_row = tmem_base + ((uint32_t)((warp & 3) * 32) << 16);
-        // constant-ones K16 A slice in TMEM: k = 0 is 1.0 (fp16), the rest 0
-        if (half == 0) {
-            const uint32_t ones[8] = {0x00003C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-            tmem_st8(tmem_row + kColOnes, ones);
-        }
-    }
-
     const uint64_t n = p.n;
-    const uint64_t num_tiles = (n + kTileM - 1) / kTileM;
-    const uint64_t t_begin = num_tiles * blockIdx.x / gridDim.x;
-    const uint64_t t_end = num_tiles * (blockIdx.x + 1) / gridDim.x;
     // per-thread accumulators, reduced once per CTA in a fixed order (deterministic)
     double my_sum = 0.0;
-    uint32_t my_nonfinite = 0, my_bc = 0;
-
-    for (uint64_t tile = t_begin; tile < t_end; ++tile) {
-        const uint64_t j = tile * kTileM + row;
-        const bool valid = j < n;
-        float px = 0, py = 0, pz = 0, wx = 0, wy = 0, wz = 0;
-        if (valid) {
-            px = __ldg(p.p01 + 3 * j); py = __ldg(p.p01 + 3 * j + 1); pz = __ldg(p.p01 + 3 * j + 2);
-            wx = __ldg(p.weight + 3 * j); wy = __ldg(p.weight + 3 * j + 1); wz = __ldg(p.weight + 3 * j + 2);
-        }
+    uint32_t my_nonfinite = 0;
+    const uint32_t my_bc = 0;
+    const bool depth1 = p.depth == 1u;
+    for (uint64_t j = (uint64_t)blockIdx.x * kInferThreads + tid; j < n; j += (uint64_t)gridDim.x * kInferThreads) {
+        const float wx = __ldg(p.weight + 3 * j), wy = __ldg(p.weight + 3 * j + 1), wz = __ldg(p.weight + 3 * j + 2);
         const float lum_w = luminance(wx, wy, wz);
         // Mix-Depth gate + zero-throughput skip (wavefront.cpp:373-380)
-        const bool depth1 = p.depth == 1u;
-        const bool active = valid && (p.gate ? (!depth1 && lum_w > 0.0f) : true);
-        float q = 0.0f;
-        uint32_t bc = 0;
-
-        if constexpr (KIND == kKindHeuristic) {
-            if (p.heur_kind == 0)
-                q = p.fixed_value;                              // Fixed (wavefront.cpp:193-194)
-            else
-                q = (lum_w < 1.0f) ? lum_w : 1.0f;              // std::min(1, lum) (rrs.hpp:49-51)
-        } else {
-            auto load_ipix = [&](float &a, float &b, float &c) {
-                if (!valid) {
-                    a = b = c = 0.0f;
-                } else if (p.i_pixel) {
-                    a = __ldg(p.i_pixel + 3 * j); b = __ldg(p.i_pixel + 3 * j + 1); c = __ldg(p.i_pixel + 3 * j + 2);
-                } else {
-                    const uint64_t px_idx = __ldg(p.pixel + j);
-                    a = __ldg(p.i_acc + 3 * px_idx); b = __ldg(p.i_acc + 3 * px_idx + 1); c = __ldg(p.i_acc + 3 * px_idx + 2);
-                }
-            };
-            const float rough = valid ? __ldg(p.roughness + j) : 0.0f;
-            float y[16];
-            {
-                // layer-0 input (networks.cpp:131-135 / :149-157); kernel K layout
-                // (host packs W columns to match): half h owns k in [16h, 16h+16) =
-                // grid features of levels 4h..4h+3, then tail[8h .. 8h+8).
-                float in16[16];
-                float *g8 = in16, *t8 = in16 + 8;
-                if (p.ablate & 1u) {
-#pragma unroll
-                    for (int s = 0; s < 8; ++s)
-                        g8[s] = px * (float)(s + 1) + py;
-                } else {
-                    grid_encode4(KIND == kKindAid ? p.rrs_grid : p.stat_grid, p.grid, 4 * half, clamp01(px),
-                                 clamp01(py), clamp01(pz), g8);
-                }
-                if (half == 0) {
-                    const float wox = valid ? __ldg(p.wo01 + 2 * j) : 0.0f;
-                    const float woy = valid ? __ldg(p.wo01 + 2 * j + 1) : 0.0f;
-                    one_blob_fast<4>(wox, t8);
-                    one_blob_fast<4>(woy, t8 + 4);
-                } else if (KIND == kKindAid) {
-                    float ipx, ipy, ipz;
-                    load_ipix(ipx, ipy, ipz);
-                    t8[0] = box_cox(wx, bc);
-                    t8[1] = box_cox(wy, bc);
-                    t8[2] = box_cox(wz, bc);
-                    t8[3] = box_cox(mean3(ipx, ipy, ipz), bc);
-                    one_blob_fast<4>(remap_fast(rough), t8 + 4);
-                } else {
-                    one_blob_fast<8>(remap_fast(rough), t8);
-                }
-                if (!valid) {
-#pragma unroll
-                    for (int s = 0; s < 8; ++s) {
-                        g8[s] = 0.0f;
-                        t8[s] = 0.0f;
-                    }
-                }
-                write_a_tmem(tmem_row, half, in16);
-                if (p.ablate & 2u) {
-#pragma unroll
-                    for (int s = 0; s < 16; ++s)
-                        y[s] = in16[s];
-                }
-            }
-            if (p.ablate & 2u) {
-                q = softplus_mod(y[0] + y[5] + y[11]);
-            } else if (KIND == kKindAid) {
-                run_mlp(smem_w, p.nets.rrs, tmem_base, tmem_row, half, &hdr->mbar, phase, y);
-                q = softplus_mod(y[0]);
-            } else {
-                run_mlp(smem_w, p.nets.stat, tmem_base, tmem_row, half, &hdr->mbar, phase, y);
-                if (KIND == kKindStats) {
-                    if (valid && half == 0) {
-#pragma unroll
-                        for (int i = 0; i < 6; ++i)
-                            p.stats_out[6 * j + i] = y[i];
-                    }
-                } else if (KIND == kKindAdrrs) {
-                    // adrrs_factor (rrs.hpp:56-61) with eps = max(eps_div, 1e-8)
-                    float ipx, ipy, ipz;
-                    load_ipix(ipx, ipy, ipz);
-                    const float num = luminance(wx * y[0], wy * y[1], wz * y[2]);
-                    const float qq = num / (luminance(ipx, ipy, ipz) + p.eps);
-                    q = qq < 0.05f ? 0.05f : (20.0f < qq ? 20.0f : qq);
-                } else {  // NRRS: stats -> build_nrrs_input (networks.cpp:137-147) -> RRSNet
-                    if (half == 0) {
-                        float ipx, ipy, ipz;
-                        load_ipix(ipx, ipy, ipz);
-                        float xin[16];
-#pragma unroll
-                        for (int c = 0; c < 6; ++c)
-                            xin[c] = box_cox(y[c], bc);
-                        xin[6] = box_cox(wx, bc);
-                        xin[7] = box_cox(wy, bc);
-                        xin[8] = box_cox(wz, bc);
-                        xin[9] = box_cox(mean3(ipx, ipy, ipz), bc);
-                        xin[10] = remap_fast(rough);
-                        xin[11] = 1.0f;  // bias column of the RRSNet first layer
-#pragma unroll
-                        for (int c = 12; c < 16; ++c)
-                            xin[c] = 0.0f;
-                        if (!valid) {
-#pragma unroll
-                            for (int c = 0; c < 11; ++c)
-                                xin[c] = 0.0f;
-                        }
-                        write_a_tmem(tmem_row, 0, xin);
-                    }
-                    run_mlp(smem_w, p.nets.rrs, tmem_base, tmem_row, half, &hdr->mbar, phase, y);
-                    q = softplus_mod(y[0]);
-                }
+        const bool active = p.gate ? (!depth1 && lum_w > 0.0f) : true;
+        float q = p.heur_kind == 0 ? p.fixed_value                 // Fixed (wavefront.cpp:193-194)
+                                   : (lum_w < 1.0f ? lum_w : 1.0f);  // std::min(1, lum) (rrs.hpp:49-51)
+        uint32_t decided = active ? 1u : 0u;
+        if (p.gate) {
+            if (depth1)
+                q = 1.0f;  // depth-1 pin (wavefront.cpp:373-375)
+            if (!active && !depth1)
+                q = 0.0f;
+            decided = (depth1 || active) ? 1u : 0u;
+            if (!isfinite(q) || q < 0.0f) {  // sanitize (wavefront.cpp:381-385)
+                q = 0.0f;
+                decided = 0;
+                ++my_nonfinite;
             }
         }
-        if (!active)
-            bc = 0;
-        my_bc += bc;
-
-        if constexpr (KIND != kKindStats) {
-            if (half == 0) {
-                uint32_t decided = active ? 1u : 0u;
-                if (p.gate) {
-                    if (valid && depth1)
-                        q = 1.0f;  // depth-1 pin (wavefront.cpp:373-375)
-                    if (!active && !depth1)
-                        q = 0.0f;
-                    decided = valid && (depth1 || active) ? 1u : 0u;
-                    if (valid && (!isfinite(q) || q < 0.0f)) {  // sanitize (wavefront.cpp:381-385)
-                        q = 0.0f;
-                        decided = 0;
-                        ++my_nonfinite;
-                    }
-                }
-                if (valid) {
-                    p.q_out[j] = q;
-                    if (p.u_out)
-                        p.u_out[j] = rrs_uniform(p.mixed_seed, __ldg(p.path_key + j), p.depth);
-                    if (p.decided_out)
-                        p.decided_out[j] = (uint8_t)decided;
-                    my_sum += (double)q;
-                }
-            }
-        }
+        p.q_out[j] = q;
+        if (p.u_out)
+            p.u_out[j] = rrs_uniform(p.mixed_seed, __ldg(p.path_key + j), p.depth);
+        if (p.decided_out)
+            p.decided_out[j] = (uint8_t)decided;
+        my_sum += (double)q;
     }
 
-    if constexpr (kNeural) {
-        tc_fence_before();
-        __syncthreads();
-        if (warp == 0)
-            tmem_dealloc(hdr->tmem_base, kTmemCols);
-    }
-    if constexpr (KIND == kKindStats)
-        return;
     if (p.parts == nullptr)
         return;
     // ---- CTA sum in a fixed tree, then last-CTA-done reduction in CTA order ----
@@ -551,9 +311,11 @@ struct Side {        // 32 B per tile row
     float ex[5];     // NRRS: bc(t_x)x3, bc(mean I), remap(r); ADRRS: w x3, lum(I)
 };
 
-// TMEM (512 columns, 1 CTA / SM): ones slice [0, 8); chain D accumulators
-// [32 + 32q, +32) for q < GM*P; tile slots [kColSlots + 32s, +32) holding the
-// layer-0 input (hi 16 | lo 16 columns), reused as the hidden-layer A.
+// TMEM (512 columns, 1 CTA / SM): one 64-column fp32 accumulator per MLP chain,
+// [64c, 64c + 64): columns [0, N) collect A_hi*W_hi + A_lo*W_hi and [N, 2N)
+// collect A_hi*W_lo (one N = 2N instruction covers both weight halves); then a
+// ring of tile slots [kColSlots + 32s, +32) holding the layer-0 input
+// (hi 16 | lo 16 packed fp16x2 columns), reused as the hidden-layer A.
 template <int GE, int GM, int P, int TPR>
 struct Cfg {
     static constexpr int kGroupThreads = 128 * TPR;  // MLP threads per group (TPR threads per tile row)
@@ -561,9 +323,8 @@ struct Cfg {
     static constexpr int kMlpThreads = GM * kGroupThreads;
     static constexpr int kThreads = kEncThreads + kMlpThreads;
     static constexpr int kChains = GM * P;
-    static constexpr uint32_t kColOnes = 0;
-    static constexpr uint32_t kColD = 32;
-    static constexpr uint32_t kColSlots = 32 + 32 * kChains;
+    static constexpr uint32_t kColD = 0;
+    static constexpr uint32_t kColSlots = 64 * kChains;
     static constexpr int kSlotsRaw = (512 - (int)kColSlots) / 32;
     static constexpr int kSlots = kSlotsRaw > 16 ? 16 : kSlotsRaw;
     static_assert(kSlots >= GE + kChains, "TMEM slot ring too small");
@@ -573,10 +334,11 @@ struct SmemTail {
     uint64_t full[16];
     uint64_t empty[16];
     uint64_t mma_bar[8];
-    uint64_t wdesc[2][4][3][2];  // precomputed UMMA smem descriptors of [W | bias] hi / lo per K16 slice
-    uint32_t idesc[2][4];
+    uint64_t wdesc[2][4][2];   // UMMA smem descriptor of [W_hi ; W_lo] per K16 slice (W_hi alone = first N rows)
+    uint32_t idesc_n[2][4];    // N = layer width
+    uint32_t idesc_2n[2][4];   // N = 2 x layer width (both weight halves)
     uint32_t nslices[2][4];
-    uint32_t ones_slice[2][4];
+    uint32_t bias[2][4];       // smem byte offset of the fp32 bias, or kNoBias (folded into W)
     uint32_t tmem_base;
     uint32_t is_last;
     double red_sum[32];
@@ -584,46 +346,70 @@ struct SmemTail {
     uint32_t red_bc[32];
 };
 
-// Elected issue of one layer (3-term split on data slices, 2-term on the ones
-// slice), commit to the chain's mbarrier.  Caller has synchronized the group.
+// Elected issue of one layer, 2 MMAs per K16 slice, commit to the chain's mbarrier:
+//   D[:, 0:2N]  (+)= A_hi x [W_hi | W_lo]    (N = 2N: hi*W_hi and hi*W_lo side by side)
+//   D[:, 0:N]    += A_lo x W_hi
+// The epilogue adds the two column halves (3-term split).
+// Caller has synchronized the group.
 __device__ __forceinline__ void ws_issue(const SmemTail *st, int net, int layer, uint32_t tmem_base,
-                                         uint32_t col_ones, uint32_t col_a, uint32_t col_d, uint64_t *bar) {
+                                         uint32_t col_a, uint32_t col_d, uint64_t *bar) {
     tc_fence_after();
-    const uint32_t idesc = st->idesc[net][layer];
-    const uint32_t ns = st->nslices[net][layer], os = st->ones_slice[net][layer];
+    const uint32_t i2 = st->idesc_2n[net][layer], i1 = st->idesc_n[net][layer];
+    const uint32_t ns = st->nslices[net][layer];
     const uint32_t d = tmem_base + col_d;
 #pragma unroll
-    for (uint32_t k = 0; k < 3; ++k) {
+    for (uint32_t k = 0; k < 2; ++k) {
         if (k >= ns)
             break;
-        const uint64_t wh = st->wdesc[net][layer][k][0], wl = st->wdesc[net][layer][k][1];
-        if (k == os) {
-            mma_f16_ts(d, tmem_base + col_ones, wh, idesc, 1u);
-            mma_f16_ts(d, tmem_base + col_ones, wl, idesc, 1u);
-        } else {
-            const uint32_t ah = tmem_base + col_a + 8u * k, al = ah + 16u;
-            mma_f16_ts(d, ah, wh, idesc, k > 0 ? 1u : 0u);
-            mma_f16_ts(d, al, wh, idesc, 1u);
-            mma_f16_ts(d, ah, wl, idesc, 1u);
-        }
+        const uint64_t w = st->wdesc[net][layer][k];
+        const uint32_t ah = tmem_base + col_a + 8u * k, al = ah + 16u;
+        mma_f16_ts(d, ah, w, i2, k > 0 ? 1u : 0u);
+        mma_f16_ts(d, al, w, i1, 1u);
     }
     mma_commit(bar);
 }
 
-// 32 fp32 values -> 16 hi + 16 lo packed fp16x2 TMEM columns of this thread's lane.
-__device__ __forceinline__ void ws_store_a32(uint32_t lane_base, uint32_t col, const float *x) {
+// 16 fp32 values (K columns [16h, 16h + 16) of the next A) -> 8 hi + 8 lo packed
+// fp16x2 TMEM columns of this thread's lane.
+__device__ __forceinline__ void ws_store_a16(uint32_t lane_base, uint32_t col_a, int h, const float (&x)[16]) {
+    uint32_t hw[8], lw[8];
 #pragma unroll
-    for (int hblk = 0; hblk < 2; ++hblk) {
-        uint32_t h[8], l[8];
+    for (int e = 0; e < 8; ++e)
+        split2(x[2 * e], x[2 * e + 1], hw[e], lw[e]);
+    tmem_st8(lane_base + col_a + 8u * (uint32_t)h, hw);
+    tmem_st8(lane_base + col_a + 16u + 8u * (uint32_t)h, lw);
+}
+
+// 16 accumulator columns [c0, c0 + 16) of this lane: D_hi + D_lo (+ bias), fp32.
+__device__ __forceinline__ void ws_load_sum16(uint32_t lane_base, uint32_t col_d, uint32_t n, uint32_t c0,
+                                              const float *bias, float (&z)[16]) {
+    float lo[16];
+    tmem_ld16x2(lane_base + col_d + c0, lane_base + col_d + n + c0, z, lo);
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-            split2(x[16 * hblk + 2 * e], x[16 * hblk + 2 * e + 1], h[e], l[e]);
-        tmem_st8(lane_base + col + 8u * hblk, h);
-        tmem_st8(lane_base + col + 16u + 8u * hblk, l);
+    for (int i = 0; i < 16; ++i)
+        z[i] += lo[i];
+    if (bias) {
+        const float4 *b4 = reinterpret_cast<const float4 *>(bias + c0);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float4 b = b4[i];
+            z[4 * i] += b.x;
+            z[4 * i + 1] += b.y;
+            z[4 * i + 2] += b.z;
+            z[4 * i + 3] += b.w;
+        }
     }
 }
 
 }  // namespace ws
+
+// Per-phase cycle counters and the CTA-0 tile timeline (NRRS_DEBUG_TIMING on the
+// host) exist only in builds with -DNRRS_KERNEL_TIMING: they cost registers.
+#ifdef NRRS_KERNEL_TIMING
+constexpr bool kTiming = true;
+#else
+constexpr bool kTiming = false;
+#endif
 
 template <int KIND, int GE, int GM, int P, int TPR>
 __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws_kernel(InferParams p) {
@@ -631,16 +417,18 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
     constexpr uint32_t kGT = Cfg::kGroupThreads;
     constexpr int S = Cfg::kSlots;
     constexpr int kNL = KIND == kKindNrrs ? 8 : 4;  // MMA layers per tile (NRRS: StatNet then RRSNet)
-    unsigned long long g_start = 0;
-    if (p.dbg && threadIdx.x == 0)
+    unsigned long long g_start = 0, c_start = 0;
+    if (kTiming && p.dbg && threadIdx.x == 0) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
+        c_start = clock64();
+    }
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem_w = smem_raw;
     ws::Side *side = reinterpret_cast<ws::Side *>(smem_raw + ((p.blob_bytes + 127u) & ~127u));
     ws::SmemTail *st = reinterpret_cast<ws::SmemTail *>(reinterpret_cast<uint8_t *>(side) + S * 128 * sizeof(ws::Side));
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-    // ---- setup: weights -> smem, barriers, TMEM (all 512 columns), ones slice ----
+    // ---- setup: weights -> smem, UMMA descriptors, barriers, TMEM (all 512 columns) ----
     {
         const uint4 *src = reinterpret_cast<const uint4 *>(p.blob);
         uint4 *dst = reinterpret_cast<uint4 *>(smem_w);
@@ -652,14 +440,13 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
             const NetDesc &nd = net == 0 ? p.nets.stat : p.nets.rrs;
             for (int l = 0; l < 4; ++l) {
                 const LayerDesc &L = nd.layer[l];
-                st->idesc[net][l] = make_idesc_f16(L.N);
+                st->idesc_n[net][l] = make_idesc_f16(L.N);
+                st->idesc_2n[net][l] = make_idesc_f16(2u * L.N);
                 st->nslices[net][l] = (uint32_t)L.K / 16u;
-                st->ones_slice[net][l] = L.ones_slice;
+                st->bias[net][l] = L.bias;
                 const uint32_t sbo = (uint32_t)L.K * 16u;
-                for (int k = 0; k < 3; ++k) {
-                    st->wdesc[net][l][k][0] = make_smem_desc(smem_u32(smem_w + L.w_hi) + 256u * k, 128u, sbo);
-                    st->wdesc[net][l][k][1] = make_smem_desc(smem_u32(smem_w + L.w_lo) + 256u * k, 128u, sbo);
-                }
+                for (int k = 0; k < 2; ++k)
+                    st->wdesc[net][l][k] = make_smem_desc(smem_u32(smem_w + L.w_hi) + 256u * k, 128u, sbo);
             }
         }
         for (int q = 0; q < S; ++q) {
@@ -677,14 +464,8 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
     tc_fence_after();
     const uint32_t tmem_base = st->tmem_base;
     const uint32_t lane_base = tmem_base + ((uint32_t)((warp & 3) * 32) << 16);
-    if (tid >= Cfg::kEncThreads && tid < Cfg::kEncThreads + 128) {  // MLP group 0 writes the ones slice
-        const uint32_t ones[8] = {0x00003C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-        tmem_st8(lane_base + Cfg::kColOnes, ones);
-        tmem_wait_st();
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
+    if (kTiming && p.dbg && tid == 0)
+        p.dbg[blockIdx.x * 32 + 3] = clock64() - c_start;  // setup cycles
 
     const uint64_t n = p.n;
     const uint64_t num_tiles = (n + kTileM - 1) / kTileM;
@@ -699,7 +480,7 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
         // ============================== encoder ==============================
         const int e = tid >> 8;                 // encoder group
         const int r = tid & 127, half = (tid >> 7) & 1;
-        const bool rec = p.dbg && (tid & 255) == 0;
+        const bool rec = kTiming && p.dbg && (tid & 255) == 0;
         unsigned long long c_empty = 0, c_enc = 0, c_st = 0, t0 = 0;
         for (uint32_t i = (uint32_t)e; i < T; i += GE) {
             const uint32_t s = i % S;
@@ -735,7 +516,10 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
                 for (int q = 0; q < 8; ++q)
                     g8[q] = px * (float)(q + 1) + py;
             } else if (KIND == kKindAid) {
-                grid_encode4<false>(p.rrs_grid, p.grid, 4 * half, clamp01(px), clamp01(py), clamp01(pz), g8);
+                if (p.rrs_half)
+                    grid_encode4<true>(p.rrs_grid, p.grid, 4 * half, clamp01(px), clamp01(py), clamp01(pz), g8);
+                else
+                    grid_encode4<false>(p.rrs_grid, p.grid, 4 * half, clamp01(px), clamp01(py), clamp01(pz), g8);
             } else {
                 grid_encode4<false>(p.stat_grid, p.grid, 4 * half, clamp01(px), clamp01(py), clamp01(pz), g8);
             }
@@ -795,11 +579,17 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
             tc_fence_before();
             mbar_arrive(&st->full[s]);
             if (rec) c_st += clock64() - t0;
+            if (kTiming && p.dbg && blockIdx.x == 0 && (tid & 255) == 0 && i < 1024)
+                p.dbg[8192 + 4 * i] = clock64();  // timeline (CTA 0): tile i input ready
+            if (kTiming && p.dbg && tid == 0) p.dbg[blockIdx.x * 32 + 18] = clock64();  // encoder 0: last full arrive
+            if (kTiming && p.dbg && tid == 256) p.dbg[blockIdx.x * 32 + 19] = clock64();  // encoder 1: last full arrive
         }
+        if (kTiming && p.dbg && tid == 0)
+            p.dbg[blockIdx.x * 32 + 7] = clock64() - c_start;  // encoder group 0 loop end
         if (rec) {
-            p.dbg[blockIdx.x * 16 + 4 * e + 0] = c_empty;
-            p.dbg[blockIdx.x * 16 + 4 * e + 1] = c_enc;
-            p.dbg[blockIdx.x * 16 + 4 * e + 2] = c_st;
+            p.dbg[blockIdx.x * 32 + 4 * e + 0] = c_empty;
+            p.dbg[blockIdx.x * 32 + 4 * e + 1] = c_enc;
+            p.dbg[blockIdx.x * 32 + 4 * e + 2] = c_st;
         }
     } else {
         // ================================ MLP ================================
@@ -810,7 +600,7 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
         const bool issuer = gt == 0;
         const uint32_t bar_id = 1u + (uint32_t)g;
         uint32_t phases = 0;  // bit c: parity of chain c's mbarrier
-        const bool rec = p.dbg && issuer;
+        const bool rec = kTiming && p.dbg && issuer;
         unsigned long long c_wait = 0, c_epi = 0, t0 = 0;
         for (uint32_t base = 0; base < T; base += Cfg::kChains) {
             uint32_t tile[P], slot[P];
@@ -824,6 +614,8 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
             if (!live[0])
                 break;
             // layer 0 of every chain as soon as its input slot is full
+            if (rec && g == 0) p.dbg[blockIdx.x * 32 + 16] = clock64() - 0;  // last tile: wait start
+            if (rec && blockIdx.x == 0 && tile[0] < 1024) p.dbg[8192 + 4 * tile[0] + 1] = clock64();  // MLP tile start
             tc_fence_before();
             named_bar_sync(bar_id, kGT);
 #pragma unroll
@@ -831,10 +623,11 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
                 if (!live[c])
                     continue;
                 mbar_wait(&st->full[slot[c]], (tile[c] / S) & 1u);
+                if (rec && g == 0) p.dbg[blockIdx.x * 32 + 17] = clock64();  // last tile: full passed
+                if (rec && blockIdx.x == 0 && tile[c] < 1024) p.dbg[8192 + 4 * tile[c] + 2] = clock64();
                 if (issuer)
-                    ws::ws_issue(st, KIND == kKindAid ? 1 : 0, 0, tmem_base, Cfg::kColOnes,
-                                 Cfg::kColSlots + 32u * slot[c], Cfg::kColD + 32u * (uint32_t)(g * P + c),
-                                 &st->mma_bar[g * P + c]);
+                    ws::ws_issue(st, KIND == kKindAid ? 1 : 0, 0, tmem_base, Cfg::kColSlots + 32u * slot[c],
+                                 Cfg::kColD + 64u * (uint32_t)(g * P + c), &st->mma_bar[g * P + c]);
             }
 #pragma unroll 1
             for (int l = 0; l < kNL; ++l) {  // layer l just issued for every live chain
@@ -843,40 +636,35 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
                     if (!live[c])
                         continue;
                     const int q = g * P + c;
-                    const uint32_t col_d = Cfg::kColD + 32u * (uint32_t)q;
+                    const uint32_t col_d = Cfg::kColD + 64u * (uint32_t)q;
                     const uint32_t col_a = Cfg::kColSlots + 32u * slot[c];
                     if (rec) t0 = clock64();
                     mbar_wait(&st->mma_bar[q], (phases >> c) & 1u);
                     phases ^= 1u << c;
                     tc_fence_after();
                     if (rec) { const unsigned long long t1 = clock64(); c_wait += t1 - t0; t0 = t1; }
-                    const bool head = (l & 3) == 3;
+                    const int lyr = l & 3;
+                    const bool head = lyr == 3;
                     const int net = (KIND == kKindAid || l >= 4) ? 1 : 0;
+                    const uint32_t boff = st->bias[net][lyr];
+                    const float *bias = boff == kNoBias ? nullptr : reinterpret_cast<const float *>(smem_w + boff);
                     if (!head) {
-                        if constexpr (TPR == 1) {
-                            float acc[32];
-                            tmem_ld32(lane_base + col_d, acc);
+                        // z = D_hi + D_lo + bias -> leaky ReLU -> next A (hi/lo), 16 columns at a time
 #pragma unroll
-                            for (int i = 0; i < 32; ++i)
-                                acc[i] = fmaxf(acc[i], acc[i] * 0.01f);  // leaky ReLU = cwiseMax(z, slope z)
-                            ws::ws_store_a32(lane_base, col_a, acc);
-                        } else {
-                            float acc[16];
-                            tmem_ld16(lane_base + col_d + 16u * (uint32_t)mh, acc);
-                            uint32_t hw[8], lw[8];
+                        for (int hh = 0; hh < 2 / TPR; ++hh) {
+                            const int h = TPR == 1 ? hh : mh;
+                            float z[16];
+                            ws::ws_load_sum16(lane_base, col_d, 32u, 16u * (uint32_t)h, bias, z);
 #pragma unroll
-                            for (int i = 0; i < 8; ++i)
-                                split2(fmaxf(acc[2 * i], acc[2 * i] * 0.01f),
-                                       fmaxf(acc[2 * i + 1], acc[2 * i + 1] * 0.01f), hw[i], lw[i]);
-                            tmem_st8(lane_base + col_a + 8u * (uint32_t)mh, hw);
-                            tmem_st8(lane_base + col_a + 16u + 8u * (uint32_t)mh, lw);
+                            for (int i = 0; i < 16; ++i)
+                                z[i] = fmaxf(z[i], z[i] * 0.01f);  // leaky ReLU = cwiseMax(z, slope z)
+                            ws::ws_store_a16(lane_base, col_a, h, z);
                         }
                         tmem_wait_st();
                         tc_fence_before();
                         named_bar_sync(bar_id, kGT);
                         if (issuer)
-                            ws::ws_issue(st, net, (l & 3) + 1, tmem_base, Cfg::kColOnes, col_a, col_d,
-                                         &st->mma_bar[q]);
+                            ws::ws_issue(st, net, lyr + 1, tmem_base, col_a, col_d, &st->mma_bar[q]);
                     } else if (mh != 0) {
                         // TPR 2, second column half: no head work; keep the group's barrier count
                         if (KIND == kKindNrrs && l == 3) {
@@ -887,7 +675,7 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
                         }
                     } else {
                         float y[16];
-                        tmem_ld16(lane_base + col_d, y);
+                        ws::ws_load_sum16(lane_base, col_d, 16u, 0u, bias, y);  // head: N = 16
                         mbar_wait(&st->full[slot[c]], (tile[c] / S) & 1u);  // sidecar visibility
                         const ws::Side sd = side[slot[c] * 128 + r];
                         const bool valid = sd.flags & 1u, active = (sd.flags >> 1) & 1u;
@@ -923,7 +711,7 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
                             tc_fence_before();
                             named_bar_sync(bar_id, kGT);
                             if (issuer)
-                                ws::ws_issue(st, 1, 0, tmem_base, Cfg::kColOnes, col_a, col_d, &st->mma_bar[q]);
+                                ws::ws_issue(st, 1, 0, tmem_base, col_a, col_d, &st->mma_bar[q]);
                         } else {
                             float qv = 0.0f;
                             if (KIND == kKindStats) {
@@ -965,26 +753,33 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
                                 }
                             }
                             mbar_arrive(&st->empty[slot[c]]);
+                            if (rec && blockIdx.x == 0 && tile[c] < 1024) p.dbg[8192 + 4 * tile[c] + 3] = clock64();
                         }
                     }
                     if (rec) c_epi += clock64() - t0;
                 }
             }
         }
+        if (rec && g == 0)
+            p.dbg[blockIdx.x * 32 + 14] = clock64();  // MLP group 0 loop end (clock64, minus start below)
         if (rec) {
-            p.dbg[blockIdx.x * 16 + 8 + 2 * g + 0] = c_wait;
-            p.dbg[blockIdx.x * 16 + 8 + 2 * g + 1] = c_epi;
+            p.dbg[blockIdx.x * 32 + 8 + 2 * g + 0] = c_wait;
+            p.dbg[blockIdx.x * 32 + 8 + 2 * g + 1] = c_epi;
         }
     }
 
     // ---- teardown + deterministic CTA reduction, then last-CTA-done ----
     tc_fence_before();
     __syncthreads();
-    if (p.dbg && tid == 0) {
+    if (kTiming && p.dbg && tid == 0) {
         unsigned long long g_end;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
-        p.dbg[blockIdx.x * 16 + 12] = g_start;
-        p.dbg[blockIdx.x * 16 + 13] = g_end;
+        p.dbg[blockIdx.x * 32 + 14] -= c_start;
+        for (int q = 16; q < 20; ++q)
+            p.dbg[blockIdx.x * 32 + q] -= c_start;
+        p.dbg[blockIdx.x * 32 + 15] = clock64() - c_start;  // CTA end
+        p.dbg[blockIdx.x * 32 + 12] = g_start;
+        p.dbg[blockIdx.x * 32 + 13] = g_end;
     }
     if (warp == 0)
         tmem_dealloc(tmem_base, 512);
@@ -1451,34 +1246,8 @@ __global__ void realize_kernel(const float *q, const float *u, int32_t *counts, 
 // ===========================================================================
 // launch wrappers (called from the C ABI layer)
 // ===========================================================================
-template <int KIND>
-static cudaError_t infer_occupancy(size_t smem, int *occ) {
-    cudaFuncAttributes a{};
-    cudaError_t e = cudaFuncGetAttributes(&a, infer_kernel<KIND>);
-    if (e != cudaSuccess)
-        return e;
-    if (smem > 48 * 1024) {
-        e = cudaFuncSetAttribute(infer_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess)
-            return e;
-    }
-    // registers: allocation granule 8 per thread, warp granule 256 -> per-CTA regs
-    const int regs = ((a.numRegs + 7) / 8) * 8 * kInferThreads;
-    const int by_regs = 65536 / (regs > 0 ? regs : 1);
-    const int by_smem = (228 * 1024) / (int)(smem + a.sharedSizeBytes + 1024);
-    int o = by_regs < by_smem ? by_regs : by_smem;
-    if (KIND != kKindHeuristic && o > (int)(512u / kTmemCols))
-        o = (int)(512u / kTmemCols);  // TMEM columns per SM
-    if (o > 8)
-        o = 8;
-    *occ = o < 1 ? 1 : o;
-    return cudaSuccess;
-}
-
 size_t infer_smem_bytes(int kind, const InferParams &p) {
-    if (kind == kKindHeuristic)
-        return sizeof(InferSmemHeader) + 64;
-    return p.blob_bytes + sizeof(InferSmemHeader) + 64;
+    return kind == kKindHeuristic ? 0 : p.blob_bytes;
 }
 
 // Pipeline shape (encoder groups GE, MLP groups GM, chains per MLP group P).
@@ -1488,7 +1257,6 @@ static cudaError_t launch_ws_cfg(const InferParams &p, int num_sms, cudaStream_t
     switch (p.ws_cfg) {
     case 1: return launch_ws<KIND, 2, 2, 1>(p, num_sms, stream, grid_out);
     case 2: return launch_ws<KIND, 2, 2, 2>(p, num_sms, stream, grid_out);
-    case 3: return launch_ws<KIND, 2, 2, 3>(p, num_sms, stream, grid_out);
     case 4: return launch_ws<KIND, 2, 3, 1>(p, num_sms, stream, grid_out);
     case 5: return launch_ws<KIND, 2, 4, 1>(p, num_sms, stream, grid_out);
     case 6: return launch_ws<KIND, 2, 2, 1, 2>(p, num_sms, stream, grid_out);
@@ -1508,19 +1276,18 @@ cudaError_t launch_infer(int kind, const InferParams &p, int num_sms, cudaStream
     case kKindStats: return launch_ws_cfg<kKindStats>(p, num_sms, stream, grid_out);
     default: break;
     }
-    const uint64_t tiles = (p.n + kTileM - 1) / kTileM;
-    const size_t smem = infer_smem_bytes(kind, p);
     int occ = 1;
-    cudaError_t e = infer_occupancy<kKindHeuristic>(smem, &occ);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, infer_kernel, kInferThreads, 0);
     if (e != cudaSuccess)
         return e;
-    uint64_t grid = (uint64_t)num_sms * (uint64_t)occ;
-    if (grid > tiles)
-        grid = tiles;
+    uint64_t grid = (uint64_t)num_sms * (uint64_t)(occ < 1 ? 1 : occ);
+    const uint64_t blocks = (p.n + kInferThreads - 1) / kInferThreads;
+    if (grid > blocks)
+        grid = blocks;
     if (grid < 1)
         grid = 1;
     *grid_out = (uint32_t)grid;
-    infer_kernel<kKindHeuristic><<<(uint32_t)grid, kInferThreads, smem, stream>>>(p);
+    infer_kernel<<<(uint32_t)grid, kInferThreads, 0, stream>>>(p);
     return cudaGetLastError();
 }
 
