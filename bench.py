@@ -34,11 +34,12 @@ sys.path.insert(0, ROOT)
 METRIC = "path vertices/sec (RRSNet+normalized RRS+compaction) at 1/2/4/8 B200"
 N_LOCAL = 1920 * 1080
 ALG_BYTES_INFER = 56 + 8   # K-A: reads p01 12, wo01 8, rough 4, t_x 12, i_pixel 12, key 8; writes q_orig 4 + u 4
-# K-A's binding resource is L2 scattered-gather throughput: hash-grid gathers per vertex
-# in 8-byte-gather equivalents (a 16-byte gather costs 1.28, measured): 7 hashed levels x (4 edge pairs x 1.28
-# + 0.5 unpaired) + dense level 0 (4 x 1.28); ceiling = 296 G/s random 8-byte gathers from a 2 MiB table
-# (profiles/r01_microbench_gather_bw.txt, tools/gather_bw.cu).
-GATHER_UNITS_PER_VERTEX = 7 * (4 * 1.28 + 0.5) + 4 * 1.28
+# K-A's binding resource is L2 scattered-gather throughput, counted in random 8-byte
+# gather requests per vertex.  AID (fp16 tables): 7 hashed levels x (4 edge pairs + 0.5 unpaired corners) +
+# dense level 0 (4 pairs) = 35.5 8-byte requests.  NRRS (fp32 tables): the same 35.5 requests, 32 of them
+# 16-byte pairs that cost 1.28 units each (measured).  Ceiling: 296 G random 8-byte gathers/s from a 2 MiB
+# table (profiles/r01_microbench_gather_bw.txt, tools/gather_bw.cu).
+GATHER_UNITS_PER_VERTEX = {"aid": 7 * 4.5 + 4, "nrrs": 7 * (4 * 1.28 + 0.5) + 4 * 1.28}
 GATHER_CEILING_PER_S = 296e9
 STAGE_READ, STAGE_WRITE = 56, 8  # SURVEY.md 8d per-vertex compulsory bytes (+ 8 B per spawned slot record)
 
@@ -418,6 +419,42 @@ def main():
             extra[name] = {"vertices_per_s": n / (statistics.mean(ts) / 1e3), "ms": statistics.mean(ts)}
             stg.close()
 
+    # ---- C1: 65,536 vertices is launch-bound; single-call latency and CUDA-graph
+    # replays of 1000 stage calls (K-A + K-B), same strategy and nets ----
+    c1 = None
+    if world == 1 and not args.no_extra:
+        n1 = 65536
+        hv1 = synthetic.gen_vertices(n1, n_pixels=n1)
+        dv1 = {k: torch.from_numpy(a.view(np.int64) if a.dtype == np.uint64 else a).to(dev)
+               for k, a in hv1.items() if k != "pixel"}
+        st1 = RrsStage(n1, nets, device=local)
+        o1 = st1.alloc_outputs(n1)
+        for _ in range(10):
+            st1.run(dv1, 2, strategy, rc=RateControl(), out=o1, sync=False)
+        torch.cuda.synchronize()
+        lat = []
+        for _ in range(50):
+            a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            st1.run(dv1, 2, strategy, rc=RateControl(), out=o1, sync=False)
+            z.record()
+            torch.cuda.synchronize()
+            lat.append(a.elapsed_time(z) * 1e3)
+        g = st1.capture(dv1, 2, strategy, o1, gain=RateControl().gain(), calls=100)
+        for _ in range(2):
+            g.replay()
+        torch.cuda.synchronize()
+        a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(10):
+            g.replay()
+        z.record()
+        torch.cuda.synchronize()
+        per_call_us = a.elapsed_time(z) * 1e3 / 1000
+        c1 = {"vertices": n1, "single_call_us": statistics.median(lat), "graph_us_per_call": per_call_us,
+              "graph_vertices_per_s": n1 / (per_call_us / 1e6), "calls_replayed": 1000}
+        st1.close()
+
     peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}
     hbm = peaks.get("hbm_gbs")
     peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)"
@@ -428,6 +465,7 @@ def main():
     prof = load_json(os.path.join(ROOT, "profiles", "ncu_summary.json")) or {}
     traffic = prof.get(f"infer_{args.variant}_dram_bytes_per_launch")
     stage_bytes = (STAGE_READ + STAGE_WRITE) * n + 8 * spawned
+    gu = GATHER_UNITS_PER_VERTEX[args.variant]
     line = {
         "metric": METRIC, "value": value, "unit": "vertices/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": 1e3 * total_s / args.steps, "higher_is_better": True,
@@ -442,9 +480,8 @@ def main():
                      "alg_bytes_per_vertex": ALG_BYTES_INFER, "peak_source": peak_src,
                      "stage_frac": (stage_bytes / (statistics.mean(step_ms) / 1e3) / 1e9) / hbm},
         "gather_roofline": {"bound": "l2_scattered_gathers", "unit": "gathers/s (8-byte equivalents)",
-                            "achieved": GATHER_UNITS_PER_VERTEX * n / infer_avg, "peak": GATHER_CEILING_PER_S,
-                            "frac": GATHER_UNITS_PER_VERTEX * n / infer_avg / GATHER_CEILING_PER_S,
-                            "units_per_vertex": GATHER_UNITS_PER_VERTEX,
+                            "achieved": gu * n / infer_avg, "peak": GATHER_CEILING_PER_S,
+                            "frac": gu * n / infer_avg / GATHER_CEILING_PER_S, "units_per_vertex": gu,
                             "peak_source": "measured, profiles/r01_microbench_gather_bw.txt"},
         "kernels_ms": {"infer": statistics.mean(infer_ms), "decide": statistics.mean(decide_ms),
                        "compact": statistics.mean(compact_ms)},
@@ -456,6 +493,8 @@ def main():
         line["e2e"] = e2e
     if extra:
         line["strategies"] = extra
+    if c1:
+        line["c1_launch_bound"] = c1
     if world == 1 and rank == 0 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args.variant)
     if rank == 0:

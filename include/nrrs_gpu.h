@@ -158,6 +158,11 @@ NRRS_API int nrrs_gpu_rrs_stage(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *d_v, u
                        const nrrs_stage_params *p, const nrrs_stage_out *d_out,
                        nrrs_stage_result *h_result);
 
+/* Synchronizes the context's stream and returns the scalars of the most recent
+ * stage call (e.g. after replaying a CUDA graph that captured nrrs_gpu_rrs_stage
+ * with h_result = NULL; the stage launches are graph-replay safe). */
+NRRS_API int nrrs_gpu_fetch_result(nrrs_gpu_ctx *ctx, nrrs_stage_result *h_result);
+
 /* Same call over HOST buffers (the reference-facing plugin path): copies the
  * SoA to the device, runs the stage, copies every non-NULL output back.
  * h_out->slots receives result.spawned records. */

@@ -183,7 +183,7 @@ struct nrrs_gpu_ctx {
     DevResult *d_res = nullptr;
     double *d_sum = nullptr;            // [0] local sum  [1] scratch sum
     unsigned long long *d_total = nullptr;
-    uint32_t decide_epoch = 0, compact_epoch = 0;
+    LaunchSync *d_sync = nullptr;  // [0] decide, [1] compact: device-side claim counter + look-back epoch
 
     // host-path pipeline: chunked H2D on copy_stream overlapped with K-A on `stream`
     cudaStream_t copy_stream = nullptr;
@@ -244,16 +244,6 @@ static int ensure_compact_scratch(nrrs_gpu_ctx *ctx, uint64_t count, uint32_t wo
     return NRRS_OK;
 }
 
-// 14-bit launch epochs; on wrap the state array is cleared once.
-static uint32_t next_epoch(nrrs_gpu_ctx *ctx, uint32_t &epoch, uint64_t *state, uint64_t cap) {
-    epoch = (epoch + 1) & 0x3FFFu;
-    if (epoch == 0) {
-        cudaMemsetAsync(state, 0, cap * sizeof(uint64_t), ctx->stream);
-        epoch = 1;
-    }
-    return epoch;
-}
-
 extern "C" {
 
 int nrrs_gpu_abi_version(void) { return NRRS_GPU_ABI_VERSION; }
@@ -295,10 +285,12 @@ int nrrs_gpu_create(int device, nrrs_gpu_ctx **out) {
     if (cudaMalloc(&ctx->d_misc, 16 * sizeof(uint32_t)) != cudaSuccess ||
         cudaMalloc(&ctx->d_res, sizeof(DevResult)) != cudaSuccess ||
         cudaMalloc(&ctx->d_sum, (kChunkSums + kMaxHostChunks) * sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&ctx->d_total, 4 * sizeof(unsigned long long)) != cudaSuccess) {
+        cudaMalloc(&ctx->d_total, 4 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&ctx->d_sync, 2 * sizeof(LaunchSync)) != cudaSuccess) {
         delete ctx;
         return NRRS_ECUDA;
     }
+    cudaMemset(ctx->d_sync, 0, 2 * sizeof(LaunchSync));
     cudaMemset(ctx->d_misc, 0, 16 * sizeof(uint32_t));
     cudaMemset(ctx->d_res, 0, sizeof(DevResult));
     cudaMemset(ctx->d_sum, 0, (kChunkSums + kMaxHostChunks) * sizeof(double));
@@ -313,7 +305,7 @@ int nrrs_gpu_destroy(nrrs_gpu_ctx *ctx) {
     cudaStreamSynchronize(ctx->stream);
     void *ptrs[] = {ctx->d_stat_grid, ctx->d_rrs_grid, ctx->blob_stat.ptr, ctx->blob_rrs.ptr, ctx->blob_both.ptr,
                     ctx->d_q, ctx->d_u, ctx->d_parts, ctx->d_part_counts, ctx->d_tile_state, ctx->d_ctile_state,
-                    ctx->d_misc, ctx->d_res, ctx->d_sum, ctx->d_total, ctx->st.p01, ctx->st.wo01, ctx->st.rough,
+                    ctx->d_misc, ctx->d_res, ctx->d_sum, ctx->d_total, ctx->d_sync, ctx->st.p01, ctx->st.wo01, ctx->st.rough,
                     ctx->st.weight, ctx->st.ipix, ctx->st.key, ctx->st.q_norm, ctx->st.q_real, ctx->st.q_orig,
                     ctx->st.u, ctx->st.k, ctx->st.offset, ctx->st.slots, ctx->st.decided};
     for (void *p : ptrs)
@@ -679,9 +671,9 @@ static int run_decide(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_stage_params *p,
     dp.offset = o->offset;
     dp.slots = o->slots;
     dp.tile_state = ctx->d_tile_state;
-    dp.tile_counter = ctx->d_misc + 1;
+    dp.sync = ctx->d_sync + 0;
+    dp.state_cap = (uint32_t)ctx->cap_tiles;
     dp.num_tiles = decide_tiles(n);
-    dp.epoch = next_epoch(ctx, ctx->decide_epoch, ctx->d_tile_state, ctx->cap_tiles);
     dp.err_flag = ctx->d_misc + 3;
     dp.total_out = total_out;
     dp.res = res;
@@ -769,6 +761,13 @@ int nrrs_gpu_rrs_stage(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, 
     if (h_result)
         return fetch_result(ctx, h_result);
     return NRRS_OK;
+}
+
+int nrrs_gpu_fetch_result(nrrs_gpu_ctx *ctx, nrrs_stage_result *h_result) {
+    if (!ctx || !h_result)
+        return NRRS_EINVAL;
+    CK(ctx, cudaSetDevice(ctx->device));
+    return fetch_result(ctx, h_result);
 }
 
 int nrrs_gpu_stage_factors(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, const nrrs_stage_params *p,
@@ -863,9 +862,9 @@ int nrrs_gpu_compact(nrrs_gpu_ctx *ctx, const void *d_in, const uint8_t *d_used,
         cp.out = d_out;
         cp.count_out = cnt;
         cp.tile_state = ctx->d_ctile_state;
-        cp.tile_counter = ctx->d_misc + 2;
+        cp.sync = ctx->d_sync + 1;
+        cp.state_cap = (uint32_t)ctx->cap_ctiles;
         cp.num_tiles = compact_tiles(count, record_words);
-        cp.epoch = next_epoch(ctx, ctx->compact_epoch, ctx->d_ctile_state, ctx->cap_ctiles);
         CK(ctx, launch_compact(record_words, cp, ctx->stream));
         ctx->launches += 1;
     }
@@ -898,9 +897,9 @@ int nrrs_gpu_compact_dev(nrrs_gpu_ctx *ctx, const void *d_in, const uint8_t *d_u
     cp.out = d_out;
     cp.count_out = cnt;
     cp.tile_state = ctx->d_ctile_state;
-    cp.tile_counter = ctx->d_misc + 2;
+    cp.sync = ctx->d_sync + 1;
+    cp.state_cap = (uint32_t)ctx->cap_ctiles;
     cp.num_tiles = compact_tiles(max_count, record_words);
-    cp.epoch = next_epoch(ctx, ctx->compact_epoch, ctx->d_ctile_state, ctx->cap_ctiles);
     CK(ctx, launch_compact(record_words, cp, ctx->stream));
     ctx->launches += 1;
     return NRRS_OK;
@@ -982,9 +981,9 @@ int nrrs_gpu_plan_spawns(nrrs_gpu_ctx *ctx, const int32_t *d_counts, uint64_t n,
     dp.capacity = capacity;
     dp.offset = d_offset;
     dp.tile_state = ctx->d_tile_state;
-    dp.tile_counter = ctx->d_misc + 1;
+    dp.sync = ctx->d_sync + 0;
+    dp.state_cap = (uint32_t)ctx->cap_tiles;
     dp.num_tiles = decide_tiles(n);
-    dp.epoch = next_epoch(ctx, ctx->decide_epoch, ctx->d_tile_state, ctx->cap_tiles);
     dp.err_flag = ctx->d_misc + 3;
     dp.total_out = ctx->d_total + 2;
     CK(ctx, launch_decide(1, dp, ctx->stream));

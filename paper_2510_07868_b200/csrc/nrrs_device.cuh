@@ -9,6 +9,8 @@
 #include <cstdint>
 #include <cuda_fp16.h>
 
+#include "nrrs_internal.h"
+
 namespace nrrs {
 
 // ---------------------------------------------------------------------------
@@ -306,8 +308,8 @@ __device__ __forceinline__ void tmem_ld16x2(uint32_t ta, uint32_t tb, float (&va
 // Decoupled look-back tile state: [63:62] flag (1 = aggregate, 2 = inclusive
 // prefix), [61:48] launch epoch, [47:0] value.  Entries written by an earlier
 // launch carry another epoch and read as "not yet published", so the state
-// array never needs a memset between launches (the host clears it only when
-// the 14-bit epoch wraps).
+// array never needs a memset between launches (LaunchSync clears it when the
+// 14-bit epoch wraps).
 // ---------------------------------------------------------------------------
 constexpr uint64_t kFlagAgg = 1ull << 62;
 constexpr uint64_t kFlagPrefix = 2ull << 62;
@@ -400,11 +402,32 @@ __device__ __forceinline__ uint64_t lookback_warp(uint64_t *state, uint32_t tile
 
 // Claims the next tile in launch order; the CTA that claims the last tile
 // resets the counter for the next launch (no claims can follow it).
-__device__ __forceinline__ uint32_t claim_tile(uint32_t *counter, uint32_t num_tiles) {
-    const uint32_t t = atomicAdd(counter, 1u);
-    if (t == num_tiles - 1)
-        atomicExch(counter, 0u);
-    return t;
+// Per-kernel launch bookkeeping, kept on the device so a stage captured in a
+// CUDA graph replays correctly: claim = [63:32] launch epoch | [31:0] tiles
+// claimed.  One atomic hands a CTA both its tile (launch order) and the epoch
+// that tags its look-back states; the last CTA to finish resets the count,
+// advances the epoch and, when the 14-bit tag wraps, clears the state array.
+__device__ __forceinline__ uint32_t claim_tile_epoch(LaunchSync *s, uint32_t *epoch) {
+    const unsigned long long v = atomicAdd(&s->claim, 1ull);
+    *epoch = (uint32_t)(v >> 32);
+    return (uint32_t)v;
+}
+
+// Thread 0 of every CTA, after the CTA's last look-back access.
+__device__ __forceinline__ void finish_launch(LaunchSync *s, uint64_t *state, uint32_t state_cap, uint32_t epoch) {
+    __threadfence();
+    if (atomicAdd(&s->done, 1u) != gridDim.x - 1)
+        return;
+    __threadfence();
+    uint32_t next = epoch + 1u;
+    if ((next & 0x3FFFu) == 0u) {  // tag wrap: no stale state may carry a reusable tag
+        for (uint32_t i = 0; i < state_cap; ++i)
+            state[i] = 0ull;
+        next += 1u;
+    }
+    s->done = 0u;
+    __threadfence();
+    atomicExch(&s->claim, (unsigned long long)next << 32);
 }
 
 }  // namespace nrrs

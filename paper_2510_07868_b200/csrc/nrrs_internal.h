@@ -7,6 +7,14 @@
 
 namespace nrrs {
 
+// Device-side launch bookkeeping of the look-back kernels (nrrs_device.cuh):
+// claim = [63:32] epoch | [31:0] tiles claimed; done = CTAs finished.
+struct LaunchSync {
+    unsigned long long claim;
+    unsigned int done;
+    unsigned int pad;
+};
+
 // infer_kernel template kinds
 enum : int {
     kKindHeuristic = 0,  // Fixed / Throughput / depth-1 pin (no MMA)
@@ -117,9 +125,9 @@ struct DecideParams {
     uint32_t *offset;
     uint32_t *slots;
     uint64_t *tile_state;
-    uint32_t *tile_counter;
+    uint32_t state_cap;     // entries of tile_state (cleared on epoch wrap)
+    LaunchSync *sync;       // device-side claim counter + epoch (graph-replay safe)
     uint32_t num_tiles;
-    uint32_t epoch;
     uint32_t *err_flag;
     unsigned long long *total_out;
     DevResult *res;
@@ -133,9 +141,9 @@ struct CompactParams {
     void *out;
     uint32_t *count_out;
     uint64_t *tile_state;
-    uint32_t *tile_counter;
+    uint32_t state_cap;
+    LaunchSync *sync;
     uint32_t num_tiles;
-    uint32_t epoch;
 };
 
 size_t infer_smem_bytes(int kind, const InferParams &p);

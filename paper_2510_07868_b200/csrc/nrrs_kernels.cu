@@ -913,7 +913,7 @@ struct Decide2Smem {
     uint32_t incl[kBSub];
     uint32_t warp_tot[kBT / 32];
     unsigned long long prefix;
-    uint32_t tile;
+    uint32_t tile, epoch;
 };
 
 template <int SRC>  // 0: counts from (q, u) with normalization; 1: counts given (plan_spawns)
@@ -922,9 +922,9 @@ __global__ void __launch_bounds__(kBT) decide2_kernel(DecideParams p) {
     Decide2Smem &sm = *reinterpret_cast<Decide2Smem *>(dsm);
     const int tid = threadIdx.x;
     if (tid == 0)
-        sm.tile = claim_tile(p.tile_counter, p.num_tiles);
+        sm.tile = claim_tile_epoch(p.sync, &sm.epoch);
     __syncthreads();
-    const uint32_t tile = sm.tile;
+    const uint32_t tile = sm.tile, epoch = sm.epoch;
     const uint64_t tbase = (uint64_t)tile * kBTile;
 
     bool apply = false;
@@ -1007,7 +1007,7 @@ __global__ void __launch_bounds__(kBT) decide2_kernel(DecideParams p) {
     uint32_t agg = 0;
     block_scan_excl<kBT>(my_total, sm.warp_tot, agg);
     if (tid < 32) {
-        const uint64_t ex = lookback_warp(p.tile_state, tile, agg, p.epoch);
+        const uint64_t ex = lookback_warp(p.tile_state, tile, agg, epoch);
         if (tid == 0)
             sm.prefix = ex;
     }
@@ -1074,6 +1074,8 @@ __global__ void __launch_bounds__(kBT) decide2_kernel(DecideParams p) {
             p.res->overflow = total > spawned ? 1u : 0u;
         }
     }
+    if (tid == 0)
+        finish_launch(p.sync, p.tile_state, p.state_cap, epoch);
 }
 
 template <int W, int IPT>
@@ -1088,9 +1090,9 @@ __global__ void __launch_bounds__(kBT) compact2_kernel(CompactParams p) {
     uint32_t *tile_s = reinterpret_cast<uint32_t *>(prefix + 1);
     const int tid = threadIdx.x;
     if (tid == 0)
-        *tile_s = claim_tile(p.tile_counter, p.num_tiles);
+        tile_s[0] = claim_tile_epoch(p.sync, tile_s + 1);
     __syncthreads();
-    const uint32_t tile = *tile_s;
+    const uint32_t tile = tile_s[0], epoch = tile_s[1];
     const uint64_t tbase = (uint64_t)tile * kTile;
     uint64_t count = p.count;
     if (p.count_in) {
@@ -1113,7 +1115,7 @@ __global__ void __launch_bounds__(kBT) compact2_kernel(CompactParams p) {
     uint32_t agg = 0;
     block_scan_excl<kBT>(my_cnt, warp_tot, agg);
     if (tid < 32) {
-        const uint64_t ex = lookback_warp(p.tile_state, tile, agg, p.epoch);
+        const uint64_t ex = lookback_warp(p.tile_state, tile, agg, epoch);
         if (tid == 0)
             *prefix = ex;
     }
@@ -1145,6 +1147,8 @@ __global__ void __launch_bounds__(kBT) compact2_kernel(CompactParams p) {
     }
     if (tile == p.num_tiles - 1 && tid == 0)
         *p.count_out = (uint32_t)(*prefix + agg);
+    if (tid == 0)
+        finish_launch(p.sync, p.tile_state, p.state_cap, epoch);
 }
 
 // ===========================================================================

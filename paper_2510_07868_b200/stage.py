@@ -199,6 +199,41 @@ class RrsStage:
                                                                  C.byref(oc), None))
         return out, None
 
+    def capture(self, vertices: Dict[str, torch.Tensor], depth: int, strategy: Strategy, out: StageOutputs,
+                gain: float = 1.0, eps_div: float = 0.0, calls: int = 1) -> "torch.cuda.CUDAGraph":
+        """Captures `calls` stage calls (K-A factors + K-B decide, no host sync) into a CUDA
+        graph.  Every launch is replay-safe (device-side look-back epochs, self-resetting
+        counters); gain and sizes are baked in, so re-capture when RateControl's gain
+        changes.  One eager call first does any scratch allocation outside the capture.
+        Read the scalars of the last replay with fetch_result()."""
+        n = int(vertices["p01"].shape[0]) if vertices["p01"].dim() == 2 else vertices["p01"].numel() // 3
+        p = self.params(depth, strategy, gain, eps_div)
+        soa = vertex_soa(vertices)
+        oc = out.c()
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(side):
+            self.ctx.bind_stream()
+            _capi.check(self.handle, self.ctx.lib.nrrs_gpu_rrs_stage(self.handle, C.byref(soa), n, C.byref(p),
+                                                                     C.byref(oc), None))
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.ctx.bind_stream()
+            for _ in range(int(calls)):
+                _capi.check(self.handle, self.ctx.lib.nrrs_gpu_rrs_stage(self.handle, C.byref(soa), n, C.byref(p),
+                                                                         C.byref(oc), None))
+        self.ctx.bind_stream()
+        return g
+
+    def fetch_result(self) -> StageResult:
+        """Scalars of the most recent stage call (e.g. after a graph replay)."""
+        self.ctx.bind_stream()
+        r = _capi.StageResultC()
+        _capi.check(self.handle, self.ctx.lib.nrrs_gpu_fetch_result(self.handle, C.byref(r)))
+        return StageResult.from_c(r)
+
     def run_host(self, vertices: Dict[str, np.ndarray], depth: int, strategy: Strategy,
                  rc: Optional[RateControl] = None, eps_div: float = 0.0,
                  out: Optional[Dict[str, np.ndarray]] = None):

@@ -343,3 +343,28 @@ def test_host_buffer_pipeline_multi_chunk_neural(nets):
     assert hres.nonfinite == dres.nonfinite > 0
     np.testing.assert_array_equal(host_out["q_norm"], _np(dev_out.q_norm))
     np.testing.assert_array_equal(host_out["slots"][:hres.spawned], _np(dev_out.slots)[:dres.spawned].view(np.uint32))
+
+
+def test_cuda_graph_replay_matches_direct_call_across_epoch_wrap():
+    """The stage captured in a CUDA graph (K-A + K-B, device-side look-back epochs) replays to
+    the same outputs as a direct call -- also after the 14-bit look-back epoch wraps (16384
+    decide launches), when the last CTA clears the tile states."""
+    on = orc.OracleNets(orc.VARIANT_AID, seed=1, randomize=True)
+    n = 100003
+    v = to_dev(orc.gen_vertices(n))
+    st = _stage(n, on)
+    strat = Strategy(StrategyKind.AidNrrs)
+    ref, rres = st.run(v, 2, strat, rc=RateControl(), full=True)
+    ref = {k: _np(getattr(ref, k)).copy() for k in ("q_norm", "q_real", "k", "offset", "slots")}
+    out = st.alloc_outputs(n, full=True)
+    g = st.capture(v, 2, strat, out, gain=RateControl().gain())
+    for reps in (1, 200, 16400):
+        for key in ("q_norm", "k", "slots"):
+            getattr(out, key).zero_()
+        for _ in range(reps):
+            g.replay()
+        res = st.fetch_result()
+        assert (res.spawned, res.total, res.dropped) == (rres.spawned, rres.total, rres.dropped)
+        for key in ("q_norm", "q_real", "k", "offset"):
+            np.testing.assert_array_equal(_np(getattr(out, key)), ref[key], err_msg=f"{reps}:{key}")
+        np.testing.assert_array_equal(_np(out.slots)[:res.spawned], ref["slots"][:res.spawned])
