@@ -418,6 +418,28 @@ def main():
                 ts.append(a.elapsed_time(b))
             extra[name] = {"vertices_per_s": n / (statistics.mean(ts) / 1e3), "ms": statistics.mean(ts)}
             stg.close()
+        # render-like, spatially coherent batch in pixel order, same strategy and nets
+        hc = synthetic.gen_cornell_vertices(1920, 1080)
+        dc = {k: torch.from_numpy(a.view(np.int64) if a.dtype == np.uint64 else a).to(dev)
+              for k, a in hc.items() if k != "pixel"}
+        stg = RrsStage(hc["roughness"].shape[0], nets, device=local)
+        o2 = stg.alloc_outputs(hc["roughness"].shape[0])
+        for _ in range(3):
+            stg.run(dc, 2, strategy, rc=None, out=o2, sync=False)
+        ts = []
+        for _ in range(5):
+            flush.zero_()
+            a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            stg.run(dc, 2, strategy, rc=None, out=o2, sync=False)
+            z.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(z))
+        extra[f"{args.variant}-nrrs-cornell-coherent"] = {
+            "vertices_per_s": hc["roughness"].shape[0] / (statistics.mean(ts) / 1e3), "ms": statistics.mean(ts),
+            "batch": "1920x1080 first hits of a closed Cornell-style box, pixel order (synthetic.gen_cornell_vertices)"}
+        stg.close()
+        del dc
 
     # ---- C1: 65,536 vertices is launch-bound; single-call latency and CUDA-graph
     # replays of 1000 stage calls (K-A + K-B), same strategy and nets ----

@@ -81,3 +81,61 @@ def gen_vertices(n: int, n_pixels: int | None = None, frame: int = 0, first: int
 def split_bound_factors(n: int, first: int = 0) -> np.ndarray:
     g = VecRng(0xACC02, np.arange(first, first + n, dtype=np.uint64))
     return g.next_float() * np.float32(4.0)
+
+
+def gen_cornell_vertices(width: int, height: int, frame: int = 0) -> dict:
+    """Render-like, spatially coherent depth-2 batch in pixel order (SURVEY.md 8d "render-derived
+    batches"): the first surface hit of each pixel's primary ray in a closed unit box seen from
+    inside (camera (0.5, 0.5, 0.02) looking +z), walls at 0 and 1 on every axis plus one block.
+    p01 is the hit point (walls give p = 0 and p = 1 exactly: the encoder's clamp edge),
+    wo01 the spherical direction back to the camera, roughness 1 on diffuse walls and 0.3 on the
+    block, t_x the Cornell albedos, i_pixel a smooth per-pixel estimate.  Not a renderer: an input
+    generator with the memory-access coherence of a real frame (the stage is otherwise unchanged)."""
+    n = width * height
+    pix = np.arange(n, dtype=np.uint64)
+    px = (pix % np.uint64(width)).astype(np.float64)
+    py = (pix // np.uint64(width)).astype(np.float64)
+    aspect = width / height
+    dx = ((px + 0.5) / width - 0.5) * aspect * 1.2
+    dy = (0.5 - (py + 0.5) / height) * 1.2
+    d = np.stack([dx, dy, np.ones(n)], axis=1)
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    o = np.array([0.5, 0.5, 0.02])
+    with np.errstate(divide="ignore", invalid="ignore"):
+        tw = np.full(n, np.inf)
+        face = np.zeros(n, np.int64)  # 0 left 1 right 2 floor 3 ceiling 4 back 5 block
+        for axis, lo_face, hi_face in ((0, 0, 1), (1, 2, 3)):
+            t_lo = np.where(d[:, axis] < 0, (0.0 - o[axis]) / d[:, axis], np.inf)
+            t_hi = np.where(d[:, axis] > 0, (1.0 - o[axis]) / d[:, axis], np.inf)
+            for t, f in ((t_lo, lo_face), (t_hi, hi_face)):
+                m = t < tw
+                tw = np.where(m, t, tw)
+                face = np.where(m, f, face)
+        t_back = (1.0 - o[2]) / d[:, 2]
+        m = t_back < tw
+        tw = np.where(m, t_back, tw)
+        face = np.where(m, 4, face)
+        bmin, bmax = np.array([0.18, 0.0, 0.45]), np.array([0.48, 0.55, 0.75])
+        t1 = (bmin - o) / d
+        t2 = (bmax - o) / d
+        tn = np.max(np.minimum(t1, t2), axis=1)
+        tf = np.min(np.maximum(t1, t2), axis=1)
+        hit_b = (tn <= tf) & (tn > 0) & (tn < tw)
+        tw = np.where(hit_b, tn, tw)
+        face = np.where(hit_b, 5, face)
+    p = np.clip(o + tw[:, None] * d, 0.0, 1.0)
+    for axis, lo_face, hi_face in ((0, 0, 1), (1, 2, 3)):  # walls exactly on the boundary
+        p[face == lo_face, axis] = 0.0
+        p[face == hi_face, axis] = 1.0
+    p[face == 4, 2] = 1.0
+    w = -d
+    theta = np.arccos(np.clip(w[:, 2], -1.0, 1.0)) / np.pi
+    phi = (np.arctan2(w[:, 1], w[:, 0]) / (2 * np.pi)) + 0.5
+    albedo = np.array([[0.63, 0.065, 0.05], [0.14, 0.45, 0.091], [0.725, 0.71, 0.68], [0.725, 0.71, 0.68],
+                       [0.725, 0.71, 0.68], [0.8, 0.8, 0.8]], np.float32)
+    rough = np.where(face == 5, 0.3, 1.0).astype(np.float32)
+    ipix = 0.5 + 0.3 * np.stack([np.sin(px / width * 6.0 + c) * np.cos(py / height * 4.0 - c)
+                                 for c in (0.0, 1.0, 2.0)], axis=1)
+    return {"p01": p.astype(np.float32), "wo01": np.stack([theta, phi], axis=1).astype(np.float32),
+            "roughness": rough, "weight": albedo[face], "i_pixel": ipix.astype(np.float32),
+            "path_key": root_path_key(pix.astype(np.uint32), frame), "pixel": pix.astype(np.uint32)}

@@ -368,3 +368,22 @@ def test_cuda_graph_replay_matches_direct_call_across_epoch_wrap():
         for key in ("q_norm", "q_real", "k", "offset"):
             np.testing.assert_array_equal(_np(getattr(out, key)), ref[key], err_msg=f"{reps}:{key}")
         np.testing.assert_array_equal(_np(out.slots)[:res.spawned], ref["slots"][:res.spawned])
+
+
+@pytest.mark.parametrize("kind", [orc.NRRS, orc.AID_NRRS])
+def test_coherent_cornell_batch_parity(kind):
+    """Render-like batch in pixel order (walls exactly at p = 0 / 1: the hash-grid clamp edge,
+    cx = res - 1) against the oracle."""
+    from paper_2510_07868_b200 import synthetic
+    on = orc.OracleNets(orc.VARIANT_AID if kind == orc.AID_NRRS else orc.VARIANT_NRRS, seed=1, randomize=True)
+    v = synthetic.gen_cornell_vertices(256, 160)
+    n = v["roughness"].shape[0]
+    assert (v["p01"] == 1.0).any() and (v["p01"] == 0.0).any()
+    ref = orc.rrs_stage(v, 2, n, queue_capacity_for(n), kind, on, gain=0.85, seed=0, threads=8)
+    st = _stage(n, on)
+    out, res = st.run(to_dev(v), 2, Strategy(StrategyKind(kind)), rc=RateControl(), full=True)
+    err = rel_err(_np(out.q_orig), ref["q_orig"], 1e-6)
+    assert err.max() <= REL_TOL, f"q_orig max rel err {err.max():.3e}"
+    assert rel_err(_np(out.q_norm), ref["q_norm"], 1e-6).max() <= REL_TOL
+    np.testing.assert_array_equal(_np(out.u), ref["u"])
+    assert np.count_nonzero(_np(out.k) != ref["k"]) <= max(3, n // 2000)
