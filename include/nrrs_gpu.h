@@ -163,6 +163,14 @@ NRRS_API int nrrs_gpu_rrs_stage(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *d_v, u
  * with h_result = NULL; the stage launches are graph-replay safe). */
 NRRS_API int nrrs_gpu_fetch_result(nrrs_gpu_ctx *ctx, nrrs_stage_result *h_result);
 
+/* Per-frame ADRRS divisor input, replaces the film loop of trace_frame
+ * (wavefront.cpp:238-243): *d_sum_out = sum over n_pixels of luminance(i_acc[p])
+ * (f32 luminance, f64 sum, fixed order).  eps_div = eps_scale *
+ * (float)(sum / n_pixels); in the tile-sharded mode sum the per-rank values in
+ * rank order first.  Asynchronous on the context stream. */
+NRRS_API int nrrs_gpu_film_luminance_sum(nrrs_gpu_ctx *ctx, const float *d_i_acc, uint64_t n_pixels,
+                                         double *d_sum_out);
+
 /* Same call over HOST buffers (the reference-facing plugin path): copies the
  * SoA to the device, runs the stage, copies every non-NULL output back.
  * h_out->slots receives result.spawned records. */

@@ -40,6 +40,7 @@ def build(force: bool = False, verbose: bool = False) -> pathlib.Path:
     build_dir.mkdir(exist_ok=True)
     log = []
     extra = ["-DNRRS_KERNEL_TIMING"] if os.environ.get("NRRS_KERNEL_TIMING") else []  # diagnostics build only
+    extra += [f"-D{d}" for d in os.environ.get("NRRS_EXTRA_DEFINES", "").split()]  # tuning experiments only
     for src in SOURCES:
         obj = build_dir / (src + ".o")
         cmd = [nvcc(), *NVCC_FLAGS, *extra, "-c", str(CSRC / src), "-o", str(obj)]

@@ -65,6 +65,7 @@ SIGNATURES = [
     ("nrrs_gpu_reserve", C.c_int, [_P, C.c_uint64, C.c_uint32]),
     ("nrrs_gpu_launch_count", C.c_uint64, [_P]),
     ("nrrs_gpu_fetch_result", C.c_int, [_P, C.POINTER(StageResultC)]),
+    ("nrrs_gpu_film_luminance_sum", C.c_int, [_P, _P, C.c_uint64, _P]),
     ("nrrs_gpu_set_weights", C.c_int, [_P, C.POINTER(NetWeights)]),
     ("nrrs_gpu_rrs_stage", C.c_int, [_P, C.POINTER(VertexSoA), C.c_uint64, C.POINTER(StageParams),
                                      C.POINTER(StageOut), C.POINTER(StageResultC)]),

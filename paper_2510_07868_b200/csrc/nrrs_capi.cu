@@ -763,6 +763,25 @@ int nrrs_gpu_rrs_stage(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, 
     return NRRS_OK;
 }
 
+int nrrs_gpu_film_luminance_sum(nrrs_gpu_ctx *ctx, const float *d_i_acc, uint64_t n_pixels, double *d_sum_out) {
+    if (!ctx || !d_sum_out || (n_pixels && !d_i_acc))
+        return NRRS_EINVAL;
+    CK(ctx, cudaSetDevice(ctx->device));
+    if (n_pixels == 0) {
+        CK(ctx, cudaMemsetAsync(d_sum_out, 0, sizeof(double), ctx->stream));
+        return NRRS_OK;
+    }
+    int rc = ensure_scratch(ctx, 1);
+    if (rc)
+        return rc;
+    uint64_t grid = (n_pixels + 4095) / 4096;
+    const uint64_t max_grid = ctx->cap_parts < (uint64_t)ctx->num_sms * 4 ? ctx->cap_parts : (uint64_t)ctx->num_sms * 4;
+    grid = grid < 1 ? 1 : (grid > max_grid ? max_grid : grid);
+    CK(ctx, launch_lum_sum(d_i_acc, n_pixels, ctx->d_parts, ctx->d_misc + 6, d_sum_out, (uint32_t)grid, ctx->stream));
+    ctx->launches += 1;
+    return NRRS_OK;
+}
+
 int nrrs_gpu_fetch_result(nrrs_gpu_ctx *ctx, nrrs_stage_result *h_result) {
     if (!ctx || !h_result)
         return NRRS_EINVAL;

@@ -153,6 +153,8 @@ uint32_t decide_tiles(uint64_t n);
 cudaError_t launch_decide(int src, const DecideParams &p, cudaStream_t stream);
 uint32_t compact_tiles(uint64_t count, uint32_t words);
 cudaError_t launch_compact(uint32_t words, const CompactParams &p, cudaStream_t stream);
+cudaError_t launch_lum_sum(const float *i_acc, uint64_t n, double *parts, uint32_t *counter, double *sum_out,
+                           uint32_t grid, cudaStream_t stream);
 cudaError_t launch_sum_check(const float *q, uint64_t n, double *parts, uint32_t *counter, uint32_t *err,
                              double *sum_out, uint32_t grid, cudaStream_t stream);
 cudaError_t launch_scale(float *q, uint64_t n, const double *sum, uint64_t n_pixels, const uint32_t *err,

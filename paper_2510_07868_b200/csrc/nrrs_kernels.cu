@@ -622,7 +622,7 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
             for (int c = 0; c < P; ++c) {
                 if (!live[c])
                     continue;
-                mbar_wait(&st->full[slot[c]], (tile[c] / S) & 1u);
+                mbar_wait_sleep(&st->full[slot[c]], (tile[c] / S) & 1u, 1000u);  // suspended, not spinning
                 if (rec && g == 0) p.dbg[blockIdx.x * 32 + 17] = clock64();  // last tile: full passed
                 if (rec && blockIdx.x == 0 && tile[c] < 1024) p.dbg[8192 + 4 * tile[c] + 2] = clock64();
                 if (issuer)
@@ -1204,6 +1204,51 @@ __global__ void __launch_bounds__(256) sum_check_kernel(const float *q, uint64_t
         *sum_out = tot;
         *counter = 0;
     }
+}
+
+// Per-frame ADRRS divisor input (wavefront.cpp:238-243): sum over pixels of the
+// f32 luminance of i_acc (left-to-right, no contraction, core.hpp:24-26), in f64,
+// per-CTA fixed tree then last-CTA-done reduction in CTA order.
+__global__ void __launch_bounds__(256) lum_sum_kernel(const float *i_acc, uint64_t n, double *parts,
+                                                      uint32_t *counter, double *sum_out) {
+    __shared__ double ws[8];
+    __shared__ uint32_t is_last;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t begin = n * blockIdx.x / gridDim.x, end = n * (blockIdx.x + 1) / gridDim.x;
+    double s = 0.0;
+    for (uint64_t i = begin + tid; i < end; i += 256)
+        s += (double)luminance(i_acc[3 * i], i_acc[3 * i + 1], i_acc[3 * i + 2]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0)
+        ws[warp] = s;
+    __syncthreads();
+    if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w)
+            t += ws[w];
+        parts[blockIdx.x] = t;
+        __threadfence();
+        is_last = atomicAdd(counter, 1u) == gridDim.x - 1 ? 1u : 0u;
+    }
+    __syncthreads();
+    if (!is_last)
+        return;
+    __threadfence();
+    if (tid == 0) {
+        double t = 0.0;
+        for (uint32_t b = 0; b < gridDim.x; ++b)
+            t += __ldcg(parts + b);
+        *sum_out = t;
+        *counter = 0;
+    }
+}
+
+cudaError_t launch_lum_sum(const float *i_acc, uint64_t n, double *parts, uint32_t *counter, double *sum_out,
+                           uint32_t grid, cudaStream_t stream) {
+    lum_sum_kernel<<<grid, 256, 0, stream>>>(i_acc, n, parts, counter, sum_out);
+    return cudaGetLastError();
 }
 
 __global__ void scale_kernel(float *q, uint64_t n, const double *sum, uint64_t n_pixels, const uint32_t *err,

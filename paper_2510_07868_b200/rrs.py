@@ -6,6 +6,8 @@ through the C ABI -- there is no CPU path.
 """
 from __future__ import annotations
 
+import numpy as np
+
 import ctypes as C
 import dataclasses
 import enum
@@ -195,3 +197,11 @@ def plan_spawns(counts: torch.Tensor, capacity: int, ctx=None) -> SpawnPlan:
 def _require_cuda(t: torch.Tensor, dtype) -> None:
     if not t.is_cuda or t.dtype != dtype or not t.is_contiguous():
         raise RuntimeError(f"expected a contiguous CUDA {dtype} tensor, got {t.dtype} on {t.device}")
+
+
+ADRRS_EPS_SCALE = 1e-4  # TraceConfig::adrrs_eps_scale (wavefront.hpp:172)
+
+
+def eps_div_from_luminance_sum(lum_sum: float, n_pixels: int, eps_scale: float = ADRRS_EPS_SCALE) -> float:
+    """eps_div = adrrs_eps_scale * float(lum_acc / n_pixels), f32 product (wavefront.cpp:242-243)."""
+    return float(np.float32(eps_scale) * np.float32(lum_sum / float(n_pixels)))

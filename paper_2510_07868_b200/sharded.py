@@ -23,11 +23,12 @@ import ctypes as C
 import dataclasses
 from typing import Callable, List, Optional
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
 from . import _capi
-from .rrs import RateControl, Strategy
+from .rrs import ADRRS_EPS_SCALE, RateControl, Strategy, eps_div_from_luminance_sum
 from .stage import RrsStage, StageOutputs, vertex_soa
 
 
@@ -84,6 +85,41 @@ def sharded_depth(local_sum: torch.Tensor, decide: Callable[[torch.Tensor], torc
                         f_norm_from_sums([float(x) for x in rank_sums_t.tolist()], n_pixels_total))
 
 
+def _gather_in_rank_order(local: torch.Tensor, group=None) -> torch.Tensor:
+    host = dist.get_backend(group) == "gloo" and local.is_cuda  # gloo exchanges host copies
+    src = local.cpu() if host else local
+    parts = [torch.zeros_like(src) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(parts, src, group=group)
+    return torch.cat(parts)
+
+
+def sharded_eps_div(local_lum_sum: torch.Tensor, n_pixels_total: int, eps_scale: float = ADRRS_EPS_SCALE,
+                    group=None) -> float:
+    """Per-frame exchange of SURVEY.md 8e: each rank's f64 sum of luminance(i_acc) over its
+    band, gathered and summed in rank order (the reference sums the film in pixel order,
+    wavefront.cpp:238-243), so every rank derives the same eps_div."""
+    total = 0.0
+    for x in _gather_in_rank_order(local_lum_sum.reshape(1).to(torch.float64), group).tolist():
+        total += x
+    return eps_div_from_luminance_sum(total, n_pixels_total, eps_scale)
+
+
+def broadcast_weights(nets, src: int = 0, group=None):
+    """Per publish() exchange of SURVEY.md 8e: rank `src`'s snapshot blocks (stat grid, stat MLP,
+    rrs grid for AID, rrs MLP; networks.cpp:199-204) are broadcast to every rank in place; the
+    caller then uploads them with set_weights.  Returns nets."""
+    for name in ("stat_grid", "stat_mlp", "rrs_grid", "rrs_mlp"):
+        a = getattr(nets, name)
+        if a.size == 0:
+            continue
+        t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32))
+        if dist.get_backend(group) == "nccl":
+            t = t.cuda()
+        dist.broadcast(t, src=src, group=group)
+        setattr(nets, name, t.cpu().numpy().astype(np.float32, copy=False))
+    return nets
+
+
 class ShardedRrsStage:
     """One rank of the tile-sharded stage (one GPU per process, NCCL over NVLink)."""
 
@@ -118,6 +154,15 @@ class ShardedRrsStage:
         _capi.check(st.handle, st.ctx.lib.nrrs_gpu_stage_decide(st.handle, n, C.byref(p), rs.data_ptr(),
                                                                 rs.numel(), C.byref(oc), self._total.data_ptr()))
         return self._total
+
+    def eps_div(self, i_acc_band: torch.Tensor, eps_scale: float = ADRRS_EPS_SCALE) -> float:
+        """Global per-frame ADRRS divisor guard from this rank's band of the film."""
+        return sharded_eps_div(self.stage.film_luminance_sum(i_acc_band), self.n_pixels_total, eps_scale,
+                               self.group)
+
+    def set_weights(self, nets, src: int = 0) -> None:
+        """publish(): broadcast rank src's snapshot, upload on every rank."""
+        self.stage.set_weights(broadcast_weights(nets, src, self.group))
 
     def run(self, vertices, depth: int, strategy: Strategy, rc: Optional[RateControl] = None,
             eps_div: float = 0.0, out: Optional[StageOutputs] = None):

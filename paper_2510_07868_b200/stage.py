@@ -26,7 +26,7 @@ import torch
 
 from . import _capi
 from .networks import NeuralRrs
-from .rrs import RateControl, Strategy, StrategyKind, queue_capacity_for
+from .rrs import ADRRS_EPS_SCALE, RateControl, Strategy, StrategyKind, eps_div_from_luminance_sum, queue_capacity_for
 
 VERTEX_FIELDS = ("p01", "wo01", "roughness", "weight", "i_pixel", "path_key")
 FIELD_SHAPES = {"p01": 3, "wo01": 2, "roughness": 1, "weight": 3, "i_pixel": 3, "path_key": 1}
@@ -226,6 +226,20 @@ class RrsStage:
                                                                          C.byref(oc), None))
         self.ctx.bind_stream()
         return g
+
+    def film_luminance_sum(self, i_acc: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Device f64 sum of luminance(i_acc[p]) over the film (wavefront.cpp:238-241), async."""
+        self.ctx.bind_stream()
+        n = i_acc.numel() // 3
+        out = out if out is not None else torch.empty(1, dtype=torch.float64, device=self.device)
+        _capi.check(self.handle, self.ctx.lib.nrrs_gpu_film_luminance_sum(self.handle, i_acc.data_ptr(), n,
+                                                                          out.data_ptr()))
+        return out
+
+    def eps_div(self, i_acc: torch.Tensor, eps_scale: float = ADRRS_EPS_SCALE) -> float:
+        """Per-frame ADRRS divisor guard (wavefront.cpp:238-243); syncs."""
+        return eps_div_from_luminance_sum(float(self.film_luminance_sum(i_acc).item()), i_acc.numel() // 3,
+                                          eps_scale)
 
     def fetch_result(self) -> StageResult:
         """Scalars of the most recent stage call (e.g. after a graph replay)."""

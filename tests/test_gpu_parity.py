@@ -387,3 +387,19 @@ def test_coherent_cornell_batch_parity(kind):
     assert rel_err(_np(out.q_norm), ref["q_norm"], 1e-6).max() <= REL_TOL
     np.testing.assert_array_equal(_np(out.u), ref["u"])
     assert np.count_nonzero(_np(out.k) != ref["k"]) <= max(3, n // 2000)
+
+
+def test_film_luminance_sum_and_eps_div():
+    """nrrs_gpu_film_luminance_sum vs the reference's sequential film loop (wavefront.cpp:238-243):
+    f64 sums agree to rounding, eps_div (f32) exactly."""
+    npx = 1920 * 1080 + 7
+    g = np.random.default_rng(3)
+    film = (g.random((npx, 3), dtype=np.float32) * np.float32(4.0)).astype(np.float32)
+    lum = (np.float32(0.2126) * film[:, 0] + np.float32(0.7152) * film[:, 1]) + np.float32(0.0722) * film[:, 2]
+    ref = float(np.cumsum(lum.astype(np.float64))[-1])  # sequential double sum
+    st = _stage(npx)
+    s = float(st.film_luminance_sum(torch.from_numpy(film).cuda()).item())
+    assert abs(s - ref) <= 1e-12 * ref
+    from paper_2510_07868_b200.rrs import eps_div_from_luminance_sum
+    assert st.eps_div(torch.from_numpy(film).cuda()) == eps_div_from_luminance_sum(ref, npx)
+    assert float(st.film_luminance_sum(torch.zeros((0, 3), device="cuda")).item()) == 0.0

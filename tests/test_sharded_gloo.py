@@ -126,3 +126,70 @@ def test_sharded_global_clip_on_overflow():
     assert ref["dropped"] > 0
     assert res[0][2] == min(int(np.sum(res[0][6])), cap) and res[0][2] + res[1][2] == cap
     assert res[0][8] == res[1][8] == 1  # overflow is a global, replicated event
+
+
+def _lum_f32(c):
+    """luminance (core.hpp:24-26), f32 left to right."""
+    c = c.astype(np.float32)
+    return (np.float32(0.2126) * c[:, 0] + np.float32(0.7152) * c[:, 1]) + np.float32(0.0722) * c[:, 2]
+
+
+def _film(npx):
+    g = np.random.default_rng(5)
+    return (g.random((npx, 3), dtype=np.float32) * np.float32(3.0)).astype(np.float32)
+
+
+def _worker_frame(rank, port, npx, result_q):
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, os.path.dirname(here))
+    from paper_2510_07868_b200 import NeuralRrs, NeuralRrsConfig, RrsVariant
+    from paper_2510_07868_b200.sharded import broadcast_weights, sharded_eps_div
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    film = _film(npx)
+    lo, hi = rank * npx // WORLD, (rank + 1) * npx // WORLD
+    local = 0.0
+    for v in _lum_f32(film[lo:hi]):  # per-rank stand-in for nrrs_gpu_film_luminance_sum
+        local += float(v)
+    eps = sharded_eps_div(torch.tensor([local], dtype=torch.float64), npx)
+    nets = NeuralRrs(NeuralRrsConfig(variant=RrsVariant.Aid, seed=1))
+    if rank == 0:
+        nets.randomize_for_benchmark()
+    broadcast_weights(nets, src=0)
+    result_q.put((rank, eps, float(nets.rrs_mlp[-1]), float(np.sum(nets.rrs_grid, dtype=np.float64)),
+                  float(np.sum(nets.stat_mlp, dtype=np.float64))))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_sharded_eps_div_and_weight_broadcast():
+    """Per-frame eps_div exchange and per-publish weight broadcast: every rank
+    gets the single-film eps_div (wavefront.cpp:238-243) and rank 0's snapshot."""
+    from paper_2510_07868_b200 import NeuralRrs, NeuralRrsConfig, RrsVariant
+    from paper_2510_07868_b200.rrs import eps_div_from_luminance_sum
+    npx = 5001
+    ctx = mp.get_context("spawn")
+    result_q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_frame, args=(r, port, npx, result_q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    res = sorted([result_q.get(timeout=240) for _ in range(WORLD)])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    lum_acc = 0.0
+    for v in _lum_f32(_film(npx)):  # the reference's sequential film loop
+        lum_acc += float(v)
+    eps_ref = float(np.float32(1e-4) * np.float32(lum_acc / npx))
+    assert eps_div_from_luminance_sum(lum_acc, npx) == eps_ref
+    assert res[0][1] == res[1][1] == eps_ref
+    ref = NeuralRrs(NeuralRrsConfig(variant=RrsVariant.Aid, seed=1)).randomize_for_benchmark()
+    for r in res:
+        assert r[2] == float(ref.rrs_mlp[-1])
+        assert r[3] == float(np.sum(ref.rrs_grid, dtype=np.float64))
+        assert r[4] == float(np.sum(ref.stat_mlp, dtype=np.float64))
