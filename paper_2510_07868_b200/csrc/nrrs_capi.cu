@@ -602,8 +602,6 @@ static int run_factors(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, 
     ip.accumulate = accumulate ? 1u : 0u;
     if (const char *ab = std::getenv("NRRS_DEBUG_ABLATE"))  // diagnostics only; results invalid
         ip.ablate = (uint32_t)std::atoi(ab);
-    if (const char *wc = std::getenv("NRRS_WS_CFG"))  // tuning sweeps only
-        ip.ws_cfg = (uint32_t)std::atoi(wc);
     unsigned long long *dbg = nullptr;
     const bool timing = std::getenv("NRRS_DEBUG_TIMING") != nullptr;  // diagnostics only
     if (timing) {

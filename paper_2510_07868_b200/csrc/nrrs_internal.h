@@ -106,7 +106,6 @@ struct InferParams {
     DevResult *res;
     uint32_t accumulate;  // chunked launches: add to res counters / sum_q instead of overwriting
     uint32_t ablate;   // debug only (env NRRS_DEBUG_ABLATE): bit0 skip grid gathers, bit1 skip MLP
-    uint32_t ws_cfg;          // pipeline variant (0 default; env NRRS_WS_CFG for tuning sweeps)
     unsigned long long *dbg;  // debug only (env NRRS_DEBUG_TIMING): per-CTA clock64 phase counters [grid][16]
 };
 

@@ -411,7 +411,7 @@ constexpr bool kTiming = true;
 constexpr bool kTiming = false;
 #endif
 
-template <int KIND, int GE, int GM, int P, int TPR>
+template <int KIND, int GE, int GM, int P, int TPR, bool HALF>  // HALF: fp16 RRSNet (AID) grid tables
 __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws_kernel(InferParams p) {
     using Cfg = ws::Cfg<GE, GM, P, TPR>;
     constexpr uint32_t kGT = Cfg::kGroupThreads;
@@ -516,10 +516,7 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
                 for (int q = 0; q < 8; ++q)
                     g8[q] = px * (float)(q + 1) + py;
             } else if (KIND == kKindAid) {
-                if (p.rrs_half)
-                    grid_encode4<true>(p.rrs_grid, p.grid, 4 * half, clamp01(px), clamp01(py), clamp01(pz), g8);
-                else
-                    grid_encode4<false>(p.rrs_grid, p.grid, 4 * half, clamp01(px), clamp01(py), clamp01(pz), g8);
+                grid_encode4<HALF>(p.rrs_grid, p.grid, 4 * half, clamp01(px), clamp01(py), clamp01(pz), g8);
             } else {
                 grid_encode4<false>(p.stat_grid, p.grid, 4 * half, clamp01(px), clamp01(py), clamp01(pz), g8);
             }
@@ -847,12 +844,12 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
     }
 }
 
-template <int KIND, int GE, int GM, int P, int TPR = 1>
+template <int KIND, int GE, int GM, int P, int TPR, bool HALF>
 static cudaError_t launch_ws(const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out) {
     using Cfg = ws::Cfg<GE, GM, P, TPR>;
     const size_t smem = ((p.blob_bytes + 127u) & ~127u) + Cfg::kSlots * 128 * sizeof(ws::Side) +
                         sizeof(ws::SmemTail) + 64;
-    cudaError_t e = cudaFuncSetAttribute(infer_ws_kernel<KIND, GE, GM, P, TPR>,
+    cudaError_t e = cudaFuncSetAttribute(infer_ws_kernel<KIND, GE, GM, P, TPR, HALF>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
         return e;
@@ -863,7 +860,7 @@ static cudaError_t launch_ws(const InferParams &p, int num_sms, cudaStream_t str
     if (grid < 1)
         grid = 1;
     *grid_out = (uint32_t)grid;
-    infer_ws_kernel<KIND, GE, GM, P, TPR><<<(uint32_t)grid, Cfg::kThreads, smem, stream>>>(p);
+    infer_ws_kernel<KIND, GE, GM, P, TPR, HALF><<<(uint32_t)grid, Cfg::kThreads, smem, stream>>>(p);
     return cudaGetLastError();
 }
 
@@ -1299,22 +1296,15 @@ size_t infer_smem_bytes(int kind, const InferParams &p) {
     return kind == kKindHeuristic ? 0 : p.blob_bytes;
 }
 
-// Pipeline shape (encoder groups GE, MLP groups GM, chains per MLP group P).
-// p.ws_cfg selects a tuned variant (0 = default); see DESIGN.md section 6.
+// Pipeline shape: 2 encoder groups, 3 MLP groups with one tile chain each, 1 thread per row (the
+// tuned default; the sweep over other shapes is recorded in DESIGN.md section 3a).
 template <int KIND>
 static cudaError_t launch_ws_cfg(const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out) {
-    switch (p.ws_cfg) {
-    case 1: return launch_ws<KIND, 2, 2, 1>(p, num_sms, stream, grid_out);
-    case 2: return launch_ws<KIND, 2, 2, 2>(p, num_sms, stream, grid_out);
-    case 4: return launch_ws<KIND, 2, 3, 1>(p, num_sms, stream, grid_out);
-    case 5: return launch_ws<KIND, 2, 4, 1>(p, num_sms, stream, grid_out);
-    case 6: return launch_ws<KIND, 2, 2, 1, 2>(p, num_sms, stream, grid_out);
-    case 7: return launch_ws<KIND, 1, 2, 1, 2>(p, num_sms, stream, grid_out);
-    case 8: return launch_ws<KIND, 2, 1, 1, 2>(p, num_sms, stream, grid_out);
-    case 9: return launch_ws<KIND, 1, 3, 1, 2>(p, num_sms, stream, grid_out);
-    default:  // tuned default: 2 encoder groups, 3 single-chain MLP groups
-        return launch_ws<KIND, 2, 3, 1>(p, num_sms, stream, grid_out);
+    if constexpr (KIND == kKindAid) {
+        if (p.rrs_half)
+            return launch_ws<KIND, 2, 3, 1, 1, true>(p, num_sms, stream, grid_out);
     }
+    return launch_ws<KIND, 2, 3, 1, 1, false>(p, num_sms, stream, grid_out);
 }
 
 cudaError_t launch_infer(int kind, const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out) {
