@@ -876,7 +876,10 @@ static cudaError_t launch_ws(const InferParams &p, int num_sms, cudaStream_t str
 constexpr int kBT = 512;            // threads
 constexpr int kBItems = 4;          // items per thread per sub-tile
 constexpr int kBSub = kBT * kBItems;  // 2048
-constexpr int kBSubs = 8;
+#ifndef NRRS_BSUBS
+#define NRRS_BSUBS 4
+#endif
+constexpr int kBSubs = NRRS_BSUBS;  // sub-tiles per CTA tile (sweep 8/4/2/1: DESIGN.md section 6)
 constexpr int kBTile = kBSub * kBSubs;  // 16384
 
 template <int NT>
