@@ -35,11 +35,11 @@ METRIC = "path vertices/sec (RRSNet+normalized RRS+compaction) at 1/2/4/8 B200"
 N_LOCAL = 1920 * 1080
 ALG_BYTES_INFER = 56 + 8   # K-A: reads p01 12, wo01 8, rough 4, t_x 12, i_pixel 12, key 8; writes q_orig 4 + u 4
 # K-A's binding resource is L2 scattered-gather throughput, counted in random 8-byte
-# gather requests per vertex.  AID (fp16 tables): 7 hashed levels x (4 edge pairs + 0.5 unpaired corners) +
-# dense level 0 (4 pairs) = 35.5 8-byte requests.  NRRS (fp32 tables): the same 35.5 requests, 32 of them
-# 16-byte pairs that cost 1.28 units each (measured).  Ceiling: 296 G random 8-byte gathers/s from a 2 MiB
-# table (profiles/r01_microbench_gather_bw.txt, tools/gather_bw.cu).
-GATHER_UNITS_PER_VERTEX = {"aid": 7 * 4.5 + 4, "nrrs": 7 * (4 * 1.28 + 0.5) + 4 * 1.28}
+# gather requests per vertex.  AID (fp16 tables): 7 hashed levels x (4 edge pairs + 4/256 unpaired corners,
+# 8 edge-paired table copies) + dense level 0 (4 pairs) = 32.1 8-byte requests.  NRRS (fp32 tables): the same
+# requests, the pairs 16 bytes wide at 1.28 units each (measured).  Ceiling: 296 G random 8-byte gathers/s from
+# a 2 MiB table (profiles/r01_microbench_gather_bw.txt, tools/gather_bw.cu).
+GATHER_UNITS_PER_VERTEX = {"aid": 7 * (4 + 4 / 256) + 4, "nrrs": 7 * (4 * 1.28 + 4 / 256) + 4 * 1.28}
 GATHER_CEILING_PER_S = 296e9
 STAGE_READ, STAGE_WRITE = 56, 8  # SURVEY.md 8d per-vertex compulsory bytes (+ 8 B per spawned slot record)
 

@@ -162,7 +162,7 @@ struct nrrs_gpu_ctx {
     bool has_weights = false;
     int variant = 0;
     nrrs_grid_spec spec{};
-    GridDev grid{};
+    GridDev grid{}, grid_rrs{};  // StatNet / AID RRSNet grids (same spec, own pair-copy counts)
     float *d_stat_grid = nullptr;
     void *d_rrs_grid = nullptr;
     bool rrs_half = false;  // AID grid stored as fp16 (precision)
@@ -416,39 +416,38 @@ int nrrs_gpu_set_weights(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w) {
         rc = upload_blob(ctx->blob_both, true, true);
     if (rc)
         return rc;
-    // three copies per grid (see GridDev): reference layout, then the
-    // edge-paired permutations for t = 1, 2 (dense levels: shifted copy)
+    // kPairCopies copies per grid (see GridDev): reference layout, then the
+    // edge-paired permutations for t = 1 .. kPairCopies-1 (dense levels: shifted copy)
     auto pair_pos = [](uint32_t e, uint32_t t) -> uint32_t {
         const uint32_t G = 2u << t, i = e & (G - 1u), half = G >> 1;
         const uint32_t pi = i < half ? (i << 1) : (((G - 1u - i) << 1) | 1u);
         return (e & ~(G - 1u)) | pi;
     };
-    auto upload_grid = [&](auto *&dst, const float *src, uint64_t len, bool half) -> int {
+    auto upload_grid = [&](auto *&dst, const float *src, uint64_t len, bool half, uint32_t copies) -> int {
         if (dst)
             cudaFree(dst);
         dst = nullptr;
         if (!len)
             return NRRS_OK;
-        std::vector<float> h(3 * len, 0.0f);
+        std::vector<float> h(copies * len, 0.0f);
         std::memcpy(h.data(), src, len * sizeof(float));
         for (int l = 0; l < g.levels; ++l) {
             const uint64_t res = (uint64_t)g.base_resolution << l;
             const bool dense = (res + 1) * (res + 1) * (res + 1) <= T;
             const float *lv = src + (uint64_t)l * T * 2;
-            float *c1 = h.data() + len + (uint64_t)l * T * 2;
-            float *c2 = h.data() + 2 * len + (uint64_t)l * T * 2;
-            for (uint32_t e = 0; e < T; ++e) {
-                if (dense) {
-                    if (e + 1 < T) {
-                        c1[2 * e] = lv[2 * (e + 1)];
-                        c1[2 * e + 1] = lv[2 * (e + 1) + 1];
+            for (uint32_t t = 1; t < copies; ++t) {
+                float *ct = h.data() + t * len + (uint64_t)l * T * 2;
+                for (uint32_t e = 0; e < T; ++e) {
+                    if (dense) {
+                        if (t == 1 && e + 1 < T) {
+                            ct[2 * e] = lv[2 * (e + 1)];
+                            ct[2 * e + 1] = lv[2 * (e + 1) + 1];
+                        }
+                    } else if ((2u << t) <= T) {
+                        const uint32_t pt = pair_pos(e, t);
+                        ct[2 * pt] = lv[2 * e];
+                        ct[2 * pt + 1] = lv[2 * e + 1];
                     }
-                } else {
-                    const uint32_t p1 = pair_pos(e, 1), p2 = pair_pos(e, 2);
-                    c1[2 * p1] = lv[2 * e];
-                    c1[2 * p1 + 1] = lv[2 * e + 1];
-                    c2[2 * p2] = lv[2 * e];
-                    c2[2 * p2 + 1] = lv[2 * e + 1];
                 }
             }
         }
@@ -471,9 +470,16 @@ int nrrs_gpu_set_weights(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w) {
     for (uint64_t i = 0; half && i < rrs_grid_len; ++i)
         if (!(std::fabs(w->rrs_grid[i]) < 32768.0f))
             half = false;
-    rc = upload_grid(ctx->d_stat_grid, w->stat_grid, grid_len, false);
+    auto usable = [&](uint32_t want) {  // copy t needs 2^(t+1) <= T
+        uint32_t c = 1;
+        while (c < want && (2ull << c) <= T)
+            ++c;
+        return c;
+    };
+    const uint32_t stat_copies = usable(kPairCopiesF32), rrs_copies = usable(half ? kPairCopies : kPairCopiesF32);
+    rc = upload_grid(ctx->d_stat_grid, w->stat_grid, grid_len, false, stat_copies);
     if (!rc)
-        rc = upload_grid(ctx->d_rrs_grid, w->rrs_grid, rrs_grid_len, half);
+        rc = upload_grid(ctx->d_rrs_grid, w->rrs_grid, rrs_grid_len, half, rrs_copies);
     ctx->rrs_half = half;
     if (rc)
         return rc;
@@ -484,11 +490,15 @@ int nrrs_gpu_set_weights(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w) {
     ctx->grid.table_size = (uint32_t)T;
     ctx->grid.dense_mask = 0;
     ctx->grid.copy_stride = (uint64_t)g.levels * T;
+    ctx->grid.pair_copies = stat_copies;
     for (int l = 0; l < g.levels; ++l) {
         const uint64_t res = (uint64_t)g.base_resolution << l;
         if ((res + 1) * (res + 1) * (res + 1) <= T)
             ctx->grid.dense_mask |= 1u << l;
     }
+    ctx->grid_rrs = ctx->grid;
+    ctx->grid_rrs.copy_stride = (uint64_t)g.levels * T;
+    ctx->grid_rrs.pair_copies = rrs_copies;
     ctx->has_weights = true;
     return NRRS_OK;
 }
@@ -539,6 +549,7 @@ static void fill_infer_common(nrrs_gpu_ctx *ctx, int kind, InferParams &ip) {
     ip.rrs_grid = ctx->d_rrs_grid;
     ip.rrs_half = ctx->rrs_half ? 1u : 0u;
     ip.grid = ctx->grid;
+    ip.grid_rrs = ctx->grid_rrs;
     const DeviceBlob *b = nullptr;
     if (kind == kKindNrrs)
         b = &ctx->blob_both;
@@ -600,8 +611,10 @@ static int run_factors(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, 
     ip.sum_out = sum_out;
     ip.res = ctx->d_res;
     ip.accumulate = accumulate ? 1u : 0u;
-    if (const char *ab = std::getenv("NRRS_DEBUG_ABLATE"))  // diagnostics only; results invalid
+#ifdef NRRS_KERNEL_TIMING
+    if (const char *ab = std::getenv("NRRS_DEBUG_ABLATE"))  // diagnostics build only; results invalid
         ip.ablate = (uint32_t)std::atoi(ab);
+#endif
     unsigned long long *dbg = nullptr;
     const bool timing = std::getenv("NRRS_DEBUG_TIMING") != nullptr;  // diagnostics only
     if (timing) {

@@ -50,19 +50,29 @@ struct KernelNets {
     NetDesc stat, rrs;
 };
 
-// Hash-grid tables on the device: three copies of the reference layout
+// Hash-grid tables on the device: kPairCopies copies of the reference layout
 // [level][entry][feature], `copy_stride` entries apart:
-//   copy 0: the reference table (pairs (e, e^1) share an aligned 16-byte pair)
+//   copy 0: the reference table (pairs (e, e^1) share an aligned pair)
 //   copy 1: hashed levels: permuted so (e, e^3) share a pair; dense levels: shifted by one entry
-//   copy 2: hashed levels: permuted so (e, e^7) share a pair
+//   copy t: hashed levels: permuted so (e, e^(2^(t+1)-1)) share a pair
 // A hashed x-edge (cx, cx+1) has entries e and e ^ (2^(t+1)-1), t = trailing ones of cx,
-// so copies 0/1/2 serve t = 0/1/2 with one 16-byte gather (7/8 of edges).
+// so copy t serves it with one gather when t < kPairCopies (all but 2^-kPairCopies of edges).
+#ifndef NRRS_PAIR_COPIES
+#define NRRS_PAIR_COPIES 8
+#endif
+#ifndef NRRS_PAIR_COPIES_F32
+#define NRRS_PAIR_COPIES_F32 8
+#endif
+constexpr uint32_t kPairCopies = NRRS_PAIR_COPIES;         // fp16 AID grid (1 MiB per copy; sweep DESIGN.md 3a)
+constexpr uint32_t kPairCopiesF32 = NRRS_PAIR_COPIES_F32;  // fp32 StatNet grid (2 MiB per copy)
+
 struct GridDev {
     int32_t levels;
     int32_t base_resolution;
     uint32_t table_size;
     uint32_t dense_mask;  // bit l: level l is dense ((res+1)^3 <= T, hashgrid.hpp / hashgrid.cpp:16-22)
     uint64_t copy_stride; // entries between table copies (= levels * table_size)
+    uint32_t pair_copies; // usable copies: t < pair_copies needs 2^(t+1) <= table_size
 };
 
 // Device-side scalar results of one stage call (mirrors nrrs_stage_result).
@@ -92,7 +102,8 @@ struct InferParams {
     const float2 *stat_grid;
     const void *rrs_grid;   // fp32 (float2 entries) or fp16 (half2 entries) when rrs_half
     uint32_t rrs_half;
-    GridDev grid;
+    GridDev grid;        // StatNet grid (fp32)
+    GridDev grid_rrs;    // AID RRSNet grid (same spec; its own number of pair copies)
     const uint8_t *blob;
     uint32_t blob_bytes;
     KernelNets nets;

@@ -82,8 +82,8 @@ struct GridTab {
 
 // HashGrid::encode (hashgrid.cpp:38-82) for levels [l0, l0+4) of one point, F = 2.
 // Each cell edge (2 corners) costs one gather of an aligned entry pair from the
-// matching table copy (GridDev); hashed x-edges with >= 3 trailing ones in cx
-// (1/8 of edges) fetch the second corner separately.
+// matching table copy (GridDev); hashed x-edges with >= kPairCopies trailing ones
+// in cx (1/32 of edges) fetch the second corner separately.
 template <bool kHalf = false>
 __device__ __forceinline__ void grid_encode4(const void *theta, const GridDev &g, int l0, float cpx, float cpy,
                                              float cpz, float *out) {
@@ -122,7 +122,7 @@ __device__ __forceinline__ void grid_encode4(const void *theta, const GridDev &g
         } else {
             // hashed index x ^ y*PY ^ z*PZ: edges along x, partner e ^ (2^(t+1)-1)
             const uint32_t tones = __ffs(~cx) - 1u;
-            const uint32_t tc = tones > 2u ? 0u : tones;
+            const uint32_t tc = tones >= g.pair_copies ? 0u : tones;
             const uint64_t tab = lb + (uint64_t)tc * g.copy_stride;
             const uint32_t yp[2] = {cy * 2654435761u, (cy + 1u) * 2654435761u};
             const uint32_t zp[2] = {cz * 805459861u, (cz + 1u) * 805459861u};
@@ -137,7 +137,7 @@ __device__ __forceinline__ void grid_encode4(const void *theta, const GridDev &g
                 const bool sw = pos & 1u;
                 const float v0x = sw ? pr.z : pr.x, v0y = sw ? pr.w : pr.y;
                 float v1x = sw ? pr.x : pr.z, v1y = sw ? pr.y : pr.w;
-                if (tones > 2u) {
+                if (tones >= g.pair_copies) {
                     const float2 v = Tab::one(theta, lb + (((cx + 1u) ^ k) & m));
                     v1x = v.x;
                     v1y = v.y;
@@ -511,12 +511,12 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
             float in16[16];
             float *g8 = in16, *t8 = in16 + 8;
             uint32_t bc = 0;
-            if (p.ablate & 1u) {
+            if (kTiming && (p.ablate & 1u)) {
 #pragma unroll
                 for (int q = 0; q < 8; ++q)
                     g8[q] = px * (float)(q + 1) + py;
             } else if (KIND == kKindAid) {
-                grid_encode4<HALF>(p.rrs_grid, p.grid, 4 * half, clamp01(px), clamp01(py), clamp01(pz), g8);
+                grid_encode4<HALF>(p.rrs_grid, p.grid_rrs, 4 * half, clamp01(px), clamp01(py), clamp01(pz), g8);
             } else {
                 grid_encode4<false>(p.stat_grid, p.grid, 4 * half, clamp01(px), clamp01(py), clamp01(pz), g8);
             }
@@ -724,7 +724,7 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
                             } else {
                                 qv = softplus_mod(y[0]);
                             }
-                            if (p.ablate & 2u)
+                            if (kTiming && (p.ablate & 2u))
                                 qv = sd.ex[0] + 1.0f;
                             if (KIND != kKindStats) {
                                 uint32_t decided = active ? 1u : 0u;
@@ -853,6 +853,13 @@ static cudaError_t launch_ws(const InferParams &p, int num_sms, cudaStream_t str
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
         return e;
+#ifdef NRRS_CARVEOUT
+    // smallest shared-memory carveout that fits: the rest of the 256 KB stays L1 for the grid levels
+    e = cudaFuncSetAttribute(infer_ws_kernel<KIND, GE, GM, P, TPR, HALF>,
+                             cudaFuncAttributePreferredSharedMemoryCarveout, NRRS_CARVEOUT);
+    if (e != cudaSuccess)
+        return e;
+#endif
     const uint64_t tiles = (p.n + kTileM - 1) / kTileM;
     uint64_t grid = (uint64_t)num_sms;
     if (grid > tiles)
