@@ -254,6 +254,9 @@ def main():
     local_total = torch.zeros(1, dtype=torch.int64, device=dev)
 
     def step(ev):
+        """One stage step.  ev = [start, end] (timed loop: nothing between the kernels, so K-B / K-C
+        launch early under programmatic dependent launch) or [start, after K-A, after K-B, end]
+        (breakdown loop)."""
         stream = torch.cuda.current_stream()
         ev[0].record(stream)
         gain = rc.gain()
@@ -263,7 +266,8 @@ def main():
         oc = out.c()
         _capi.check(stage.handle, lib.nrrs_gpu_stage_factors(stage.handle, C.byref(soa), n, C.byref(p),
                                                              C.byref(oc), local_sum.data_ptr()))
-        ev[1].record(stream)
+        if len(ev) == 4:
+            ev[1].record(stream)
         if sh is None:
             _capi.check(stage.handle, lib.nrrs_gpu_stage_decide(stage.handle, n, C.byref(p), local_sum.data_ptr(), 1,
                                                                 C.byref(oc), local_total.data_ptr()))
@@ -273,14 +277,15 @@ def main():
             from paper_2510_07868_b200.sharded import sharded_depth
             sharded_depth(local_sum, lambda rs: sh.decide(n, 2, strategy, out, rs, gain, 0.0), cap, npx, None, rc)
             count_src = sh._total
-        ev[2].record(stream)
+        if len(ev) == 4:
+            ev[2].record(stream)
         _capi.check(stage.handle, lib.nrrs_gpu_compact_dev(stage.handle, out.slots.data_ptr(), used.data_ptr(),
                                                            count_src.data_ptr(), slot_cap, 2, compacted.data_ptr(),
                                                            d_count.data_ptr()))
-        ev[3].record(stream)
+        ev[-1].record(stream)
 
-    def events():
-        return [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    def events(k=2):
+        return [torch.cuda.Event(enable_timing=True) for _ in range(k)]
 
     stage.ctx.bind_stream()
     for _ in range(max(args.warmup, 3)):
@@ -303,11 +308,19 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     launches = stage.ctx.launch_count() - launches0
-    step_ms = [e[0].elapsed_time(e[3]) for e in evs]
-    infer_ms = [e[0].elapsed_time(e[1]) for e in evs]
-    decide_ms = [e[1].elapsed_time(e[2]) for e in evs]
-    compact_ms = [e[2].elapsed_time(e[3]) for e in evs]
+    step_ms = [e[0].elapsed_time(e[1]) for e in evs]
     total_s = sum(step_ms) / 1e3
+    # per-kernel breakdown (separate loop: events between the kernels serialize their launches)
+    bevs = []
+    for _ in range(min(args.steps, 10)):
+        flush.zero_()
+        ev = events(4)
+        step(ev)
+        bevs.append(ev)
+    torch.cuda.synchronize()
+    infer_ms = [e[0].elapsed_time(e[1]) for e in bevs]
+    decide_ms = [e[1].elapsed_time(e[2]) for e in bevs]
+    compact_ms = [e[2].elapsed_time(e[3]) for e in bevs]
     t = torch.tensor([total_s], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)  # max over ranks
