@@ -403,3 +403,38 @@ def test_film_luminance_sum_and_eps_div():
     from paper_2510_07868_b200.rrs import eps_div_from_luminance_sum
     assert st.eps_div(torch.from_numpy(film).cuda()) == eps_div_from_luminance_sum(ref, npx)
     assert float(st.film_luminance_sum(torch.zeros((0, 3), device="cuda")).item()) == 0.0
+
+
+def test_stage_error_paths_and_recovery():
+    """The fused stage fails like the reference's fail() paths (wavefront.cpp:198-211, :70-78,
+    rrs.cpp) with the documented status codes, and the context stays usable afterwards."""
+    import ctypes as C
+    from paper_2510_07868_b200 import _capi
+    from paper_2510_07868_b200.stage import vertex_soa
+    n = 1000
+    v = orc.gen_vertices(n)
+    dv = to_dev(v)
+    st = RrsStage(n)  # no networks
+    for kind, code in ((StrategyKind.Nrrs, _capi.NRRS_ESTATE), (StrategyKind.AidNrrs, _capi.NRRS_ESTATE),
+                       (StrategyKind.AdrrsNn, _capi.NRRS_ESTATE), (StrategyKind.AdrrsTree, _capi.NRRS_EINVAL)):
+        with pytest.raises(_capi.NrrsError) as ei:
+            st.run(dv, 2, Strategy(kind))
+        assert ei.value.code == code, kind
+    # depth 1 pins q = 1 and needs no networks (wavefront.cpp:373-375)
+    out, res = st.run(dv, 1, Strategy(StrategyKind.Nrrs))
+    assert res.total == n and np.all(_np(out.q_norm) == 1.0)
+    lib = _capi.lib()
+    out = st.alloc_outputs(n)
+    oc = out.c()
+    soa = vertex_soa(dv)
+    r = _capi.StageResultC()
+    for depth, npx, cap, kind in ((0, n, 0, 1), (2, n, n - 1, 1), (2, 0, 0, 1), (2, n, 0, 99)):
+        p = _capi.StageParams(depth, npx, cap, _capi.StrategyC(kind, 1.0), 1.0, 0.0, 0)
+        rc = lib.nrrs_gpu_rrs_stage(st.handle, C.byref(soa), n, C.byref(p), C.byref(oc), C.byref(r))
+        assert rc == _capi.NRRS_EINVAL, (depth, npx, cap, kind)
+        assert lib.nrrs_gpu_last_error(st.handle)
+    # still usable: a valid call matches the oracle bit for bit
+    ref = orc.rrs_stage(v, 2, n, queue_capacity_for(n), orc.THROUGHPUT, None, gain=0.85, seed=0)
+    out, res = st.run(dv, 2, Strategy(StrategyKind.Throughput), rc=RateControl(), full=True)
+    np.testing.assert_array_equal(_np(out.k), ref["k"])
+    assert res.spawned == ref["spawned"]
