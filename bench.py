@@ -268,20 +268,22 @@ def main():
                                                              C.byref(oc), local_sum.data_ptr()))
         if len(ev) == 4:
             ev[1].record(stream)
+        def compact(count_src):
+            if len(ev) == 4:
+                ev[2].record(stream)
+            _capi.check(stage.handle, lib.nrrs_gpu_compact_dev(stage.handle, out.slots.data_ptr(), used.data_ptr(),
+                                                               count_src.data_ptr(), slot_cap, 2, compacted.data_ptr(),
+                                                               d_count.data_ptr()))
         if sh is None:
             _capi.check(stage.handle, lib.nrrs_gpu_stage_decide(stage.handle, n, C.byref(p), local_sum.data_ptr(), 1,
                                                                 C.byref(oc), local_total.data_ptr()))
-            count_src = local_total
+            compact(local_total)
         else:
             sh.stage.ctx.bind_stream()
             from paper_2510_07868_b200.sharded import sharded_depth
-            sharded_depth(local_sum, lambda rs: sh.decide(n, 2, strategy, out, rs, gain, 0.0), cap, npx, None, rc)
-            count_src = sh._total
-        if len(ev) == 4:
-            ev[2].record(stream)
-        _capi.check(stage.handle, lib.nrrs_gpu_compact_dev(stage.handle, out.slots.data_ptr(), used.data_ptr(),
-                                                           count_src.data_ptr(), slot_cap, 2, compacted.data_ptr(),
-                                                           d_count.data_ptr()))
+            # this rank's compaction needs only its own queue: queued before the host waits for the totals
+            sharded_depth(local_sum, lambda rs: sh.decide(n, 2, strategy, out, rs, gain, 0.0), cap, npx, None, rc,
+                          after_exchange=lambda: compact(sh._total))
         ev[-1].record(stream)
 
     def events(k=2):

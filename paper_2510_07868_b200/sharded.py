@@ -62,10 +62,14 @@ def f_norm_from_sums(rank_sums: List[float], n_pixels_total: int) -> float:
 
 
 def sharded_depth(local_sum: torch.Tensor, decide: Callable[[torch.Tensor], torch.Tensor], capacity: int,
-                  n_pixels_total: int, group=None, rc: Optional[RateControl] = None) -> ShardOutcome:
+                  n_pixels_total: int, group=None, rc: Optional[RateControl] = None,
+                  after_exchange: Optional[Callable[[], None]] = None) -> ShardOutcome:
     """Runs the two exchanges of one depth.  local_sum: [1] float64 on the
     collective's device; decide(rank_sums) launches phase 2 and returns the
-    rank's [1] int64 realized total."""
+    rank's [1] int64 realized total.  after_exchange() (optional) is called once
+    the second exchange is issued and before the host reads its result: device
+    work that needs only this rank's queue (e.g. its compaction) is queued
+    there, so the GPU does not idle through the host round trip."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     host = dist.get_backend(group) == "gloo" and local_sum.is_cuda  # gloo exchanges host copies
@@ -77,12 +81,14 @@ def sharded_depth(local_sum: torch.Tensor, decide: Callable[[torch.Tensor], torc
     src = local_total.cpu() if host else local_total
     totals = [torch.zeros_like(src) for _ in range(world)]
     dist.all_gather(totals, src, group=group)
-    tot = [int(t.item()) for t in totals]
+    if after_exchange is not None:
+        after_exchange()
+    tot = [int(x) for x in torch.cat(totals).tolist()]  # the one host wait of the depth
+    sums_h = [float(x) for x in rank_sums_t.tolist()]
     base, kept, spawned, dropped = global_clip(tot, rank, capacity)
     if rc is not None and dropped > 0:
         rc.note_overflow()
-    return ShardOutcome([float(x) for x in rank_sums_t.tolist()], tot, base, kept, spawned, dropped,
-                        f_norm_from_sums([float(x) for x in rank_sums_t.tolist()], n_pixels_total))
+    return ShardOutcome(sums_h, tot, base, kept, spawned, dropped, f_norm_from_sums(sums_h, n_pixels_total))
 
 
 def _gather_in_rank_order(local: torch.Tensor, group=None) -> torch.Tensor:
