@@ -141,13 +141,25 @@ def cpu_baseline(variant: str, n_sample: int = N_LOCAL):
     nets = orc.OracleNets(var, seed=1, randomize=True)
     cap = orc.lib().orc_queue_capacity_for(n_sample)
     best = float("inf")
-    for _ in range(2):
+    for _ in range(5):
         t0 = time.perf_counter()
         orc.rrs_stage(v, 2, n_sample, cap, kind, nets, gain=0.85, seed=0, threads=threads)
         best = min(best, time.perf_counter() - t0)
     return {"value": n_sample / best, "unit": "vertices/s", "cores": threads, "kind": "port",
-            "sample": f"{n_sample} synthetic vertices, {variant}-nrrs, depth 2, best of 2 "
+            "host": host_cpu(),
+            "sample": f"{n_sample} synthetic vertices (the full workload), {variant}-nrrs, depth 2, best of 5 "
                       f"(factor pass over {threads} threads + serial normalize/realize/plan/slots)"}
+
+
+def host_cpu() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def run_reference(args):
@@ -182,7 +194,7 @@ def run_reference(args):
             "config": {"workload": f"{args.variant}-nrrs stage, 1920x1080 synthetic vertices at depth 2 "
                                    f"(full batch each step)",
                        "n_pixels": args.vertices, "strategy": f"{args.variant}-nrrs", "depth": 2},
-            "cpu_baseline": {"value": value, "unit": "vertices/s", "cores": threads, "kind": "port",
+            "cpu_baseline": {"value": value, "unit": "vertices/s", "cores": threads, "kind": "port", "host": host_cpu(),
                              "sample": f"the full {sample}-vertex batch per step; the reference does not build here "
                                        "(Eigen absent): C restatement of the reference path"},
             "e2e": {"value": value, "unit": "vertices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
