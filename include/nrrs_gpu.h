@@ -133,6 +133,35 @@ typedef struct {
     uint32_t overflow;       /* 1 iff dropped > 0: caller does rc.note_overflow() (wavefront.cpp:407-411) */
 } nrrs_stage_result;
 
+/* TrainSample (networks.hpp:20-32): 80 bytes, the reference's field order and layout. */
+typedef struct {
+    float position[3];  /* scene-normalized p01 */
+    float omega_o[2];   /* wo01 */
+    float roughness;
+    float t_x[3];       /* path weight into the vertex */
+    float i_pixel[3];   /* film.i_acc[pixel] */
+    float lo_sample[3]; /* s / weight per channel (0 where weight <= 0) */
+    float q_norm;
+    float q_real;
+    uint32_t pixel;
+    float k_i;          /* this frame's samples in the pixel */
+    uint16_t depth;
+    uint16_t pad;
+} nrrs_train_sample;
+
+/* The VertexRec fields the suffix side reads, SoA for one depth (wavefront.cpp:46-65). */
+typedef struct {
+    const float *p01;       /* [3n] */
+    const float *wo01;      /* [2n] */
+    const float *roughness; /* [n] */
+    const float *weight;    /* [3n] */
+    const uint32_t *pixel;  /* [n] */
+    const float *q_norm;    /* [n] */
+    const float *q_real;    /* [n] */
+    const uint8_t *decided; /* [n] */
+    const double *s;        /* [3n] suffix contribution after the reverse pass */
+} nrrs_vertex_rec_soa;
+
 typedef struct nrrs_gpu_ctx nrrs_gpu_ctx;
 
 /* ---- context ------------------------------------------------------------ */
@@ -177,6 +206,39 @@ NRRS_API int nrrs_gpu_film_luminance_sum(nrrs_gpu_ctx *ctx, const float *d_i_acc
 NRRS_API int nrrs_gpu_rrs_stage_host(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *h_v, uint64_t n,
                             const nrrs_stage_params *p, const nrrs_stage_out *h_out,
                             nrrs_stage_result *h_result);
+
+/* ---- suffix side of trace_frame: film folds, reverse pass,
+ * TrainSample emission, Film updates.  Bit-identical to the reference's sequential
+ * f64 folds.  Device buffers; stream-ordered. */
+
+/* d_dst[key[i]] += d_terms[i] (f64 x3) for i = 0..n-1 in item order.  Keys must be
+ * non-decreasing (queue order is pixel and parent order); negative keys (no parent)
+ * are skipped.  Replaces frame[pixel] += term (wavefront.cpp:299, :317, :355, :485),
+ * parent.s += term (:301, :319) and, one call per depth d = B..2 with the depth-d
+ * parent indices and s, the reverse pass (:505-507).  Syncs; EINVAL if the keys are
+ * out of order or out of range. */
+NRRS_API int nrrs_gpu_fold_ordered(nrrs_gpu_ctx *ctx, double *d_dst, uint64_t n_dst, const int32_t *d_keys,
+                                   const double *d_terms, uint64_t n);
+
+/* TrainSample emission for one depth (wavefront.cpp:510-537): one record per decided
+ * vertex whose lo = s / weight is finite, in vertex order, written at
+ * d_out[*d_count_in ...]; *d_count_out = *d_count_in + records (pass distinct counters;
+ * call for depths 1..B-1 in order).  Non-finite lo adds to *d_nonfinite.  k_i is set by
+ * nrrs_gpu_train_k_i.  Asynchronous. */
+NRRS_API int nrrs_gpu_emit_train(nrrs_gpu_ctx *ctx, uint32_t depth, const nrrs_vertex_rec_soa *d_v, uint64_t n,
+                                 const float *d_i_acc, nrrs_train_sample *d_out, uint64_t capacity,
+                                 const uint64_t *d_count_in, uint64_t *d_count_out, uint64_t *d_nonfinite);
+
+/* k_i of the frame's samples [start, *d_end) = number of those samples with the same
+ * pixel (wavefront.cpp:539-543).  Syncs; ESIZE if an emission ran past capacity. */
+NRRS_API int nrrs_gpu_train_k_i(nrrs_gpu_ctx *ctx, nrrs_train_sample *d_samples, uint64_t start,
+                                const uint64_t *d_end, uint64_t capacity, uint32_t n_pixels);
+
+/* Film::add_frame (wavefront.cpp:104-111): sum += frame, samples += 1, i_cur = float(frame). */
+NRRS_API int nrrs_gpu_film_add_frame(nrrs_gpu_ctx *ctx, double *d_sum, uint32_t *d_samples, float *d_i_cur,
+                                     const double *d_frame, uint32_t n_pixels);
+/* Film::roll_acc (wavefront.cpp:113-116): i_acc = 0.5f * i_acc + 0.5f * i_cur. */
+NRRS_API int nrrs_gpu_film_roll_acc(nrrs_gpu_ctx *ctx, float *d_i_acc, const float *d_i_cur, uint32_t n_pixels);
 
 /* ---- tile-sharded stage (multi-rank), two phases per depth:
  * phase 1: factors + RrsRound uniforms; writes this rank's sum of sanitized

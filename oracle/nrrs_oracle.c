@@ -554,6 +554,86 @@ uint32_t orc_compact_slots(const uint32_t *slots, const uint8_t *used, uint32_t 
 /* vertex i draws from RngStream(0xC0FFEE, i) in the order of
  * test_networks.cpp:37-51 (position, omega_o, roughness, t_x, i_pixel),
  * each vector component drawn left to right. */
+/* ---- suffix side of trace_frame ---- */
+
+/* wavefront.cpp:299 / :317 / :355 / :485 (frame[pixel] += term), :301 / :319
+ * (parent.s += term), :505-507 (verts[d-1][v.parent].s += v.s): sequential f64. */
+void orc_fold_ordered(double *dst, const int32_t *keys, const double *terms, size_t n) {
+    for (size_t i = 0; i < n; ++i) {
+        if (keys[i] < 0)
+            continue;
+        for (int c = 0; c < 3; ++c)
+            dst[3 * (size_t)keys[i] + c] += terms[3 * i + c];
+    }
+}
+
+/* wavefront.cpp:512-537: decided vertices with finite lo = float(s / weight) */
+size_t orc_emit_train(uint32_t depth, size_t n, const float *p01, const float *wo01, const float *rough,
+                      const float *weight, const uint32_t *pixel, const float *q_norm, const float *q_real,
+                      const uint8_t *decided, const double *s, const float *i_acc, orc_train_sample *out,
+                      uint64_t *nonfinite) {
+    size_t w = 0;
+    for (size_t j = 0; j < n; ++j) {
+        if (!decided[j])
+            continue;
+        float lo[3];
+        for (int c = 0; c < 3; ++c)
+            lo[c] = weight[3 * j + c] > 0.0f ? (float)(s[3 * j + c] / (double)weight[3 * j + c]) : 0.0f;
+        if (!(isfinite(lo[0]) && isfinite(lo[1]) && isfinite(lo[2]))) {
+            ++*nonfinite;
+            continue;
+        }
+        orc_train_sample t;
+        memset(&t, 0, sizeof t);
+        for (int c = 0; c < 3; ++c) {
+            t.position[c] = p01[3 * j + c];
+            t.t_x[c] = weight[3 * j + c];
+            t.i_pixel[c] = i_acc[3 * (size_t)pixel[j] + c];
+            t.lo_sample[c] = lo[c];
+        }
+        t.omega_o[0] = wo01[2 * j];
+        t.omega_o[1] = wo01[2 * j + 1];
+        t.roughness = rough[j];
+        t.q_norm = q_norm[j];
+        t.q_real = q_real[j];
+        t.pixel = pixel[j];
+        t.k_i = 1.0f;
+        t.depth = (uint16_t)depth;
+        out[w++] = t;
+    }
+    return w;
+}
+
+/* wavefront.cpp:539-543 */
+void orc_train_k_i(orc_train_sample *s, size_t start, size_t end, uint32_t n_pixels) {
+    uint32_t *per_pixel = (uint32_t *)calloc(n_pixels ? n_pixels : 1, sizeof(uint32_t));
+    for (size_t i = start; i < end; ++i)
+        per_pixel[s[i].pixel] += 1u;
+    for (size_t i = start; i < end; ++i)
+        s[i].k_i = (float)per_pixel[s[i].pixel];
+    free(per_pixel);
+}
+
+/* Film::add_frame (wavefront.cpp:104-111) */
+void orc_film_add_frame(double *sum, uint32_t *samples, float *i_cur, const double *frame, size_t n_pixels) {
+    for (size_t i = 0; i < n_pixels; ++i) {
+        for (int c = 0; c < 3; ++c) {
+            sum[3 * i + c] += frame[3 * i + c];
+            i_cur[3 * i + c] = (float)frame[3 * i + c];
+        }
+        samples[i] += 1u;
+    }
+}
+
+/* Film::roll_acc (wavefront.cpp:113-116) */
+void orc_film_roll_acc(float *i_acc, const float *i_cur, size_t n_pixels) {
+    for (size_t i = 0; i < 3 * n_pixels; ++i) {
+        const float a = 0.5f * i_acc[i];
+        const float b = 0.5f * i_cur[i];
+        i_acc[i] = a + b;
+    }
+}
+
 void orc_gen_vertices(size_t n, uint32_t n_pixels, uint32_t frame, float *p01, float *wo01,
                       float *rough, float *t_x, float *i_pixel, uint64_t *path_key,
                       uint32_t *pixel) {

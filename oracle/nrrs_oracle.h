@@ -144,6 +144,28 @@ void orc_rrs_stage(const orc_vertices *v, size_t n, const orc_stage_params *p, c
 /* order-preserving compaction (wavefront.cpp:488-497) of 2-word slot records */
 uint32_t orc_compact_slots(const uint32_t *slots, const uint8_t *used, uint32_t count, uint32_t *out);
 
+/* ---- suffix side of trace_frame ---- */
+/* dst[key[i]] += term[i] (f64 x3) in item order, negative keys skipped: the frame / parent
+ * folds (wavefront.cpp:299-319, :355, :485) and one depth of the reverse pass (:505-507). */
+void orc_fold_ordered(double *dst, const int32_t *keys, const double *terms, size_t n);
+/* TrainSample (networks.hpp:20-32), 80 bytes */
+typedef struct {
+    float position[3], omega_o[2], roughness, t_x[3], i_pixel[3], lo_sample[3], q_norm, q_real;
+    uint32_t pixel;
+    float k_i;
+    uint16_t depth, pad;
+} orc_train_sample;
+/* one depth of the emission loop (wavefront.cpp:512-537); returns the records written */
+size_t orc_emit_train(uint32_t depth, size_t n, const float *p01, const float *wo01, const float *rough,
+                      const float *weight, const uint32_t *pixel, const float *q_norm, const float *q_real,
+                      const uint8_t *decided, const double *s, const float *i_acc, orc_train_sample *out,
+                      uint64_t *nonfinite);
+/* k_i = per-pixel count over out[start, end) (wavefront.cpp:539-543) */
+void orc_train_k_i(orc_train_sample *s, size_t start, size_t end, uint32_t n_pixels);
+/* Film::add_frame / roll_acc (wavefront.cpp:104-116) */
+void orc_film_add_frame(double *sum, uint32_t *samples, float *i_cur, const double *frame, size_t n_pixels);
+void orc_film_roll_acc(float *i_acc, const float *i_cur, size_t n_pixels);
+
 /* ---- synthetic inputs (generator follows test_networks.cpp:37-51) ---- */
 void orc_gen_vertices(size_t n, uint32_t n_pixels, uint32_t frame, float *p01, float *wo01,
                       float *rough, float *t_x, float *i_pixel, uint64_t *path_key,

@@ -54,6 +54,12 @@ class StageResultC(C.Structure):
                 ("overflow", C.c_uint32)]
 
 
+class VertexRecSoA(C.Structure):
+    _fields_ = [("p01", C.c_void_p), ("wo01", C.c_void_p), ("roughness", C.c_void_p), ("weight", C.c_void_p),
+                ("pixel", C.c_void_p), ("q_norm", C.c_void_p), ("q_real", C.c_void_p), ("decided", C.c_void_p),
+                ("s", C.c_void_p)]
+
+
 # (name, restype, argtypes) for every entry point declared in include/nrrs_gpu.h
 _P = C.c_void_p
 SIGNATURES = [
@@ -66,6 +72,12 @@ SIGNATURES = [
     ("nrrs_gpu_launch_count", C.c_uint64, [_P]),
     ("nrrs_gpu_fetch_result", C.c_int, [_P, C.POINTER(StageResultC)]),
     ("nrrs_gpu_film_luminance_sum", C.c_int, [_P, _P, C.c_uint64, _P]),
+    ("nrrs_gpu_fold_ordered", C.c_int, [_P, _P, C.c_uint64, _P, _P, C.c_uint64]),
+    ("nrrs_gpu_emit_train", C.c_int, [_P, C.c_uint32, C.POINTER(VertexRecSoA), C.c_uint64, _P, _P, C.c_uint64,
+                                      _P, _P, _P]),
+    ("nrrs_gpu_train_k_i", C.c_int, [_P, _P, C.c_uint64, _P, C.c_uint64, C.c_uint32]),
+    ("nrrs_gpu_film_add_frame", C.c_int, [_P, _P, _P, _P, _P, C.c_uint32]),
+    ("nrrs_gpu_film_roll_acc", C.c_int, [_P, _P, _P, C.c_uint32]),
     ("nrrs_gpu_set_weights", C.c_int, [_P, C.POINTER(NetWeights)]),
     ("nrrs_gpu_rrs_stage", C.c_int, [_P, C.POINTER(VertexSoA), C.c_uint64, C.POINTER(StageParams),
                                      C.POINTER(StageOut), C.POINTER(StageResultC)]),

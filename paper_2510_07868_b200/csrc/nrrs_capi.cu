@@ -183,7 +183,11 @@ struct nrrs_gpu_ctx {
     DevResult *d_res = nullptr;
     double *d_sum = nullptr;            // [0] local sum  [1] scratch sum
     unsigned long long *d_total = nullptr;
-    LaunchSync *d_sync = nullptr;  // [0] decide, [1] compact: device-side claim counter + look-back epoch
+    LaunchSync *d_sync = nullptr;  // [0] decide, [1] compact, [2] train emission: claim counter + look-back epoch
+    uint64_t *d_etile_state = nullptr;
+    uint64_t cap_etiles = 0;
+    uint32_t *d_hist = nullptr;
+    uint64_t cap_hist = 0;
 
     // host-path pipeline: chunked H2D on copy_stream overlapped with K-A on `stream`
     cudaStream_t copy_stream = nullptr;
@@ -286,11 +290,11 @@ int nrrs_gpu_create(int device, nrrs_gpu_ctx **out) {
         cudaMalloc(&ctx->d_res, sizeof(DevResult)) != cudaSuccess ||
         cudaMalloc(&ctx->d_sum, (kChunkSums + kMaxHostChunks) * sizeof(double)) != cudaSuccess ||
         cudaMalloc(&ctx->d_total, 4 * sizeof(unsigned long long)) != cudaSuccess ||
-        cudaMalloc(&ctx->d_sync, 2 * sizeof(LaunchSync)) != cudaSuccess) {
+        cudaMalloc(&ctx->d_sync, 3 * sizeof(LaunchSync)) != cudaSuccess) {
         delete ctx;
         return NRRS_ECUDA;
     }
-    cudaMemset(ctx->d_sync, 0, 2 * sizeof(LaunchSync));
+    cudaMemset(ctx->d_sync, 0, 3 * sizeof(LaunchSync));
     cudaMemset(ctx->d_misc, 0, 16 * sizeof(uint32_t));
     cudaMemset(ctx->d_res, 0, sizeof(DevResult));
     cudaMemset(ctx->d_sum, 0, (kChunkSums + kMaxHostChunks) * sizeof(double));
@@ -305,7 +309,7 @@ int nrrs_gpu_destroy(nrrs_gpu_ctx *ctx) {
     cudaStreamSynchronize(ctx->stream);
     void *ptrs[] = {ctx->d_stat_grid, ctx->d_rrs_grid, ctx->blob_stat.ptr, ctx->blob_rrs.ptr, ctx->blob_both.ptr,
                     ctx->d_q, ctx->d_u, ctx->d_parts, ctx->d_part_counts, ctx->d_tile_state, ctx->d_ctile_state,
-                    ctx->d_misc, ctx->d_res, ctx->d_sum, ctx->d_total, ctx->d_sync, ctx->st.p01, ctx->st.wo01, ctx->st.rough,
+                    ctx->d_misc, ctx->d_res, ctx->d_sum, ctx->d_total, ctx->d_sync, ctx->d_etile_state, ctx->d_hist, ctx->st.p01, ctx->st.wo01, ctx->st.rough,
                     ctx->st.weight, ctx->st.ipix, ctx->st.key, ctx->st.q_norm, ctx->st.q_real, ctx->st.q_orig,
                     ctx->st.u, ctx->st.k, ctx->st.offset, ctx->st.slots, ctx->st.decided};
     for (void *p : ptrs)
@@ -789,6 +793,113 @@ int nrrs_gpu_film_luminance_sum(nrrs_gpu_ctx *ctx, const float *d_i_acc, uint64_
     const uint64_t max_grid = ctx->cap_parts < (uint64_t)ctx->num_sms * 4 ? ctx->cap_parts : (uint64_t)ctx->num_sms * 4;
     grid = grid < 1 ? 1 : (grid > max_grid ? max_grid : grid);
     CK(ctx, launch_lum_sum(d_i_acc, n_pixels, ctx->d_parts, ctx->d_misc + 6, d_sum_out, (uint32_t)grid, ctx->stream));
+    ctx->launches += 1;
+    return NRRS_OK;
+}
+
+// ---- suffix side: folds, reverse pass, TrainSample emission, Film ----
+static_assert(sizeof(nrrs_train_sample) == 80, "TrainSample is 80 bytes (networks.hpp:20-32)");
+int nrrs_gpu_fold_ordered(nrrs_gpu_ctx *ctx, double *d_dst, uint64_t n_dst, const int32_t *d_keys,
+                          const double *d_terms, uint64_t n) {
+    if (!ctx || (n && (!d_dst || !d_keys || !d_terms)))
+        return NRRS_EINVAL;
+    if (n == 0)
+        return NRRS_OK;
+    CK(ctx, cudaSetDevice(ctx->device));
+    uint32_t *err = ctx->d_misc + 9;
+    CK(ctx, cudaMemsetAsync(err, 0, sizeof(uint32_t), ctx->stream));
+    CK(ctx, launch_fold_ordered(d_dst, n_dst, d_keys, d_terms, n, err, ctx->stream));
+    ctx->launches += 1;
+    uint32_t h = 0;
+    CK(ctx, cudaMemcpyAsync(&h, err, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(ctx, cudaStreamSynchronize(ctx->stream));
+    if (h & 1u)
+        return fail(ctx, NRRS_EINVAL, "fold_ordered: keys are not in queue order (non-decreasing)");
+    if (h & 2u)
+        return fail(ctx, NRRS_EINVAL, "fold_ordered: key out of range (n_dst = %llu)", (unsigned long long)n_dst);
+    return NRRS_OK;
+}
+
+int nrrs_gpu_emit_train(nrrs_gpu_ctx *ctx, uint32_t depth, const nrrs_vertex_rec_soa *v, uint64_t n,
+                        const float *d_i_acc, nrrs_train_sample *d_out, uint64_t capacity, const uint64_t *d_count_in,
+                        uint64_t *d_count_out, uint64_t *d_nonfinite) {
+    if (!ctx || !v || !d_count_in || !d_count_out || !d_nonfinite || d_count_in == d_count_out)
+        return NRRS_EINVAL;
+    CK(ctx, cudaSetDevice(ctx->device));
+    if (n == 0) {
+        CK(ctx, cudaMemcpyAsync(d_count_out, d_count_in, sizeof(uint64_t), cudaMemcpyDeviceToDevice, ctx->stream));
+        return NRRS_OK;
+    }
+    if (!v->p01 || !v->wo01 || !v->roughness || !v->weight || !v->pixel || !v->q_norm || !v->q_real ||
+        !v->decided || !v->s || !d_i_acc || !d_out)
+        return fail(ctx, NRRS_EINVAL, "emit_train: every vertex field, i_acc and out are required");
+    const uint64_t tiles = emit_tiles(n) + 1;
+    if (tiles > ctx->cap_etiles) {
+        CK(ctx, grow(ctx->d_etile_state, ctx->cap_etiles, tiles));
+        CK(ctx, cudaMemsetAsync(ctx->d_etile_state, 0, tiles * sizeof(uint64_t), ctx->stream));
+    }
+    TrainParams p{};
+    p.p01 = v->p01;
+    p.wo01 = v->wo01;
+    p.roughness = v->roughness;
+    p.weight = v->weight;
+    p.pixel = v->pixel;
+    p.q_norm = v->q_norm;
+    p.q_real = v->q_real;
+    p.decided = v->decided;
+    p.s = v->s;
+    p.i_acc = d_i_acc;
+    p.n = n;
+    p.depth = depth;
+    p.out = d_out;
+    p.capacity = capacity;
+    p.base_in = reinterpret_cast<const unsigned long long *>(d_count_in);
+    p.base_out = reinterpret_cast<unsigned long long *>(d_count_out);
+    p.nonfinite = reinterpret_cast<unsigned long long *>(d_nonfinite);
+    p.err = ctx->d_misc + 10;
+    p.tile_state = ctx->d_etile_state;
+    p.state_cap = (uint32_t)ctx->cap_etiles;
+    p.sync = ctx->d_sync + 2;
+    p.num_tiles = emit_tiles(n);
+    CK(ctx, launch_emit_train(p, ctx->stream));
+    ctx->launches += 1;
+    return NRRS_OK;
+}
+
+int nrrs_gpu_train_k_i(nrrs_gpu_ctx *ctx, nrrs_train_sample *d_samples, uint64_t start, const uint64_t *d_end,
+                       uint64_t capacity, uint32_t n_pixels) {
+    if (!ctx || !d_samples || !d_end || n_pixels == 0)
+        return NRRS_EINVAL;
+    CK(ctx, cudaSetDevice(ctx->device));
+    CK(ctx, grow(ctx->d_hist, ctx->cap_hist, n_pixels));
+    CK(ctx, launch_k_i(d_samples, start, reinterpret_cast<const unsigned long long *>(d_end), capacity, ctx->d_hist,
+                       n_pixels, ctx->num_sms, ctx->stream));
+    ctx->launches += 2;
+    uint32_t h = 0;
+    CK(ctx, cudaMemcpyAsync(&h, ctx->d_misc + 10, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(ctx, cudaMemsetAsync(ctx->d_misc + 10, 0, sizeof(uint32_t), ctx->stream));
+    CK(ctx, cudaStreamSynchronize(ctx->stream));
+    if (h)
+        return fail(ctx, NRRS_ESIZE, "emit_train: more training samples than capacity %llu",
+                    (unsigned long long)capacity);
+    return NRRS_OK;
+}
+
+int nrrs_gpu_film_add_frame(nrrs_gpu_ctx *ctx, double *d_sum, uint32_t *d_samples, float *d_i_cur,
+                            const double *d_frame, uint32_t n_pixels) {
+    if (!ctx || (n_pixels && (!d_sum || !d_samples || !d_i_cur || !d_frame)))
+        return NRRS_EINVAL;
+    CK(ctx, cudaSetDevice(ctx->device));
+    CK(ctx, launch_film_add_frame(d_sum, d_samples, d_i_cur, d_frame, n_pixels, ctx->num_sms, ctx->stream));
+    ctx->launches += 1;
+    return NRRS_OK;
+}
+
+int nrrs_gpu_film_roll_acc(nrrs_gpu_ctx *ctx, float *d_i_acc, const float *d_i_cur, uint32_t n_pixels) {
+    if (!ctx || (n_pixels && (!d_i_acc || !d_i_cur)))
+        return NRRS_EINVAL;
+    CK(ctx, cudaSetDevice(ctx->device));
+    CK(ctx, launch_film_roll_acc(d_i_acc, d_i_cur, n_pixels, ctx->num_sms, ctx->stream));
     ctx->launches += 1;
     return NRRS_OK;
 }

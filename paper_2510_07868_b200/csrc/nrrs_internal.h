@@ -5,6 +5,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "../../include/nrrs_gpu.h"
+
 namespace nrrs {
 
 // Device-side launch bookkeeping of the look-back kernels (nrrs_device.cuh):
@@ -155,6 +157,38 @@ struct CompactParams {
     LaunchSync *sync;
     uint32_t num_tiles;
 };
+
+// TrainSample emission for one depth (nrrs_film.cu).
+struct TrainParams {
+    const float *p01, *wo01, *roughness, *weight;
+    const uint32_t *pixel;
+    const float *q_norm, *q_real;
+    const uint8_t *decided;
+    const double *s;
+    const float *i_acc;
+    uint64_t n;
+    uint32_t depth;
+    nrrs_train_sample *out;
+    uint64_t capacity;
+    const unsigned long long *base_in;  // samples already in `out` (device)
+    unsigned long long *base_out;       // base_in + this depth's samples (device)
+    unsigned long long *nonfinite;
+    uint32_t *err;
+    uint64_t *tile_state;
+    uint32_t state_cap;
+    LaunchSync *sync;
+    uint32_t num_tiles;
+};
+
+uint32_t emit_tiles(uint64_t n);
+cudaError_t launch_fold_ordered(double *dst, uint64_t n_dst, const int32_t *keys, const double *terms, uint64_t n,
+                                uint32_t *err, cudaStream_t stream);
+cudaError_t launch_film_add_frame(double *sum, uint32_t *samples, float *i_cur, const double *frame, uint64_t n,
+                                  int num_sms, cudaStream_t stream);
+cudaError_t launch_film_roll_acc(float *i_acc, const float *i_cur, uint64_t n, int num_sms, cudaStream_t stream);
+cudaError_t launch_emit_train(const TrainParams &p, cudaStream_t stream);
+cudaError_t launch_k_i(nrrs_train_sample *s, uint64_t start, const unsigned long long *end, uint64_t capacity,
+                       uint32_t *hist, uint32_t n_pixels, int num_sms, cudaStream_t stream);
 
 size_t infer_smem_bytes(int kind, const InferParams &p);
 cudaError_t launch_infer(int kind, const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out);

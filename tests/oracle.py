@@ -90,6 +90,11 @@ def lib() -> C.CDLL:
             "orc_gen_vertices": (None, [C.c_size_t, u32, u32, p, p, p, p, p, p, p]),
             "orc_gen_split_bound_factors": (None, [C.c_size_t, p]),
             "orc_init_nets": (None, [i, p, u64, i, p, p, p, p]),
+            "orc_fold_ordered": (None, [p, p, p, C.c_size_t]),
+            "orc_emit_train": (C.c_size_t, [u32, C.c_size_t, p, p, p, p, p, p, p, p, p, p, p, p]),
+            "orc_train_k_i": (None, [p, C.c_size_t, C.c_size_t, u32]),
+            "orc_film_add_frame": (None, [p, p, p, p, C.c_size_t]),
+            "orc_film_roll_acc": (None, [p, p, C.c_size_t]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -229,3 +234,75 @@ def threads_available() -> int:
         return len(os.sched_getaffinity(0))
     except AttributeError:
         return os.cpu_count() or 1
+
+
+# ---- suffix side of trace_frame ----
+TRAIN_SAMPLE_DTYPE = np.dtype([("position", "<f4", 3), ("omega_o", "<f4", 2), ("roughness", "<f4"),
+                               ("t_x", "<f4", 3), ("i_pixel", "<f4", 3), ("lo_sample", "<f4", 3),
+                               ("q_norm", "<f4"), ("q_real", "<f4"), ("pixel", "<u4"), ("k_i", "<f4"),
+                               ("depth", "<u2"), ("pad", "<u2")])
+
+
+def fold_ordered(dst: np.ndarray, keys: np.ndarray, terms: np.ndarray) -> None:
+    """In place: dst[keys[i]] += terms[i] (f64 x3), item order, negative keys skipped."""
+    keys = np.ascontiguousarray(keys, dtype=np.int32)
+    terms = np.ascontiguousarray(terms, dtype=np.float64)
+    assert dst.dtype == np.float64 and dst.flags.c_contiguous
+    lib().orc_fold_ordered(ptr(dst), ptr(keys), ptr(terms), keys.size)
+
+
+def reverse_pass(verts: list) -> None:
+    for d in range(len(verts) - 1, 1, -1):
+        fold_ordered(verts[d - 1]["s"], verts[d]["parent"], verts[d]["s"])
+
+
+def emit_train(verts: list, i_acc: np.ndarray, n_pixels: int):
+    """TrainSamples for depths 1..B-1 then k_i (wavefront.cpp:510-543) -> (records, nonfinite)."""
+    total = sum(int(verts[d]["pixel"].size) for d in range(1, len(verts)))
+    out = np.zeros(max(total, 1), TRAIN_SAMPLE_DTYPE)
+    nf = C.c_uint64(0)
+    w = 0
+    for d in range(1, len(verts)):
+        v = {k: np.ascontiguousarray(a) for k, a in verts[d].items()}
+        n = int(v["pixel"].size)
+        sub = out[w:]
+        w += lib().orc_emit_train(d, n, ptr(v["p01"]), ptr(v["wo01"]), ptr(v["roughness"]), ptr(v["weight"]),
+                                  ptr(v["pixel"]), ptr(v["q_norm"]), ptr(v["q_real"]), ptr(v["decided"]),
+                                  ptr(v["s"]), ptr(np.ascontiguousarray(i_acc)), sub.ctypes.data, C.byref(nf))
+    lib().orc_train_k_i(out.ctypes.data, 0, w, n_pixels)
+    return out[:w], nf.value
+
+
+def film_add_frame(sum_: np.ndarray, samples: np.ndarray, i_cur: np.ndarray, frame: np.ndarray) -> None:
+    lib().orc_film_add_frame(ptr(sum_), ptr(samples), ptr(i_cur), ptr(np.ascontiguousarray(frame)), samples.size)
+
+
+def film_roll_acc(i_acc: np.ndarray, i_cur: np.ndarray) -> None:
+    lib().orc_film_roll_acc(ptr(i_acc), ptr(i_cur), i_acc.size // 3)
+
+
+def gen_vertex_tree(depth_sizes: list, n_pixels: int, seed: int = 7) -> list:
+    """Synthetic per-depth VertexRec SoA in queue order (pixel and parent non-decreasing):
+    index 0 unused, depth 1 has one vertex per pixel prefix, deeper vertices pick sorted parents.
+    s (f64) holds the vertices' own film terms before the reverse pass."""
+    g = np.random.default_rng(seed)
+    verts = [None]
+    prev_pixel = None
+    for d, n in enumerate(depth_sizes, start=1):
+        if d == 1:
+            pixel = np.sort(g.integers(0, n_pixels, n)).astype(np.uint32)
+            parent = np.full(n, -1, np.int32)
+        else:
+            parent = np.sort(g.integers(0, depth_sizes[d - 2], n)).astype(np.int32)
+            pixel = prev_pixel[parent]
+        w = (g.random((n, 3), dtype=np.float32) * np.float32(2.0) - np.float32(0.25)).astype(np.float32)
+        s = g.standard_normal((n, 3)) * 3.0
+        s[g.random(n) < 0.002, 1] = np.inf  # non-finite suffix -> counted, no sample
+        verts.append({"parent": parent, "pixel": pixel, "weight": w, "s": s,
+                      "p01": g.random((n, 3), dtype=np.float32), "wo01": g.random((n, 2), dtype=np.float32),
+                      "roughness": g.random(n, dtype=np.float32),
+                      "q_norm": g.random(n, dtype=np.float32) * np.float32(3),
+                      "q_real": g.random(n, dtype=np.float32) * np.float32(3),
+                      "decided": (g.random(n) < 0.8).astype(np.uint8)})
+        prev_pixel = pixel
+    return verts

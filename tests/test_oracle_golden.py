@@ -276,3 +276,45 @@ def test_oracle_stage_threads_invariant():
     b = orc.rrs_stage(v, 2, 3000, 3375, orc.AID_NRRS, nets, threads=4)
     for key in ("q_orig", "q_norm", "q_real", "u", "k", "offset", "slots"):
         np.testing.assert_array_equal(a[key], b[key])
+
+
+def test_oracle_film_kat():
+    """Film add_frame / mean / roll_acc / reset (test_engine.cpp:619-642) on the oracle."""
+    k = json.loads((GOLDEN / "reference_kats.json").read_text())["film"]
+    n = k["width"] * k["height"]
+    s = np.zeros((n, 3)); samples = np.zeros(n, np.uint32)
+    i_cur = np.zeros((n, 3), np.float32); i_acc = np.zeros((n, 3), np.float32)
+    orc.film_add_frame(s, samples, i_cur, np.array(k["frame1"], np.float64))
+    assert samples.tolist() == k["samples_after1"]
+    assert (s[0] / samples[0]).astype(np.float32).tolist() == k["mean0_after1"]
+    assert i_cur[1].tolist() == k["i_cur1_after1"]
+    orc.film_roll_acc(i_acc, i_cur)
+    assert i_acc[0].tolist() == k["i_acc0_after_roll1"]
+    orc.film_roll_acc(i_acc, i_cur)
+    assert i_acc[0].tolist() == k["i_acc0_after_roll2"]
+    orc.film_add_frame(s, samples, i_cur, np.array(k["frame2"], np.float64))
+    assert samples[0] == k["samples0_after2"]
+    assert (s[0] / samples[0]).astype(np.float32).tolist() == k["mean0_after2"]
+
+
+def test_oracle_reverse_pass_and_emission_semantics():
+    """Reverse pass cascades subtree sums into parents (wavefront.cpp:505-507); emission keeps
+    decided vertices with finite lo = s / weight (0 where weight <= 0) and sets k_i per pixel."""
+    verts = [None,
+             {"parent": np.array([-1, -1], np.int32), "pixel": np.array([0, 1], np.uint32),
+              "s": np.array([[1.0, 1, 1], [2, 2, 2]]), "weight": np.array([[1, 1, 1], [2, 0, -1]], np.float32)},
+             {"parent": np.array([0, 0, 1], np.int32), "pixel": np.array([0, 0, 1], np.uint32),
+              "s": np.array([[0.5, 0, 0], [0.25, 0, 0], [1, 1, 1]]), "weight": np.ones((3, 3), np.float32)}]
+    orc.reverse_pass(verts)
+    assert verts[1]["s"].tolist() == [[1.75, 1, 1], [3, 3, 3]]
+    for d in (1, 2):
+        n = verts[d]["pixel"].size
+        verts[d].update(p01=np.zeros((n, 3), np.float32), wo01=np.zeros((n, 2), np.float32),
+                        roughness=np.ones(n, np.float32), q_norm=np.ones(n, np.float32),
+                        q_real=np.ones(n, np.float32), decided=np.array([1] * n, np.uint8))
+    i_acc = np.ones((2, 3), np.float32)
+    recs, nf = orc.emit_train(verts, i_acc, 2)
+    assert nf == 0 and len(recs) == 5
+    assert recs[1]["lo_sample"].tolist() == [1.5, 0.0, 0.0]  # weight 0 and -1 channels read as 0
+    assert recs["k_i"].tolist() == [3.0, 2.0, 3.0, 3.0, 2.0]  # pixel 0: 3 samples, pixel 1: 2
+    assert recs["depth"].tolist() == [1, 1, 2, 2, 2]
