@@ -506,6 +506,52 @@ def main():
               "graph_vertices_per_s": n1 / (per_call_us / 1e6), "calls_replayed": 1000}
         st1.close()
 
+    # ---- suffix side: reverse pass + TrainSample emission + k_i + Film update
+    # over a synthetic 4-depth vertex tree in queue order, 2,073,600 depth-1 vertices ----
+    suffix = None
+    if world == 1 and not args.no_extra:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import oracle as orc_gen  # synthetic tree generator (host-side input only)
+        from paper_2510_07868_b200.film import GpuFilm, SuffixStage
+        sizes = [n, int(n * 0.85), int(n * 0.6), int(n * 0.4)]
+        tree = orc_gen.gen_vertex_tree(sizes, n)
+        gv = [None] + [{k: torch.from_numpy(np.ascontiguousarray(a)).to(dev) for k, a in v.items()}
+                       for v in tree[1:]]
+        s0 = [None] + [v["s"].clone() for v in gv[1:]]
+        sx = SuffixStage(local)
+        film = GpuFilm(1920, 1080, sx)
+        frame = torch.rand((1920 * 1080, 3), dtype=torch.float64, device=dev)
+        i_acc = torch.rand((n, 3), dtype=torch.float32, device=dev)
+        recs = torch.empty((sum(sizes), 80), dtype=torch.uint8, device=dev)
+
+        def suffix_step():
+            for d in range(1, len(gv)):
+                gv[d]["s"].copy_(s0[d])
+            sx.reverse_pass(gv)
+            cnt, _ = sx.emit_train(gv, i_acc, n, recs)
+            film.add_frame(frame)
+            film.roll_acc()
+            return cnt
+
+        for _ in range(3):
+            suffix_step()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(5):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            cnt = suffix_step()
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        nv = sum(sizes)
+        suffix = {"vertices": nv, "depths": len(sizes), "train_samples": cnt, "ms": 1e3 * statistics.mean(ts),
+                  "vertices_per_s": nv / statistics.mean(ts),
+                  "note": "wall time per frame incl. the host syncs of fold/k_i error checks; bit-exact vs the "
+                          "reference order (tests/test_gpu_film.py)"}
+        sx.close()
+        del gv, s0, recs
+
     peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}
     hbm = peaks.get("hbm_gbs")
     peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)"
@@ -546,6 +592,8 @@ def main():
         line["strategies"] = extra
     if c1:
         line["c1_launch_bound"] = c1
+    if suffix:
+        line["suffix_stage"] = suffix
     if world == 1 and rank == 0 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args.variant)
     if rank == 0:
