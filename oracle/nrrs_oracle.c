@@ -554,6 +554,151 @@ uint32_t orc_compact_slots(const uint32_t *slots, const uint8_t *used, uint32_t 
 /* vertex i draws from RngStream(0xC0FFEE, i) in the order of
  * test_networks.cpp:37-51 (position, omega_o, roughness, t_x, i_pixel),
  * each vector component drawn left to right. */
+/* ---- StatNet training step (networks.cpp:349-391, mlp.cpp:74-111, hashgrid.cpp:84-103,
+ * optimizer.hpp) ---- */
+
+void orc_relative_l2(float pred, float target, float eps, float *value, float *d_pred) {
+    const float d = pred - target;
+    const float inv = 1.0f / (target * target + eps);
+    *value = d * d * inv;
+    *d_pred = 2.0f * d * inv;
+}
+
+/* Mlp::forward keeping the workspace (pre / post activations of the hidden layers) */
+static void mlp_forward_ws(int in, int out, const float *theta, const float *x, float pre[HLAYERS][HID],
+                           float post[HLAYERS][HID], float *y) {
+    const float slope = 0.01f;
+    const float *a = x;
+    for (int l = 0; l <= HLAYERS; ++l) {
+        const int li = layer_in(in, l), lo = layer_out(out, l);
+        const float *w = theta + layer_offset(in, out, l);
+        const float *b = w + lo * li;
+        float z[HID];
+        for (int r = 0; r < lo; ++r) {
+            float s = 0.0f;
+            for (int c2 = 0; c2 < li; ++c2)
+                s += w[c2 * lo + r] * a[c2];
+            z[r] = s + b[r];
+        }
+        if (l < HLAYERS) {
+            for (int r = 0; r < lo; ++r) {
+                pre[l][r] = z[r];
+                const float zs = z[r] * slope;
+                post[l][r] = z[r] < zs ? zs : z[r];
+            }
+            a = post[l];
+        } else {
+            for (int r = 0; r < lo; ++r)
+                y[r] = z[r];
+        }
+    }
+}
+
+/* Mlp::backward for one sample, accumulating into grad (mlp.cpp:74-111) */
+static void mlp_backward_1(int in, int out, const float *theta, const float *x, float pre[HLAYERS][HID],
+                           float post[HLAYERS][HID], const float *d_y, float *grad, float *d_x) {
+    const float slope = 0.01f;
+    float delta[HID], d_a[HID];
+    for (int r = 0; r < out; ++r)
+        delta[r] = d_y[r];
+    int lo = out;
+    for (int l = HLAYERS; l >= 0; --l) {
+        const int li = layer_in(in, l);
+        const float *w = theta + layer_offset(in, out, l);
+        float *gw = grad + layer_offset(in, out, l);
+        float *gb = gw + lo * li;
+        const float *below = l == 0 ? x : post[l - 1];
+        for (int c2 = 0; c2 < li; ++c2)
+            for (int r = 0; r < lo; ++r)
+                gw[c2 * lo + r] += delta[r] * below[c2];
+        for (int r = 0; r < lo; ++r)
+            gb[r] += delta[r];
+        for (int c2 = 0; c2 < li; ++c2) {  /* d_a = W^T delta */
+            float s = 0.0f;
+            for (int r = 0; r < lo; ++r)
+                s += w[c2 * lo + r] * delta[r];
+            d_a[c2] = s;
+        }
+        if (l == 0) {
+            for (int c2 = 0; c2 < li; ++c2)
+                d_x[c2] = d_a[c2];
+        } else {
+            for (int r = 0; r < HID; ++r)  /* leaky-ReLU derivative on the stored pre-activation */
+                delta[r] = pre[l - 1][r] <= 0.0f ? d_a[r] * slope : d_a[r];
+            lo = HID;
+        }
+    }
+}
+
+double orc_stat_loss(const orc_grid_spec *g, const float *stat_grid, const float *stat_mlp,
+                     const orc_train_sample *batch, size_t n, float eps, float d_scale,
+                     float *g_mlp, float *g_grid) {
+    const int F = g->features, L = g->levels, gd = L * F, in = gd + 16;
+    const uint32_t stride = (1u << g->log2_table_size) * (uint32_t)F;
+    if (g_mlp)
+        memset(g_mlp, 0, sizeof(float) * (size_t)orc_mlp_param_count(in, 6));
+    if (g_grid)
+        memset(g_grid, 0, sizeof(float) * orc_grid_param_count(g));
+    if (n == 0)
+        return 0.0;
+    const float inv_n = 1.0f / (float)n;
+    double loss = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+        const orc_train_sample *s = batch + i;
+        float x[64], pre[HLAYERS][HID], post[HLAYERS][HID], y[6];
+        orc_grid_encode(g, stat_grid, s->position, x);
+        orc_build_stat_tail(s->omega_o, s->roughness, x + gd);
+        mlp_forward_ws(in, 6, stat_mlp, x, pre, post, y);
+        float d_y[6];
+        for (int c2 = 0; c2 < 3; ++c2) {
+            float vm, dm, v2, d2;
+            orc_relative_l2(y[c2], s->lo_sample[c2], eps, &vm, &dm);
+            orc_relative_l2(y[3 + c2], s->lo_sample[c2] * s->lo_sample[c2], eps, &v2, &d2);
+            loss += (double)vm + (double)v2;
+            d_y[c2] = dm * inv_n * d_scale;
+            d_y[3 + c2] = d2 * inv_n * d_scale;
+        }
+        if (!g_mlp)
+            continue;
+        float d_x[64];
+        mlp_backward_1(in, 6, stat_mlp, x, pre, post, d_y, g_mlp, d_x);
+        for (int l = 0; l < L; ++l) {  /* HashGrid::encode_backward: grad[base + f] += w * d_out */
+            const int res = g->base_resolution << l;
+            const float fx = clamp01(s->position[0]) * (float)res, fy = clamp01(s->position[1]) * (float)res,
+                        fz = clamp01(s->position[2]) * (float)res;
+            uint32_t cx = (uint32_t)fx, cy = (uint32_t)fy, cz = (uint32_t)fz;
+            if (cx > (uint32_t)(res - 1)) cx = (uint32_t)(res - 1);
+            if (cy > (uint32_t)(res - 1)) cy = (uint32_t)(res - 1);
+            if (cz > (uint32_t)(res - 1)) cz = (uint32_t)(res - 1);
+            const float tx = fx - (float)cx, ty = fy - (float)cy, tz = fz - (float)cz;
+            for (int c2 = 0; c2 < 8; ++c2) {
+                const uint32_t ox = (c2 & 1), oy = (c2 >> 1) & 1, oz = (c2 >> 2) & 1;
+                const float w = (ox ? tx : 1.0f - tx) * (oy ? ty : 1.0f - ty) * (oz ? tz : 1.0f - tz);
+                const uint32_t base = (uint32_t)l * stride + grid_vertex_index(g, l, cx + ox, cy + oy, cz + oz) * (uint32_t)F;
+                for (int f = 0; f < F; ++f)
+                    g_grid[base + f] += w * d_x[l * F + f];
+            }
+        }
+    }
+    return loss * (double)inv_n;
+}
+
+void orc_adam_step(float *theta, const float *grad, float *m, float *v, size_t n, int64_t t, float lr,
+                   float beta1, float beta2, float eps) {
+    const float c1 = 1.0f / (1.0f - powf(beta1, (float)t));
+    const float c2 = 1.0f / (1.0f - powf(beta2, (float)t));
+    for (size_t i = 0; i < n; ++i) {
+        m[i] = beta1 * m[i] + (1.0f - beta1) * grad[i];
+        v[i] = beta2 * v[i] + (1.0f - beta2) * (grad[i] * grad[i]);
+        theta[i] -= lr * (m[i] * c1) / (sqrtf(v[i] * c2) + eps);
+    }
+}
+
+void orc_ema_update(float *shadow, const float *theta, size_t n, float decay) {
+    for (size_t i = 0; i < n; ++i)
+        shadow[i] = decay * shadow[i] + (1.0f - decay) * theta[i];
+}
+
 /* ---- suffix side of trace_frame ---- */
 
 /* wavefront.cpp:299 / :317 / :355 / :485 (frame[pixel] += term), :301 / :319

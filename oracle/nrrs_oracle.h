@@ -166,6 +166,21 @@ void orc_train_k_i(orc_train_sample *s, size_t start, size_t end, uint32_t n_pix
 void orc_film_add_frame(double *sum, uint32_t *samples, float *i_cur, const double *frame, size_t n_pixels);
 void orc_film_roll_acc(float *i_acc, const float *i_cur, size_t n_pixels);
 
+/* ---- StatNet training step ---- */
+/* RelL2 (networks.cpp:110-114) */
+void orc_relative_l2(float pred, float target, float eps, float *value, float *d_pred);
+/* NeuralRrs::stat_loss_impl (networks.cpp:349-391): batch-mean relative L2 of the 6 stats
+ * against (lo, lo^2); with g_mlp / g_grid non-NULL also the gradients (scaled by d_scale),
+ * through Mlp::backward (mlp.cpp:74-111) and HashGrid::encode_backward (hashgrid.cpp:84-103). */
+double orc_stat_loss(const orc_grid_spec *g, const float *stat_grid, const float *stat_mlp,
+                     const orc_train_sample *batch, size_t n, float eps, float d_scale,
+                     float *g_mlp, float *g_grid);
+/* Adam::step (optimizer.hpp:21-32) with the step counter already incremented to t */
+void orc_adam_step(float *theta, const float *grad, float *m, float *v, size_t n, int64_t t, float lr,
+                   float beta1, float beta2, float eps);
+/* EmaTracker::update (optimizer.hpp:54-61) */
+void orc_ema_update(float *shadow, const float *theta, size_t n, float decay);
+
 /* ---- synthetic inputs (generator follows test_networks.cpp:37-51) ---- */
 void orc_gen_vertices(size_t n, uint32_t n_pixels, uint32_t frame, float *p01, float *wo01,
                       float *rough, float *t_x, float *i_pixel, uint64_t *path_key,

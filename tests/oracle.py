@@ -95,6 +95,10 @@ def lib() -> C.CDLL:
             "orc_train_k_i": (None, [p, C.c_size_t, C.c_size_t, u32]),
             "orc_film_add_frame": (None, [p, p, p, p, C.c_size_t]),
             "orc_film_roll_acc": (None, [p, p, C.c_size_t]),
+            "orc_relative_l2": (None, [f, f, f, p, p]),
+            "orc_stat_loss": (d, [p, p, p, p, C.c_size_t, f, f, p, p]),
+            "orc_adam_step": (None, [p, p, p, p, C.c_size_t, C.c_int64, f, f, f, f]),
+            "orc_ema_update": (None, [p, p, C.c_size_t, f]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -306,3 +310,38 @@ def gen_vertex_tree(depth_sizes: list, n_pixels: int, seed: int = 7) -> list:
                       "decided": (g.random(n) < 0.8).astype(np.uint8)})
         prev_pixel = pixel
     return verts
+
+
+# ---- StatNet training step ----
+def stat_loss(nets: "OracleNets", batch: np.ndarray, eps: float = 0.01, d_scale: float = 1.0, grads: bool = True):
+    """NeuralRrs::stat_loss_impl -> (loss, g_mlp, g_grid) (gradients None when grads=False)."""
+    batch = np.ascontiguousarray(batch, dtype=TRAIN_SAMPLE_DTYPE)
+    gm = np.zeros_like(nets.stat_mlp) if grads else None
+    gg = np.zeros_like(nets.stat_grid) if grads else None
+    loss = lib().orc_stat_loss(C.byref(nets.spec), ptr(nets.stat_grid), ptr(nets.stat_mlp), batch.ctypes.data,
+                               batch.size, eps, d_scale, ptr(gm), ptr(gg))
+    return loss, gm, gg
+
+
+def adam_step(theta, grad, m, v, t, lr, beta1=0.9, beta2=0.999, eps=1e-8):
+    lib().orc_adam_step(ptr(theta), ptr(np.ascontiguousarray(grad, np.float32)), ptr(m), ptr(v), theta.size, t,
+                        lr, beta1, beta2, eps)
+
+
+def ema_update(shadow, theta, decay=0.99):
+    lib().orc_ema_update(ptr(shadow), ptr(theta), theta.size, decay)
+
+
+def gen_train_batch(n: int, seed: int = 11) -> np.ndarray:
+    """Synthetic TrainSamples (position, omega_o, roughness, lo_sample), test_networks.cpp:37-51 style."""
+    g = np.random.default_rng(seed)
+    b = np.zeros(n, TRAIN_SAMPLE_DTYPE)
+    b["position"] = g.random((n, 3), dtype=np.float32)
+    b["omega_o"] = g.random((n, 2), dtype=np.float32)
+    b["roughness"] = g.random(n, dtype=np.float32)
+    b["t_x"] = np.float32(0.2) + g.random((n, 3), dtype=np.float32)
+    b["lo_sample"] = np.float32(0.5) + g.random((n, 3), dtype=np.float32)
+    b["pixel"] = g.integers(0, 1024, n).astype(np.uint32)
+    b["k_i"] = 1.0
+    b["depth"] = 2
+    return b

@@ -318,3 +318,59 @@ def test_oracle_reverse_pass_and_emission_semantics():
     assert recs[1]["lo_sample"].tolist() == [1.5, 0.0, 0.0]  # weight 0 and -1 channels read as 0
     assert recs["k_i"].tolist() == [3.0, 2.0, 3.0, 3.0, 2.0]  # pixel 0: 3 samples, pixel 1: 2
     assert recs["depth"].tolist() == [1, 1, 2, 2, 2]
+
+
+def test_oracle_relative_l2_kat():
+    """RelL2 (networks.cpp:110-114): value (p-t)^2/(t^2+eps), d = 2(p-t)/(t^2+eps)."""
+    import ctypes as C
+    v, d = C.c_float(), C.c_float()
+    orc.lib().orc_relative_l2(1.5, 1.0, 0.01, C.byref(v), C.byref(d))
+    assert v.value == np.float32(np.float32(0.25) * (np.float32(1) / np.float32(1.01)))
+    assert d.value == np.float32(np.float32(1.0) * (np.float32(1) / np.float32(1.01)))
+
+
+def test_oracle_stat_loss_gradient_matches_finite_differences():
+    """The oracle's StatNet gradient (Mlp::backward + HashGrid::encode_backward) against central
+    differences of its own loss, as test_networks.cpp:239-303 checks the reference.  Between
+    leaky-ReLU kinks the relative-L2 loss is quadratic in any single parameter, so central
+    differences are exact up to rounding; kink crossings are allowed for a few parameters."""
+    nets = orc.OracleNets(orc.VARIANT_NRRS, seed=3, randomize=True)
+    batch = orc.gen_train_batch(12)
+    loss, gm, gg = orc.stat_loss(nets, batch)
+    assert np.isfinite(loss) and loss > 0
+
+    def fd(arr, k):
+        saved = arr[k]
+        h = np.float32(max(0.05 * abs(float(saved)), 1e-2))
+        arr[k] = saved + h
+        lp = orc.stat_loss(nets, batch, grads=False)[0]
+        arr[k] = saved - h
+        lm = orc.stat_loss(nets, batch, grads=False)[0]
+        arr[k] = saved
+        return (lp - lm) / (2.0 * float(h))
+
+    bad = checked = 0
+    for k in range(0, nets.stat_mlp.size, 5):
+        ref = fd(nets.stat_mlp, k)
+        checked += 1
+        bad += abs(gm[k] - ref) > 2e-2 * max(abs(ref), 1e-2)
+    assert checked > 600 and bad <= checked // 10, (bad, checked)
+    touched = np.flatnonzero(gg)
+    assert touched.size > 100
+    sel = touched[:: max(1, touched.size // 150)]
+    badg = sum(abs(gg[k] - fd(nets.stat_grid, k)) > 2e-2 * max(abs(fd(nets.stat_grid, k)), 1e-3) for k in sel)
+    assert badg <= sel.size // 10, (badg, sel.size)
+
+
+def test_oracle_adam_and_ema_match_formulas():
+    """Adam::step with bias correction and EmaTracker::update (optimizer.hpp:21-61)."""
+    g = np.random.default_rng(0)
+    theta = g.standard_normal(64).astype(np.float32); grad = g.standard_normal(64).astype(np.float32)
+    m = np.zeros(64, np.float32); v = np.zeros(64, np.float32)
+    th0 = theta.copy()
+    orc.adam_step(theta, grad, m, v, 1, 0.005)
+    # first step: m = 0.1 g, v = 0.001 g^2, c1 = 1/0.1, c2 = 1/0.001 -> update = lr * g / (|g| + eps)
+    np.testing.assert_allclose(theta, th0 - 0.005 * grad / (np.abs(grad) + 1e-8), rtol=1e-5, atol=1e-7)
+    sh = th0.copy()
+    orc.ema_update(sh, theta, 0.99)
+    np.testing.assert_allclose(sh, 0.99 * th0 + 0.01 * theta, rtol=1e-6)
