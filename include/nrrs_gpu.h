@@ -240,6 +240,26 @@ NRRS_API int nrrs_gpu_film_add_frame(nrrs_gpu_ctx *ctx, double *d_sum, uint32_t 
 /* Film::roll_acc (wavefront.cpp:113-116): i_acc = 0.5f * i_acc + 0.5f * i_cur. */
 NRRS_API int nrrs_gpu_film_roll_acc(nrrs_gpu_ctx *ctx, float *d_i_acc, const float *d_i_cur, uint32_t n_pixels);
 
+/* ---- online training, StatNet step ---- */
+
+/* NeuralRrs::stat_loss_impl (networks.cpp:349-391) for one batch of TrainSamples on the
+ * live StatNet parameters (reference layouts): batch-mean relative L2 of the 6 stats against
+ * (lo, lo^2), and its gradient scaled by d_scale through Mlp::backward (mlp.cpp:74-111) and
+ * HashGrid::encode_backward (hashgrid.cpp:84-103).  d_g_mlp / d_g_grid are overwritten;
+ * *h_loss = the loss, *h_finite = 1 iff the loss and every gradient entry are finite (the
+ * apply_step test, networks.cpp:462-470).  Syncs. */
+NRRS_API int nrrs_gpu_stat_loss_grad(nrrs_gpu_ctx *ctx, const nrrs_grid_spec *spec, const float *d_stat_grid,
+                                     const float *d_stat_mlp, const nrrs_train_sample *d_batch, uint64_t n,
+                                     float eps, float d_scale, float *d_g_mlp, float *d_g_grid, double *h_loss,
+                                     int32_t *h_finite);
+
+/* apply_step's update (networks.cpp:471-478): grad *= inv_scale, Adam::step with the step
+ * counter already advanced to t (optimizer.hpp:21-32), then the EMA shadow (optimizer.hpp:54-61;
+ * d_shadow may be NULL).  Asynchronous. */
+NRRS_API int nrrs_gpu_adam_ema(nrrs_gpu_ctx *ctx, float *d_theta, const float *d_grad, float *d_m, float *d_v,
+                               float *d_shadow, uint64_t n, int64_t t, float lr, float beta1, float beta2,
+                               float eps, float inv_scale, float ema_decay);
+
 /* ---- tile-sharded stage (multi-rank), two phases per depth:
  * phase 1: factors + RrsRound uniforms; writes this rank's sum of sanitized
  *          factors (double) to d_local_sum.  The caller all-gathers it.

@@ -188,6 +188,13 @@ struct nrrs_gpu_ctx {
     uint64_t cap_etiles = 0;
     uint32_t *d_hist = nullptr;
     uint64_t cap_hist = 0;
+    // StatNet training scratch
+    float *d_tws = nullptr;
+    uint64_t cap_tws = 0;
+    double *d_tloss = nullptr;
+    uint64_t cap_tloss = 0;
+    float *d_tpart = nullptr;
+    uint64_t cap_tpart = 0;
 
     // host-path pipeline: chunked H2D on copy_stream overlapped with K-A on `stream`
     cudaStream_t copy_stream = nullptr;
@@ -309,7 +316,7 @@ int nrrs_gpu_destroy(nrrs_gpu_ctx *ctx) {
     cudaStreamSynchronize(ctx->stream);
     void *ptrs[] = {ctx->d_stat_grid, ctx->d_rrs_grid, ctx->blob_stat.ptr, ctx->blob_rrs.ptr, ctx->blob_both.ptr,
                     ctx->d_q, ctx->d_u, ctx->d_parts, ctx->d_part_counts, ctx->d_tile_state, ctx->d_ctile_state,
-                    ctx->d_misc, ctx->d_res, ctx->d_sum, ctx->d_total, ctx->d_sync, ctx->d_etile_state, ctx->d_hist, ctx->st.p01, ctx->st.wo01, ctx->st.rough,
+                    ctx->d_misc, ctx->d_res, ctx->d_sum, ctx->d_total, ctx->d_sync, ctx->d_etile_state, ctx->d_hist, ctx->d_tws, ctx->d_tloss, ctx->d_tpart, ctx->st.p01, ctx->st.wo01, ctx->st.rough,
                     ctx->st.weight, ctx->st.ipix, ctx->st.key, ctx->st.q_norm, ctx->st.q_real, ctx->st.q_orig,
                     ctx->st.u, ctx->st.k, ctx->st.offset, ctx->st.slots, ctx->st.decided};
     for (void *p : ptrs)
@@ -900,6 +907,86 @@ int nrrs_gpu_film_roll_acc(nrrs_gpu_ctx *ctx, float *d_i_acc, const float *d_i_c
         return NRRS_EINVAL;
     CK(ctx, cudaSetDevice(ctx->device));
     CK(ctx, launch_film_roll_acc(d_i_acc, d_i_cur, n_pixels, ctx->num_sms, ctx->stream));
+    ctx->launches += 1;
+    return NRRS_OK;
+}
+
+// ---- online training: StatNet step ----
+int nrrs_gpu_stat_loss_grad(nrrs_gpu_ctx *ctx, const nrrs_grid_spec *spec, const float *d_stat_grid,
+                            const float *d_stat_mlp, const nrrs_train_sample *d_batch, uint64_t n, float eps,
+                            float d_scale, float *d_g_mlp, float *d_g_grid, double *h_loss, int32_t *h_finite) {
+    if (!ctx || !spec || !d_stat_grid || !d_stat_mlp || !d_g_mlp || !d_g_grid || !h_loss || !h_finite ||
+        (n && !d_batch))
+        return NRRS_EINVAL;
+    if (spec->features != 2 || spec->levels < 1 || spec->levels * 2 + 16 > 32 || spec->log2_table_size < 1 ||
+        spec->log2_table_size > 30)
+        return fail(ctx, NRRS_EINVAL, "stat_loss_grad: unsupported grid spec");
+    CK(ctx, cudaSetDevice(ctx->device));
+    const int in = spec->levels * 2 + 16, P = train_param_count(in);
+    const uint64_t T = 1ull << spec->log2_table_size, ngrid = (uint64_t)spec->levels * T * 2;
+    CK(ctx, cudaMemsetAsync(d_g_grid, 0, ngrid * sizeof(float), ctx->stream));
+    if (n == 0) {
+        CK(ctx, cudaMemsetAsync(d_g_mlp, 0, (size_t)P * sizeof(float), ctx->stream));
+        CK(ctx, cudaStreamSynchronize(ctx->stream));
+        *h_loss = 0.0;
+        *h_finite = 1;
+        return NRRS_OK;
+    }
+    const uint64_t blocks = (n + 255) / 256;
+    const uint32_t dw = train_dw_ctas(n);
+    CK(ctx, grow(ctx->d_tws, ctx->cap_tws, train_ws_floats(n)));
+    CK(ctx, grow(ctx->d_tloss, ctx->cap_tloss, blocks + 1));
+    CK(ctx, grow(ctx->d_tpart, ctx->cap_tpart, (uint64_t)dw * P));
+    TrainStepParams p{};
+    p.batch = d_batch;
+    p.n = n;
+    p.theta_grid = d_stat_grid;
+    p.mlp = d_stat_mlp;
+    p.in = in;
+    p.grid.levels = spec->levels;
+    p.grid.base_resolution = spec->base_resolution;
+    p.grid.table_size = (uint32_t)T;
+    p.grid.dense_mask = 0;
+    for (int l = 0; l < spec->levels; ++l) {
+        const uint64_t res = (uint64_t)spec->base_resolution << l;
+        if ((res + 1) * (res + 1) * (res + 1) <= T)
+            p.grid.dense_mask |= 1u << l;
+    }
+    p.eps = eps;
+    p.d_scale = d_scale;
+    p.inv_n = 1.0f / (float)n;
+    p.ws = ctx->d_tws;
+    p.g_grid = d_g_grid;
+    p.loss_parts = ctx->d_tloss;
+    uint32_t *nonfinite = ctx->d_misc + 11;
+    double *loss_out = ctx->d_sum + 3;
+    CK(ctx, cudaMemsetAsync(nonfinite, 0, sizeof(uint32_t), ctx->stream));
+    CK(ctx, launch_stat_train(p, ctx->d_tpart, dw, d_g_mlp, loss_out, nonfinite, ngrid, ctx->stream));
+    ctx->launches += 3;
+    uint32_t nf = 0;
+    CK(ctx, cudaMemcpyAsync(h_loss, loss_out, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(ctx, cudaMemcpyAsync(&nf, nonfinite, sizeof nf, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(ctx, cudaStreamSynchronize(ctx->stream));
+    *h_finite = (nf == 0 && std::isfinite(*h_loss)) ? 1 : 0;
+    return NRRS_OK;
+}
+
+int nrrs_gpu_adam_ema(nrrs_gpu_ctx *ctx, float *d_theta, const float *d_grad, float *d_m, float *d_v,
+                      float *d_shadow, uint64_t n, int64_t t, float lr, float beta1, float beta2, float eps,
+                      float inv_scale, float ema_decay) {
+    if (!ctx || t < 1 || (n && (!d_theta || !d_grad || !d_m || !d_v)))
+        return NRRS_EINVAL;
+    CK(ctx, cudaSetDevice(ctx->device));
+    AdamParams a{};
+    a.lr = lr;
+    a.beta1 = beta1;
+    a.beta2 = beta2;
+    a.eps = eps;
+    a.c1 = 1.0f / (1.0f - std::pow(beta1, (float)t));  // optimizer.hpp:28-29 (float pow)
+    a.c2 = 1.0f / (1.0f - std::pow(beta2, (float)t));
+    a.inv_scale = inv_scale;
+    a.decay = ema_decay;
+    CK(ctx, launch_adam_ema(d_theta, d_grad, d_m, d_v, d_shadow, n, a, ctx->num_sms, ctx->stream));
     ctx->launches += 1;
     return NRRS_OK;
 }

@@ -190,6 +190,34 @@ cudaError_t launch_emit_train(const TrainParams &p, cudaStream_t stream);
 cudaError_t launch_k_i(nrrs_train_sample *s, uint64_t start, const unsigned long long *end, uint64_t capacity,
                        uint32_t *hist, uint32_t n_pixels, int num_sms, cudaStream_t stream);
 
+// StatNet training step (nrrs_train.cu)
+struct TrainGrid {
+    int32_t levels, base_resolution;
+    uint32_t table_size, dense_mask;
+};
+struct TrainStepParams {
+    const nrrs_train_sample *batch;
+    uint64_t n;
+    const float *theta_grid;  // live StatNet grid, reference layout [level][entry][feature]
+    const float *mlp;         // live StatNet MLP theta (mlp.cpp:7-32 layout)
+    int32_t in;               // StatNet input width (levels * 2 + 16)
+    TrainGrid grid;
+    float eps, d_scale, inv_n;
+    float *ws;                // per-sample workspace
+    float *g_grid;            // zeroed by the caller
+    double *loss_parts;       // [blocks]
+};
+struct AdamParams {
+    float lr, beta1, beta2, eps, c1, c2, inv_scale, decay;
+};
+size_t train_ws_floats(uint64_t n);
+int train_param_count(int in);
+uint32_t train_dw_ctas(uint64_t n);
+cudaError_t launch_stat_train(const TrainStepParams &p, float *partials, uint32_t dw_ctas, float *g_mlp,
+                              double *loss_out, uint32_t *nonfinite, uint64_t ngrid, cudaStream_t stream);
+cudaError_t launch_adam_ema(float *theta, const float *grad, float *m, float *v, float *shadow, uint64_t n,
+                            const AdamParams &a, int num_sms, cudaStream_t stream);
+
 size_t infer_smem_bytes(int kind, const InferParams &p);
 cudaError_t launch_infer(int kind, const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out);
 uint32_t infer_max_grid(int num_sms);

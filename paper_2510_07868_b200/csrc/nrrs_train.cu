@@ -1,0 +1,337 @@
+// nrrs_train.cu -- one StatNet training step on the GPU:
+// NeuralRrs::stat_loss_impl (networks.cpp:349-391) with Mlp::backward
+// (mlp.cpp:74-111) and HashGrid::encode_backward (hashgrid.cpp:84-103), then
+// Adam (optimizer.hpp:21-32) and the EMA shadow (optimizer.hpp:54-61).
+//
+//   stat_fwd_bwd_kernel  one thread per TrainSample: grid encode + stat tail,
+//                        MLP forward (fp32), relative-L2 loss and d_y, the
+//                        backward through the MLP, and the grid gradient by
+//                        scatter-add; activations and deltas go to a per-sample
+//                        workspace record for the weight gradients
+//   stat_dw_kernel       dW = sum_s delta_s in_s^T, db = sum_s delta_s: per-CTA
+//                        partials over sample chunks staged in smem, then a
+//                        fixed-order reduction over CTAs
+//   adam_ema_kernel      grad * inv_scale -> Adam with bias correction -> EMA
+#include "nrrs_device.cuh"
+#include "nrrs_internal.h"
+
+#include <cuda_runtime.h>
+
+namespace nrrs {
+
+constexpr int kTH = 32;                       // hidden width (mlp.hpp)
+constexpr int kTOut = 6;                      // StatNet outputs
+constexpr int kWs = 4 * kTH + 3 * kTH + 8;    // per-sample workspace: in0, post0..2, delta0..2, delta3
+constexpr int kDwChunk = 32;                  // samples staged per smem chunk in stat_dw_kernel
+
+__host__ __device__ inline int stat_param_count(int in) {
+    return (kTH * in + kTH) + 2 * (kTH * kTH + kTH) + (kTOut * kTH + kTOut);
+}
+__host__ __device__ inline int stat_layer_offset(int in, int l) {
+    return l == 0 ? 0 : (kTH * in + kTH) + (l - 1) * (kTH * kTH + kTH);
+}
+
+// one_blob_encode (encodings.hpp:31-44), exact exp
+__device__ __forceinline__ void one_blob_exact(float x, int bins, float *out) {
+    const float sigma = 1.0f / (float)bins;
+    const float inv_two_sigma2 = 1.0f / (2.0f * sigma * sigma);
+    float sum = 0.0f;
+    for (int i = 0; i < bins; ++i) {
+        const float d = x - ((float)i + 0.5f) / (float)bins;
+        out[i] = expf(-d * d * inv_two_sigma2);
+        sum += out[i];
+    }
+    const float inv = 1.0f / sum;
+    for (int i = 0; i < bins; ++i)
+        out[i] *= inv;
+}
+
+// the 8 corners of level l: table offsets (floats) and trilinear weights (hashgrid.cpp:38-82)
+__device__ __forceinline__ void grid_corners(const TrainGrid &g, int l, const float p[3], uint32_t base[8],
+                                             float w[8]) {
+    const uint32_t res = (uint32_t)g.base_resolution << l;
+    float f[3];
+    uint32_t c[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const float v = p[a] < 0.0f ? 0.0f : (1.0f < p[a] ? 1.0f : p[a]);
+        f[a] = v * (float)res;
+        c[a] = min((uint32_t)f[a], res - 1u);
+    }
+    const float tx = f[0] - (float)c[0], ty = f[1] - (float)c[1], tz = f[2] - (float)c[2];
+    const bool dense = (g.dense_mask >> l) & 1u;
+    const uint32_t nn = res + 1u, m = g.table_size - 1u;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t ox = k & 1, oy = (k >> 1) & 1, oz = k >> 2;
+        w[k] = (ox ? tx : 1.0f - tx) * (oy ? ty : 1.0f - ty) * (oz ? tz : 1.0f - tz);
+        const uint32_t x = c[0] + ox, y = c[1] + oy, z = c[2] + oz;
+        const uint32_t idx = dense ? (x * nn + y) * nn + z : (x ^ (y * 2654435761u) ^ (z * 805459861u)) & m;
+        base[k] = ((uint32_t)l * g.table_size + idx) * 2u;
+    }
+}
+
+__global__ void __launch_bounds__(256) stat_fwd_bwd_kernel(TrainStepParams p) {
+    extern __shared__ float w_s[];
+    const int tid = threadIdx.x;
+    const int in = p.in, P = stat_param_count(in);
+    for (int i = tid; i < P; i += blockDim.x)
+        w_s[i] = p.mlp[i];
+    __syncthreads();
+    const float slope = 0.01f;
+    const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + tid;
+    double my_loss = 0.0;
+    if (s < p.n) {
+        const nrrs_train_sample &t = p.batch[s];
+        float *ws = p.ws + s * kWs;
+        const int gd = 2 * p.grid.levels;
+        float a[kTH];
+        // ---- encode_stat_inputs (networks.cpp:206-217): grid features, then the stat tail ----
+        for (int l = 0; l < p.grid.levels; ++l) {
+            uint32_t base[8];
+            float w[8];
+            grid_corners(p.grid, l, t.position, base, w);
+            float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                a0 += w[k] * __ldg(p.theta_grid + base[k]);
+                a1 += w[k] * __ldg(p.theta_grid + base[k] + 1);
+            }
+            a[2 * l] = a0;
+            a[2 * l + 1] = a1;
+        }
+        one_blob_exact(t.omega_o[0], 4, a + gd);
+        one_blob_exact(t.omega_o[1], 4, a + gd + 4);
+        one_blob_exact(1.0f - expf(-t.roughness), 8, a + gd + 8);  // roughness_remap (encodings.hpp:65-67)
+        for (int i = in; i < kTH; ++i)
+            a[i] = 0.0f;
+        for (int i = 0; i < kTH; ++i)
+            ws[i] = a[i];
+        // ---- Mlp::forward (mlp.cpp:52-72), keeping post-activations ----
+        for (int l = 0; l < 3; ++l) {
+            const int li = l == 0 ? in : kTH;
+            const float *W = w_s + stat_layer_offset(in, l), *b = W + kTH * li;
+            float z[kTH];
+            for (int r = 0; r < kTH; ++r) {
+                float acc = 0.0f;
+                for (int c = 0; c < li; ++c)
+                    acc += W[c * kTH + r] * a[c];
+                z[r] = acc + b[r];
+            }
+            for (int r = 0; r < kTH; ++r) {
+                const float zs = z[r] * slope;
+                a[r] = z[r] < zs ? zs : z[r];  // cwiseMax(z, slope z)
+                ws[kTH * (l + 1) + r] = a[r];
+            }
+        }
+        float y[kTOut];
+        {
+            const float *W = w_s + stat_layer_offset(in, 3), *b = W + kTOut * kTH;
+            for (int r = 0; r < kTOut; ++r) {
+                float acc = 0.0f;
+                for (int c = 0; c < kTH; ++c)
+                    acc += W[c * kTOut + r] * a[c];
+                y[r] = acc + b[r];
+            }
+        }
+        // ---- relative L2 against (lo, lo^2) (networks.cpp:370-381) ----
+        float dy[kTOut];
+        for (int c = 0; c < 3; ++c) {
+            const float lo = t.lo_sample[c];
+            const float t2 = lo * lo;
+            const float d1 = y[c] - lo, inv1 = 1.0f / (lo * lo + p.eps);
+            const float d2 = y[3 + c] - t2, inv2 = 1.0f / (t2 * t2 + p.eps);
+            my_loss += (double)(d1 * d1 * inv1) + (double)(d2 * d2 * inv2);
+            dy[c] = 2.0f * d1 * inv1 * p.inv_n * p.d_scale;
+            dy[3 + c] = 2.0f * d2 * inv2 * p.inv_n * p.d_scale;
+        }
+        // ---- Mlp::backward (mlp.cpp:74-111) ----
+        float *dws = ws + 4 * kTH;  // delta0 [32], delta1 [32], delta2 [32], delta3 [8]
+        for (int r = 0; r < kTOut; ++r)
+            dws[3 * kTH + r] = dy[r];
+        float delta[kTH];
+        {
+            const float *W = w_s + stat_layer_offset(in, 3);
+            for (int c = 0; c < kTH; ++c) {
+                float acc = 0.0f;
+                for (int r = 0; r < kTOut; ++r)
+                    acc += W[c * kTOut + r] * dy[r];
+                delta[c] = a[c] <= 0.0f ? acc * slope : acc;  // post2 <= 0 <=> pre2 <= 0
+            }
+        }
+        for (int l = 2; l >= 0; --l) {
+            for (int r = 0; r < kTH; ++r)
+                dws[kTH * l + r] = delta[r];
+            const int li = l == 0 ? in : kTH;
+            const float *W = w_s + stat_layer_offset(in, l);
+            float da[kTH];
+            for (int c = 0; c < li; ++c) {
+                float acc = 0.0f;
+                for (int r = 0; r < kTH; ++r)
+                    acc += W[c * kTH + r] * delta[r];
+                da[c] = acc;
+            }
+            if (l > 0) {
+                const float *post = ws + kTH * l;  // post_{l-1}
+                for (int c = 0; c < kTH; ++c)
+                    delta[c] = post[c] <= 0.0f ? da[c] * slope : da[c];
+            } else {
+                // ---- HashGrid::encode_backward: grad[base + f] += w * d_x ----
+                for (int lv = 0; lv < p.grid.levels; ++lv) {
+                    uint32_t base[8];
+                    float w[8];
+                    grid_corners(p.grid, lv, t.position, base, w);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        atomicAdd(p.g_grid + base[k], w[k] * da[2 * lv]);
+                        atomicAdd(p.g_grid + base[k] + 1, w[k] * da[2 * lv + 1]);
+                    }
+                }
+            }
+        }
+    }
+    // block sum of the per-sample loss terms (fixed order) -> loss_parts[block]
+    __shared__ double red[8];
+    double v = my_loss;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((tid & 31) == 0)
+        red[tid >> 5] = v;
+    __syncthreads();
+    if (tid == 0) {
+        double b = 0.0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i)
+            b += red[i];
+        p.loss_parts[blockIdx.x] = b;
+    }
+}
+
+// weight / bias gradients from the workspace: CTA b sums samples [b*per, (b+1)*per)
+__global__ void __launch_bounds__(256) stat_dw_kernel(const float *ws, uint64_t n, int in, uint64_t per,
+                                                      float *partials) {
+    __shared__ float st[kDwChunk][kWs];
+    const int tid = threadIdx.x, P = stat_param_count(in);
+    constexpr int kMaxOwn = 14;  // ceil(3366 / 256)
+    float acc[kMaxOwn];
+    int doff[kMaxOwn], ioff[kMaxOwn];
+#pragma unroll
+    for (int k = 0; k < kMaxOwn; ++k) {
+        acc[k] = 0.0f;
+        doff[k] = -1;
+        ioff[k] = -1;
+        const int q = tid + 256 * k;
+        if (q >= P)
+            continue;
+        int l = 3;
+        while (l > 0 && q < stat_layer_offset(in, l))
+            --l;
+        const int li = l == 0 ? in : kTH, lo = l == 3 ? kTOut : kTH;
+        const int e = q - stat_layer_offset(in, l);
+        if (e < lo * li) {  // column-major W: e = c * lo + r
+            doff[k] = 4 * kTH + kTH * l + e % lo;
+            ioff[k] = kTH * l + e / lo;
+        } else {            // bias r
+            doff[k] = 4 * kTH + kTH * l + (e - lo * li);
+            ioff[k] = -1;
+        }
+    }
+    const uint64_t s0 = (uint64_t)blockIdx.x * per, s1 = s0 + per < n ? s0 + per : n;
+    for (uint64_t c0 = s0; c0 < s1; c0 += kDwChunk) {
+        const int cnt = (int)(s1 - c0 < (uint64_t)kDwChunk ? s1 - c0 : (uint64_t)kDwChunk);
+        for (int i = tid; i < cnt * kWs; i += 256)
+            st[i / kWs][i % kWs] = ws[c0 * kWs + i];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kMaxOwn; ++k) {
+            if (doff[k] < 0)
+                continue;
+            float a = acc[k];
+            for (int j = 0; j < cnt; ++j)
+                a += st[j][doff[k]] * (ioff[k] >= 0 ? st[j][ioff[k]] : 1.0f);
+            acc[k] = a;
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int k = 0; k < kMaxOwn; ++k) {
+        const int q = tid + 256 * k;
+        if (q < P)
+            partials[(uint64_t)blockIdx.x * P + q] = acc[k];
+    }
+}
+
+// g_mlp[q] = sum over CTAs (fixed order); loss = sum of block parts * inv_n; finite flags
+__global__ void stat_reduce_kernel(const float *partials, int nparts, int P, float *g_mlp, const double *loss_parts,
+                                   int nloss, float inv_n, double *loss_out, const float *g_grid, uint64_t ngrid,
+                                   uint32_t *nonfinite) {
+    const int tid = threadIdx.x + blockIdx.x * blockDim.x;
+    for (int q = tid; q < P; q += gridDim.x * blockDim.x) {
+        float s = 0.0f;
+        for (int b = 0; b < nparts; ++b)
+            s += partials[(uint64_t)b * P + q];
+        g_mlp[q] = s;
+        if (!isfinite(s))
+            atomicOr(nonfinite, 1u);
+    }
+    for (uint64_t i = tid; i < ngrid; i += (uint64_t)gridDim.x * blockDim.x)
+        if (!isfinite(g_grid[i]))
+            atomicOr(nonfinite, 1u);
+    if (tid == 0) {
+        double l = 0.0;
+        for (int b = 0; b < nloss; ++b)
+            l += loss_parts[b];
+        *loss_out = l * (double)inv_n;
+    }
+}
+
+// grad *= inv_scale; Adam::step (optimizer.hpp:21-32); EmaTracker::update (:54-61)
+__global__ void adam_ema_kernel(float *theta, const float *grad, float *m, float *v, float *shadow, uint64_t n,
+                                AdamParams a) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const float g = __fmul_rn(grad[i], a.inv_scale);
+        const float mi = __fadd_rn(__fmul_rn(a.beta1, m[i]), __fmul_rn(__fsub_rn(1.0f, a.beta1), g));
+        const float vi = __fadd_rn(__fmul_rn(a.beta2, v[i]), __fmul_rn(__fsub_rn(1.0f, a.beta2), __fmul_rn(g, g)));
+        m[i] = mi;
+        v[i] = vi;
+        const float upd = __fdiv_rn(__fmul_rn(a.lr, __fmul_rn(mi, a.c1)), __fadd_rn(__fsqrt_rn(__fmul_rn(vi, a.c2)), a.eps));
+        const float th = __fsub_rn(theta[i], upd);
+        theta[i] = th;
+        if (shadow)
+            shadow[i] = __fadd_rn(__fmul_rn(a.decay, shadow[i]), __fmul_rn(__fsub_rn(1.0f, a.decay), th));
+    }
+}
+
+// ---- launchers ----
+size_t train_ws_floats(uint64_t n) { return (size_t)n * kWs; }
+int train_param_count(int in) { return stat_param_count(in); }
+uint32_t train_dw_ctas(uint64_t n) {
+    const uint64_t c = (n + 511) / 512;
+    return (uint32_t)(c < 1 ? 1 : (c > 256 ? 256 : c));
+}
+
+cudaError_t launch_stat_train(const TrainStepParams &p, float *partials, uint32_t dw_ctas, float *g_mlp,
+                              double *loss_out, uint32_t *nonfinite, uint64_t ngrid, cudaStream_t stream) {
+    const uint32_t blocks = (uint32_t)((p.n + 255) / 256);
+    const size_t smem = (size_t)stat_param_count(p.in) * sizeof(float);
+    cudaError_t e = cudaFuncSetAttribute(stat_fwd_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess)
+        return e;
+    stat_fwd_bwd_kernel<<<blocks, 256, smem, stream>>>(p);
+    const uint64_t per = (p.n + dw_ctas - 1) / dw_ctas;
+    stat_dw_kernel<<<dw_ctas, 256, 0, stream>>>(p.ws, p.n, p.in, per, partials);
+    stat_reduce_kernel<<<64, 256, 0, stream>>>(partials, (int)dw_ctas, stat_param_count(p.in), g_mlp, p.loss_parts,
+                                               (int)blocks, p.inv_n, loss_out, p.g_grid, ngrid, nonfinite);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_adam_ema(float *theta, const float *grad, float *m, float *v, float *shadow, uint64_t n,
+                            const AdamParams &a, int num_sms, cudaStream_t stream) {
+    if (n == 0)
+        return cudaSuccess;
+    const uint64_t want = (n + 255) / 256, cap = (uint64_t)num_sms * 8;
+    adam_ema_kernel<<<(uint32_t)(want < cap ? want : cap), 256, 0, stream>>>(theta, grad, m, v, shadow, n, a);
+    return cudaGetLastError();
+}
+
+}  // namespace nrrs

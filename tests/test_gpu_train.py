@@ -1,0 +1,93 @@
+"""GPU: one StatNet training step against the oracle: loss and
+gradients (Mlp/HashGrid backward, FD-pinned on the oracle side), Adam + EMA bit for bit
+on equal gradients, a short training sequence, and the loss-scale skip on non-finite
+batches (networks.cpp:349-391, :462-552; optimizer.hpp)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as orc
+from helpers import mirror_nets
+
+pytestmark = pytest.mark.gpu
+
+
+def _batch(n, seed=11):
+    b = orc.gen_train_batch(n, seed)
+    return b, torch.from_numpy(b.view(np.uint8).reshape(n, 80).copy()).cuda()
+
+
+def _rel(a, b):
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
+
+
+@pytest.fixture(scope="module")
+def onets():
+    return orc.OracleNets(orc.VARIANT_NRRS, seed=3, randomize=True)
+
+
+def test_stat_loss_and_gradients_match_oracle(onets):
+    from paper_2510_07868_b200.training import StatNetTrainer
+    hb, db = _batch(4097)
+    loss, gm, gg = orc.stat_loss(onets, hb)
+    tr = StatNetTrainer(mirror_nets(onets))
+    gl, fin = tr.loss_and_grad(db)
+    assert fin and abs(gl - loss) <= 1e-6 * abs(loss)
+    assert _rel(tr.g_mlp.cpu().numpy(), gm) < 1e-4
+    assert _rel(tr.g_grid.cpu().numpy(), gg) < 1e-4
+    tr.close()
+
+
+def test_adam_ema_bitexact_on_equal_gradients(onets):
+    from paper_2510_07868_b200.training import StatNetTrainer
+    hb, _ = _batch(512)
+    _, gm, gg = orc.stat_loss(onets, hb)
+    tr = StatNetTrainer(mirror_nets(onets))
+    theta, m, v, sh = onets.stat_mlp.copy(), np.zeros_like(gm), np.zeros_like(gm), onets.stat_mlp.copy()
+    for t in (1, 2, 3):
+        tr.g_mlp.copy_(torch.from_numpy(gm))
+        tr._adam(tr.adam_mlp, tr.mlp, tr.g_mlp, tr.shadow_mlp, 1.0)
+        orc.adam_step(theta, gm, m, v, t, 0.005)
+        orc.ema_update(sh, theta, 0.99)
+    np.testing.assert_array_equal(tr.mlp.cpu().numpy(), theta)
+    np.testing.assert_array_equal(tr.adam_mlp.m.cpu().numpy(), m)
+    np.testing.assert_array_equal(tr.adam_mlp.v.cpu().numpy(), v)
+    np.testing.assert_array_equal(tr.shadow_mlp.cpu().numpy(), sh)
+    tr.close()
+
+
+def test_training_sequence_tracks_oracle_and_lowers_loss(onets):
+    from paper_2510_07868_b200.training import StatNetTrainer
+    nets = orc.OracleNets(orc.VARIANT_NRRS, seed=3, randomize=True)
+    tr = StatNetTrainer(mirror_nets(nets))
+    st = {k: (np.zeros_like(getattr(nets, k)), np.zeros_like(getattr(nets, k))) for k in ("stat_mlp", "stat_grid")}
+    losses = []
+    for step in range(1, 6):
+        hb, db = _batch(8192, seed=100 + step)
+        gl, applied = tr.step(db)
+        loss, gm, gg = orc.stat_loss(nets, hb)
+        assert applied and abs(gl - loss) <= 1e-4 * abs(loss), (step, gl, loss)
+        for k, g in (("stat_mlp", gm), ("stat_grid", gg)):
+            orc.adam_step(getattr(nets, k), g, st[k][0], st[k][1], step, 0.005)
+        losses.append(loss)
+    assert _rel(tr.mlp.cpu().numpy(), nets.stat_mlp) < 1e-3
+    assert _rel(tr.grid.cpu().numpy(), nets.stat_grid) < 1e-3
+    hb, db = _batch(8192, seed=100)
+    assert tr.loss_and_grad(db)[0] < orc.stat_loss(orc.OracleNets(orc.VARIANT_NRRS, seed=3, randomize=True), hb,
+                                                   grads=False)[0]
+    tr.close()
+
+
+def test_non_finite_batch_is_skipped_and_halves_the_loss_scale(onets):
+    from paper_2510_07868_b200.training import StatNetTrainer
+    hb, _ = _batch(300)
+    hb["lo_sample"][17, 1] = np.inf
+    db = torch.from_numpy(hb.view(np.uint8).reshape(300, 80).copy()).cuda()
+    tr = StatNetTrainer(mirror_nets(onets))
+    before = tr.mlp.clone()
+    loss, applied = tr.step(db)
+    assert not applied and tr.scale == 0.5 and tr.skipped_steps == 1
+    assert torch.equal(tr.mlp, before)
+    tr.close()
