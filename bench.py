@@ -552,6 +552,41 @@ def main():
         sx.close()
         del gv, s0, recs
 
+    # ---- online training: one StatNet step at the reference batch (1 << 16) ----
+    train = None
+    if world == 1 and not args.no_extra:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import oracle as orc_gen  # synthetic TrainSamples (host-side input only)
+        from paper_2510_07868_b200.training import StatNetTrainer
+        nb = 1 << 16
+        hb = orc_gen.gen_train_batch(nb, seed=5)
+        db = torch.from_numpy(hb.view(np.uint8).reshape(nb, 80).copy()).to(dev)
+        tr = StatNetTrainer(NeuralRrs(NeuralRrsConfig(variant=RrsVariant.Nrrs, seed=1)).randomize_for_benchmark(),
+                            device=local)
+        for _ in range(3):
+            tr.step(db)
+        torch.cuda.synchronize()
+        ts, losses = [], []
+        for _ in range(10):
+            t0 = time.perf_counter()
+            loss, _ = tr.step(db)
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+            losses.append(loss)
+        # the same step on the host: the oracle's stat_loss_impl + Adam/EMA (1 thread, C port)
+        on = orc_gen.OracleNets(orc_gen.VARIANT_NRRS, seed=1, randomize=True)
+        t0 = time.perf_counter()
+        _, gm_h, gg_h = orc_gen.stat_loss(on, hb)
+        for arr, g in ((on.stat_mlp, gm_h), (on.stat_grid, gg_h)):
+            orc_gen.adam_step(arr, g, np.zeros_like(arr), np.zeros_like(arr), 1, 0.005)
+            orc_gen.ema_update(arr.copy(), arr)
+        cpu_ms = 1e3 * (time.perf_counter() - t0)
+        train = {"batch": nb, "ms_per_step": 1e3 * statistics.mean(ts), "samples_per_s": nb / statistics.mean(ts),
+                 "cpu_port_ms_per_step": cpu_ms,
+                 "params": int(tr.grid.numel() + tr.mlp.numel()), "loss_first": losses[0], "loss_last": losses[-1],
+                 "note": "step_statnet: loss + gradients + Adam + EMA, wall time incl. the finite-check sync"}
+        tr.close()
+
     peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}
     hbm = peaks.get("hbm_gbs")
     peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)"
@@ -594,6 +629,8 @@ def main():
         line["c1_launch_bound"] = c1
     if suffix:
         line["suffix_stage"] = suffix
+    if train:
+        line["statnet_train_step"] = train
     if world == 1 and rank == 0 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args.variant)
     if rank == 0:
