@@ -683,6 +683,127 @@ double orc_stat_loss(const orc_grid_spec *g, const float *stat_grid, const float
     return loss * (double)inv_n;
 }
 
+/* grad_pixelvar_wrt_rr / _split (networks.cpp:116-130) */
+static float grad_pixelvar_wrt_rr(const float weight[3], const float h_sample[3], float p_rr) {
+    const float w = orc_luminance(weight), h = orc_luminance(h_sample);
+    return -(w * w) * (h * h) / (p_rr * p_rr);
+}
+static float grad_pixelvar_wrt_split(const float weight[3], float h_variance_lum, float n_s) {
+    const float w = orc_luminance(weight);
+    return -(w * w) * h_variance_lum / (n_s * n_s);
+}
+/* encodings.hpp:77-83 */
+static float softplus_mod_grad(float x) {
+    if (x < 0.0f) {
+        const float e = expf(x);
+        return e / (1.0f + e);
+    }
+    return 0.5f;
+}
+
+void orc_rrs_loss(int variant, const orc_grid_spec *g, const float *snap_stat_grid, const float *snap_stat_mlp,
+                  const float *rrs_grid, const float *rrs_mlp, const orc_train_sample *batch, size_t n,
+                  const orc_pixel_error *errors, size_t n_errors, float e_avg, int phase, float gamma_min,
+                  float gamma_avg, float gamma_rrs, float eps, float d_scale, float *g_mlp, float *g_grid,
+                  orc_rrs_parts *parts) {
+    const int F = g->features, L = g->levels, gd = L * F;
+    const int in = variant == ORC_VARIANT_NRRS ? 11 : gd + 16;
+    const uint32_t stride = (1u << g->log2_table_size) * (uint32_t)F;
+    memset(parts, 0, sizeof *parts);
+    if (g_mlp)
+        memset(g_mlp, 0, sizeof(float) * (size_t)orc_mlp_param_count(in, 1));
+    if (g_grid && variant == ORC_VARIANT_AID)
+        memset(g_grid, 0, sizeof(float) * orc_grid_param_count(g));
+    if (n == 0)
+        return;
+    const float inv_n = 1.0f / (float)n;
+    for (size_t i = 0; i < n; ++i) {
+        const orc_train_sample *s = batch + i;
+        /* snapshot_stats_batch (networks.cpp:219-224) */
+        float xs[64], stats[6];
+        orc_grid_encode(g, snap_stat_grid, s->position, xs);
+        orc_build_stat_tail(s->omega_o, s->roughness, xs + gd);
+        orc_mlp_forward(gd + 16, 6, snap_stat_mlp, xs, stats);
+        /* encode_rrs_inputs (networks.cpp:226-250) */
+        float x[64];
+        if (variant == ORC_VARIANT_NRRS) {
+            orc_build_nrrs_input(stats, stats + 3, s->t_x, s->i_pixel, s->roughness, x);
+        } else {
+            orc_grid_encode(g, rrs_grid, s->position, x);
+            orc_build_aid_tail(s->omega_o, s->t_x, s->i_pixel, s->roughness, x + gd);
+        }
+        float pre[HLAYERS][HID], post[HLAYERS][HID], y[1];
+        mlp_forward_ws(in, 1, rrs_mlp, x, pre, post, y);
+        const float z = y[0], q = orc_softplus_mod(z);
+        float d_q = 0.0f;
+        if (phase == 0) {
+            float v, d;
+            orc_relative_l2(q, 1.0f, eps, &v, &d);
+            parts->rrs += v;
+            d_q = d * inv_n;
+        } else {
+            const size_t px = s->pixel;
+            const float inv_k = s->k_i > 0.0f ? 1.0f / s->k_i : 1.0f;
+            if (px < n_errors) {
+                const orc_pixel_error *pe = errors + px;
+                float gvar = 0.0f;
+                if (s->q_real < 1.0f) {
+                    if (s->q_real > 0.0f)
+                        gvar = grad_pixelvar_wrt_rr(s->t_x, s->lo_sample, s->q_real);
+                } else {
+                    float var[3];
+                    for (int c2 = 0; c2 < 3; ++c2) {
+                        const float vv = stats[3 + c2] - stats[c2] * stats[c2];
+                        var[c2] = vv < 0.0f ? 0.0f : vv;  /* cwiseMax(0) */
+                    }
+                    gvar = grad_pixelvar_wrt_split(s->t_x, orc_luminance(var), s->q_real);
+                }
+                const float de_dq = pe->inv_denom * gvar * inv_k;
+                parts->min += pe->e * inv_k;
+                const float dev = pe->e - e_avg;
+                parts->avg += dev * dev * inv_k;
+                d_q += (gamma_min * de_dq + gamma_avg * 2.0f * dev * de_dq) * inv_n;
+            } else {
+                ++parts->skipped;
+            }
+            const float dq_gap = q - s->q_norm;
+            parts->rrs += dq_gap * dq_gap;
+            d_q += gamma_rrs * 2.0f * dq_gap * inv_n;
+        }
+        if (!g_mlp)
+            continue;
+        const float dy = d_q * softplus_mod_grad(z) * d_scale;
+        float d_x[64];
+        mlp_backward_1(in, 1, rrs_mlp, x, pre, post, &dy, g_mlp, d_x);
+        if (variant == ORC_VARIANT_AID && g_grid) {
+            for (int l = 0; l < L; ++l) {
+                const int res = g->base_resolution << l;
+                const float fx = clamp01(s->position[0]) * (float)res, fy = clamp01(s->position[1]) * (float)res,
+                            fz = clamp01(s->position[2]) * (float)res;
+                uint32_t cx = (uint32_t)fx, cy = (uint32_t)fy, cz = (uint32_t)fz;
+                if (cx > (uint32_t)(res - 1)) cx = (uint32_t)(res - 1);
+                if (cy > (uint32_t)(res - 1)) cy = (uint32_t)(res - 1);
+                if (cz > (uint32_t)(res - 1)) cz = (uint32_t)(res - 1);
+                const float tx = fx - (float)cx, ty = fy - (float)cy, tz = fz - (float)cz;
+                for (int c2 = 0; c2 < 8; ++c2) {
+                    const uint32_t ox = (c2 & 1), oy = (c2 >> 1) & 1, oz = (c2 >> 2) & 1;
+                    const float w = (ox ? tx : 1.0f - tx) * (oy ? ty : 1.0f - ty) * (oz ? tz : 1.0f - tz);
+                    const uint32_t base = (uint32_t)l * stride +
+                                          grid_vertex_index(g, l, cx + ox, cy + oy, cz + oz) * (uint32_t)F;
+                    for (int f = 0; f < F; ++f)
+                        g_grid[base + f] += w * d_x[l * F + f];
+                }
+            }
+        }
+    }
+    parts->min *= (double)inv_n;
+    parts->avg *= (double)inv_n;
+    parts->rrs *= (double)inv_n;
+    parts->total = phase == 0 ? parts->rrs
+                              : (double)gamma_min * parts->min + (double)gamma_avg * parts->avg +
+                                    (double)gamma_rrs * parts->rrs;
+}
+
 void orc_adam_step(float *theta, const float *grad, float *m, float *v, size_t n, int64_t t, float lr,
                    float beta1, float beta2, float eps) {
     const float c1 = 1.0f / (1.0f - powf(beta1, (float)t));

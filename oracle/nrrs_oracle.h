@@ -175,6 +175,17 @@ void orc_relative_l2(float pred, float target, float eps, float *value, float *d
 double orc_stat_loss(const orc_grid_spec *g, const float *stat_grid, const float *stat_mlp,
                      const orc_train_sample *batch, size_t n, float eps, float d_scale,
                      float *g_mlp, float *g_grid);
+/* PixelError (networks.hpp:86-92) and the RRSNet loss parts (networks.hpp:219-224) */
+typedef struct { float e, inv_denom; } orc_pixel_error;
+typedef struct { double min, avg, rrs, total; uint32_t skipped; } orc_rrs_parts;
+/* NeuralRrs::rrs_loss_impl (networks.cpp:418-460): snapshot stats from (snap_stat_grid,
+ * snap_stat_mlp), RRSNet on the live (rrs_grid, rrs_mlp) of `variant`; phase 0 = Warmup,
+ * 1 = Full.  Gradients (scaled by d_scale) into g_mlp / g_grid when non-NULL. */
+void orc_rrs_loss(int variant, const orc_grid_spec *g, const float *snap_stat_grid, const float *snap_stat_mlp,
+                  const float *rrs_grid, const float *rrs_mlp, const orc_train_sample *batch, size_t n,
+                  const orc_pixel_error *errors, size_t n_errors, float e_avg, int phase, float gamma_min,
+                  float gamma_avg, float gamma_rrs, float eps, float d_scale, float *g_mlp, float *g_grid,
+                  orc_rrs_parts *parts);
 /* Adam::step (optimizer.hpp:21-32) with the step counter already incremented to t */
 void orc_adam_step(float *theta, const float *grad, float *m, float *v, size_t n, int64_t t, float lr,
                    float beta1, float beta2, float eps);

@@ -98,6 +98,7 @@ def lib() -> C.CDLL:
             "orc_relative_l2": (None, [f, f, f, p, p]),
             "orc_stat_loss": (d, [p, p, p, p, C.c_size_t, f, f, p, p]),
             "orc_adam_step": (None, [p, p, p, p, C.c_size_t, C.c_int64, f, f, f, f]),
+            "orc_rrs_loss": (None, [i, p, p, p, p, p, p, C.c_size_t, p, C.c_size_t, f, i, f, f, f, f, f, p, p, p]),
             "orc_ema_update": (None, [p, p, C.c_size_t, f]),
         }
         for name, (res, args) in sig.items():
@@ -345,3 +346,35 @@ def gen_train_batch(n: int, seed: int = 11) -> np.ndarray:
     b["k_i"] = 1.0
     b["depth"] = 2
     return b
+
+
+class RrsParts(C.Structure):
+    _fields_ = [("min", C.c_double), ("avg", C.c_double), ("rrs", C.c_double), ("total", C.c_double),
+                ("skipped", C.c_uint32)]
+
+
+PIXEL_ERROR_DTYPE = np.dtype([("e", "<f4"), ("inv_denom", "<f4")])
+GAMMA_MIN, GAMMA_AVG, GAMMA_RRS, LOSS_EPS = 0.05, 0.01, 0.01, 0.01   # NeuralRrsConfig (networks.hpp:94-106)
+
+
+def rrs_loss(nets: "OracleNets", snap_stat_grid, snap_stat_mlp, batch, errors, e_avg: float, phase: int,
+             d_scale: float = 1.0, grads: bool = True):
+    """NeuralRrs::rrs_loss_impl -> (parts, g_mlp, g_grid)."""
+    batch = np.ascontiguousarray(batch, dtype=TRAIN_SAMPLE_DTYPE)
+    errors = np.ascontiguousarray(errors, dtype=PIXEL_ERROR_DTYPE)
+    gm = np.zeros_like(nets.rrs_mlp) if grads else None
+    gg = np.zeros_like(nets.rrs_grid) if (grads and nets.rrs_grid.size) else None
+    parts = RrsParts()
+    lib().orc_rrs_loss(nets.variant, C.byref(nets.spec), ptr(snap_stat_grid), ptr(snap_stat_mlp),
+                       ptr(nets.rrs_grid) if nets.rrs_grid.size else None, ptr(nets.rrs_mlp), batch.ctypes.data,
+                       batch.size, errors.ctypes.data, errors.size, e_avg, phase, GAMMA_MIN, GAMMA_AVG, GAMMA_RRS,
+                       LOSS_EPS, d_scale, ptr(gm), ptr(gg), C.byref(parts))
+    return parts, gm, gg
+
+
+def gen_pixel_errors(n_pixels: int, seed: int = 13) -> np.ndarray:
+    g = np.random.default_rng(seed)
+    e = np.zeros(n_pixels, PIXEL_ERROR_DTYPE)
+    e["e"] = g.random(n_pixels, dtype=np.float32) * np.float32(2.0)
+    e["inv_denom"] = np.float32(1.0) / (g.random(n_pixels, dtype=np.float32) + np.float32(0.01))
+    return e

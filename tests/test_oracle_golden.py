@@ -374,3 +374,46 @@ def test_oracle_adam_and_ema_match_formulas():
     sh = th0.copy()
     orc.ema_update(sh, theta, 0.99)
     np.testing.assert_allclose(sh, 0.99 * th0 + 0.01 * theta, rtol=1e-6)
+
+
+@pytest.mark.parametrize("variant", [orc.VARIANT_NRRS, orc.VARIANT_AID], ids=["nrrs", "aid"])
+@pytest.mark.parametrize("phase", [0, 1], ids=["warmup", "full"])
+def test_oracle_rrs_loss_gradient_matches_finite_differences(variant, phase):
+    """The oracle's RRSNet gradient (rrs_loss_impl, networks.cpp:418-460) against central
+    differences of its own total loss.  Warmup: relative L2 of q to 1.  Full phase: the
+    variance-transfer terms (grad_pixelvar_wrt_rr / _split) have no scalar objective
+    (networks.cpp:410-417), so the FD check runs without pixel-error records; the total is then
+    exactly gamma_rrs times the recorded-factor regression, which FD can check."""
+    nets = orc.OracleNets(variant, seed=5, randomize=True)
+    b = orc.gen_train_batch(10, seed=21)
+    b["q_real"] = np.array([0.5, 1.5, 0.0, 2.0, 0.9, 1.0, 3.0, 0.2, 1.2, 0.7], np.float32)
+    b["q_norm"] = b["q_real"] * np.float32(1.1)
+    b["k_i"] = np.float32(2.0)
+    errors = orc.gen_pixel_errors(1024)
+    if phase == 1:
+        errors = errors[:0]  # no pixel errors: the loss is exactly the regression term, FD-checkable
+    parts, gm, gg = orc.rrs_loss(nets, nets.stat_grid, nets.stat_mlp, b, errors, 0.3, phase)
+    assert np.isfinite(parts.total) and parts.total > 0
+
+    def fd(arr, k):
+        saved = arr[k]
+        h = np.float32(max(0.05 * abs(float(saved)), 1e-2))
+        arr[k] = saved + h
+        lp = orc.rrs_loss(nets, nets.stat_grid, nets.stat_mlp, b, errors, 0.3, phase, grads=False)[0].total
+        arr[k] = saved - h
+        lm = orc.rrs_loss(nets, nets.stat_grid, nets.stat_mlp, b, errors, 0.3, phase, grads=False)[0].total
+        arr[k] = saved
+        return (lp - lm) / (2.0 * float(h)) * (1.0 if phase == 0 else 1.0 / orc.GAMMA_RRS)
+
+    scale = 1.0 if phase == 0 else 1.0 / orc.GAMMA_RRS  # full phase: d(total)/dq = gamma_rrs * d(rrs)/dq
+    bad = checked = 0
+    for k in range(0, nets.rrs_mlp.size, 7):
+        ref = fd(nets.rrs_mlp, k)
+        checked += 1
+        bad += abs(gm[k] * scale - ref) > 3e-2 * max(abs(ref), 1e-3)
+    assert checked > 300 and bad <= checked // 8, (bad, checked)
+    if variant == orc.VARIANT_AID:
+        sel = np.flatnonzero(gg)[::97][:60]
+        badg = sum(abs(gg[k] * scale - fd(nets.rrs_grid, k)) > 3e-2 * max(abs(fd(nets.rrs_grid, k)), 1e-4)
+                   for k in sel)
+        assert badg <= max(2, sel.size // 8), (badg, sel.size)
