@@ -253,6 +253,21 @@ NRRS_API int nrrs_gpu_stat_loss_grad(nrrs_gpu_ctx *ctx, const nrrs_grid_spec *sp
                                      float eps, float d_scale, float *d_g_mlp, float *d_g_grid, double *h_loss,
                                      int32_t *h_finite);
 
+/* NeuralRrs::rrs_loss_impl (networks.cpp:418-460) for one batch: stats from the published
+ * StatNet snapshot (d_snap_*), the RRSNet (variant 0 NRRS / 1 AID; d_rrs_grid AID only) on
+ * its live parameters.  phase 0 = Warmup (relative L2 of q to 1), 1 = Full (variance-
+ * transfer gradients through d_errors = {e, inv_denom} per pixel, plus the recorded-factor
+ * regression; gamma weights as NeuralRrsConfig).  Gradients scaled by d_scale overwrite
+ * d_g_mlp / d_g_grid; h_parts = {min, avg, rrs, total} (networks.hpp:219-224); *h_skipped
+ * counts samples without a pixel error; *h_finite as in nrrs_gpu_stat_loss_grad.  Syncs. */
+NRRS_API int nrrs_gpu_rrs_loss_grad(nrrs_gpu_ctx *ctx, int32_t variant, const nrrs_grid_spec *spec,
+                                    const float *d_snap_stat_grid, const float *d_snap_stat_mlp,
+                                    const float *d_rrs_grid, const float *d_rrs_mlp,
+                                    const nrrs_train_sample *d_batch, uint64_t n, const float *d_errors,
+                                    uint64_t n_errors, float e_avg, int32_t phase, float gamma_min,
+                                    float gamma_avg, float gamma_rrs, float eps, float d_scale, float *d_g_mlp,
+                                    float *d_g_grid, double *h_parts, uint32_t *h_skipped, int32_t *h_finite);
+
 /* apply_step's update (networks.cpp:471-478): grad *= inv_scale, Adam::step with the step
  * counter already advanced to t (optimizer.hpp:21-32), then the EMA shadow (optimizer.hpp:54-61;
  * d_shadow may be NULL).  Asynchronous. */

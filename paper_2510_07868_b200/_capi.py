@@ -80,6 +80,10 @@ SIGNATURES = [
     ("nrrs_gpu_film_roll_acc", C.c_int, [_P, _P, _P, C.c_uint32]),
     ("nrrs_gpu_stat_loss_grad", C.c_int, [_P, C.POINTER(GridSpec), _P, _P, _P, C.c_uint64, C.c_float, C.c_float, _P,
                                           _P, C.POINTER(C.c_double), C.POINTER(C.c_int32)]),
+    ("nrrs_gpu_rrs_loss_grad", C.c_int, [_P, C.c_int32, C.POINTER(GridSpec), _P, _P, _P, _P, _P, C.c_uint64, _P,
+                                         C.c_uint64, C.c_float, C.c_int32, C.c_float, C.c_float, C.c_float,
+                                         C.c_float, C.c_float, _P, _P, C.POINTER(C.c_double),
+                                         C.POINTER(C.c_uint32), C.POINTER(C.c_int32)]),
     ("nrrs_gpu_adam_ema", C.c_int, [_P, _P, _P, _P, _P, _P, C.c_uint64, C.c_int64, C.c_float, C.c_float, C.c_float,
                                     C.c_float, C.c_float, C.c_float]),
     ("nrrs_gpu_set_weights", C.c_int, [_P, C.POINTER(NetWeights)]),

@@ -971,6 +971,91 @@ int nrrs_gpu_stat_loss_grad(nrrs_gpu_ctx *ctx, const nrrs_grid_spec *spec, const
     return NRRS_OK;
 }
 
+int nrrs_gpu_rrs_loss_grad(nrrs_gpu_ctx *ctx, int32_t variant, const nrrs_grid_spec *spec,
+                           const float *d_snap_stat_grid, const float *d_snap_stat_mlp, const float *d_rrs_grid,
+                           const float *d_rrs_mlp, const nrrs_train_sample *d_batch, uint64_t n,
+                           const float *d_errors, uint64_t n_errors, float e_avg, int32_t phase, float gamma_min,
+                           float gamma_avg, float gamma_rrs, float eps, float d_scale, float *d_g_mlp,
+                           float *d_g_grid, double *h_parts, uint32_t *h_skipped, int32_t *h_finite) {
+    if (!ctx || !spec || !d_snap_stat_grid || !d_snap_stat_mlp || !d_rrs_mlp || !d_g_mlp || !h_parts ||
+        !h_skipped || !h_finite || (n && !d_batch) || (variant != 0 && variant != 1) || (phase != 0 && phase != 1) ||
+        (variant == 1 && (!d_rrs_grid || !d_g_grid)) || (n_errors && !d_errors))
+        return NRRS_EINVAL;
+    if (spec->features != 2 || spec->levels < 1 || spec->levels * 2 + 16 > 32 || spec->log2_table_size < 1 ||
+        spec->log2_table_size > 30)
+        return fail(ctx, NRRS_EINVAL, "rrs_loss_grad: unsupported grid spec");
+    CK(ctx, cudaSetDevice(ctx->device));
+    const int in = variant == 0 ? 11 : spec->levels * 2 + 16, P = train_rrs_param_count(in);
+    const uint64_t T = 1ull << spec->log2_table_size, ngrid = variant == 1 ? (uint64_t)spec->levels * T * 2 : 0;
+    if (ngrid)
+        CK(ctx, cudaMemsetAsync(d_g_grid, 0, ngrid * sizeof(float), ctx->stream));
+    for (int j = 0; j < 4; ++j)
+        h_parts[j] = 0.0;
+    *h_skipped = 0;
+    if (n == 0) {
+        CK(ctx, cudaMemsetAsync(d_g_mlp, 0, (size_t)P * sizeof(float), ctx->stream));
+        CK(ctx, cudaStreamSynchronize(ctx->stream));
+        *h_finite = 1;
+        return NRRS_OK;
+    }
+    const uint64_t blocks = (n + 255) / 256;
+    const uint32_t dw = train_dw_ctas(n);
+    CK(ctx, grow(ctx->d_tws, ctx->cap_tws, train_ws_floats(n)));
+    CK(ctx, grow(ctx->d_tloss, ctx->cap_tloss, 3 * blocks + 4));
+    CK(ctx, grow(ctx->d_tpart, ctx->cap_tpart, (uint64_t)dw * P));
+    RrsStepParams p{};
+    p.batch = d_batch;
+    p.n = n;
+    p.variant = variant;
+    p.in = in;
+    p.grid.levels = spec->levels;
+    p.grid.base_resolution = spec->base_resolution;
+    p.grid.table_size = (uint32_t)T;
+    p.grid.dense_mask = 0;
+    for (int l = 0; l < spec->levels; ++l) {
+        const uint64_t res = (uint64_t)spec->base_resolution << l;
+        if ((res + 1) * (res + 1) * (res + 1) <= T)
+            p.grid.dense_mask |= 1u << l;
+    }
+    p.snap_grid = d_snap_stat_grid;
+    p.snap_mlp = d_snap_stat_mlp;
+    p.rrs_grid = d_rrs_grid;
+    p.rrs_mlp = d_rrs_mlp;
+    p.errors = d_errors;
+    p.n_errors = n_errors;
+    p.e_avg = e_avg;
+    p.phase = phase;
+    p.gamma_min = gamma_min;
+    p.gamma_avg = gamma_avg;
+    p.gamma_rrs = gamma_rrs;
+    p.eps = eps;
+    p.d_scale = d_scale;
+    p.inv_n = 1.0f / (float)n;
+    p.ws = ctx->d_tws;
+    p.g_grid = variant == 1 ? d_g_grid : nullptr;
+    p.parts = ctx->d_tloss + 4;
+    uint32_t *flags = ctx->d_misc + 11;  // [11] non-finite, [12] skipped
+    p.skipped = ctx->d_misc + 12;
+    CK(ctx, cudaMemsetAsync(flags, 0, 2 * sizeof(uint32_t), ctx->stream));
+    CK(ctx, launch_rrs_train(p, ctx->d_tpart, dw, d_g_mlp, ctx->d_tloss, flags, ngrid, ctx->stream));
+    ctx->launches += 3;
+    double sums[3];
+    uint32_t hf[2];
+    CK(ctx, cudaMemcpyAsync(sums, ctx->d_tloss, sizeof sums, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(ctx, cudaMemcpyAsync(hf, flags, sizeof hf, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(ctx, cudaStreamSynchronize(ctx->stream));
+    const double inv_n = (double)(1.0f / (float)n);
+    h_parts[0] = sums[0] * inv_n;  // parts->min *= inv_n (networks.cpp:448-450)
+    h_parts[1] = sums[1] * inv_n;
+    h_parts[2] = sums[2] * inv_n;
+    h_parts[3] = phase == 0 ? h_parts[2]
+                            : (double)gamma_min * h_parts[0] + (double)gamma_avg * h_parts[1] +
+                                  (double)gamma_rrs * h_parts[2];
+    *h_skipped = hf[1];
+    *h_finite = (hf[0] == 0 && std::isfinite(h_parts[3])) ? 1 : 0;
+    return NRRS_OK;
+}
+
 int nrrs_gpu_adam_ema(nrrs_gpu_ctx *ctx, float *d_theta, const float *d_grad, float *d_m, float *d_v,
                       float *d_shadow, uint64_t n, int64_t t, float lr, float beta1, float beta2, float eps,
                       float inv_scale, float ema_decay) {

@@ -207,11 +207,32 @@ struct TrainStepParams {
     float *g_grid;            // zeroed by the caller
     double *loss_parts;       // [blocks]
 };
+struct RrsStepParams {
+    const nrrs_train_sample *batch;
+    uint64_t n;
+    int32_t variant;                     // 0 NRRS, 1 AID
+    int32_t in;                          // RRSNet input width (11 or levels * 2 + 16)
+    TrainGrid grid;
+    const float *snap_grid, *snap_mlp;   // published StatNet snapshot
+    const float *rrs_grid, *rrs_mlp;     // live RRSNet (rrs_grid: AID only)
+    const float *errors;                 // PixelError {e, inv_denom} per pixel
+    uint64_t n_errors;
+    float e_avg;
+    int32_t phase;                       // 0 Warmup, 1 Full
+    float gamma_min, gamma_avg, gamma_rrs, eps, d_scale, inv_n;
+    float *ws;
+    float *g_grid;                       // zeroed by the caller (AID)
+    double *parts;                       // [blocks][3] min, avg, rrs
+    uint32_t *skipped;
+};
 struct AdamParams {
     float lr, beta1, beta2, eps, c1, c2, inv_scale, decay;
 };
 size_t train_ws_floats(uint64_t n);
 int train_param_count(int in);
+int train_rrs_param_count(int in);
+cudaError_t launch_rrs_train(const RrsStepParams &p, float *partials, uint32_t dw_ctas, float *g_mlp,
+                             double *parts_out, uint32_t *nonfinite, uint64_t ngrid, cudaStream_t stream);
 uint32_t train_dw_ctas(uint64_t n);
 cudaError_t launch_stat_train(const TrainStepParams &p, float *partials, uint32_t dw_ctas, float *g_mlp,
                               double *loss_out, uint32_t *nonfinite, uint64_t ngrid, cudaStream_t stream);

@@ -24,10 +24,11 @@ constexpr int kTOut = 6;                      // StatNet outputs
 constexpr int kWs = 4 * kTH + 3 * kTH + 8;    // per-sample workspace: in0, post0..2, delta0..2, delta3
 constexpr int kDwChunk = 32;                  // samples staged per smem chunk in stat_dw_kernel
 
-__host__ __device__ inline int stat_param_count(int in) {
-    return (kTH * in + kTH) + 2 * (kTH * kTH + kTH) + (kTOut * kTH + kTOut);
+__host__ __device__ inline int mlp_params(int in, int out) {
+    return (kTH * in + kTH) + 2 * (kTH * kTH + kTH) + (out * kTH + out);
 }
-__host__ __device__ inline int stat_layer_offset(int in, int l) {
+__host__ __device__ inline int stat_param_count(int in) { return mlp_params(in, kTOut); }
+__host__ __device__ inline int stat_layer_offset(int in, int l) {  // hidden layers and head start (any out)
     return l == 0 ? 0 : (kTH * in + kTH) + (l - 1) * (kTH * kTH + kTH);
 }
 
@@ -208,10 +209,11 @@ __global__ void __launch_bounds__(256) stat_fwd_bwd_kernel(TrainStepParams p) {
 }
 
 // weight / bias gradients from the workspace: CTA b sums samples [b*per, (b+1)*per)
-__global__ void __launch_bounds__(256) stat_dw_kernel(const float *ws, uint64_t n, int in, uint64_t per,
-                                                      float *partials) {
+template <int OUT>
+__global__ void __launch_bounds__(256) mlp_dw_kernel(const float *ws, uint64_t n, int in, uint64_t per,
+                                                     float *partials) {
     __shared__ float st[kDwChunk][kWs];
-    const int tid = threadIdx.x, P = stat_param_count(in);
+    const int tid = threadIdx.x, P = mlp_params(in, OUT);
     constexpr int kMaxOwn = 14;  // ceil(3366 / 256)
     float acc[kMaxOwn];
     int doff[kMaxOwn], ioff[kMaxOwn];
@@ -226,7 +228,7 @@ __global__ void __launch_bounds__(256) stat_dw_kernel(const float *ws, uint64_t 
         int l = 3;
         while (l > 0 && q < stat_layer_offset(in, l))
             --l;
-        const int li = l == 0 ? in : kTH, lo = l == 3 ? kTOut : kTH;
+        const int li = l == 0 ? in : kTH, lo = l == 3 ? OUT : kTH;
         const int e = q - stat_layer_offset(in, l);
         if (e < lo * li) {  // column-major W: e = c * lo + r
             doff[k] = 4 * kTH + kTH * l + e % lo;
@@ -302,9 +304,273 @@ __global__ void adam_ema_kernel(float *theta, const float *grad, float *m, float
     }
 }
 
+// ---- RRSNet step: NeuralRrs::rrs_loss_impl (networks.cpp:418-460) ----
+
+// plain forward of the published StatNet snapshot (snapshot_stats_batch, networks.cpp:219-224)
+__device__ __forceinline__ void snapshot_stats(const RrsStepParams &p, const float *w_stat,
+                                               const nrrs_train_sample &t, float st[6]) {
+    const int gd = 2 * p.grid.levels, in = gd + 16;
+    float a[kTH];
+    for (int l = 0; l < p.grid.levels; ++l) {
+        uint32_t base[8];
+        float w[8];
+        grid_corners(p.grid, l, t.position, base, w);
+        float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            a0 += w[k] * __ldg(p.snap_grid + base[k]);
+            a1 += w[k] * __ldg(p.snap_grid + base[k] + 1);
+        }
+        a[2 * l] = a0;
+        a[2 * l + 1] = a1;
+    }
+    one_blob_exact(t.omega_o[0], 4, a + gd);
+    one_blob_exact(t.omega_o[1], 4, a + gd + 4);
+    one_blob_exact(1.0f - expf(-t.roughness), 8, a + gd + 8);
+    for (int l = 0; l < 3; ++l) {
+        const int li = l == 0 ? in : kTH;
+        const float *W = w_stat + stat_layer_offset(in, l), *b = W + kTH * li;
+        float z[kTH];
+        for (int r = 0; r < kTH; ++r) {
+            float acc = 0.0f;
+            for (int c = 0; c < li; ++c)
+                acc += W[c * kTH + r] * a[c];
+            z[r] = acc + b[r];
+        }
+        for (int r = 0; r < kTH; ++r) {
+            const float zs = z[r] * 0.01f;
+            a[r] = z[r] < zs ? zs : z[r];
+        }
+    }
+    const float *W = w_stat + stat_layer_offset(in, 3), *b = W + kTOut * kTH;
+    for (int r = 0; r < kTOut; ++r) {
+        float acc = 0.0f;
+        for (int c = 0; c < kTH; ++c)
+            acc += W[c * kTOut + r] * a[c];
+        st[r] = acc + b[r];
+    }
+}
+
+__device__ __forceinline__ float box_cox_exact(float x) {  // encodings.hpp:54-62, lambda 0.5
+    if (x < 0.0f)
+        x = 0.0f;
+    return (powf(x, 0.5f) - 1.0f) / 0.5f;
+}
+
+__global__ void __launch_bounds__(256) rrs_fwd_bwd_kernel(RrsStepParams p) {
+    extern __shared__ float w_s[];
+    const int tid = threadIdx.x;
+    const int gd = 2 * p.grid.levels, Ps = stat_param_count(gd + 16), Pr = mlp_params(p.in, 1);
+    float *w_stat = w_s, *w_rrs = w_s + Ps;
+    for (int i = tid; i < Ps; i += blockDim.x)
+        w_stat[i] = p.snap_mlp[i];
+    for (int i = tid; i < Pr; i += blockDim.x)
+        w_rrs[i] = p.rrs_mlp[i];
+    __syncthreads();
+    const float slope = 0.01f;
+    const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + tid;
+    double pmin = 0.0, pavg = 0.0, prrs = 0.0;
+    uint32_t skipped = 0;
+    if (s < p.n) {
+        const nrrs_train_sample &t = p.batch[s];
+        float *ws = p.ws + s * kWs;
+        float st[6];
+        snapshot_stats(p, w_stat, t, st);
+        // encode_rrs_inputs (networks.cpp:226-250)
+        float a[kTH];
+        const float imean = (t.i_pixel[0] + (t.i_pixel[1] + t.i_pixel[2])) / 3.0f;
+        if (p.variant == 0) {  // build_nrrs_input (networks.cpp:137-147)
+            for (int c = 0; c < 3; ++c) {
+                a[c] = box_cox_exact(st[c]);
+                a[3 + c] = box_cox_exact(st[3 + c]);
+                a[6 + c] = box_cox_exact(t.t_x[c]);
+            }
+            a[9] = box_cox_exact(imean);
+            a[10] = 1.0f - expf(-t.roughness);
+        } else {                // AID: own grid + build_aid_tail (networks.cpp:149-157)
+            for (int l = 0; l < p.grid.levels; ++l) {
+                uint32_t base[8];
+                float w[8];
+                grid_corners(p.grid, l, t.position, base, w);
+                float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    a0 += w[k] * __ldg(p.rrs_grid + base[k]);
+                    a1 += w[k] * __ldg(p.rrs_grid + base[k] + 1);
+                }
+                a[2 * l] = a0;
+                a[2 * l + 1] = a1;
+            }
+            one_blob_exact(t.omega_o[0], 4, a + gd);
+            one_blob_exact(t.omega_o[1], 4, a + gd + 4);
+            for (int c = 0; c < 3; ++c)
+                a[gd + 8 + c] = box_cox_exact(t.t_x[c]);
+            a[gd + 11] = box_cox_exact(imean);
+            one_blob_exact(1.0f - expf(-t.roughness), 4, a + gd + 12);
+        }
+        for (int i = p.in; i < kTH; ++i)
+            a[i] = 0.0f;
+        for (int i = 0; i < kTH; ++i)
+            ws[i] = a[i];
+        for (int l = 0; l < 3; ++l) {
+            const int li = l == 0 ? p.in : kTH;
+            const float *W = w_rrs + stat_layer_offset(p.in, l), *b = W + kTH * li;
+            float z[kTH];
+            for (int r = 0; r < kTH; ++r) {
+                float acc = 0.0f;
+                for (int c = 0; c < li; ++c)
+                    acc += W[c * kTH + r] * a[c];
+                z[r] = acc + b[r];
+            }
+            for (int r = 0; r < kTH; ++r) {
+                const float zs = z[r] * slope;
+                a[r] = z[r] < zs ? zs : z[r];
+                ws[kTH * (l + 1) + r] = a[r];
+            }
+        }
+        const float *Wh = w_rrs + stat_layer_offset(p.in, 3);
+        float zacc = 0.0f;
+        for (int c = 0; c < kTH; ++c)
+            zacc += Wh[c] * a[c];
+        const float z = zacc + Wh[kTH];
+        const float q = z < 0.0f ? log1pf(expf(z)) : 0.5f * z + 0.6931471805599453f;  // softplus_mod
+        float d_q = 0.0f;
+        if (p.phase == 0) {
+            const float d = q - 1.0f, inv = 1.0f / (1.0f + p.eps);
+            prrs += (double)(d * d * inv);
+            d_q = 2.0f * d * inv * p.inv_n;
+        } else {
+            const uint32_t px = t.pixel;
+            const float inv_k = t.k_i > 0.0f ? 1.0f / t.k_i : 1.0f;
+            if (px < p.n_errors) {
+                const float pe_e = p.errors[2 * px], pe_inv = p.errors[2 * px + 1];
+                float gvar = 0.0f;
+                const float wl = luminance(t.t_x[0], t.t_x[1], t.t_x[2]);
+                if (t.q_real < 1.0f) {
+                    if (t.q_real > 0.0f) {
+                        const float hl = luminance(t.lo_sample[0], t.lo_sample[1], t.lo_sample[2]);
+                        gvar = -(wl * wl) * (hl * hl) / (t.q_real * t.q_real);
+                    }
+                } else {
+                    float var[3];
+                    for (int c = 0; c < 3; ++c) {
+                        const float v = st[3 + c] - st[c] * st[c];
+                        var[c] = v < 0.0f ? 0.0f : v;
+                    }
+                    gvar = -(wl * wl) * luminance(var[0], var[1], var[2]) / (t.q_real * t.q_real);
+                }
+                const float de_dq = pe_inv * gvar * inv_k;
+                pmin += (double)(pe_e * inv_k);
+                const float dev = pe_e - p.e_avg;
+                pavg += (double)(dev * dev * inv_k);
+                d_q += (p.gamma_min * de_dq + p.gamma_avg * 2.0f * dev * de_dq) * p.inv_n;
+            } else {
+                skipped = 1;
+            }
+            const float gap = q - t.q_norm;
+            prrs += (double)(gap * gap);
+            d_q += p.gamma_rrs * 2.0f * gap * p.inv_n;
+        }
+        const float sg = z < 0.0f ? expf(z) / (1.0f + expf(z)) : 0.5f;  // softplus_mod_grad
+        const float dy = d_q * sg * p.d_scale;
+        // Mlp::backward (mlp.cpp:74-111)
+        float *dws = ws + 4 * kTH;
+        dws[3 * kTH] = dy;
+        float delta[kTH];
+        for (int c = 0; c < kTH; ++c) {
+            const float acc = Wh[c] * dy;
+            delta[c] = a[c] <= 0.0f ? acc * slope : acc;
+        }
+        for (int l = 2; l >= 0; --l) {
+            for (int r = 0; r < kTH; ++r)
+                dws[kTH * l + r] = delta[r];
+            const int li = l == 0 ? p.in : kTH;
+            const float *W = w_rrs + stat_layer_offset(p.in, l);
+            float da[kTH];
+            for (int c = 0; c < li; ++c) {
+                float acc = 0.0f;
+                for (int r = 0; r < kTH; ++r)
+                    acc += W[c * kTH + r] * delta[r];
+                da[c] = acc;
+            }
+            if (l > 0) {
+                const float *post = ws + kTH * l;
+                for (int c = 0; c < kTH; ++c)
+                    delta[c] = post[c] <= 0.0f ? da[c] * slope : da[c];
+            } else if (p.variant == 1 && p.g_grid) {
+                for (int lv = 0; lv < p.grid.levels; ++lv) {
+                    uint32_t base[8];
+                    float w[8];
+                    grid_corners(p.grid, lv, t.position, base, w);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        atomicAdd(p.g_grid + base[k], w[k] * da[2 * lv]);
+                        atomicAdd(p.g_grid + base[k] + 1, w[k] * da[2 * lv + 1]);
+                    }
+                }
+            }
+        }
+    }
+    __shared__ double red[3][8];
+    __shared__ uint32_t reds[8];
+    double v[3] = {pmin, pavg, prrs};
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+            v[j] += __shfl_xor_sync(0xffffffffu, v[j], o);
+    const uint32_t sk = __reduce_add_sync(0xffffffffu, skipped);
+    if ((tid & 31) == 0) {
+        for (int j = 0; j < 3; ++j)
+            red[j][tid >> 5] = v[j];
+        reds[tid >> 5] = sk;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double b[3] = {0.0, 0.0, 0.0};
+        uint32_t bs = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+            for (int j = 0; j < 3; ++j)
+                b[j] += red[j][i];
+            bs += reds[i];
+        }
+        for (int j = 0; j < 3; ++j)
+            p.parts[3 * blockIdx.x + j] = b[j];
+        if (bs)
+            atomicAdd(p.skipped, bs);
+    }
+}
+
+// g_mlp = sum of CTA partials (fixed order), loss parts summed over blocks, finite flags
+__global__ void rrs_reduce_kernel(const float *partials, int nparts, int P, float *g_mlp, const double *parts,
+                                  int nblocks, double *parts_out, const float *g_grid, uint64_t ngrid,
+                                  uint32_t *nonfinite) {
+    const int tid = threadIdx.x + blockIdx.x * blockDim.x;
+    for (int q = tid; q < P; q += gridDim.x * blockDim.x) {
+        float s = 0.0f;
+        for (int b = 0; b < nparts; ++b)
+            s += partials[(uint64_t)b * P + q];
+        g_mlp[q] = s;
+        if (!isfinite(s))
+            atomicOr(nonfinite, 1u);
+    }
+    for (uint64_t i = tid; i < ngrid; i += (uint64_t)gridDim.x * blockDim.x)
+        if (!isfinite(g_grid[i]))
+            atomicOr(nonfinite, 1u);
+    if (tid == 0) {
+        double t[3] = {0.0, 0.0, 0.0};
+        for (int b = 0; b < nblocks; ++b)
+            for (int j = 0; j < 3; ++j)
+                t[j] += parts[3 * b + j];
+        for (int j = 0; j < 3; ++j)
+            parts_out[j] = t[j];
+    }
+}
+
 // ---- launchers ----
 size_t train_ws_floats(uint64_t n) { return (size_t)n * kWs; }
 int train_param_count(int in) { return stat_param_count(in); }
+int train_rrs_param_count(int in) { return mlp_params(in, 1); }
 uint32_t train_dw_ctas(uint64_t n) {
     const uint64_t c = (n + 511) / 512;
     return (uint32_t)(c < 1 ? 1 : (c > 256 ? 256 : c));
@@ -319,9 +585,25 @@ cudaError_t launch_stat_train(const TrainStepParams &p, float *partials, uint32_
         return e;
     stat_fwd_bwd_kernel<<<blocks, 256, smem, stream>>>(p);
     const uint64_t per = (p.n + dw_ctas - 1) / dw_ctas;
-    stat_dw_kernel<<<dw_ctas, 256, 0, stream>>>(p.ws, p.n, p.in, per, partials);
+    mlp_dw_kernel<kTOut><<<dw_ctas, 256, 0, stream>>>(p.ws, p.n, p.in, per, partials);
     stat_reduce_kernel<<<64, 256, 0, stream>>>(partials, (int)dw_ctas, stat_param_count(p.in), g_mlp, p.loss_parts,
                                                (int)blocks, p.inv_n, loss_out, p.g_grid, ngrid, nonfinite);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rrs_train(const RrsStepParams &p, float *partials, uint32_t dw_ctas, float *g_mlp,
+                             double *parts_out, uint32_t *nonfinite, uint64_t ngrid, cudaStream_t stream) {
+    const uint32_t blocks = (uint32_t)((p.n + 255) / 256);
+    const int gd = 2 * p.grid.levels;
+    const size_t smem = (size_t)(stat_param_count(gd + 16) + mlp_params(p.in, 1)) * sizeof(float);
+    cudaError_t e = cudaFuncSetAttribute(rrs_fwd_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess)
+        return e;
+    rrs_fwd_bwd_kernel<<<blocks, 256, smem, stream>>>(p);
+    const uint64_t per = (p.n + dw_ctas - 1) / dw_ctas;
+    mlp_dw_kernel<1><<<dw_ctas, 256, 0, stream>>>(p.ws, p.n, p.in, per, partials);
+    rrs_reduce_kernel<<<64, 256, 0, stream>>>(partials, (int)dw_ctas, mlp_params(p.in, 1), g_mlp, p.parts,
+                                              (int)blocks, parts_out, p.g_grid, ngrid, nonfinite);
     return cudaGetLastError();
 }
 

@@ -91,3 +91,60 @@ def test_non_finite_batch_is_skipped_and_halves_the_loss_scale(onets):
     assert not applied and tr.scale == 0.5 and tr.skipped_steps == 1
     assert torch.equal(tr.mlp, before)
     tr.close()
+
+
+def _rrs_batch(n, seed=31, n_pixels=2048):
+    b = orc.gen_train_batch(n, seed)
+    g = np.random.default_rng(seed)
+    b["q_real"] = (g.random(n, dtype=np.float32) * np.float32(3.0)).astype(np.float32)
+    b["q_real"][::11] = 0.0
+    b["q_norm"] = b["q_real"] * np.float32(0.9)
+    b["k_i"] = (1 + g.integers(0, 4, n)).astype(np.float32)
+    b["pixel"] = g.integers(0, n_pixels + 64, n).astype(np.uint32)  # some pixels without an error record
+    b["i_pixel"] = np.float32(0.3) + g.random((n, 3), dtype=np.float32)
+    return b, torch.from_numpy(b.view(np.uint8).reshape(n, 80).copy()).cuda()
+
+
+@pytest.mark.parametrize("variant", [orc.VARIANT_NRRS, orc.VARIANT_AID], ids=["nrrs", "aid"])
+@pytest.mark.parametrize("phase", [0, 1], ids=["warmup", "full"])
+def test_rrs_loss_and_gradients_match_oracle(variant, phase):
+    from paper_2510_07868_b200.training import RrsNetTrainer
+    nets = orc.OracleNets(variant, seed=5, randomize=True)
+    hb, db = _rrs_batch(3001)
+    errors = orc.gen_pixel_errors(2048)
+    parts, gm, gg = orc.rrs_loss(nets, nets.stat_grid, nets.stat_mlp, hb, errors, 0.4, phase, d_scale=0.5)
+    tr = RrsNetTrainer(mirror_nets(nets))
+    snap_g = torch.from_numpy(nets.stat_grid).cuda()
+    snap_m = torch.from_numpy(nets.stat_mlp).cuda()
+    de = torch.from_numpy(errors.view(np.float32).copy()).cuda()
+    gp, sk, fin = tr.loss_and_grad(db, snap_g, snap_m, de, 0.4, phase, d_scale=0.5)
+    assert fin and sk == parts.skipped
+    for k in ("min", "avg", "rrs", "total"):
+        ref = getattr(parts, k)
+        assert abs(gp[k] - ref) <= 1e-5 * max(abs(ref), 1e-12), (k, gp[k], ref)
+    assert _rel(tr.g_mlp.cpu().numpy(), gm) < 2e-4
+    if variant == orc.VARIANT_AID:
+        assert _rel(tr.g_grid.cpu().numpy(), gg) < 2e-4
+    tr.close()
+
+
+def test_train_frame_warmup_drives_q_to_one_and_publishes():
+    """NeuralRrs::train_frame in the warmup phase (q regressed to 1) + publish: the RRSNet loss
+    falls and the published snapshot loads into the inference stage."""
+    from paper_2510_07868_b200 import NeuralRrs, NeuralRrsConfig, RrsStage, RrsVariant, Strategy, StrategyKind
+    from paper_2510_07868_b200.training import WARMUP, NeuralRrsTrainer
+    nets = NeuralRrs(NeuralRrsConfig(variant=RrsVariant.Aid, seed=1)).randomize_for_benchmark()
+    tr = NeuralRrsTrainer(nets, batch=8192)
+    _, db = _rrs_batch(16384, seed=9)
+    first = tr.train_frame(db, None, 0.0, WARMUP)
+    for _ in range(20):
+        last = tr.train_frame(db, None, 0.0, WARMUP)
+    assert last["loss_rrs"] < first["loss_rrs"] and last["loss_stat"] < first["loss_stat"]
+    assert tr.stat.steps == 42 and tr.rrs.steps == 42
+    published = tr.publish()
+    st = RrsStage(4096, published)
+    v = orc.gen_vertices(4096)
+    out, res = st.run({k: torch.from_numpy(np.ascontiguousarray(a.view(np.int64) if a.dtype == np.uint64 else a)).cuda()
+                       for k, a in v.items() if k != "pixel"}, 2, Strategy(StrategyKind.AidNrrs))
+    assert np.isfinite(res.f_norm) and res.total > 0
+    tr.close()
