@@ -557,7 +557,7 @@ def main():
     if world == 1 and not args.no_extra:
         sys.path.insert(0, os.path.join(ROOT, "tests"))
         import oracle as orc_gen  # synthetic TrainSamples (host-side input only)
-        from paper_2510_07868_b200.training import StatNetTrainer
+        from paper_2510_07868_b200.training import FULL, NeuralRrsTrainer, StatNetTrainer
         nb = 1 << 16
         hb = orc_gen.gen_train_batch(nb, seed=5)
         db = torch.from_numpy(hb.view(np.uint8).reshape(nb, 80).copy()).to(dev)
@@ -581,10 +581,29 @@ def main():
             orc_gen.adam_step(arr, g, np.zeros_like(arr), np.zeros_like(arr), 1, 0.005)
             orc_gen.ema_update(arr.copy(), arr)
         cpu_ms = 1e3 * (time.perf_counter() - t0)
+        # a whole train_frame chunk: StatNet step + AID RRSNet step (full phase, pixel errors)
+        ntr = NeuralRrsTrainer(nets, device=local, batch=nb)
+        hb2 = hb.copy()
+        hb2["q_real"] = np.float32(1.5)
+        hb2["q_norm"] = np.float32(1.2)
+        db2 = torch.from_numpy(hb2.view(np.uint8).reshape(nb, 80).copy()).to(dev)
+        errs = torch.rand((1024, 2), dtype=torch.float32, device=dev)
+        for _ in range(3):
+            ntr.train_frame(db2, errs, 0.5, FULL)
+        torch.cuda.synchronize()
+        tf = []
+        for _ in range(10):
+            t0 = time.perf_counter()
+            ntr.train_frame(db2, errs, 0.5, FULL)
+            torch.cuda.synchronize()
+            tf.append(time.perf_counter() - t0)
+        ntr.close()
         train = {"batch": nb, "ms_per_step": 1e3 * statistics.mean(ts), "samples_per_s": nb / statistics.mean(ts),
+                 "train_frame_chunk_ms": 1e3 * statistics.mean(tf),
                  "cpu_port_ms_per_step": cpu_ms,
                  "params": int(tr.grid.numel() + tr.mlp.numel()), "loss_first": losses[0], "loss_last": losses[-1],
-                 "note": "step_statnet: loss + gradients + Adam + EMA, wall time incl. the finite-check sync"}
+                 "note": "ms_per_step: step_statnet (loss + gradients + Adam + EMA); train_frame_chunk_ms: "
+                         "step_statnet + step_rrsnet (AID, full phase); wall time incl. the finite-check syncs"}
         tr.close()
 
     peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}
