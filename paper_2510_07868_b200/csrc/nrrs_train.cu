@@ -1,14 +1,18 @@
-// nrrs_train.cu -- one StatNet training step on the GPU:
-// NeuralRrs::stat_loss_impl (networks.cpp:349-391) with Mlp::backward
-// (mlp.cpp:74-111) and HashGrid::encode_backward (hashgrid.cpp:84-103), then
-// Adam (optimizer.hpp:21-32) and the EMA shadow (optimizer.hpp:54-61).
+// nrrs_train.cu -- online training steps on the GPU:
+// NeuralRrs::stat_loss_impl (networks.cpp:349-391) and rrs_loss_impl
+// (:418-460) with Mlp::backward (mlp.cpp:74-111) and HashGrid::encode_backward
+// (hashgrid.cpp:84-103), then Adam (optimizer.hpp:21-32) and the EMA shadow
+// (optimizer.hpp:54-61).
 //
 //   stat_fwd_bwd_kernel  one thread per TrainSample: grid encode + stat tail,
 //                        MLP forward (fp32), relative-L2 loss and d_y, the
 //                        backward through the MLP, and the grid gradient by
 //                        scatter-add; activations and deltas go to a per-sample
 //                        workspace record for the weight gradients
-//   stat_dw_kernel       dW = sum_s delta_s in_s^T, db = sum_s delta_s: per-CTA
+//   rrs_fwd_bwd_kernel   the same for the RRSNet: snapshot StatNet stats, NRRS
+//                        (11 inputs) or AID (own grid + tail) input, softplus,
+//                        warmup / full-phase loss, backward, AID grid scatter
+//   mlp_dw_kernel<OUT>   dW = sum_s delta_s in_s^T, db = sum_s delta_s: per-CTA
 //                        partials over sample chunks staged in smem, then a
 //                        fixed-order reduction over CTAs
 //   adam_ema_kernel      grad * inv_scale -> Adam with bias correction -> EMA
