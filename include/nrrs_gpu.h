@@ -162,6 +162,19 @@ typedef struct {
     const double *s;        /* [3n] suffix contribution after the reverse pass */
 } nrrs_vertex_rec_soa;
 
+/* Material (bsdf.hpp:10-20) and Camera (scene.hpp:12-20) of a scene. */
+typedef struct {
+    int32_t kind;        /* 0 diffuse, 1 conductor */
+    float albedo[3];
+    float roughness;     /* GGX alpha, conductor only */
+    float emission[3];
+} nrrs_material;
+typedef struct {
+    float position[3], look_at[3], up[3];
+    float vfov_deg;
+} nrrs_camera;
+
+typedef struct nrrs_scene nrrs_scene;
 typedef struct nrrs_gpu_ctx nrrs_gpu_ctx;
 
 /* ---- context ------------------------------------------------------------ */
@@ -274,6 +287,41 @@ NRRS_API int nrrs_gpu_rrs_loss_grad(nrrs_gpu_ctx *ctx, int32_t variant, const nr
 NRRS_API int nrrs_gpu_adam_ema(nrrs_gpu_ctx *ctx, float *d_theta, const float *d_grad, float *d_m, float *d_v,
                                float *d_shadow, uint64_t n, int64_t t, float lr, float beta1, float beta2,
                                float eps, float inv_scale, float ema_decay);
+
+/* ---- render front-end (first part) ---- */
+
+/* TriMesh + materials + camera on the device; the BVH is built on the host exactly like
+ * Bvh::build (geometry.cpp:88-137: median split on the longest axis, nth_element, leaves of
+ * <= 4) and Scene::finalize's normalization (scene.cpp:23-37).  Host arrays. */
+NRRS_API int nrrs_gpu_scene_create(nrrs_gpu_ctx *ctx, const float *h_positions, uint32_t n_vertices,
+                                   const uint32_t *h_indices, uint32_t n_triangles, const uint32_t *h_material_ids,
+                                   const nrrs_material *h_materials, uint32_t n_materials,
+                                   const nrrs_camera *camera, nrrs_scene **out);
+NRRS_API int nrrs_gpu_scene_destroy(nrrs_scene *scene);
+NRRS_API uint32_t nrrs_gpu_scene_node_count(const nrrs_scene *scene);
+
+/* Depth-1 camera rays of a width x height film (wavefront.cpp:253-268): pixel p's key is
+ * root_path_key(p, frame), its jitter path_stream(seed, key, 1, CameraJitter).  d_o / d_d [3n],
+ * d_keys [n].  Asynchronous. */
+NRRS_API int nrrs_gpu_camera_rays(nrrs_gpu_ctx *ctx, const nrrs_scene *scene, uint32_t width, uint32_t height,
+                                  uint64_t seed, uint32_t frame, float *d_o, float *d_d, uint64_t *d_keys);
+
+/* Closest hits (Bvh::intersect, geometry.cpp:139-171); d_t_max may be NULL (inf).  Misses
+ * return t = inf, tri = 0xFFFFFFFF.  d_u / d_v may be NULL.  Asynchronous. */
+NRRS_API int nrrs_gpu_intersect(nrrs_gpu_ctx *ctx, const nrrs_scene *scene, const float *d_o, const float *d_d,
+                                const float *d_t_max, uint64_t n, float *d_t, uint32_t *d_tri, float *d_u,
+                                float *d_v);
+/* Synchronizes the context stream and reports (then clears) a degenerate ray direction seen by
+ * nrrs_gpu_intersect since the last check: NRRS_EINVAL with the reference's message. */
+NRRS_API int nrrs_gpu_render_check(nrrs_gpu_ctx *ctx);
+
+/* dispatch (wavefront.cpp:125-138: d_class 0 miss, 1 light, 2 surface) and the surface
+ * vertex fields the RRS stage reads (wavefront.cpp:330-345): p01, wo01, roughness, material
+ * (d_material may be NULL).  Asynchronous. */
+NRRS_API int nrrs_gpu_surface_records(nrrs_gpu_ctx *ctx, const nrrs_scene *scene, const float *d_o,
+                                      const float *d_d, const float *d_t, const uint32_t *d_tri, uint64_t n,
+                                      uint8_t *d_class, float *d_p01, float *d_wo01, float *d_roughness,
+                                      uint32_t *d_material);
 
 /* ---- tile-sharded stage (multi-rank), two phases per depth:
  * phase 1: factors + RrsRound uniforms; writes this rank's sum of sanitized

@@ -820,6 +820,151 @@ void orc_ema_update(float *shadow, const float *theta, size_t n, float decay) {
         shadow[i] = decay * shadow[i] + (1.0f - decay) * theta[i];
 }
 
+/* ---- render front-end (first part) ---- */
+
+static void v3_sub(const float a[3], const float b[3], float r[3]) { r[0] = a[0] - b[0]; r[1] = a[1] - b[1]; r[2] = a[2] - b[2]; }
+static float v3_dot(const float a[3], const float b[3]) { return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2]; }
+static void v3_cross(const float a[3], const float b[3], float r[3]) {
+    const float x = a[1] * b[2] - a[2] * b[1], y = a[2] * b[0] - a[0] * b[2], z = a[0] * b[1] - a[1] * b[0];
+    r[0] = x; r[1] = y; r[2] = z;
+}
+static void v3_normalize(float v[3]) {  /* Eigen normalized(): v / sqrt(squaredNorm) if > 0 */
+    const float sq = (v[0] * v[0] + v[1] * v[1]) + v[2] * v[2];
+    if (sq > 0.0f) {
+        const float n = sqrtf(sq);
+        v[0] = v[0] / n; v[1] = v[1] / n; v[2] = v[2] / n;
+    }
+}
+
+void orc_camera_ray(const float pos[3], const float look_at[3], const float up[3], float vfov_deg, float u, float v,
+                    float aspect, float o[3], float d[3]) {
+    float fwd[3], right[3], cup[3];
+    v3_sub(look_at, pos, fwd);
+    v3_normalize(fwd);
+    v3_cross(fwd, up, right);
+    v3_normalize(right);
+    v3_cross(right, fwd, cup);
+    const float tan_half = tanf(0.5f * vfov_deg * 3.14159265358979323846f / 180.0f);
+    const float px = (2.0f * u - 1.0f) * tan_half * aspect;
+    const float py = (1.0f - 2.0f * v) * tan_half;
+    for (int a = 0; a < 3; ++a) {
+        o[a] = pos[a];
+        d[a] = (fwd[a] + px * right[a]) + py * cup[a];
+    }
+    v3_normalize(d);
+}
+
+void orc_path_floats2(uint64_t seed, uint64_t key, uint32_t depth, uint64_t purpose, float *a, float *b) {
+    orc_rng r;
+    orc_rng_init(&r, seed, orc_mix_bits2(key, ((uint64_t)depth << 8) ^ purpose));
+    *a = orc_rng_next_float(&r);
+    *b = orc_rng_next_float(&r);
+}
+
+/* geometry.cpp:46-70 */
+static int tri_hit(const float *pos, const uint32_t *idx, uint32_t tri, const float o[3], const float d[3],
+                   float t_min, float t_max, float *t, float *u, float *v) {
+    const float *p0 = pos + 3 * idx[3 * tri], *p1 = pos + 3 * idx[3 * tri + 1], *p2 = pos + 3 * idx[3 * tri + 2];
+    float e1[3], e2[3], pv[3], tv[3], qv[3];
+    v3_sub(p1, p0, e1);
+    v3_sub(p2, p0, e2);
+    v3_cross(d, e2, pv);
+    const float det = v3_dot(e1, pv);
+    if (fabsf(det) < 1e-12f)
+        return 0;
+    const float inv_det = 1.0f / det;
+    v3_sub(o, p0, tv);
+    const float uu = v3_dot(tv, pv) * inv_det;
+    if (uu < 0.0f || uu > 1.0f)
+        return 0;
+    v3_cross(tv, e1, qv);
+    const float vv = v3_dot(d, qv) * inv_det;
+    if (vv < 0.0f || uu + vv > 1.0f)
+        return 0;
+    const float tt = v3_dot(e2, qv) * inv_det;
+    if (tt <= t_min || tt >= *t || tt >= t_max)
+        return 0;
+    *t = tt; *u = uu; *v = vv;
+    return 1;
+}
+
+void orc_intersect_brute(const float *pos, const uint32_t *idx, uint32_t n_tri, const float o[3], const float d[3],
+                         float t_max, float *t, uint32_t *tri, float *u, float *v) {
+    *t = INFINITY; *tri = 0xFFFFFFFFu; *u = 0.0f; *v = 0.0f;
+    for (uint32_t k = 0; k < n_tri; ++k)
+        if (tri_hit(pos, idx, k, o, d, 1e-4f, t_max, t, u, v))
+            *tri = k;
+}
+
+void orc_render_depth1(const orc_scene *s, uint32_t width, uint32_t height, uint64_t seed, uint32_t frame,
+                       float *ray_o, float *ray_d, float *hit_t, uint32_t *hit_tri, uint8_t *cls, float *p01,
+                       float *wo01, float *roughness, uint64_t *path_key) {
+    /* Scene::finalize normalization (scene.cpp:23-37) */
+    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (uint32_t i = 0; i < s->n_vert; ++i)
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = s->pos[3 * i + a] < lo[a] ? s->pos[3 * i + a] : lo[a];
+            hi[a] = s->pos[3 * i + a] > hi[a] ? s->pos[3 * i + a] : hi[a];
+        }
+    float span = 0.0f;
+    for (int a = 0; a < 3; ++a)
+        span = (hi[a] - lo[a]) > span ? (hi[a] - lo[a]) : span;
+    if (span < 1e-6f)
+        span = 1e-6f;
+    const float scale = 1.0f / (span * 1.02f);
+    float off[3];
+    for (int a = 0; a < 3; ++a)
+        off[a] = lo[a] - span * 0.01f;
+    const float aspect = (float)width / (float)height;
+    for (uint32_t p = 0; p < width * height; ++p) {
+        const uint64_t key = orc_root_path_key(p, frame);
+        path_key[p] = key;
+        float j0, j1;
+        orc_path_floats2(seed, key, 1, 0x11, &j0, &j1);  /* Draw::CameraJitter */
+        const float u = ((float)(p % width) + j0) / (float)width;
+        const float v = ((float)(p / width) + j1) / (float)height;
+        float *o = ray_o + 3 * p, *d = ray_d + 3 * p;
+        orc_camera_ray(s->cam_pos, s->cam_look, s->cam_up, s->vfov, u, v, aspect, o, d);
+        float t, uu, vv;
+        uint32_t tri;
+        orc_intersect_brute(s->pos, s->idx, s->n_tri, o, d, INFINITY, &t, &tri, &uu, &vv);
+        hit_t[p] = t;
+        hit_tri[p] = tri;
+        p01[3 * p] = p01[3 * p + 1] = p01[3 * p + 2] = 0.0f;
+        wo01[2 * p] = wo01[2 * p + 1] = 0.0f;
+        roughness[p] = 0.0f;
+        if (tri == 0xFFFFFFFFu) {
+            cls[p] = 0;
+            continue;
+        }
+        const uint32_t m = s->mat_of_tri[tri];
+        const float *alb = s->mat_albedo + 3 * m;
+        const float amax = alb[0] > alb[1] ? (alb[0] > alb[2] ? alb[0] : alb[2]) : (alb[1] > alb[2] ? alb[1] : alb[2]);
+        const int scattering = s->mat_kind[m] == 1 || amax > 0.0f;
+        cls[p] = scattering ? 2 : 1;
+        if (!scattering)
+            continue;
+        float pt[3], wo[3];
+        for (int a = 0; a < 3; ++a) {
+            pt[a] = o[a] + t * d[a];
+            wo[a] = -d[a];
+        }
+        for (int a = 0; a < 3; ++a) {
+            float q = (pt[a] - off[a]) * scale;
+            q = q < 0.0f ? 0.0f : q;
+            p01[3 * p + a] = q > 1.0f ? 1.0f : q;
+        }
+        const float z = wo[2] < -1.0f ? -1.0f : (wo[2] > 1.0f ? 1.0f : wo[2]);
+        const float theta = acosf(z);
+        float phi = atan2f(wo[1], wo[0]);
+        if (phi < 0.0f)
+            phi += 2.0f * 3.14159265358979323846f;
+        wo01[2 * p] = theta * 0.31830988618379067154f;
+        wo01[2 * p + 1] = phi * (0.5f * 0.31830988618379067154f);
+        roughness[p] = s->mat_kind[m] == 1 ? s->mat_roughness[m] : 1.0f;
+    }
+}
+
 /* ---- suffix side of trace_frame ---- */
 
 /* wavefront.cpp:299 / :317 / :355 / :485 (frame[pixel] += term), :301 / :319

@@ -192,6 +192,27 @@ void orc_adam_step(float *theta, const float *grad, float *m, float *v, size_t n
 /* EmaTracker::update (optimizer.hpp:54-61) */
 void orc_ema_update(float *shadow, const float *theta, size_t n, float decay);
 
+/* ---- render front-end (first part) ---- */
+/* Camera::generate_ray (scene.cpp:10-21) */
+void orc_camera_ray(const float pos[3], const float look_at[3], const float up[3], float vfov_deg, float u, float v,
+                    float aspect, float o[3], float d[3]);
+/* path_stream(seed, key, depth, purpose) first two next_float() (rng.hpp:78-82) */
+void orc_path_floats2(uint64_t seed, uint64_t key, uint32_t depth, uint64_t purpose, float *a, float *b);
+/* intersect_triangle over every triangle in index order (geometry.cpp:46-70, Bvh::intersect_brute_force) */
+void orc_intersect_brute(const float *pos, const uint32_t *idx, uint32_t n_tri, const float o[3], const float d[3],
+                         float t_max, float *t, uint32_t *tri, float *u, float *v);
+/* trace_frame's depth-1 front end (wavefront.cpp:253-268, :282-345): camera rays with jitter, closest hit
+ * (brute force), dispatch (:125-138: 0 miss, 1 light, 2 surface) and the surface fields
+ * (Scene::interaction scene.cpp:50-64, normalize_position :93-96, dir_to_spherical01 core.hpp:52-58). */
+typedef struct {
+    const float *pos; const uint32_t *idx; const uint32_t *mat_of_tri; uint32_t n_vert, n_tri;
+    const int32_t *mat_kind; const float *mat_albedo; const float *mat_roughness; const float *mat_emission;
+    float cam_pos[3], cam_look[3], cam_up[3], vfov;
+} orc_scene;
+void orc_render_depth1(const orc_scene *s, uint32_t width, uint32_t height, uint64_t seed, uint32_t frame,
+                       float *ray_o, float *ray_d, float *hit_t, uint32_t *hit_tri, uint8_t *cls, float *p01,
+                       float *wo01, float *roughness, uint64_t *path_key);
+
 /* ---- synthetic inputs (generator follows test_networks.cpp:37-51) ---- */
 void orc_gen_vertices(size_t n, uint32_t n_pixels, uint32_t frame, float *p01, float *wo01,
                       float *rough, float *t_x, float *i_pixel, uint64_t *path_key,

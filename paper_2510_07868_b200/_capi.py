@@ -60,6 +60,16 @@ class VertexRecSoA(C.Structure):
                 ("s", C.c_void_p)]
 
 
+class MaterialC(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("albedo", C.c_float * 3), ("roughness", C.c_float),
+                ("emission", C.c_float * 3)]
+
+
+class CameraC(C.Structure):
+    _fields_ = [("position", C.c_float * 3), ("look_at", C.c_float * 3), ("up", C.c_float * 3),
+                ("vfov_deg", C.c_float)]
+
+
 # (name, restype, argtypes) for every entry point declared in include/nrrs_gpu.h
 _P = C.c_void_p
 SIGNATURES = [
@@ -86,6 +96,14 @@ SIGNATURES = [
                                          C.POINTER(C.c_uint32), C.POINTER(C.c_int32)]),
     ("nrrs_gpu_adam_ema", C.c_int, [_P, _P, _P, _P, _P, _P, C.c_uint64, C.c_int64, C.c_float, C.c_float, C.c_float,
                                     C.c_float, C.c_float, C.c_float]),
+    ("nrrs_gpu_scene_create", C.c_int, [_P, _P, C.c_uint32, _P, C.c_uint32, _P, C.POINTER(MaterialC), C.c_uint32,
+                                        C.POINTER(CameraC), C.POINTER(_P)]),
+    ("nrrs_gpu_scene_destroy", C.c_int, [_P]),
+    ("nrrs_gpu_scene_node_count", C.c_uint32, [_P]),
+    ("nrrs_gpu_camera_rays", C.c_int, [_P, _P, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32, _P, _P, _P]),
+    ("nrrs_gpu_intersect", C.c_int, [_P, _P, _P, _P, _P, C.c_uint64, _P, _P, _P, _P]),
+    ("nrrs_gpu_render_check", C.c_int, [_P]),
+    ("nrrs_gpu_surface_records", C.c_int, [_P, _P, _P, _P, _P, _P, C.c_uint64, _P, _P, _P, _P, _P]),
     ("nrrs_gpu_set_weights", C.c_int, [_P, C.POINTER(NetWeights)]),
     ("nrrs_gpu_rrs_stage", C.c_int, [_P, C.POINTER(VertexSoA), C.c_uint64, C.POINTER(StageParams),
                                      C.POINTER(StageOut), C.POINTER(StageResultC)]),

@@ -11,6 +11,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -1072,6 +1073,250 @@ int nrrs_gpu_adam_ema(nrrs_gpu_ctx *ctx, float *d_theta, const float *d_grad, fl
     a.inv_scale = inv_scale;
     a.decay = ema_decay;
     CK(ctx, launch_adam_ema(d_theta, d_grad, d_m, d_v, d_shadow, n, a, ctx->num_sms, ctx->stream));
+    ctx->launches += 1;
+    return NRRS_OK;
+}
+
+// ---- render front-end ----
+}  // extern "C"
+
+struct nrrs_scene {
+    int device = 0;
+    RenderScene dev{};
+    void *bufs[10] = {};
+};
+
+namespace {
+struct HostBvh {  // Bvh::build_recursive (geometry.cpp:88-121)
+    std::vector<BvhNodeDev> nodes;
+    std::vector<uint32_t> prims;
+    const float *pos;
+    const uint32_t *idx;
+    void tri_bounds(uint32_t t, float lo[3], float hi[3]) const {
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = INFINITY;
+            hi[a] = -INFINITY;
+        }
+        for (int k = 0; k < 3; ++k)
+            for (int a = 0; a < 3; ++a) {
+                const float v = pos[3 * idx[3 * t + k] + a];
+                lo[a] = std::min(lo[a], v);
+                hi[a] = std::max(hi[a], v);
+            }
+    }
+    uint32_t build(uint32_t begin, uint32_t end, const std::vector<float> &centers) {
+        const uint32_t id = (uint32_t)nodes.size();
+        nodes.emplace_back();
+        float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        for (uint32_t i = begin; i < end; ++i) {
+            float l[3], h[3];
+            tri_bounds(prims[i], l, h);
+            for (int a = 0; a < 3; ++a) {
+                lo[a] = std::min(lo[a], l[a]);
+                hi[a] = std::max(hi[a], h[a]);
+            }
+        }
+        for (int a = 0; a < 3; ++a) {
+            nodes[id].lo[a] = lo[a];
+            nodes[id].hi[a] = hi[a];
+        }
+        const uint32_t count = end - begin;
+        if (count <= 4) {
+            nodes[id].offset = begin;
+            nodes[id].count = (uint16_t)count;
+            return id;
+        }
+        const float ex[3] = {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]};
+        int axis = 0;
+        if (ex[1] > ex[0])
+            axis = 1;
+        if (ex[2] > ex[axis])
+            axis = 2;
+        const uint32_t mid = begin + count / 2;
+        std::nth_element(prims.begin() + begin, prims.begin() + mid, prims.begin() + end,
+                         [&](uint32_t a, uint32_t b) { return centers[3 * a + axis] < centers[3 * b + axis]; });
+        nodes[id].axis = (uint8_t)axis;
+        build(begin, mid, centers);
+        const uint32_t right = build(mid, end, centers);
+        nodes[id].offset = right;
+        nodes[id].count = 0;
+        return id;
+    }
+};
+}  // namespace
+
+extern "C" {
+
+int nrrs_gpu_scene_create(nrrs_gpu_ctx *ctx, const float *pos, uint32_t n_vert, const uint32_t *idx, uint32_t n_tri,
+                          const uint32_t *mat_ids, const nrrs_material *mats, uint32_t n_mats,
+                          const nrrs_camera *cam, nrrs_scene **out) {
+    if (!ctx || !out || !cam || (n_vert && !pos) || (n_tri && (!idx || !mat_ids)) || (n_mats && !mats))
+        return NRRS_EINVAL;
+    *out = nullptr;
+    for (uint32_t t = 0; t < 3ull * n_tri; ++t)
+        if (idx[t] >= n_vert)
+            return fail(ctx, NRRS_EINVAL, "scene: triangle index out of range");
+    for (uint32_t t = 0; t < n_tri; ++t)
+        if (mat_ids[t] >= n_mats)
+            return fail(ctx, NRRS_EINVAL, "scene: material id out of range");
+    CK(ctx, cudaSetDevice(ctx->device));
+    HostBvh b;
+    b.pos = pos;
+    b.idx = idx;
+    if (n_tri) {
+        b.prims.resize(n_tri);
+        std::vector<float> centers(3ull * n_tri);
+        for (uint32_t i = 0; i < n_tri; ++i) {
+            b.prims[i] = i;
+            float lo[3], hi[3];
+            b.tri_bounds(i, lo, hi);
+            for (int a = 0; a < 3; ++a)
+                centers[3ull * i + a] = (lo[a] + hi[a]) * 0.5f;  // AABB::center
+        }
+        b.nodes.reserve(2ull * n_tri);
+        b.build(0, n_tri, centers);
+    }
+    auto *s = new nrrs_scene();
+    s->device = ctx->device;
+    RenderScene &d = s->dev;
+    auto up = [&](int slot, const void *src, size_t bytes) -> void * {
+        void *p = nullptr;
+        if (bytes && cudaMalloc(&p, bytes) == cudaSuccess)
+            cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice);
+        s->bufs[slot] = p;
+        return p;
+    };
+    std::vector<int32_t> kind(n_mats);
+    std::vector<float> alb(3ull * n_mats), rough(n_mats), emi(3ull * n_mats);
+    for (uint32_t m = 0; m < n_mats; ++m) {
+        kind[m] = mats[m].kind;
+        rough[m] = mats[m].roughness;
+        for (int a = 0; a < 3; ++a) {
+            alb[3ull * m + a] = mats[m].albedo[a];
+            emi[3ull * m + a] = mats[m].emission[a];
+        }
+    }
+    d.pos = (const float *)up(0, pos, 12ull * n_vert);
+    d.idx = (const uint32_t *)up(1, idx, 12ull * n_tri);
+    d.mat_of_tri = (const uint32_t *)up(2, mat_ids, 4ull * n_tri);
+    d.nodes = (const BvhNodeDev *)up(3, b.nodes.data(), b.nodes.size() * sizeof(BvhNodeDev));
+    d.prims = (const uint32_t *)up(4, b.prims.data(), 4ull * b.prims.size());
+    d.mat_kind = (const int32_t *)up(5, kind.data(), 4ull * n_mats);
+    d.mat_albedo = (const float *)up(6, alb.data(), 12ull * n_mats);
+    d.mat_roughness = (const float *)up(7, rough.data(), 4ull * n_mats);
+    d.mat_emission = (const float *)up(8, emi.data(), 12ull * n_mats);
+    d.n_nodes = (uint32_t)b.nodes.size();
+    d.n_tri = n_tri;
+    // Scene::finalize normalization (scene.cpp:23-37)
+    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (uint32_t i = 0; i < n_vert; ++i)
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = std::min(lo[a], pos[3ull * i + a]);
+            hi[a] = std::max(hi[a], pos[3ull * i + a]);
+        }
+    if (n_vert == 0) {
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = 0.0f;
+            hi[a] = 1.0f;
+        }
+    }
+    float span = std::max(std::max(hi[0] - lo[0], hi[1] - lo[1]), hi[2] - lo[2]);
+    span = std::max(span, 1e-6f);
+    d.norm_scale = 1.0f / (span * 1.02f);
+    for (int a = 0; a < 3; ++a)
+        d.norm_offset[a] = lo[a] - span * 0.01f;
+    // Camera::generate_ray's basis (scene.cpp:10-15)
+    auto normalize = [](float v[3]) {
+        const float sq = (v[0] * v[0] + v[1] * v[1]) + v[2] * v[2];
+        if (sq > 0.0f) {
+            const float n = std::sqrt(sq);
+            v[0] = v[0] / n;
+            v[1] = v[1] / n;
+            v[2] = v[2] / n;
+        }
+    };
+    auto cross = [](const float a[3], const float b2[3], float r[3]) {
+        const float x = a[1] * b2[2] - a[2] * b2[1], y = a[2] * b2[0] - a[0] * b2[2], z = a[0] * b2[1] - a[1] * b2[0];
+        r[0] = x;
+        r[1] = y;
+        r[2] = z;
+    };
+    float fwd[3] = {cam->look_at[0] - cam->position[0], cam->look_at[1] - cam->position[1],
+                    cam->look_at[2] - cam->position[2]};
+    normalize(fwd);
+    float right[3], cup[3];
+    cross(fwd, cam->up, right);
+    normalize(right);
+    cross(right, fwd, cup);
+    for (int a = 0; a < 3; ++a) {
+        d.cam_pos[a] = cam->position[a];
+        d.cam_fwd[a] = fwd[a];
+        d.cam_right[a] = right[a];
+        d.cam_up[a] = cup[a];
+    }
+    d.tan_half = std::tan(0.5f * cam->vfov_deg * 3.14159265358979323846f / 180.0f);
+    d.aspect = 1.0f;
+    *out = s;
+    return NRRS_OK;
+}
+
+int nrrs_gpu_scene_destroy(nrrs_scene *s) {
+    if (!s)
+        return NRRS_OK;
+    cudaSetDevice(s->device);
+    for (void *p : s->bufs)
+        if (p)
+            cudaFree(p);
+    delete s;
+    return NRRS_OK;
+}
+
+uint32_t nrrs_gpu_scene_node_count(const nrrs_scene *s) { return s ? s->dev.n_nodes : 0; }
+
+int nrrs_gpu_camera_rays(nrrs_gpu_ctx *ctx, const nrrs_scene *scene, uint32_t width, uint32_t height, uint64_t seed,
+                         uint32_t frame, float *d_o, float *d_d, uint64_t *d_keys) {
+    if (!ctx || !scene || !width || !height || !d_o || !d_d || !d_keys)
+        return NRRS_EINVAL;
+    CK(ctx, cudaSetDevice(ctx->device));
+    RenderScene s = scene->dev;
+    s.aspect = (float)width / (float)height;
+    CK(ctx, launch_camera(s, width, height, h_mix_bits(seed), frame, d_o, d_d, d_keys, ctx->num_sms, ctx->stream));
+    ctx->launches += 1;
+    return NRRS_OK;
+}
+
+int nrrs_gpu_intersect(nrrs_gpu_ctx *ctx, const nrrs_scene *scene, const float *d_o, const float *d_d,
+                       const float *d_t_max, uint64_t n, float *d_t, uint32_t *d_tri, float *d_u, float *d_v) {
+    if (!ctx || !scene || (n && (!d_o || !d_d || !d_t || !d_tri)))
+        return NRRS_EINVAL;
+    CK(ctx, cudaSetDevice(ctx->device));
+    CK(ctx, launch_intersect(scene->dev, d_o, d_d, d_t_max, n, d_t, d_tri, d_u, d_v, ctx->d_misc + 13, ctx->num_sms,
+                             ctx->stream));
+    ctx->launches += 1;
+    return NRRS_OK;
+}
+
+int nrrs_gpu_render_check(nrrs_gpu_ctx *ctx) {
+    if (!ctx)
+        return NRRS_EINVAL;
+    CK(ctx, cudaSetDevice(ctx->device));
+    uint32_t h = 0;
+    CK(ctx, cudaMemcpyAsync(&h, ctx->d_misc + 13, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(ctx, cudaMemsetAsync(ctx->d_misc + 13, 0, sizeof h, ctx->stream));
+    CK(ctx, cudaStreamSynchronize(ctx->stream));
+    if (h & 1u)
+        return fail(ctx, NRRS_EINVAL, "Bvh::intersect: degenerate ray direction");
+    return NRRS_OK;
+}
+
+int nrrs_gpu_surface_records(nrrs_gpu_ctx *ctx, const nrrs_scene *scene, const float *d_o, const float *d_d,
+                             const float *d_t, const uint32_t *d_tri, uint64_t n, uint8_t *d_class, float *d_p01,
+                             float *d_wo01, float *d_roughness, uint32_t *d_material) {
+    if (!ctx || !scene || (n && (!d_o || !d_d || !d_t || !d_tri || !d_class || !d_p01 || !d_wo01 || !d_roughness)))
+        return NRRS_EINVAL;
+    CK(ctx, cudaSetDevice(ctx->device));
+    CK(ctx, launch_surface(scene->dev, d_o, d_d, d_t, d_tri, n, d_class, d_p01, d_wo01, d_roughness, d_material,
+                           ctx->num_sms, ctx->stream));
     ctx->launches += 1;
     return NRRS_OK;
 }

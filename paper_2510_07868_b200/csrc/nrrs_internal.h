@@ -239,6 +239,34 @@ cudaError_t launch_stat_train(const TrainStepParams &p, float *partials, uint32_
 cudaError_t launch_adam_ema(float *theta, const float *grad, float *m, float *v, float *shadow, uint64_t n,
                             const AdamParams &a, int num_sms, cudaStream_t stream);
 
+// Render front-end (nrrs_render.cu): Bvh::Node (geometry.hpp) flattened for the device
+struct BvhNodeDev {
+    float lo[3], hi[3];
+    uint32_t offset;  // leaf: first prim; inner: right child (left child = this + 1)
+    uint16_t count;   // > 0: leaf
+    uint8_t axis, pad;
+};
+struct RenderScene {
+    const float *pos;            // [3 * n_vert]
+    const uint32_t *idx;         // [3 * n_tri]
+    const uint32_t *mat_of_tri;  // [n_tri]
+    const BvhNodeDev *nodes;
+    const uint32_t *prims;
+    uint32_t n_nodes, n_tri;
+    const int32_t *mat_kind;     // 0 diffuse, 1 conductor
+    const float *mat_albedo, *mat_roughness, *mat_emission;
+    float norm_offset[3], norm_scale;
+    float cam_pos[3], cam_fwd[3], cam_right[3], cam_up[3], tan_half, aspect;
+};
+cudaError_t launch_camera(const RenderScene &s, uint32_t width, uint32_t height, uint64_t mixed_seed, uint32_t frame,
+                          float *o, float *d, uint64_t *keys, int num_sms, cudaStream_t stream);
+cudaError_t launch_intersect(const RenderScene &s, const float *o, const float *d, const float *tmax, uint64_t n,
+                             float *t, uint32_t *tri, float *u, float *v, uint32_t *err, int num_sms,
+                             cudaStream_t stream);
+cudaError_t launch_surface(const RenderScene &s, const float *o, const float *d, const float *t, const uint32_t *tri,
+                           uint64_t n, uint8_t *cls, float *p01, float *wo01, float *rough, uint32_t *material,
+                           int num_sms, cudaStream_t stream);
+
 size_t infer_smem_bytes(int kind, const InferParams &p);
 cudaError_t launch_infer(int kind, const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out);
 uint32_t infer_max_grid(int num_sms);

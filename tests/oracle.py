@@ -100,6 +100,10 @@ def lib() -> C.CDLL:
             "orc_adam_step": (None, [p, p, p, p, C.c_size_t, C.c_int64, f, f, f, f]),
             "orc_rrs_loss": (None, [i, p, p, p, p, p, p, C.c_size_t, p, C.c_size_t, f, i, f, f, f, f, f, p, p, p]),
             "orc_ema_update": (None, [p, p, C.c_size_t, f]),
+            "orc_camera_ray": (None, [p, p, p, f, f, f, f, p, p]),
+            "orc_path_floats2": (None, [u64, u64, u32, u64, p, p]),
+            "orc_intersect_brute": (None, [p, p, u32, p, p, f, p, p, p, p]),
+            "orc_render_depth1": (None, [p, u32, u32, u64, u32, p, p, p, p, p, p, p, p, p]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -378,3 +382,102 @@ def gen_pixel_errors(n_pixels: int, seed: int = 13) -> np.ndarray:
     e["e"] = g.random(n_pixels, dtype=np.float32) * np.float32(2.0)
     e["inv_denom"] = np.float32(1.0) / (g.random(n_pixels, dtype=np.float32) + np.float32(0.01))
     return e
+
+
+# ---- render front-end ----
+class OrcScene(C.Structure):
+    _fields_ = [("pos", C.c_void_p), ("idx", C.c_void_p), ("mat_of_tri", C.c_void_p), ("n_vert", C.c_uint32),
+                ("n_tri", C.c_uint32), ("mat_kind", C.c_void_p), ("mat_albedo", C.c_void_p),
+                ("mat_roughness", C.c_void_p), ("mat_emission", C.c_void_p), ("cam_pos", C.c_float * 3),
+                ("cam_look", C.c_float * 3), ("cam_up", C.c_float * 3), ("vfov", C.c_float)]
+
+
+def render_depth1(desc, width: int, height: int, seed: int, frame: int) -> dict:
+    """orc_render_depth1: camera rays, brute-force closest hits, dispatch class, surface fields."""
+    pos, idx, mid = desc.arrays()
+    kind = np.array([m.kind for m in desc.materials], np.int32)
+    alb = np.array([m.albedo for m in desc.materials], np.float32).reshape(-1)
+    rough = np.array([m.roughness for m in desc.materials], np.float32)
+    emi = np.array([m.emission for m in desc.materials], np.float32).reshape(-1)
+    f3 = lambda v: (C.c_float * 3)(*[float(np.float32(x)) for x in v])
+    cam = desc.camera
+    sc = OrcScene(pos.ctypes.data, idx.ctypes.data, mid.ctypes.data, pos.shape[0], mid.size, kind.ctypes.data,
+                  alb.ctypes.data, rough.ctypes.data, emi.ctypes.data, f3(cam.position), f3(cam.look_at),
+                  f3(cam.up), float(np.float32(cam.vfov_deg)))
+    n = width * height
+    out = {"o": np.zeros((n, 3), np.float32), "d": np.zeros((n, 3), np.float32), "t": np.zeros(n, np.float32),
+           "tri": np.zeros(n, np.uint32), "class": np.zeros(n, np.uint8), "p01": np.zeros((n, 3), np.float32),
+           "wo01": np.zeros((n, 2), np.float32), "roughness": np.zeros(n, np.float32),
+           "path_key": np.zeros(n, np.uint64)}
+    lib().orc_render_depth1(C.byref(sc), width, height, seed & (2**64 - 1), frame, ptr(out["o"]), ptr(out["d"]),
+                            ptr(out["t"]), ptr(out["tri"]), ptr(out["class"]), ptr(out["p01"]), ptr(out["wo01"]),
+                            ptr(out["roughness"]), ptr(out["path_key"]))
+    return out
+
+
+def intersect_brute(pos: np.ndarray, idx: np.ndarray, o: np.ndarray, d: np.ndarray, t_max=None) -> dict:
+    """Bvh::intersect_brute_force per ray (geometry.cpp:46-70 in triangle order)."""
+    n = o.shape[0]
+    pos = np.ascontiguousarray(pos, np.float32)
+    idx = np.ascontiguousarray(idx, np.uint32)
+    o = np.ascontiguousarray(o, np.float32)
+    d = np.ascontiguousarray(d, np.float32)
+    t = np.zeros(n, np.float32)
+    tri = np.zeros(n, np.uint32)
+    u = np.zeros(n, np.float32)
+    v = np.zeros(n, np.float32)
+    L = lib()
+    ft, fu, fv, ut = C.c_float(), C.c_float(), C.c_float(), C.c_uint32()
+    n_tri = idx.size // 3
+    for r in range(n):
+        tm = np.float32(np.inf) if t_max is None else np.float32(t_max[r])
+        L.orc_intersect_brute(pos.ctypes.data, idx.ctypes.data, n_tri, o[r].ctypes.data, d[r].ctypes.data,
+                              float(tm), C.byref(ft), C.byref(ut), C.byref(fu), C.byref(fv))
+        t[r], tri[r], u[r], v[r] = ft.value, ut.value, fu.value, fv.value
+    return {"t": t, "tri": tri, "u": u, "v": v}
+
+
+def _rng(seed: int, seq: int):
+    r = (C.c_uint64 * 2)()
+    lib().orc_rng_init(r, seed, seq)
+    return r
+
+
+def random_soup(tris: int, seed: int):
+    """test_geometry.cpp:14-29 random_soup (arguments drawn left to right): positions [3*tris, 3] f32,
+    indices [3*tris] u32, material ids [tris] (all 0)."""
+    L = lib()
+    r = _rng(seed, 0)
+    nf = lambda: np.float32(L.orc_rng_next_float(r))
+    pos = np.zeros((3 * tris, 3), np.float32)
+    f4, f2, f07, h = np.float32(4), np.float32(2), np.float32(0.7), np.float32(0.5)
+    for i in range(tris):
+        base = np.array([nf() * f4 - f2 for _ in range(3)], np.float32)
+        for k in range(3):
+            jit = np.array([nf() - h for _ in range(3)], np.float32)
+            pos[3 * i + k] = base + f07 * jit
+    return pos, np.arange(3 * tris, dtype=np.uint32), np.zeros(tris, np.uint32)
+
+
+def random_rays(n: int, seed: int, seq: int, extent: float = 8.0, t_max: bool = False):
+    """test_geometry.cpp:47-53 / :70-75: origins in [-extent/2, extent/2)^3, random_unit directions
+    (:31-38), optional t_max = 2 + 4u."""
+    L = lib()
+    r = _rng(seed, seq)
+    nf = lambda: np.float32(L.orc_rng_next_float(r))
+    e, he = np.float32(extent), np.float32(extent / 2)
+    o = np.zeros((n, 3), np.float32)
+    d = np.zeros((n, 3), np.float32)
+    tm = np.full(n, np.inf, np.float32)
+    one, two = np.float32(1), np.float32(2)
+    for i in range(n):
+        o[i] = [nf() * e - he for _ in range(3)]
+        while True:
+            v = np.array([nf() * two - one for _ in range(3)], np.float32)
+            n2 = (v[0] * v[0] + v[1] * v[1]) + v[2] * v[2]
+            if np.float32(1e-4) < n2 < one:
+                d[i] = v / np.sqrt(n2)
+                break
+        if t_max:
+            tm[i] = np.float32(2) + np.float32(4) * nf()
+    return o, d, tm

@@ -417,3 +417,57 @@ def test_oracle_rrs_loss_gradient_matches_finite_differences(variant, phase):
         badg = sum(abs(gg[k] * scale - fd(nets.rrs_grid, k)) > 3e-2 * max(abs(fd(nets.rrs_grid, k)), 1e-4)
                    for k in sel)
         assert badg <= max(2, sel.size // 8), (badg, sel.size)
+
+
+# ---- render front-end oracle ----
+def test_camera_ray_known_answers():
+    """test_geometry.cpp:325-333 "camera rays hit the view center"."""
+    L = orc.lib()
+    f3 = lambda *v: np.array(v, np.float32)
+    o, d = np.zeros(3, np.float32), np.zeros(3, np.float32)
+    pos, look, up = f3(0, 0, 5), f3(0, 0, 0), f3(0, 1, 0)  # kept alive across the calls
+    L.orc_camera_ray(orc.ptr(pos), orc.ptr(look), orc.ptr(up), 40.0, 0.5, 0.5, 1.0, orc.ptr(o), orc.ptr(d))
+    assert np.linalg.norm(d - f3(0, 0, -1)) < 1e-6
+    L.orc_camera_ray(orc.ptr(pos), orc.ptr(look), orc.ptr(up), 40.0, 0.0, 0.0, 1.0, orc.ptr(o), orc.ptr(d))
+    assert d[0] < 0 and d[1] > 0
+    assert np.array_equal(o, f3(0, 0, 5))
+
+
+@pytest.mark.parametrize("name", ["cornell", "caustic", "furnace"])
+def test_builtin_scene_oracle_depth1(name):
+    """test_geometry.cpp:355-363 (center ray hits) and :245-255 (normalized positions in the unit cube)."""
+    from paper_2510_07868_b200 import render
+    desc = getattr(render, f"make_{name}_scene")()
+    w, h = 32, 24
+    r = orc.render_depth1(desc, w, h, 7, 0)
+    assert r["tri"][(h // 2) * w + w // 2] != 0xFFFFFFFF
+    assert r["p01"].min() >= 0.0 and r["p01"].max() <= 1.0
+    surf = r["class"] == 2
+    assert surf.any()
+    assert (r["wo01"][surf] >= 0).all() and (r["wo01"][surf] <= 1).all()
+    mats = np.array([m.kind for m in desc.materials])
+    tri_mat = np.array(desc.material_ids)[r["tri"][surf]]
+    want = np.where(mats[tri_mat] == render.CONDUCTOR,
+                    np.array([m.roughness for m in desc.materials], np.float32)[tri_mat], np.float32(1.0))
+    assert np.array_equal(r["roughness"][surf], want)
+    # keys follow root_path_key(p, frame)
+    assert int(r["path_key"][5]) == orc.lib().orc_root_path_key(5, 0)
+
+
+def test_cornell_mesh_matches_reference_layout():
+    """make_cornell_scene: 6 quads + 2 boxes = 18 quads, 36 triangles, 5 materials."""
+    from paper_2510_07868_b200 import render
+    s = render.make_cornell_scene()
+    pos, idx, mid = s.arrays()
+    assert pos.shape == (72, 3) and idx.size == 108 and mid.size == 36 and len(s.materials) == 5
+    assert np.array_equal(pos[2], np.float32([1, 0, 1]))  # (corner + e1) + e2 of the floor
+    assert list(mid[10:12]) == [4, 4]                      # the lamp
+
+
+def test_random_soup_bvh_oracle_hits():
+    pos, idx, _ = orc.random_soup(50, 5)
+    o, d, _ = orc.random_rays(200, 99, 1)
+    r = orc.intersect_brute(pos, idx, o, d)
+    hit = r["tri"] != 0xFFFFFFFF
+    assert hit.any() and (r["t"][hit] > 1e-4).all() and np.isinf(r["t"][~hit]).all()
+    assert ((r["u"][hit] >= 0) & (r["v"][hit] >= 0) & (r["u"][hit] + r["v"][hit] <= 1)).all()
