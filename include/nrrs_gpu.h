@@ -175,6 +175,39 @@ typedef struct {
 } nrrs_camera;
 
 typedef struct nrrs_scene nrrs_scene;
+typedef struct nrrs_tracer nrrs_tracer;
+
+/* TraceConfig (wavefront.hpp:128-140): the fields trace_frame reads. */
+typedef struct {
+    uint32_t width, height;
+    int32_t max_depth;        /* B */
+    uint32_t queue_capacity;  /* 0 = queue_capacity_for(W*H) */
+    uint64_t seed;
+    uint32_t frame_index;
+    float adrrs_eps_scale;    /* 1e-4 in the reference */
+    int32_t collect_training;
+} nrrs_trace_config;
+
+/* RateControl (rrs.hpp:23-36), updated in place on overflow. */
+typedef struct {
+    float f_rate, alpha, eps;
+    int32_t enabled;
+    uint64_t overflow_events;
+} nrrs_rate_control;
+
+/* FrameReport (wavefront.hpp:175-186). */
+typedef struct {
+    uint64_t camera_rays, scatter_rays, shadow_rays, nonfinite_drops, overflow_events, bias_drop_events,
+        train_samples;
+    uint32_t depth_counts[32];
+} nrrs_frame_report;
+
+/* Film (wavefront.hpp:78-123) on the device: sum [3n] f64, samples [n], i_cur / i_acc / normal [3n] f32. */
+typedef struct {
+    double *sum;
+    uint32_t *samples;
+    float *i_cur, *i_acc, *normal;
+} nrrs_film_dev;
 typedef struct nrrs_gpu_ctx nrrs_gpu_ctx;
 
 /* ---- context ------------------------------------------------------------ */
@@ -299,6 +332,9 @@ NRRS_API int nrrs_gpu_scene_create(nrrs_gpu_ctx *ctx, const float *h_positions, 
                                    const nrrs_camera *camera, nrrs_scene **out);
 NRRS_API int nrrs_gpu_scene_destroy(nrrs_scene *scene);
 NRRS_API uint32_t nrrs_gpu_scene_node_count(const nrrs_scene *scene);
+NRRS_API uint32_t nrrs_gpu_scene_light_count(const nrrs_scene *scene);
+/* Scene::env_emission (scene.hpp:45), radiance of escaped rays */
+NRRS_API int nrrs_gpu_scene_set_env(nrrs_scene *scene, const float env[3]);
 
 /* Depth-1 camera rays of a width x height film (wavefront.cpp:253-268): pixel p's key is
  * root_path_key(p, frame), its jitter path_stream(seed, key, 1, CameraJitter).  d_o / d_d [3n],
@@ -322,6 +358,29 @@ NRRS_API int nrrs_gpu_surface_records(nrrs_gpu_ctx *ctx, const nrrs_scene *scene
                                       const float *d_d, const float *d_t, const uint32_t *d_tri, uint64_t n,
                                       uint8_t *d_class, float *d_p01, float *d_wo01, float *d_roughness,
                                       uint32_t *d_material);
+
+/* ---- trace_frame on the GPU ---- */
+
+/* Device queues and per-depth VertexRec storage for films up to max_pixels and depths up to
+ * max_depth (capacity 0 = queue_capacity_for(max_pixels)). */
+NRRS_API int nrrs_gpu_tracer_create(nrrs_gpu_ctx *ctx, uint32_t max_pixels, int32_t max_depth, uint32_t capacity,
+                                    nrrs_tracer **out);
+NRRS_API int nrrs_gpu_tracer_destroy(nrrs_tracer *tracer);
+
+/* trace_frame (wavefront.cpp:217-551): camera rays, then per depth closest hits, dispatch, the
+ * miss / emitter / emission film terms, the RRS stage with assignment[depth-1] (networks from
+ * nrrs_gpu_set_weights), NEE + BSDF sampling per child slot, the ordered film folds and the
+ * order-preserving compaction; then the reverse pass, TrainSample emission into d_train (appended
+ * at *h_train_count, which is advanced) and Film::add_frame.  Film buffers are device pointers;
+ * film->normal receives the depth-1 normals.  Synchronous (a few host reads per depth). */
+NRRS_API int nrrs_gpu_trace_frame(nrrs_tracer *tracer, const nrrs_scene *scene, const nrrs_trace_config *cfg,
+                                  const nrrs_strategy *assignment, nrrs_rate_control *rc, const nrrs_film_dev *film,
+                                  nrrs_train_sample *d_train, uint64_t train_capacity, uint64_t *h_train_count,
+                                  nrrs_frame_report *report);
+/* The last frame's f64 radiance buffer [3 * W * H] (device) and depth-d vertex records. */
+NRRS_API int nrrs_gpu_tracer_frame_buffer(const nrrs_tracer *tracer, const double **d_frame);
+NRRS_API int nrrs_gpu_tracer_vertices(const nrrs_tracer *tracer, int32_t depth, nrrs_vertex_rec_soa *out,
+                                      uint32_t *count);
 
 /* ---- tile-sharded stage (multi-rank), two phases per depth:
  * phase 1: factors + RrsRound uniforms; writes this rank's sum of sanitized

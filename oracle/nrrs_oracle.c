@@ -1108,3 +1108,618 @@ void orc_init_nets(int variant, const orc_grid_spec *g, uint64_t seed, int rando
         for (size_t i = 0; i < gn; ++i)
             rrs_grid[i] *= 1e4f;
 }
+
+/* ---- trace_frame ---- */
+#define ORC_PI 3.14159265358979323846f
+#define ORC_INV_PI 0.31830988618379067154f
+
+static void face_normal(const orc_scene *s, uint32_t tri, float n[3]) { /* geometry.cpp:22-28 */
+    const float *p0 = s->pos + 3 * s->idx[3 * tri], *p1 = s->pos + 3 * s->idx[3 * tri + 1],
+                *p2 = s->pos + 3 * s->idx[3 * tri + 2];
+    float e1[3], e2[3], c[3];
+    v3_sub(p1, p0, e1);
+    v3_sub(p2, p0, e2);
+    v3_cross(e1, e2, c);
+    const float len = sqrtf(v3_dot(c, c));
+    if (len > 0.0f) {
+        n[0] = c[0] / len; n[1] = c[1] / len; n[2] = c[2] / len;
+    } else {
+        n[0] = 0.0f; n[1] = 0.0f; n[2] = 1.0f;
+    }
+}
+static float tri_area(const orc_scene *s, uint32_t tri) { /* geometry.cpp:16-20 */
+    const float *p0 = s->pos + 3 * s->idx[3 * tri], *p1 = s->pos + 3 * s->idx[3 * tri + 1],
+                *p2 = s->pos + 3 * s->idx[3 * tri + 2];
+    float e1[3], e2[3], c[3];
+    v3_sub(p1, p0, e1);
+    v3_sub(p2, p0, e2);
+    v3_cross(e1, e2, c);
+    return 0.5f * sqrtf(v3_dot(c, c));
+}
+static float fmaxf3(const float v[3]) { /* Eigen maxCoeff */
+    float m = v[0];
+    if (v[1] > m) m = v[1];
+    if (v[2] > m) m = v[2];
+    return m;
+}
+static float stdmaxf(float a, float b) { return a < b ? b : a; }
+static float stdminf(float a, float b) { return b < a ? b : a; }
+
+static float mis_power2(float a, float b) { /* wavefront.cpp:15-21 */
+    const double a2 = (double)a * (double)a, b2 = (double)b * (double)b;
+    if (a2 + b2 <= 0.0)
+        return 0.0f;
+    return (float)(a2 / (a2 + b2));
+}
+static void build_frame(const float n[3], float t[3], float b[3]) { /* core.hpp:43-50 */
+    const float sign = copysignf(1.0f, n[2]);
+    const float a = -1.0f / (sign + n[2]);
+    const float c = n[0] * n[1] * a;
+    t[0] = 1.0f + sign * n[0] * n[0] * a; t[1] = sign * c; t[2] = -sign * n[0];
+    b[0] = c; b[1] = sign + n[1] * n[1] * a; b[2] = -n[1];
+}
+static void to_world(const float n[3], const float l[3], float w[3]) { /* bsdf.cpp:35-39 */
+    float t[3], b[3];
+    build_frame(n, t, b);
+    for (int a = 0; a < 3; ++a)
+        w[a] = (l[0] * t[a] + l[1] * b[a]) + l[2] * n[a];
+}
+static float ggx_d(float cos_h, float alpha) {
+    if (cos_h <= 0.0f)
+        return 0.0f;
+    const float a2 = alpha * alpha;
+    const float d = stdmaxf(cos_h * cos_h * (a2 - 1.0f) + 1.0f, 1e-12f);
+    return a2 / (ORC_PI * d * d);
+}
+static float smith_g1(float cos_v, float alpha) {
+    if (cos_v <= 0.0f)
+        return 0.0f;
+    const float a2 = alpha * alpha;
+    return 2.0f * cos_v / (cos_v + sqrtf(a2 + (1.0f - a2) * cos_v * cos_v));
+}
+static void schlick(const float f0[3], float cos_i, float out[3]) {
+    float m = 1.0f - cos_i;
+    m = m < 0.0f ? 0.0f : (1.0f < m ? 1.0f : m); /* std::clamp */
+    const float m2 = m * m;
+    for (int a = 0; a < 3; ++a)
+        out[a] = f0[a] + (1.0f - f0[a]) * (m2 * m2 * m);
+}
+static void half_vec(const float wo[3], const float wi[3], float h[3]) {
+    for (int a = 0; a < 3; ++a)
+        h[a] = wo[a] + wi[a];
+    v3_normalize(h);
+}
+static void bsdf_eval(int kind, const float alb[3], float rough, const float n[3], const float wo[3],
+                      const float wi[3], float f[3]) { /* bsdf.cpp:43-61 */
+    f[0] = f[1] = f[2] = 0.0f;
+    const float cos_o = v3_dot(n, wo), cos_i = v3_dot(n, wi);
+    if (cos_o <= 0.0f || cos_i <= 0.0f)
+        return;
+    if (kind == 0) {
+        for (int a = 0; a < 3; ++a)
+            f[a] = alb[a] * ORC_INV_PI;
+        return;
+    }
+    float h[3], fr[3];
+    half_vec(wo, wi, h);
+    const float alpha = stdmaxf(rough, 1e-3f);
+    const float d = ggx_d(v3_dot(n, h), alpha);
+    const float g = smith_g1(cos_o, alpha) * smith_g1(cos_i, alpha);
+    schlick(alb, v3_dot(wo, h), fr);
+    const float sc = d * g / (4.0f * cos_o * cos_i);
+    for (int a = 0; a < 3; ++a)
+        f[a] = fr[a] * sc;
+}
+static float bsdf_pdf(int kind, float rough, const float n[3], const float wo[3], const float wi[3]) {
+    const float cos_o = v3_dot(n, wo), cos_i = v3_dot(n, wi); /* bsdf.cpp:63-83 */
+    if (cos_o <= 0.0f || cos_i <= 0.0f)
+        return 0.0f;
+    if (kind == 0)
+        return cos_i * ORC_INV_PI;
+    float h[3];
+    half_vec(wo, wi, h);
+    const float cos_h = v3_dot(n, h);
+    const float alpha = stdmaxf(rough, 1e-3f);
+    const float d = ggx_d(cos_h, alpha);
+    const float dot_oh = v3_dot(wo, h);
+    if (dot_oh <= 0.0f)
+        return 0.0f;
+    return d * cos_h / (4.0f * dot_oh);
+}
+
+int orc_bsdf_sample(int kind, const float alb[3], float rough, const float n[3], const float wo[3], float u1,
+                    float u2, float wi[3], float *pdf, float thr[3]) { /* bsdf.cpp:85-133 */
+    const float cos_o = v3_dot(n, wo);
+    if (cos_o <= 0.0f)
+        return 0;
+    if (kind == 0) {
+        const float r = sqrtf(u1);
+        const float phi = 2.0f * ORC_PI * u2;
+        const float loc[3] = {r * cosf(phi), r * sinf(phi), sqrtf(stdmaxf(0.0f, 1.0f - u1))};
+        to_world(n, loc, wi);
+        const float cos_i = v3_dot(n, wi);
+        if (cos_i <= 0.0f)
+            return 0;
+        *pdf = cos_i * ORC_INV_PI;
+        thr[0] = alb[0]; thr[1] = alb[1]; thr[2] = alb[2];
+        return 1;
+    }
+    const float alpha = stdmaxf(rough, 1e-3f);
+    const float tan2 = alpha * alpha * u1 / stdmaxf(1.0f - u1, 1e-12f);
+    const float cos_h = 1.0f / sqrtf(1.0f + tan2);
+    const float sin_h = sqrtf(stdmaxf(0.0f, 1.0f - cos_h * cos_h));
+    const float phi = 2.0f * ORC_PI * u2;
+    const float loc[3] = {sin_h * cosf(phi), sin_h * sinf(phi), cos_h};
+    float h[3], fr[3];
+    to_world(n, loc, h);
+    const float dot_oh = v3_dot(wo, h);
+    if (dot_oh <= 0.0f)
+        return 0;
+    for (int a = 0; a < 3; ++a)
+        wi[a] = 2.0f * dot_oh * h[a] - wo[a];
+    const float cos_i = v3_dot(n, wi);
+    if (cos_i <= 0.0f)
+        return 0;
+    const float nh = v3_dot(n, h);
+    *pdf = ggx_d(nh, alpha) * nh / (4.0f * dot_oh);
+    if (!(*pdf > 0.0f) || !isfinite(*pdf))
+        return 0;
+    const float g = smith_g1(cos_o, alpha) * smith_g1(cos_i, alpha);
+    schlick(alb, dot_oh, fr);
+    const float sc = g * dot_oh / (cos_o * nh);
+    for (int a = 0; a < 3; ++a)
+        thr[a] = fr[a] * sc;
+    return 1;
+}
+
+static int occluded_brute(const orc_scene *s, const float o[3], const float d[3], float t_max) {
+    for (uint32_t k = 0; k < s->n_tri; ++k) { /* Bvh::occluded: any hit in (kRayEps, t_max) */
+        float t = t_max, u, v;
+        if (tri_hit(s->pos, s->idx, k, o, d, 1e-4f, t_max, &t, &u, &v))
+            return 1;
+    }
+    return 0;
+}
+
+typedef struct {
+    uint32_t n;
+    uint32_t *tris;
+    float *areas;
+    int32_t *index_of_tri;
+} orc_lights;
+
+static void light_pdf(const orc_lights *L, uint32_t tri, float *pdf) { /* scene.cpp:84-91 */
+    const int32_t i = L->index_of_tri[tri];
+    *pdf = i < 0 ? 0.0f : 1.0f / ((float)L->n * L->areas[i]);
+}
+
+static void hit_emission(const orc_scene *s, const orc_lights *L, const float d[3], uint32_t tri, float dist,
+                         float prev_pdf, float out[3]) { /* wavefront.cpp:28-41 */
+    const float *e = s->mat_emission + 3 * s->mat_of_tri[tri];
+    out[0] = out[1] = out[2] = 0.0f;
+    if (!(fmaxf3(e) > 0.0f))
+        return;
+    float mis = 1.0f;
+    if (prev_pdf >= 0.0f) {
+        float pdf_area;
+        light_pdf(L, tri, &pdf_area);
+        if (pdf_area > 0.0f) {
+            float nl[3];
+            face_normal(s, tri, nl);
+            const float cos_l = fabsf(v3_dot(nl, d));
+            const float pdf_sa = pdf_area * dist * dist / stdmaxf(cos_l, 1e-8f);
+            mis = mis_power2(prev_pdf, pdf_sa);
+        }
+    }
+    for (int a = 0; a < 3; ++a)
+        out[a] = e[a] * mis;
+}
+
+typedef struct {
+    float p[3], n_s[3], wo[3], weight[3], p01[3], wo01[2], roughness;
+    uint32_t material, pixel;
+    int32_t parent;
+    uint64_t key;
+    float rrs, q_norm, q_real;
+    int decided;
+    double emit[3], nee[3], s[3];
+} orc_vrec;
+
+int orc_trace_frame(const orc_scene *s, const orc_trace_cfg *cfg, const orc_strategy *assignment,
+                    const orc_nets *nets, orc_rate_control *rc, const float *i_acc, double *frame, float *normals,
+                    orc_train_sample *train, size_t train_cap, size_t *n_train, orc_frame_report *rep) {
+    const int B = cfg->max_depth;
+    if (B < 1 || B > 32)
+        return -1;
+    const uint32_t npx = cfg->width * cfg->height;
+    if (npx == 0)
+        return -1;
+    const uint32_t cap = cfg->capacity ? cfg->capacity : orc_queue_capacity_for(npx);
+    if (cap < npx)
+        return -1;
+    memset(rep, 0, sizeof *rep);
+    /* Scene::finalize: lights + normalization (scene.cpp:23-48) */
+    orc_lights L;
+    L.n = 0;
+    L.tris = (uint32_t *)malloc(sizeof(uint32_t) * (s->n_tri + 1));
+    L.areas = (float *)malloc(sizeof(float) * (s->n_tri + 1));
+    L.index_of_tri = (int32_t *)malloc(sizeof(int32_t) * (s->n_tri + 1));
+    for (uint32_t t = 0; t < s->n_tri; ++t) {
+        L.index_of_tri[t] = -1;
+        const float a = tri_area(s, t);
+        if (fmaxf3(s->mat_emission + 3 * s->mat_of_tri[t]) > 0.0f && a > 0.0f) {
+            L.index_of_tri[t] = (int32_t)L.n;
+            L.tris[L.n] = t;
+            L.areas[L.n] = a;
+            ++L.n;
+        }
+    }
+    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (uint32_t i = 0; i < s->n_vert; ++i)
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = stdminf(lo[a], s->pos[3 * i + a]);
+            hi[a] = stdmaxf(hi[a], s->pos[3 * i + a]);
+        }
+    if (s->n_vert == 0) {
+        lo[0] = lo[1] = lo[2] = 0.0f;
+        hi[0] = hi[1] = hi[2] = 1.0f;
+    }
+    float span = stdmaxf(stdmaxf(hi[0] - lo[0], hi[1] - lo[1]), hi[2] - lo[2]);
+    span = stdmaxf(span, 1e-6f);
+    const float nscale = 1.0f / (span * 1.02f);
+    float noff[3];
+    for (int a = 0; a < 3; ++a)
+        noff[a] = lo[a] - span * 0.01f;
+
+    double lum_acc = 0.0;
+    for (uint32_t p = 0; p < npx; ++p)
+        lum_acc += (double)orc_luminance(i_acc + 3 * p);
+    const float eps_div = cfg->adrrs_eps_scale * (float)(lum_acc / (double)npx);
+
+    orc_path_state *queue = (orc_path_state *)calloc(cap, sizeof(orc_path_state));
+    orc_path_state *next = (orc_path_state *)calloc(cap, sizeof(orc_path_state));
+    uint8_t *used = (uint8_t *)calloc(cap, 1);
+    orc_vrec *verts[33] = {0};
+    uint32_t nverts[33] = {0};
+    float *hit_t = (float *)malloc(sizeof(float) * cap);
+    uint32_t *hit_tri = (uint32_t *)malloc(sizeof(uint32_t) * cap);
+    uint8_t *cls = (uint8_t *)malloc(cap);
+    const float aspect = (float)cfg->width / (float)cfg->height;
+    for (uint32_t p = 0; p < npx; ++p) { /* wavefront.cpp:253-268 */
+        orc_path_state *q = &queue[p];
+        memset(q, 0, sizeof *q);
+        q->pixel = p;
+        q->key = orc_root_path_key(p, cfg->frame_index);
+        float j0, j1;
+        orc_path_floats2(cfg->seed, q->key, 1, 0x11, &j0, &j1);
+        const float u = ((float)(p % cfg->width) + j0) / (float)cfg->width;
+        const float v = ((float)(p / cfg->width) + j1) / (float)cfg->height;
+        orc_camera_ray(s->cam_pos, s->cam_look, s->cam_up, s->vfov, u, v, aspect, q->o, q->d);
+        q->t_max = INFINITY;
+        q->w[0] = q->w[1] = q->w[2] = 1.0f;
+        q->prev_pdf = -1.0f;
+        q->rrs = 1.0f;
+        q->parent = -1;
+        q->depth = 1;
+    }
+    uint32_t n = npx;
+    rep->camera_rays = npx;
+    memset(normals, 0, sizeof(float) * 3 * npx);
+    int rc_err = 0;
+
+    for (int depth = 1; depth <= B; ++depth) {
+        if (n == 0)
+            break;
+        rep->depth_counts[depth - 1] = n;
+        if (depth >= 2)
+            rep->scatter_rays += n;
+        for (uint32_t i = 0; i < n; ++i) {
+            float u, v;
+            orc_intersect_brute(s->pos, s->idx, s->n_tri, queue[i].o, queue[i].d, queue[i].t_max, &hit_t[i],
+                                &hit_tri[i], &u, &v);
+            if (hit_tri[i] == 0xFFFFFFFFu) {
+                cls[i] = 0;
+            } else {
+                const uint32_t m = s->mat_of_tri[hit_tri[i]];
+                const int scat = s->mat_kind[m] == 1 || fmaxf3(s->mat_albedo + 3 * m) > 0.0f;
+                cls[i] = scat ? 2 : 1;
+            }
+        }
+        orc_vrec *up = depth >= 2 ? verts[depth - 1] : NULL;
+        for (uint32_t i = 0; i < n; ++i) { /* misses (:295-303) */
+            if (cls[i] != 0 || !(fmaxf3(cfg->env) > 0.0f))
+                continue;
+            const orc_path_state *q = &queue[i];
+            double term[3];
+            for (int a = 0; a < 3; ++a)
+                term[a] = (double)(q->w[a] * cfg->env[a]);
+            for (int a = 0; a < 3; ++a)
+                frame[3 * q->pixel + a] += term[a];
+            if (up && q->parent >= 0)
+                for (int a = 0; a < 3; ++a)
+                    up[q->parent].s[a] += term[a];
+        }
+        for (uint32_t i = 0; i < n; ++i) { /* pure emitters (:305-321) */
+            if (cls[i] != 1)
+                continue;
+            const orc_path_state *q = &queue[i];
+            if (depth == 1) {
+                float nl[3];
+                face_normal(s, hit_tri[i], nl);
+                if (v3_dot(nl, q->d) > 0.0f)
+                    for (int a = 0; a < 3; ++a)
+                        nl[a] = -nl[a];
+                memcpy(normals + 3 * q->pixel, nl, sizeof nl);
+            }
+            float em[3];
+            hit_emission(s, &L, q->d, hit_tri[i], hit_t[i], q->prev_pdf, em);
+            if (fmaxf3(em) > 0.0f) {
+                double term[3];
+                for (int a = 0; a < 3; ++a)
+                    term[a] = (double)(q->w[a] * em[a]);
+                for (int a = 0; a < 3; ++a)
+                    frame[3 * q->pixel + a] += term[a];
+                if (up && q->parent >= 0)
+                    for (int a = 0; a < 3; ++a)
+                        up[q->parent].s[a] += term[a];
+            }
+        }
+        uint32_t ns = 0;
+        for (uint32_t i = 0; i < n; ++i)
+            ns += cls[i] == 2;
+        orc_vrec *vd = (orc_vrec *)calloc(ns ? ns : 1, sizeof(orc_vrec));
+        verts[depth] = vd;
+        nverts[depth] = ns;
+        uint32_t j = 0;
+        for (uint32_t i = 0; i < n; ++i) { /* surface vertices (:324-352) */
+            if (cls[i] != 2)
+                continue;
+            const orc_path_state *q = &queue[i];
+            orc_vrec *v = &vd[j++];
+            const uint32_t tri = hit_tri[i];
+            float ns_[3];
+            face_normal(s, tri, ns_); /* shading_normal without per-vertex normals */
+            for (int a = 0; a < 3; ++a) {
+                v->p[a] = q->o[a] + hit_t[i] * q->d[a];
+                v->wo[a] = -q->d[a];
+            }
+            if (v3_dot(ns_, v->wo) < 0.0f)
+                for (int a = 0; a < 3; ++a)
+                    ns_[a] = -ns_[a];
+            memcpy(v->n_s, ns_, sizeof ns_);
+            memcpy(v->weight, q->w, sizeof q->w);
+            v->material = s->mat_of_tri[tri];
+            v->pixel = q->pixel;
+            v->parent = q->parent;
+            v->key = q->key;
+            v->rrs = q->rrs;
+            v->q_norm = 1.0f;
+            v->q_real = 1.0f;
+            for (int a = 0; a < 3; ++a) {
+                float qq = (v->p[a] - noff[a]) * nscale;
+                qq = stdmaxf(qq, 0.0f);
+                v->p01[a] = stdminf(qq, 1.0f);
+            }
+            const float z = v->wo[2] < -1.0f ? -1.0f : (v->wo[2] > 1.0f ? 1.0f : v->wo[2]);
+            const float theta = acosf(z);
+            float phi = atan2f(v->wo[1], v->wo[0]);
+            if (phi < 0.0f)
+                phi += 2.0f * ORC_PI;
+            v->wo01[0] = theta * ORC_INV_PI;
+            v->wo01[1] = phi * (0.5f * ORC_INV_PI);
+            v->roughness = s->mat_kind[v->material] == 1 ? s->mat_roughness[v->material] : 1.0f;
+            float em[3];
+            hit_emission(s, &L, q->d, tri, hit_t[i], q->prev_pdf, em);
+            if (fmaxf3(em) > 0.0f)
+                for (int a = 0; a < 3; ++a)
+                    v->emit[a] = (double)(q->w[a] * em[a]);
+            if (depth == 1)
+                memcpy(normals + 3 * q->pixel, v->n_s, sizeof v->n_s);
+        }
+        for (j = 0; j < ns; ++j)
+            for (int a = 0; a < 3; ++a) {
+                vd[j].s[a] = vd[j].emit[a];
+                frame[3 * vd[j].pixel + a] += vd[j].emit[a];
+            }
+        if (depth == B)
+            break;
+
+        /* the RRS decision block (:363-425) */
+        const orc_strategy st = assignment[depth - 1];
+        float *p01 = (float *)malloc(sizeof(float) * 3 * (ns + 1)), *wo01 = (float *)malloc(sizeof(float) * 2 * (ns + 1));
+        float *rough = (float *)malloc(sizeof(float) * (ns + 1)), *wgt = (float *)malloc(sizeof(float) * 3 * (ns + 1));
+        float *ipx = (float *)malloc(sizeof(float) * 3 * (ns + 1));
+        uint64_t *keys = (uint64_t *)malloc(sizeof(uint64_t) * (ns + 1));
+        for (j = 0; j < ns; ++j) {
+            memcpy(p01 + 3 * j, vd[j].p01, 12);
+            memcpy(wo01 + 2 * j, vd[j].wo01, 8);
+            rough[j] = vd[j].roughness;
+            memcpy(wgt + 3 * j, vd[j].weight, 12);
+            memcpy(ipx + 3 * j, i_acc + 3 * vd[j].pixel, 12);
+            keys[j] = vd[j].key;
+        }
+        orc_vertices ov = {p01, wo01, rough, wgt, ipx, keys};
+        orc_stage_params sp;
+        memset(&sp, 0, sizeof sp);
+        sp.depth = (uint32_t)depth;
+        sp.n_pixels = npx;
+        sp.capacity = cap;
+        sp.kind = st.kind;
+        sp.fixed_value = st.fixed_value;
+        sp.gain = rc->enabled ? rc->f_rate * rc->alpha : 1.0f;
+        sp.eps_div = eps_div;
+        sp.seed = cfg->seed;
+        sp.threads = 1;
+        orc_stage_out so;
+        memset(&so, 0, sizeof so);
+        const size_t nn = ns + 1;
+        so.q_orig = (float *)malloc(sizeof(float) * nn);
+        so.q_norm = (float *)malloc(sizeof(float) * nn);
+        so.q_real = (float *)malloc(sizeof(float) * nn);
+        so.u = (float *)malloc(sizeof(float) * nn);
+        so.k = (int *)malloc(sizeof(int) * nn);
+        so.offset = (uint32_t *)malloc(sizeof(uint32_t) * nn);
+        so.decided = (uint8_t *)malloc(nn);
+        so.slots = (uint32_t *)malloc(sizeof(uint32_t) * 2 * (size_t)cap);
+        orc_rrs_stage(&ov, ns, &sp, nets, &so);
+        rep->nonfinite_drops += so.nonfinite;
+        if (so.dropped > 0) {
+            rc->overflow_events += 1;
+            rc->alpha *= (1.0f - rc->eps);
+            rep->overflow_events += 1;
+            rep->bias_drop_events += so.dropped;
+        }
+        for (j = 0; j < ns; ++j) {
+            vd[j].q_norm = so.q_norm[j];
+            vd[j].q_real = so.q_real[j];
+            vd[j].decided = so.decided[j];
+        }
+        /* children (:413-482) */
+        memset(used, 0, so.spawned);
+        for (j = 0; j < ns; ++j) {
+            orc_vrec *v = &vd[j];
+            const uint32_t off = so.offset[j];
+            const uint32_t rem = so.spawned - (so.spawned < off ? so.spawned : off);
+            const uint32_t kept = (uint32_t)so.k[j] < rem ? (uint32_t)so.k[j] : rem;
+            const int kind = s->mat_kind[v->material];
+            const float *alb = s->mat_albedo + 3 * v->material;
+            const float mrough = s->mat_roughness[v->material];
+            const float qr = v->q_real;
+            for (uint32_t c = 0; c < kept; ++c) {
+                const uint64_t ck = orc_child_path_key(v->key, c);
+                float pick, l1, l2, b1, b2, dummy;
+                orc_path_floats2(cfg->seed, ck, (uint32_t)depth, 0x33, &pick, &dummy);
+                orc_path_floats2(cfg->seed, ck, (uint32_t)depth, 0x44, &l1, &l2);
+                /* sample_nee (:155-184) over Scene::sample_light (scene.cpp:66-82) */
+                if (L.n > 0) {
+                    uint32_t li = (uint32_t)(pick * (float)L.n);
+                    if (li > L.n - 1)
+                        li = L.n - 1;
+                    const uint32_t lt = L.tris[li];
+                    const float su = sqrtf(l1);
+                    const float bu = 1.0f - su, bv = l2 * su;
+                    const float *q0 = s->pos + 3 * s->idx[3 * lt], *q1 = s->pos + 3 * s->idx[3 * lt + 1],
+                                *q2 = s->pos + 3 * s->idx[3 * lt + 2];
+                    float lp[3], ln[3], wl[3];
+                    for (int a = 0; a < 3; ++a)
+                        lp[a] = ((1.0f - bu - bv) * q0[a] + bu * q1[a]) + bv * q2[a];
+                    face_normal(s, lt, ln);
+                    const float *le = s->mat_emission + 3 * s->mat_of_tri[lt];
+                    const float pdf_area = 1.0f / ((float)L.n * L.areas[li]);
+                    if (pdf_area > 0.0f) {
+                        v3_sub(lp, v->p, wl);
+                        const float dist2 = v3_dot(wl, wl);
+                        if (dist2 > 1e-12f) {
+                            const float dist = sqrtf(dist2);
+                            for (int a = 0; a < 3; ++a)
+                                wl[a] = wl[a] / dist;
+                            const float cos_l = fabsf(v3_dot(ln, wl));
+                            if (cos_l > 1e-7f) {
+                                float f[3];
+                                bsdf_eval(kind, alb, mrough, v->n_s, v->wo, wl, f);
+                                const float cos_v = v3_dot(v->n_s, wl);
+                                if (!(cos_v <= 0.0f || fmaxf3(f) <= 0.0f || fmaxf3(le) <= 0.0f)) {
+                                    const float scale = cos_v * cos_l / (dist2 * pdf_area);
+                                    const float pdf_l = pdf_area * dist2 / stdmaxf(cos_l, 1e-8f);
+                                    const float pdf_b = bsdf_pdf(kind, mrough, v->n_s, v->wo, wl);
+                                    rep->shadow_rays += 1;
+                                    if (!occluded_brute(s, v->p, wl, dist * (1.0f - 1e-3f))) {
+                                        const float mis = mis_power2(pdf_l, pdf_b);
+                                        for (int a = 0; a < 3; ++a) {
+                                            const float wq = v->weight[a] / qr;
+                                            v->nee[a] += (double)(wq * ((f[a] * le[a]) * scale * mis));
+                                        }
+                                    }
+                                }
+                            }
+                        }
+                    }
+                }
+                orc_path_floats2(cfg->seed, ck, (uint32_t)depth, 0x22, &b1, &b2);
+                float wi[3], pdf, thr[3];
+                if (!orc_bsdf_sample(kind, alb, mrough, v->n_s, v->wo, b1, b2, wi, &pdf, thr))
+                    continue;
+                orc_path_state *ch = &next[off + c];
+                memset(ch, 0, sizeof *ch);
+                for (int a = 0; a < 3; ++a) {
+                    ch->o[a] = v->p[a];
+                    ch->d[a] = wi[a];
+                    ch->w[a] = v->weight[a] * thr[a] / qr;
+                }
+                ch->t_max = INFINITY;
+                if (!(isfinite(ch->w[0]) && isfinite(ch->w[1]) && isfinite(ch->w[2]))) {
+                    rep->nonfinite_drops += 1;
+                    continue;
+                }
+                ch->key = ck;
+                ch->prev_pdf = pdf;
+                ch->rrs = v->rrs * qr;
+                ch->pixel = v->pixel;
+                ch->parent = (int32_t)j;
+                ch->depth = (uint16_t)(depth + 1);
+                used[off + c] = 1;
+            }
+        }
+        for (j = 0; j < ns; ++j)
+            for (int a = 0; a < 3; ++a) {
+                frame[3 * vd[j].pixel + a] += vd[j].nee[a];
+                vd[j].s[a] += vd[j].nee[a];
+            }
+        uint32_t w = 0;
+        for (uint32_t slot = 0; slot < so.spawned; ++slot)
+            if (used[slot])
+                queue[w++] = next[slot];
+        n = w;
+        free(p01); free(wo01); free(rough); free(wgt); free(ipx); free(keys);
+        free(so.q_orig); free(so.q_norm); free(so.q_real); free(so.u); free(so.k); free(so.offset);
+        free(so.decided); free(so.slots);
+    }
+    /* reverse pass (:504-507) */
+    for (int d = B; d >= 2; --d)
+        for (uint32_t j = 0; j < nverts[d]; ++j)
+            if (verts[d][j].parent >= 0)
+                for (int a = 0; a < 3; ++a)
+                    verts[d - 1][verts[d][j].parent].s[a] += verts[d][j].s[a];
+    if (cfg->collect_training && train) { /* :511-544 */
+        const size_t start = *n_train;
+        for (int d = 1; d < B; ++d) {
+            const orc_vrec *vd = verts[d];
+            for (uint32_t j = 0; vd && j < nverts[d]; ++j) {
+                const orc_vrec *v = &vd[j];
+                if (!v->decided)
+                    continue;
+                float lo_[3];
+                for (int a = 0; a < 3; ++a)
+                    lo_[a] = v->weight[a] > 0.0f ? (float)(v->s[a] / (double)v->weight[a]) : 0.0f;
+                if (!(isfinite(lo_[0]) && isfinite(lo_[1]) && isfinite(lo_[2]))) {
+                    rep->nonfinite_drops += 1;
+                    continue;
+                }
+                if (*n_train >= train_cap) {
+                    rc_err = -1;
+                    continue;
+                }
+                orc_train_sample *t = &train[(*n_train)++];
+                memset(t, 0, sizeof *t);
+                memcpy(t->position, v->p01, 12);
+                memcpy(t->omega_o, v->wo01, 8);
+                t->roughness = v->roughness;
+                memcpy(t->t_x, v->weight, 12);
+                memcpy(t->i_pixel, i_acc + 3 * v->pixel, 12);
+                memcpy(t->lo_sample, lo_, 12);
+                t->q_norm = v->q_norm;
+                t->q_real = v->q_real;
+                t->pixel = v->pixel;
+                t->k_i = 1.0f;
+                t->depth = (uint16_t)d;
+            }
+        }
+        orc_train_k_i(train, start, *n_train, npx);
+        rep->train_samples = *n_train - start;
+    }
+    for (int d = 0; d <= B; ++d)
+        free(verts[d]);
+    free(queue); free(next); free(used); free(hit_t); free(hit_tri); free(cls);
+    free(L.tris); free(L.areas); free(L.index_of_tri);
+    return rc_err;
+}

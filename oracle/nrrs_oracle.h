@@ -213,6 +213,42 @@ void orc_render_depth1(const orc_scene *s, uint32_t width, uint32_t height, uint
                        float *ray_o, float *ray_d, float *hit_t, uint32_t *hit_tri, uint8_t *cls, float *p01,
                        float *wo01, float *roughness, uint64_t *path_key);
 
+/* ---- trace_frame: wavefront.cpp:217-551 sequentially, brute-force hits ---- */
+typedef struct {
+    float o[3], d[3], t_max, w[3];
+    uint64_t key;
+    float prev_pdf, rrs;
+    uint32_t pixel;
+    int32_t parent;
+    uint16_t depth, pad16;
+    uint32_t pad;
+} orc_path_state; /* PathState (wavefront.hpp:17-26), 72 bytes */
+typedef struct { int kind; float fixed_value; } orc_strategy;
+typedef struct { float f_rate, alpha, eps; int enabled; uint64_t overflow_events; } orc_rate_control;
+typedef struct {
+    uint32_t width, height;
+    int max_depth;
+    uint32_t capacity;        /* 0 = queue_capacity_for(W*H) */
+    uint64_t seed;
+    uint32_t frame_index;
+    float adrrs_eps_scale;    /* TraceConfig (wavefront.hpp:128-140) */
+    int collect_training;
+    float env[3];             /* Scene::env_emission */
+} orc_trace_cfg;
+typedef struct {
+    uint64_t camera_rays, scatter_rays, shadow_rays, nonfinite_drops, overflow_events, bias_drop_events,
+        train_samples;
+    uint32_t depth_counts[32];
+} orc_frame_report;
+/* One frame into frame[3*npx] (f64, zero on entry) and normals[3*npx]; i_acc is Film::i_acc.
+ * Appends TrainSamples to train[*n_train..train_cap).  Returns 0, or -1 where the reference throws. */
+int orc_trace_frame(const orc_scene *s, const orc_trace_cfg *cfg, const orc_strategy *assignment,
+                    const orc_nets *nets, orc_rate_control *rc, const float *i_acc, double *frame, float *normals,
+                    orc_train_sample *train, size_t train_cap, size_t *n_train, orc_frame_report *rep);
+/* bsdf_sample (bsdf.cpp:85-133) for one material: kind, albedo, roughness */
+int orc_bsdf_sample(int kind, const float albedo[3], float roughness, const float n[3], const float wo[3], float u1,
+                    float u2, float wi[3], float *pdf, float thr[3]);
+
 /* ---- synthetic inputs (generator follows test_networks.cpp:37-51) ---- */
 void orc_gen_vertices(size_t n, uint32_t n_pixels, uint32_t frame, float *p01, float *wo01,
                       float *rough, float *t_x, float *i_pixel, uint64_t *path_key,

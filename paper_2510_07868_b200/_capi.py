@@ -70,6 +70,28 @@ class CameraC(C.Structure):
                 ("vfov_deg", C.c_float)]
 
 
+class TraceConfigC(C.Structure):
+    _fields_ = [("width", C.c_uint32), ("height", C.c_uint32), ("max_depth", C.c_int32),
+                ("queue_capacity", C.c_uint32), ("seed", C.c_uint64), ("frame_index", C.c_uint32),
+                ("adrrs_eps_scale", C.c_float), ("collect_training", C.c_int32)]
+
+
+class RateControlC(C.Structure):
+    _fields_ = [("f_rate", C.c_float), ("alpha", C.c_float), ("eps", C.c_float), ("enabled", C.c_int32),
+                ("overflow_events", C.c_uint64)]
+
+
+class FrameReportC(C.Structure):
+    _fields_ = [("camera_rays", C.c_uint64), ("scatter_rays", C.c_uint64), ("shadow_rays", C.c_uint64),
+                ("nonfinite_drops", C.c_uint64), ("overflow_events", C.c_uint64), ("bias_drop_events", C.c_uint64),
+                ("train_samples", C.c_uint64), ("depth_counts", C.c_uint32 * 32)]
+
+
+class FilmDevC(C.Structure):
+    _fields_ = [("sum", C.c_void_p), ("samples", C.c_void_p), ("i_cur", C.c_void_p), ("i_acc", C.c_void_p),
+                ("normal", C.c_void_p)]
+
+
 # (name, restype, argtypes) for every entry point declared in include/nrrs_gpu.h
 _P = C.c_void_p
 SIGNATURES = [
@@ -103,6 +125,15 @@ SIGNATURES = [
     ("nrrs_gpu_camera_rays", C.c_int, [_P, _P, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32, _P, _P, _P]),
     ("nrrs_gpu_intersect", C.c_int, [_P, _P, _P, _P, _P, C.c_uint64, _P, _P, _P, _P]),
     ("nrrs_gpu_render_check", C.c_int, [_P]),
+    ("nrrs_gpu_scene_light_count", C.c_uint32, [_P]),
+    ("nrrs_gpu_scene_set_env", C.c_int, [_P, C.POINTER(C.c_float)]),
+    ("nrrs_gpu_tracer_create", C.c_int, [_P, C.c_uint32, C.c_int32, C.c_uint32, C.POINTER(_P)]),
+    ("nrrs_gpu_tracer_destroy", C.c_int, [_P]),
+    ("nrrs_gpu_trace_frame", C.c_int, [_P, _P, C.POINTER(TraceConfigC), C.POINTER(StrategyC),
+                                       C.POINTER(RateControlC), C.POINTER(FilmDevC), _P, C.c_uint64,
+                                       C.POINTER(C.c_uint64), C.POINTER(FrameReportC)]),
+    ("nrrs_gpu_tracer_frame_buffer", C.c_int, [_P, C.POINTER(_P)]),
+    ("nrrs_gpu_tracer_vertices", C.c_int, [_P, C.c_int32, C.POINTER(VertexRecSoA), C.POINTER(C.c_uint32)]),
     ("nrrs_gpu_surface_records", C.c_int, [_P, _P, _P, _P, _P, _P, C.c_uint64, _P, _P, _P, _P, _P]),
     ("nrrs_gpu_set_weights", C.c_int, [_P, C.POINTER(NetWeights)]),
     ("nrrs_gpu_rrs_stage", C.c_int, [_P, C.POINTER(VertexSoA), C.c_uint64, C.POINTER(StageParams),

@@ -1083,7 +1083,7 @@ int nrrs_gpu_adam_ema(nrrs_gpu_ctx *ctx, float *d_theta, const float *d_grad, fl
 struct nrrs_scene {
     int device = 0;
     RenderScene dev{};
-    void *bufs[10] = {};
+    void *bufs[13] = {};
 };
 
 namespace {
@@ -1207,6 +1207,30 @@ int nrrs_gpu_scene_create(nrrs_gpu_ctx *ctx, const float *pos, uint32_t n_vert, 
     d.mat_emission = (const float *)up(8, emi.data(), 12ull * n_mats);
     d.n_nodes = (uint32_t)b.nodes.size();
     d.n_tri = n_tri;
+    // Scene::finalize's light list: emissive triangles of positive area (scene.cpp:38-47)
+    std::vector<uint32_t> ltris;
+    std::vector<float> lareas;
+    std::vector<int32_t> lindex(n_tri, -1);
+    for (uint32_t t = 0; t < n_tri; ++t) {
+        const float *p0 = pos + 3ull * idx[3ull * t], *p1 = pos + 3ull * idx[3ull * t + 1],
+                    *p2 = pos + 3ull * idx[3ull * t + 2];
+        const float e1[3] = {p1[0] - p0[0], p1[1] - p0[1], p1[2] - p0[2]};
+        const float e2[3] = {p2[0] - p0[0], p2[1] - p0[1], p2[2] - p0[2]};
+        const float c[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2],
+                            e1[0] * e2[1] - e1[1] * e2[0]};
+        const float area = 0.5f * std::sqrt((c[0] * c[0] + c[1] * c[1]) + c[2] * c[2]);  // triangle_area
+        const float *em = mats[mat_ids[t]].emission;
+        if (std::max(std::max(em[0], em[1]), em[2]) > 0.0f && area > 0.0f) {
+            lindex[t] = (int32_t)ltris.size();
+            ltris.push_back(t);
+            lareas.push_back(area);
+        }
+    }
+    d.light_tris = (const uint32_t *)up(9, ltris.data(), 4ull * ltris.size());
+    d.light_areas = (const float *)up(10, lareas.data(), 4ull * lareas.size());
+    d.light_index = (const int32_t *)up(11, lindex.data(), 4ull * lindex.size());
+    d.n_lights = (uint32_t)ltris.size();
+    d.env[0] = d.env[1] = d.env[2] = 0.0f;
     // Scene::finalize normalization (scene.cpp:23-37)
     float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
     for (uint32_t i = 0; i < n_vert; ++i)
@@ -1272,6 +1296,15 @@ int nrrs_gpu_scene_destroy(nrrs_scene *s) {
 }
 
 uint32_t nrrs_gpu_scene_node_count(const nrrs_scene *s) { return s ? s->dev.n_nodes : 0; }
+uint32_t nrrs_gpu_scene_light_count(const nrrs_scene *s) { return s ? s->dev.n_lights : 0; }
+
+int nrrs_gpu_scene_set_env(nrrs_scene *s, const float env[3]) {
+    if (!s || !env)
+        return NRRS_EINVAL;
+    for (int a = 0; a < 3; ++a)
+        s->dev.env[a] = env[a];
+    return NRRS_OK;
+}
 
 int nrrs_gpu_camera_rays(nrrs_gpu_ctx *ctx, const nrrs_scene *scene, uint32_t width, uint32_t height, uint64_t seed,
                          uint32_t frame, float *d_o, float *d_d, uint64_t *d_keys) {
@@ -1318,6 +1351,316 @@ int nrrs_gpu_surface_records(nrrs_gpu_ctx *ctx, const nrrs_scene *scene, const f
     CK(ctx, launch_surface(scene->dev, d_o, d_d, d_t, d_tri, n, d_class, d_p01, d_wo01, d_roughness, d_material,
                            ctx->num_sms, ctx->stream));
     ctx->launches += 1;
+    return NRRS_OK;
+}
+
+
+// ---- trace_frame on the GPU ----
+}  // extern "C"
+
+struct nrrs_tracer {
+    nrrs_gpu_ctx *ctx = nullptr;
+    uint32_t max_pixels = 0, cap = 0;
+    int max_depth = 0;
+    std::vector<void *> bufs;
+    PathStateDev *queue = nullptr, *next = nullptr;
+    uint8_t *cls = nullptr, *is_surf = nullptr, *used = nullptr;
+    float *hit_t = nullptr;
+    uint32_t *pair = nullptr, *surf = nullptr, *rank = nullptr, *slots = nullptr, *d_ns = nullptr, *d_n = nullptr;
+    double *term = nullptr, *slot_term = nullptr, *frame = nullptr, *d_lum = nullptr;
+    uint64_t *d_train_count = nullptr, *d_train_nonfinite = nullptr;
+    TraceCounters *d_cnt = nullptr;
+    std::vector<VertexRecDev> verts;  // [max_depth + 1], index 0 unused
+    std::vector<uint32_t> nverts;
+};
+
+template <class T>
+static T *tracer_alloc(nrrs_tracer *t, uint64_t count) {
+    void *p = nullptr;
+    if (cudaMalloc(&p, (count ? count : 1) * sizeof(T)) != cudaSuccess)
+        return nullptr;
+    t->bufs.push_back(p);
+    return static_cast<T *>(p);
+}
+
+extern "C" {
+
+int nrrs_gpu_tracer_destroy(nrrs_tracer *t) {
+    if (!t)
+        return NRRS_OK;
+    cudaSetDevice(t->ctx->device);
+    cudaStreamSynchronize(t->ctx->stream);
+    for (void *p : t->bufs)
+        cudaFree(p);
+    delete t;
+    return NRRS_OK;
+}
+
+int nrrs_gpu_tracer_create(nrrs_gpu_ctx *ctx, uint32_t max_pixels, int32_t max_depth, uint32_t capacity,
+                           nrrs_tracer **out) {
+    if (!ctx || !out || max_pixels == 0 || max_depth < 1 || max_depth > 32)
+        return NRRS_EINVAL;
+    *out = nullptr;
+    const uint32_t cap = capacity ? capacity : nrrs_queue_capacity_for(max_pixels);
+    if (cap < max_pixels)
+        return fail(ctx, NRRS_EINVAL, "trace_frame: queue capacity below the pixel count");
+    CK(ctx, cudaSetDevice(ctx->device));
+    auto *t = new nrrs_tracer();
+    t->ctx = ctx;
+    t->max_pixels = max_pixels;
+    t->cap = cap;
+    t->max_depth = max_depth;
+    bool ok = (t->queue = tracer_alloc<PathStateDev>(t, cap)) && (t->next = tracer_alloc<PathStateDev>(t, cap)) &&
+              (t->cls = tracer_alloc<uint8_t>(t, cap)) && (t->is_surf = tracer_alloc<uint8_t>(t, cap)) &&
+              (t->used = tracer_alloc<uint8_t>(t, cap)) && (t->hit_t = tracer_alloc<float>(t, cap)) &&
+              (t->pair = tracer_alloc<uint32_t>(t, 2ull * cap)) && (t->surf = tracer_alloc<uint32_t>(t, 2ull * cap)) &&
+              (t->rank = tracer_alloc<uint32_t>(t, cap)) && (t->slots = tracer_alloc<uint32_t>(t, 2ull * cap)) &&
+              (t->d_ns = tracer_alloc<uint32_t>(t, 1)) && (t->d_n = tracer_alloc<uint32_t>(t, 1)) &&
+              (t->term = tracer_alloc<double>(t, 3ull * cap)) && (t->slot_term = tracer_alloc<double>(t, 3ull * cap)) &&
+              (t->frame = tracer_alloc<double>(t, 3ull * max_pixels)) && (t->d_lum = tracer_alloc<double>(t, 1)) &&
+              (t->d_train_count = tracer_alloc<uint64_t>(t, 2)) && (t->d_train_nonfinite = tracer_alloc<uint64_t>(t, 1)) &&
+              (t->d_cnt = tracer_alloc<TraceCounters>(t, 1));
+    t->verts.assign((size_t)max_depth + 1, VertexRecDev{});
+    t->nverts.assign((size_t)max_depth + 1, 0u);
+    for (int d = 1; ok && d <= max_depth; ++d) {
+        VertexRecDev &v = t->verts[(size_t)d];
+        ok = (v.p = tracer_alloc<float>(t, 3ull * cap)) && (v.n_s = tracer_alloc<float>(t, 3ull * cap)) &&
+             (v.wo = tracer_alloc<float>(t, 3ull * cap)) && (v.weight = tracer_alloc<float>(t, 3ull * cap)) &&
+             (v.p01 = tracer_alloc<float>(t, 3ull * cap)) && (v.wo01 = tracer_alloc<float>(t, 2ull * cap)) &&
+             (v.rough = tracer_alloc<float>(t, cap)) && (v.material = tracer_alloc<uint32_t>(t, cap)) &&
+             (v.pixel = tracer_alloc<uint32_t>(t, cap)) && (v.parent = tracer_alloc<int32_t>(t, cap)) &&
+             (v.key = tracer_alloc<uint64_t>(t, cap)) && (v.rrs = tracer_alloc<float>(t, cap)) &&
+             (v.q_norm = tracer_alloc<float>(t, cap)) && (v.q_real = tracer_alloc<float>(t, cap)) &&
+             (v.decided = tracer_alloc<uint8_t>(t, cap)) && (v.k = tracer_alloc<int32_t>(t, cap)) &&
+             (v.offset = tracer_alloc<uint32_t>(t, cap)) && (v.s = tracer_alloc<double>(t, 3ull * cap));
+    }
+    if (!ok) {
+        nrrs_gpu_tracer_destroy(t);
+        return fail(ctx, NRRS_ECUDA, "tracer: out of device memory (%u pixels, depth %d)", max_pixels, max_depth);
+    }
+    *out = t;
+    return NRRS_OK;
+}
+
+int nrrs_gpu_trace_frame(nrrs_tracer *t, const nrrs_scene *scene, const nrrs_trace_config *cfg,
+                         const nrrs_strategy *assignment, nrrs_rate_control *rc, const nrrs_film_dev *film,
+                         nrrs_train_sample *d_train, uint64_t train_capacity, uint64_t *h_train_count,
+                         nrrs_frame_report *report) {
+    if (!t || !scene || !cfg || !assignment || !rc || !film || !report)
+        return NRRS_EINVAL;
+    nrrs_gpu_ctx *ctx = t->ctx;
+    const int B = cfg->max_depth;
+    if (B < 1)
+        return fail(ctx, NRRS_EINVAL, "trace_frame: max_depth must be at least 1");
+    if (B > t->max_depth)
+        return fail(ctx, NRRS_ESIZE, "trace_frame: max_depth %d above the tracer's %d", B, t->max_depth);
+    const uint64_t npx64 = (uint64_t)cfg->width * cfg->height;
+    if (npx64 == 0)
+        return fail(ctx, NRRS_EINVAL, "trace_frame: film has no pixels");
+    if (npx64 > t->max_pixels)
+        return fail(ctx, NRRS_ESIZE, "trace_frame: %llu pixels above the tracer's %u", (unsigned long long)npx64,
+                    t->max_pixels);
+    const uint32_t npx = (uint32_t)npx64;
+    const uint32_t cap = cfg->queue_capacity ? cfg->queue_capacity : nrrs_queue_capacity_for(npx);
+    if (cap < npx)
+        return fail(ctx, NRRS_EINVAL, "trace_frame: queue capacity below the pixel count");
+    if (cap > t->cap)
+        return fail(ctx, NRRS_ESIZE, "trace_frame: queue capacity %u above the tracer's %u", cap, t->cap);
+    for (int d = 2; d < B; ++d) {  // check_context (wavefront.cpp:70-78)
+        const int32_t k = assignment[d - 1].kind;
+        if (k == NRRS_ADRRS_TREE)
+            return fail(ctx, NRRS_EINVAL, "trace_frame: adrrs-tree strategy needs an octree cache");
+        if ((k == NRRS_ADRRS_NN || k == NRRS_NRRS || k == NRRS_AID_NRRS) && !ctx->has_weights)
+            return fail(ctx, NRRS_EINVAL, "trace_frame: neural strategy needs networks");
+    }
+    if (!film->sum || !film->samples || !film->i_cur || !film->i_acc || !film->normal)
+        return fail(ctx, NRRS_EINVAL, "trace_frame: every film buffer is required");
+    if (cfg->collect_training && (!d_train || !h_train_count))
+        return fail(ctx, NRRS_EINVAL, "trace_frame: training output requires a sample buffer and count");
+    CK(ctx, cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    RenderScene sc = scene->dev;
+    sc.aspect = (float)cfg->width / (float)cfg->height;  // Camera::generate_ray's aspect (wavefront.cpp:265-266)
+    const uint64_t mixed = h_mix_bits(cfg->seed);
+    std::memset(report, 0, sizeof *report);
+    int rc_ = 0;
+
+    // ADRRS division guard (wavefront.cpp:238-243)
+    rc_ = nrrs_gpu_film_luminance_sum(ctx, film->i_acc, npx, t->d_lum);
+    if (rc_)
+        return rc_;
+    double lum = 0.0;
+    CK(ctx, cudaMemcpyAsync(&lum, t->d_lum, sizeof lum, cudaMemcpyDeviceToHost, st));
+    CK(ctx, cudaMemsetAsync(t->frame, 0, 24ull * npx, st));
+    CK(ctx, cudaMemsetAsync(film->normal, 0, 12ull * npx, st));
+    CK(ctx, cudaMemsetAsync(t->d_cnt, 0, sizeof(TraceCounters), st));
+    CK(ctx, cudaMemsetAsync(ctx->d_misc + 13, 0, sizeof(uint32_t), st));
+    CK(ctx, cudaStreamSynchronize(st));
+    const float eps_div = cfg->adrrs_eps_scale * (float)(lum / (double)npx);
+
+    CK(ctx, launch_trace_camera(sc, cfg->width, cfg->height, mixed, cfg->frame_index, t->queue, ctx->num_sms, st));
+    ctx->launches += 1;
+    report->camera_rays = npx;
+    uint32_t n = npx;
+    std::fill(t->nverts.begin(), t->nverts.end(), 0u);
+    for (int depth = 1; depth <= B; ++depth) {
+        if (n == 0)
+            break;
+        report->depth_counts[depth - 1] = n;
+        if (depth >= 2)
+            report->scatter_rays += n;
+        CK(ctx, launch_trace_shade(sc, t->queue, n, (uint32_t)depth, t->cls, t->is_surf, t->hit_t, t->pair, t->term,
+                                   film->normal, ctx->d_misc + 13, ctx->num_sms, st));
+        uint32_t ns = 0;
+        rc_ = nrrs_gpu_compact(ctx, t->pair, t->is_surf, n, 2, t->surf, t->d_ns, &ns);  // dispatch order (:125-138)
+        if (rc_)
+            return rc_;
+        VertexRecDev &vd = t->verts[(size_t)depth];
+        t->nverts[(size_t)depth] = ns;
+        CK(ctx, launch_trace_records(sc, t->queue, t->surf, t->d_ns, ns, t->hit_t, t->rank, vd, (uint32_t)depth,
+                                     film->normal, ctx->num_sms, st));
+        ctx->launches += 2;
+        if (depth >= 2) {
+            CK(ctx, launch_trace_fold_parent(t->queue, n, t->cls, t->term, t->verts[(size_t)depth - 1].s, st));
+            ctx->launches += 1;
+        }
+        if (depth == B) {  // terminal vertices: emission only (:358-361)
+            CK(ctx, launch_trace_fold_frame(t->queue, n, t->cls, t->term, t->rank, vd, 0, nullptr, t->frame, st));
+            ctx->launches += 1;
+            n = 0;
+            break;
+        }
+        // the RRS decision block (:363-425) through the stage
+        nrrs_vertex_soa soa{};
+        soa.p01 = vd.p01;
+        soa.wo01 = vd.wo01;
+        soa.roughness = vd.rough;
+        soa.weight = vd.weight;
+        soa.path_key = vd.key;
+        soa.pixel = vd.pixel;
+        soa.i_acc = film->i_acc;
+        nrrs_stage_params sp{};
+        sp.depth = (uint32_t)depth;
+        sp.n_pixels = npx;
+        sp.capacity = cap;
+        sp.strategy = assignment[depth - 1];
+        sp.gain = rc->enabled ? rc->f_rate * rc->alpha : 1.0f;  // RateControl::gain (rrs.hpp:30)
+        sp.eps_div = eps_div;
+        sp.seed = cfg->seed;
+        nrrs_stage_out so{};
+        so.q_norm = vd.q_norm;
+        so.q_real = vd.q_real;
+        so.slots = t->slots;
+        so.k = vd.k;
+        so.offset = vd.offset;
+        so.decided = vd.decided;
+        nrrs_stage_result res{};
+        rc_ = nrrs_gpu_rrs_stage(ctx, &soa, ns, &sp, &so, &res);
+        if (rc_)
+            return rc_;
+        report->nonfinite_drops += res.nonfinite;
+        if (res.dropped > 0) {  // (:407-411)
+            rc->overflow_events += 1;
+            rc->alpha *= (1.0f - rc->eps);
+            report->overflow_events += 1;
+            report->bias_drop_events += res.dropped;
+        }
+        CK(ctx, launch_trace_scatter(sc, vd, t->slots, res.spawned, (uint32_t)depth, mixed, t->next, t->used,
+                                     t->slot_term, t->d_cnt, ctx->num_sms, st));
+        CK(ctx, launch_trace_fold_frame(t->queue, n, t->cls, t->term, t->rank, vd, res.spawned, t->slot_term,
+                                        t->frame, st));
+        ctx->launches += 2;
+        uint32_t next_n = 0;
+        rc_ = nrrs_gpu_compact(ctx, t->next, t->used, res.spawned, 18, t->queue, t->d_n, &next_n);  // (:488-497)
+        if (rc_)
+            return rc_;
+        n = next_n;
+    }
+    // reverse pass (:502-507)
+    for (int d = B; d >= 2; --d) {
+        const uint32_t nd = t->nverts[(size_t)d];
+        if (nd == 0)
+            continue;
+        rc_ = nrrs_gpu_fold_ordered(ctx, t->verts[(size_t)d - 1].s, t->nverts[(size_t)d - 1],
+                                    t->verts[(size_t)d].parent, t->verts[(size_t)d].s, nd);
+        if (rc_)
+            return rc_;
+    }
+    // TrainSample emission (:509-544)
+    if (cfg->collect_training) {
+        const uint64_t start = *h_train_count;
+        CK(ctx, cudaMemcpyAsync(t->d_train_count, &start, sizeof start, cudaMemcpyHostToDevice, st));
+        CK(ctx, cudaMemsetAsync(t->d_train_nonfinite, 0, sizeof(uint64_t), st));
+        int cur = 0;
+        for (int d = 1; d < B; ++d) {
+            const VertexRecDev &v = t->verts[(size_t)d];
+            nrrs_vertex_rec_soa rs{};
+            rs.p01 = v.p01;
+            rs.wo01 = v.wo01;
+            rs.roughness = v.rough;
+            rs.weight = v.weight;
+            rs.pixel = v.pixel;
+            rs.q_norm = v.q_norm;
+            rs.q_real = v.q_real;
+            rs.decided = v.decided;
+            rs.s = v.s;
+            rc_ = nrrs_gpu_emit_train(ctx, (uint32_t)d, &rs, t->nverts[(size_t)d], film->i_acc, d_train,
+                                      train_capacity, t->d_train_count + cur, t->d_train_count + (1 - cur),
+                                      t->d_train_nonfinite);
+            if (rc_)
+                return rc_;
+            cur = 1 - cur;
+        }
+        rc_ = nrrs_gpu_train_k_i(ctx, d_train, start, t->d_train_count + cur, train_capacity, npx);
+        if (rc_)
+            return rc_;
+        uint64_t end = 0, nf = 0;
+        CK(ctx, cudaMemcpyAsync(&end, t->d_train_count + cur, sizeof end, cudaMemcpyDeviceToHost, st));
+        CK(ctx, cudaMemcpyAsync(&nf, t->d_train_nonfinite, sizeof nf, cudaMemcpyDeviceToHost, st));
+        CK(ctx, cudaStreamSynchronize(st));
+        if (end > train_capacity)
+            return fail(ctx, NRRS_ESIZE, "trace_frame: %llu training samples above the capacity %llu",
+                        (unsigned long long)end, (unsigned long long)train_capacity);
+        report->nonfinite_drops += nf;
+        report->train_samples = end - start;
+        *h_train_count = end;
+    }
+    rc_ = nrrs_gpu_film_add_frame(ctx, film->sum, film->samples, film->i_cur, t->frame, npx);  // (:548)
+    if (rc_)
+        return rc_;
+    TraceCounters c{};
+    uint32_t err = 0;
+    CK(ctx, cudaMemcpyAsync(&c, t->d_cnt, sizeof c, cudaMemcpyDeviceToHost, st));
+    CK(ctx, cudaMemcpyAsync(&err, ctx->d_misc + 13, sizeof err, cudaMemcpyDeviceToHost, st));
+    CK(ctx, cudaStreamSynchronize(st));
+    report->shadow_rays = c.shadow_rays;
+    report->nonfinite_drops += c.nonfinite;
+    if (err)
+        return fail(ctx, NRRS_EINVAL, "Bvh::intersect: degenerate ray direction");
+    return NRRS_OK;
+}
+
+int nrrs_gpu_tracer_frame_buffer(const nrrs_tracer *t, const double **d_frame) {
+    if (!t || !d_frame)
+        return NRRS_EINVAL;
+    *d_frame = t->frame;
+    return NRRS_OK;
+}
+
+int nrrs_gpu_tracer_vertices(const nrrs_tracer *t, int32_t depth, nrrs_vertex_rec_soa *out, uint32_t *count) {
+    if (!t || !out || !count || depth < 1 || depth > t->max_depth)
+        return NRRS_EINVAL;
+    const VertexRecDev &v = t->verts[(size_t)depth];
+    out->p01 = v.p01;
+    out->wo01 = v.wo01;
+    out->roughness = v.rough;
+    out->weight = v.weight;
+    out->pixel = v.pixel;
+    out->q_norm = v.q_norm;
+    out->q_real = v.q_real;
+    out->decided = v.decided;
+    out->s = v.s;
+    *count = t->nverts[(size_t)depth];
     return NRRS_OK;
 }
 

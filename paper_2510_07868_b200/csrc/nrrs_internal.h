@@ -257,7 +257,55 @@ struct RenderScene {
     const float *mat_albedo, *mat_roughness, *mat_emission;
     float norm_offset[3], norm_scale;
     float cam_pos[3], cam_fwd[3], cam_right[3], cam_up[3], tan_half, aspect;
+    // Scene::finalize's light list (scene.cpp:38-47) and env_emission
+    const uint32_t *light_tris;
+    const float *light_areas;
+    const int32_t *light_index;  // [n_tri], -1 = not a light
+    uint32_t n_lights;
+    float env[3];
 };
+// PathState (wavefront.hpp:17-26), 72 bytes = 18 words (compact_kernel<18>)
+struct PathStateDev {
+    float o[3], d[3], t_max, w[3];
+    uint64_t key;
+    float prev_pdf, rrs;
+    uint32_t pixel;
+    int32_t parent;
+    uint16_t depth, pad16;
+    uint32_t pad;
+};
+static_assert(sizeof(PathStateDev) == 72, "PathState is 72 bytes");
+// VertexRec (wavefront.cpp:46-65) of one depth, SoA; s starts as the emission term
+struct VertexRecDev {
+    float *p, *n_s, *wo, *weight, *p01, *wo01, *rough;
+    uint32_t *material, *pixel;
+    int32_t *parent;
+    uint64_t *key;
+    float *rrs, *q_norm, *q_real;
+    uint8_t *decided;
+    int32_t *k;
+    uint32_t *offset;
+    double *s;
+};
+struct TraceCounters {
+    unsigned long long shadow_rays, nonfinite;
+};
+cudaError_t launch_trace_camera(const RenderScene &s, uint32_t width, uint32_t height, uint64_t mixed_seed,
+                                uint32_t frame, PathStateDev *q, int num_sms, cudaStream_t stream);
+cudaError_t launch_trace_shade(const RenderScene &s, const PathStateDev *q, uint32_t n, uint32_t depth,
+                               uint8_t *cls, uint8_t *is_surf, float *hit_t, uint32_t *pair, double *term,
+                               float *normals, uint32_t *err, int num_sms, cudaStream_t stream);
+cudaError_t launch_trace_records(const RenderScene &s, const PathStateDev *q, const uint32_t *surf, const uint32_t *ns,
+                                 uint32_t n_max, const float *hit_t, uint32_t *rank, VertexRecDev v, uint32_t depth,
+                                 float *normals, int num_sms, cudaStream_t stream);
+cudaError_t launch_trace_scatter(const RenderScene &s, VertexRecDev v, const uint32_t *slots, uint32_t spawned,
+                                 uint32_t depth, uint64_t mixed_seed, PathStateDev *next, uint8_t *used,
+                                 double *slot_term, TraceCounters *cnt, int num_sms, cudaStream_t stream);
+cudaError_t launch_trace_fold_frame(const PathStateDev *q, uint32_t n, const uint8_t *cls, const double *term,
+                                    const uint32_t *rank, VertexRecDev v, uint32_t spawned, const double *slot_term,
+                                    double *frame, cudaStream_t stream);
+cudaError_t launch_trace_fold_parent(const PathStateDev *q, uint32_t n, const uint8_t *cls, const double *term,
+                                     double *up_s, cudaStream_t stream);
 cudaError_t launch_camera(const RenderScene &s, uint32_t width, uint32_t height, uint64_t mixed_seed, uint32_t frame,
                           float *o, float *d, uint64_t *keys, int num_sms, cudaStream_t stream);
 cudaError_t launch_intersect(const RenderScene &s, const float *o, const float *d, const float *tmax, uint64_t n,

@@ -103,6 +103,7 @@ class GpuFilm:
         self.samples = torch.zeros(n, dtype=torch.int32, device=dev)
         self.i_cur = torch.zeros((n, 3), dtype=torch.float32, device=dev)
         self.i_acc = torch.zeros((n, 3), dtype=torch.float32, device=dev)
+        self.normal = torch.zeros((n, 3), dtype=torch.float32, device=dev)
 
     def pixel_count(self) -> int:
         return self.width * self.height

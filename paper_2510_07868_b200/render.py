@@ -53,6 +53,7 @@ class SceneDesc:
     material_ids: List[int] = field(default_factory=list)
     materials: List[Material] = field(default_factory=list)
     camera: Camera = field(default_factory=Camera)
+    env_emission: Sequence[float] = (0.0, 0.0, 0.0)
 
     def add_quad(self, corner, e1, e2, material_id: int) -> None:
         """add_quad (scene.cpp:98-109): float32 corner + e1 + e2, two triangles."""
@@ -161,6 +162,12 @@ class GpuScene:
             self.ctx.handle, pos.ctypes.data, pos.shape[0], idx.ctypes.data, self.n_tri, mid.ctypes.data, mats,
             len(desc.materials), C.byref(cam), C.byref(h)))
         self.handle = h
+        env = (C.c_float * 3)(*[float(np.float32(x)) for x in desc.env_emission])
+        _capi.check(self.ctx.handle, self.ctx.lib.nrrs_gpu_scene_set_env(self.handle, env))
+
+    @property
+    def light_count(self) -> int:
+        return int(self.ctx.lib.nrrs_gpu_scene_light_count(self.handle))
 
     @property
     def node_count(self) -> int:
@@ -232,5 +239,80 @@ class GpuScene:
             pass
 
 
-__all__ = ["Material", "Camera", "SceneDesc", "GpuScene", "make_cornell_scene", "make_caustic_scene",
+@dataclass
+class TraceConfig:
+    """TraceConfig (wavefront.hpp:128-140): the fields trace_frame reads."""
+    max_depth: int = 8
+    queue_capacity: int = 0
+    seed: int = 0
+    frame_index: int = 0
+    adrrs_eps_scale: float = 1e-4
+    collect_training: bool = False
+
+
+@dataclass
+class FrameReport:
+    """FrameReport (wavefront.hpp:175-186)."""
+    camera_rays: int = 0
+    scatter_rays: int = 0
+    shadow_rays: int = 0
+    nonfinite_drops: int = 0
+    overflow_events: int = 0
+    bias_drop_events: int = 0
+    train_samples: int = 0
+    depth_counts: List[int] = field(default_factory=list)
+
+
+class Tracer:
+    """trace_frame on one GPU (wavefront.cpp:217-551) through nrrs_gpu_trace_frame: device
+    queues and per-depth vertex records sized for films up to max_pixels."""
+
+    def __init__(self, scene: GpuScene, max_pixels: int, max_depth: int, capacity: int = 0):
+        self.scene = scene
+        self.ctx = scene.ctx
+        self.max_depth = int(max_depth)
+        h = C.c_void_p()
+        _capi.check(self.ctx.handle, self.ctx.lib.nrrs_gpu_tracer_create(self.ctx.handle, int(max_pixels),
+                                                                         self.max_depth, int(capacity), C.byref(h)))
+        self.handle = h
+
+    def trace_frame(self, assignment, cfg: TraceConfig, rc, film, train: Optional[torch.Tensor] = None,
+                    train_count: int = 0):
+        """Renders one frame into `film` (a film.GpuFilm); returns (FrameReport, train_count).
+        `assignment` holds one rrs.Strategy per depth; `rc` is an rrs.RateControl (updated)."""
+        from . import rrs as _rrs
+        if len(assignment) != cfg.max_depth:
+            raise RuntimeError("trace_frame: assignment must have one entry per depth")
+        self.ctx.bind_stream()
+        strat = (_capi.StrategyC * len(assignment))(*[s.c() for s in assignment])
+        c = _capi.TraceConfigC(film.width, film.height, cfg.max_depth, cfg.queue_capacity, cfg.seed & (2**64 - 1),
+                               cfg.frame_index, float(np.float32(cfg.adrrs_eps_scale)), int(cfg.collect_training))
+        rcc = _capi.RateControlC(rc.f_rate, rc.alpha, rc.eps, int(rc.enabled), rc.overflow_events)
+        fd = _capi.FilmDevC(film.sum.data_ptr(), film.samples.data_ptr(), film.i_cur.data_ptr(),
+                            film.i_acc.data_ptr(), film.normal.data_ptr())
+        rep = _capi.FrameReportC()
+        cnt = C.c_uint64(train_count)
+        cap = 0 if train is None else int(train.numel() * train.element_size() // 80)
+        _capi.check(self.ctx.handle, self.ctx.lib.nrrs_gpu_trace_frame(
+            self.handle, self.scene.handle, C.byref(c), strat, C.byref(rcc), C.byref(fd),
+            train.data_ptr() if train is not None else None, cap, C.byref(cnt), C.byref(rep)))
+        rc.alpha = float(np.float32(rcc.alpha))
+        rc.overflow_events = int(rcc.overflow_events)
+        r = FrameReport(rep.camera_rays, rep.scatter_rays, rep.shadow_rays, rep.nonfinite_drops, rep.overflow_events,
+                        rep.bias_drop_events, rep.train_samples, list(rep.depth_counts[:cfg.max_depth]))
+        return r, int(cnt.value)
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self.ctx.lib.nrrs_gpu_tracer_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+__all__ = ["TraceConfig", "FrameReport", "Tracer", "Material", "Camera", "SceneDesc", "GpuScene", "make_cornell_scene", "make_caustic_scene",
            "make_furnace_scene", "DIFFUSE", "CONDUCTOR", "NO_HIT", "CLASS_MISS", "CLASS_LIGHT", "CLASS_SURFACE"]

@@ -104,6 +104,8 @@ def lib() -> C.CDLL:
             "orc_path_floats2": (None, [u64, u64, u32, u64, p, p]),
             "orc_intersect_brute": (None, [p, p, u32, p, p, f, p, p, p, p]),
             "orc_render_depth1": (None, [p, u32, u32, u64, u32, p, p, p, p, p, p, p, p, p]),
+            "orc_trace_frame": (i, [p, p, p, p, p, p, p, p, p, C.c_size_t, p, p]),
+            "orc_bsdf_sample": (i, [i, p, f, p, p, f, f, p, p, p]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -481,3 +483,74 @@ def random_rays(n: int, seed: int, seq: int, extent: float = 8.0, t_max: bool = 
         if t_max:
             tm[i] = np.float32(2) + np.float32(4) * nf()
     return o, d, tm
+
+
+class OrcTraceCfg(C.Structure):
+    _fields_ = [("width", C.c_uint32), ("height", C.c_uint32), ("max_depth", C.c_int), ("capacity", C.c_uint32),
+                ("seed", C.c_uint64), ("frame_index", C.c_uint32), ("adrrs_eps_scale", C.c_float),
+                ("collect_training", C.c_int), ("env", C.c_float * 3)]
+
+
+class OrcStrategy(C.Structure):
+    _fields_ = [("kind", C.c_int), ("fixed_value", C.c_float)]
+
+
+class OrcRateControl(C.Structure):
+    _fields_ = [("f_rate", C.c_float), ("alpha", C.c_float), ("eps", C.c_float), ("enabled", C.c_int),
+                ("overflow_events", C.c_uint64)]
+
+
+class OrcFrameReport(C.Structure):
+    _fields_ = [("camera_rays", C.c_uint64), ("scatter_rays", C.c_uint64), ("shadow_rays", C.c_uint64),
+                ("nonfinite_drops", C.c_uint64), ("overflow_events", C.c_uint64), ("bias_drop_events", C.c_uint64),
+                ("train_samples", C.c_uint64), ("depth_counts", C.c_uint32 * 32)]
+
+
+def _orc_scene(desc):
+    pos, idx, mid = desc.arrays()
+    keep = {"pos": pos, "idx": idx, "mid": mid,
+            "kind": np.array([m.kind for m in desc.materials], np.int32),
+            "alb": np.array([m.albedo for m in desc.materials], np.float32).reshape(-1),
+            "rough": np.array([m.roughness for m in desc.materials], np.float32),
+            "emi": np.array([m.emission for m in desc.materials], np.float32).reshape(-1)}
+    f3 = lambda v: (C.c_float * 3)(*[float(np.float32(x)) for x in v])
+    cam = desc.camera
+    sc = OrcScene(pos.ctypes.data, idx.ctypes.data, mid.ctypes.data, pos.shape[0], mid.size, keep["kind"].ctypes.data,
+                  keep["alb"].ctypes.data, keep["rough"].ctypes.data, keep["emi"].ctypes.data, f3(cam.position),
+                  f3(cam.look_at), f3(cam.up), float(np.float32(cam.vfov_deg)))
+    return sc, keep
+
+
+def trace_frame(desc, width: int, height: int, assignment, max_depth: int, seed: int = 0, frame_index: int = 0,
+                i_acc: np.ndarray | None = None, rc=None, nets: "OracleNets | None" = None, capacity: int = 0,
+                collect_training: bool = False, adrrs_eps_scale: float = 1e-4, train_cap: int = 0):
+    """orc_trace_frame: the reference's trace_frame run sequentially (brute-force hits).  assignment:
+    list of (kind, fixed_value); rc: dict(f_rate, alpha, eps, enabled) updated in place.  Returns
+    dict(frame [n,3] f64, normals, train (structured array), report)."""
+    sc, keep = _orc_scene(desc)
+    npx = width * height
+    i_acc = np.zeros((npx, 3), np.float32) if i_acc is None else np.ascontiguousarray(i_acc, np.float32)
+    rc = rc if rc is not None else {"f_rate": 0.85, "alpha": 1.0, "eps": 0.01, "enabled": 1, "overflow_events": 0}
+    rcc = OrcRateControl(rc["f_rate"], rc["alpha"], rc["eps"], int(rc["enabled"]), rc.get("overflow_events", 0))
+    cfg = OrcTraceCfg(width, height, max_depth, capacity, seed & (2**64 - 1), frame_index,
+                      float(np.float32(adrrs_eps_scale)), int(collect_training),
+                      (C.c_float * 3)(*[float(np.float32(x)) for x in desc.env_emission]))
+    strat = (OrcStrategy * max_depth)(*[OrcStrategy(int(k), float(v)) for k, v in assignment])
+    frame = np.zeros((npx, 3), np.float64)
+    normals = np.zeros((npx, 3), np.float32)
+    from paper_2510_07868_b200.film import TRAIN_SAMPLE_DTYPE
+    cap = train_cap if train_cap else (npx * 8 if collect_training else 0)
+    train = np.zeros(max(cap, 1), TRAIN_SAMPLE_DTYPE)
+    n_train = C.c_size_t(0)
+    rep = OrcFrameReport()
+    r = lib().orc_trace_frame(C.byref(sc), C.byref(cfg), strat, C.byref(nets.c) if nets is not None else None,
+                              C.byref(rcc), ptr(i_acc), ptr(frame), ptr(normals), ptr(train), cap,
+                              C.byref(n_train), C.byref(rep))
+    if r != 0:
+        raise RuntimeError("orc_trace_frame failed")
+    rc["alpha"] = float(np.float32(rcc.alpha))
+    rc["overflow_events"] = int(rcc.overflow_events)
+    report = {k: int(getattr(rep, k)) for k in ("camera_rays", "scatter_rays", "shadow_rays", "nonfinite_drops",
+                                                 "overflow_events", "bias_drop_events", "train_samples")}
+    report["depth_counts"] = list(rep.depth_counts[:max_depth])
+    return {"frame": frame, "normals": normals, "train": train[:n_train.value], "report": report}

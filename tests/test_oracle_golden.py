@@ -471,3 +471,64 @@ def test_random_soup_bvh_oracle_hits():
     hit = r["tri"] != 0xFFFFFFFF
     assert hit.any() and (r["t"][hit] > 1e-4).all() and np.isinf(r["t"][~hit]).all()
     assert ((r["u"][hit] >= 0) & (r["v"][hit] >= 0) & (r["u"][hit] + r["v"][hit] <= 1)).all()
+
+
+@pytest.mark.parametrize("B", [1, 3, 5])
+def test_oracle_trace_frame_furnace(B):
+    """Closed furnace, fixed:1: every path reaches depth B (test_harness.cpp:326-352 ray accounting)
+    and the image mean follows Le (1 - a^B) / (1 - a) (scene.cpp:229-230)."""
+    from paper_2510_07868_b200 import render
+    desc = render.make_furnace_scene()
+    w = h = 24
+    r = orc.trace_frame(desc, w, h, [(0, 1.0)] * B, B, seed=9)
+    rep = r["report"]
+    assert rep["depth_counts"] == [w * h] * B
+    assert rep["camera_rays"] + rep["scatter_rays"] == w * h * B
+    assert rep["overflow_events"] == 0 and rep["bias_drop_events"] == 0
+    expect = 0.5 * (1 - 0.7 ** B) / 0.3
+    assert (r["frame"] > 0).all()
+    np.testing.assert_allclose(r["frame"].mean(0), expect, rtol=0.02 if B > 1 else 1e-6)
+
+
+def test_oracle_trace_frame_training_and_rate_control():
+    """Training collection (wavefront.cpp:511-544): k_i counts per pixel, depths < B, finite targets;
+    a capacity of W*H with fixed:2 forces plan_spawns clipping and one alpha decay per overflow."""
+    from paper_2510_07868_b200 import render
+    desc = render.make_cornell_scene()
+    w, h = 24, 20
+    r = orc.trace_frame(desc, w, h, [(0, 1.0), (1, 1.0), (1, 1.0), (1, 1.0)], 4, seed=1, collect_training=True)
+    t = r["train"]
+    assert len(t) == r["report"]["train_samples"] > 0
+    assert t["depth"].max() < 4 and np.isfinite(t["lo_sample"]).all()
+    counts = np.bincount(t["pixel"], minlength=w * h)
+    np.testing.assert_array_equal(t["k_i"], counts[t["pixel"]].astype(np.float32))
+    rc = {"f_rate": 0.85, "alpha": 1.0, "eps": 0.01, "enabled": 1, "overflow_events": 0}
+    r = orc.trace_frame(desc, w, h, [(0, 1.0), (0, 2.0), (1, 1.0), (1, 1.0)], 4, seed=1, rc=rc, capacity=w * h)
+    assert r["report"]["overflow_events"] >= 1 and r["report"]["bias_drop_events"] > 0
+    alpha = np.float32(1.0)
+    for _ in range(r["report"]["overflow_events"]):  # RateControl::note_overflow in float (rrs.hpp:32-35)
+        alpha = np.float32(alpha * (np.float32(1.0) - np.float32(0.01)))
+    assert rc["alpha"] == alpha < 1.0
+
+
+def test_oracle_bsdf_sample_identities():
+    """bsdf.cpp:85-133: diffuse throughput is the albedo with pdf cos/pi; conductor samples stay in
+    the upper hemisphere (test_geometry.cpp diffuse / conductor consistency cases)."""
+    L = orc.lib()
+    n = np.array([0, 0, 1], np.float32)
+    wo = np.array([0.3, -0.2, 0.9], np.float32)
+    wo /= np.float32(np.sqrt(np.float32((wo * wo).sum())))
+    alb = np.array([0.6, 0.4, 0.2], np.float32)
+    wi, thr = np.zeros(3, np.float32), np.zeros(3, np.float32)
+    pdf = C.c_float()
+    g = np.random.default_rng(5)
+    for u1, u2 in g.random((200, 2), dtype=np.float32):
+        ok = L.orc_bsdf_sample(0, orc.ptr(alb), 0.5, orc.ptr(n), orc.ptr(wo), float(u1), float(u2), orc.ptr(wi),
+                               C.byref(pdf), orc.ptr(thr))
+        if ok:
+            assert np.array_equal(thr, alb)
+            assert abs(pdf.value - wi[2] / np.pi) < 1e-6
+        ok = L.orc_bsdf_sample(1, orc.ptr(alb), 0.15, orc.ptr(n), orc.ptr(wo), float(u1), float(u2), orc.ptr(wi),
+                               C.byref(pdf), orc.ptr(thr))
+        if ok:
+            assert wi[2] > 0 and pdf.value > 0 and np.isfinite(thr).all()
