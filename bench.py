@@ -606,6 +606,59 @@ def main():
                          "step_statnet + step_rrsnet (AID, full phase); wall time incl. the finite-check syncs"}
         tr.close()
 
+    # ---- GPU trace_frame: configs[2] shape C3, AID-NRRS at depths >= 2 on
+    # builtin:cornell 1920x1080, B = 16, the RRS stage inside the full wavefront renderer ----
+    trace = None
+    if world == 1 and not args.no_extra:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import oracle as orc_gen  # CPU port timing only
+        from paper_2510_07868_b200 import render as rnd
+        from paper_2510_07868_b200.film import GpuFilm, SuffixStage
+        from paper_2510_07868_b200.rrs import Strategy as St, StrategyKind as SK
+        tw, th, tb = 1920, 1080, 16
+        kind = SK.AidNrrs if variant == RrsVariant.Aid else SK.Nrrs
+        tst = RrsStage(tw * th, nets, device=local)
+        desc = rnd.make_cornell_scene()
+        tscene = rnd.GpuScene(desc, ctx=tst.ctx)
+        tracer = rnd.Tracer(tscene, tw * th, tb)
+        tfilm = GpuFilm(tw, th, SuffixStage(ctx=tst.ctx))
+        assign = [St()] + [St(kind)] * (tb - 1)
+        trc = RateControl()
+        reps, tts = [], []
+        for f in range(6):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rep_f, _ = tracer.trace_frame(assign, rnd.TraceConfig(max_depth=tb, seed=7, frame_index=f), trc, tfilm)
+            torch.cuda.synchronize()
+            tts.append(time.perf_counter() - t0)
+            reps.append(rep_f)
+            tfilm.roll_acc()
+        tts, reps = tts[2:], reps[2:]  # frames 0-1 warm up (the first roll_acc'd frame pays one-time costs)
+        nverts = statistics.mean(sum(r.depth_counts) for r in reps)
+        rays = statistics.mean(r.camera_rays + r.scatter_rays + r.shadow_rays for r in reps)
+        ms = 1e3 * statistics.median(tts)
+        # the same frame shape through the C port of the reference loop (1 thread, brute-force hits,
+        # a 96x54 crop of the film so the sample stays a few seconds)
+        on = orc_gen.OracleNets(orc_gen.VARIANT_AID if variant == RrsVariant.Aid else orc_gen.VARIANT_NRRS, seed=1,
+                                randomize=True)
+        cw, ch = 96, 54
+        t0 = time.perf_counter()
+        cr = orc_gen.trace_frame(desc, cw, ch, [(0, 1.0)] + [(int(kind), 1.0)] * (tb - 1), tb, seed=7, nets=on)
+        cpu_s = time.perf_counter() - t0
+        trace = {"config": "C3 shape: builtin:cornell 1920x1080, B=16, fixed at depth 1 then "
+                           f"{'aid-nrrs' if kind == SK.AidNrrs else 'nrrs'} (random-init networks), RateControl on",
+                 "ms_per_frame": ms, "path_vertices_per_frame": nverts, "path_vertices_per_s": nverts / (ms / 1e3),
+                 "rays_per_s": rays / (ms / 1e3), "depth_counts": reps[-1].depth_counts,
+                 "shadow_rays": reps[-1].shadow_rays,
+                 "cpu_port": {"sample": f"{cw}x{ch} crop, same scene / depth / strategy, 1 thread",
+                              "path_vertices_per_s": sum(cr["report"]["depth_counts"]) / cpu_s, "cores": 1},
+                 "note": "wall time per frame incl. ~3 host syncs per depth; camera + per-depth shade / compaction "
+                         "/ RRS stage / scatter (NEE + BSDF) / folds, reverse pass, Film::add_frame"}
+        tracer.close()
+        tscene.close()
+        tst.close()
+
     peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}
     hbm = peaks.get("hbm_gbs")
     peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)"
@@ -650,6 +703,8 @@ def main():
         line["suffix_stage"] = suffix
     if train:
         line["statnet_train_step"] = train
+    if trace is not None:
+        line["trace_frame"] = trace
     if world == 1 and rank == 0 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args.variant)
     if rank == 0:
