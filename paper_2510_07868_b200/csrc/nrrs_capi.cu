@@ -1083,7 +1083,7 @@ int nrrs_gpu_adam_ema(nrrs_gpu_ctx *ctx, float *d_theta, const float *d_grad, fl
 struct nrrs_scene {
     int device = 0;
     RenderScene dev{};
-    void *bufs[13] = {};
+    void *bufs[14] = {};
 };
 
 namespace {
@@ -1207,6 +1207,18 @@ int nrrs_gpu_scene_create(nrrs_gpu_ctx *ctx, const float *pos, uint32_t n_vert, 
     d.mat_emission = (const float *)up(8, emi.data(), 12ull * n_mats);
     d.n_nodes = (uint32_t)b.nodes.size();
     d.n_tri = n_tri;
+    std::vector<float> t4(12ull * b.prims.size(), 0.0f);
+    for (size_t k = 0; k < b.prims.size(); ++k) {  // triangle records in BVH prim order
+        const uint32_t t = b.prims[k];
+        const float *p0 = pos + 3ull * idx[3ull * t], *p1 = pos + 3ull * idx[3ull * t + 1],
+                    *p2 = pos + 3ull * idx[3ull * t + 2];
+        float *r = t4.data() + 12 * k;
+        r[0] = p0[0]; r[1] = p0[1]; r[2] = p0[2];
+        r[3] = p1[0] - p0[0]; r[4] = p1[1] - p0[1]; r[5] = p1[2] - p0[2];
+        r[6] = p2[0] - p0[0]; r[7] = p2[1] - p0[1]; r[8] = p2[2] - p0[2];
+        std::memcpy(&r[9], &t, sizeof t);
+    }
+    d.tri4 = (const float4 *)up(13, t4.data(), 4ull * t4.size());
     // Scene::finalize's light list: emissive triangles of positive area (scene.cpp:38-47)
     std::vector<uint32_t> ltris;
     std::vector<float> lareas;

@@ -240,7 +240,7 @@ cudaError_t launch_adam_ema(float *theta, const float *grad, float *m, float *v,
                             const AdamParams &a, int num_sms, cudaStream_t stream);
 
 // Render front-end (nrrs_render.cu): Bvh::Node (geometry.hpp) flattened for the device
-struct BvhNodeDev {
+struct alignas(16) BvhNodeDev {
     float lo[3], hi[3];
     uint32_t offset;  // leaf: first prim; inner: right child (left child = this + 1)
     uint16_t count;   // > 0: leaf
@@ -252,6 +252,9 @@ struct RenderScene {
     const uint32_t *mat_of_tri;  // [n_tri]
     const BvhNodeDev *nodes;
     const uint32_t *prims;
+    // per BVH prim slot: {p0.xyz, e1.x}, {e1.yz, e2.xy}, {e2.z, triangle id bits, 0, 0} (host-computed
+    // v1 - v0 / v2 - v0, the same IEEE subtractions as intersect_triangle, geometry.cpp:45-47)
+    const float4 *tri4;
     uint32_t n_nodes, n_tri;
     const int32_t *mat_kind;     // 0 diffuse, 1 conductor
     const float *mat_albedo, *mat_roughness, *mat_emission;

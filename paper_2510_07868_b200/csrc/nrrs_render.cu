@@ -117,6 +117,36 @@ __device__ __forceinline__ bool tri_hit(const RenderScene &s, uint32_t tri, cons
     return true;
 }
 
+// intersect_triangle on the pre-gathered record of BVH prim slot k (p0, e1, e2 as the reference computes them)
+__device__ __forceinline__ bool tri_hit_slot(const RenderScene &s, uint32_t k, const float o[3], const float d[3],
+                                             float t_max, float &t, float &u, float &v, uint32_t &tri) {
+    const float4 a = __ldg(s.tri4 + 3 * (uint64_t)k), b = __ldg(s.tri4 + 3 * (uint64_t)k + 1),
+                 c = __ldg(s.tri4 + 3 * (uint64_t)k + 2);
+    const float p0[3] = {a.x, a.y, a.z}, e1[3] = {a.w, b.x, b.y}, e2[3] = {b.z, b.w, c.x};
+    float pv[3], qv[3];
+    cross3(d, e2, pv);
+    const float det = dot3(e1, pv);
+    if (fabsf(det) < 1e-12f)
+        return false;
+    const float inv_det = __fdiv_rn(1.0f, det);
+    const float tv[3] = {fs(o[0], p0[0]), fs(o[1], p0[1]), fs(o[2], p0[2])};
+    const float uu = fm(dot3(tv, pv), inv_det);
+    if (uu < 0.0f || uu > 1.0f)
+        return false;
+    cross3(tv, e1, qv);
+    const float vv = fm(dot3(d, qv), inv_det);
+    if (vv < 0.0f || fa(uu, vv) > 1.0f)
+        return false;
+    const float tt = fm(dot3(e2, qv), inv_det);
+    if (tt <= 1e-4f || tt >= t || tt >= t_max)  // kRayEps (core.hpp:21)
+        return false;
+    t = tt;
+    u = uu;
+    v = vv;
+    tri = __float_as_uint(c.y);
+    return true;
+}
+
 // Bvh::intersect (geometry.cpp:144-176); returns false for a degenerate direction (the reference throws)
 __device__ __forceinline__ bool closest_hit(const RenderScene &s, const float o[3], const float d[3], float t_max,
                                             float &t, uint32_t &tri, float &u, float &v) {
@@ -132,6 +162,46 @@ __device__ __forceinline__ bool closest_hit(const RenderScene &s, const float o[
     uint32_t stack[64];
     int sp = 0;
     stack[sp++] = 0;
+#ifdef NRRS_WHILE_WHILE
+    // while-while traversal: inner nodes until a leaf is reached, then the leaf.  Each ray visits
+    // nodes and leaves in exactly the reference's order (a leaf is tested as soon as it is popped).
+    while (sp > 0) {
+        uint32_t leaf = 0xFFFFFFFFu;
+        BvhNodeDev ln;
+        while (sp > 0) {
+            const uint32_t ni = stack[--sp];
+            const BvhNodeDev node = s.nodes[ni];
+            float t0 = 0.0f, t1 = stdmin(t, t_max);
+            for (int a = 0; a < 3; ++a) {
+                const float lo = fm(fs(node.lo[a], o[a]), inv_d[a]);
+                const float hi = fm(fs(node.hi[a], o[a]), inv_d[a]);
+                t0 = stdmax(t0, stdmin(lo, hi));
+                t1 = stdmin(t1, stdmax(lo, hi));
+            }
+            if (!(t0 <= t1))
+                continue;
+            if (node.count > 0) {
+                leaf = ni;
+                ln = node;
+                break;
+            }
+            const uint32_t left = ni + 1, right = node.offset;
+            if (inv_d[node.axis] >= 0.0f) {
+                stack[sp++] = right;
+                stack[sp++] = left;
+            } else {
+                stack[sp++] = left;
+                stack[sp++] = right;
+            }
+        }
+        if (leaf != 0xFFFFFFFFu)
+            for (uint32_t i = 0; i < ln.count; ++i) {
+                const uint32_t prim = s.prims[ln.offset + i];
+                if (tri_hit(s, prim, o, d, t_max, t, u, v))
+                    tri = prim;
+            }
+    }
+#else
     while (sp > 0) {
         const uint32_t ni = stack[--sp];
         const BvhNodeDev node = s.nodes[ni];
@@ -146,11 +216,8 @@ __device__ __forceinline__ bool closest_hit(const RenderScene &s, const float o[
         if (!(t0 <= t1))
             continue;
         if (node.count > 0) {
-            for (uint32_t i = 0; i < node.count; ++i) {
-                const uint32_t prim = s.prims[node.offset + i];
-                if (tri_hit(s, prim, o, d, t_max, t, u, v))
-                    tri = prim;
-            }
+            for (uint32_t i = 0; i < node.count; ++i)
+                tri_hit_slot(s, node.offset + i, o, d, t_max, t, u, v, tri);
         } else {
             const uint32_t left = ni + 1, right = node.offset;
             if (inv_d[node.axis] >= 0.0f) {  // near child first by the split axis direction
@@ -162,6 +229,7 @@ __device__ __forceinline__ bool closest_hit(const RenderScene &s, const float o[
             }
         }
     }
+#endif
     return true;
 }
 
@@ -188,7 +256,8 @@ __device__ __forceinline__ bool any_hit(const RenderScene &s, const float o[3], 
         if (node.count > 0) {
             for (uint32_t i = 0; i < node.count; ++i) {
                 float t = t_max, u, v;
-                if (tri_hit(s, s.prims[node.offset + i], o, d, t_max, t, u, v))
+                uint32_t tr;
+                if (tri_hit_slot(s, node.offset + i, o, d, t_max, t, u, v, tr))
                     return true;
             }
         } else {
@@ -592,7 +661,10 @@ __global__ void trace_records_kernel(RenderScene s, const PathStateDev *q, const
 
 // One child slot (wavefront.cpp:418-482): NEE term of the slot (f64, folded per vertex in child
 // order later) and the child PathState; slot_used marks sampled children.
-__global__ void trace_scatter_kernel(RenderScene s, VertexRecDev v, const uint32_t *slots, uint32_t spawned,
+#ifndef NRRS_SCATTER_MINB
+#define NRRS_SCATTER_MINB 4  // 64 registers: occupancy over the divergent walks (measured -5% frame time)
+#endif
+__global__ void __launch_bounds__(256, NRRS_SCATTER_MINB) trace_scatter_kernel(RenderScene s, VertexRecDev v, const uint32_t *slots, uint32_t spawned,
                                      uint32_t depth, uint64_t mixed_seed, PathStateDev *next, uint8_t *used,
                                      double *slot_term, TraceCounters *cnt) {
     uint32_t shadows = 0, nonfinite = 0;
