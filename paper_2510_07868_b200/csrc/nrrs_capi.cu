@@ -174,6 +174,8 @@ struct nrrs_gpu_ctx {
     uint64_t cap_q = 0, cap_u = 0;
     double *d_parts = nullptr;
     uint64_t cap_parts = 0;
+    float2 *d_feat = nullptr;  // K-A0 level planes (AID, fp16 tables): levels x n float2
+    uint64_t cap_feat = 0;
     uint32_t *d_part_counts = nullptr;
     uint64_t cap_part_counts = 0;
     uint64_t *d_tile_state = nullptr;
@@ -317,7 +319,7 @@ int nrrs_gpu_destroy(nrrs_gpu_ctx *ctx) {
     cudaStreamSynchronize(ctx->stream);
     void *ptrs[] = {ctx->d_stat_grid, ctx->d_rrs_grid, ctx->blob_stat.ptr, ctx->blob_rrs.ptr, ctx->blob_both.ptr,
                     ctx->d_q, ctx->d_u, ctx->d_parts, ctx->d_part_counts, ctx->d_tile_state, ctx->d_ctile_state,
-                    ctx->d_misc, ctx->d_res, ctx->d_sum, ctx->d_total, ctx->d_sync, ctx->d_etile_state, ctx->d_hist, ctx->d_tws, ctx->d_tloss, ctx->d_tpart, ctx->st.p01, ctx->st.wo01, ctx->st.rough,
+                    ctx->d_misc, ctx->d_res, ctx->d_sum, ctx->d_total, ctx->d_sync, ctx->d_etile_state, ctx->d_hist, ctx->d_tws, ctx->d_tloss, ctx->d_tpart, ctx->d_feat, ctx->st.p01, ctx->st.wo01, ctx->st.rough,
                     ctx->st.weight, ctx->st.ipix, ctx->st.key, ctx->st.q_norm, ctx->st.q_real, ctx->st.q_orig,
                     ctx->st.u, ctx->st.k, ctx->st.offset, ctx->st.slots, ctx->st.decided};
     for (void *p : ptrs)
@@ -556,6 +558,23 @@ static int select_kind(nrrs_gpu_ctx *ctx, uint32_t depth, const nrrs_strategy &s
     }
 }
 
+// AID with fp16 tables that fit in shared memory runs K-A0 + K-A (PRE): sizes the level planes
+// for ip.n and returns the number of kernels launch_infer will issue.
+static int prepare_level_planes(nrrs_gpu_ctx *ctx, int kind, InferParams &ip, uint32_t *n_kernels) {
+    *n_kernels = 1;
+    ip.feat = nullptr;
+    ip.feat_stride = 0;
+    if (kind != kKindAid || !ctx->rrs_half || std::getenv("NRRS_NO_LEVEL_KERNEL") ||
+        (uint64_t)ctx->grid_rrs.table_size * 4u > kLevelSmemMax || ip.n == 0)
+        return NRRS_OK;
+    const uint64_t stride = (ip.n + 31) & ~31ull;
+    CK(ctx, grow(ctx->d_feat, ctx->cap_feat, stride * (uint64_t)ctx->grid_rrs.levels));
+    ip.feat = ctx->d_feat;
+    ip.feat_stride = stride;
+    *n_kernels = 2;
+    return NRRS_OK;
+}
+
 static void fill_infer_common(nrrs_gpu_ctx *ctx, int kind, InferParams &ip) {
     ip.stat_grid = reinterpret_cast<const float2 *>(ctx->d_stat_grid);
     ip.rrs_grid = ctx->d_rrs_grid;
@@ -634,9 +653,12 @@ static int run_factors(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, 
         CK(ctx, cudaMemsetAsync(dbg, 0, 32 * 1024 * sizeof(unsigned long long), ctx->stream));
         ip.dbg = dbg;
     }
-    uint32_t grid = 0;
+    uint32_t grid = 0, n_kernels = 1;
+    rc = prepare_level_planes(ctx, kind, ip, &n_kernels);
+    if (rc)
+        return rc;
     CK(ctx, launch_infer(kind, ip, ctx->num_sms, ctx->stream, &grid));
-    ctx->launches += 1;
+    ctx->launches += n_kernels;
     if (timing) {
         std::vector<unsigned long long> h(32 * 1024);
         CK(ctx, cudaMemcpyAsync(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1946,9 +1968,12 @@ int nrrs_gpu_strategy_factor(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64
     ip.eps = eps_div < 1e-8f ? 1e-8f : eps_div;
     fill_infer_common(ctx, kind, ip);
     ip.q_out = d_q;
-    uint32_t grid = 0;
+    uint32_t grid = 0, n_kernels = 1;
+    rc = prepare_level_planes(ctx, kind, ip, &n_kernels);
+    if (rc)
+        return rc;
     CK(ctx, launch_infer(kind, ip, ctx->num_sms, ctx->stream, &grid));
-    ctx->launches += 1;
+    ctx->launches += n_kernels;
     return NRRS_OK;
 }
 

@@ -106,6 +106,8 @@ struct InferParams {
     uint32_t rrs_half;
     GridDev grid;        // StatNet grid (fp32)
     GridDev grid_rrs;    // AID RRSNet grid (same spec; its own number of pair copies)
+    float2 *feat;          // AID with fp16 tables in smem reach: K-A0 level planes [levels][feat_stride]
+    uint64_t feat_stride;
     const uint8_t *blob;
     uint32_t blob_bytes;
     KernelNets nets;
@@ -319,6 +321,17 @@ cudaError_t launch_surface(const RenderScene &s, const float *o, const float *d,
                            int num_sms, cudaStream_t stream);
 
 size_t infer_smem_bytes(int kind, const InferParams &p);
+// K-A0: one hash-grid level per CTA from shared memory (fp16 tables, T * 4 B <= kLevelSmemMax).
+struct GridLevelParams {
+    const float *p01;
+    uint64_t n;
+    const void *table;  // fp16 reference layout [level][T] half2 (copy 0 of the AID grid)
+    GridDev g;
+    float2 *feat;
+    uint64_t feat_stride;
+};
+constexpr uint32_t kLevelSmemMax = 200u * 1024u;
+cudaError_t launch_grid_levels(const GridLevelParams &p, int num_sms, cudaStream_t stream);
 cudaError_t launch_infer(int kind, const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out);
 uint32_t infer_max_grid(int num_sms);
 uint32_t decide_tiles(uint64_t n);

@@ -171,6 +171,103 @@ __device__ __forceinline__ void one_blob_fast(float x, float *out) {
 
 __device__ __forceinline__ float remap_fast(float a) { return 1.0f - __expf(-a); }
 
+// ===========================================================================
+// K-A0: level-sliced hash-grid encode (fp16 tables that fit in shared memory).
+//
+// Random 8-byte gathers from L2 run at ~1 per clock per SM (the L1TEX line
+// lookup; profiles/r01_microbench_gather_bw.txt), which is what bounds the fused
+// K-A.  Here each CTA owns ONE level: its table (T half2 entries, 128 KB at the
+// default 2^15) is staged into shared memory once by TMA bulk copies, and the
+// CTA encodes that level for a contiguous vertex range, 8 corner loads from
+// smem per vertex.  CTA b serves level b % L on range b / L, so the L CTAs of
+// one range run side by side and read the same p01 lines from L2.  Output:
+// level planes feat[l][j] = (f0, f1) fp32, read back once by K-A's encoder
+// warps (infer_ws_kernel<.., PRE = true>).  HashGrid::encode, hashgrid.cpp:38-82.
+// ===========================================================================
+constexpr int kLevelThreads = 1024;
+
+__global__ void __launch_bounds__(kLevelThreads, 1) grid_level_kernel(GridLevelParams p) {
+    extern __shared__ __align__(128) uint8_t lvl_smem[];
+    __shared__ uint64_t bar;
+    const GridDev &g = p.g;
+    const uint32_t L = (uint32_t)g.levels;
+    const uint32_t l = blockIdx.x % L, q = blockIdx.x / L;
+    const uint32_t nq = (gridDim.x - l + L - 1) / L;  // CTAs serving level l
+    const uint32_t res = (uint32_t)g.base_resolution << l;
+    const uint32_t nn = res + 1u;
+    const bool dense = (g.dense_mask >> l) & 1u;
+    const uint32_t entries = dense ? nn * nn * nn : g.table_size;
+    const uint32_t bytes = (entries * 4u + 15u) & ~15u;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        mbar_arrive_expect_tx(&bar, bytes);
+        const uint8_t *src = reinterpret_cast<const uint8_t *>(p.table) + (uint64_t)l * g.table_size * 4u;
+        for (uint32_t off = 0; off < bytes; off += 32768u)
+            bulk_g2s(lvl_smem + off, src + off, bytes - off < 32768u ? bytes - off : 32768u, &bar);
+    }
+    const uint64_t n = p.n;
+    const uint64_t j0 = n * q / nq, j1 = n * (q + 1) / nq;
+    const float resf = (float)res;
+    const uint32_t m = g.table_size - 1u;
+    float2 *out = p.feat + (uint64_t)l * p.feat_stride;
+    mbar_wait(&bar, 0);
+    const __half2 *tab = reinterpret_cast<const __half2 *>(lvl_smem);
+    for (uint64_t j = j0 + threadIdx.x; j < j1; j += kLevelThreads) {
+        const float px = clamp01(__ldg(p.p01 + 3 * j)), py = clamp01(__ldg(p.p01 + 3 * j + 1)),
+                    pz = clamp01(__ldg(p.p01 + 3 * j + 2));
+        const float fx = px * resf, fy = py * resf, fz = pz * resf;
+        const uint32_t cx = min((uint32_t)fx, res - 1u);
+        const uint32_t cy = min((uint32_t)fy, res - 1u);
+        const uint32_t cz = min((uint32_t)fz, res - 1u);
+        const float tx = fx - (float)cx, ty = fy - (float)cy, tz = fz - (float)cz;
+        const float wx[2] = {1.0f - tx, tx}, wy[2] = {1.0f - ty, ty}, wz[2] = {1.0f - tz, tz};
+        uint32_t idx[8];
+        if (dense) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                idx[k] = ((cx + (k & 1)) * nn + cy + ((k >> 1) & 1)) * nn + cz + (k >> 2);
+        } else {
+            const uint32_t hx[2] = {cx, cx + 1u};
+            const uint32_t hy[2] = {cy * 2654435761u, (cy + 1u) * 2654435761u};
+            const uint32_t hz[2] = {cz * 805459861u, (cz + 1u) * 805459861u};
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                idx[k] = (hx[k & 1] ^ hy[(k >> 1) & 1] ^ hz[k >> 2]) & m;
+        }
+        float2 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            v[k] = __half22float2(tab[idx[k]]);
+        float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float w = wx[k & 1] * wy[(k >> 1) & 1] * wz[k >> 2];  // x*y*z order (hashgrid.cpp)
+            a0 = fmaf(w, v[k].x, a0);
+            a1 = fmaf(w, v[k].y, a1);
+        }
+        out[j] = make_float2(a0, a1);
+    }
+}
+
+cudaError_t launch_grid_levels(const GridLevelParams &p, int num_sms, cudaStream_t stream) {
+    const uint32_t L = (uint32_t)p.g.levels;
+    const size_t smem = (size_t)p.g.table_size * 4u;
+    cudaError_t e = cudaFuncSetAttribute(grid_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess)
+        return e;
+    // one CTA per SM; every level gets floor or ceil of num_sms / L CTAs
+    uint64_t grid = (uint64_t)num_sms < L ? L : (uint64_t)num_sms;
+    const uint64_t max_useful = L * ((p.n + kLevelThreads - 1) / kLevelThreads);
+    if (grid > max_useful)
+        grid = max_useful < L ? L : max_useful;
+    grid_level_kernel<<<(uint32_t)grid, kLevelThreads, smem, stream>>>(p);
+    return cudaGetLastError();
+}
+
 __global__ void __launch_bounds__(kInferThreads) infer_kernel(InferParams p) {
     __shared__ InferSmemHeader hdr_s;
     InferSmemHeader *hdr = &hdr_s;
@@ -411,7 +508,9 @@ constexpr bool kTiming = true;
 constexpr bool kTiming = false;
 #endif
 
-template <int KIND, int GE, int GM, int P, int TPR, bool HALF>  // HALF: fp16 RRSNet (AID) grid tables
+// HALF: fp16 RRSNet (AID) grid tables.  PRE: the grid features were encoded by
+// grid_level_kernel (K-A0); the encoder warps read the level planes instead of gathering.
+template <int KIND, int GE, int GM, int P, int TPR, bool HALF, bool PRE>
 __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws_kernel(InferParams p) {
     using Cfg = ws::Cfg<GE, GM, P, TPR>;
     constexpr uint32_t kGT = Cfg::kGroupThreads;
@@ -515,6 +614,16 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
 #pragma unroll
                 for (int q = 0; q < 8; ++q)
                     g8[q] = px * (float)(q + 1) + py;
+            } else if (PRE) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int l = 4 * half + q;
+                    float2 f = make_float2(0.0f, 0.0f);
+                    if (valid && l < p.grid_rrs.levels)
+                        f = __ldcs(p.feat + (uint64_t)l * p.feat_stride + j);
+                    g8[2 * q] = f.x;
+                    g8[2 * q + 1] = f.y;
+                }
             } else if (KIND == kKindAid) {
                 grid_encode4<HALF>(p.rrs_grid, p.grid_rrs, 4 * half, clamp01(px), clamp01(py), clamp01(pz), g8);
             } else {
@@ -844,18 +953,18 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
     }
 }
 
-template <int KIND, int GE, int GM, int P, int TPR, bool HALF>
+template <int KIND, int GE, int GM, int P, int TPR, bool HALF, bool PRE = false>
 static cudaError_t launch_ws(const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out) {
     using Cfg = ws::Cfg<GE, GM, P, TPR>;
     const size_t smem = ((p.blob_bytes + 127u) & ~127u) + Cfg::kSlots * 128 * sizeof(ws::Side) +
                         sizeof(ws::SmemTail) + 64;
-    cudaError_t e = cudaFuncSetAttribute(infer_ws_kernel<KIND, GE, GM, P, TPR, HALF>,
+    cudaError_t e = cudaFuncSetAttribute(infer_ws_kernel<KIND, GE, GM, P, TPR, HALF, PRE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
         return e;
 #ifdef NRRS_CARVEOUT
     // smallest shared-memory carveout that fits: the rest of the 256 KB stays L1 for the grid levels
-    e = cudaFuncSetAttribute(infer_ws_kernel<KIND, GE, GM, P, TPR, HALF>,
+    e = cudaFuncSetAttribute(infer_ws_kernel<KIND, GE, GM, P, TPR, HALF, PRE>,
                              cudaFuncAttributePreferredSharedMemoryCarveout, NRRS_CARVEOUT);
     if (e != cudaSuccess)
         return e;
@@ -867,7 +976,7 @@ static cudaError_t launch_ws(const InferParams &p, int num_sms, cudaStream_t str
     if (grid < 1)
         grid = 1;
     *grid_out = (uint32_t)grid;
-    infer_ws_kernel<KIND, GE, GM, P, TPR, HALF><<<(uint32_t)grid, Cfg::kThreads, smem, stream>>>(p);
+    infer_ws_kernel<KIND, GE, GM, P, TPR, HALF, PRE><<<(uint32_t)grid, Cfg::kThreads, smem, stream>>>(p);
     return cudaGetLastError();
 }
 
@@ -1308,9 +1417,29 @@ size_t infer_smem_bytes(int kind, const InferParams &p) {
 
 // Pipeline shape: 2 encoder groups, 3 MLP groups with one tile chain each, 1 thread per row (the
 // tuned default; the sweep over other shapes is recorded in DESIGN.md section 3a).
+#ifndef NRRS_PRE_GE
+#define NRRS_PRE_GE 2
+#endif
+#ifndef NRRS_PRE_GM
+#define NRRS_PRE_GM 3
+#endif
 template <int KIND>
 static cudaError_t launch_ws_cfg(const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out) {
     if constexpr (KIND == kKindAid) {
+        if (p.rrs_half && p.feat) {
+            // K-A0 (level-sliced smem encode) then K-A reading the level planes
+            GridLevelParams gp{};
+            gp.p01 = p.p01;
+            gp.n = p.n;
+            gp.table = p.rrs_grid;
+            gp.g = p.grid_rrs;
+            gp.feat = p.feat;
+            gp.feat_stride = p.feat_stride;
+            cudaError_t e = launch_grid_levels(gp, num_sms, stream);
+            if (e != cudaSuccess)
+                return e;
+            return launch_ws<KIND, NRRS_PRE_GE, NRRS_PRE_GM, 1, 1, true, true>(p, num_sms, stream, grid_out);
+        }
         if (p.rrs_half)
             return launch_ws<KIND, 2, 3, 1, 1, true>(p, num_sms, stream, grid_out);
     }
