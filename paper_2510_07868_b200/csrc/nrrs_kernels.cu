@@ -42,7 +42,7 @@ struct InferSmemHeader {
 __device__ __forceinline__ void split2(float v0, float v1, uint32_t &h, uint32_t &l) {
     const __half2 hh = __float22half2_rn(make_float2(v0, v1));
     const float2 b = __half22float2(hh);
-    const __half2 ll = __float22half2_rn(make_float2(v0 - b.x, v1 - b.y));
+    const __half2 ll = __float22half2_rn(upk2(fsub2(pk2(v0, v1), pk2(b.x, b.y))));
     h = *reinterpret_cast<const uint32_t *>(&hh);
     l = *reinterpret_cast<const uint32_t *>(&ll);
 }
@@ -185,10 +185,71 @@ __device__ __forceinline__ float remap_fast(float a) { return 1.0f - __expf(-a);
 // warps (infer_ws_kernel<.., PRE = true>).  HashGrid::encode, hashgrid.cpp:38-82.
 // ===========================================================================
 constexpr int kLevelThreads = 1024;
+#ifndef NRRS_LEVEL_PER_THREAD
+#define NRRS_LEVEL_PER_THREAD 3
+#endif
+constexpr uint32_t kLevelPer = NRRS_LEVEL_PER_THREAD;             // vertices per thread per block
+constexpr uint32_t kLevelBlock = kLevelPer * kLevelThreads;  // staged p01 block (12 B per vertex), double-buffered
+
+// Per-level constants of K-A0 (uniform over the CTA).
+struct LevelConsts {
+    uint32_t res, nn, m4;  // resolution, res + 1, (T - 1) * 4
+    float resf;
+    bool dense;
+    uint32_t doff4[8];     // dense corner offsets * 4
+};
+
+// One level of HashGrid::encode for one point from the shared-memory table
+// (hashgrid.cpp:38-82): cell and weights per axis, 8 corner entries (byte offsets
+// idx * 4: the hash is computed on pre-scaled terms, ((a ^ b) & m) * 4 =
+// (4a ^ 4b) & 4m), weights w = wx * (wy * wz) as x-pairs, (f0, f1) accumulated as
+// one fp32x2 FMA per corner.
+__device__ __forceinline__ float2 level_encode(const uint8_t *tab, const LevelConsts &c, float px, float py,
+                                               float pz) {
+    const float fx = __saturatef(px) * c.resf, fy = __saturatef(py) * c.resf, fz = __saturatef(pz) * c.resf;
+    const uint32_t cx = min((uint32_t)fx, c.res - 1u);
+    const uint32_t cy = min((uint32_t)fy, c.res - 1u);
+    const uint32_t cz = min((uint32_t)fz, c.res - 1u);
+    const float tx = fx - (float)cx, ty = fy - (float)cy, tz = fz - (float)cz;
+    const uint64_t wxp = pk2(1.0f - tx, tx);
+    const float wy[2] = {1.0f - ty, ty}, wz[2] = {1.0f - tz, tz};
+    uint32_t idx4[8];
+    if (c.dense) {
+        const uint32_t b4 = ((cx * c.nn + cy) * c.nn + cz) * 4u;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            idx4[k] = b4 + c.doff4[k];
+    } else {
+        const uint32_t hx0 = cx * 4u, hx1 = hx0 + 4u;
+        const uint32_t hy0 = cy * (2654435761u * 4u), hy1 = hy0 + 2654435761u * 4u;
+        const uint32_t hz0 = cz * (805459861u * 4u), hz1 = hz0 + 805459861u * 4u;
+        const uint32_t hyz[4] = {hy0 ^ hz0, hy1 ^ hz0, hy0 ^ hz1, hy1 ^ hz1};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            idx4[2 * q] = (hx0 ^ hyz[q]) & c.m4;
+            idx4[2 * q + 1] = (hx1 ^ hyz[q]) & c.m4;
+        }
+    }
+    uint32_t raw[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        raw[k] = *reinterpret_cast<const uint32_t *>(tab + idx4[k]);
+    uint64_t acc[2] = {pk2(0.0f, 0.0f), pk2(0.0f, 0.0f)};  // oz = 0 / 1 (two short FMA chains)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {  // corners (0, oy, oz), (1, oy, oz); q = oy + 2 oz
+        const float2 w = upk2(fmul2(wxp, pk2(wy[q & 1] * wz[q >> 1], wy[q & 1] * wz[q >> 1])));
+        const float2 v0 = __half22float2(*reinterpret_cast<const __half2 *>(&raw[2 * q]));
+        const float2 v1 = __half22float2(*reinterpret_cast<const __half2 *>(&raw[2 * q + 1]));
+        acc[q >> 1] = ffma2(pk2(w.x, w.x), pk2(v0.x, v0.y), acc[q >> 1]);
+        acc[q >> 1] = ffma2(pk2(w.y, w.y), pk2(v1.x, v1.y), acc[q >> 1]);
+    }
+    const float2 a = upk2(acc[0]), b = upk2(acc[1]);
+    return make_float2(a.x + b.x, a.y + b.y);
+}
 
 __global__ void __launch_bounds__(kLevelThreads, 1) grid_level_kernel(GridLevelParams p) {
     extern __shared__ __align__(128) uint8_t lvl_smem[];
-    __shared__ uint64_t bar;
+    __shared__ uint64_t bar[5];  // [0] table, [1..2] p01 blocks full, [3..4] p01 blocks empty
     const GridDev &g = p.g;
     const uint32_t L = (uint32_t)g.levels;
     const uint32_t l = blockIdx.x % L, q = blockIdx.x / L;
@@ -198,64 +259,96 @@ __global__ void __launch_bounds__(kLevelThreads, 1) grid_level_kernel(GridLevelP
     const bool dense = (g.dense_mask >> l) & 1u;
     const uint32_t entries = dense ? nn * nn * nn : g.table_size;
     const uint32_t bytes = (entries * 4u + 15u) & ~15u;
+    const uint32_t tab_bytes = g.table_size * 4u;
+    float *pbuf = reinterpret_cast<float *>(lvl_smem + tab_bytes);  // 2 x kLevelBlock x 3 floats
+    const uint64_t n = p.n;
+    // CTA range, 4-vertex aligned so every staged block starts on a 16-byte boundary
+    const uint64_t j0 = (n * q / nq) & ~3ull;
+    const uint64_t j1 = q + 1 == nq ? n : ((n * (q + 1) / nq) & ~3ull);
+    const bool staged = (reinterpret_cast<uintptr_t>(p.p01) & 15u) == 0;
+    const uint32_t nblocks = (uint32_t)((j1 - j0 + kLevelBlock - 1) / kLevelBlock);
+    // staged bytes of block b: whole 4-vertex groups only (the <= 3 tail vertices load directly)
+    auto issue = [&](uint32_t b) {
+        const uint64_t s = j0 + (uint64_t)b * kLevelBlock;
+        const uint64_t e = s + kLevelBlock < j1 ? s + kLevelBlock : j1;
+        const uint32_t nb = (uint32_t)((e - s) & ~3ull) * 12u;
+        mbar_arrive_expect_tx(&bar[1 + (b & 1)], nb);
+        if (nb)
+            bulk_g2s(pbuf + (b & 1) * kLevelBlock * 3, p.p01 + 3 * s, nb, &bar[1 + (b & 1)]);
+    };
     if (threadIdx.x == 0) {
-        mbar_init(&bar, 1);
+        for (int i = 0; i < 3; ++i)
+            mbar_init(&bar[i], 1);
+        mbar_init(&bar[3], kLevelThreads);
+        mbar_init(&bar[4], kLevelThreads);
         fence_barrier_init();
+        mbar_arrive_expect_tx(&bar[0], bytes);
+        const uint8_t *src = reinterpret_cast<const uint8_t *>(p.table) + (uint64_t)l * tab_bytes;
+        for (uint32_t off = 0; off < bytes; off += 32768u)
+            bulk_g2s(lvl_smem + off, src + off, bytes - off < 32768u ? bytes - off : 32768u, &bar[0]);
+        if (staged)
+            for (uint32_t b = 0; b < 2 && b < nblocks; ++b)
+                issue(b);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        mbar_arrive_expect_tx(&bar, bytes);
-        const uint8_t *src = reinterpret_cast<const uint8_t *>(p.table) + (uint64_t)l * g.table_size * 4u;
-        for (uint32_t off = 0; off < bytes; off += 32768u)
-            bulk_g2s(lvl_smem + off, src + off, bytes - off < 32768u ? bytes - off : 32768u, &bar);
-    }
-    const uint64_t n = p.n;
-    const uint64_t j0 = n * q / nq, j1 = n * (q + 1) / nq;
-    const float resf = (float)res;
-    const uint32_t m = g.table_size - 1u;
+    LevelConsts c;
+    c.res = res;
+    c.nn = nn;
+    c.m4 = (g.table_size - 1u) * 4u;
+    c.resf = (float)res;
+    c.dense = dense;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        c.doff4[k] = (((k & 1) * nn + ((k >> 1) & 1)) * nn + (k >> 2)) * 4u;
     float2 *out = p.feat + (uint64_t)l * p.feat_stride;
-    mbar_wait(&bar, 0);
-    const __half2 *tab = reinterpret_cast<const __half2 *>(lvl_smem);
-    for (uint64_t j = j0 + threadIdx.x; j < j1; j += kLevelThreads) {
-        const float px = clamp01(__ldg(p.p01 + 3 * j)), py = clamp01(__ldg(p.p01 + 3 * j + 1)),
-                    pz = clamp01(__ldg(p.p01 + 3 * j + 2));
-        const float fx = px * resf, fy = py * resf, fz = pz * resf;
-        const uint32_t cx = min((uint32_t)fx, res - 1u);
-        const uint32_t cy = min((uint32_t)fy, res - 1u);
-        const uint32_t cz = min((uint32_t)fz, res - 1u);
-        const float tx = fx - (float)cx, ty = fy - (float)cy, tz = fz - (float)cz;
-        const float wx[2] = {1.0f - tx, tx}, wy[2] = {1.0f - ty, ty}, wz[2] = {1.0f - tz, tz};
-        uint32_t idx[8];
-        if (dense) {
+    mbar_wait(&bar[0], 0);
+    for (uint32_t b = 0; b < nblocks; ++b) {
+        const uint64_t s = j0 + (uint64_t)b * kLevelBlock;
+        const uint32_t cnt = (uint32_t)((j1 - s) < kLevelBlock ? (j1 - s) : kLevelBlock);
+        const uint32_t cnt4 = staged ? (cnt & ~3u) : 0u;
+        const float *pb = pbuf + (b & 1) * kLevelBlock * 3;
+        if (staged)
+            mbar_wait(&bar[1 + (b & 1)], (b >> 1) & 1u);
+        // kLevelPer vertices per thread (t, t + 1024, ...): independent smem gathers in flight together
+        float pv[kLevelPer][3];
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
-                idx[k] = ((cx + (k & 1)) * nn + cy + ((k >> 1) & 1)) * nn + cz + (k >> 2);
-        } else {
-            const uint32_t hx[2] = {cx, cx + 1u};
-            const uint32_t hy[2] = {cy * 2654435761u, (cy + 1u) * 2654435761u};
-            const uint32_t hz[2] = {cz * 805459861u, (cz + 1u) * 805459861u};
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-                idx[k] = (hx[k & 1] ^ hy[(k >> 1) & 1] ^ hz[k >> 2]) & m;
+        for (int u = 0; u < (int)kLevelPer; ++u) {
+            const uint32_t t = threadIdx.x + u * kLevelThreads;
+            if (t < cnt4) {
+                pv[u][0] = pb[3 * t];
+                pv[u][1] = pb[3 * t + 1];
+                pv[u][2] = pb[3 * t + 2];
+            } else if (t < cnt) {
+                const float *g3 = p.p01 + 3 * (s + t);
+                pv[u][0] = __ldg(g3);
+                pv[u][1] = __ldg(g3 + 1);
+                pv[u][2] = __ldg(g3 + 2);
+            } else {
+                pv[u][0] = pv[u][1] = pv[u][2] = 0.0f;
+            }
         }
-        float2 v[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-            v[k] = __half22float2(tab[idx[k]]);
-        float a0 = 0.0f, a1 = 0.0f;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const float w = wx[k & 1] * wy[(k >> 1) & 1] * wz[k >> 2];  // x*y*z order (hashgrid.cpp)
-            a0 = fmaf(w, v[k].x, a0);
-            a1 = fmaf(w, v[k].y, a1);
+        if (staged)
+            mbar_arrive(&bar[3 + (b & 1)]);  // this thread is done with buffer b & 1
+        if (staged && threadIdx.x == 0 && b + 2 < nblocks) {
+            mbar_wait(&bar[3 + (b & 1)], (b >> 1) & 1u);
+            fence_proxy_async_smem();
+            issue(b + 2);
         }
-        out[j] = make_float2(a0, a1);
+        float2 r[kLevelPer];
+#pragma unroll
+        for (int u = 0; u < (int)kLevelPer; ++u)
+            r[u] = level_encode(lvl_smem, c, pv[u][0], pv[u][1], pv[u][2]);
+        float2 *ob = out + s + threadIdx.x;
+#pragma unroll
+        for (int u = 0; u < (int)kLevelPer; ++u)
+            if (threadIdx.x + u * kLevelThreads < cnt)
+                __stcs(ob + u * kLevelThreads, r[u]);
     }
 }
 
 cudaError_t launch_grid_levels(const GridLevelParams &p, int num_sms, cudaStream_t stream) {
     const uint32_t L = (uint32_t)p.g.levels;
-    const size_t smem = (size_t)p.g.table_size * 4u;
+    const size_t smem = (size_t)p.g.table_size * 4u + 2u * kLevelBlock * 12u;
     cudaError_t e = cudaFuncSetAttribute(grid_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
         return e;
@@ -477,24 +570,22 @@ __device__ __forceinline__ void ws_store_a16(uint32_t lane_base, uint32_t col_a,
     tmem_st8(lane_base + col_a + 16u + 8u * (uint32_t)h, lw);
 }
 
-// 16 accumulator columns [c0, c0 + 16) of this lane: D_hi + D_lo (+ bias), fp32.
+// 16 accumulator columns [c0, c0 + 16) of this lane: D_hi + D_lo (+ bias), fp32
+// (element order of the scalar form; the adds run as fp32x2 pairs).
 __device__ __forceinline__ void ws_load_sum16(uint32_t lane_base, uint32_t col_d, uint32_t n, uint32_t c0,
                                               const float *bias, float (&z)[16]) {
     float lo[16];
     tmem_ld16x2(lane_base + col_d + c0, lane_base + col_d + n + c0, z, lo);
 #pragma unroll
-    for (int i = 0; i < 16; ++i)
-        z[i] += lo[i];
-    if (bias) {
-        const float4 *b4 = reinterpret_cast<const float4 *>(bias + c0);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const float4 b = b4[i];
-            z[4 * i] += b.x;
-            z[4 * i + 1] += b.y;
-            z[4 * i + 2] += b.z;
-            z[4 * i + 3] += b.w;
+    for (int i = 0; i < 8; ++i) {
+        uint64_t v = fadd2(pk2(z[2 * i], z[2 * i + 1]), pk2(lo[2 * i], lo[2 * i + 1]));
+        if (bias) {
+            const float2 b = reinterpret_cast<const float2 *>(bias + c0)[i];
+            v = fadd2(v, pk2(b.x, b.y));
         }
+        const float2 f = upk2(v);
+        z[2 * i] = f.x;
+        z[2 * i + 1] = f.y;
     }
 }
 
@@ -762,8 +853,11 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
                             float z[16];
                             ws::ws_load_sum16(lane_base, col_d, 32u, 16u * (uint32_t)h, bias, z);
 #pragma unroll
-                            for (int i = 0; i < 16; ++i)
-                                z[i] = fmaxf(z[i], z[i] * 0.01f);  // leaky ReLU = cwiseMax(z, slope z)
+                            for (int i = 0; i < 8; ++i) {  // leaky ReLU = cwiseMax(z, slope z)
+                                const float2 t = upk2(fmul2(pk2(z[2 * i], z[2 * i + 1]), pk2(0.01f, 0.01f)));
+                                z[2 * i] = fmaxf(z[2 * i], t.x);
+                                z[2 * i + 1] = fmaxf(z[2 * i + 1], t.y);
+                            }
                             ws::ws_store_a16(lane_base, col_a, h, z);
                         }
                         tmem_wait_st();
