@@ -506,6 +506,15 @@ struct Side {        // 32 B per tile row
 // collect A_hi*W_lo (one N = 2N instruction covers both weight halves); then a
 // ring of tile slots [kColSlots + 32s, +32) holding the layer-0 input
 // (hi 16 | lo 16 packed fp16x2 columns), reused as the hidden-layer A.
+// NRRS_MMA3 = 1: three N-wide MMAs per K16 slice accumulate A_hi*W_hi + A_lo*W_hi +
+// A_hi*W_lo into ONE 32-column accumulator (same tensor work as the N = 2N form; the
+// epilogue reads half the TMEM columns and skips the hi + lo add).
+#ifndef NRRS_MMA3
+#define NRRS_MMA3 1
+#endif
+constexpr bool kMma3 = NRRS_MMA3 != 0;
+constexpr uint32_t kDCols = kMma3 ? 32u : 64u;
+
 template <int GE, int GM, int P, int TPR>
 struct Cfg {
     static constexpr int kGroupThreads = 128 * TPR;  // MLP threads per group (TPR threads per tile row)
@@ -514,7 +523,7 @@ struct Cfg {
     static constexpr int kThreads = kEncThreads + kMlpThreads;
     static constexpr int kChains = GM * P;
     static constexpr uint32_t kColD = 0;
-    static constexpr uint32_t kColSlots = 64 * kChains;
+    static constexpr uint32_t kColSlots = kDCols * kChains;
     static constexpr int kSlotsRaw = (512 - (int)kColSlots) / 32;
     static constexpr int kSlots = kSlotsRaw > 16 ? 16 : kSlotsRaw;
     static_assert(kSlots >= GE + kChains, "TMEM slot ring too small");
@@ -525,6 +534,7 @@ struct SmemTail {
     uint64_t empty[16];
     uint64_t mma_bar[8];
     uint64_t wdesc[2][4][2];   // UMMA smem descriptor of [W_hi ; W_lo] per K16 slice (W_hi alone = first N rows)
+    uint64_t wdesc_lo[2][4][2];  // W_lo alone (rows N .. 2N)
     uint32_t idesc_n[2][4];    // N = layer width
     uint32_t idesc_2n[2][4];   // N = 2 x layer width (both weight halves)
     uint32_t nslices[2][4];
@@ -553,8 +563,14 @@ __device__ __forceinline__ void ws_issue(const SmemTail *st, int net, int layer,
             break;
         const uint64_t w = st->wdesc[net][layer][k];
         const uint32_t ah = tmem_base + col_a + 8u * k, al = ah + 16u;
-        mma_f16_ts(d, ah, w, i2, k > 0 ? 1u : 0u);
-        mma_f16_ts(d, al, w, i1, 1u);
+        if (kMma3) {
+            mma_f16_ts(d, ah, w, i1, k > 0 ? 1u : 0u);
+            mma_f16_ts(d, al, w, i1, 1u);
+            mma_f16_ts(d, ah, st->wdesc_lo[net][layer][k], i1, 1u);
+        } else {
+            mma_f16_ts(d, ah, w, i2, k > 0 ? 1u : 0u);
+            mma_f16_ts(d, al, w, i1, 1u);
+        }
     }
     mma_commit(bar);
 }
@@ -575,10 +591,15 @@ __device__ __forceinline__ void ws_store_a16(uint32_t lane_base, uint32_t col_a,
 __device__ __forceinline__ void ws_load_sum16(uint32_t lane_base, uint32_t col_d, uint32_t n, uint32_t c0,
                                               const float *bias, float (&z)[16]) {
     float lo[16];
-    tmem_ld16x2(lane_base + col_d + c0, lane_base + col_d + n + c0, z, lo);
+    if (kMma3)
+        tmem_ld16(lane_base + col_d + c0, z);
+    else
+        tmem_ld16x2(lane_base + col_d + c0, lane_base + col_d + n + c0, z, lo);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        uint64_t v = fadd2(pk2(z[2 * i], z[2 * i + 1]), pk2(lo[2 * i], lo[2 * i + 1]));
+        uint64_t v = pk2(z[2 * i], z[2 * i + 1]);
+        if (!kMma3)
+            v = fadd2(v, pk2(lo[2 * i], lo[2 * i + 1]));
         if (bias) {
             const float2 b = reinterpret_cast<const float2 *>(bias + c0)[i];
             v = fadd2(v, pk2(b.x, b.y));
@@ -635,8 +656,11 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
                 st->nslices[net][l] = (uint32_t)L.K / 16u;
                 st->bias[net][l] = L.bias;
                 const uint32_t sbo = (uint32_t)L.K * 16u;
-                for (int k = 0; k < 2; ++k)
+                for (int k = 0; k < 2; ++k) {
                     st->wdesc[net][l][k] = make_smem_desc(smem_u32(smem_w + L.w_hi) + 256u * k, 128u, sbo);
+                    st->wdesc_lo[net][l][k] =
+                        make_smem_desc(smem_u32(smem_w + L.w_hi) + 256u * k + ((uint32_t)L.N / 8u) * sbo, 128u, sbo);
+                }
             }
         }
         for (int q = 0; q < S; ++q) {
@@ -666,7 +690,118 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
     uint32_t my_nonfinite = 0, my_bc = 0;
     const bool depth1 = p.depth == 1u;
 
-    if (tid < Cfg::kEncThreads) {
+    if (PRE && tid < Cfg::kEncThreads) {
+        // ===================== encoder, AID with level planes =====================
+        // The grid features come from K-A0.  The loads of tile i + GE are issued
+        // before tile i is processed (one tile of register prefetch), so their HBM
+        // latency overlaps the slot wait and the tail encodings of tile i.
+        const int e = tid >> 8;
+        const int r = tid & 127, half = (tid >> 7) & 1;
+        struct In {
+            float f[8];
+            float wx, wy, wz, a, b, c;  // weight; half 0: wo01.xy, -; half 1: i_pixel (or i_acc[pixel]) xyz
+            float rough;
+            uint64_t key;
+            bool valid;
+        };
+        auto load = [&](uint32_t i, In &x) {
+            const uint64_t j = (t_begin + i) * kTileM + r;
+            x.valid = j < n;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int l = 4 * half + q;
+                float2 f = make_float2(0.0f, 0.0f);
+                if (x.valid && l < p.grid_rrs.levels)
+                    f = __ldcs(p.feat + (uint64_t)l * p.feat_stride + j);
+                x.f[2 * q] = f.x;
+                x.f[2 * q + 1] = f.y;
+            }
+            x.wx = x.wy = x.wz = x.a = x.b = x.c = x.rough = 0.0f;
+            x.key = 0;
+            if (!x.valid)
+                return;
+            x.wx = __ldg(p.weight + 3 * j);
+            x.wy = __ldg(p.weight + 3 * j + 1);
+            x.wz = __ldg(p.weight + 3 * j + 2);
+            if (half == 0) {
+                x.a = __ldg(p.wo01 + 2 * j);
+                x.b = __ldg(p.wo01 + 2 * j + 1);
+                x.key = __ldg(p.path_key + j);
+            } else {
+                if (p.i_pixel) {
+                    x.a = __ldg(p.i_pixel + 3 * j);
+                    x.b = __ldg(p.i_pixel + 3 * j + 1);
+                    x.c = __ldg(p.i_pixel + 3 * j + 2);
+                } else {
+                    const uint64_t px_idx = __ldg(p.pixel + j);
+                    x.a = __ldg(p.i_acc + 3 * px_idx);
+                    x.b = __ldg(p.i_acc + 3 * px_idx + 1);
+                    x.c = __ldg(p.i_acc + 3 * px_idx + 2);
+                }
+                x.rough = __ldg(p.roughness + j);
+            }
+        };
+        In nxt;
+        if ((uint32_t)e < T)
+            load((uint32_t)e, nxt);
+        for (uint32_t i = (uint32_t)e; i < T; i += GE) {
+            const In cur = nxt;
+            if (i + GE < T)
+                load(i + GE, nxt);
+            const uint32_t s = i % S;
+            if (i >= (uint32_t)S)
+            {
+#if NRRS_ENC_ONE_POLLER
+                // one warp polls the slot, the group's other warps block in bar.sync (no issue slots)
+                if ((tid & 255) < 32)
+                    mbar_wait_sleep(&st->empty[s], ((i / S) - 1u) & 1u, 1000u);
+                named_bar_sync(1u + (uint32_t)GM + (uint32_t)e, 256u);
+#else
+                mbar_wait_sleep(&st->empty[s], ((i / S) - 1u) & 1u, 1000u);
+#endif
+            }
+            const bool valid = cur.valid;
+            const bool active = valid && (p.gate ? (!depth1 && luminance(cur.wx, cur.wy, cur.wz) > 0.0f) : true);
+            float in16[16];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                in16[q] = cur.f[q];
+            float *t8 = in16 + 8;
+            uint32_t bc = 0;
+            ws::Side sd{};
+            if (half == 0) {
+                one_blob_fast<4>(cur.a, t8);
+                one_blob_fast<4>(cur.b, t8 + 4);
+                sd.key = cur.key;
+                sd.flags = (valid ? 1u : 0u) | (active ? 2u : 0u);
+            } else {
+                t8[0] = box_cox(cur.wx, bc);
+                t8[1] = box_cox(cur.wy, bc);
+                t8[2] = box_cox(cur.wz, bc);
+                t8[3] = box_cox(mean3(cur.a, cur.b, cur.c), bc);
+                one_blob_fast<4>(remap_fast(cur.rough), t8 + 4);
+            }
+            if (!valid) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q)
+                    in16[q] = 0.0f;
+            }
+            if (active)
+                my_bc += bc;
+            const uint32_t col = Cfg::kColSlots + 32u * s;
+            uint32_t hw[8], lw[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                split2(in16[2 * q], in16[2 * q + 1], hw[q], lw[q]);
+            tmem_st8(lane_base + col + 8u * half, hw);
+            tmem_st8(lane_base + col + 16u + 8u * half, lw);
+            if (half == 0)
+                side[s * 128 + r] = sd;
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&st->full[s]);
+        }
+    } else if (tid < Cfg::kEncThreads) {
         // ============================== encoder ==============================
         const int e = tid >> 8;                 // encoder group
         const int r = tid & 127, half = (tid >> 7) & 1;
@@ -676,7 +811,16 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
             const uint32_t s = i % S;
             if (rec) t0 = clock64();
             if (i >= (uint32_t)S)
+            {
+#if NRRS_ENC_ONE_POLLER
+                // one warp polls the slot, the group's other warps block in bar.sync (no issue slots)
+                if ((tid & 255) < 32)
+                    mbar_wait_sleep(&st->empty[s], ((i / S) - 1u) & 1u, 1000u);
+                named_bar_sync(1u + (uint32_t)GM + (uint32_t)e, 256u);
+#else
                 mbar_wait_sleep(&st->empty[s], ((i / S) - 1u) & 1u, 1000u);
+#endif
+            }
             if (rec) { const unsigned long long t1 = clock64(); c_empty += t1 - t0; t0 = t1; }
             const uint64_t j = (t_begin + i) * kTileM + r;
             const bool valid = j < n;
@@ -819,12 +963,13 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
             for (int c = 0; c < P; ++c) {
                 if (!live[c])
                     continue;
-                mbar_wait_sleep(&st->full[slot[c]], (tile[c] / S) & 1u, 1000u);  // suspended, not spinning
+                if (issuer)  // only the MMA issuer needs the input slot; the group waits on the MMA
+                    mbar_wait_sleep(&st->full[slot[c]], (tile[c] / S) & 1u, 1000u);
                 if (rec && g == 0) p.dbg[blockIdx.x * 32 + 17] = clock64();  // last tile: full passed
                 if (rec && blockIdx.x == 0 && tile[c] < 1024) p.dbg[8192 + 4 * tile[c] + 2] = clock64();
                 if (issuer)
                     ws::ws_issue(st, KIND == kKindAid ? 1 : 0, 0, tmem_base, Cfg::kColSlots + 32u * slot[c],
-                                 Cfg::kColD + 64u * (uint32_t)(g * P + c), &st->mma_bar[g * P + c]);
+                                 Cfg::kColD + ws::kDCols * (uint32_t)(g * P + c), &st->mma_bar[g * P + c]);
             }
 #pragma unroll 1
             for (int l = 0; l < kNL; ++l) {  // layer l just issued for every live chain
@@ -833,7 +978,7 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
                     if (!live[c])
                         continue;
                     const int q = g * P + c;
-                    const uint32_t col_d = Cfg::kColD + 64u * (uint32_t)q;
+                    const uint32_t col_d = Cfg::kColD + ws::kDCols * (uint32_t)q;
                     const uint32_t col_a = Cfg::kColSlots + 32u * slot[c];
                     if (rec) t0 = clock64();
                     mbar_wait(&st->mma_bar[q], (phases >> c) & 1u);
@@ -1515,7 +1660,10 @@ size_t infer_smem_bytes(int kind, const InferParams &p) {
 #define NRRS_PRE_GE 2
 #endif
 #ifndef NRRS_PRE_GM
-#define NRRS_PRE_GM 3
+#define NRRS_PRE_GM 4
+#endif
+#ifndef NRRS_PRE_P
+#define NRRS_PRE_P 1
 #endif
 template <int KIND>
 static cudaError_t launch_ws_cfg(const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out) {
@@ -1532,7 +1680,7 @@ static cudaError_t launch_ws_cfg(const InferParams &p, int num_sms, cudaStream_t
             cudaError_t e = launch_grid_levels(gp, num_sms, stream);
             if (e != cudaSuccess)
                 return e;
-            return launch_ws<KIND, NRRS_PRE_GE, NRRS_PRE_GM, 1, 1, true, true>(p, num_sms, stream, grid_out);
+            return launch_ws<KIND, NRRS_PRE_GE, NRRS_PRE_GM, NRRS_PRE_P, 1, true, true>(p, num_sms, stream, grid_out);
         }
         if (p.rrs_half)
             return launch_ws<KIND, 2, 3, 1, 1, true>(p, num_sms, stream, grid_out);
