@@ -41,6 +41,11 @@ ALG_BYTES_INFER = 56 + 8   # K-A: reads p01 12, wo01 8, rough 4, t_x 12, i_pixel
 # a 2 MiB table (profiles/r01_microbench_gather_bw.txt, tools/gather_bw.cu).
 GATHER_UNITS_PER_VERTEX = {"aid": 7 * (4 + 4 / 256) + 4, "nrrs": 7 * (4 * 1.28 + 4 / 256) + 4 * 1.28}
 GATHER_CEILING_PER_S = 296e9
+# AID with fp16 tables runs K-A0 first: one hash-grid level per CTA from shared memory, 8 random 4-byte
+# corner loads per vertex and level = 64 per vertex.  Ceiling: 8.54 random 4-byte loads/cycle/SM from a
+# 128 KB shared-memory table at 32 warps/SM = 2,484 G loads/s (profiles/r01_microbench_gather_bw.txt).
+SMEM_LOADS_PER_VERTEX = 64
+SMEM_LOAD_CEILING_PER_S = 2484.46e9
 STAGE_READ, STAGE_WRITE = 56, 8  # SURVEY.md 8d per-vertex compulsory bytes (+ 8 B per spawned slot record)
 
 
@@ -335,6 +340,21 @@ def main():
     infer_ms = [e[0].elapsed_time(e[1]) for e in bevs]
     decide_ms = [e[1].elapsed_time(e[2]) for e in bevs]
     compact_ms = [e[2].elapsed_time(e[3]) for e in bevs]
+    # K-A0 alone (the level-plane encode the AID stage launches first), same batch, same L2 flush
+    levels_ms = []
+    if args.variant == "aid":
+        planes = torch.empty((8, n, 2), dtype=torch.float32, device=dev)
+        for _ in range(min(args.steps, 10)):
+            flush.zero_()
+            ev = events()
+            ev[0].record(torch.cuda.current_stream())
+            _capi.check(stage.handle, lib.nrrs_gpu_encode_levels(stage.handle, dv["p01"].data_ptr(), n,
+                                                                 planes.data_ptr(), n))
+            ev[1].record(torch.cuda.current_stream())
+            levels_ms.append(ev)
+        torch.cuda.synchronize()
+        levels_ms = [e[0].elapsed_time(e[1]) for e in levels_ms]
+        del planes
     t = torch.tensor([total_s], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)  # max over ranks
@@ -680,19 +700,34 @@ def main():
                    "depth": 2, "gain": 0.85, "parallelism": f"tile-sharded dp{world}",
                    "l2": "flushed between timed steps (256 MiB write outside the events)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": traffic, "kernel": f"infer_ws_kernel<{'Aid' if args.variant == 'aid' else 'Nrrs'}> (warp-specialized, 2 encoder + 3 MLP groups)",
+                     "traffic": traffic,
+                     "kernel": ("K-A0 grid_level_kernel + K-A infer_ws_kernel<Aid, level planes> (2 encoder + 4 MLP "
+                                "groups): the strategy-factor step of the stage, timed as one unit"
+                                if args.variant == "aid" else
+                                "infer_ws_kernel<Nrrs> (warp-specialized, 2 encoder + 3 MLP groups, L2 gathers)"),
                      "alg_bytes_per_vertex": ALG_BYTES_INFER, "peak_source": peak_src,
                      "stage_frac": (stage_bytes / (statistics.mean(step_ms) / 1e3) / 1e9) / hbm},
-        "gather_roofline": {"bound": "l2_scattered_gathers", "unit": "gathers/s (8-byte equivalents)",
-                            "achieved": gu * n / infer_avg, "peak": GATHER_CEILING_PER_S,
-                            "frac": gu * n / infer_avg / GATHER_CEILING_PER_S, "units_per_vertex": gu,
-                            "peak_source": "measured, profiles/r01_microbench_gather_bw.txt"},
         "kernels_ms": {"infer": statistics.mean(infer_ms), "decide": statistics.mean(decide_ms),
                        "compact": statistics.mean(compact_ms)},
         "clocks": clk.summary(),
         "gpu_launches": launches,
         "spawned": spawned,
     }
+    if levels_ms:
+        lv = statistics.mean(levels_ms) / 1e3
+        line["kernels_ms"]["infer_grid_levels"] = 1e3 * lv  # K-A0 alone; "infer" = K-A0 + K-A
+        line["gather_roofline"] = {
+            "bound": "smem_random_loads", "kernel": "K-A0 grid_level_kernel", "unit": "4-byte loads/s",
+            "achieved": SMEM_LOADS_PER_VERTEX * n / lv, "peak": SMEM_LOAD_CEILING_PER_S,
+            "frac": SMEM_LOADS_PER_VERTEX * n / lv / SMEM_LOAD_CEILING_PER_S,
+            "units_per_vertex": SMEM_LOADS_PER_VERTEX,
+            "peak_source": "measured, profiles/r01_microbench_gather_bw.txt (tools/gather_bw.cu)"}
+    else:
+        line["gather_roofline"] = {
+            "bound": "l2_scattered_gathers", "unit": "gathers/s (8-byte equivalents)",
+            "achieved": gu * n / infer_avg, "peak": GATHER_CEILING_PER_S,
+            "frac": gu * n / infer_avg / GATHER_CEILING_PER_S, "units_per_vertex": gu,
+            "peak_source": "measured, profiles/r01_microbench_gather_bw.txt"}
     if e2e:
         line["e2e"] = e2e
     if extra:

@@ -432,6 +432,12 @@ NRRS_API int nrrs_gpu_strategy_factor(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *
                              const nrrs_strategy *s, float eps_div, float *d_q);
 /* NeuralRrs::predict_stats (networks.hpp:133) batched: d_stats[6j..6j+5] = mean(3), m2(3) */
 NRRS_API int nrrs_gpu_predict_stats(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *d_v, uint64_t n, float *d_stats);
+/* HashGrid::encode (hashgrid.cpp:38-82) of the AID RRSNet grid, batched and level-major: the K-A0
+ * kernel the AID stage runs first (one level per CTA from shared memory, fp16 tables).
+ * d_planes[l * plane_stride + j] = (feature 0, feature 1) of level l for point d_p01[3j..3j+2].
+ * ESTATE unless AID weights with fp16 tables that fit in shared memory are installed. */
+NRRS_API int nrrs_gpu_encode_levels(nrrs_gpu_ctx *ctx, const float *d_p01, uint64_t n, float *d_planes,
+                                    uint64_t plane_stride);
 
 /* ---- host helpers (pure arithmetic, no device) ---- */
 NRRS_API uint32_t nrrs_queue_capacity_for(uint32_t n_pixels); /* wavefront.cpp:82-84 */

@@ -156,6 +156,7 @@ SIGNATURES = [
     ("nrrs_gpu_strategy_factor", C.c_int, [_P, C.POINTER(VertexSoA), C.c_uint64, C.POINTER(StrategyC),
                                            C.c_float, _P]),
     ("nrrs_gpu_predict_stats", C.c_int, [_P, C.POINTER(VertexSoA), C.c_uint64, _P]),
+    ("nrrs_gpu_encode_levels", C.c_int, [_P, _P, C.c_uint64, _P, C.c_uint64]),
     ("nrrs_queue_capacity_for", C.c_uint32, [C.c_uint32]),
     ("nrrs_rng_fill", None, [C.c_uint64, C.c_uint64, C.POINTER(C.c_float), C.c_uint64, C.c_float, C.c_float]),
     ("nrrs_root_path_key", C.c_uint64, [C.c_uint32, C.c_uint32]),

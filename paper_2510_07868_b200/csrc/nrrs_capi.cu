@@ -1977,6 +1977,28 @@ int nrrs_gpu_strategy_factor(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64
     return NRRS_OK;
 }
 
+int nrrs_gpu_encode_levels(nrrs_gpu_ctx *ctx, const float *d_p01, uint64_t n, float *d_planes,
+                           uint64_t plane_stride) {
+    if (!ctx || (n && (!d_p01 || !d_planes)) || plane_stride < n)
+        return ctx ? fail(ctx, NRRS_EINVAL, "encode_levels: null buffer or plane_stride < n") : NRRS_EINVAL;
+    if (!ctx->has_weights || ctx->variant != NRRS_VARIANT_AID || !ctx->rrs_half ||
+        (uint64_t)ctx->grid_rrs.table_size * 4u > kLevelSmemMax)
+        return fail(ctx, NRRS_ESTATE, "encode_levels: needs AID weights with fp16 tables that fit in shared memory");
+    if (!n)
+        return NRRS_OK;
+    CK(ctx, cudaSetDevice(ctx->device));
+    GridLevelParams gp{};
+    gp.p01 = d_p01;
+    gp.n = n;
+    gp.table = ctx->d_rrs_grid;
+    gp.g = ctx->grid_rrs;
+    gp.feat = reinterpret_cast<float2 *>(d_planes);
+    gp.feat_stride = plane_stride;
+    CK(ctx, launch_grid_levels(gp, ctx->num_sms, ctx->stream));
+    ctx->launches += 1;
+    return NRRS_OK;
+}
+
 int nrrs_gpu_predict_stats(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, float *d_stats) {
     if (!ctx || (n && !d_stats))
         return NRRS_EINVAL;

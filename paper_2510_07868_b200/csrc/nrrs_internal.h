@@ -330,7 +330,7 @@ struct GridLevelParams {
     float2 *feat;
     uint64_t feat_stride;
 };
-constexpr uint32_t kLevelSmemMax = 160u * 1024u;  // table bytes; + 48 KB of staged p01 blocks
+constexpr uint32_t kLevelSmemMax = 150u * 1024u;  // table bytes; + 72 KB of staged p01 blocks <= 227 KB
 cudaError_t launch_grid_levels(const GridLevelParams &p, int num_sms, cudaStream_t stream);
 cudaError_t launch_infer(int kind, const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out);
 uint32_t infer_max_grid(int num_sms);

@@ -303,6 +303,16 @@ class RrsStage:
         _capi.check(self.handle, self.ctx.lib.nrrs_gpu_predict_stats(self.handle, C.byref(soa), n, st.data_ptr()))
         return st
 
+    def encode_levels(self, p01: torch.Tensor) -> torch.Tensor:
+        """Batched HashGrid::encode (hashgrid.cpp:38-82) of the AID RRSNet grid through K-A0:
+        [levels, n, 2] level planes (fp16 tables staged in shared memory)."""
+        n = p01.numel() // 3
+        levels = self.nets.cfg.grid.levels if self.nets is not None else 0
+        planes = torch.empty((levels, n, 2), dtype=torch.float32, device=self.device)
+        _capi.check(self.handle, self.ctx.lib.nrrs_gpu_encode_levels(self.handle, p01.data_ptr(), n,
+                                                                     planes.data_ptr(), n))
+        return planes
+
     def close(self) -> None:
         self.ctx.close()
 

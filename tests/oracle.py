@@ -230,6 +230,17 @@ def strategy_factors(kind: int, v: dict, nets: OracleNets | None, eps_div: float
     return q
 
 
+def grid_encode(spec: GridSpec, theta: np.ndarray, p01: np.ndarray) -> np.ndarray:
+    """HashGrid::encode (hashgrid.cpp:38-82) per point: [n, levels * features] float32."""
+    L = lib()
+    theta = np.ascontiguousarray(theta, np.float32)
+    p01 = np.ascontiguousarray(p01, np.float32).reshape(-1, 3)
+    out = np.zeros((p01.shape[0], spec.levels * spec.features), np.float32)
+    for i in range(p01.shape[0]):
+        L.orc_grid_encode(C.byref(spec), ptr(theta), p01[i].ctypes.data, out[i].ctypes.data)
+    return out
+
+
 def predict_stats(nets: OracleNets, v: dict) -> np.ndarray:
     n = int(v["roughness"].shape[0])
     st = np.empty((n, 6), np.float32)

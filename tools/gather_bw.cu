@@ -53,6 +53,29 @@ __global__ void smem_gather(int entries, int iters, float *out) {
     if (acc == 12345.f) out[0] = acc;
 }
 
+// Random 4-byte (half2) / 8-byte loads from a 2^15-entry shared-memory table (the K-A0
+// level table), cheap LCG indices so the loads, not the index math, bind.
+template <typename T, int ILP>
+__global__ void smem_gather_pow2(uint32_t mask, int iters, float *out) {
+    extern __shared__ __align__(16) uint8_t raw2[];
+    T *tab2 = reinterpret_cast<T *>(raw2);
+    for (uint32_t i = threadIdx.x; i <= mask; i += blockDim.x) tab2[i] = T{};
+    __syncthreads();
+    uint32_t s[ILP];
+#pragma unroll
+    for (int k = 0; k < ILP; ++k) s[k] = hash(blockIdx.x * blockDim.x * ILP + threadIdx.x * ILP + k);
+    uint32_t acc = 0;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < ILP; ++k) {
+            s[k] = s[k] * 1664525u + 1013904223u;
+            const T v = tab2[(s[k] >> 9) & mask];
+            acc ^= *reinterpret_cast<const uint32_t *>(&v);
+        }
+    }
+    if (acc == 12345u) out[0] = (float)acc;
+}
+
 int main() {
     int sms = 0; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     int clk = 0; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
@@ -100,6 +123,29 @@ int main() {
         double cyc = ms * 1e-3 * clk * 1e3;
         printf("smem table %5d entries: %.2f G gathers/s, %.2f gathers/cycle/SM\n", entries, loads / ms / 1e6,
                loads / cyc / sms);
+    }
+    cudaFuncSetAttribute(smem_gather_pow2<uint32_t, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(smem_gather_pow2<uint2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    for (int width : {4, 8}) {
+        for (int warps : {16, 32}) {
+            const int blocks = sms, threads = warps * 32;
+            const uint32_t entries = width == 4 ? 32768u : 16384u;  // 128 KB either way
+            auto run = [&] {
+                if (width == 4)
+                    smem_gather_pow2<uint32_t, 8><<<blocks, threads, entries * 4>>>(entries - 1, iters, o);
+                else
+                    smem_gather_pow2<uint2, 8><<<blocks, threads, entries * 8>>>(entries - 1, iters, o);
+            };
+            run();
+            cudaEventRecord(a);
+            run();
+            cudaEventRecord(b); cudaEventSynchronize(b);
+            float ms; cudaEventElapsedTime(&ms, a, b);
+            double loads = (double)blocks * threads * iters * 8;
+            double cyc = ms * 1e-3 * clk * 1e3;
+            printf("smem %d-byte random loads, 128 KB table, warps/SM %2d: %.2f G loads/s, %.2f loads/cycle/SM\n",
+                   width, warps, loads / ms / 1e6, loads / cyc / sms);
+        }
     }
     printf("status %s (clock %d MHz)\n", cudaGetErrorString(cudaDeviceSynchronize()), clk / 1000);
     return 0;
