@@ -253,6 +253,22 @@ NRRS_API int nrrs_gpu_rrs_stage_host(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *h
                             const nrrs_stage_params *p, const nrrs_stage_out *h_out,
                             nrrs_stage_result *h_result);
 
+/* Asynchronous form of nrrs_gpu_rrs_stage_host for a stream of independent
+ * batches: enqueues the copies and the stage and returns a ticket.  Two calls
+ * may be in flight per context (double-buffered device staging): the inputs of
+ * call i+1 stream in while the outputs of call i stream out (PCIe is full
+ * duplex).  Host buffers must stay valid until nrrs_gpu_stage_host_wait returns
+ * for the ticket, and should be pinned for the copies to overlap.  h_out->slots
+ * receives the whole [2 * capacity] array; records [0, result.spawned) are valid.
+ * p->gain is taken as given: a caller running RateControl across calls applies
+ * the overflow of call i to the first call it issues after waiting for i.
+ * ESTATE when a third call is issued before the oldest one was waited for. */
+NRRS_API int nrrs_gpu_rrs_stage_host_async(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *h_v, uint64_t n,
+                                           const nrrs_stage_params *p, const nrrs_stage_out *h_out,
+                                           uint64_t *ticket);
+/* Blocks until the call `ticket` has finished and its outputs are in host memory. */
+NRRS_API int nrrs_gpu_stage_host_wait(nrrs_gpu_ctx *ctx, uint64_t ticket, nrrs_stage_result *h_result);
+
 /* ---- suffix side of trace_frame: film folds, reverse pass,
  * TrainSample emission, Film updates.  Bit-identical to the reference's sequential
  * f64 folds.  Device buffers; stream-ordered. */

@@ -140,6 +140,9 @@ SIGNATURES = [
                                      C.POINTER(StageOut), C.POINTER(StageResultC)]),
     ("nrrs_gpu_rrs_stage_host", C.c_int, [_P, C.POINTER(VertexSoA), C.c_uint64, C.POINTER(StageParams),
                                           C.POINTER(StageOut), C.POINTER(StageResultC)]),
+    ("nrrs_gpu_rrs_stage_host_async", C.c_int, [_P, C.POINTER(VertexSoA), C.c_uint64, C.POINTER(StageParams),
+                                                C.POINTER(StageOut), C.POINTER(C.c_uint64)]),
+    ("nrrs_gpu_stage_host_wait", C.c_int, [_P, C.c_uint64, C.POINTER(StageResultC)]),
     ("nrrs_gpu_stage_factors", C.c_int, [_P, C.POINTER(VertexSoA), C.c_uint64, C.POINTER(StageParams),
                                          C.POINTER(StageOut), _P]),
     ("nrrs_gpu_stage_decide", C.c_int, [_P, C.c_uint64, C.POINTER(StageParams), _P, C.c_int32,

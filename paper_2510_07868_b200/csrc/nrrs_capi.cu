@@ -150,6 +150,7 @@ struct DeviceBlob {
 };
 
 static constexpr int kMaxHostChunks = 8;
+static constexpr uint64_t kAsyncHostChunks = 1;  // nrrs_gpu_rrs_stage_host_async (NRRS_ASYNC_CHUNKS overrides)
 static constexpr uint32_t kChunkSums = 8;  // d_sum[8 ..] : per-chunk sums of the host path
 
 struct nrrs_gpu_ctx {
@@ -213,7 +214,17 @@ struct nrrs_gpu_ctx {
         uint32_t *offset = nullptr, *slots = nullptr;
         uint8_t *decided = nullptr;
         uint64_t cap = 0, cap_slots = 0;
-    } st;
+    } st, st_async[2];
+
+    // asynchronous host path (nrrs_gpu_rrs_stage_host_async): two staging sets, a D2H stream so
+    // call i's results go back while call i+1's inputs come in (PCIe is full duplex)
+    cudaStream_t d2h_stream = nullptr;
+    cudaEvent_t ev_kb_done[2] = {}, ev_d2h_done[2] = {};
+    DevResult *d_res_hist = nullptr;  // [2] per-set snapshot of d_res after K-B
+    DevResult *h_res_pinned = nullptr;  // [2] pinned host copies
+    uint64_t next_ticket = 0;
+    bool in_flight[2] = {false, false};
+    uint64_t set_ticket[2] = {0, 0};
 };
 
 static int fail(nrrs_gpu_ctx *ctx, int code, const char *fmt, ...) {
@@ -325,6 +336,23 @@ int nrrs_gpu_destroy(nrrs_gpu_ctx *ctx) {
     for (void *p : ptrs)
         if (p)
             cudaFree(p);
+    for (auto &S : ctx->st_async) {
+        void *sp[] = {S.p01, S.wo01, S.rough, S.weight, S.ipix, S.key, S.q_norm, S.q_real, S.q_orig, S.u,
+                      S.k, S.offset, S.slots, S.decided};
+        for (void *p : sp)
+            if (p)
+                cudaFree(p);
+    }
+    if (ctx->d2h_stream) {
+        cudaStreamSynchronize(ctx->d2h_stream);
+        cudaStreamDestroy(ctx->d2h_stream);
+        for (int b = 0; b < 2; ++b) {
+            cudaEventDestroy(ctx->ev_kb_done[b]);
+            cudaEventDestroy(ctx->ev_d2h_done[b]);
+        }
+        cudaFree(ctx->d_res_hist);
+        cudaFreeHost(ctx->h_res_pinned);
+    }
     if (ctx->copy_stream) {
         cudaStreamSynchronize(ctx->copy_stream);
         cudaStreamDestroy(ctx->copy_stream);
@@ -2027,16 +2055,11 @@ int nrrs_gpu_predict_stats(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t
 }
 
 // ---- host-buffer entry: H2D, stage, D2H ----
-int nrrs_gpu_rrs_stage_host(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *h, uint64_t n, const nrrs_stage_params *p,
-                            const nrrs_stage_out *ho, nrrs_stage_result *h_result) {
-    if (!ctx || !h || !ho || !ho->q_norm || !ho->q_real || !ho->slots)
-        return NRRS_EINVAL;
-    uint32_t cap = 0;
-    int rc = resolve_capacity(ctx, p, &cap);
-    if (rc)
-        return rc;
-    CK(ctx, cudaSetDevice(ctx->device));
-    auto &s = ctx->st;
+}  // extern "C"
+
+using Staging = decltype(nrrs_gpu_ctx::st);
+
+static int ensure_staging(nrrs_gpu_ctx *ctx, Staging &s, uint64_t n, uint32_t cap) {
     if (n > s.cap) {
         float **fp[] = {&s.p01, &s.wo01, &s.rough, &s.weight, &s.ipix, &s.q_norm, &s.q_real, &s.q_orig, &s.u};
         const int mult[] = {3, 2, 1, 3, 3, 1, 1, 1, 1};
@@ -2061,27 +2084,15 @@ int nrrs_gpu_rrs_stage_host(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *h, uint64_
         CK(ctx, cudaMalloc(&s.slots, (size_t)cap * 2 * sizeof(uint32_t)));
         s.cap_slots = cap;
     }
-    if (!h->i_pixel)
-        return fail(ctx, NRRS_EINVAL, "stage_host: pass i_pixel (gathered per vertex)");
-    if (n > 0xFFFFFFFFull)
-        return fail(ctx, NRRS_EINVAL, "stage: more than 2^32 vertices");
-    nrrs_stage_out dout{};
-    dout.q_norm = s.q_norm;
-    dout.q_real = s.q_real;
-    dout.slots = s.slots;
-    dout.k = ho->k ? s.k : nullptr;
-    dout.offset = ho->offset ? s.offset : nullptr;
-    dout.decided = ho->decided ? s.decided : nullptr;
-    dout.q_orig = s.q_orig;
-    dout.u = s.u;
-    nrrs_stage_result r{};
-    if (n == 0) {
-        rc = nrrs_gpu_rrs_stage(ctx, nullptr, 0, p, &dout, &r);
-        if (!rc && h_result)
-            *h_result = r;
-        return rc;
-    }
-    rc = ensure_scratch(ctx, n);
+    return NRRS_OK;
+}
+
+// Enqueues H2D (chunked, copy_stream) + K-A per chunk + K-B (stream) for the staging set `s`.
+// `inputs_free` (optional) is an event the H2D must wait for before overwriting `s`.
+static int enqueue_host_stage(nrrs_gpu_ctx *ctx, Staging &s, const nrrs_vertex_soa *h, uint64_t n,
+                              const nrrs_stage_params *p, uint32_t cap, nrrs_stage_out *dout,
+                              cudaEvent_t inputs_free, uint64_t max_chunks) {
+    int rc = ensure_scratch(ctx, n);
     if (rc)
         return rc;
     // Pipeline: chunk c's H2D (copy_stream) overlaps K-A of chunks < c (stream).  Each chunk's K-A
@@ -2095,12 +2106,16 @@ int nrrs_gpu_rrs_stage_host(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *h, uint64_
     }
     const uint64_t min_chunk = 1ull << 17;
     uint64_t nc = n < 2 * min_chunk ? 1 : (n + min_chunk - 1) / min_chunk;
-    if (nc > (uint64_t)kMaxHostChunks)
-        nc = kMaxHostChunks;
+    if (nc > max_chunks)
+        nc = max_chunks;
     const uint64_t chunk = ((n + nc - 1) / nc + 127) / 128 * 128;
     nc = (n + chunk - 1) / chunk;
-    CK(ctx, cudaEventRecord(ctx->ev_start, ctx->stream));  // staging buffers free once prior work is done
-    CK(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_start, 0));
+    if (inputs_free) {
+        CK(ctx, cudaStreamWaitEvent(ctx->copy_stream, inputs_free, 0));
+    } else {
+        CK(ctx, cudaEventRecord(ctx->ev_start, ctx->stream));  // staging buffers free once prior work is done
+        CK(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_start, 0));
+    }
     double *chunk_sums = ctx->d_sum + kChunkSums;
     for (uint64_t c = 0; c < nc; ++c) {
         const uint64_t base = c * chunk, cn = n - base < chunk ? n - base : chunk;
@@ -2128,14 +2143,76 @@ int nrrs_gpu_rrs_stage_host(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *h, uint64_
         dv.weight = h->weight ? s.weight + 3 * base : nullptr;
         dv.i_pixel = s.ipix + 3 * base;
         dv.path_key = h->path_key ? s.key + base : nullptr;
-        rc = run_factors(ctx, &dv, cn, p, s.q_orig + base, s.u + base, dout.decided ? dout.decided + base : nullptr,
+        rc = run_factors(ctx, &dv, cn, p, s.q_orig + base, s.u + base, dout->decided ? dout->decided + base : nullptr,
                          chunk_sums + c, c > 0);
         if (rc) {
             cudaStreamSynchronize(ctx->copy_stream);
             return rc;
         }
     }
-    rc = run_decide(ctx, n, p, s.q_orig, s.u, chunk_sums, (int)nc, p->n_pixels, cap, &dout, ctx->d_total, ctx->d_res);
+    return run_decide(ctx, n, p, s.q_orig, s.u, chunk_sums, (int)nc, p->n_pixels, cap, dout, ctx->d_total, ctx->d_res);
+}
+
+static int check_host_call(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *h, uint64_t n, const nrrs_stage_out *ho) {
+    if (!h || !ho || !ho->q_norm || !ho->q_real || !ho->slots)
+        return fail(ctx, NRRS_EINVAL, "stage_host: null vertex SoA or required output (q_norm, q_real, slots)");
+    if (n && !h->i_pixel)
+        return fail(ctx, NRRS_EINVAL, "stage_host: pass i_pixel (gathered per vertex)");
+    if (n > 0xFFFFFFFFull)
+        return fail(ctx, NRRS_EINVAL, "stage: more than 2^32 vertices");
+    return NRRS_OK;
+}
+
+static nrrs_stage_out staging_out(const Staging &s, const nrrs_stage_out *ho) {
+    nrrs_stage_out dout{};
+    dout.q_norm = s.q_norm;
+    dout.q_real = s.q_real;
+    dout.slots = s.slots;
+    dout.k = ho->k ? s.k : nullptr;
+    dout.offset = ho->offset ? s.offset : nullptr;
+    dout.decided = ho->decided ? s.decided : nullptr;
+    dout.q_orig = s.q_orig;
+    dout.u = s.u;
+    return dout;
+}
+
+static void to_result(const DevResult &r, nrrs_stage_result *h) {
+    h->f_norm = r.f_norm;
+    h->sum_q = r.sum_q;
+    h->total = r.total;
+    h->dropped = r.dropped;
+    h->nonfinite = r.nonfinite;
+    h->box_cox_clamps = r.box_cox_clamps;
+    h->spawned = r.spawned;
+    h->overflow = r.overflow;
+}
+
+extern "C" {
+
+int nrrs_gpu_rrs_stage_host(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *h, uint64_t n, const nrrs_stage_params *p,
+                            const nrrs_stage_out *ho, nrrs_stage_result *h_result) {
+    if (!ctx)
+        return NRRS_EINVAL;
+    int rc = check_host_call(ctx, h, n, ho);
+    uint32_t cap = 0;
+    if (!rc)
+        rc = resolve_capacity(ctx, p, &cap);
+    if (rc)
+        return rc;
+    CK(ctx, cudaSetDevice(ctx->device));
+    auto &s = ctx->st;
+    rc = ensure_staging(ctx, s, n, cap);
+    if (rc)
+        return rc;
+    nrrs_stage_out dout = staging_out(s, ho);
+    nrrs_stage_result r{};
+    if (n == 0) {
+        rc = nrrs_gpu_rrs_stage(ctx, nullptr, 0, p, &dout, &r);
+        if (!rc && h_result)
+            *h_result = r;
+        return rc;
+    }
+    rc = enqueue_host_stage(ctx, s, h, n, p, cap, &dout, nullptr, kMaxHostChunks);
     if (rc)
         return rc;
     auto d2h = [&](void *dst, const void *src, size_t bytes) -> int {
@@ -2158,6 +2235,92 @@ int nrrs_gpu_rrs_stage_host(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *h, uint64_
     CK(ctx, cudaStreamSynchronize(ctx->stream));
     if (h_result)
         *h_result = r;
+    return NRRS_OK;
+}
+
+int nrrs_gpu_rrs_stage_host_async(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *h, uint64_t n,
+                                  const nrrs_stage_params *p, const nrrs_stage_out *ho, uint64_t *ticket) {
+    if (!ctx || !ticket)
+        return NRRS_EINVAL;
+    int rc = check_host_call(ctx, h, n, ho);
+    uint32_t cap = 0;
+    if (!rc)
+        rc = resolve_capacity(ctx, p, &cap);
+    if (rc)
+        return rc;
+    if (n == 0)
+        return fail(ctx, NRRS_EINVAL, "stage_host_async: empty batch (use nrrs_gpu_rrs_stage_host)");
+    const uint64_t t = ctx->next_ticket;
+    const int b = (int)(t & 1u);
+    if (ctx->in_flight[b])
+        return fail(ctx, NRRS_ESTATE, "stage_host_async: wait for ticket %llu before issuing another call",
+                    (unsigned long long)ctx->set_ticket[b]);
+    CK(ctx, cudaSetDevice(ctx->device));
+    if (!ctx->d2h_stream) {
+        CK(ctx, cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            CK(ctx, cudaEventCreateWithFlags(&ctx->ev_kb_done[i], cudaEventDisableTiming));
+            CK(ctx, cudaEventCreateWithFlags(&ctx->ev_d2h_done[i], cudaEventDisableTiming));
+            CK(ctx, cudaEventRecord(ctx->ev_d2h_done[i], ctx->d2h_stream));
+        }
+        CK(ctx, cudaMalloc(&ctx->d_res_hist, 2 * sizeof(DevResult)));
+        CK(ctx, cudaMallocHost(&ctx->h_res_pinned, 2 * sizeof(DevResult)));
+    }
+    Staging &s = ctx->st_async[b];
+    rc = ensure_staging(ctx, s, n, cap);
+    if (rc)
+        return rc;
+    nrrs_stage_out dout = staging_out(s, ho);
+    // set b is free once the D2H of the call that last used it is done
+    // two calls in flight already overlap the copies with the other call's kernels: fewer, larger H2D
+    // pieces (each cudaMemcpyAsync costs a few microseconds of link time)
+    const char *mc = std::getenv("NRRS_ASYNC_CHUNKS");
+    rc = enqueue_host_stage(ctx, s, h, n, p, cap, &dout, ctx->ev_d2h_done[b],
+                            mc ? (uint64_t)std::max(1, std::min(std::atoi(mc), kMaxHostChunks)) : kAsyncHostChunks);
+    if (rc)
+        return rc;
+    // snapshot the scalars before the next call's K-A reuses d_res, then hand set b to the D2H stream
+    CK(ctx, cudaMemcpyAsync(ctx->d_res_hist + b, ctx->d_res, sizeof(DevResult), cudaMemcpyDeviceToDevice,
+                            ctx->stream));
+    CK(ctx, cudaEventRecord(ctx->ev_kb_done[b], ctx->stream));
+    CK(ctx, cudaStreamWaitEvent(ctx->d2h_stream, ctx->ev_kb_done[b], 0));
+    auto d2h = [&](void *dst, const void *src, size_t bytes) -> int {
+        if (dst && bytes)
+            CK(ctx, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->d2h_stream));
+        return NRRS_OK;
+    };
+    rc = d2h(ho->q_norm, s.q_norm, n * 4);
+    if (!rc) rc = d2h(ho->q_real, s.q_real, n * 4);
+    if (!rc) rc = d2h(ho->k, s.k, n * 4);
+    if (!rc) rc = d2h(ho->offset, s.offset, n * 4);
+    if (!rc) rc = d2h(ho->decided, s.decided, n);
+    if (!rc) rc = d2h(ho->q_orig, s.q_orig, n * 4);
+    if (!rc) rc = d2h(ho->u, s.u, n * 4);
+    // the spawned count is not known on the host yet: the whole slot array comes back (the D2H
+    // direction has headroom while the next call's inputs stream in); [0, spawned) is valid
+    if (!rc) rc = d2h(ho->slots, s.slots, (size_t)cap * 8);
+    if (!rc) rc = d2h(ctx->h_res_pinned + b, ctx->d_res_hist + b, sizeof(DevResult));
+    if (rc)
+        return rc;
+    CK(ctx, cudaEventRecord(ctx->ev_d2h_done[b], ctx->d2h_stream));
+    ctx->in_flight[b] = true;
+    ctx->set_ticket[b] = t;
+    ctx->next_ticket = t + 1;
+    *ticket = t;
+    return NRRS_OK;
+}
+
+int nrrs_gpu_stage_host_wait(nrrs_gpu_ctx *ctx, uint64_t ticket, nrrs_stage_result *h_result) {
+    if (!ctx)
+        return NRRS_EINVAL;
+    const int b = (int)(ticket & 1u);
+    if (!ctx->in_flight[b] || ctx->set_ticket[b] != ticket)
+        return fail(ctx, NRRS_EINVAL, "stage_host_wait: ticket %llu is not in flight", (unsigned long long)ticket);
+    CK(ctx, cudaSetDevice(ctx->device));
+    CK(ctx, cudaEventSynchronize(ctx->ev_d2h_done[b]));
+    ctx->in_flight[b] = false;
+    if (h_result)
+        to_result(ctx->h_res_pinned[b], h_result);
     return NRRS_OK;
 }
 

@@ -509,6 +509,9 @@ struct Side {        // 32 B per tile row
 // NRRS_MMA3 = 1: three N-wide MMAs per K16 slice accumulate A_hi*W_hi + A_lo*W_hi +
 // A_hi*W_lo into ONE 32-column accumulator (same tensor work as the N = 2N form; the
 // epilogue reads half the TMEM columns and skips the hi + lo add).
+#ifndef NRRS_MMA_WAIT_HINT
+#define NRRS_MMA_WAIT_HINT 0  // ns suspend hint of the MLP groups' MMA-completion wait (0: plain try_wait loop)
+#endif
 #ifndef NRRS_MMA3
 #define NRRS_MMA3 1
 #endif
@@ -981,7 +984,11 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
                     const uint32_t col_d = Cfg::kColD + ws::kDCols * (uint32_t)q;
                     const uint32_t col_a = Cfg::kColSlots + 32u * slot[c];
                     if (rec) t0 = clock64();
+#if NRRS_MMA_WAIT_HINT
+                    mbar_wait_sleep(&st->mma_bar[q], (phases >> c) & 1u, NRRS_MMA_WAIT_HINT);
+#else
                     mbar_wait(&st->mma_bar[q], (phases >> c) & 1u);
+#endif
                     phases ^= 1u << c;
                     tc_fence_after();
                     if (rec) { const unsigned long long t1 = clock64(); c_wait += t1 - t0; t0 = t1; }

@@ -274,6 +274,37 @@ class RrsStage:
             rc.note_overflow()
         return out, res
 
+    def _host_args(self, vertices, out, n):
+        def hp(name, src):
+            a = src.get(name)
+            return a.ctypes.data if a is not None else None
+        soa = _capi.VertexSoA(hp("p01", vertices), hp("wo01", vertices), hp("roughness", vertices),
+                              hp("weight", vertices), hp("i_pixel", vertices), hp("path_key", vertices), None, None)
+        oc = _capi.StageOut(hp("q_norm", out), hp("q_real", out), hp("slots", out), hp("k", out), hp("offset", out),
+                            hp("decided", out), hp("q_orig", out), hp("u", out))
+        return soa, oc
+
+    def submit_host(self, vertices: Dict[str, np.ndarray], depth: int, strategy: Strategy, gain: float = 1.0,
+                    eps_div: float = 0.0, out: Optional[Dict[str, np.ndarray]] = None):
+        """Asynchronous host-buffer stage (nrrs_gpu_rrs_stage_host_async) for a stream of independent
+        batches: returns (ticket, out).  Two calls may be in flight; keep `vertices` and `out` alive
+        (pinned) until wait_host(ticket).  out["slots"] receives all `capacity` records."""
+        n = int(vertices["roughness"].shape[0]) if "roughness" in vertices else vertices["p01"].size // 3
+        if out is None:
+            out = {"q_norm": np.empty(n, np.float32), "q_real": np.empty(n, np.float32),
+                   "slots": np.empty((self.capacity, 2), np.uint32)}
+        p = self.params(depth, strategy, gain, eps_div)
+        soa, oc = self._host_args(vertices, out, n)
+        t = C.c_uint64(0)
+        _capi.check(self.handle, self.ctx.lib.nrrs_gpu_rrs_stage_host_async(self.handle, C.byref(soa), n, C.byref(p),
+                                                                            C.byref(oc), C.byref(t)))
+        return int(t.value), out
+
+    def wait_host(self, ticket: int) -> "StageResult":
+        r = _capi.StageResultC()
+        _capi.check(self.handle, self.ctx.lib.nrrs_gpu_stage_host_wait(self.handle, int(ticket), C.byref(r)))
+        return StageResult.from_c(r)
+
     def compact(self, records: torch.Tensor, used: torch.Tensor, count: int, out: torch.Tensor,
                 d_count: Optional[torch.Tensor] = None, sync: bool = True) -> Optional[int]:
         """Order-preserving compaction of filled slots (wavefront.cpp:488-497).

@@ -488,3 +488,43 @@ def test_aid_stage_with_and_without_level_kernel(c1_vertices, monkeypatch):
         outs.append(_np(out.q_orig))
         st.close()
     assert rel_err(outs[0], outs[1], 1e-6).max() <= 2e-4
+
+
+def test_host_buffer_async_pipeline_matches_sync(nets):
+    """nrrs_gpu_rrs_stage_host_async: three different multi-chunk batches issued with two in
+    flight (inputs of one call streaming in while the previous call's outputs stream out) give
+    exactly the synchronous host path's outputs for each batch; a third concurrent call and a
+    stale ticket are refused."""
+    n = 300_007
+    st = _stage(n, nets)
+    kind = StrategyKind.AidNrrs if nets.variant == orc.VARIANT_AID else StrategyKind.Nrrs
+    batches = []
+    for f in range(3):
+        v = orc.gen_vertices(n, frame=f)
+        batches.append({k: torch.from_numpy(np.ascontiguousarray(a).view(np.int64) if a.dtype == np.uint64
+                                            else np.ascontiguousarray(a)).pin_memory().numpy()
+                        for k, a in v.items() if k != "pixel"})
+        batches[-1]["path_key"] = batches[-1]["path_key"].view(np.uint64)
+    refs = [st.run_host(b, 2, Strategy(kind), rc=RateControl()) for b in batches]
+
+    def pinned_out():
+        return {"q_norm": torch.empty(n, dtype=torch.float32).pin_memory().numpy(),
+                "q_real": torch.empty(n, dtype=torch.float32).pin_memory().numpy(),
+                "slots": torch.empty((st.capacity, 2), dtype=torch.int32).pin_memory().numpy().view(np.uint32)}
+    gain = RateControl().gain()
+    t0, o0 = st.submit_host(batches[0], 2, Strategy(kind), gain, out=pinned_out())
+    t1, o1 = st.submit_host(batches[1], 2, Strategy(kind), gain, out=pinned_out())
+    with pytest.raises(RuntimeError, match="wait for ticket"):
+        st.submit_host(batches[2], 2, Strategy(kind), gain, out=pinned_out())
+    r0 = st.wait_host(t0)
+    t2, o2 = st.submit_host(batches[2], 2, Strategy(kind), gain, out=pinned_out())
+    r1 = st.wait_host(t1)
+    r2 = st.wait_host(t2)
+    with pytest.raises(RuntimeError, match="not in flight"):
+        st.wait_host(t2)
+    for (ref_out, ref_res), out, res in zip(refs, (o0, o1, o2), (r0, r1, r2)):
+        assert res.spawned == ref_res.spawned and res.total == ref_res.total and res.dropped == ref_res.dropped
+        assert res.f_norm == ref_res.f_norm and res.nonfinite == ref_res.nonfinite
+        np.testing.assert_array_equal(out["q_norm"], ref_out["q_norm"])
+        np.testing.assert_array_equal(out["q_real"], ref_out["q_real"])
+        np.testing.assert_array_equal(out["slots"][:res.spawned], ref_out["slots"][:ref_res.spawned])

@@ -25,9 +25,13 @@ out = st.alloc_outputs(n)
 for _ in range(reps):
     st.run(dv, 2, Strategy(strat), rc=RateControl(), out=out, sync=False)
 torch.cuda.synchronize()
-a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-a.record()
-st.run(dv, 2, Strategy(strat), rc=RateControl(), out=out, sync=False)
-b.record()
-torch.cuda.synchronize()
-print(f"{kind} n={n}: stage {a.elapsed_time(b):.3f} ms")
+times = []
+for _ in range(max(reps, 1)):
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    st.run(dv, 2, Strategy(strat), rc=RateControl(), out=out, sync=False)
+    b.record()
+    torch.cuda.synchronize()
+    times.append(a.elapsed_time(b))
+times.sort()
+print(f"{kind} n={n}: stage {times[len(times) // 2]:.3f} ms (median of {len(times)}, min {times[0]:.3f})")
