@@ -1272,7 +1272,6 @@ __device__ __forceinline__ uint32_t block_scan_excl(uint32_t v, uint32_t *warp_t
 
 struct Decide2Smem {
     uint32_t k[kBTile];
-    uint32_t incl[kBSub];
     uint32_t warp_tot[kBT / 32];
     unsigned long long prefix;
     uint32_t tile, epoch;
@@ -1391,14 +1390,6 @@ __global__ void __launch_bounds__(kBT) decide2_kernel(DecideParams p) {
         uint32_t sagg = 0;
         const uint32_t texcl = block_scan_excl<kBT>(ts, sm.warp_tot, sagg);
         {
-            uint32_t run = texcl;
-#pragma unroll
-            for (int i = 0; i < kBItems; ++i) {
-                run += k[i];
-                sm.incl[tid * kBItems + i] = run;
-            }
-        }
-        {
             // offsets (wavefront.cpp:148) and this thread's slot records: child c of
             // item j lands in slot cum + c while cum + c < capacity (:421-425, :436)
             uint64_t cum = sub_base + texcl;
@@ -1467,12 +1458,37 @@ __global__ void __launch_bounds__(kBT) compact2_kernel(CompactParams p) {
     for (int sub = 0; sub < kBSubs; ++sub) {
         const uint64_t first = tbase + (uint64_t)sub * kSub + (uint64_t)tid * IPT;
         uint32_t m = 0;
+        if (IPT == 4 && first + 4 <= count && (reinterpret_cast<uintptr_t>(p.used + first) & 3u) == 0) {
+            const uint32_t w4 = __ldcs(reinterpret_cast<const unsigned int *>(p.used + first));
 #pragma unroll
-        for (int i = 0; i < IPT; ++i)
-            if (first + i < count && p.used[first + i])
-                m |= 1u << i;
+            for (int i = 0; i < 4; ++i)
+                m |= ((w4 >> (8 * i)) & 0xffu) ? (1u << i) : 0u;
+        } else {
+#pragma unroll
+            for (int i = 0; i < IPT; ++i)
+                if (first + i < count && p.used[first + i])
+                    m |= 1u << i;
+        }
         masks[sub * kBT + tid] = (uint8_t)m;
         my_cnt += __popc(m);
+    }
+    const uint32_t *in = reinterpret_cast<const uint32_t *>(p.in);
+    // slot records (W = 2): every sub-tile's records are requested now, so their HBM round trip
+    // overlaps the block scan and the look-back instead of following it sub-tile by sub-tile
+    constexpr bool kVec = W == 2 && IPT == 4;
+    constexpr int kPre = kVec ? kBSubs : 1;
+    uint4 pre[kPre][2];
+    const bool vec_ok = kVec && (reinterpret_cast<uintptr_t>(in) & 15u) == 0;
+    if (kVec) {
+#pragma unroll
+        for (int sub = 0; sub < kPre; ++sub) {
+            const uint64_t first = tbase + (uint64_t)sub * kSub + (uint64_t)tid * IPT;
+            if (vec_ok && first + 4 <= count && masks[sub * kBT + tid]) {
+                const uint4 *in4 = reinterpret_cast<const uint4 *>(in + first * 2);
+                pre[sub][0] = __ldcs(in4);
+                pre[sub][1] = __ldcs(in4 + 1);
+            }
+        }
     }
     uint32_t agg = 0;
     block_scan_excl<kBT>(my_cnt, warp_tot, agg);
@@ -1483,27 +1499,45 @@ __global__ void __launch_bounds__(kBT) compact2_kernel(CompactParams p) {
     }
     __syncthreads();
     uint64_t out_base = *prefix;
-    const uint32_t *in = reinterpret_cast<const uint32_t *>(p.in);
     // pass 2: stage kept records of each sub-tile in smem, write them coalesced
-#pragma unroll 1
+#pragma unroll
     for (int sub = 0; sub < kBSubs; ++sub) {
         const uint64_t first = tbase + (uint64_t)sub * kSub + (uint64_t)tid * IPT;
         const uint32_t m = masks[sub * kBT + tid];
         uint32_t sagg = 0;
         uint32_t pos = block_scan_excl<kBT>(__popc(m), warp_tot, sagg);
+        if (kVec && vec_ok && m && first + 4 <= count) {
+            // 4 slot records = 32 contiguous bytes, loaded above as two 16-byte requests
+            const uint4 a = pre[kVec ? sub : 0][0], b = pre[kVec ? sub : 0][1];
+            const uint2 rec[4] = {make_uint2(a.x, a.y), make_uint2(a.z, a.w), make_uint2(b.x, b.y),
+                                  make_uint2(b.z, b.w)};
+            uint2 *st2 = reinterpret_cast<uint2 *>(stage);
 #pragma unroll
-        for (int i = 0; i < IPT; ++i) {
-            if (m & (1u << i)) {
+            for (int i = 0; i < 4; ++i)
+                if (m & (1u << i))
+                    st2[pos++] = rec[i];
+        } else {
 #pragma unroll
-                for (int w = 0; w < W; ++w)
-                    stage[pos * W + w] = __ldcs(in + (first + i) * W + w);
-                ++pos;
+            for (int i = 0; i < IPT; ++i) {
+                if (m & (1u << i)) {
+#pragma unroll
+                    for (int w = 0; w < W; ++w)
+                        stage[pos * W + w] = __ldcs(in + (first + i) * W + w);
+                    ++pos;
+                }
             }
         }
         __syncthreads();
-        uint32_t *out = reinterpret_cast<uint32_t *>(p.out) + out_base * W;
-        for (uint32_t w = tid; w < sagg * W; w += kBT)
-            __stcs(out + w, stage[w]);
+        if (W == 2) {
+            uint2 *out2 = reinterpret_cast<uint2 *>(p.out) + out_base;
+            const uint2 *st2 = reinterpret_cast<const uint2 *>(stage);
+            for (uint32_t r = tid; r < sagg; r += kBT)
+                __stcs(out2 + r, st2[r]);
+        } else {
+            uint32_t *out = reinterpret_cast<uint32_t *>(p.out) + out_base * W;
+            for (uint32_t w = tid; w < sagg * W; w += kBT)
+                __stcs(out + w, stage[w]);
+        }
         out_base += sagg;
         __syncthreads();
     }
