@@ -1199,6 +1199,270 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
     }
 }
 
+// ===========================================================================
+// K-A, AID over level planes, no encoder warps: GM groups of 4 warps (one thread per tile
+// row) each run a tile end to end -- load the row's 8 level planes and tail inputs, tail
+// encodings, fp16 hi/lo layer-0 A into the group's own TMEM columns, then the 4-layer
+// tcgen05 chain and the head -- so GM chains are in flight per SM instead of one per MLP
+// group behind shared encoder groups.  TMEM: per group 32 accumulator + 32 A columns.
+// ===========================================================================
+template <int GM>
+__global__ void __launch_bounds__(GM * 128, 1) infer_aid_fused_kernel(InferParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem_w = smem_raw;
+    ws::SmemTail *st = reinterpret_cast<ws::SmemTail *>(smem_raw + ((p.blob_bytes + 127u) & ~127u));
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int kThreads = GM * 128;
+    static_assert(GM * 64 <= 512 && GM <= 8, "TMEM: 64 columns per group");
+    {
+        const uint4 *src = reinterpret_cast<const uint4 *>(p.blob);
+        uint4 *dst = reinterpret_cast<uint4 *>(smem_w);
+        for (uint32_t i = tid; i < p.blob_bytes / 16u; i += kThreads)
+            dst[i] = __ldg(src + i);
+    }
+    if (tid == 0) {
+        const NetDesc &nd = p.nets.rrs;
+        for (int l = 0; l < 4; ++l) {
+            const LayerDesc &L = nd.layer[l];
+            st->idesc_n[1][l] = make_idesc_f16(L.N);
+            st->idesc_2n[1][l] = make_idesc_f16(2u * L.N);
+            st->nslices[1][l] = (uint32_t)L.K / 16u;
+            st->bias[1][l] = L.bias;
+            const uint32_t sbo = (uint32_t)L.K * 16u;
+            for (int k = 0; k < 2; ++k) {
+                st->wdesc[1][l][k] = make_smem_desc(smem_u32(smem_w + L.w_hi) + 256u * k, 128u, sbo);
+                st->wdesc_lo[1][l][k] =
+                    make_smem_desc(smem_u32(smem_w + L.w_hi) + 256u * k + ((uint32_t)L.N / 8u) * sbo, 128u, sbo);
+            }
+        }
+        for (int q = 0; q < GM; ++q)
+            mbar_init(&st->mma_bar[q], 1);
+        fence_barrier_init();
+    }
+    if (warp == 0)
+        tmem_alloc(&st->tmem_base, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = st->tmem_base;
+    const uint32_t lane_base = tmem_base + ((uint32_t)((warp & 3) * 32) << 16);
+    const int g = tid >> 7, r = tid & 127;
+    const bool issuer = r == 0;
+    const uint32_t bar_id = 1u + (uint32_t)g;
+    const uint32_t col_d = 64u * (uint32_t)g, col_a = col_d + 32u;
+
+    const uint64_t n = p.n;
+    const uint64_t num_tiles = (n + kTileM - 1) / kTileM;
+    const uint64_t t_begin = num_tiles * blockIdx.x / gridDim.x;
+    const uint64_t t_end = num_tiles * (blockIdx.x + 1) / gridDim.x;
+    const uint32_t T = (uint32_t)(t_end - t_begin);
+    double my_sum = 0.0;
+    uint32_t my_nonfinite = 0, my_bc = 0;
+    const bool depth1 = p.depth == 1u;
+    const int levels = p.grid_rrs.levels;
+    uint32_t phase = 0;
+
+    for (uint32_t i = (uint32_t)g; i < T; i += GM) {
+        const uint64_t j = (t_begin + i) * kTileM + r;
+        const bool valid = j < n;
+        // ---- row inputs: level planes + tail inputs ----
+        float f[16];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            float2 v = make_float2(0.0f, 0.0f);
+            if (valid && q < levels)
+                v = __ldcs(p.feat + (uint64_t)q * p.feat_stride + j);
+            f[2 * q] = v.x;
+            f[2 * q + 1] = v.y;
+        }
+        float wx = 0, wy = 0, wz = 0, wox = 0, woy = 0, ia = 0, ib = 0, ic = 0, rough = 0;
+        uint64_t key = 0;
+        if (valid) {
+            wx = __ldg(p.weight + 3 * j); wy = __ldg(p.weight + 3 * j + 1); wz = __ldg(p.weight + 3 * j + 2);
+            wox = __ldg(p.wo01 + 2 * j); woy = __ldg(p.wo01 + 2 * j + 1);
+            if (p.i_pixel) {
+                ia = __ldg(p.i_pixel + 3 * j); ib = __ldg(p.i_pixel + 3 * j + 1); ic = __ldg(p.i_pixel + 3 * j + 2);
+            } else {
+                const uint64_t px_idx = __ldg(p.pixel + j);
+                ia = __ldg(p.i_acc + 3 * px_idx); ib = __ldg(p.i_acc + 3 * px_idx + 1); ic = __ldg(p.i_acc + 3 * px_idx + 2);
+            }
+            rough = __ldg(p.roughness + j);
+            key = __ldg(p.path_key + j);
+        }
+        const bool active = valid && (p.gate ? (!depth1 && luminance(wx, wy, wz) > 0.0f) : true);
+        // ---- layer-0 input (build_aid_tail, networks.cpp:149-157) in the packed K order ----
+        uint32_t bc = 0;
+        float x0[16], x1[16];  // K columns [0,16): grid 0-7 | tail 0-7; [16,32): grid 8-15 | tail 8-15
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            x0[q] = f[q];
+            x1[q] = f[8 + q];
+        }
+        one_blob_fast<4>(wox, x0 + 8);
+        one_blob_fast<4>(woy, x0 + 12);
+        x1[8] = box_cox(wx, bc);
+        x1[9] = box_cox(wy, bc);
+        x1[10] = box_cox(wz, bc);
+        x1[11] = box_cox(mean3(ia, ib, ic), bc);
+        one_blob_fast<4>(remap_fast(rough), x1 + 12);
+        if (!valid) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                x0[q] = x1[q] = 0.0f;
+        }
+        if (active)
+            my_bc += bc;
+        // the group's previous tile finished reading D and A before the barrier below
+        ws::ws_store_a16(lane_base, col_a, 0, x0);
+        ws::ws_store_a16(lane_base, col_a, 1, x1);
+        tmem_wait_st();
+        tc_fence_before();
+        named_bar_sync(bar_id, 128);
+        if (issuer)
+            ws::ws_issue(st, 1, 0, tmem_base, col_a, col_d, &st->mma_bar[g]);
+        // ---- 4-layer chain ----
+#pragma unroll 1
+        for (int l = 0; l < 4; ++l) {
+            mbar_wait(&st->mma_bar[g], phase);
+            phase ^= 1u;
+            tc_fence_after();
+            const uint32_t boff = st->bias[1][l];
+            const float *bias = boff == kNoBias ? nullptr : reinterpret_cast<const float *>(smem_w + boff);
+            if (l < 3) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    float z[16];
+                    ws::ws_load_sum16(lane_base, col_d, 32u, 16u * (uint32_t)h, bias, z);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {  // leaky ReLU = cwiseMax(z, slope z)
+                        const float2 t = upk2(fmul2(pk2(z[2 * q], z[2 * q + 1]), pk2(0.01f, 0.01f)));
+                        z[2 * q] = fmaxf(z[2 * q], t.x);
+                        z[2 * q + 1] = fmaxf(z[2 * q + 1], t.y);
+                    }
+                    ws::ws_store_a16(lane_base, col_a, h, z);
+                }
+                tmem_wait_st();
+                tc_fence_before();
+                named_bar_sync(bar_id, 128);
+                if (issuer)
+                    ws::ws_issue(st, 1, l + 1, tmem_base, col_a, col_d, &st->mma_bar[g]);
+            } else {
+                float y[16];
+                ws::ws_load_sum16(lane_base, col_d, 16u, 0u, bias, y);  // head: N = 16
+                tc_fence_before();
+                float qv = softplus_mod(y[0]);
+                uint32_t decided = active ? 1u : 0u;
+                if (p.gate) {
+                    if (valid && depth1)
+                        qv = 1.0f;
+                    if (!active && !depth1)
+                        qv = 0.0f;
+                    decided = valid && (depth1 || active) ? 1u : 0u;
+                    if (valid && (!isfinite(qv) || qv < 0.0f)) {  // sanitize (wavefront.cpp:381-385)
+                        qv = 0.0f;
+                        decided = 0;
+                        ++my_nonfinite;
+                    }
+                }
+                if (valid) {
+                    p.q_out[j] = qv;
+                    if (p.u_out)
+                        p.u_out[j] = rrs_uniform(p.mixed_seed, key, p.depth);
+                    if (p.decided_out)
+                        p.decided_out[j] = (uint8_t)decided;
+                    my_sum += (double)qv;
+                }
+            }
+        }
+    }
+
+    // ---- teardown + deterministic CTA reduction, then last-CTA-done ----
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0)
+        tmem_dealloc(tmem_base, 512);
+    if (p.parts == nullptr)
+        return;
+    {
+        double sv = my_sum;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+            sv += __shfl_xor_sync(0xffffffffu, sv, o);
+        const uint32_t nf = __reduce_add_sync(0xffffffffu, my_nonfinite);
+        const uint32_t bcs = __reduce_add_sync(0xffffffffu, my_bc);
+        if (lane == 0) {
+            st->red_sum[warp] = sv;
+            st->red_nf[warp] = nf;
+            st->red_bc[warp] = bcs;
+        }
+        __syncthreads();
+    }
+    constexpr int kWarps = kThreads / 32;
+    if (tid == 0) {
+        double cs = 0.0;
+        uint32_t cn = 0, cb = 0;
+        for (int w = 0; w < kWarps; ++w) {
+            cs += st->red_sum[w];
+            cn += st->red_nf[w];
+            cb += st->red_bc[w];
+        }
+        p.parts[blockIdx.x] = cs;
+        p.part_counts[2 * blockIdx.x] = cn;
+        p.part_counts[2 * blockIdx.x + 1] = cb;
+        __threadfence();
+        st->is_last = atomicAdd(p.counter, 1u) == gridDim.x - 1 ? 1u : 0u;
+    }
+    __syncthreads();
+    if (!st->is_last)
+        return;
+    __threadfence();
+    if (warp == 0) {
+        double sv = 0.0;
+        uint32_t nf = 0, bcs = 0;
+        for (uint32_t b = lane; b < gridDim.x; b += 32) {
+            sv += __ldcg(p.parts + b);
+            nf += __ldcg(p.part_counts + 2 * b);
+            bcs += __ldcg(p.part_counts + 2 * b + 1);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+            sv += __shfl_xor_sync(0xffffffffu, sv, o);
+        nf = __reduce_add_sync(0xffffffffu, nf);
+        bcs = __reduce_add_sync(0xffffffffu, bcs);
+        if (lane == 0) {
+            *p.sum_out = sv;
+            if (p.accumulate) {
+                p.res->sum_q += sv;
+                p.res->nonfinite += nf;
+                p.res->box_cox_clamps += bcs;
+            } else {
+                p.res->sum_q = sv;
+                p.res->nonfinite = nf;
+                p.res->box_cox_clamps = bcs;
+            }
+            *p.counter = 0;  // self-cleaning for the next launch
+        }
+    }
+}
+
+template <int GM>
+static cudaError_t launch_aid_fused(const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out) {
+    const size_t smem = ((p.blob_bytes + 127u) & ~127u) + sizeof(ws::SmemTail) + 64;
+    cudaError_t e = cudaFuncSetAttribute(infer_aid_fused_kernel<GM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess)
+        return e;
+    const uint64_t tiles = (p.n + kTileM - 1) / kTileM;
+    uint64_t grid = (uint64_t)num_sms;
+    if (grid > tiles)
+        grid = tiles;
+    if (grid < 1)
+        grid = 1;
+    *grid_out = (uint32_t)grid;
+    infer_aid_fused_kernel<GM><<<(uint32_t)grid, GM * 128, smem, stream>>>(p);
+    return cudaGetLastError();
+}
+
 template <int KIND, int GE, int GM, int P, int TPR, bool HALF, bool PRE = false>
 static cudaError_t launch_ws(const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out) {
     using Cfg = ws::Cfg<GE, GM, P, TPR>;
@@ -1697,6 +1961,9 @@ size_t infer_smem_bytes(int kind, const InferParams &p) {
 
 // Pipeline shape: 2 encoder groups, 3 MLP groups with one tile chain each, 1 thread per row (the
 // tuned default; the sweep over other shapes is recorded in DESIGN.md section 3a).
+#ifndef NRRS_AID_FUSED
+#define NRRS_AID_FUSED 8  // K-A over level planes as NRRS_AID_FUSED self-contained groups (0: encoder + MLP groups)
+#endif
 #ifndef NRRS_PRE_GE
 #define NRRS_PRE_GE 2
 #endif
@@ -1721,7 +1988,11 @@ static cudaError_t launch_ws_cfg(const InferParams &p, int num_sms, cudaStream_t
             cudaError_t e = launch_grid_levels(gp, num_sms, stream);
             if (e != cudaSuccess)
                 return e;
+#if NRRS_AID_FUSED
+            return launch_aid_fused<NRRS_AID_FUSED>(p, num_sms, stream, grid_out);
+#else
             return launch_ws<KIND, NRRS_PRE_GE, NRRS_PRE_GM, NRRS_PRE_P, 1, true, true>(p, num_sms, stream, grid_out);
+#endif
         }
         if (p.rrs_half)
             return launch_ws<KIND, 2, 3, 1, 1, true>(p, num_sms, stream, grid_out);
