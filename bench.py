@@ -737,8 +737,8 @@ def main():
                    "l2": "flushed between timed steps (256 MiB write outside the events)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic,
-                     "kernel": ("K-A0 grid_level_kernel + K-A infer_ws_kernel<Aid, level planes> (2 encoder + 4 MLP "
-                                "groups): the strategy-factor step of the stage, timed as one unit"
+                     "kernel": ("K-A0 grid_level_kernel + K-A infer_aid_fused_kernel<8> (level planes, 8 self-contained "
+                                "MLP groups): the strategy-factor step of the stage, timed as one unit"
                                 if args.variant == "aid" else
                                 "infer_ws_kernel<Nrrs> (warp-specialized, 2 encoder + 3 MLP groups, L2 gathers)"),
                      "alg_bytes_per_vertex": ALG_BYTES_INFER, "peak_source": peak_src,
