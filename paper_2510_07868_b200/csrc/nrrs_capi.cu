@@ -150,7 +150,8 @@ struct DeviceBlob {
 };
 
 static constexpr int kMaxHostChunks = 8;
-static constexpr uint64_t kAsyncHostChunks = 1;  // nrrs_gpu_rrs_stage_host_async (NRRS_ASYNC_CHUNKS overrides)
+static constexpr uint64_t kAsyncHostChunks = 1;
+static constexpr uint64_t kSyncHostChunks = 3;  // nrrs_gpu_rrs_stage_host (NRRS_SYNC_CHUNKS overrides)  // nrrs_gpu_rrs_stage_host_async (NRRS_ASYNC_CHUNKS overrides)
 static constexpr uint32_t kChunkSums = 8;  // d_sum[8 ..] : per-chunk sums of the host path
 
 struct nrrs_gpu_ctx {
@@ -2212,7 +2213,9 @@ int nrrs_gpu_rrs_stage_host(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *h, uint64_
             *h_result = r;
         return rc;
     }
-    rc = enqueue_host_stage(ctx, s, h, n, p, cap, &dout, nullptr, kMaxHostChunks);
+    const char *sc = std::getenv("NRRS_SYNC_CHUNKS");
+    rc = enqueue_host_stage(ctx, s, h, n, p, cap, &dout, nullptr,
+                            sc ? (uint64_t)std::max(1, std::min(std::atoi(sc), kMaxHostChunks)) : kSyncHostChunks);
     if (rc)
         return rc;
     auto d2h = [&](void *dst, const void *src, size_t bytes) -> int {
