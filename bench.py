@@ -714,6 +714,38 @@ def main():
         tracer.close()
         tscene.close()
         tst.close()
+        # configs[1]: NRRS full wavefront render, builtin:cornell 512x512, 16 spp (16 frames), B = 12
+        cw1, ch1, cb1, nf1 = 512, 512, 12, 16
+        nets1 = NeuralRrs(NeuralRrsConfig(variant=RrsVariant.Nrrs, seed=1)).randomize_for_benchmark()
+        st1 = RrsStage(cw1 * ch1, nets1, device=local)
+        sc1 = rnd.GpuScene(desc, ctx=st1.ctx)
+        tr1 = rnd.Tracer(sc1, cw1 * ch1, cb1)
+        film1 = GpuFilm(cw1, ch1, SuffixStage(ctx=st1.ctx))
+        assign1 = [St()] + [St(SK.Nrrs)] * (cb1 - 1)
+        rc1 = RateControl()
+        for f in range(2):  # warm-up frames (one-time allocations)
+            tr1.trace_frame(assign1, rnd.TraceConfig(max_depth=cb1, seed=11, frame_index=f), rc1, film1)
+            film1.roll_acc()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        reps1 = []
+        for f in range(nf1):
+            r1, _ = tr1.trace_frame(assign1, rnd.TraceConfig(max_depth=cb1, seed=11, frame_index=2 + f), rc1, film1)
+            film1.roll_acc()
+            reps1.append(r1)
+        torch.cuda.synchronize()
+        s1 = time.perf_counter() - t0
+        v1 = sum(sum(r.depth_counts) for r in reps1)
+        trace["configs1"] = {
+            "config": "configs[1]: NRRS full wavefront render, builtin:cornell 512x512, 16 spp (16 frames), max "
+                      "depth 12, fixed at depth 1 then nrrs (random-init networks), RateControl on",
+            "render_ms": 1e3 * s1, "ms_per_frame": 1e3 * s1 / nf1, "path_vertices": v1,
+            "path_vertices_per_s": v1 / s1, "depth_counts_last_frame": reps1[-1].depth_counts,
+            "note": "wall time of the 16 frames (camera, per-depth shade / stage / scatter / folds, reverse pass, "
+                    "Film::add_frame, roll_acc); path vertices = surface vertices over all depths and frames"}
+        tr1.close()
+        sc1.close()
+        st1.close()
 
     peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}
     hbm = peaks.get("hbm_gbs")
