@@ -110,6 +110,36 @@ def sharded_eps_div(local_lum_sum: torch.Tensor, n_pixels_total: int, eps_scale:
     return eps_div_from_luminance_sum(total, n_pixels_total, eps_scale)
 
 
+def row_band(rank: int, world: int, height: int):
+    """Contiguous pixel-row band [row0, row1) of `rank` (rank order == row order, as even as
+    possible), the partition that keeps the global queue the concatenation of the rank queues."""
+    return height * rank // world, height * (rank + 1) // world
+
+
+def gather_film(band: torch.Tensor, dst: int = 0, group=None) -> Optional[torch.Tensor]:
+    """Per-frame film exchange of SURVEY.md 8e: each rank's band of f64 film rows ([px_band, ...],
+    pixel order) is gathered to rank `dst` in rank order, which is pixel order for row bands;
+    bands may differ in size (padded to the largest for the collective).  Returns the full film
+    on `dst`, None elsewhere."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    host = dist.get_backend(group) == "gloo" and band.is_cuda
+    src = band.cpu() if host else band
+    n_local = torch.tensor([src.shape[0]], dtype=torch.int64, device=src.device)
+    sizes = [torch.zeros_like(n_local) for _ in range(world)]
+    dist.all_gather(sizes, n_local, group=group)
+    sizes = [int(x.item()) for x in sizes]
+    rows = max(sizes)
+    pad = torch.zeros((rows,) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
+    pad[:src.shape[0]] = src
+    parts = [torch.zeros_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad, group=group)  # gather-to-dst as an all-gather: sizes are tiny next to NVLink
+    if rank != dst:
+        return None
+    full = torch.cat([p[:k] for p, k in zip(parts, sizes)])
+    return full.to(band.device)
+
+
 def broadcast_weights(nets, src: int = 0, group=None):
     """Per publish() exchange of SURVEY.md 8e: rank `src`'s snapshot blocks (stat grid, stat MLP,
     rrs grid for AID, rrs MLP; networks.cpp:199-204) are broadcast to every rank in place; the

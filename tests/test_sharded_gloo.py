@@ -193,3 +193,39 @@ def test_sharded_eps_div_and_weight_broadcast():
         assert r[2] == float(ref.rrs_mlp[-1])
         assert r[3] == float(np.sum(ref.rrs_grid, dtype=np.float64))
         assert r[4] == float(np.sum(ref.stat_mlp, dtype=np.float64))
+
+
+def _worker_film(rank, port, width, height, result_q):
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, os.path.dirname(here))
+    from paper_2510_07868_b200.sharded import gather_film, row_band
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    r0, r1 = row_band(rank, WORLD, height)
+    full = torch.arange(width * height * 3, dtype=torch.float64).reshape(width * height, 3) * 0.5
+    band = full[r0 * width:r1 * width].clone()
+    out = gather_film(band, dst=0)
+    result_q.put((rank, None if out is None else out.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_film_gather_row_bands():
+    """Per-frame film gather of SURVEY.md 8e: uneven row bands (7 rows over 2 ranks) land on
+    rank 0 in pixel order, bit for bit; other ranks get nothing."""
+    width, height = 5, 7
+    ctx = mp.get_context("spawn")
+    result_q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_film, args=(r, port, width, height, result_q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    res = dict(result_q.get(timeout=240) for _ in range(WORLD))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref = (np.arange(width * height * 3, dtype=np.float64).reshape(-1, 3) * 0.5)
+    np.testing.assert_array_equal(res[0], ref)
+    assert res[1] is None
