@@ -181,8 +181,8 @@ __device__ __forceinline__ float remap_fast(float a) { return 1.0f - __expf(-a);
 // CTA encodes that level for a contiguous vertex range, 8 corner loads from
 // smem per vertex.  CTA b serves level b % L on range b / L, so the L CTAs of
 // one range run side by side and read the same p01 lines from L2.  Output:
-// level planes feat[l][j] = (f0, f1) fp32, read back once by K-A's encoder
-// warps (infer_ws_kernel<.., PRE = true>).  HashGrid::encode, hashgrid.cpp:38-82.
+// level planes feat[l][j] = (f0, f1) fp32, read back once by the groups of
+// infer_aid_fused_kernel.  HashGrid::encode, hashgrid.cpp:38-82.
 // ===========================================================================
 constexpr int kLevelThreads = 1024;
 #ifndef NRRS_LEVEL_PER_THREAD
@@ -623,9 +623,8 @@ constexpr bool kTiming = true;
 constexpr bool kTiming = false;
 #endif
 
-// HALF: fp16 RRSNet (AID) grid tables.  PRE: the grid features were encoded by
-// grid_level_kernel (K-A0); the encoder warps read the level planes instead of gathering.
-template <int KIND, int GE, int GM, int P, int TPR, bool HALF, bool PRE>
+// HALF: fp16 RRSNet (AID) grid tables.
+template <int KIND, int GE, int GM, int P, int TPR, bool HALF>
 __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws_kernel(InferParams p) {
     using Cfg = ws::Cfg<GE, GM, P, TPR>;
     constexpr uint32_t kGT = Cfg::kGroupThreads;
@@ -693,118 +692,7 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
     uint32_t my_nonfinite = 0, my_bc = 0;
     const bool depth1 = p.depth == 1u;
 
-    if (PRE && tid < Cfg::kEncThreads) {
-        // ===================== encoder, AID with level planes =====================
-        // The grid features come from K-A0.  The loads of tile i + GE are issued
-        // before tile i is processed (one tile of register prefetch), so their HBM
-        // latency overlaps the slot wait and the tail encodings of tile i.
-        const int e = tid >> 8;
-        const int r = tid & 127, half = (tid >> 7) & 1;
-        struct In {
-            float f[8];
-            float wx, wy, wz, a, b, c;  // weight; half 0: wo01.xy, -; half 1: i_pixel (or i_acc[pixel]) xyz
-            float rough;
-            uint64_t key;
-            bool valid;
-        };
-        auto load = [&](uint32_t i, In &x) {
-            const uint64_t j = (t_begin + i) * kTileM + r;
-            x.valid = j < n;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int l = 4 * half + q;
-                float2 f = make_float2(0.0f, 0.0f);
-                if (x.valid && l < p.grid_rrs.levels)
-                    f = __ldcs(p.feat + (uint64_t)l * p.feat_stride + j);
-                x.f[2 * q] = f.x;
-                x.f[2 * q + 1] = f.y;
-            }
-            x.wx = x.wy = x.wz = x.a = x.b = x.c = x.rough = 0.0f;
-            x.key = 0;
-            if (!x.valid)
-                return;
-            x.wx = __ldg(p.weight + 3 * j);
-            x.wy = __ldg(p.weight + 3 * j + 1);
-            x.wz = __ldg(p.weight + 3 * j + 2);
-            if (half == 0) {
-                x.a = __ldg(p.wo01 + 2 * j);
-                x.b = __ldg(p.wo01 + 2 * j + 1);
-                x.key = __ldg(p.path_key + j);
-            } else {
-                if (p.i_pixel) {
-                    x.a = __ldg(p.i_pixel + 3 * j);
-                    x.b = __ldg(p.i_pixel + 3 * j + 1);
-                    x.c = __ldg(p.i_pixel + 3 * j + 2);
-                } else {
-                    const uint64_t px_idx = __ldg(p.pixel + j);
-                    x.a = __ldg(p.i_acc + 3 * px_idx);
-                    x.b = __ldg(p.i_acc + 3 * px_idx + 1);
-                    x.c = __ldg(p.i_acc + 3 * px_idx + 2);
-                }
-                x.rough = __ldg(p.roughness + j);
-            }
-        };
-        In nxt;
-        if ((uint32_t)e < T)
-            load((uint32_t)e, nxt);
-        for (uint32_t i = (uint32_t)e; i < T; i += GE) {
-            const In cur = nxt;
-            if (i + GE < T)
-                load(i + GE, nxt);
-            const uint32_t s = i % S;
-            if (i >= (uint32_t)S)
-            {
-#if NRRS_ENC_ONE_POLLER
-                // one warp polls the slot, the group's other warps block in bar.sync (no issue slots)
-                if ((tid & 255) < 32)
-                    mbar_wait_sleep(&st->empty[s], ((i / S) - 1u) & 1u, 1000u);
-                named_bar_sync(1u + (uint32_t)GM + (uint32_t)e, 256u);
-#else
-                mbar_wait_sleep(&st->empty[s], ((i / S) - 1u) & 1u, 1000u);
-#endif
-            }
-            const bool valid = cur.valid;
-            const bool active = valid && (p.gate ? (!depth1 && luminance(cur.wx, cur.wy, cur.wz) > 0.0f) : true);
-            float in16[16];
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                in16[q] = cur.f[q];
-            float *t8 = in16 + 8;
-            uint32_t bc = 0;
-            ws::Side sd{};
-            if (half == 0) {
-                one_blob_fast<4>(cur.a, t8);
-                one_blob_fast<4>(cur.b, t8 + 4);
-                sd.key = cur.key;
-                sd.flags = (valid ? 1u : 0u) | (active ? 2u : 0u);
-            } else {
-                t8[0] = box_cox(cur.wx, bc);
-                t8[1] = box_cox(cur.wy, bc);
-                t8[2] = box_cox(cur.wz, bc);
-                t8[3] = box_cox(mean3(cur.a, cur.b, cur.c), bc);
-                one_blob_fast<4>(remap_fast(cur.rough), t8 + 4);
-            }
-            if (!valid) {
-#pragma unroll
-                for (int q = 0; q < 16; ++q)
-                    in16[q] = 0.0f;
-            }
-            if (active)
-                my_bc += bc;
-            const uint32_t col = Cfg::kColSlots + 32u * s;
-            uint32_t hw[8], lw[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                split2(in16[2 * q], in16[2 * q + 1], hw[q], lw[q]);
-            tmem_st8(lane_base + col + 8u * half, hw);
-            tmem_st8(lane_base + col + 16u + 8u * half, lw);
-            if (half == 0)
-                side[s * 128 + r] = sd;
-            tmem_wait_st();
-            tc_fence_before();
-            mbar_arrive(&st->full[s]);
-        }
-    } else if (tid < Cfg::kEncThreads) {
+    if (tid < Cfg::kEncThreads) {
         // ============================== encoder ==============================
         const int e = tid >> 8;                 // encoder group
         const int r = tid & 127, half = (tid >> 7) & 1;
@@ -852,16 +740,6 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
 #pragma unroll
                 for (int q = 0; q < 8; ++q)
                     g8[q] = px * (float)(q + 1) + py;
-            } else if (PRE) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int l = 4 * half + q;
-                    float2 f = make_float2(0.0f, 0.0f);
-                    if (valid && l < p.grid_rrs.levels)
-                        f = __ldcs(p.feat + (uint64_t)l * p.feat_stride + j);
-                    g8[2 * q] = f.x;
-                    g8[2 * q + 1] = f.y;
-                }
             } else if (KIND == kKindAid) {
                 grid_encode4<HALF>(p.rrs_grid, p.grid_rrs, 4 * half, clamp01(px), clamp01(py), clamp01(pz), g8);
             } else {
@@ -1463,18 +1341,18 @@ static cudaError_t launch_aid_fused(const InferParams &p, int num_sms, cudaStrea
     return cudaGetLastError();
 }
 
-template <int KIND, int GE, int GM, int P, int TPR, bool HALF, bool PRE = false>
+template <int KIND, int GE, int GM, int P, int TPR, bool HALF>
 static cudaError_t launch_ws(const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out) {
     using Cfg = ws::Cfg<GE, GM, P, TPR>;
     const size_t smem = ((p.blob_bytes + 127u) & ~127u) + Cfg::kSlots * 128 * sizeof(ws::Side) +
                         sizeof(ws::SmemTail) + 64;
-    cudaError_t e = cudaFuncSetAttribute(infer_ws_kernel<KIND, GE, GM, P, TPR, HALF, PRE>,
+    cudaError_t e = cudaFuncSetAttribute(infer_ws_kernel<KIND, GE, GM, P, TPR, HALF>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
         return e;
 #ifdef NRRS_CARVEOUT
     // smallest shared-memory carveout that fits: the rest of the 256 KB stays L1 for the grid levels
-    e = cudaFuncSetAttribute(infer_ws_kernel<KIND, GE, GM, P, TPR, HALF, PRE>,
+    e = cudaFuncSetAttribute(infer_ws_kernel<KIND, GE, GM, P, TPR, HALF>,
                              cudaFuncAttributePreferredSharedMemoryCarveout, NRRS_CARVEOUT);
     if (e != cudaSuccess)
         return e;
@@ -1486,7 +1364,7 @@ static cudaError_t launch_ws(const InferParams &p, int num_sms, cudaStream_t str
     if (grid < 1)
         grid = 1;
     *grid_out = (uint32_t)grid;
-    infer_ws_kernel<KIND, GE, GM, P, TPR, HALF, PRE><<<(uint32_t)grid, Cfg::kThreads, smem, stream>>>(p);
+    infer_ws_kernel<KIND, GE, GM, P, TPR, HALF><<<(uint32_t)grid, Cfg::kThreads, smem, stream>>>(p);
     return cudaGetLastError();
 }
 
@@ -1962,16 +1840,7 @@ size_t infer_smem_bytes(int kind, const InferParams &p) {
 // Pipeline shape: 2 encoder groups, 3 MLP groups with one tile chain each, 1 thread per row (the
 // tuned default; the sweep over other shapes is recorded in DESIGN.md section 3a).
 #ifndef NRRS_AID_FUSED
-#define NRRS_AID_FUSED 8  // K-A over level planes as NRRS_AID_FUSED self-contained groups (0: encoder + MLP groups)
-#endif
-#ifndef NRRS_PRE_GE
-#define NRRS_PRE_GE 2
-#endif
-#ifndef NRRS_PRE_GM
-#define NRRS_PRE_GM 4
-#endif
-#ifndef NRRS_PRE_P
-#define NRRS_PRE_P 1
+#define NRRS_AID_FUSED 8  // K-A over level planes as NRRS_AID_FUSED self-contained groups
 #endif
 template <int KIND>
 static cudaError_t launch_ws_cfg(const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out) {
@@ -1988,11 +1857,7 @@ static cudaError_t launch_ws_cfg(const InferParams &p, int num_sms, cudaStream_t
             cudaError_t e = launch_grid_levels(gp, num_sms, stream);
             if (e != cudaSuccess)
                 return e;
-#if NRRS_AID_FUSED
             return launch_aid_fused<NRRS_AID_FUSED>(p, num_sms, stream, grid_out);
-#else
-            return launch_ws<KIND, NRRS_PRE_GE, NRRS_PRE_GM, NRRS_PRE_P, 1, true, true>(p, num_sms, stream, grid_out);
-#endif
         }
         if (p.rrs_half)
             return launch_ws<KIND, 2, 3, 1, 1, true>(p, num_sms, stream, grid_out);
