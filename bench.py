@@ -270,6 +270,8 @@ def main():
     local_sum = torch.zeros(1, dtype=torch.float64, device=dev)
     local_total = torch.zeros(1, dtype=torch.int64, device=dev)
 
+    pending = [None]  # N > 1: the last depth's device-side scalars (sharded_depth_async)
+
     def step(ev):
         """One stage step.  ev = [start, end] (timed loop: nothing between the kernels, so K-B / K-C
         launch early under programmatic dependent launch) or [start, after K-A, after K-B, end]
@@ -297,10 +299,11 @@ def main():
             compact(local_total)
         else:
             sh.stage.ctx.bind_stream()
-            from paper_2510_07868_b200.sharded import sharded_depth
-            # this rank's compaction needs only its own queue: queued before the host waits for the totals
-            sharded_depth(local_sum, lambda rs: sh.decide(n, 2, strategy, out, rs, gain, 0.0), cap, npx, None, rc,
-                          after_exchange=lambda: compact(sh._total))
+            from paper_2510_07868_b200.sharded import sharded_depth_async
+            # no host wait inside the depth: the global clip runs on the device (NCCL path) and this rank's
+            # compaction needs only its own queue; the scalars are read after the timed loop
+            pending[0] = sharded_depth_async(local_sum, lambda rs: sh.decide(n, 2, strategy, out, rs, gain, 0.0), cap,
+                                             npx, sh.stage, None, after_exchange=lambda clip: compact(sh._total))
         ev[-1].record(stream)
 
     def events(k=2):
@@ -361,6 +364,9 @@ def main():
     total_s = float(t.item())
     value = world * n * args.steps / total_s
     res = _capi.StageResultC()
+    if sh is not None and pending[0] is not None:
+        po = pending[0].resolve(rc)  # the last timed depth's global outcome (host read after the loop)
+        assert po.dropped == 0 or po.spawned == cap
     spawned = int(min(int(local_total.item()), cap)) if sh is None else int(sh._total.item())
 
     # ---- e2e: the C ABI host-buffer entry (H2D + stage + D2H every step) ----

@@ -418,6 +418,11 @@ NRRS_API int nrrs_gpu_stage_decide(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_sta
 NRRS_API int nrrs_gpu_sharded_clip(const uint64_t *h_rank_totals, int32_t nranks, int32_t rank,
                           uint32_t capacity, uint64_t *h_base, uint32_t *h_kept,
                           uint32_t *h_spawned_global, uint64_t *h_dropped_global);
+/* The same clip on the device, asynchronous on the context stream, so a depth of the
+ * tile-sharded stage needs no host round trip: d_rank_totals = the all-gathered u64
+ * totals (device), d_out[4] = base, kept, spawned (global), dropped (global). */
+NRRS_API int nrrs_gpu_sharded_clip_dev(nrrs_gpu_ctx *ctx, const uint64_t *d_rank_totals, int32_t nranks,
+                                       int32_t rank, uint32_t capacity, uint64_t *d_out);
 
 /* ---- order-preserving compaction of filled slots (wavefront.cpp:488-497):
  * keeps record s iff d_used[s] != 0, in slot order.  Records are

@@ -147,6 +147,7 @@ SIGNATURES = [
                                          C.POINTER(StageOut), _P]),
     ("nrrs_gpu_stage_decide", C.c_int, [_P, C.c_uint64, C.POINTER(StageParams), _P, C.c_int32,
                                         C.POINTER(StageOut), _P]),
+    ("nrrs_gpu_sharded_clip_dev", C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_uint32, _P]),
     ("nrrs_gpu_sharded_clip", C.c_int, [C.POINTER(C.c_uint64), C.c_int32, C.c_int32, C.c_uint32,
                                         C.POINTER(C.c_uint64), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
                                         C.POINTER(C.c_uint64)]),

@@ -1806,6 +1806,17 @@ int nrrs_gpu_sharded_clip(const uint64_t *totals, int32_t nranks, int32_t rank, 
     return NRRS_OK;
 }
 
+int nrrs_gpu_sharded_clip_dev(nrrs_gpu_ctx *ctx, const uint64_t *d_rank_totals, int32_t nranks, int32_t rank,
+                              uint32_t capacity, uint64_t *d_out) {
+    if (!ctx || !d_rank_totals || !d_out || nranks < 1 || rank < 0 || rank >= nranks)
+        return ctx ? fail(ctx, NRRS_EINVAL, "sharded_clip_dev: invalid arguments") : NRRS_EINVAL;
+    CK(ctx, cudaSetDevice(ctx->device));
+    CK(ctx, launch_sharded_clip(reinterpret_cast<const unsigned long long *>(d_rank_totals), nranks, rank, capacity,
+                                reinterpret_cast<unsigned long long *>(d_out), ctx->stream));
+    ctx->launches += 1;
+    return NRRS_OK;
+}
+
 int nrrs_gpu_compact(nrrs_gpu_ctx *ctx, const void *d_in, const uint8_t *d_used, uint32_t count,
                      uint32_t record_words, void *d_out, uint32_t *d_count, uint32_t *h_count) {
     if (!ctx || (count && (!d_in || !d_used || !d_out)))

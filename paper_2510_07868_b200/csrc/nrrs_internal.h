@@ -332,6 +332,8 @@ struct GridLevelParams {
 };
 constexpr uint32_t kLevelSmemMax = 150u * 1024u;  // table bytes; + 72 KB of staged p01 blocks <= 227 KB
 cudaError_t launch_grid_levels(const GridLevelParams &p, int num_sms, cudaStream_t stream);
+cudaError_t launch_sharded_clip(const unsigned long long *totals, int nranks, int rank, uint32_t capacity,
+                                unsigned long long *out, cudaStream_t stream);
 cudaError_t launch_infer(int kind, const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out);
 uint32_t infer_max_grid(int num_sms);
 uint32_t decide_tiles(uint64_t n);

@@ -346,6 +346,34 @@ __global__ void __launch_bounds__(kLevelThreads, 1) grid_level_kernel(GridLevelP
     }
 }
 
+// nrrs_gpu_sharded_clip on the device (one thread): the rank's global slot base, kept records,
+// global spawned and dropped from the all-gathered rank totals (wavefront.cpp:141-154 across ranks).
+__global__ void sharded_clip_kernel(const unsigned long long *totals, int nranks, int rank, uint32_t capacity,
+                                    unsigned long long *out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0)
+        return;
+    unsigned long long base = 0, all = 0;
+    for (int r = 0; r < nranks; ++r) {
+        if (r < rank)
+            base += totals[r];
+        all += totals[r];
+    }
+    const unsigned long long cap = capacity;
+    const unsigned long long room = cap - (base < cap ? base : cap);
+    const unsigned long long kept = totals[rank] < room ? totals[rank] : room;
+    const unsigned long long spawned = all < cap ? all : cap;
+    out[0] = base;
+    out[1] = kept;
+    out[2] = spawned;
+    out[3] = all - spawned;
+}
+
+cudaError_t launch_sharded_clip(const unsigned long long *totals, int nranks, int rank, uint32_t capacity,
+                                unsigned long long *out, cudaStream_t stream) {
+    sharded_clip_kernel<<<1, 32, 0, stream>>>(totals, nranks, rank, capacity, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_grid_levels(const GridLevelParams &p, int num_sms, cudaStream_t stream) {
     const uint32_t L = (uint32_t)p.g.levels;
     const size_t smem = (size_t)p.g.table_size * 4u + 2u * kLevelBlock * 12u;

@@ -91,6 +91,59 @@ def sharded_depth(local_sum: torch.Tensor, decide: Callable[[torch.Tensor], torc
     return ShardOutcome(sums_h, tot, base, kept, spawned, dropped, f_norm_from_sums(sums_h, n_pixels_total))
 
 
+@dataclasses.dataclass
+class PendingDepth:
+    """A depth of the sharded protocol whose scalars are still on the device."""
+    rank_sums: torch.Tensor   # [world] f64, rank order
+    rank_totals: torch.Tensor  # [world] i64, rank order
+    clip: Optional[torch.Tensor]  # [4] i64: base, kept, spawned, dropped (None on the host-exchange path)
+    n_pixels_total: int
+    capacity: int
+    rank: int
+
+    def resolve(self, rc: Optional[RateControl] = None) -> ShardOutcome:
+        """Reads the depth's scalars (one host wait) and applies the overflow to RateControl."""
+        tot = [int(x) for x in self.rank_totals.tolist()]
+        sums_h = [float(x) for x in self.rank_sums.tolist()]
+        if self.clip is not None:
+            base, kept, spawned, dropped = (int(x) for x in self.clip.tolist())
+        else:
+            base, kept, spawned, dropped = global_clip(tot, self.rank, self.capacity)
+        if rc is not None and dropped > 0:
+            rc.note_overflow()
+        return ShardOutcome(sums_h, tot, base, kept, spawned, dropped, f_norm_from_sums(sums_h, self.n_pixels_total))
+
+
+def sharded_depth_async(local_sum: torch.Tensor, decide: Callable[[torch.Tensor], torch.Tensor], capacity: int,
+                        n_pixels_total: int, stage: Optional[RrsStage] = None, group=None,
+                        after_exchange: Optional[Callable[[torch.Tensor], None]] = None) -> PendingDepth:
+    """sharded_depth without the host wait: the global clip runs on the device
+    (nrrs_gpu_sharded_clip_dev on `stage`'s context stream) when the collective's tensors live on
+    the GPU, so consecutive depths queue back to back.  after_exchange(clip) receives the [4]
+    device tensor (kept = clip[1]) or None on the gloo host-exchange path.  The caller reads the
+    scalars with PendingDepth.resolve(rc) when it needs them; RateControl sees the overflow then."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    host = dist.get_backend(group) == "gloo" and local_sum.is_cuda
+    src = local_sum.cpu() if host else local_sum
+    sums = [torch.zeros_like(src) for _ in range(world)]
+    dist.all_gather(sums, src, group=group)
+    rank_sums_t = torch.cat(sums).to(local_sum.device)
+    local_total = decide(rank_sums_t)
+    src = local_total.cpu() if host else local_total
+    totals = [torch.zeros_like(src) for _ in range(world)]
+    dist.all_gather(totals, src, group=group)
+    totals_t = torch.cat(totals)
+    clip = None
+    if not host and stage is not None and totals_t.is_cuda:
+        clip = torch.empty(4, dtype=torch.int64, device=totals_t.device)
+        _capi.check(stage.handle, stage.ctx.lib.nrrs_gpu_sharded_clip_dev(stage.handle, totals_t.data_ptr(), world,
+                                                                          rank, int(capacity), clip.data_ptr()))
+    if after_exchange is not None:
+        after_exchange(clip)
+    return PendingDepth(rank_sums_t, totals_t, clip, n_pixels_total, capacity, rank)
+
+
 def _gather_in_rank_order(local: torch.Tensor, group=None) -> torch.Tensor:
     host = dist.get_backend(group) == "gloo" and local.is_cuda  # gloo exchanges host copies
     src = local.cpu() if host else local

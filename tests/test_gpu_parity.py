@@ -528,3 +528,21 @@ def test_host_buffer_async_pipeline_matches_sync(nets):
         np.testing.assert_array_equal(out["q_norm"], ref_out["q_norm"])
         np.testing.assert_array_equal(out["q_real"], ref_out["q_real"])
         np.testing.assert_array_equal(out["slots"][:res.spawned], ref_out["slots"][:ref_res.spawned])
+
+
+def test_sharded_clip_dev_matches_host():
+    """nrrs_gpu_sharded_clip_dev (the device form the NCCL path uses, no host round trip) equals
+    the host nrrs_gpu_sharded_clip for every rank, with and without a global overflow."""
+    import ctypes as C
+    from paper_2510_07868_b200 import _capi
+    from paper_2510_07868_b200.sharded import global_clip
+    st = _stage(1024)
+    lib = st.ctx.lib
+    for totals, cap in (([300, 250, 0, 400], 1200), ([700, 600, 500, 10], 1500), ([5], 4), ([0, 0], 10)):
+        d_tot = torch.tensor(totals, dtype=torch.int64, device="cuda")
+        for rank in range(len(totals)):
+            out = torch.zeros(4, dtype=torch.int64, device="cuda")
+            _capi.check(st.handle, lib.nrrs_gpu_sharded_clip_dev(st.handle, d_tot.data_ptr(), len(totals), rank, cap,
+                                                                 out.data_ptr()))
+            torch.cuda.synchronize()
+            assert tuple(int(x) for x in out.tolist()) == global_clip(totals, rank, cap)

@@ -229,3 +229,42 @@ def test_film_gather_row_bands():
     ref = (np.arange(width * height * 3, dtype=np.float64).reshape(-1, 3) * 0.5)
     np.testing.assert_array_equal(res[0], ref)
     assert res[1] is None
+
+
+def _worker_async(rank, port, result_q):
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, os.path.dirname(here))
+    from paper_2510_07868_b200.rrs import RateControl
+    from paper_2510_07868_b200.sharded import sharded_depth, sharded_depth_async
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    local_sum = torch.tensor([10.5 + rank], dtype=torch.float64)
+    totals = [700, 650]
+    decide = lambda rs: torch.tensor([totals[rank]], dtype=torch.int64)  # noqa: E731
+    seen = []
+    rc_a, rc_b = RateControl(), RateControl()
+    ref = sharded_depth(local_sum, decide, 1200, 1000, None, rc_a)
+    pend = sharded_depth_async(local_sum, decide, 1200, 1000, None, None, after_exchange=lambda c: seen.append(c))
+    got = pend.resolve(rc_b)
+    result_q.put((rank, ref == got, seen == [None], rc_a.alpha == rc_b.alpha < 1.0))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_sharded_depth_async_matches_sync():
+    """sharded_depth_async (device-side clip on NCCL; host clip on gloo, read at resolve())
+    gives the same outcome and RateControl update as sharded_depth, here with a global overflow."""
+    ctx = mp.get_context("spawn")
+    result_q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_async, args=(r, port, result_q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    res = [result_q.get(timeout=240) for _ in range(WORLD)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in res:
+        assert r[1] and r[2] and r[3], r
