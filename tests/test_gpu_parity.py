@@ -546,3 +546,22 @@ def test_sharded_clip_dev_matches_host():
                                                                  out.data_ptr()))
             torch.cuda.synchronize()
             assert tuple(int(x) for x in out.tolist()) == global_clip(totals, rank, cap)
+
+
+@pytest.mark.parametrize("n", [1, 127, 129, 4099])
+def test_aid_stage_ragged_sizes(n):
+    """AID stage (K-A0 + fused-group K-A) on batches that are not whole 128-row tiles, down to one
+    vertex: factors within 1e-3 of the oracle, RrsRound uniforms exact, decisions equal when fed the
+    GPU's own factors."""
+    on = orc.OracleNets(orc.VARIANT_AID, seed=1, randomize=True)
+    v = orc.gen_vertices(n)
+    cap = queue_capacity_for(n)
+    ref = orc.rrs_stage(v, 2, n, cap, orc.AID_NRRS, on, gain=0.85, seed=0, threads=4)
+    st = _stage(n, on)
+    out, res = st.run(to_dev(v), 2, Strategy(StrategyKind.AidNrrs), rc=RateControl(), full=True)
+    torch.cuda.synchronize()
+    assert rel_err(_np(out.q_orig), ref["q_orig"], 1e-6).max() <= REL_TOL
+    np.testing.assert_array_equal(_np(out.u), ref["u"])
+    dec = oracle_decide(_np(out.q_orig), _np(out.u), n, cap, 0.85)
+    np.testing.assert_array_equal(_np(out.k), dec["k"])
+    assert res.spawned == dec["spawned"]
