@@ -1867,6 +1867,18 @@ size_t infer_smem_bytes(int kind, const InferParams &p) {
 
 // Pipeline shape: 2 encoder groups, 3 MLP groups with one tile chain each, 1 thread per row (the
 // tuned default; the sweep over other shapes is recorded in DESIGN.md section 3a).
+#ifndef NRRS_WS_GE
+#define NRRS_WS_GE 2  // fused-gather K-A for NRRS: encoder groups
+#endif
+#ifndef NRRS_WS_GM
+#define NRRS_WS_GM 3  // fused-gather K-A: MLP groups
+#endif
+#ifndef NRRS_WS4_GE
+#define NRRS_WS4_GE 3  // fused-gather K-A for the 4-layer kinds (ADRRS-NN, stats, AID with fp32 tables)
+#endif
+#ifndef NRRS_WS4_GM
+#define NRRS_WS4_GM 2
+#endif
 #ifndef NRRS_AID_FUSED
 #define NRRS_AID_FUSED 8  // K-A over level planes as NRRS_AID_FUSED self-contained groups
 #endif
@@ -1888,9 +1900,14 @@ static cudaError_t launch_ws_cfg(const InferParams &p, int num_sms, cudaStream_t
             return launch_aid_fused<NRRS_AID_FUSED>(p, num_sms, stream, grid_out);
         }
         if (p.rrs_half)
-            return launch_ws<KIND, 2, 3, 1, 1, true>(p, num_sms, stream, grid_out);
+            return launch_ws<KIND, NRRS_WS4_GE, NRRS_WS4_GM, 1, 1, true>(p, num_sms, stream, grid_out);
     }
-    return launch_ws<KIND, 2, 3, 1, 1, false>(p, num_sms, stream, grid_out);
+    // NRRS chains 8 MMA layers per tile (StatNet then RRSNet): 2 encoder + 3 MLP groups; the 4-layer
+    // kinds are gather-bound and run 3 encoder + 2 MLP groups (ADRRS-NN 0.397 -> 0.377 ms)
+    if constexpr (KIND == kKindNrrs)
+        return launch_ws<KIND, NRRS_WS_GE, NRRS_WS_GM, 1, 1, false>(p, num_sms, stream, grid_out);
+    else
+        return launch_ws<KIND, NRRS_WS4_GE, NRRS_WS4_GM, 1, 1, false>(p, num_sms, stream, grid_out);
 }
 
 cudaError_t launch_infer(int kind, const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out) {
