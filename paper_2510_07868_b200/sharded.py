@@ -114,6 +114,20 @@ class PendingDepth:
         return ShardOutcome(sums_h, tot, base, kept, spawned, dropped, f_norm_from_sums(sums_h, self.n_pixels_total))
 
 
+def _all_gather_flat(x: torch.Tensor, host: bool, group=None) -> torch.Tensor:
+    """[1] per rank -> [world] in rank order: one all_gather_into_tensor on NCCL (no list copies),
+    the list form on gloo (host copies)."""
+    world = dist.get_world_size(group)
+    if not host and x.is_cuda and dist.get_backend(group) == "nccl":
+        out = torch.empty(world * x.numel(), dtype=x.dtype, device=x.device)
+        dist.all_gather_into_tensor(out, x.reshape(-1), group=group)
+        return out
+    src = x.cpu() if host else x
+    parts = [torch.zeros_like(src) for _ in range(world)]
+    dist.all_gather(parts, src, group=group)
+    return torch.cat(parts)
+
+
 def sharded_depth_async(local_sum: torch.Tensor, decide: Callable[[torch.Tensor], torch.Tensor], capacity: int,
                         n_pixels_total: int, stage: Optional[RrsStage] = None, group=None,
                         after_exchange: Optional[Callable[[torch.Tensor], None]] = None) -> PendingDepth:
@@ -125,15 +139,9 @@ def sharded_depth_async(local_sum: torch.Tensor, decide: Callable[[torch.Tensor]
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     host = dist.get_backend(group) == "gloo" and local_sum.is_cuda
-    src = local_sum.cpu() if host else local_sum
-    sums = [torch.zeros_like(src) for _ in range(world)]
-    dist.all_gather(sums, src, group=group)
-    rank_sums_t = torch.cat(sums).to(local_sum.device)
+    rank_sums_t = _all_gather_flat(local_sum, host, group).to(local_sum.device)
     local_total = decide(rank_sums_t)
-    src = local_total.cpu() if host else local_total
-    totals = [torch.zeros_like(src) for _ in range(world)]
-    dist.all_gather(totals, src, group=group)
-    totals_t = torch.cat(totals)
+    totals_t = _all_gather_flat(local_total, host, group)
     clip = None
     if not host and stage is not None and totals_t.is_cuda:
         clip = torch.empty(4, dtype=torch.int64, device=totals_t.device)
