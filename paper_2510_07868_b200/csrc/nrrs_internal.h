@@ -120,6 +120,7 @@ struct InferParams {
     double *sum_out;   // local sum of q
     DevResult *res;
     uint32_t accumulate;  // chunked launches: add to res counters / sum_q instead of overwriting
+    uint32_t in_bulk;  // set by launch_aid_fused: K-A stages row inputs by TMA (aligned inputs)
     uint32_t ablate;   // debug only (env NRRS_DEBUG_ABLATE): bit0 skip grid gathers, bit1 skip MLP
     unsigned long long *dbg;  // debug only (env NRRS_DEBUG_TIMING): per-CTA clock64 phase counters [grid][16]
 };

@@ -1112,6 +1112,21 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
 // tcgen05 chain and the head -- so GM chains are in flight per SM instead of one per MLP
 // group behind shared encoder groups.  TMEM: per group 32 accumulator + 32 A columns.
 // ===========================================================================
+// Per-group input slot of infer_aid_fused_kernel (one 128-row tile, field-major so each
+// thread's row reads are bank-conflict free): 8 level planes (float2), weight (3 f32),
+// wo01 (2 f32), i_pixel (3 f32; or the u32 pixel index), roughness, path_key.
+constexpr uint32_t kAidInPlane = 8u * kTileM;
+constexpr uint32_t kAidInWeight = 8u * kAidInPlane;
+constexpr uint32_t kAidInWo = kAidInWeight + 12u * kTileM;
+constexpr uint32_t kAidInIpx = kAidInWo + 8u * kTileM;
+constexpr uint32_t kAidInRough = kAidInIpx + 12u * kTileM;
+constexpr uint32_t kAidInKey = kAidInRough + 4u * kTileM;
+constexpr uint32_t kAidInBytes = kAidInKey + 8u * kTileM;
+static_assert(kAidInBytes % 128u == 0, "slot alignment");
+__host__ __device__ constexpr uint32_t aid_in_offset(uint32_t blob_bytes) {
+    return ((blob_bytes + 127u) & ~127u) + (((uint32_t)sizeof(ws::SmemTail) + 127u) & ~127u);
+}
+
 template <int GM>
 __global__ void __launch_bounds__(GM * 128, 1) infer_aid_fused_kernel(InferParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1141,8 +1156,10 @@ __global__ void __launch_bounds__(GM * 128, 1) infer_aid_fused_kernel(InferParam
                     make_smem_desc(smem_u32(smem_w + L.w_hi) + 256u * k + ((uint32_t)L.N / 8u) * sbo, 128u, sbo);
             }
         }
-        for (int q = 0; q < GM; ++q)
+        for (int q = 0; q < GM; ++q) {
             mbar_init(&st->mma_bar[q], 1);
+            mbar_init(&st->full[q], 1);
+        }
         fence_barrier_init();
     }
     if (warp == 0)
@@ -1168,32 +1185,85 @@ __global__ void __launch_bounds__(GM * 128, 1) infer_aid_fused_kernel(InferParam
     const int levels = p.grid_rrs.levels;
     uint32_t phase = 0;
 
+    // Row inputs of the group's NEXT tile are staged into its smem slot by TMA bulk copies
+    // (issued right after the current tile's layer-0 MMA, so they land during the 4-layer
+    // chain); a partial last tile, or unaligned inputs, load directly.
+    uint8_t *in_s = smem_raw + aid_in_offset(p.blob_bytes) + (uint32_t)g * kAidInBytes;
+    const bool in_bulk = p.in_bulk != 0u;
+    const uint64_t full_tiles = n / kTileM;
+    uint32_t in_phase = 0;
+    auto issue_in = [&](uint64_t tile) {  // issuer only; the group has finished reading the slot
+        const uint64_t j0 = tile * kTileM;
+        const uint32_t ipx_bytes = p.i_pixel ? 12u * kTileM : 4u * kTileM;
+        mbar_arrive_expect_tx(&st->full[g], (uint32_t)levels * 8u * kTileM + 12u * kTileM + 8u * kTileM +
+                                                ipx_bytes + 4u * kTileM + 8u * kTileM);
+        for (int q = 0; q < levels; ++q)
+            bulk_g2s(in_s + kAidInPlane * q, p.feat + (uint64_t)q * p.feat_stride + j0, 8u * kTileM, &st->full[g]);
+        bulk_g2s(in_s + kAidInWeight, p.weight + 3 * j0, 12u * kTileM, &st->full[g]);
+        bulk_g2s(in_s + kAidInWo, p.wo01 + 2 * j0, 8u * kTileM, &st->full[g]);
+        if (p.i_pixel)
+            bulk_g2s(in_s + kAidInIpx, p.i_pixel + 3 * j0, ipx_bytes, &st->full[g]);
+        else
+            bulk_g2s(in_s + kAidInIpx, p.pixel + j0, ipx_bytes, &st->full[g]);
+        bulk_g2s(in_s + kAidInRough, p.roughness + j0, 4u * kTileM, &st->full[g]);
+        bulk_g2s(in_s + kAidInKey, p.path_key + j0, 8u * kTileM, &st->full[g]);
+    };
+    if (in_bulk && r == 32 && (uint32_t)g < T && t_begin + (uint32_t)g < full_tiles)
+        issue_in(t_begin + (uint32_t)g);
+
     for (uint32_t i = (uint32_t)g; i < T; i += GM) {
         const uint64_t j = (t_begin + i) * kTileM + r;
         const bool valid = j < n;
+        const bool staged = in_bulk && t_begin + i < full_tiles;
         // ---- row inputs: level planes + tail inputs ----
         float f[16];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            float2 v = make_float2(0.0f, 0.0f);
-            if (valid && q < levels)
-                v = __ldcs(p.feat + (uint64_t)q * p.feat_stride + j);
-            f[2 * q] = v.x;
-            f[2 * q + 1] = v.y;
-        }
         float wx = 0, wy = 0, wz = 0, wox = 0, woy = 0, ia = 0, ib = 0, ic = 0, rough = 0;
         uint64_t key = 0;
-        if (valid) {
-            wx = __ldg(p.weight + 3 * j); wy = __ldg(p.weight + 3 * j + 1); wz = __ldg(p.weight + 3 * j + 2);
-            wox = __ldg(p.wo01 + 2 * j); woy = __ldg(p.wo01 + 2 * j + 1);
+        if (staged) {
+            mbar_wait(&st->full[g], in_phase);
+            in_phase ^= 1u;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                float2 v = make_float2(0.0f, 0.0f);
+                if (q < levels)
+                    v = reinterpret_cast<const float2 *>(in_s + kAidInPlane * q)[r];
+                f[2 * q] = v.x;
+                f[2 * q + 1] = v.y;
+            }
+            const float *w3 = reinterpret_cast<const float *>(in_s + kAidInWeight) + 3 * r;
+            wx = w3[0]; wy = w3[1]; wz = w3[2];
+            const float2 wo = reinterpret_cast<const float2 *>(in_s + kAidInWo)[r];
+            wox = wo.x; woy = wo.y;
             if (p.i_pixel) {
-                ia = __ldg(p.i_pixel + 3 * j); ib = __ldg(p.i_pixel + 3 * j + 1); ic = __ldg(p.i_pixel + 3 * j + 2);
+                const float *i3 = reinterpret_cast<const float *>(in_s + kAidInIpx) + 3 * r;
+                ia = i3[0]; ib = i3[1]; ic = i3[2];
             } else {
-                const uint64_t px_idx = __ldg(p.pixel + j);
+                const uint64_t px_idx = reinterpret_cast<const uint32_t *>(in_s + kAidInIpx)[r];
                 ia = __ldg(p.i_acc + 3 * px_idx); ib = __ldg(p.i_acc + 3 * px_idx + 1); ic = __ldg(p.i_acc + 3 * px_idx + 2);
             }
-            rough = __ldg(p.roughness + j);
-            key = __ldg(p.path_key + j);
+            rough = reinterpret_cast<const float *>(in_s + kAidInRough)[r];
+            key = reinterpret_cast<const uint64_t *>(in_s + kAidInKey)[r];
+        } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                float2 v = make_float2(0.0f, 0.0f);
+                if (valid && q < levels)
+                    v = __ldcs(p.feat + (uint64_t)q * p.feat_stride + j);
+                f[2 * q] = v.x;
+                f[2 * q + 1] = v.y;
+            }
+            if (valid) {
+                wx = __ldg(p.weight + 3 * j); wy = __ldg(p.weight + 3 * j + 1); wz = __ldg(p.weight + 3 * j + 2);
+                wox = __ldg(p.wo01 + 2 * j); woy = __ldg(p.wo01 + 2 * j + 1);
+                if (p.i_pixel) {
+                    ia = __ldg(p.i_pixel + 3 * j); ib = __ldg(p.i_pixel + 3 * j + 1); ic = __ldg(p.i_pixel + 3 * j + 2);
+                } else {
+                    const uint64_t px_idx = __ldg(p.pixel + j);
+                    ia = __ldg(p.i_acc + 3 * px_idx); ib = __ldg(p.i_acc + 3 * px_idx + 1); ic = __ldg(p.i_acc + 3 * px_idx + 2);
+                }
+                rough = __ldg(p.roughness + j);
+                key = __ldg(p.path_key + j);
+            }
         }
         const bool active = valid && (p.gate ? (!depth1 && luminance(wx, wy, wz) > 0.0f) : true);
         // ---- layer-0 input (build_aid_tail, networks.cpp:149-157) in the packed K order ----
@@ -1226,6 +1296,12 @@ __global__ void __launch_bounds__(GM * 128, 1) infer_aid_fused_kernel(InferParam
         named_bar_sync(bar_id, 128);
         if (issuer)
             ws::ws_issue(st, 1, 0, tmem_base, col_a, col_d, &st->mma_bar[g]);
+        // every thread of the group has consumed its slot row (barrier above); a second warp
+        // issues the copies so the MMA issuer's warp goes straight to the layer-0 wait
+        if (r == 32 && in_bulk && i + GM < T && t_begin + i + GM < full_tiles) {
+            fence_proxy_async_smem();
+            issue_in(t_begin + i + GM);
+        }
         // ---- 4-layer chain ----
 #pragma unroll 1
         for (int l = 0; l < 4; ++l) {
@@ -1351,9 +1427,23 @@ __global__ void __launch_bounds__(GM * 128, 1) infer_aid_fused_kernel(InferParam
     }
 }
 
+static bool aligned16(const void *q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; }
+
 template <int GM>
-static cudaError_t launch_aid_fused(const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out) {
-    const size_t smem = ((p.blob_bytes + 127u) & ~127u) + sizeof(ws::SmemTail) + 64;
+static cudaError_t launch_aid_fused(const InferParams &p_in, int num_sms, cudaStream_t stream, uint32_t *grid_out) {
+    InferParams p = p_in;
+    // TMA-staged row inputs need 16-byte aligned field bases and plane stride (whole tiles are
+    // 16-byte multiples); otherwise every tile loads directly.
+    const size_t smem_direct = ((p.blob_bytes + 127u) & ~127u) + sizeof(ws::SmemTail) + 64;
+    const size_t smem_staged = (size_t)aid_in_offset(p.blob_bytes) + (size_t)GM * kAidInBytes;
+    p.in_bulk = 0;
+#ifndef NRRS_AID_NO_PREFETCH
+    if (smem_staged <= 227u * 1024u && p.grid_rrs.levels <= 8 && (p.feat_stride & 1u) == 0 && aligned16(p.feat) &&
+        aligned16(p.weight) && aligned16(p.wo01) && aligned16(p.roughness) && aligned16(p.path_key) &&
+        (p.i_pixel ? aligned16(p.i_pixel) : (p.pixel != nullptr && aligned16(p.pixel))))
+        p.in_bulk = 1;
+#endif
+    const size_t smem = p.in_bulk ? smem_staged : smem_direct;
     cudaError_t e = cudaFuncSetAttribute(infer_aid_fused_kernel<GM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess)
