@@ -120,8 +120,8 @@ __device__ __forceinline__ bool tri_hit(const RenderScene &s, uint32_t tri, cons
 // intersect_triangle on the pre-gathered record of BVH prim slot k (p0, e1, e2 as the reference computes them)
 __device__ __forceinline__ bool tri_hit_slot(const RenderScene &s, uint32_t k, const float o[3], const float d[3],
                                              float t_max, float &t, float &u, float &v, uint32_t &tri) {
-    const float4 a = __ldg(s.tri4 + 3 * (uint64_t)k), b = __ldg(s.tri4 + 3 * (uint64_t)k + 1),
-                 c = __ldg(s.tri4 + 3 * (uint64_t)k + 2);
+    // generic loads: s.tri4 may point into shared memory (stage_scene)
+    const float4 a = s.tri4[3 * (uint64_t)k], b = s.tri4[3 * (uint64_t)k + 1], c = s.tri4[3 * (uint64_t)k + 2];
     const float p0[3] = {a.x, a.y, a.z}, e1[3] = {a.w, b.x, b.y}, e2[3] = {b.z, b.w, c.x};
     float pv[3], qv[3];
     cross3(d, e2, pv);
@@ -558,12 +558,36 @@ __device__ __forceinline__ void hit_emission(const RenderScene &s, const float d
         out[a] = fm(e[a], mis);
 }
 
+// BVH nodes and triangle records staged into this CTA's shared memory when the launch gave room
+// for them (scene_smem_bytes): the walks' dependent node / triangle loads then hit smem instead of
+// L1/L2.  Same data, same arithmetic.  All threads of the CTA must call it.
+__device__ __forceinline__ RenderScene stage_scene(const RenderScene &s) {
+    extern __shared__ __align__(16) uint8_t scene_smem[];
+    uint32_t dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    RenderScene ls = s;
+    const uint32_t nb = s.n_nodes * (uint32_t)sizeof(BvhNodeDev), tb = s.n_tri * 48u;
+    if (dyn != 0 && dyn >= nb + tb) {
+        const uint4 *sn = reinterpret_cast<const uint4 *>(s.nodes), *st4 = reinterpret_cast<const uint4 *>(s.tri4);
+        uint4 *dn = reinterpret_cast<uint4 *>(scene_smem), *dt = reinterpret_cast<uint4 *>(scene_smem + nb);
+        for (uint32_t i = threadIdx.x; i < nb / 16u; i += blockDim.x)
+            dn[i] = __ldg(sn + i);
+        for (uint32_t i = threadIdx.x; i < tb / 16u; i += blockDim.x)
+            dt[i] = __ldg(st4 + i);
+        ls.nodes = reinterpret_cast<const BvhNodeDev *>(scene_smem);
+        ls.tri4 = reinterpret_cast<const float4 *>(scene_smem + nb);
+    }
+    __syncthreads();
+    return ls;
+}
+
 // Per queue entry: closest hit, dispatch class (0 miss, 1 light, 2 surface), the miss / light
 // film term (f64, zero when the reference adds nothing), depth-1 light normals, and the
 // (entry, triangle) pair the surface compaction keeps.
-__global__ void trace_shade_kernel(RenderScene s, const PathStateDev *q, uint32_t n, uint32_t depth, uint8_t *cls,
+__global__ void trace_shade_kernel(RenderScene s_in, const PathStateDev *q, uint32_t n, uint32_t depth, uint8_t *cls,
                                    uint8_t *is_surf, float *hit_t, uint32_t *pair, double *term, float *normals,
                                    uint32_t *err) {
+    const RenderScene s = stage_scene(s_in);
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const PathStateDev &st = q[i];
         const float o[3] = {st.o[0], st.o[1], st.o[2]}, d[3] = {st.d[0], st.d[1], st.d[2]};
@@ -664,9 +688,10 @@ __global__ void trace_records_kernel(RenderScene s, const PathStateDev *q, const
 #ifndef NRRS_SCATTER_MINB
 #define NRRS_SCATTER_MINB 4  // 64 registers: occupancy over the divergent walks (measured -5% frame time)
 #endif
-__global__ void __launch_bounds__(256, NRRS_SCATTER_MINB) trace_scatter_kernel(RenderScene s, VertexRecDev v, const uint32_t *slots, uint32_t spawned,
+__global__ void __launch_bounds__(256, NRRS_SCATTER_MINB) trace_scatter_kernel(RenderScene s_in, VertexRecDev v, const uint32_t *slots, uint32_t spawned,
                                      uint32_t depth, uint64_t mixed_seed, PathStateDev *next, uint8_t *used,
                                      double *slot_term, TraceCounters *cnt) {
+    const RenderScene s = stage_scene(s_in);
     uint32_t shadows = 0, nonfinite = 0;
     for (uint32_t sl = blockIdx.x * blockDim.x + threadIdx.x; sl < spawned; sl += gridDim.x * blockDim.x) {
         const uint32_t j = slots[2 * (uint64_t)sl], c = slots[2 * (uint64_t)sl + 1];
@@ -890,12 +915,19 @@ cudaError_t launch_trace_camera(const RenderScene &s, uint32_t width, uint32_t h
     return cudaGetLastError();
 }
 
+// Dynamic smem for stage_scene: the scene's nodes + triangle records when they fit in 16 KB
+// (a few CTAs per SM keep their occupancy), else 0 (walks read global memory).
+static size_t scene_smem_bytes(const RenderScene &s) {
+    const size_t b = (size_t)s.n_nodes * sizeof(BvhNodeDev) + (size_t)s.n_tri * 48u;
+    return b <= 16384 ? b : 0;
+}
+
 cudaError_t launch_trace_shade(const RenderScene &s, const PathStateDev *q, uint32_t n, uint32_t depth,
                                uint8_t *cls, uint8_t *is_surf, float *hit_t, uint32_t *pair, double *term,
                                float *normals, uint32_t *err, int num_sms, cudaStream_t stream) {
     if (n == 0)
         return cudaSuccess;
-    trace_shade_kernel<<<grid_for(n, num_sms), 256, 0, stream>>>(s, q, n, depth, cls, is_surf, hit_t, pair, term,
+    trace_shade_kernel<<<grid_for(n, num_sms), 256, scene_smem_bytes(s), stream>>>(s, q, n, depth, cls, is_surf, hit_t, pair, term,
                                                                  normals, err);
     return cudaGetLastError();
 }
@@ -915,7 +947,7 @@ cudaError_t launch_trace_scatter(const RenderScene &s, VertexRecDev v, const uin
                                  double *slot_term, TraceCounters *cnt, int num_sms, cudaStream_t stream) {
     if (spawned == 0)
         return cudaSuccess;
-    trace_scatter_kernel<<<grid_for(spawned, num_sms), 256, 0, stream>>>(s, v, slots, spawned, depth, mixed_seed, next,
+    trace_scatter_kernel<<<grid_for(spawned, num_sms), 256, scene_smem_bytes(s), stream>>>(s, v, slots, spawned, depth, mixed_seed, next,
                                                                          used, slot_term, cnt);
     return cudaGetLastError();
 }
