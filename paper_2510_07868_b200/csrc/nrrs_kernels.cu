@@ -631,9 +631,9 @@ __device__ __forceinline__ void ws_load_sum16(uint32_t lane_base, uint32_t col_d
         uint64_t v = pk2(z[2 * i], z[2 * i + 1]);
         if (!kMma3)
             v = fadd2(v, pk2(lo[2 * i], lo[2 * i + 1]));
-        if (bias) {
-            const float2 b = reinterpret_cast<const float2 *>(bias + c0)[i];
-            v = fadd2(v, pk2(b.x, b.y));
+        if (bias) {  // 16-byte bias loads (the blob keeps every bias 64-byte aligned)
+            const float4 b4 = reinterpret_cast<const float4 *>(bias + c0)[i >> 1];
+            v = fadd2(v, (i & 1) ? pk2(b4.z, b4.w) : pk2(b4.x, b4.y));
         }
         const float2 f = upk2(v);
         z[2 * i] = f.x;
