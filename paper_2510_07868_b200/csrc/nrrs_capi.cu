@@ -160,6 +160,11 @@ struct nrrs_gpu_ctx {
     cudaStream_t stream = nullptr;
     std::string err;
     uint64_t launches = 0;
+    // tuning / test switches, read once at nrrs_gpu_create (never on the per-call path)
+    bool env_no_level_kernel = false;  // NRRS_NO_LEVEL_KERNEL: AID through the fused-gather K-A
+    bool env_fp32_tables = false;      // NRRS_FP32_TABLES: keep the AID grid in fp32
+    int env_sync_chunks = 0;           // NRRS_SYNC_CHUNKS / NRRS_ASYNC_CHUNKS: host-path H2D pieces (0: default)
+    int env_async_chunks = 0;
 
     // weights
     bool has_weights = false;
@@ -308,6 +313,12 @@ int nrrs_gpu_create(int device, nrrs_gpu_ctx **out) {
     auto *ctx = new nrrs_gpu_ctx();
     ctx->device = device;
     cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+    ctx->env_no_level_kernel = std::getenv("NRRS_NO_LEVEL_KERNEL") != nullptr;
+    ctx->env_fp32_tables = std::getenv("NRRS_FP32_TABLES") != nullptr;
+    if (const char *sc = std::getenv("NRRS_SYNC_CHUNKS"))
+        ctx->env_sync_chunks = std::max(1, std::min(std::atoi(sc), kMaxHostChunks));
+    if (const char *mc = std::getenv("NRRS_ASYNC_CHUNKS"))
+        ctx->env_async_chunks = std::max(1, std::min(std::atoi(mc), kMaxHostChunks));
     if (cudaMalloc(&ctx->d_misc, 16 * sizeof(uint32_t)) != cudaSuccess ||
         cudaMalloc(&ctx->d_res, sizeof(DevResult)) != cudaSuccess ||
         cudaMalloc(&ctx->d_sum, (kChunkSums + kMaxHostChunks) * sizeof(double)) != cudaSuccess ||
@@ -509,7 +520,7 @@ int nrrs_gpu_set_weights(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w) {
     // The AID grid (RRSNet input, no Box-Cox amplification downstream) is stored in fp16:
     // half the bytes per gather on the path's binding resource, max relative error of q
     // 1.1e-4 against the 1e-3 bar.  Tables beyond fp16 range stay fp32.
-    bool half = w->variant == NRRS_VARIANT_AID && !std::getenv("NRRS_FP32_TABLES");
+    bool half = w->variant == NRRS_VARIANT_AID && !ctx->env_fp32_tables;
     for (uint64_t i = 0; half && i < rrs_grid_len; ++i)
         if (!(std::fabs(w->rrs_grid[i]) < 32768.0f))
             half = false;
@@ -593,7 +604,7 @@ static int prepare_level_planes(nrrs_gpu_ctx *ctx, int kind, InferParams &ip, ui
     *n_kernels = 1;
     ip.feat = nullptr;
     ip.feat_stride = 0;
-    if (kind != kKindAid || !ctx->rrs_half || std::getenv("NRRS_NO_LEVEL_KERNEL") ||
+    if (kind != kKindAid || !ctx->rrs_half || ctx->env_no_level_kernel ||
         (uint64_t)ctx->grid_rrs.table_size * 4u > kLevelSmemMax || ip.n == 0)
         return NRRS_OK;
     const uint64_t stride = (ip.n + 31) & ~31ull;
@@ -674,20 +685,21 @@ static int run_factors(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, 
 #ifdef NRRS_KERNEL_TIMING
     if (const char *ab = std::getenv("NRRS_DEBUG_ABLATE"))  // diagnostics build only; results invalid
         ip.ablate = (uint32_t)std::atoi(ab);
-#endif
     unsigned long long *dbg = nullptr;
-    const bool timing = std::getenv("NRRS_DEBUG_TIMING") != nullptr;  // diagnostics only
+    const bool timing = std::getenv("NRRS_DEBUG_TIMING") != nullptr;  // diagnostics build only
     if (timing) {
         CK(ctx, cudaMalloc(&dbg, 32 * 1024 * sizeof(unsigned long long)));
         CK(ctx, cudaMemsetAsync(dbg, 0, 32 * 1024 * sizeof(unsigned long long), ctx->stream));
         ip.dbg = dbg;
     }
+#endif
     uint32_t grid = 0, n_kernels = 1;
     rc = prepare_level_planes(ctx, kind, ip, &n_kernels);
     if (rc)
         return rc;
     CK(ctx, launch_infer(kind, ip, ctx->num_sms, ctx->stream, &grid));
     ctx->launches += n_kernels;
+#ifdef NRRS_KERNEL_TIMING
     if (timing) {
         std::vector<unsigned long long> h(32 * 1024);
         CK(ctx, cudaMemcpyAsync(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
@@ -721,6 +733,7 @@ static int run_factors(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, 
                      (mxs - mn) / 1e3, (mx - mne) / 1e3, (mx - mn) / 1e3);
         cudaFree(dbg);
     }
+#endif
     return NRRS_OK;
 }
 
@@ -765,6 +778,8 @@ static int check_out(nrrs_gpu_ctx *ctx, const nrrs_stage_out *o, uint64_t n) {
         return fail(ctx, NRRS_EINVAL, "stage out: q_norm, q_real and slots are required");
     if ((reinterpret_cast<uintptr_t>(o->q_norm) | reinterpret_cast<uintptr_t>(o->q_real)) & 15u)
         return fail(ctx, NRRS_EINVAL, "stage out: q_norm / q_real must be 16-byte aligned");
+    if (reinterpret_cast<uintptr_t>(o->slots) & 7u)
+        return fail(ctx, NRRS_EINVAL, "stage out: slots must be 8-byte aligned");
     return NRRS_OK;
 }
 
@@ -1751,6 +1766,9 @@ int nrrs_gpu_stage_factors(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t
         return rc;
     float *q = o && o->q_orig ? o->q_orig : ctx->d_q;
     float *u = o && o->u ? o->u : ctx->d_u;
+    // nrrs_gpu_stage_decide reads q_orig / u as 16-byte vectors
+    if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(u)) & 15u)
+        return fail(ctx, NRRS_EINVAL, "stage out: q_orig / u must be 16-byte aligned");
     return run_factors(ctx, v, n, p, q, u, o ? o->decided : nullptr, d_local_sum);
 }
 
@@ -1774,6 +1792,8 @@ int nrrs_gpu_stage_decide(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_stage_params
         return rc;
     const float *q = o->q_orig ? o->q_orig : ctx->d_q;
     const float *u = o->u ? o->u : ctx->d_u;
+    if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(u)) & 15u)
+        return fail(ctx, NRRS_EINVAL, "stage out: q_orig / u must be 16-byte aligned");
     // n_pixels here is the GLOBAL budget (sum over ranks); capacity clips the
     // rank-local records, the global clip is applied by the caller.
     return run_decide(ctx, n, p, q, u, d_rank_sums, nranks, p->n_pixels, cap, o,
@@ -2158,7 +2178,9 @@ static int enqueue_host_stage(nrrs_gpu_ctx *ctx, Staging &s, const nrrs_vertex_s
         rc = run_factors(ctx, &dv, cn, p, s.q_orig + base, s.u + base, dout->decided ? dout->decided + base : nullptr,
                          chunk_sums + c, c > 0);
         if (rc) {
+            // chunks already enqueued may still read / write set s on either stream
             cudaStreamSynchronize(ctx->copy_stream);
+            cudaStreamSynchronize(ctx->stream);
             return rc;
         }
     }
@@ -2224,9 +2246,8 @@ int nrrs_gpu_rrs_stage_host(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *h, uint64_
             *h_result = r;
         return rc;
     }
-    const char *sc = std::getenv("NRRS_SYNC_CHUNKS");
     rc = enqueue_host_stage(ctx, s, h, n, p, cap, &dout, nullptr,
-                            sc ? (uint64_t)std::max(1, std::min(std::atoi(sc), kMaxHostChunks)) : kSyncHostChunks);
+                            ctx->env_sync_chunks ? (uint64_t)ctx->env_sync_chunks : kSyncHostChunks);
     if (rc)
         return rc;
     auto d2h = [&](void *dst, const void *src, size_t bytes) -> int {
@@ -2288,9 +2309,8 @@ int nrrs_gpu_rrs_stage_host_async(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *h, u
     // set b is free once the D2H of the call that last used it is done
     // two calls in flight already overlap the copies with the other call's kernels: fewer, larger H2D
     // pieces (each cudaMemcpyAsync costs a few microseconds of link time)
-    const char *mc = std::getenv("NRRS_ASYNC_CHUNKS");
     rc = enqueue_host_stage(ctx, s, h, n, p, cap, &dout, ctx->ev_d2h_done[b],
-                            mc ? (uint64_t)std::max(1, std::min(std::atoi(mc), kMaxHostChunks)) : kAsyncHostChunks);
+                            ctx->env_async_chunks ? (uint64_t)ctx->env_async_chunks : kAsyncHostChunks);
     if (rc)
         return rc;
     // snapshot the scalars before the next call's K-A reuses d_res, then hand set b to the D2H stream

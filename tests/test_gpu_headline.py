@@ -1,0 +1,61 @@
+"""GPU parity at the benchmarked sizes (VERDICT r1 "What's weak" #1).
+
+The C1-sized parity tests run at most one K-A tile per group (65,536 vertices = 512 tiles over
+148 CTAs).  The paths that only run at the headline size -- next-tile TMA staging, the cross-tile
+mbarrier phase toggling, many look-back tiles in K-B -- are checked here against the oracle:
+
+* AID-NRRS at the configs[2] shape (2,073,600 vertices, Npx = 1920 x 1080, depth 2) and NRRS at
+  1,228,800 vertices (every group runs >= 2 tiles);
+* q_orig within the north-star 1e-3 relative on EVERY vertex (the oracle runs the whole batch on
+  all host threads; networks.cpp:266-281 restated);
+* the GPU's own q_orig and u fed through the oracle's decide chain (rrs.cpp:8-45,
+  wavefront.cpp:141-154, :390-425) give bit-identical q_norm, q_real, k, offsets and slot records.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as orc
+from helpers import mirror_nets, oracle_decide, rel_err, to_dev
+from paper_2510_07868_b200 import RateControl, RrsStage, Strategy, StrategyKind, queue_capacity_for
+
+pytestmark = pytest.mark.gpu
+REL_TOL = 1e-3  # north_star: RRSNet outputs within 1e-3 relative
+
+CASES = [
+    pytest.param(orc.VARIANT_AID, orc.AID_NRRS, 1920 * 1080, id="aid-2073600"),
+    pytest.param(orc.VARIANT_NRRS, orc.NRRS, 1_228_800, id="nrrs-1228800"),
+]
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+@pytest.mark.parametrize("variant,kind,n", CASES)
+def test_headline_size_parity(variant, kind, n):
+    v = orc.gen_vertices(n)
+    on = orc.OracleNets(variant, seed=1, randomize=True)
+    cap = queue_capacity_for(n)
+    ref = orc.rrs_stage(v, 2, n, cap, kind, on, gain=0.85, seed=0, threads=orc.threads_available())
+    st = RrsStage(n, mirror_nets(on))
+    out, res = st.run(to_dev(v), 2, Strategy(StrategyKind(kind)), rc=RateControl(), full=True)
+    torch.cuda.synchronize()
+    q = _np(out.q_orig)
+    err = rel_err(q, ref["q_orig"], 1e-6)
+    assert err.max() <= REL_TOL, f"q_orig max rel err {err.max():.3e} at vertex {int(err.argmax())}"
+    np.testing.assert_array_equal(_np(out.u), ref["u"])
+    np.testing.assert_array_equal(_np(out.decided), ref["decided"])
+    assert abs(res.f_norm - ref["f_norm"]) <= REL_TOL * ref["f_norm"]
+    # the decision chain on the GPU's own factors: bit-exact against the oracle's chain
+    dec = oracle_decide(q, _np(out.u), n, cap, 0.85)
+    assert np.float32(res.f_norm) == np.float32(dec["f_norm"])
+    np.testing.assert_array_equal(_np(out.q_norm), dec["q_norm"])
+    np.testing.assert_array_equal(_np(out.q_real), dec["q_real"])
+    np.testing.assert_array_equal(_np(out.k), dec["k"])
+    np.testing.assert_array_equal(_np(out.offset).view(np.uint32), dec["offset"])
+    assert res.total == dec["total"] and res.spawned == dec["spawned"] and res.dropped == dec["dropped"]
+    np.testing.assert_array_equal(_np(out.slots)[:res.spawned].view(np.uint32), dec["slots"])
+    st.close()
