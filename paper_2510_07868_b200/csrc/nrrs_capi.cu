@@ -737,6 +737,43 @@ static int run_factors(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, 
     return NRRS_OK;
 }
 
+
+#ifdef NRRS_KERNEL_TIMING
+// Diagnostics build only (NRRS_KERNEL_TIMING, env NRRS_DEBUG_TIMING): per-tile phase stamps of
+// the last K-B / K-C launch, printed as microseconds after the earliest tile start.
+static unsigned long long *phase_dbg(nrrs_gpu_ctx *ctx) {
+    static unsigned long long *buf = nullptr;
+    if (!std::getenv("NRRS_DEBUG_TIMING"))
+        return nullptr;
+    if (!buf)
+        cudaMalloc(&buf, 8 * 4096 * sizeof(unsigned long long));
+    cudaMemsetAsync(buf, 0, 8 * 4096 * sizeof(unsigned long long), ctx->stream);
+    return buf;
+}
+static void phase_dump(nrrs_gpu_ctx *ctx, const char *what, unsigned long long *buf, uint32_t tiles) {
+    if (!buf)
+        return;
+    std::vector<unsigned long long> h(8 * (size_t)tiles);
+    cudaMemcpyAsync(h.data(), buf, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+    unsigned long long t0 = ~0ull;
+    for (uint32_t t = 0; t < tiles; ++t)
+        if (h[8 * t] && h[8 * t] < t0)
+            t0 = h[8 * t];
+    std::fprintf(stderr, "[nrrs phases] %s tiles %u (us after first start: min / median / max)\n", what, tiles);
+    for (int k = 0; k < 7; ++k) {
+        std::vector<double> v;
+        for (uint32_t t = 0; t < tiles; ++t)
+            if (h[8 * t + k])
+                v.push_back(k == 6 ? (double)h[8 * t + k] : (double)(h[8 * t + k] - t0) / 1e3);
+        if (v.empty())
+            continue;
+        std::sort(v.begin(), v.end());
+        std::fprintf(stderr, "  phase %d: %.2f / %.2f / %.2f\n", k, v.front(), v[v.size() / 2], v.back());
+    }
+}
+#endif
+
 static int run_decide(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_stage_params *p, const float *q, const float *u,
                       const double *rank_sums, int nranks, uint64_t n_pixels, uint32_t capacity,
                       const nrrs_stage_out *o, unsigned long long *total_out, DevResult *res) {
@@ -764,7 +801,13 @@ static int run_decide(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_stage_params *p,
     dp.err_flag = ctx->d_misc + 3;
     dp.total_out = total_out;
     dp.res = res;
-    CK(ctx, launch_decide(0, dp, ctx->stream));
+#ifdef NRRS_KERNEL_TIMING
+    dp.dbg = phase_dbg(ctx);
+#endif
+    CK(ctx, launch_decide(0, dp, ctx->num_sms, ctx->stream));
+#ifdef NRRS_KERNEL_TIMING
+    phase_dump(ctx, "decide3", dp.dbg, dp.num_tiles);
+#endif
     ctx->launches += 1;
     return NRRS_OK;
 }
@@ -1860,7 +1903,13 @@ int nrrs_gpu_compact(nrrs_gpu_ctx *ctx, const void *d_in, const uint8_t *d_used,
         cp.sync = ctx->d_sync + 1;
         cp.state_cap = (uint32_t)ctx->cap_ctiles;
         cp.num_tiles = compact_tiles(count, record_words);
-        CK(ctx, launch_compact(record_words, cp, ctx->stream));
+#ifdef NRRS_KERNEL_TIMING
+        cp.dbg = phase_dbg(ctx);
+#endif
+        CK(ctx, launch_compact(record_words, cp, ctx->num_sms, ctx->stream));
+#ifdef NRRS_KERNEL_TIMING
+        phase_dump(ctx, "compact3", cp.dbg, cp.num_tiles);
+#endif
         ctx->launches += 1;
     }
     if (h_count) {
@@ -1895,7 +1944,7 @@ int nrrs_gpu_compact_dev(nrrs_gpu_ctx *ctx, const void *d_in, const uint8_t *d_u
     cp.sync = ctx->d_sync + 1;
     cp.state_cap = (uint32_t)ctx->cap_ctiles;
     cp.num_tiles = compact_tiles(max_count, record_words);
-    CK(ctx, launch_compact(record_words, cp, ctx->stream));
+    CK(ctx, launch_compact(record_words, cp, ctx->num_sms, ctx->stream));
     ctx->launches += 1;
     return NRRS_OK;
 }
@@ -1981,7 +2030,7 @@ int nrrs_gpu_plan_spawns(nrrs_gpu_ctx *ctx, const int32_t *d_counts, uint64_t n,
     dp.num_tiles = decide_tiles(n);
     dp.err_flag = ctx->d_misc + 3;
     dp.total_out = ctx->d_total + 2;
-    CK(ctx, launch_decide(1, dp, ctx->stream));
+    CK(ctx, launch_decide(1, dp, ctx->num_sms, ctx->stream));
     ctx->launches += 1;
     uint32_t err = 0;
     unsigned long long total = 0;

@@ -88,6 +88,33 @@ __device__ __forceinline__ float softplus_mod(float x) {
 
 __device__ __forceinline__ float mean3(float x, float y, float z) { return (x + (y + z)) / 3.0f; }
 
+// Tolerance-path forms of the encodings (the network inputs; q within 1e-3): single MUFU
+// ops with flush-to-zero instead of the IEEE / denormal-safe sequences.  The clamp count of
+// box_cox (an integer output) is the exact predicate.
+__device__ __forceinline__ float ex2_ftz(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_ftz(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float sqrt_ftz(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float box_cox_fast(float x, uint32_t &clamps) {
+    if (x < 0.0f) {
+        ++clamps;
+        x = 0.0f;
+    }
+    return (sqrt_ftz(x) - 1.0f) * 2.0f;
+}
+__device__ __forceinline__ float mean3_fast(float x, float y, float z) { return (x + (y + z)) * (1.0f / 3.0f); }
+
 // stochastic_round (encodings.hpp:21-27) on a sanitized q >= 0.
 __device__ __forceinline__ uint32_t stochastic_round(float q, float u) {
     const float fl = floorf(q);
@@ -364,6 +391,18 @@ constexpr uint64_t kValueMask = (1ull << 48) - 1;
 
 __device__ __forceinline__ void st_release_u64(uint64_t *p, uint64_t v) {
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Relaxed (no fence) forms: a published aggregate carries its value in the same word, so readers
+// need no ordering against the publisher's other stores -- and a release would first wait for
+// every store the CTA has in flight.
+__device__ __forceinline__ void st_relaxed_u64(uint64_t *p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
 }
 
 __device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t *p) {

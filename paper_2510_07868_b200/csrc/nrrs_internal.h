@@ -146,6 +146,9 @@ struct DecideParams {
     uint32_t *err_flag;
     unsigned long long *total_out;
     DevResult *res;
+    uint32_t tile_items;      // items per tile (multiple of 512; set by launch_decide / launch_compact)
+    uint32_t single_wave;     // every tile resident at once: prefix = sum of predecessor aggregates
+    unsigned long long *dbg;  // NRRS_KERNEL_TIMING builds only: per-tile %globaltimer phase stamps [tile][8]
 };
 
 struct CompactParams {
@@ -159,6 +162,9 @@ struct CompactParams {
     uint32_t state_cap;
     LaunchSync *sync;
     uint32_t num_tiles;
+    uint32_t tile_items;      // items per tile (multiple of 512; set by launch_decide / launch_compact)
+    uint32_t single_wave;     // every tile resident at once: prefix = sum of predecessor aggregates
+    unsigned long long *dbg;  // NRRS_KERNEL_TIMING builds only: per-tile %globaltimer phase stamps [tile][8]
 };
 
 // TrainSample emission for one depth (nrrs_film.cu).
@@ -337,10 +343,12 @@ cudaError_t launch_sharded_clip(const unsigned long long *totals, int nranks, in
                                 unsigned long long *out, cudaStream_t stream);
 cudaError_t launch_infer(int kind, const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out);
 uint32_t infer_max_grid(int num_sms);
+// Upper bounds of the look-back tile count (state array sizes); the launchers pick the tile shape
+// (one wave of <= num_sms tiles when the batch fits) and fill num_tiles / tile_items / single_wave.
 uint32_t decide_tiles(uint64_t n);
-cudaError_t launch_decide(int src, const DecideParams &p, cudaStream_t stream);
+cudaError_t launch_decide(int src, DecideParams p, int num_sms, cudaStream_t stream);
 uint32_t compact_tiles(uint64_t count, uint32_t words);
-cudaError_t launch_compact(uint32_t words, const CompactParams &p, cudaStream_t stream);
+cudaError_t launch_compact(uint32_t words, CompactParams p, int num_sms, cudaStream_t stream);
 cudaError_t launch_lum_sum(const float *i_acc, uint64_t n, double *parts, uint32_t *counter, double *sum_out,
                            uint32_t grid, cudaStream_t stream);
 cudaError_t launch_sum_check(const float *q, uint64_t n, double *parts, uint32_t *counter, uint32_t *err,

@@ -152,24 +152,25 @@ __device__ __forceinline__ void grid_encode4(const void *theta, const GridDev &g
     }
 }
 
-// one_blob_encode (encodings.hpp:31-44) with the fast exp (tolerance path).
+// one_blob_encode (encodings.hpp:31-44), tolerance path: exp(-d^2 / (2 sigma^2)) as one
+// flush-to-zero ex2 per bin with log2(e) folded into the constant, approximate reciprocal.
 template <int BINS>
 __device__ __forceinline__ void one_blob_fast(float x, float *out) {
-    constexpr float inv_two_sigma2 = (float)(BINS * BINS) * 0.5f;
+    constexpr float k = -(float)(BINS * BINS) * 0.5f * 1.4426950408889634f;
     float sum = 0.0f;
 #pragma unroll
     for (int i = 0; i < BINS; ++i) {
         const float d = x - ((float)i + 0.5f) / (float)BINS;
-        out[i] = __expf(-d * d * inv_two_sigma2);
+        out[i] = ex2_ftz(d * d * k);
         sum += out[i];
     }
-    const float inv = __fdividef(1.0f, sum);
+    const float inv = rcp_ftz(sum);
 #pragma unroll
     for (int i = 0; i < BINS; ++i)
         out[i] *= inv;
 }
 
-__device__ __forceinline__ float remap_fast(float a) { return 1.0f - __expf(-a); }
+__device__ __forceinline__ float remap_fast(float a) { return 1.0f - ex2_ftz(a * -1.4426950408889634f); }
 
 // ===========================================================================
 // K-A0: level-sliced hash-grid encode (fp16 tables that fit in shared memory).
@@ -249,7 +250,7 @@ __device__ __forceinline__ float2 level_encode(const uint8_t *tab, const LevelCo
 
 __global__ void __launch_bounds__(kLevelThreads, 1) grid_level_kernel(GridLevelParams p) {
     extern __shared__ __align__(128) uint8_t lvl_smem[];
-    __shared__ uint64_t bar[5];  // [0] table, [1..2] p01 blocks full, [3..4] p01 blocks empty
+    __shared__ uint64_t bar[1];  // table landed
     const GridDev &g = p.g;
     const uint32_t L = (uint32_t)g.levels;
     const uint32_t l = blockIdx.x % L, q = blockIdx.x / L;
@@ -260,35 +261,15 @@ __global__ void __launch_bounds__(kLevelThreads, 1) grid_level_kernel(GridLevelP
     const uint32_t entries = dense ? nn * nn * nn : g.table_size;
     const uint32_t bytes = (entries * 4u + 15u) & ~15u;
     const uint32_t tab_bytes = g.table_size * 4u;
-    float *pbuf = reinterpret_cast<float *>(lvl_smem + tab_bytes);  // 2 x kLevelBlock x 3 floats
     const uint64_t n = p.n;
-    // CTA range, 4-vertex aligned so every staged block starts on a 16-byte boundary
-    const uint64_t j0 = (n * q / nq) & ~3ull;
-    const uint64_t j1 = q + 1 == nq ? n : ((n * (q + 1) / nq) & ~3ull);
-    const bool staged = (reinterpret_cast<uintptr_t>(p.p01) & 15u) == 0;
-    const uint32_t nblocks = (uint32_t)((j1 - j0 + kLevelBlock - 1) / kLevelBlock);
-    // staged bytes of block b: whole 4-vertex groups only (the <= 3 tail vertices load directly)
-    auto issue = [&](uint32_t b) {
-        const uint64_t s = j0 + (uint64_t)b * kLevelBlock;
-        const uint64_t e = s + kLevelBlock < j1 ? s + kLevelBlock : j1;
-        const uint32_t nb = (uint32_t)((e - s) & ~3ull) * 12u;
-        mbar_arrive_expect_tx(&bar[1 + (b & 1)], nb);
-        if (nb)
-            bulk_g2s(pbuf + (b & 1) * kLevelBlock * 3, p.p01 + 3 * s, nb, &bar[1 + (b & 1)]);
-    };
+    const uint64_t j0 = n * q / nq, j1 = n * (q + 1) / nq;  // this CTA's vertex range
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 3; ++i)
-            mbar_init(&bar[i], 1);
-        mbar_init(&bar[3], kLevelThreads);
-        mbar_init(&bar[4], kLevelThreads);
+        mbar_init(&bar[0], 1);
         fence_barrier_init();
         mbar_arrive_expect_tx(&bar[0], bytes);
         const uint8_t *src = reinterpret_cast<const uint8_t *>(p.table) + (uint64_t)l * tab_bytes;
         for (uint32_t off = 0; off < bytes; off += 32768u)
             bulk_g2s(lvl_smem + off, src + off, bytes - off < 32768u ? bytes - off : 32768u, &bar[0]);
-        if (staged)
-            for (uint32_t b = 0; b < 2 && b < nblocks; ++b)
-                issue(b);
     }
     __syncthreads();
     LevelConsts c;
@@ -301,25 +282,16 @@ __global__ void __launch_bounds__(kLevelThreads, 1) grid_level_kernel(GridLevelP
     for (int k = 0; k < 8; ++k)
         c.doff4[k] = (((k & 1) * nn + ((k >> 1) & 1)) * nn + (k >> 2)) * 4u;
     float2 *out = p.feat + (uint64_t)l * p.feat_stride;
-    mbar_wait(&bar[0], 0);
-    for (uint32_t b = 0; b < nblocks; ++b) {
-        const uint64_t s = j0 + (uint64_t)b * kLevelBlock;
-        const uint32_t cnt = (uint32_t)((j1 - s) < kLevelBlock ? (j1 - s) : kLevelBlock);
-        const uint32_t cnt4 = staged ? (cnt & ~3u) : 0u;
-        const float *pb = pbuf + (b & 1) * kLevelBlock * 3;
-        if (staged)
-            mbar_wait(&bar[1 + (b & 1)], (b >> 1) & 1u);
-        // kLevelPer vertices per thread (t, t + 1024, ...): independent smem gathers in flight together
-        float pv[kLevelPer][3];
+    // kLevelPer vertices per thread per block (t, t + 1024, ...); the next block's p01 is loaded
+    // into registers before this block's gathers, so its L2 round trip hides behind them (no
+    // shared-memory staging and no barrier in the loop: every thread owns its own vertices).
+    float pv[kLevelPer][3];
+    auto load_block = [&](uint64_t s) {
 #pragma unroll
         for (int u = 0; u < (int)kLevelPer; ++u) {
-            const uint32_t t = threadIdx.x + u * kLevelThreads;
-            if (t < cnt4) {
-                pv[u][0] = pb[3 * t];
-                pv[u][1] = pb[3 * t + 1];
-                pv[u][2] = pb[3 * t + 2];
-            } else if (t < cnt) {
-                const float *g3 = p.p01 + 3 * (s + t);
+            const uint64_t j = s + threadIdx.x + (uint64_t)u * kLevelThreads;
+            if (j < j1) {
+                const float *g3 = p.p01 + 3 * j;
                 pv[u][0] = __ldg(g3);
                 pv[u][1] = __ldg(g3 + 1);
                 pv[u][2] = __ldg(g3 + 2);
@@ -327,22 +299,29 @@ __global__ void __launch_bounds__(kLevelThreads, 1) grid_level_kernel(GridLevelP
                 pv[u][0] = pv[u][1] = pv[u][2] = 0.0f;
             }
         }
-        if (staged)
-            mbar_arrive(&bar[3 + (b & 1)]);  // this thread is done with buffer b & 1
-        if (staged && threadIdx.x == 0 && b + 2 < nblocks) {
-            mbar_wait(&bar[3 + (b & 1)], (b >> 1) & 1u);
-            fence_proxy_async_smem();
-            issue(b + 2);
+    };
+    load_block(j0);
+    mbar_wait(&bar[0], 0);
+    for (uint64_t s = j0; s < j1; s += kLevelBlock) {
+        float cur[kLevelPer][3];
+#pragma unroll
+        for (int u = 0; u < (int)kLevelPer; ++u) {
+            cur[u][0] = pv[u][0];
+            cur[u][1] = pv[u][1];
+            cur[u][2] = pv[u][2];
         }
+        if (s + kLevelBlock < j1)
+            load_block(s + kLevelBlock);
         float2 r[kLevelPer];
 #pragma unroll
         for (int u = 0; u < (int)kLevelPer; ++u)
-            r[u] = level_encode(lvl_smem, c, pv[u][0], pv[u][1], pv[u][2]);
-        float2 *ob = out + s + threadIdx.x;
+            r[u] = level_encode(lvl_smem, c, cur[u][0], cur[u][1], cur[u][2]);
 #pragma unroll
-        for (int u = 0; u < (int)kLevelPer; ++u)
-            if (threadIdx.x + u * kLevelThreads < cnt)
-                __stcs(ob + u * kLevelThreads, r[u]);
+        for (int u = 0; u < (int)kLevelPer; ++u) {
+            const uint64_t j = s + threadIdx.x + (uint64_t)u * kLevelThreads;
+            if (j < j1)
+                __stcs(out + j, r[u]);
+        }
     }
 }
 
@@ -376,7 +355,7 @@ cudaError_t launch_sharded_clip(const unsigned long long *totals, int nranks, in
 
 cudaError_t launch_grid_levels(const GridLevelParams &p, int num_sms, cudaStream_t stream) {
     const uint32_t L = (uint32_t)p.g.levels;
-    const size_t smem = (size_t)p.g.table_size * 4u + 2u * kLevelBlock * 12u;
+    const size_t smem = (size_t)p.g.table_size * 4u;
     cudaError_t e = cudaFuncSetAttribute(grid_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
         return e;
@@ -784,10 +763,10 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
                 if (KIND == kKindNrrs) {
                     float ipx, ipy, ipz;
                     load_ipix(ipx, ipy, ipz);
-                    sd.ex[0] = box_cox(wx, bc);
-                    sd.ex[1] = box_cox(wy, bc);
-                    sd.ex[2] = box_cox(wz, bc);
-                    sd.ex[3] = box_cox(mean3(ipx, ipy, ipz), bc);
+                    sd.ex[0] = box_cox_fast(wx, bc);
+                    sd.ex[1] = box_cox_fast(wy, bc);
+                    sd.ex[2] = box_cox_fast(wz, bc);
+                    sd.ex[3] = box_cox_fast(mean3_fast(ipx, ipy, ipz), bc);
                     sd.ex[4] = remap_fast(rough);
                 } else if (KIND == kKindAdrrs) {
                     float ipx, ipy, ipz;
@@ -800,10 +779,10 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
             } else if (KIND == kKindAid) {
                 float ipx, ipy, ipz;
                 load_ipix(ipx, ipy, ipz);
-                t8[0] = box_cox(wx, bc);
-                t8[1] = box_cox(wy, bc);
-                t8[2] = box_cox(wz, bc);
-                t8[3] = box_cox(mean3(ipx, ipy, ipz), bc);
+                t8[0] = box_cox_fast(wx, bc);
+                t8[1] = box_cox_fast(wy, bc);
+                t8[2] = box_cox_fast(wz, bc);
+                t8[3] = box_cox_fast(mean3_fast(ipx, ipy, ipz), bc);
                 one_blob_fast<4>(remap_fast(rough), t8 + 4);
             } else {
                 one_blob_fast<8>(remap_fast(rough), t8);
@@ -944,7 +923,7 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
                             uint32_t bc = 0;
 #pragma unroll
                             for (int k = 0; k < 6; ++k)
-                                xin[k] = box_cox(y[k], bc);
+                                xin[k] = box_cox_fast(y[k], bc);
 #pragma unroll
                             for (int k = 0; k < 5; ++k)
                                 xin[6 + k] = sd.ex[k];
@@ -1276,10 +1255,10 @@ __global__ void __launch_bounds__(GM * 128, 1) infer_aid_fused_kernel(InferParam
         }
         one_blob_fast<4>(wox, x0 + 8);
         one_blob_fast<4>(woy, x0 + 12);
-        x1[8] = box_cox(wx, bc);
-        x1[9] = box_cox(wy, bc);
-        x1[10] = box_cox(wz, bc);
-        x1[11] = box_cox(mean3(ia, ib, ic), bc);
+        x1[8] = box_cox_fast(wx, bc);
+        x1[9] = box_cox_fast(wy, bc);
+        x1[10] = box_cox_fast(wz, bc);
+        x1[11] = box_cox_fast(mean3_fast(ia, ib, ic), bc);
         one_blob_fast<4>(remap_fast(rough), x1 + 12);
         if (!valid) {
 #pragma unroll
@@ -1530,167 +1509,6 @@ __device__ __forceinline__ uint32_t block_scan_excl(uint32_t v, uint32_t *warp_t
     return before + inc - v;
 }
 
-struct Decide2Smem {
-    uint32_t k[kBTile];
-    uint32_t warp_tot[kBT / 32];
-    unsigned long long prefix;
-    uint32_t tile, epoch;
-};
-
-template <int SRC>  // 0: counts from (q, u) with normalization; 1: counts given (plan_spawns)
-__global__ void __launch_bounds__(kBT) decide2_kernel(DecideParams p) {
-    extern __shared__ __align__(16) uint8_t dsm[];
-    Decide2Smem &sm = *reinterpret_cast<Decide2Smem *>(dsm);
-    const int tid = threadIdx.x;
-    if (tid == 0)
-        sm.tile = claim_tile_epoch(p.sync, &sm.epoch);
-    __syncthreads();
-    const uint32_t tile = sm.tile, epoch = sm.epoch;
-    const uint64_t tbase = (uint64_t)tile * kBTile;
-
-    bool apply = false;
-    float scale = 1.0f;
-    if (SRC == 0) {
-        double sum = 0.0;
-        for (int r = 0; r < p.nranks; ++r)
-            sum += p.rank_sums[r];
-        if (sum > 0.0) {
-            const double f = __ddiv_rn((double)p.n_pixels, sum);  // F = Npx / sum (rrs.cpp:17)
-            if (f < 1.0) {
-                apply = true;
-                scale = __double2float_rn(f);  // s = float(F)  (rrs.cpp:19)
-            }
-            if (tile == 0 && tid == 0 && p.res)
-                p.res->f_norm = f;
-        } else if (tile == 0 && tid == 0 && p.res) {
-            p.res->f_norm = 1.0;
-        }
-    }
-
-    // ---- pass 1: factors -> counts (smem), q_norm / q_real out ----
-    uint32_t my_total = 0;
-    uint32_t bad = 0;
-#pragma unroll
-    for (int sub = 0; sub < kBSubs; ++sub) {
-        const uint64_t first = tbase + (uint64_t)sub * kBSub + (uint64_t)tid * kBItems;
-        uint32_t k[kBItems];
-        if (SRC == 0) {
-            float q[kBItems], u[kBItems];
-            const bool full = first + kBItems <= p.n;
-            if (full) {
-                const float4 qa = __ldcs(reinterpret_cast<const float4 *>(p.q + first));
-                const float4 ua = __ldcs(reinterpret_cast<const float4 *>(p.u + first));
-                q[0] = qa.x; q[1] = qa.y; q[2] = qa.z; q[3] = qa.w;
-                u[0] = ua.x; u[1] = ua.y; u[2] = ua.z; u[3] = ua.w;
-            } else {
-#pragma unroll
-                for (int i = 0; i < kBItems; ++i) {
-                    const bool ok = first + i < p.n;
-                    q[i] = ok ? p.q[first + i] : 0.0f;
-                    u[i] = ok ? p.u[first + i] : 0.0f;
-                }
-            }
-            float qn[kBItems], qr[kBItems];
-#pragma unroll
-            for (int i = 0; i < kBItems; ++i) {
-                qn[i] = apply ? __fmul_rn(q[i], scale) : q[i];  // q *= float(F)  (rrs.cpp:18-21)
-                qr[i] = __fmul_rn(qn[i], p.gain);               // q_real = q * gain (wavefront.cpp:396)
-                k[i] = stochastic_round(qr[i], u[i]);           // (rrs.cpp:35-45)
-            }
-            if (full) {
-                __stcs(reinterpret_cast<float4 *>(p.q_norm + first), make_float4(qn[0], qn[1], qn[2], qn[3]));
-                __stcs(reinterpret_cast<float4 *>(p.q_real + first), make_float4(qr[0], qr[1], qr[2], qr[3]));
-            } else {
-#pragma unroll
-                for (int i = 0; i < kBItems; ++i)
-                    if (first + i < p.n) {
-                        p.q_norm[first + i] = qn[i];
-                        p.q_real[first + i] = qr[i];
-                    }
-            }
-        } else {
-#pragma unroll
-            for (int i = 0; i < kBItems; ++i) {
-                const int32_t c = first + i < p.n ? p.counts_in[first + i] : 0;
-                if (c < 0)
-                    bad = 1;
-                k[i] = c < 0 ? 0u : (uint32_t)c;
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < kBItems; ++i) {
-            sm.k[sub * kBSub + tid * kBItems + i] = k[i];
-            my_total += k[i];
-        }
-    }
-    if (bad)
-        atomicOr(p.err_flag, 1u);
-    uint32_t agg = 0;
-    block_scan_excl<kBT>(my_total, sm.warp_tot, agg);
-    if (tid < 32) {
-        const uint64_t ex = lookback_warp(p.tile_state, tile, agg, epoch);
-        if (tid == 0)
-            sm.prefix = ex;
-    }
-    __syncthreads();
-    const uint64_t P = sm.prefix;
-    const uint64_t cap = p.capacity;
-
-    // ---- pass 2: offsets and slot records, sub-tile by sub-tile ----
-    uint64_t sub_base = P;
-#pragma unroll 1
-    for (int sub = 0; sub < kBSubs; ++sub) {
-        const uint64_t first = tbase + (uint64_t)sub * kBSub + (uint64_t)tid * kBItems;
-        uint32_t k[kBItems], ts = 0;
-#pragma unroll
-        for (int i = 0; i < kBItems; ++i) {
-            k[i] = sm.k[sub * kBSub + tid * kBItems + i];
-            ts += k[i];
-        }
-        uint32_t sagg = 0;
-        const uint32_t texcl = block_scan_excl<kBT>(ts, sm.warp_tot, sagg);
-        {
-            // offsets (wavefront.cpp:148) and this thread's slot records: child c of
-            // item j lands in slot cum + c while cum + c < capacity (:421-425, :436)
-            uint64_t cum = sub_base + texcl;
-            uint2 *slots = reinterpret_cast<uint2 *>(p.slots);
-#pragma unroll
-            for (int i = 0; i < kBItems; ++i) {
-                const uint64_t j = first + i;
-                if (j < p.n) {
-                    if (p.offset)
-                        p.offset[j] = (uint32_t)(cum < cap ? cum : cap);  // min(cum, capacity)
-                    if (p.k_out)
-                        p.k_out[j] = (int32_t)k[i];
-                    if (p.slots) {
-                        const uint64_t kept64 = cum < cap ? (cap - cum < k[i] ? cap - cum : k[i]) : 0;
-                        for (uint32_t c = 0; c < (uint32_t)kept64; ++c)
-                            __stcs(slots + cum + c, make_uint2((uint32_t)j + p.parent_base, c));
-                    }
-                }
-                cum += k[i];
-            }
-        }
-        sub_base += sagg;
-        __syncthreads();
-    }
-
-    if (tile == p.num_tiles - 1 && tid == 0) {
-        const uint64_t total = P + agg;
-        if (p.total_out)
-            *p.total_out = total;
-        if (p.res) {
-            const uint64_t spawned = total < cap ? total : cap;
-            p.res->total = total;
-            p.res->spawned = (uint32_t)spawned;
-            p.res->dropped = total - spawned;
-            p.res->overflow = total > spawned ? 1u : 0u;
-        }
-    }
-    if (tid == 0)
-        finish_launch(p.sync, p.tile_state, p.state_cap, epoch);
-}
-
 template <int W, int IPT>
 __global__ void __launch_bounds__(kBT) compact2_kernel(CompactParams p) {
     constexpr int kSub = kBT * IPT;
@@ -1803,6 +1621,423 @@ __global__ void __launch_bounds__(kBT) compact2_kernel(CompactParams p) {
     }
     if (tile == p.num_tiles - 1 && tid == 0)
         *p.count_out = (uint32_t)(*prefix + agg);
+    if (tid == 0)
+        finish_launch(p.sync, p.tile_state, p.state_cap, epoch);
+}
+
+// ===========================================================================
+// K-B / K-C, register-resident single-pass versions (round 2).
+//
+// A tile is up to 32 warps x 512 items; the launcher sizes it so the whole batch is ONE wave of
+// <= one tile per SM (2,073,600 vertices: 145 tiles of 14,336), larger batches use 16,384-item
+// tiles in several waves.  Items are warp-striped so every vector access is a fully coalesced
+// 512-byte warp request: lane l of warp w holds items w * 512 + 128 i + 4 l + e (group i, element
+// e).  One pass: all loads in flight at once, counts, 4 warp scans + one block reduction, the
+// tile's exclusive prefix (single wave: the sum of every predecessor's published aggregate, one
+// L2 round trip; several waves: the warp-parallel decoupled look-back), then the outputs.  A
+// warp's slot records of one item group are contiguous in the queue, so they are staged in the
+// warp's shared-memory buffer and leave as full 256-byte warp stores.  Index arithmetic is 32-bit
+// (n < 2^32 and the capacity is a u32; positions are tile-relative).
+// ===========================================================================
+constexpr int kD3T = 1024;            // threads
+constexpr int kD3Tile = kD3T * 16;    // items per full tile
+constexpr int kD3Warp = 512;          // items per warp
+constexpr int kD3Stage = 256;         // staged slot records per warp and item group (2 KB)
+
+__device__ __forceinline__ void stamp(unsigned long long *dbg, uint32_t tile, int k) {
+#ifdef NRRS_KERNEL_TIMING
+    if (dbg && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        dbg[tile * 8 + k] = t;
+    }
+#endif
+}
+
+struct Scan3Smem {
+    uint32_t warp_tot[kD3T / 32];
+    unsigned long long prefix;
+    uint32_t tile, epoch;
+};
+
+// Tile-relative exclusive position of this lane's first item of each group (items in (warp, i,
+// lane, e) order) from the per-group lane sums s[i]; the tile total in `agg`.
+__device__ __forceinline__ void scan4_positions(const uint32_t (&s)[4], Scan3Smem &sm, uint32_t (&excl)[4],
+                                                uint32_t &agg) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t run = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        uint32_t inc = s[i];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o)
+                inc += t;
+        }
+        excl[i] = run + inc - s[i];
+        run += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (lane == 0)
+        sm.warp_tot[warp] = run;
+    __syncthreads();
+    const uint32_t t = lane < (int)(blockDim.x >> 5) ? sm.warp_tot[lane] : 0u;
+    uint32_t before = lane < warp ? t : 0u, all = t;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        before += __shfl_xor_sync(0xffffffffu, before, o);
+        all += __shfl_xor_sync(0xffffffffu, all, o);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        excl[i] += before;
+    agg = all;
+}
+
+// Exclusive prefix of `tile` (warp 0, every lane gets it).  single_wave: every tile of the launch
+// is resident, so the prefix is the sum of all predecessors' aggregates, read at once; each tile's
+// state word sits on its own 128-byte line (kStatePad) so the ~N^2 / 2 polls spread over N L2
+// lines instead of hammering a few.
+constexpr uint32_t kStatePad = 16;
+__device__ __forceinline__ uint64_t tile_prefix(uint64_t *state, uint32_t tile, uint64_t agg, uint32_t epoch,
+                                                bool single_wave, unsigned long long *dbg = nullptr) {
+    if (!single_wave)
+        return lookback_warp(state, tile, agg, epoch);
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t tag = (uint64_t)(epoch & 0x3FFFu) << 48;
+    if (lane == 0)
+        st_relaxed_u64(&state[tile * kStatePad], kFlagAgg | tag | agg);
+    // up to 8 predecessors per lane (single wave: <= 256 tiles), requested together
+    const uint32_t ep = epoch & 0x3FFFu;
+    uint64_t st[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        const uint32_t t = lane + 32u * (uint32_t)r;
+        st[r] = t < tile ? ld_relaxed_u64(&state[t * kStatePad]) : 0ull;
+    }
+    uint64_t v = 0;
+    uint32_t polls = 0;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        const uint32_t t = lane + 32u * (uint32_t)r;
+        if (t < tile) {
+            while ((st[r] >> 62) == 0 || ((st[r] >> 48) & 0x3FFFu) != ep) {
+                st[r] = ld_relaxed_u64(&state[t * kStatePad]);
+                ++polls;
+            }
+            v += st[r] & kValueMask;
+        }
+    }
+#ifdef NRRS_KERNEL_TIMING
+    polls = __reduce_max_sync(0xffffffffu, polls);
+    if (dbg && lane == 0) {
+        unsigned long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        dbg[tile * 8 + 5] = t1;
+        dbg[tile * 8 + 6] = polls + 1;
+    }
+#else
+    (void)polls;
+#endif
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <int SRC>  // 0: counts from (q, u) with normalization; 1: counts given (plan_spawns)
+__global__ void __launch_bounds__(kD3T, 1) decide3_kernel(DecideParams p) {
+    __shared__ Scan3Smem sm;
+    extern __shared__ uint4 kq[];  // [group i][thread]: the thread's counts, parked between scan and writes
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0)
+        sm.tile = claim_tile_epoch(p.sync, &sm.epoch);
+    __syncthreads();
+    const uint32_t tile = sm.tile, epoch = sm.epoch;
+    stamp(p.dbg, tile, 0);
+    // this tile's items end at min(n, (tile + 1) * tile_items): warps past a short tile idle
+    const uint32_t n = min((uint32_t)p.n, (tile + 1u) * p.tile_items);
+    const uint32_t wbase = tile * p.tile_items + (uint32_t)warp * kD3Warp + 4u * (uint32_t)lane;
+
+    bool apply = false;
+    float scale = 1.0f;
+    if (SRC == 0) {
+        double sum = 0.0;
+        for (int r = 0; r < p.nranks; ++r)
+            sum += p.rank_sums[r];
+        if (sum > 0.0) {
+            const double f = __ddiv_rn((double)p.n_pixels, sum);  // F = Npx / sum (rrs.cpp:17)
+            if (f < 1.0) {
+                apply = true;
+                scale = __double2float_rn(f);  // s = float(F)  (rrs.cpp:19)
+            }
+            if (tile == 0 && tid == 0 && p.res)
+                p.res->f_norm = f;
+        } else if (tile == 0 && tid == 0 && p.res) {
+            p.res->f_norm = 1.0;
+        }
+    }
+    // items of this thread that exist, per group
+    uint32_t nv[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t first = wbase + 128u * (uint32_t)i;
+        nv[i] = first >= n ? 0u : (n - first < 4u ? n - first : 4u);
+    }
+    // ---- load every item of this thread (all requests in flight together) ----
+    uint32_t gs[4];
+    bool bad = false;
+    if (SRC == 0) {
+        float4 q4[4], u4[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t first = wbase + 128u * (uint32_t)i;
+            if (nv[i] == 4u) {
+                q4[i] = __ldcs(reinterpret_cast<const float4 *>(p.q + first));
+                u4[i] = __ldcs(reinterpret_cast<const float4 *>(p.u + first));
+            } else {
+                float qq[4], uu[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    qq[e] = (uint32_t)e < nv[i] ? p.q[first + e] : 0.0f;
+                    uu[e] = (uint32_t)e < nv[i] ? p.u[first + e] : 1.0f;
+                }
+                q4[i] = make_float4(qq[0], qq[1], qq[2], qq[3]);
+                u4[i] = make_float4(uu[0], uu[1], uu[2], uu[3]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t first = wbase + 128u * (uint32_t)i;
+            const float q[4] = {q4[i].x, q4[i].y, q4[i].z, q4[i].w};
+            const float u[4] = {u4[i].x, u4[i].y, u4[i].z, u4[i].w};
+            float qn[4], qr[4];
+            uint32_t k[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                qn[e] = apply ? __fmul_rn(q[e], scale) : q[e];  // q *= float(F)  (rrs.cpp:18-21)
+                qr[e] = __fmul_rn(qn[e], p.gain);               // q_real = q * gain (wavefront.cpp:396)
+                k[e] = stochastic_round(qr[e], u[e]);           // (rrs.cpp:35-45); padding has q = 0, u = 1
+            }
+            if (nv[i] == 4u) {
+                __stcs(reinterpret_cast<float4 *>(p.q_norm + first), make_float4(qn[0], qn[1], qn[2], qn[3]));
+                __stcs(reinterpret_cast<float4 *>(p.q_real + first), make_float4(qr[0], qr[1], qr[2], qr[3]));
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if ((uint32_t)e < nv[i]) {
+                        p.q_norm[first + e] = qn[e];
+                        p.q_real[first + e] = qr[e];
+                    }
+            }
+            gs[i] = k[0] + k[1] + k[2] + k[3];
+            kq[i * kD3T + tid] = make_uint4(k[0], k[1], k[2], k[3]);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t first = wbase + 128u * (uint32_t)i;
+            uint32_t k[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int32_t c = (uint32_t)e < nv[i] ? p.counts_in[first + e] : 0;
+                bad |= c < 0;
+                k[e] = c < 0 ? 0u : (uint32_t)c;
+            }
+            gs[i] = k[0] + k[1] + k[2] + k[3];
+            kq[i * kD3T + tid] = make_uint4(k[0], k[1], k[2], k[3]);
+        }
+        if (bad)
+            atomicOr(p.err_flag, 1u);
+    }
+    stamp(p.dbg, tile, 1);
+    // ---- tile scan + prefix ----
+    uint32_t excl[4], agg = 0;
+    scan4_positions(gs, sm, excl, agg);
+    stamp(p.dbg, tile, 2);
+    if (warp == 0) {
+        const uint64_t ex = tile_prefix(p.tile_state, tile, agg, epoch, p.single_wave != 0u, p.dbg);
+        if (lane == 0)
+            sm.prefix = ex;
+    }
+    __syncthreads();
+    const uint64_t P = sm.prefix;
+    const uint64_t cap = p.capacity;
+    stamp(p.dbg, tile, 3);
+    // room left in the queue at this tile's first record (positions below are tile-relative)
+    const uint32_t room = P < cap ? (uint32_t)(cap - P) : 0u;
+    const bool vec_out = ((reinterpret_cast<uintptr_t>(p.offset) | reinterpret_cast<uintptr_t>(p.k_out)) & 15u) == 0;
+    uint2 *slots = reinterpret_cast<uint2 *>(p.slots) + P;
+    uint2 *wbuf = reinterpret_cast<uint2 *>(kq + 4 * kD3T) + warp * kD3Stage;
+    // ---- offsets (wavefront.cpp:148) and slot records: child c of item j lands in slot
+    // cum + c while cum + c < capacity (:421-425, :436) ----
+#pragma unroll 1
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t first = wbase + 128u * (uint32_t)i;
+        uint32_t pos = excl[i];
+        const uint32_t gbase = __shfl_sync(0xffffffffu, pos, 0);
+        const uint32_t gtot = __shfl_sync(0xffffffffu, pos + gs[i], 31) - gbase;
+        const uint4 k4 = kq[i * kD3T + tid];
+        const uint32_t kk[4] = {k4.x, k4.y, k4.z, k4.w};
+        uint32_t off[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const uint64_t cum = P + pos;
+            off[e] = (uint32_t)(cum < cap ? cum : cap);  // min(cum, capacity)
+            const uint32_t kept = pos < room ? min(kk[e], room - pos) : 0u;
+            const uint32_t rel = pos - gbase;
+            const uint32_t j = first + (uint32_t)e + p.parent_base;
+#pragma unroll
+            for (uint32_t c = 0; c < 4u; ++c)
+                if (c < kept && rel + c < (uint32_t)kD3Stage)
+                    wbuf[rel + c] = make_uint2(j, c);
+            if (kept > 4u || (kept && rel + kept > (uint32_t)kD3Stage)) {  // rare: large counts
+                for (uint32_t c = 0; c < kept; ++c)
+                    if (c >= 4u || rel + c >= (uint32_t)kD3Stage) {
+                        if (rel + c < (uint32_t)kD3Stage)
+                            wbuf[rel + c] = make_uint2(j, c);
+                        else
+                            __stcs(slots + pos + c, make_uint2(j, c));
+                    }
+            }
+            pos += kk[e];
+        }
+        if (p.slots) {
+            __syncwarp();
+            const uint32_t groom = gbase < room ? room - gbase : 0u;
+            uint32_t nw = gtot < groom ? gtot : groom;
+            nw = nw < (uint32_t)kD3Stage ? nw : (uint32_t)kD3Stage;
+            for (uint32_t r = (uint32_t)lane; r < nw; r += 32u)
+                __stcs(slots + gbase + r, wbuf[r]);
+            __syncwarp();
+        }
+        if (p.offset || p.k_out) {
+            if (nv[i] == 4u && vec_out) {
+                if (p.offset)
+                    *reinterpret_cast<uint4 *>(p.offset + first) = make_uint4(off[0], off[1], off[2], off[3]);
+                if (p.k_out)
+                    *reinterpret_cast<int4 *>(p.k_out + first) =
+                        make_int4((int)kk[0], (int)kk[1], (int)kk[2], (int)kk[3]);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if ((uint32_t)e < nv[i]) {
+                        if (p.offset)
+                            p.offset[first + e] = off[e];
+                        if (p.k_out)
+                            p.k_out[first + e] = (int32_t)kk[e];
+                    }
+            }
+        }
+    }
+    if (tile == p.num_tiles - 1 && tid == 0) {
+        const uint64_t total = P + agg;
+        if (p.total_out)
+            *p.total_out = total;
+        if (p.res) {
+            const uint64_t spawned = total < cap ? total : cap;
+            p.res->total = total;
+            p.res->spawned = (uint32_t)spawned;
+            p.res->dropped = total - spawned;
+            p.res->overflow = total > spawned ? 1u : 0u;
+        }
+    }
+#ifdef NRRS_KERNEL_TIMING
+    __syncthreads();
+    stamp(p.dbg, tile, 4);
+#endif
+    if (tid == 0)
+        finish_launch(p.sync, p.tile_state, p.state_cap, epoch);
+}
+
+// Order-preserving compaction of 8-byte records (slot records, surface pairs) by a used mask
+// (wavefront.cpp:488-497), same tile shape as decide3: 16 records and their mask bytes per
+// thread in registers, one prefix per tile, kept records staged per warp and written in order.
+__global__ void __launch_bounds__(kD3T, 1) compact3_kernel(CompactParams p) {
+    __shared__ Scan3Smem sm;
+    __shared__ uint2 cbuf[kD3T / 32 * 128];  // per-warp staging of one item group's kept records
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0)
+        sm.tile = claim_tile_epoch(p.sync, &sm.epoch);
+    __syncthreads();
+    const uint32_t tile = sm.tile, epoch = sm.epoch;
+    stamp(p.dbg, tile, 0);
+    uint64_t count64 = p.count;
+    if (p.count_in) {
+        const uint64_t c = *p.count_in;
+        count64 = c < count64 ? c : count64;
+    }
+    const uint32_t count = min((uint32_t)count64, (tile + 1u) * p.tile_items);
+    const uint32_t wbase = tile * p.tile_items + (uint32_t)warp * kD3Warp + 4u * (uint32_t)lane;
+    const uint2 *in = reinterpret_cast<const uint2 *>(p.in);
+    const bool vec = (reinterpret_cast<uintptr_t>(p.in) & 15u) == 0 && (reinterpret_cast<uintptr_t>(p.used) & 3u) == 0;
+    uint32_t m[4];
+    uint2 rec[16];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t first = wbase + 128u * (uint32_t)i;
+        const uint32_t nvi = first >= count ? 0u : (count - first < 4u ? count - first : 4u);
+        m[i] = 0;
+        if (vec && nvi == 4u) {
+            const uint32_t w4 = __ldcs(reinterpret_cast<const unsigned int *>(p.used + first));
+            const uint4 a = __ldcs(reinterpret_cast<const uint4 *>(in + first));
+            const uint4 b = __ldcs(reinterpret_cast<const uint4 *>(in + first) + 1);
+            rec[4 * i] = make_uint2(a.x, a.y);
+            rec[4 * i + 1] = make_uint2(a.z, a.w);
+            rec[4 * i + 2] = make_uint2(b.x, b.y);
+            rec[4 * i + 3] = make_uint2(b.z, b.w);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                m[i] |= ((w4 >> (8 * e)) & 0xffu) ? (1u << e) : 0u;
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                rec[4 * i + e] = make_uint2(0u, 0u);
+                if ((uint32_t)e < nvi && p.used[first + e]) {
+                    m[i] |= 1u << e;
+                    rec[4 * i + e] = __ldcs(in + first + e);
+                }
+            }
+        }
+    }
+    uint32_t gs[4], excl[4], agg = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        gs[i] = __popc(m[i]);
+    stamp(p.dbg, tile, 1);
+    scan4_positions(gs, sm, excl, agg);
+    stamp(p.dbg, tile, 2);
+    if (warp == 0) {
+        const uint64_t ex = tile_prefix(p.tile_state, tile, agg, epoch, p.single_wave != 0u, p.dbg);
+        if (lane == 0)
+            sm.prefix = ex;
+    }
+    __syncthreads();
+    stamp(p.dbg, tile, 3);
+    // a warp's kept records of one item group (<= 128) are contiguous in the output: stage them
+    // in the warp's buffer and write them as full warp stores
+    uint2 *out = reinterpret_cast<uint2 *>(p.out) + sm.prefix;
+    uint2 *wbuf = cbuf + warp * 128;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t gbase = __shfl_sync(0xffffffffu, excl[i], 0);
+        const uint32_t gtot = __shfl_sync(0xffffffffu, excl[i] + gs[i], 31) - gbase;
+        uint32_t pos = excl[i] - gbase;
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (m[i] & (1u << e))
+                wbuf[pos++] = rec[4 * i + e];
+        __syncwarp();
+        for (uint32_t r = (uint32_t)lane; r < gtot; r += 32u)
+            __stcs(out + gbase + r, wbuf[r]);
+        __syncwarp();
+    }
+    if (tile == p.num_tiles - 1 && tid == 0)
+        *p.count_out = (uint32_t)(sm.prefix + agg);
+#ifdef NRRS_KERNEL_TIMING
+    __syncthreads();
+    stamp(p.dbg, tile, 4);
+#endif
     if (tid == 0)
         finish_launch(p.sync, p.tile_state, p.state_cap, epoch);
 }
@@ -2025,24 +2260,48 @@ cudaError_t launch_infer(int kind, const InferParams &p, int num_sms, cudaStream
 
 uint32_t infer_max_grid(int num_sms) { return (uint32_t)num_sms * 16u; }
 
-uint32_t decide_tiles(uint64_t n) { return (uint32_t)((n + kBTile - 1) / kBTile); }
+// Tile shape of decide3 / compact3: batches up to num_sms full tiles run as one wave with the
+// items spread evenly over the SMs (512-item warp granularity); larger ones use full tiles.
+static void scan_tile_shape(uint64_t n, int num_sms, uint32_t *items, uint32_t *tiles, uint32_t *single) {
+    const uint64_t sms = num_sms < 1 ? 1 : (uint64_t)num_sms;
+    if (n <= sms * (uint64_t)kD3Tile && sms <= 256) {
+        uint64_t per = (n + sms - 1) / sms;
+        per = (per + kD3Warp - 1) / kD3Warp * kD3Warp;
+        if (per == 0)
+            per = kD3Warp;
+        *items = (uint32_t)per;
+        *tiles = (uint32_t)((n + per - 1) / per);
+        *single = 1u;
+    } else {
+        *items = (uint32_t)kD3Tile;
+        *tiles = (uint32_t)((n + kD3Tile - 1) / kD3Tile);
+        *single = 0u;
+    }
+}
 
-cudaError_t launch_decide(int src, const DecideParams &p, cudaStream_t stream) {
-    if (p.num_tiles == 0)
+uint32_t decide_tiles(uint64_t n) {
+    // state entries: full tiles (several waves), or <= 256 padded single-wave tiles
+    const uint64_t full = (n + kD3Tile - 1) / kD3Tile, one_wave = 256u * kStatePad;
+    return (uint32_t)(full > one_wave ? full : one_wave);
+}
+
+cudaError_t launch_decide(int src, DecideParams p, int num_sms, cudaStream_t stream) {
+    if (p.n == 0)
         return cudaSuccess;
-    const size_t smem = sizeof(Decide2Smem);
+    scan_tile_shape(p.n, num_sms, &p.tile_items, &p.num_tiles, &p.single_wave);
+    const int smem = 4 * kD3T * (int)sizeof(uint4) + (kD3T / 32) * kD3Stage * (int)sizeof(uint2);
     cudaError_t e;
     if (src == 0) {
-        e = cudaFuncSetAttribute(decide2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess)
-            return e;
-        decide2_kernel<0><<<p.num_tiles, kBT, smem, stream>>>(p);
+        e = cudaFuncSetAttribute(decide3_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e == cudaSuccess)
+            decide3_kernel<0><<<p.num_tiles, kD3T, smem, stream>>>(p);
     } else {
-        e = cudaFuncSetAttribute(decide2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess)
-            return e;
-        decide2_kernel<1><<<p.num_tiles, kBT, smem, stream>>>(p);
+        e = cudaFuncSetAttribute(decide3_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e == cudaSuccess)
+            decide3_kernel<1><<<p.num_tiles, kD3T, smem, stream>>>(p);
     }
+    if (e != cudaSuccess)
+        return e;
     return cudaGetLastError();
 }
 
@@ -2052,18 +2311,20 @@ static size_t compact2_smem() {
 }
 
 uint32_t compact_tiles(uint64_t count, uint32_t words) {
-    const uint64_t tile = words == 2 ? (uint64_t)kBT * 4 * kBSubs : (uint64_t)kBT * 1 * kBSubs;
+    if (words == 2)
+        return decide_tiles(count);
+    const uint64_t tile = (uint64_t)kBT * 1 * kBSubs;
     return (uint32_t)((count + tile - 1) / tile);
 }
 
-cudaError_t launch_compact(uint32_t words, const CompactParams &p, cudaStream_t stream) {
-    if (p.num_tiles == 0)
+cudaError_t launch_compact(uint32_t words, CompactParams p, int num_sms, cudaStream_t stream) {
+    if (p.count == 0)
         return cudaSuccess;
     if (words == 2) {
-        const size_t smem = compact2_smem<2, 4>();
-        cudaFuncSetAttribute(compact2_kernel<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        compact2_kernel<2, 4><<<p.num_tiles, kBT, smem, stream>>>(p);
+        scan_tile_shape(p.count, num_sms, &p.tile_items, &p.num_tiles, &p.single_wave);
+        compact3_kernel<<<p.num_tiles, kD3T, 0, stream>>>(p);
     } else if (words == 18) {
+        p.num_tiles = compact_tiles(p.count, words);
         const size_t smem = compact2_smem<18, 1>();
         cudaFuncSetAttribute(compact2_kernel<18, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         compact2_kernel<18, 1><<<p.num_tiles, kBT, smem, stream>>>(p);

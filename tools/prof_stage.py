@@ -1,14 +1,16 @@
-"""Minimal driver for ncu captures: runs the stage on a synthetic batch `reps` times.
+"""Minimal driver for ncu captures: runs the stage (K-A, K-B) and the slot compaction (K-C, ~10%
+invalid slots as in bench.py) on a synthetic batch `reps` times.
 usage: python tools/prof_stage.py [aid|nrrs|adrrs|throughput] [n] [reps]"""
-import sys
+import ctypes as C
 import os
+import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 
 from paper_2510_07868_b200 import (NeuralRrs, NeuralRrsConfig, RateControl, RrsStage, RrsVariant, Strategy,
-                                   StrategyKind, synthetic)
+                                   StrategyKind, _capi, synthetic)
 
 kind = sys.argv[1] if len(sys.argv) > 1 else "aid"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 1920 * 1080
@@ -22,16 +24,31 @@ dv = {k: torch.from_numpy(a.view(np.int64) if a.dtype == np.uint64 else a).cuda(
       if k != "pixel"}
 st = RrsStage(n, nets)
 out = st.alloc_outputs(n)
+cap = st.capacity
+idx = torch.arange(cap, dtype=torch.int64, device="cuda")
+used = (((idx * 2654435761) >> 7) % 10 != 0).to(torch.uint8)
+compacted = torch.empty((cap, 2), dtype=torch.int32, device="cuda")
+d_count = torch.zeros(1, dtype=torch.int32, device="cuda")
+lib = _capi.lib()
+
+
+def step():
+    res = st.run(dv, 2, Strategy(strat), rc=RateControl(), out=out, sync=False)
+    _capi.check(st.handle, lib.nrrs_gpu_compact(st.handle, out.slots.data_ptr(), used.data_ptr(), cap, 2,
+                                                compacted.data_ptr(), d_count.data_ptr(), None))
+    return res
+
+
 for _ in range(reps):
-    st.run(dv, 2, Strategy(strat), rc=RateControl(), out=out, sync=False)
+    step()
 torch.cuda.synchronize()
 times = []
 for _ in range(max(reps, 1)):
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    st.run(dv, 2, Strategy(strat), rc=RateControl(), out=out, sync=False)
+    step()
     b.record()
     torch.cuda.synchronize()
     times.append(a.elapsed_time(b))
 times.sort()
-print(f"{kind} n={n}: stage {times[len(times) // 2]:.3f} ms (median of {len(times)}, min {times[0]:.3f})")
+print(f"{kind} n={n}: stage+compact {times[len(times) // 2]:.3f} ms (median of {len(times)}, min {times[0]:.3f})")
