@@ -20,6 +20,7 @@ host threads, bounded samples.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -47,6 +48,16 @@ GATHER_CEILING_PER_S = 296e9
 SMEM_LOADS_PER_VERTEX = 64
 SMEM_LOAD_CEILING_PER_S = 2484.46e9
 STAGE_READ, STAGE_WRITE = 56, 8  # SURVEY.md 8d per-vertex compulsory bytes (+ 8 B per spawned slot record)
+
+
+class _DevPtr:
+    """A raw device address with the data_ptr() accessor the ABI wrappers use."""
+
+    def __init__(self, addr: int):
+        self.addr = addr
+
+    def data_ptr(self) -> int:
+        return self.addr
 
 
 def parse():
@@ -254,9 +265,10 @@ def main():
         sh = None
         stage = RrsStage(npx, nets, device=local)
     stage.reserve(n)
-    out = stage.alloc_outputs(n)
-    out.q_orig = torch.empty(n, dtype=torch.float32, device=dev)
-    out.u = torch.empty(n, dtype=torch.float32, device=dev)
+    _tp = ctypes.c_void_p()
+    _capi.check(stage.handle, _capi.lib().nrrs_gpu_stage_total_dev(stage.handle, ctypes.byref(_tp)))
+    total_dev = _DevPtr(_tp.value)  # the stage's device-side realized total (compaction bound)
+    out = stage.alloc_outputs(n)  # q_norm, q_real, slots (q_orig / u stay context scratch)
     slot_cap = stage.capacity
     slot_idx = torch.arange(slot_cap, dtype=torch.int64, device=dev)
     # synthetic BSDF validity per slot (~10% invalid samples), fixed hash of the slot index
@@ -283,8 +295,9 @@ def main():
         from paper_2510_07868_b200.stage import vertex_soa
         soa = vertex_soa(dv)
         oc = out.c()
-        _capi.check(stage.handle, lib.nrrs_gpu_stage_factors(stage.handle, C.byref(soa), n, C.byref(p),
-                                                             C.byref(oc), local_sum.data_ptr()))
+        if not (sh is None and len(ev) == 2):
+            _capi.check(stage.handle, lib.nrrs_gpu_stage_factors(stage.handle, C.byref(soa), n, C.byref(p),
+                                                                 C.byref(oc), local_sum.data_ptr()))
         if len(ev) == 4:
             ev[1].record(stream)
         def compact(count_src):
@@ -293,7 +306,12 @@ def main():
             _capi.check(stage.handle, lib.nrrs_gpu_compact_dev(stage.handle, out.slots.data_ptr(), used.data_ptr(),
                                                                count_src.data_ptr(), slot_cap, 2, compacted.data_ptr(),
                                                                d_count.data_ptr()))
-        if sh is None:
+        if sh is None and len(ev) == 2:
+            # the drop-in call (nrrs_gpu_rrs_stage, asynchronous), then the compaction of its slot records
+            _capi.check(stage.handle, lib.nrrs_gpu_rrs_stage(stage.handle, C.byref(soa), n, C.byref(p), C.byref(oc),
+                                                             None))
+            compact(total_dev)
+        elif sh is None:
             _capi.check(stage.handle, lib.nrrs_gpu_stage_decide(stage.handle, n, C.byref(p), local_sum.data_ptr(), 1,
                                                                 C.byref(oc), local_total.data_ptr()))
             compact(local_total)
@@ -367,7 +385,11 @@ def main():
     if sh is not None and pending[0] is not None:
         po = pending[0].resolve(rc)  # the last timed depth's global outcome (host read after the loop)
         assert po.dropped == 0 or po.spawned == cap
-    spawned = int(min(int(local_total.item()), cap)) if sh is None else int(sh._total.item())
+    if sh is None:
+        _capi.check(stage.handle, lib.nrrs_gpu_fetch_result(stage.handle, ctypes.byref(res)))
+        spawned = int(res.spawned)
+    else:
+        spawned = int(sh._total.item())
 
     # ---- e2e: the C ABI host-buffer entry (H2D + stage + D2H every step) ----
     e2e = None

@@ -238,6 +238,13 @@ NRRS_API int nrrs_gpu_rrs_stage(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *d_v, u
  * with h_result = NULL; the stage launches are graph-replay safe). */
 NRRS_API int nrrs_gpu_fetch_result(nrrs_gpu_ctx *ctx, nrrs_stage_result *h_result);
 
+/* Device address of the u64 realized child total (the reference's plan_spawns
+ * `total` before the capacity clip, wavefront.cpp:141-154) that every
+ * nrrs_gpu_rrs_stage call writes, so a stream-ordered consumer such as
+ * nrrs_gpu_compact_dev (bounded by the capacity) can follow the stage without a
+ * host round trip.  Stable for the context's lifetime. */
+NRRS_API int nrrs_gpu_stage_total_dev(nrrs_gpu_ctx *ctx, const uint64_t **d_total);
+
 /* Per-frame ADRRS divisor input, replaces the film loop of trace_frame
  * (wavefront.cpp:238-243): *d_sum_out = sum over n_pixels of luminance(i_acc[p])
  * (f32 luminance, f64 sum, fixed order).  eps_div = eps_scale *

@@ -9,8 +9,8 @@ import subprocess
 PKG = pathlib.Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libnrrs_gpu.so"
-SOURCES = ["nrrs_kernels.cu", "nrrs_film.cu", "nrrs_train.cu", "nrrs_render.cu", "nrrs_capi.cu"]
-HEADERS = ["nrrs_device.cuh", "nrrs_internal.h", "../../include/nrrs_gpu.h"]
+SOURCES = ["nrrs_kernels.cu", "nrrs_fused.cu", "nrrs_film.cu", "nrrs_train.cu", "nrrs_render.cu", "nrrs_capi.cu"]
+HEADERS = ["nrrs_device.cuh", "nrrs_ka.cuh", "nrrs_internal.h", "../../include/nrrs_gpu.h"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

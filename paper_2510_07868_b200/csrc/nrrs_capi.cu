@@ -163,6 +163,7 @@ struct nrrs_gpu_ctx {
     // tuning / test switches, read once at nrrs_gpu_create (never on the per-call path)
     bool env_no_level_kernel = false;  // NRRS_NO_LEVEL_KERNEL: AID through the fused-gather K-A
     bool env_fp32_tables = false;      // NRRS_FP32_TABLES: keep the AID grid in fp32
+    bool env_fused = false;            // NRRS_FUSED: AID through the fused single-kernel stage (nrrs_fused.cu)
     int env_sync_chunks = 0;           // NRRS_SYNC_CHUNKS / NRRS_ASYNC_CHUNKS: host-path H2D pieces (0: default)
     int env_async_chunks = 0;
 
@@ -183,6 +184,11 @@ struct nrrs_gpu_ctx {
     uint64_t cap_parts = 0;
     float2 *d_feat = nullptr;  // K-A0 level planes (AID, fp16 tables): levels x n float2
     uint64_t cap_feat = 0;
+    // fused AID stage (nrrs_fused.cu): level-plane ring, grid-barrier / ring counters, prefix words
+    float2 *d_ring = nullptr;
+    uint64_t cap_ring = 0;
+    uint32_t *d_fsync = nullptr;
+    uint64_t *d_fstate = nullptr;
     uint32_t *d_part_counts = nullptr;
     uint64_t cap_part_counts = 0;
     uint64_t *d_tile_state = nullptr;
@@ -315,6 +321,7 @@ int nrrs_gpu_create(int device, nrrs_gpu_ctx **out) {
     cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
     ctx->env_no_level_kernel = std::getenv("NRRS_NO_LEVEL_KERNEL") != nullptr;
     ctx->env_fp32_tables = std::getenv("NRRS_FP32_TABLES") != nullptr;
+    ctx->env_fused = std::getenv("NRRS_FUSED") != nullptr;
     if (const char *sc = std::getenv("NRRS_SYNC_CHUNKS"))
         ctx->env_sync_chunks = std::max(1, std::min(std::atoi(sc), kMaxHostChunks));
     if (const char *mc = std::getenv("NRRS_ASYNC_CHUNKS"))
@@ -342,7 +349,7 @@ int nrrs_gpu_destroy(nrrs_gpu_ctx *ctx) {
     cudaStreamSynchronize(ctx->stream);
     void *ptrs[] = {ctx->d_stat_grid, ctx->d_rrs_grid, ctx->blob_stat.ptr, ctx->blob_rrs.ptr, ctx->blob_both.ptr,
                     ctx->d_q, ctx->d_u, ctx->d_parts, ctx->d_part_counts, ctx->d_tile_state, ctx->d_ctile_state,
-                    ctx->d_misc, ctx->d_res, ctx->d_sum, ctx->d_total, ctx->d_sync, ctx->d_etile_state, ctx->d_hist, ctx->d_tws, ctx->d_tloss, ctx->d_tpart, ctx->d_feat, ctx->st.p01, ctx->st.wo01, ctx->st.rough,
+                    ctx->d_misc, ctx->d_res, ctx->d_sum, ctx->d_total, ctx->d_sync, ctx->d_etile_state, ctx->d_hist, ctx->d_tws, ctx->d_tloss, ctx->d_tpart, ctx->d_feat, ctx->d_ring, ctx->d_fsync, ctx->d_fstate, ctx->st.p01, ctx->st.wo01, ctx->st.rough,
                     ctx->st.weight, ctx->st.ipix, ctx->st.key, ctx->st.q_norm, ctx->st.q_real, ctx->st.q_orig,
                     ctx->st.u, ctx->st.k, ctx->st.offset, ctx->st.slots, ctx->st.decided};
     for (void *p : ptrs)
@@ -761,11 +768,12 @@ static void phase_dump(nrrs_gpu_ctx *ctx, const char *what, unsigned long long *
         if (h[8 * t] && h[8 * t] < t0)
             t0 = h[8 * t];
     std::fprintf(stderr, "[nrrs phases] %s tiles %u (us after first start: min / median / max)\n", what, tiles);
-    for (int k = 0; k < 7; ++k) {
+    const bool polls = std::strncmp(what, "aid_stage", 9) != 0;  // K-B / K-C stamp 6 counts polls
+    for (int k = 0; k < 8; ++k) {
         std::vector<double> v;
         for (uint32_t t = 0; t < tiles; ++t)
             if (h[8 * t + k])
-                v.push_back(k == 6 ? (double)h[8 * t + k] : (double)(h[8 * t + k] - t0) / 1e3);
+                v.push_back(k == 6 && polls ? (double)h[8 * t + k] : (double)(h[8 * t + k] - t0) / 1e3);
         if (v.empty())
             continue;
         std::sort(v.begin(), v.end());
@@ -808,6 +816,101 @@ static int run_decide(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_stage_params *p,
 #ifdef NRRS_KERNEL_TIMING
     phase_dump(ctx, "decide3", dp.dbg, dp.num_tiles);
 #endif
+    ctx->launches += 1;
+    return NRRS_OK;
+}
+
+// The AID stage as one fused kernel (nrrs_fused.cu), opt-in (NRRS_FUSED): AID kind with fp16 tables
+// that fit in shared memory, enough tiles for one producer CTA per level.  Measured slower than
+// K-A0 + K-A + K-B on B200 (both halves are issue-bound, so sharing the SMs
+// adds their instruction streams), hence not the default.  Returns 1 (not applicable:
+// the caller runs K-A0 + K-A + K-B), 0 (launched) or an error status.
+static int run_fused_stage(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, const nrrs_stage_params *p,
+                           const nrrs_stage_out *o, uint32_t cap) {
+    if (!ctx->env_fused || ctx->env_no_level_kernel)
+        return 1;
+    int kind = 0, heur = 0;
+    int rc = select_kind(ctx, p->depth, p->strategy, &kind, &heur);
+    if (rc)
+        return rc;
+    if (kind != kKindAid || !ctx->rrs_half || (uint64_t)ctx->grid_rrs.table_size * 4u > kLevelSmemMax)
+        return 1;
+    if (!std::isfinite(p->gain) || p->gain < 0.0f)
+        return fail(ctx, NRRS_EINVAL, "stage: gain must be finite and >= 0 (got %g)", (double)p->gain);
+    rc = check_soa(ctx, v, kind);
+    if (rc)
+        return rc;
+    uint32_t ctas = 0, tpc = 0, rounds = 0, park = 0;
+    if (!aid_stage_shape(n, ctx->num_sms, (uint32_t)ctx->grid_rrs.levels, &ctas, &tpc, &rounds, &park))
+        return 1;
+    const size_t smem = aid_stage_smem_bytes(ctx->blob_rrs.bytes, ctx->grid_rrs.table_size);
+    if (smem > 227u * 1024u)
+        return 1;
+    const uint64_t ring = aid_stage_ring_floats2((uint32_t)ctx->grid_rrs.levels, ctas);
+    CK(ctx, grow(ctx->d_ring, ctx->cap_ring, ring));
+    if (!ctx->d_fsync) {
+        CK(ctx, cudaMalloc(&ctx->d_fsync, aid_stage_sync_words() * sizeof(uint32_t)));
+        CK(ctx, cudaMemsetAsync(ctx->d_fsync, 0, aid_stage_sync_words() * sizeof(uint32_t), ctx->stream));
+        CK(ctx, cudaMalloc(&ctx->d_fstate, 256 * 16 * sizeof(uint64_t)));
+        CK(ctx, cudaMemsetAsync(ctx->d_fstate, 0, 256 * 16 * sizeof(uint64_t), ctx->stream));
+    }
+    AidStageParams fp{};
+    InferParams &ip = fp.f;
+    ip.p01 = v->p01;
+    ip.wo01 = v->wo01;
+    ip.roughness = v->roughness;
+    ip.weight = v->weight;
+    ip.i_pixel = v->i_pixel;
+    ip.path_key = v->path_key;
+    ip.pixel = v->pixel;
+    ip.i_acc = v->i_acc;
+    ip.n = n;
+    ip.depth = p->depth;
+    ip.gate = 1;
+    ip.eps = p->eps_div < 1e-8f ? 1e-8f : p->eps_div;
+    ip.mixed_seed = h_mix_bits(p->seed);
+    fill_infer_common(ctx, kind, ip);
+    // q_orig / u only when the caller asked for them, or as scratch when TMEM cannot park them
+    ip.q_out = o->q_orig ? o->q_orig : (park ? nullptr : ctx->d_q);
+    ip.u_out = o->u ? o->u : (park ? nullptr : ctx->d_u);
+    ip.decided_out = o->decided;
+    ip.parts = ctx->d_parts;
+    ip.part_counts = ctx->d_part_counts;
+    ip.sum_out = ctx->d_sum;
+    ip.res = ctx->d_res;
+    auto al16 = [](const void *q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
+    ip.in_bulk = (al16(v->weight) && al16(v->wo01) && al16(v->roughness) && al16(v->path_key) &&
+                  (v->i_pixel ? al16(v->i_pixel) : (v->pixel != nullptr && al16(v->pixel))))
+                     ? 1u
+                     : 0u;
+    const bool adaptive = p->strategy.kind != NRRS_FIXED;
+    fp.ring = ctx->d_ring;
+    fp.sync = ctx->d_fsync;
+    fp.state = ctx->d_fstate;
+    fp.n_pixels = p->n_pixels;
+    fp.gain = (p->depth >= 2 && adaptive) ? p->gain : 1.0f;  // wavefront.cpp:391
+    fp.capacity = cap;
+    fp.q_norm = o->q_norm;
+    fp.q_real = o->q_real;
+    fp.k_out = o->k;
+    fp.offset = o->offset;
+    fp.slots = o->slots;
+    fp.total_out = ctx->d_total;
+    fp.tpc = tpc;
+    fp.rounds = rounds;
+    fp.park_tmem = park;
+#ifdef NRRS_KERNEL_TIMING
+    fp.dbg = phase_dbg(ctx);
+#endif
+    const cudaError_t e = launch_aid_stage(fp, ctas, ctx->stream);
+#ifdef NRRS_KERNEL_TIMING
+    phase_dump(ctx, "aid_stage (0 start, 1 producers, 2 loader, 3 MLP, 4 barrier, 5 end)", fp.dbg, ctas);
+#endif
+    if (e == cudaErrorCooperativeLaunchTooLarge) {
+        (void)cudaGetLastError();
+        return 1;  // the CTAs cannot all be resident (shared device): the three-kernel path
+    }
+    CK(ctx, e);
     ctx->launches += 1;
     return NRRS_OK;
 }
@@ -873,12 +976,21 @@ int nrrs_gpu_rrs_stage(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, 
         DevResult r{};
         r.f_norm = 1.0;  // all-zero (empty) input passes through with F = 1 (rrs.cpp:15-16)
         CK(ctx, cudaMemcpyAsync(ctx->d_res, &r, sizeof r, cudaMemcpyHostToDevice, ctx->stream));
+        CK(ctx, cudaMemsetAsync(ctx->d_total, 0, sizeof(unsigned long long), ctx->stream));
         if (h_result)
             return fetch_result(ctx, h_result);
         return NRRS_OK;
     }
     rc = ensure_scratch(ctx, n);
     if (rc)
+        return rc;
+    rc = run_fused_stage(ctx, v, n, p, o, cap);
+    if (rc == NRRS_OK) {
+        if (h_result)
+            return fetch_result(ctx, h_result);
+        return NRRS_OK;
+    }
+    if (rc != 1)
         return rc;
     float *q = o->q_orig ? o->q_orig : ctx->d_q;
     float *u = o->u ? o->u : ctx->d_u;
@@ -1782,6 +1894,13 @@ int nrrs_gpu_tracer_vertices(const nrrs_tracer *t, int32_t depth, nrrs_vertex_re
     out->decided = v.decided;
     out->s = v.s;
     *count = t->nverts[(size_t)depth];
+    return NRRS_OK;
+}
+
+int nrrs_gpu_stage_total_dev(nrrs_gpu_ctx *ctx, const uint64_t **d_total) {
+    if (!ctx || !d_total)
+        return NRRS_EINVAL;
+    *d_total = reinterpret_cast<const uint64_t *>(ctx->d_total);
     return NRRS_OK;
 }
 

@@ -125,6 +125,26 @@ struct InferParams {
     unsigned long long *dbg;  // debug only (env NRRS_DEBUG_TIMING): per-CTA clock64 phase counters [grid][16]
 };
 
+// The fused AID-NRRS stage (nrrs_fused.cu): factor inputs + decision outputs.
+struct AidStageParams {
+    InferParams f;         // inputs, nets, grid, gate, seed; f.q_out / f.u_out: q_orig / u (optional when
+                           // park_tmem), f.decided_out optional; f.parts / part_counts / sum_out / res used
+    float2 *ring;          // level-plane ring [3][levels][ctas][4 * 128]
+    uint32_t *sync;        // grid barrier + ring counters (aid_stage_sync_words, zeroed once)
+    uint64_t *state;       // per-CTA prefix words [ctas * kStatePad]
+    uint64_t n_pixels;
+    float gain;
+    uint32_t capacity;
+    uint32_t parent_base;
+    float *q_norm, *q_real;
+    int32_t *k_out;
+    uint32_t *offset;
+    uint32_t *slots;
+    unsigned long long *total_out;
+    uint32_t tpc, rounds, park_tmem;
+    unsigned long long *dbg;  // NRRS_KERNEL_TIMING builds only: per-CTA %globaltimer role stamps [cta][8]
+};
+
 struct DecideParams {
     const float *q, *u;
     const int32_t *counts_in;
@@ -349,6 +369,13 @@ uint32_t decide_tiles(uint64_t n);
 cudaError_t launch_decide(int src, DecideParams p, int num_sms, cudaStream_t stream);
 uint32_t compact_tiles(uint64_t count, uint32_t words);
 cudaError_t launch_compact(uint32_t words, CompactParams p, int num_sms, cudaStream_t stream);
+// fused AID stage (nrrs_fused.cu)
+size_t aid_stage_smem_bytes(uint32_t blob_bytes, uint32_t table_size);
+uint32_t aid_stage_ring_floats2(uint32_t levels, uint32_t ctas);
+uint32_t aid_stage_sync_words();
+bool aid_stage_shape(uint64_t n, int num_sms, uint32_t levels, uint32_t *ctas, uint32_t *tpc, uint32_t *rounds,
+                     uint32_t *park);
+cudaError_t launch_aid_stage(const AidStageParams &p, uint32_t ctas, cudaStream_t stream);
 cudaError_t launch_lum_sum(const float *i_acc, uint64_t n, double *parts, uint32_t *counter, double *sum_out,
                            uint32_t grid, cudaStream_t stream);
 cudaError_t launch_sum_check(const float *q, uint64_t n, double *parts, uint32_t *counter, uint32_t *err,

@@ -15,8 +15,11 @@
 // networks.cpp:131-281, hashgrid.cpp:38-82, mlp.cpp:52-72, rrs.cpp:8-45.
 #include "nrrs_device.cuh"
 #include "nrrs_internal.h"
+#include "nrrs_ka.cuh"
 
 #include <cuda_runtime.h>
+
+#include <cstdlib>
 
 namespace nrrs {
 
@@ -27,7 +30,6 @@ namespace nrrs {
 // streaming kernel, one thread per vertex.  The neural kinds run the
 // warp-specialized tcgen05 pipeline further down (namespace ws).
 // ===========================================================================
-constexpr int kTileM = 128;           // vertices per MMA tile (UMMA M)
 constexpr int kInferThreads = 256;    // heuristic kernel block
 
 struct InferSmemHeader {
@@ -36,16 +38,6 @@ struct InferSmemHeader {
     uint32_t warp_cnt[8];
     uint32_t warp_bc[8];
 };
-
-// fp32 -> fp16 hi/lo split of two values with packed conversions
-// (x = hi + lo to ~22 bits).
-__device__ __forceinline__ void split2(float v0, float v1, uint32_t &h, uint32_t &l) {
-    const __half2 hh = __float22half2_rn(make_float2(v0, v1));
-    const float2 b = __half22float2(hh);
-    const __half2 ll = __float22half2_rn(upk2(fsub2(pk2(v0, v1), pk2(b.x, b.y))));
-    h = *reinterpret_cast<const uint32_t *>(&hh);
-    l = *reinterpret_cast<const uint32_t *>(&ll);
-}
 
 // Position of entry e in the copy that pairs (e, e ^ (2^(t+1)-1)) into one
 // aligned 16-byte pair (t = 0: the reference layout).  Mirrors pair_pos in
@@ -152,26 +144,6 @@ __device__ __forceinline__ void grid_encode4(const void *theta, const GridDev &g
     }
 }
 
-// one_blob_encode (encodings.hpp:31-44), tolerance path: exp(-d^2 / (2 sigma^2)) as one
-// flush-to-zero ex2 per bin with log2(e) folded into the constant, approximate reciprocal.
-template <int BINS>
-__device__ __forceinline__ void one_blob_fast(float x, float *out) {
-    constexpr float k = -(float)(BINS * BINS) * 0.5f * 1.4426950408889634f;
-    float sum = 0.0f;
-#pragma unroll
-    for (int i = 0; i < BINS; ++i) {
-        const float d = x - ((float)i + 0.5f) / (float)BINS;
-        out[i] = ex2_ftz(d * d * k);
-        sum += out[i];
-    }
-    const float inv = rcp_ftz(sum);
-#pragma unroll
-    for (int i = 0; i < BINS; ++i)
-        out[i] *= inv;
-}
-
-__device__ __forceinline__ float remap_fast(float a) { return 1.0f - ex2_ftz(a * -1.4426950408889634f); }
-
 // ===========================================================================
 // K-A0: level-sliced hash-grid encode (fp16 tables that fit in shared memory).
 //
@@ -191,62 +163,6 @@ constexpr int kLevelThreads = 1024;
 #endif
 constexpr uint32_t kLevelPer = NRRS_LEVEL_PER_THREAD;             // vertices per thread per block
 constexpr uint32_t kLevelBlock = kLevelPer * kLevelThreads;  // staged p01 block (12 B per vertex), double-buffered
-
-// Per-level constants of K-A0 (uniform over the CTA).
-struct LevelConsts {
-    uint32_t res, nn, m4;  // resolution, res + 1, (T - 1) * 4
-    float resf;
-    bool dense;
-    uint32_t doff4[8];     // dense corner offsets * 4
-};
-
-// One level of HashGrid::encode for one point from the shared-memory table
-// (hashgrid.cpp:38-82): cell and weights per axis, 8 corner entries (byte offsets
-// idx * 4: the hash is computed on pre-scaled terms, ((a ^ b) & m) * 4 =
-// (4a ^ 4b) & 4m), weights w = wx * (wy * wz) as x-pairs, (f0, f1) accumulated as
-// one fp32x2 FMA per corner.
-__device__ __forceinline__ float2 level_encode(const uint8_t *tab, const LevelConsts &c, float px, float py,
-                                               float pz) {
-    const float fx = __saturatef(px) * c.resf, fy = __saturatef(py) * c.resf, fz = __saturatef(pz) * c.resf;
-    const uint32_t cx = min((uint32_t)fx, c.res - 1u);
-    const uint32_t cy = min((uint32_t)fy, c.res - 1u);
-    const uint32_t cz = min((uint32_t)fz, c.res - 1u);
-    const float tx = fx - (float)cx, ty = fy - (float)cy, tz = fz - (float)cz;
-    const uint64_t wxp = pk2(1.0f - tx, tx);
-    const float wy[2] = {1.0f - ty, ty}, wz[2] = {1.0f - tz, tz};
-    uint32_t idx4[8];
-    if (c.dense) {
-        const uint32_t b4 = ((cx * c.nn + cy) * c.nn + cz) * 4u;
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-            idx4[k] = b4 + c.doff4[k];
-    } else {
-        const uint32_t hx0 = cx * 4u, hx1 = hx0 + 4u;
-        const uint32_t hy0 = cy * (2654435761u * 4u), hy1 = hy0 + 2654435761u * 4u;
-        const uint32_t hz0 = cz * (805459861u * 4u), hz1 = hz0 + 805459861u * 4u;
-        const uint32_t hyz[4] = {hy0 ^ hz0, hy1 ^ hz0, hy0 ^ hz1, hy1 ^ hz1};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            idx4[2 * q] = (hx0 ^ hyz[q]) & c.m4;
-            idx4[2 * q + 1] = (hx1 ^ hyz[q]) & c.m4;
-        }
-    }
-    uint32_t raw[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-        raw[k] = *reinterpret_cast<const uint32_t *>(tab + idx4[k]);
-    uint64_t acc[2] = {pk2(0.0f, 0.0f), pk2(0.0f, 0.0f)};  // oz = 0 / 1 (two short FMA chains)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {  // corners (0, oy, oz), (1, oy, oz); q = oy + 2 oz
-        const float2 w = upk2(fmul2(wxp, pk2(wy[q & 1] * wz[q >> 1], wy[q & 1] * wz[q >> 1])));
-        const float2 v0 = __half22float2(*reinterpret_cast<const __half2 *>(&raw[2 * q]));
-        const float2 v1 = __half22float2(*reinterpret_cast<const __half2 *>(&raw[2 * q + 1]));
-        acc[q >> 1] = ffma2(pk2(w.x, w.x), pk2(v0.x, v0.y), acc[q >> 1]);
-        acc[q >> 1] = ffma2(pk2(w.y, w.y), pk2(v1.x, v1.y), acc[q >> 1]);
-    }
-    const float2 a = upk2(acc[0]), b = upk2(acc[1]);
-    return make_float2(a.x + b.x, a.y + b.y);
-}
 
 __global__ void __launch_bounds__(kLevelThreads, 1) grid_level_kernel(GridLevelParams p) {
     extern __shared__ __align__(128) uint8_t lvl_smem[];
@@ -500,127 +416,6 @@ __global__ void __launch_bounds__(kInferThreads) infer_kernel(InferParams p) {
 //  group g owns i = g (mod GM), slot s = i mod S.  Gathers of tile i+1.. run
 //  while MLP groups chain tiles i, i-1.
 // ===========================================================================
-namespace ws {
-
-struct Side {        // 32 B per tile row
-    uint64_t key;
-    uint32_t flags;  // bit0 valid, bit1 active
-    float ex[5];     // NRRS: bc(t_x)x3, bc(mean I), remap(r); ADRRS: w x3, lum(I)
-};
-
-// TMEM (512 columns, 1 CTA / SM): one 64-column fp32 accumulator per MLP chain,
-// [64c, 64c + 64): columns [0, N) collect A_hi*W_hi + A_lo*W_hi and [N, 2N)
-// collect A_hi*W_lo (one N = 2N instruction covers both weight halves); then a
-// ring of tile slots [kColSlots + 32s, +32) holding the layer-0 input
-// (hi 16 | lo 16 packed fp16x2 columns), reused as the hidden-layer A.
-// NRRS_MMA3 = 1: three N-wide MMAs per K16 slice accumulate A_hi*W_hi + A_lo*W_hi +
-// A_hi*W_lo into ONE 32-column accumulator (same tensor work as the N = 2N form; the
-// epilogue reads half the TMEM columns and skips the hi + lo add).
-#ifndef NRRS_MMA_WAIT_HINT
-#define NRRS_MMA_WAIT_HINT 0  // ns suspend hint of the MLP groups' MMA-completion wait (0: plain try_wait loop)
-#endif
-#ifndef NRRS_MMA3
-#define NRRS_MMA3 1
-#endif
-constexpr bool kMma3 = NRRS_MMA3 != 0;
-constexpr uint32_t kDCols = kMma3 ? 32u : 64u;
-
-template <int GE, int GM, int P, int TPR>
-struct Cfg {
-    static constexpr int kGroupThreads = 128 * TPR;  // MLP threads per group (TPR threads per tile row)
-    static constexpr int kEncThreads = GE * 256;
-    static constexpr int kMlpThreads = GM * kGroupThreads;
-    static constexpr int kThreads = kEncThreads + kMlpThreads;
-    static constexpr int kChains = GM * P;
-    static constexpr uint32_t kColD = 0;
-    static constexpr uint32_t kColSlots = kDCols * kChains;
-    static constexpr int kSlotsRaw = (512 - (int)kColSlots) / 32;
-    static constexpr int kSlots = kSlotsRaw > 16 ? 16 : kSlotsRaw;
-    static_assert(kSlots >= GE + kChains, "TMEM slot ring too small");
-};
-
-struct SmemTail {
-    uint64_t full[16];
-    uint64_t empty[16];
-    uint64_t mma_bar[8];
-    uint64_t wdesc[2][4][2];   // UMMA smem descriptor of [W_hi ; W_lo] per K16 slice (W_hi alone = first N rows)
-    uint64_t wdesc_lo[2][4][2];  // W_lo alone (rows N .. 2N)
-    uint32_t idesc_n[2][4];    // N = layer width
-    uint32_t idesc_2n[2][4];   // N = 2 x layer width (both weight halves)
-    uint32_t nslices[2][4];
-    uint32_t bias[2][4];       // smem byte offset of the fp32 bias, or kNoBias (folded into W)
-    uint32_t tmem_base;
-    uint32_t is_last;
-    double red_sum[32];
-    uint32_t red_nf[32];
-    uint32_t red_bc[32];
-};
-
-// Elected issue of one layer, 2 MMAs per K16 slice, commit to the chain's mbarrier:
-//   D[:, 0:2N]  (+)= A_hi x [W_hi | W_lo]    (N = 2N: hi*W_hi and hi*W_lo side by side)
-//   D[:, 0:N]    += A_lo x W_hi
-// The epilogue adds the two column halves (3-term split).
-// Caller has synchronized the group.
-__device__ __forceinline__ void ws_issue(const SmemTail *st, int net, int layer, uint32_t tmem_base,
-                                         uint32_t col_a, uint32_t col_d, uint64_t *bar) {
-    tc_fence_after();
-    const uint32_t i2 = st->idesc_2n[net][layer], i1 = st->idesc_n[net][layer];
-    const uint32_t ns = st->nslices[net][layer];
-    const uint32_t d = tmem_base + col_d;
-#pragma unroll
-    for (uint32_t k = 0; k < 2; ++k) {
-        if (k >= ns)
-            break;
-        const uint64_t w = st->wdesc[net][layer][k];
-        const uint32_t ah = tmem_base + col_a + 8u * k, al = ah + 16u;
-        if (kMma3) {
-            mma_f16_ts(d, ah, w, i1, k > 0 ? 1u : 0u);
-            mma_f16_ts(d, al, w, i1, 1u);
-            mma_f16_ts(d, ah, st->wdesc_lo[net][layer][k], i1, 1u);
-        } else {
-            mma_f16_ts(d, ah, w, i2, k > 0 ? 1u : 0u);
-            mma_f16_ts(d, al, w, i1, 1u);
-        }
-    }
-    mma_commit(bar);
-}
-
-// 16 fp32 values (K columns [16h, 16h + 16) of the next A) -> 8 hi + 8 lo packed
-// fp16x2 TMEM columns of this thread's lane.
-__device__ __forceinline__ void ws_store_a16(uint32_t lane_base, uint32_t col_a, int h, const float (&x)[16]) {
-    uint32_t hw[8], lw[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e)
-        split2(x[2 * e], x[2 * e + 1], hw[e], lw[e]);
-    tmem_st8(lane_base + col_a + 8u * (uint32_t)h, hw);
-    tmem_st8(lane_base + col_a + 16u + 8u * (uint32_t)h, lw);
-}
-
-// 16 accumulator columns [c0, c0 + 16) of this lane: D_hi + D_lo (+ bias), fp32
-// (element order of the scalar form; the adds run as fp32x2 pairs).
-__device__ __forceinline__ void ws_load_sum16(uint32_t lane_base, uint32_t col_d, uint32_t n, uint32_t c0,
-                                              const float *bias, float (&z)[16]) {
-    float lo[16];
-    if (kMma3)
-        tmem_ld16(lane_base + col_d + c0, z);
-    else
-        tmem_ld16x2(lane_base + col_d + c0, lane_base + col_d + n + c0, z, lo);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        uint64_t v = pk2(z[2 * i], z[2 * i + 1]);
-        if (!kMma3)
-            v = fadd2(v, pk2(lo[2 * i], lo[2 * i + 1]));
-        if (bias) {  // 16-byte bias loads (the blob keeps every bias 64-byte aligned)
-            const float4 b4 = reinterpret_cast<const float4 *>(bias + c0)[i >> 1];
-            v = fadd2(v, (i & 1) ? pk2(b4.z, b4.w) : pk2(b4.x, b4.y));
-        }
-        const float2 f = upk2(v);
-        z[2 * i] = f.x;
-        z[2 * i + 1] = f.y;
-    }
-}
-
-}  // namespace ws
 
 // Per-phase cycle counters and the CTA-0 tile timeline (NRRS_DEBUG_TIMING on the
 // host) exist only in builds with -DNRRS_KERNEL_TIMING: they cost registers.
@@ -1091,21 +886,6 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
 // tcgen05 chain and the head -- so GM chains are in flight per SM instead of one per MLP
 // group behind shared encoder groups.  TMEM: per group 32 accumulator + 32 A columns.
 // ===========================================================================
-// Per-group input slot of infer_aid_fused_kernel (one 128-row tile, field-major so each
-// thread's row reads are bank-conflict free): 8 level planes (float2), weight (3 f32),
-// wo01 (2 f32), i_pixel (3 f32; or the u32 pixel index), roughness, path_key.
-constexpr uint32_t kAidInPlane = 8u * kTileM;
-constexpr uint32_t kAidInWeight = 8u * kAidInPlane;
-constexpr uint32_t kAidInWo = kAidInWeight + 12u * kTileM;
-constexpr uint32_t kAidInIpx = kAidInWo + 8u * kTileM;
-constexpr uint32_t kAidInRough = kAidInIpx + 12u * kTileM;
-constexpr uint32_t kAidInKey = kAidInRough + 4u * kTileM;
-constexpr uint32_t kAidInBytes = kAidInKey + 8u * kTileM;
-static_assert(kAidInBytes % 128u == 0, "slot alignment");
-__host__ __device__ constexpr uint32_t aid_in_offset(uint32_t blob_bytes) {
-    return ((blob_bytes + 127u) & ~127u) + (((uint32_t)sizeof(ws::SmemTail) + 127u) & ~127u);
-}
-
 template <int GM>
 __global__ void __launch_bounds__(GM * 128, 1) infer_aid_fused_kernel(InferParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1308,10 +1088,9 @@ __global__ void __launch_bounds__(GM * 128, 1) infer_aid_fused_kernel(InferParam
                 if (issuer)
                     ws::ws_issue(st, 1, l + 1, tmem_base, col_a, col_d, &st->mma_bar[g]);
             } else {
-                float y[16];
-                ws::ws_load_sum16(lane_base, col_d, 16u, 0u, bias, y);  // head: N = 16
+                const float y0 = ws::ws_load_head1(lane_base, col_d, bias);  // head: one output
                 tc_fence_before();
-                float qv = softplus_mod(y[0]);
+                float qv = softplus_mod(y0);
                 uint32_t decided = active ? 1u : 0u;
                 if (p.gate) {
                     if (valid && depth1)
@@ -1639,112 +1418,6 @@ __global__ void __launch_bounds__(kBT) compact2_kernel(CompactParams p) {
 // warp's shared-memory buffer and leave as full 256-byte warp stores.  Index arithmetic is 32-bit
 // (n < 2^32 and the capacity is a u32; positions are tile-relative).
 // ===========================================================================
-constexpr int kD3T = 1024;            // threads
-constexpr int kD3Tile = kD3T * 16;    // items per full tile
-constexpr int kD3Warp = 512;          // items per warp
-constexpr int kD3Stage = 256;         // staged slot records per warp and item group (2 KB)
-
-__device__ __forceinline__ void stamp(unsigned long long *dbg, uint32_t tile, int k) {
-#ifdef NRRS_KERNEL_TIMING
-    if (dbg && threadIdx.x == 0) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        dbg[tile * 8 + k] = t;
-    }
-#endif
-}
-
-struct Scan3Smem {
-    uint32_t warp_tot[kD3T / 32];
-    unsigned long long prefix;
-    uint32_t tile, epoch;
-};
-
-// Tile-relative exclusive position of this lane's first item of each group (items in (warp, i,
-// lane, e) order) from the per-group lane sums s[i]; the tile total in `agg`.
-__device__ __forceinline__ void scan4_positions(const uint32_t (&s)[4], Scan3Smem &sm, uint32_t (&excl)[4],
-                                                uint32_t &agg) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t run = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        uint32_t inc = s[i];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o)
-                inc += t;
-        }
-        excl[i] = run + inc - s[i];
-        run += __shfl_sync(0xffffffffu, inc, 31);
-    }
-    if (lane == 0)
-        sm.warp_tot[warp] = run;
-    __syncthreads();
-    const uint32_t t = lane < (int)(blockDim.x >> 5) ? sm.warp_tot[lane] : 0u;
-    uint32_t before = lane < warp ? t : 0u, all = t;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        before += __shfl_xor_sync(0xffffffffu, before, o);
-        all += __shfl_xor_sync(0xffffffffu, all, o);
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-        excl[i] += before;
-    agg = all;
-}
-
-// Exclusive prefix of `tile` (warp 0, every lane gets it).  single_wave: every tile of the launch
-// is resident, so the prefix is the sum of all predecessors' aggregates, read at once; each tile's
-// state word sits on its own 128-byte line (kStatePad) so the ~N^2 / 2 polls spread over N L2
-// lines instead of hammering a few.
-constexpr uint32_t kStatePad = 16;
-__device__ __forceinline__ uint64_t tile_prefix(uint64_t *state, uint32_t tile, uint64_t agg, uint32_t epoch,
-                                                bool single_wave, unsigned long long *dbg = nullptr) {
-    if (!single_wave)
-        return lookback_warp(state, tile, agg, epoch);
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint64_t tag = (uint64_t)(epoch & 0x3FFFu) << 48;
-    if (lane == 0)
-        st_relaxed_u64(&state[tile * kStatePad], kFlagAgg | tag | agg);
-    // up to 8 predecessors per lane (single wave: <= 256 tiles), requested together
-    const uint32_t ep = epoch & 0x3FFFu;
-    uint64_t st[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-        const uint32_t t = lane + 32u * (uint32_t)r;
-        st[r] = t < tile ? ld_relaxed_u64(&state[t * kStatePad]) : 0ull;
-    }
-    uint64_t v = 0;
-    uint32_t polls = 0;
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-        const uint32_t t = lane + 32u * (uint32_t)r;
-        if (t < tile) {
-            while ((st[r] >> 62) == 0 || ((st[r] >> 48) & 0x3FFFu) != ep) {
-                st[r] = ld_relaxed_u64(&state[t * kStatePad]);
-                ++polls;
-            }
-            v += st[r] & kValueMask;
-        }
-    }
-#ifdef NRRS_KERNEL_TIMING
-    polls = __reduce_max_sync(0xffffffffu, polls);
-    if (dbg && lane == 0) {
-        unsigned long long t1;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-        dbg[tile * 8 + 5] = t1;
-        dbg[tile * 8 + 6] = polls + 1;
-    }
-#else
-    (void)polls;
-#endif
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-        v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
 template <int SRC>  // 0: counts from (q, u) with normalization; 1: counts given (plan_spawns)
 __global__ void __launch_bounds__(kD3T, 1) decide3_kernel(DecideParams p) {
     __shared__ Scan3Smem sm;
@@ -1865,44 +1538,49 @@ __global__ void __launch_bounds__(kD3T, 1) decide3_kernel(DecideParams p) {
     const uint64_t cap = p.capacity;
     stamp(p.dbg, tile, 3);
     // room left in the queue at this tile's first record (positions below are tile-relative)
-    const uint32_t room = P < cap ? (uint32_t)(cap - P) : 0u;
+    const uint32_t room = P < cap ? (uint32_t)min(cap - P, (uint64_t)0xFFFFFFFFu) : 0u;
     const bool vec_out = ((reinterpret_cast<uintptr_t>(p.offset) | reinterpret_cast<uintptr_t>(p.k_out)) & 15u) == 0;
     uint2 *slots = reinterpret_cast<uint2 *>(p.slots) + P;
     uint2 *wbuf = reinterpret_cast<uint2 *>(kq + 4 * kD3T) + warp * kD3Stage;
-    // ---- offsets (wavefront.cpp:148) and slot records: child c of item j lands in slot
-    // cum + c while cum + c < capacity (:421-425, :436) ----
-#pragma unroll 1
+    // ---- slot records (wavefront.cpp:421-425, :436) and offsets (:148).  A warp's records of one
+    // item group are contiguous in the queue and in (item, child) order, so they are staged
+    // unclipped at their group-relative position and the capacity clip is a truncation of the
+    // copy-out; counts above 4 or groups beyond the staging buffer take the general loop. ----
+#pragma unroll
     for (int i = 0; i < 4; ++i) {
         const uint32_t first = wbase + 128u * (uint32_t)i;
-        uint32_t pos = excl[i];
-        const uint32_t gbase = __shfl_sync(0xffffffffu, pos, 0);
-        const uint32_t gtot = __shfl_sync(0xffffffffu, pos + gs[i], 31) - gbase;
+        const uint32_t gbase = __shfl_sync(0xffffffffu, excl[i], 0);
+        const uint32_t gtot = __shfl_sync(0xffffffffu, excl[i] + gs[i], 31) - gbase;
         const uint4 k4 = kq[i * kD3T + tid];
         const uint32_t kk[4] = {k4.x, k4.y, k4.z, k4.w};
-        uint32_t off[4];
+        if (p.slots) {
+            const bool big = __any_sync(0xffffffffu, (k4.x | k4.y | k4.z | k4.w) > 4u) || gtot > (uint32_t)kD3Stage;
+            uint32_t rel = excl[i] - gbase;
+            if (!big) {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const uint64_t cum = P + pos;
-            off[e] = (uint32_t)(cum < cap ? cum : cap);  // min(cum, capacity)
-            const uint32_t kept = pos < room ? min(kk[e], room - pos) : 0u;
-            const uint32_t rel = pos - gbase;
-            const uint32_t j = first + (uint32_t)e + p.parent_base;
+                for (int e = 0; e < 4; ++e) {
+                    const uint32_t j = first + (uint32_t)e + p.parent_base;
 #pragma unroll
-            for (uint32_t c = 0; c < 4u; ++c)
-                if (c < kept && rel + c < (uint32_t)kD3Stage)
-                    wbuf[rel + c] = make_uint2(j, c);
-            if (kept > 4u || (kept && rel + kept > (uint32_t)kD3Stage)) {  // rare: large counts
-                for (uint32_t c = 0; c < kept; ++c)
-                    if (c >= 4u || rel + c >= (uint32_t)kD3Stage) {
+                    for (uint32_t c = 0; c < 4u; ++c)
+                        if (c < kk[e])
+                            wbuf[rel + c] = make_uint2(j, c);
+                    rel += kk[e];
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const uint32_t j = first + (uint32_t)e + p.parent_base;
+                    const uint32_t pos = excl[i] + (rel - (excl[i] - gbase));  // tile-relative
+                    const uint32_t kept = pos < room ? min(kk[e], room - pos) : 0u;
+                    for (uint32_t c = 0; c < kept; ++c) {
                         if (rel + c < (uint32_t)kD3Stage)
                             wbuf[rel + c] = make_uint2(j, c);
                         else
                             __stcs(slots + pos + c, make_uint2(j, c));
                     }
+                    rel += kk[e];
+                }
             }
-            pos += kk[e];
-        }
-        if (p.slots) {
             __syncwarp();
             const uint32_t groom = gbase < room ? room - gbase : 0u;
             uint32_t nw = gtot < groom ? gtot : groom;
@@ -1912,6 +1590,13 @@ __global__ void __launch_bounds__(kD3T, 1) decide3_kernel(DecideParams p) {
             __syncwarp();
         }
         if (p.offset || p.k_out) {
+            uint32_t off[4];
+            uint64_t cum = P + excl[i];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                off[e] = (uint32_t)(cum < cap ? cum : cap);  // min(cum, capacity)
+                cum += kk[e];
+            }
             if (nv[i] == 4u && vec_out) {
                 if (p.offset)
                     *reinterpret_cast<uint4 *>(p.offset + first) = make_uint4(off[0], off[1], off[2], off[3]);

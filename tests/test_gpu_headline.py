@@ -59,3 +59,42 @@ def test_headline_size_parity(variant, kind, n):
     assert res.total == dec["total"] and res.spawned == dec["spawned"] and res.dropped == dec["dropped"]
     np.testing.assert_array_equal(_np(out.slots)[:res.spawned].view(np.uint32), dec["slots"])
     st.close()
+
+
+@pytest.mark.parametrize("n", [1920 * 1080, 65_536, 8 * 128 * 3 + 77])
+def test_fused_aid_stage_matches_three_kernel_path(n, monkeypatch):  # NRRS_FUSED=1 (opt-in path)
+    """The fused AID stage (one persistent kernel: level-sliced encode over an L2 ring, tcgen05 MLP,
+    in-kernel normalization / rounding / slot emission) against K-A0 + K-A + K-B on the same batch:
+    identical q_orig and u (same per-row arithmetic), and identical decisions whenever float(F)
+    agrees (the double sum of q is reduced in a different order)."""
+    v = orc.gen_vertices(n)
+    on = orc.OracleNets(orc.VARIANT_AID, seed=1, randomize=True)
+    outs = []
+    for fused in (True, False):
+        if fused:
+            monkeypatch.setenv("NRRS_FUSED", "1")
+        else:
+            monkeypatch.delenv("NRRS_FUSED", raising=False)
+        st = RrsStage(n, mirror_nets(on))
+        out, res = st.run(to_dev(v), 2, Strategy(StrategyKind.AidNrrs), rc=RateControl(), full=True)
+        torch.cuda.synchronize()
+        outs.append(({k: _np(getattr(out, k)).copy() for k in ("q_orig", "u", "q_norm", "q_real", "k", "offset",
+                                                                 "decided")},
+                     _np(out.slots)[:res.spawned].copy(), res))
+        st.close()
+    (a, sa, ra), (b, sb, rb) = outs
+    np.testing.assert_array_equal(a["q_orig"], b["q_orig"])
+    np.testing.assert_array_equal(a["u"], b["u"])
+    np.testing.assert_array_equal(a["decided"], b["decided"])
+    assert abs(ra.sum_q - rb.sum_q) <= 1e-12 * abs(rb.sum_q)
+    assert np.float32(ra.f_norm) == np.float32(rb.f_norm)
+    for key in ("q_norm", "q_real", "k", "offset"):
+        np.testing.assert_array_equal(a[key], b[key], err_msg=key)
+    assert ra.total == rb.total and ra.spawned == rb.spawned and ra.dropped == rb.dropped
+    np.testing.assert_array_equal(sa, sb)
+
+
+def test_fused_aid_stage_headline_oracle_parity(monkeypatch):
+    """The opt-in fused stage at the configs[2] size against the oracle directly."""
+    monkeypatch.setenv("NRRS_FUSED", "1")
+    test_headline_size_parity(orc.VARIANT_AID, orc.AID_NRRS, 1920 * 1080)
