@@ -206,7 +206,7 @@ def run_reference(args):
     value = sample / statistics.mean(times)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "vertices/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 sum; CPU port)", "data": "synthetic",
             "config": {"workload": f"{args.variant}-nrrs stage, 1920x1080 synthetic vertices at depth 2 "
                                    f"(full batch each step)",
                        "n_pixels": args.vertices, "strategy": f"{args.variant}-nrrs", "depth": 2},
@@ -265,6 +265,8 @@ def main():
         sh = None
         stage = RrsStage(npx, nets, device=local)
     stage.reserve(n)
+    _half, _perr = stage.table_precision()
+    aid_tables = {"fp16": _half, "error_budget_probe_max_rel_err": _perr, "budget": 2.5e-4}
     _tp = ctypes.c_void_p()
     _capi.check(stage.handle, _capi.lib().nrrs_gpu_stage_total_dev(stage.handle, ctypes.byref(_tp)))
     total_dev = _DevPtr(_tp.value)  # the stage's device-side realized total (compaction bound)
@@ -531,6 +533,31 @@ def main():
                 ts.append(a.elapsed_time(b))
             extra[name] = {"vertices_per_s": n / (statistics.mean(ts) / 1e3), "ms": statistics.mean(ts)}
             stg.close()
+        # the configs[2] batch again, through alternative AID forms chosen at context creation:
+        # fp32 grid tables (no fp16 error budget spent) and the opt-in fused single-kernel stage
+        if variant == RrsVariant.Aid:
+            for name, env in (("aid-nrrs-fp32-tables", "NRRS_FP32_TABLES"), ("aid-nrrs-fused-kernel", "NRRS_FUSED")):
+                os.environ[env] = "1"
+                try:
+                    stg = RrsStage(npx, nets, device=local)
+                finally:
+                    del os.environ[env]
+                o2 = stg.alloc_outputs(n)
+                for _ in range(3):
+                    stg.run(dv, 2, strategy, rc=None, out=o2, sync=False)
+                ts = []
+                for _ in range(5):
+                    flush.zero_()
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record()
+                    stg.run(dv, 2, strategy, rc=None, out=o2, sync=False)
+                    b.record()
+                    torch.cuda.synchronize()
+                    ts.append(a.elapsed_time(b))
+                half, perr = stg.table_precision()
+                extra[name] = {"vertices_per_s": n / (statistics.mean(ts) / 1e3), "ms": statistics.mean(ts),
+                               "aid_fp16_tables": half}
+                stg.close()
         # render-like, spatially coherent batch in pixel order, same strategy and nets
         hc = synthetic.gen_cornell_vertices(1920, 1080)
         dc = {k: torch.from_numpy(a.view(np.int64) if a.dtype == np.uint64 else a).to(dev)
@@ -789,12 +816,13 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "vertices/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": 1e3 * total_s / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp16x3-split MMA (fp32 accumulate), fp16 AID grid, f32 encodings; f64 sum", "data": "synthetic",
         "config": {"workload": f"configs[2] shape: {args.variant}-nrrs stage over a 1920x1080 synthetic vertex "
                                f"batch per GPU at depth 2 (SURVEY.md 8d), + compaction (~10% invalid slots)",
                    "vertices_per_gpu": n, "n_pixels": npx, "capacity": cap, "strategy": f"{args.variant}-nrrs",
                    "depth": 2, "gain": 0.85, "parallelism": f"tile-sharded dp{world}",
-                   "l2": "flushed between timed steps (256 MiB write outside the events)"},
+                   "l2": "flushed between timed steps (256 MiB write outside the events)",
+                   "aid_tables": aid_tables},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic,
                      "kernel": ("K-A0 grid_level_kernel + K-A infer_aid_fused_kernel<8> (level planes, 8 self-contained "

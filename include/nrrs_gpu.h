@@ -245,6 +245,13 @@ NRRS_API int nrrs_gpu_fetch_result(nrrs_gpu_ctx *ctx, nrrs_stage_result *h_resul
  * host round trip.  Stable for the context's lifetime. */
 NRRS_API int nrrs_gpu_stage_total_dev(nrrs_gpu_ctx *ctx, const uint64_t **d_total);
 
+/* Table precision chosen at nrrs_gpu_set_weights for the AID RRSNet grid: fp16
+ * only when the error-budget probe (16,384 fixed vertices through the fp16 and
+ * the fp32 tables of the same snapshot) keeps max |dq| / q <= 2.5e-4, a quarter
+ * of the 1e-3 tolerance; *probe_rel_err < 0 when no probe ran (NRRS variant,
+ * NRRS_FP32_TABLES, or |theta| beyond fp16 range). */
+NRRS_API int nrrs_gpu_weights_info(nrrs_gpu_ctx *ctx, int32_t *aid_fp16_tables, double *probe_rel_err);
+
 /* Per-frame ADRRS divisor input, replaces the film loop of trace_frame
  * (wavefront.cpp:238-243): *d_sum_out = sum over n_pixels of luminance(i_acc[p])
  * (f32 luminance, f64 sum, fixed order).  eps_div = eps_scale *

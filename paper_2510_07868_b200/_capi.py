@@ -104,6 +104,7 @@ SIGNATURES = [
     ("nrrs_gpu_launch_count", C.c_uint64, [_P]),
     ("nrrs_gpu_fetch_result", C.c_int, [_P, C.POINTER(StageResultC)]),
     ("nrrs_gpu_stage_total_dev", C.c_int, [_P, C.POINTER(C.c_void_p)]),
+    ("nrrs_gpu_weights_info", C.c_int, [_P, C.POINTER(C.c_int32), C.POINTER(C.c_double)]),
     ("nrrs_gpu_film_luminance_sum", C.c_int, [_P, _P, C.c_uint64, _P]),
     ("nrrs_gpu_fold_ordered", C.c_int, [_P, _P, C.c_uint64, _P, _P, C.c_uint64]),
     ("nrrs_gpu_emit_train", C.c_int, [_P, C.c_uint32, C.POINTER(VertexRecSoA), C.c_uint64, _P, _P, C.c_uint64,

@@ -175,6 +175,7 @@ struct nrrs_gpu_ctx {
     float *d_stat_grid = nullptr;
     void *d_rrs_grid = nullptr;
     bool rrs_half = false;  // AID grid stored as fp16 (precision)
+    double rrs_half_probe_err = -1.0;  // error-budget probe of the fp16 AID tables (< 0: not run)
     DeviceBlob blob_stat, blob_rrs, blob_both;  // ADRRS/STATS, AID, NRRS
 
     // scratch
@@ -279,6 +280,80 @@ static int ensure_compact_scratch(nrrs_gpu_ctx *ctx, uint64_t count, uint32_t wo
         CK(ctx, cudaMemsetAsync(ctx->d_ctile_state, 0, tiles * sizeof(uint64_t), ctx->stream));
     }
     return NRRS_OK;
+}
+
+static int run_factors(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, const nrrs_stage_params *p,
+                       float *q_out, float *u_out, uint8_t *decided_out, double *sum_out, bool accumulate = false);
+
+// Error-budget gate of the fp16 AID tables: the RRSNet factors of a fixed probe
+// batch (16,384 vertices, U[0,1)^3 positions, the SURVEY 8d tail ranges) through the fp16 tables and
+// through the fp32 tables of the same snapshot; fp16 is kept only when the largest relative difference
+// of q stays within a quarter of the north-star 1e-3 tolerance.  `upload32` installs the fp32 tables.
+constexpr double kHalfTableBudget = 2.5e-4;
+template <typename Upload32>
+static int aid_table_probe(nrrs_gpu_ctx *ctx, Upload32 upload32) {
+    constexpr uint32_t n = 16384;
+    std::vector<float> p01(3 * n), wo(2 * n), ro(n), wt(3 * n), ip(3 * n);
+    std::vector<uint64_t> key(n);
+    uint64_t s = 0x243F6A8885A308D3ull;
+    auto u01 = [&]() {
+        s = s * 6364136223846793005ull + 1442695040888963407ull;
+        return (float)(s >> 40) * 0x1p-24f;
+    };
+    for (uint32_t i = 0; i < n; ++i) {
+        for (int a = 0; a < 3; ++a) p01[3 * i + a] = u01();
+        for (int a = 0; a < 2; ++a) wo[2 * i + a] = u01();
+        ro[i] = u01();
+        for (int a = 0; a < 3; ++a) wt[3 * i + a] = 0.2f + u01();
+        for (int a = 0; a < 3; ++a) ip[3 * i + a] = 0.5f + u01();
+        key[i] = i;
+    }
+    float *d = nullptr;
+    const size_t floats = 3 * n + 2 * n + n + 3 * n + 3 * n + 2 * n /* q16, q32 */ + 2 * n /* key */;
+    CK(ctx, cudaMalloc(&d, floats * sizeof(float)));
+    float *dp = d, *dw = dp + 3 * n, *dr = dw + 2 * n, *dt = dr + n, *di = dt + 3 * n, *q16 = di + 3 * n,
+          *q32 = q16 + n;
+    uint64_t *dk = reinterpret_cast<uint64_t *>(q32 + n);
+    auto up = [&](float *dst, const std::vector<float> &src) {
+        return cudaMemcpy(dst, src.data(), src.size() * sizeof(float), cudaMemcpyHostToDevice);
+    };
+    int rc = NRRS_OK;
+    if (up(dp, p01) != cudaSuccess || up(dw, wo) != cudaSuccess || up(dr, ro) != cudaSuccess ||
+        up(dt, wt) != cudaSuccess || up(di, ip) != cudaSuccess ||
+        cudaMemcpy(dk, key.data(), n * 8, cudaMemcpyHostToDevice) != cudaSuccess)
+        rc = fail(ctx, NRRS_ECUDA, "probe upload failed");
+    nrrs_vertex_soa v{};
+    v.p01 = dp;
+    v.wo01 = dw;
+    v.roughness = dr;
+    v.weight = dt;
+    v.i_pixel = di;
+    v.path_key = dk;
+    nrrs_stage_params p{};
+    p.depth = 2;
+    p.n_pixels = n;
+    p.strategy.kind = NRRS_AID_NRRS;
+    double worst = 0.0;
+    if (!rc)
+        rc = run_factors(ctx, &v, n, &p, q16, nullptr, nullptr, ctx->d_sum + 1);
+    if (!rc)
+        rc = upload32();  // fp32 tables now installed
+    if (!rc)
+        rc = run_factors(ctx, &v, n, &p, q32, nullptr, nullptr, ctx->d_sum + 1);
+    if (!rc) {
+        std::vector<float> a(n), b(n);
+        if (cudaMemcpyAsync(a.data(), q16, n * 4, cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+            cudaMemcpyAsync(b.data(), q32, n * 4, cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+            cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+            rc = fail(ctx, NRRS_ECUDA, "probe readback failed");
+        for (uint32_t i = 0; !rc && i < n; ++i) {
+            const double r = std::fabs((double)a[i] - (double)b[i]) / std::max(std::fabs((double)b[i]), 1e-6);
+            worst = std::isfinite(r) ? std::max(worst, r) : 1e30;
+        }
+    }
+    cudaFree(d);
+    ctx->rrs_half_probe_err = worst;
+    return rc;
 }
 
 extern "C" {
@@ -561,6 +636,35 @@ int nrrs_gpu_set_weights(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w) {
     ctx->grid_rrs.copy_stride = (uint64_t)g.levels * T;
     ctx->grid_rrs.pair_copies = rrs_copies;
     ctx->has_weights = true;
+    ctx->rrs_half_probe_err = -1.0;
+    if (half) {
+        // error-budget gate: keep the fp16 tables only if the probe stays within budget
+        void *half_grid = ctx->d_rrs_grid;  // installed for the probe's first pass
+        void *f32_grid = nullptr;
+        rc = aid_table_probe(ctx, [&]() -> int {
+            f32_grid = nullptr;
+            const int r = upload_grid(f32_grid, w->rrs_grid, rrs_grid_len, false, usable(kPairCopiesF32));
+            ctx->d_rrs_grid = f32_grid;
+            ctx->rrs_half = false;
+            ctx->grid_rrs.pair_copies = usable(kPairCopiesF32);
+            return r;
+        });
+        if (rc) {
+            if (f32_grid) cudaFree(f32_grid);
+            ctx->d_rrs_grid = half_grid;
+            ctx->rrs_half = true;
+            ctx->grid_rrs.pair_copies = rrs_copies;
+            return rc;
+        }
+        if (ctx->rrs_half_probe_err <= kHalfTableBudget) {
+            cudaFree(f32_grid);
+            ctx->d_rrs_grid = half_grid;
+            ctx->rrs_half = true;
+            ctx->grid_rrs.pair_copies = rrs_copies;
+        } else {
+            cudaFree(half_grid);  // over budget: the fp32 tables stay installed
+        }
+    }
     return NRRS_OK;
 }
 
@@ -655,7 +759,7 @@ static int check_soa(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, int kind) {
 }
 
 static int run_factors(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, const nrrs_stage_params *p,
-                       float *q_out, float *u_out, uint8_t *decided_out, double *sum_out, bool accumulate = false) {
+                       float *q_out, float *u_out, uint8_t *decided_out, double *sum_out, bool accumulate) {
     int kind = 0, heur = 0;
     int rc = select_kind(ctx, p->depth, p->strategy, &kind, &heur);
     if (rc)
@@ -1894,6 +1998,16 @@ int nrrs_gpu_tracer_vertices(const nrrs_tracer *t, int32_t depth, nrrs_vertex_re
     out->decided = v.decided;
     out->s = v.s;
     *count = t->nverts[(size_t)depth];
+    return NRRS_OK;
+}
+
+int nrrs_gpu_weights_info(nrrs_gpu_ctx *ctx, int32_t *aid_fp16_tables, double *probe_rel_err) {
+    if (!ctx)
+        return NRRS_EINVAL;
+    if (aid_fp16_tables)
+        *aid_fp16_tables = ctx->rrs_half ? 1 : 0;
+    if (probe_rel_err)
+        *probe_rel_err = ctx->rrs_half_probe_err;
     return NRRS_OK;
 }
 

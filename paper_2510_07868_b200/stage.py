@@ -153,6 +153,12 @@ class RrsStage:
         _capi.check(self.handle, self.ctx.lib.nrrs_gpu_set_weights(self.handle, C.byref(w)))
         self.nets = nets
 
+    def table_precision(self) -> tuple:
+        """(AID grid stored in fp16?, error-budget probe max relative error of q; < 0 if not run)."""
+        h, e = C.c_int32(0), C.c_double(0.0)
+        _capi.check(self.handle, self.ctx.lib.nrrs_gpu_weights_info(self.handle, C.byref(h), C.byref(e)))
+        return bool(h.value), float(e.value)
+
     def reserve(self, max_vertices: int) -> None:
         _capi.check(self.handle, self.ctx.lib.nrrs_gpu_reserve(self.handle, int(max_vertices), self.capacity))
 

@@ -148,3 +148,47 @@ def test_train_frame_warmup_drives_q_to_one_and_publishes():
                        for k, a in v.items() if k != "pixel"}, 2, Strategy(StrategyKind.AidNrrs))
     assert np.isfinite(res.f_norm) and res.total > 0
     tr.close()
+
+
+@pytest.mark.parametrize("variant", [orc.VARIANT_NRRS, orc.VARIANT_AID], ids=["nrrs", "aid"])
+def test_trained_weights_stage_parity(variant):
+    """Parity on TRAINED weights (every other parity test uses the x1e4-scaled
+    random grids): train_frame (warmup, then the full variance-transfer phase) on the GPU, publish
+    (networks.cpp:199-204), then the inference stage against the oracle holding the same snapshot:
+    q_orig within the north-star 1e-3 relative, RrsRound uniforms exact, and the decisions on the
+    GPU's own factors bit-exact through the oracle's decide chain."""
+    from helpers import oracle_decide, rel_err
+    from paper_2510_07868_b200 import NeuralRrs, NeuralRrsConfig, RateControl, RrsStage, RrsVariant, Strategy, \
+        StrategyKind
+    from paper_2510_07868_b200.training import FULL, WARMUP, NeuralRrsTrainer
+    rv = RrsVariant.Aid if variant == orc.VARIANT_AID else RrsVariant.Nrrs
+    nets = NeuralRrs(NeuralRrsConfig(variant=rv, seed=1)).randomize_for_benchmark()
+    tr = NeuralRrsTrainer(nets, batch=8192)
+    b, db = _rrs_batch(16384, seed=9)
+    for _ in range(6):
+        tr.train_frame(db, None, 0.0, WARMUP)
+    errors = torch.from_numpy(orc.gen_pixel_errors(2048).view(np.float32).copy()).cuda()
+    for _ in range(6):
+        tr.train_frame(db, errors, 0.5, FULL)
+    pub = tr.publish()
+    tr.close()
+    on = orc.OracleNets(variant, arrays=(pub.stat_grid, pub.stat_mlp, pub.rrs_grid, pub.rrs_mlp))
+    n = 65_536
+    v = orc.gen_vertices(n)
+    kind = orc.AID_NRRS if variant == orc.VARIANT_AID else orc.NRRS
+    from helpers import to_dev
+    from paper_2510_07868_b200 import queue_capacity_for
+    cap = queue_capacity_for(n)
+    ref = orc.rrs_stage(v, 2, n, cap, kind, on, gain=0.85, seed=0, threads=orc.threads_available())
+    st = RrsStage(n, pub)
+    out, res = st.run(to_dev(v), 2, Strategy(StrategyKind(kind)), rc=RateControl(), full=True)
+    torch.cuda.synchronize()
+    q = out.q_orig.cpu().numpy()
+    assert np.all(np.isfinite(q))
+    err = rel_err(q, ref["q_orig"], 1e-6)
+    assert err.max() <= 1e-3, f"trained-weight q_orig max rel err {err.max():.3e}"
+    np.testing.assert_array_equal(out.u.cpu().numpy(), ref["u"])
+    dec = oracle_decide(q, out.u.cpu().numpy(), n, cap, 0.85)
+    np.testing.assert_array_equal(out.k.cpu().numpy(), dec["k"])
+    np.testing.assert_array_equal(out.slots.cpu().numpy()[:res.spawned].view(np.uint32), dec["slots"])
+    st.close()
