@@ -589,3 +589,22 @@ def test_fp16_table_error_budget_gate(grid_scale):
     fin = np.isfinite(ref["q_orig"])
     assert rel_err(_np(out.q_orig)[fin], ref["q_orig"][fin], 1e-6).max() <= REL_TOL
     st.close()
+
+
+@pytest.mark.parametrize("variant", [orc.VARIANT_NRRS, orc.VARIANT_AID], ids=["nrrs", "aid"])
+def test_stage_matches_reference_compiled_networks(variant):
+    """The GPU factors against predict_q / predict_stats computed by the REFERENCE's own network
+    code (tests/golden/ref_nets_golden.npz, generated by compiling networks.cpp / mlp.cpp /
+    hashgrid.cpp unmodified): q within the north-star 1e-3, stats within 1e-3."""
+    g = np.load(GOLDEN / "ref_nets_golden.npz")
+    v = {k: g[k] for k in ("p01", "wo01", "roughness", "weight", "i_pixel", "path_key")}
+    name = "aid" if variant == orc.VARIANT_AID else "nrrs"
+    on = orc.OracleNets(variant, seed=1, randomize=True)
+    st = _stage(v["roughness"].shape[0], on)
+    kind = StrategyKind.AidNrrs if variant == orc.VARIANT_AID else StrategyKind.Nrrs
+    q = _np(st.strategy_factor(to_dev(v), Strategy(kind)))
+    assert rel_err(q, g[f"{name}_q"], 1e-6).max() <= REL_TOL
+    stats = _np(st.predict_stats(to_dev(v)))
+    ref = g[f"{name}_stats"]
+    assert np.max(np.abs(stats - ref) / np.maximum(np.abs(ref), 1e-2)) <= REL_TOL
+    st.close()

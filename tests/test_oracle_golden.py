@@ -532,3 +532,20 @@ def test_oracle_bsdf_sample_identities():
                                C.byref(pdf), orc.ptr(thr))
         if ok:
             assert wi[2] > 0 and pdf.value > 0 and np.isfinite(thr).all()
+
+
+def test_oracle_matches_reference_compiled_networks():
+    """The oracle's StatNet / RRSNet forward (grid encode + input builders + MLP) against the
+    REFERENCE's own networks.cpp / mlp.cpp / hashgrid.cpp, compiled unmodified against the Eigen
+    subset shim (oracle/eigen_shim) and fed the benchmark snapshots through the reference's
+    NRRSCK01 loader (tests/golden/make_ref_golden.py): predict_stats bit-identical, predict_q
+    within 1e-6 relative (libm exp / log1p rounding)."""
+    import numpy as np
+    g = np.load(pathlib.Path(__file__).parent / "golden" / "ref_nets_golden.npz")
+    v = {k: g[k] for k in ("p01", "wo01", "roughness", "weight", "i_pixel", "path_key")}
+    for name, variant in (("nrrs", orc.VARIANT_NRRS), ("aid", orc.VARIANT_AID)):
+        on = orc.OracleNets(variant, seed=1, randomize=True)
+        np.testing.assert_array_equal(orc.predict_stats(on, v), g[f"{name}_stats"])
+        q = orc.predict_q(on, v)
+        ref = g[f"{name}_q"]
+        assert np.max(np.abs(q - ref) / np.abs(ref)) <= 1e-6, name
