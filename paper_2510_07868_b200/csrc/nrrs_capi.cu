@@ -212,6 +212,11 @@ struct nrrs_gpu_ctx {
     uint64_t cap_tloss = 0;
     float *d_tpart = nullptr;
     uint64_t cap_tpart = 0;
+    // deterministic grid-gradient scatter (nrrs_train.cu GridScatter): 4 u32 + 1 float2 per contribution
+    uint32_t *d_gsc = nullptr;
+    uint64_t cap_gsc = 0;
+    uint8_t *d_gsc_tmp = nullptr;
+    uint64_t cap_gsc_tmp = 0;
 
     // host-path pipeline: chunked H2D on copy_stream overlapped with K-A on `stream`
     cudaStream_t copy_stream = nullptr;
@@ -424,7 +429,7 @@ int nrrs_gpu_destroy(nrrs_gpu_ctx *ctx) {
     cudaStreamSynchronize(ctx->stream);
     void *ptrs[] = {ctx->d_stat_grid, ctx->d_rrs_grid, ctx->blob_stat.ptr, ctx->blob_rrs.ptr, ctx->blob_both.ptr,
                     ctx->d_q, ctx->d_u, ctx->d_parts, ctx->d_part_counts, ctx->d_tile_state, ctx->d_ctile_state,
-                    ctx->d_misc, ctx->d_res, ctx->d_sum, ctx->d_total, ctx->d_sync, ctx->d_etile_state, ctx->d_hist, ctx->d_tws, ctx->d_tloss, ctx->d_tpart, ctx->d_feat, ctx->d_ring, ctx->d_fsync, ctx->d_fstate, ctx->st.p01, ctx->st.wo01, ctx->st.rough,
+                    ctx->d_misc, ctx->d_res, ctx->d_sum, ctx->d_total, ctx->d_sync, ctx->d_etile_state, ctx->d_hist, ctx->d_tws, ctx->d_tloss, ctx->d_tpart, ctx->d_gsc, ctx->d_gsc_tmp, ctx->d_feat, ctx->d_ring, ctx->d_fsync, ctx->d_fstate, ctx->st.p01, ctx->st.wo01, ctx->st.rough,
                     ctx->st.weight, ctx->st.ipix, ctx->st.key, ctx->st.q_norm, ctx->st.q_real, ctx->st.q_orig,
                     ctx->st.u, ctx->st.k, ctx->st.offset, ctx->st.slots, ctx->st.decided};
     for (void *p : ptrs)
@@ -1237,6 +1242,23 @@ int nrrs_gpu_film_roll_acc(nrrs_gpu_ctx *ctx, float *d_i_acc, const float *d_i_c
     return NRRS_OK;
 }
 
+
+// Scratch of the deterministic grid-gradient scatter for n samples of `levels` levels.
+static int ensure_scatter(nrrs_gpu_ctx *ctx, uint64_t n, int levels, GridScatter *sc) {
+    const uint64_t m = n * (uint64_t)levels * 8u;
+    CK(ctx, grow(ctx->d_gsc, ctx->cap_gsc, 6 * m));  // keys, keys_sorted, slots, slots_sorted, vals (2 words)
+    const uint64_t tb = grid_scatter_sort_bytes(m);
+    CK(ctx, grow(ctx->d_gsc_tmp, ctx->cap_gsc_tmp, tb));
+    sc->keys = ctx->d_gsc;
+    sc->keys_sorted = ctx->d_gsc + m;
+    sc->slots = ctx->d_gsc + 2 * m;
+    sc->slots_sorted = ctx->d_gsc + 3 * m;
+    sc->vals = reinterpret_cast<float2 *>(ctx->d_gsc + 4 * m);
+    sc->sort_tmp = ctx->d_gsc_tmp;
+    sc->sort_tmp_bytes = tb;
+    return NRRS_OK;
+}
+
 // ---- online training: StatNet step ----
 int nrrs_gpu_stat_loss_grad(nrrs_gpu_ctx *ctx, const nrrs_grid_spec *spec, const float *d_stat_grid,
                             const float *d_stat_mlp, const nrrs_train_sample *d_batch, uint64_t n, float eps,
@@ -1284,6 +1306,11 @@ int nrrs_gpu_stat_loss_grad(nrrs_gpu_ctx *ctx, const nrrs_grid_spec *spec, const
     p.ws = ctx->d_tws;
     p.g_grid = d_g_grid;
     p.loss_parts = ctx->d_tloss;
+    {
+        const int rc = ensure_scatter(ctx, n, spec->levels, &p.scatter);
+        if (rc)
+            return rc;
+    }
     uint32_t *nonfinite = ctx->d_misc + 11;
     double *loss_out = ctx->d_sum + 3;
     CK(ctx, cudaMemsetAsync(nonfinite, 0, sizeof(uint32_t), ctx->stream));
@@ -1359,6 +1386,11 @@ int nrrs_gpu_rrs_loss_grad(nrrs_gpu_ctx *ctx, int32_t variant, const nrrs_grid_s
     p.inv_n = 1.0f / (float)n;
     p.ws = ctx->d_tws;
     p.g_grid = variant == 1 ? d_g_grid : nullptr;
+    if (variant == 1) {
+        const int rc = ensure_scatter(ctx, n, spec->levels, &p.scatter);
+        if (rc)
+            return rc;
+    }
     p.parts = ctx->d_tloss + 4;
     uint32_t *flags = ctx->d_misc + 11;  // [11] non-finite, [12] skipped
     p.skipped = ctx->d_misc + 12;

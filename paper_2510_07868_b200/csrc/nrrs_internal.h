@@ -224,6 +224,18 @@ struct TrainGrid {
     int32_t levels, base_resolution;
     uint32_t table_size, dense_mask;
 };
+// HashGrid::encode_backward without float atomics: every (sample, level, corner) contribution
+// w * d_out goes to slot (s * levels + l) * 8 + c with its entry as key; a stable radix sort by
+// entry then sums each entry's run sequentially in slot order -- the reference's own loop order
+// (hashgrid.cpp:84-103), so the gradient is bit-identical from run to run.
+struct GridScatter {
+    uint32_t *keys, *keys_sorted, *slots, *slots_sorted;  // [n * levels * 8]; keys pre-set to 0xFFFFFFFF
+    float2 *vals;                                          // [n * levels * 8]
+    void *sort_tmp;
+    size_t sort_tmp_bytes;
+};
+size_t grid_scatter_sort_bytes(uint64_t contributions);
+
 struct TrainStepParams {
     const nrrs_train_sample *batch;
     uint64_t n;
@@ -235,6 +247,7 @@ struct TrainStepParams {
     float *ws;                // per-sample workspace
     float *g_grid;            // zeroed by the caller
     double *loss_parts;       // [blocks]
+    GridScatter scatter;      // deterministic grid-gradient scatter (launch_*_train fills it)
 };
 struct RrsStepParams {
     const nrrs_train_sample *batch;
@@ -253,6 +266,7 @@ struct RrsStepParams {
     float *g_grid;                       // zeroed by the caller (AID)
     double *parts;                       // [blocks][3] min, avg, rrs
     uint32_t *skipped;
+    GridScatter scatter;                 // deterministic grid-gradient scatter (launch_*_train fills it)
 };
 struct AdamParams {
     float lr, beta1, beta2, eps, c1, c2, inv_scale, decay;

@@ -19,6 +19,8 @@
 #include "nrrs_device.cuh"
 #include "nrrs_internal.h"
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include <cuda_runtime.h>
 
 namespace nrrs {
@@ -188,8 +190,9 @@ __global__ void __launch_bounds__(256) stat_fwd_bwd_kernel(TrainStepParams p) {
                     grid_corners(p.grid, lv, t.position, base, w);
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
-                        atomicAdd(p.g_grid + base[k], w[k] * da[2 * lv]);
-                        atomicAdd(p.g_grid + base[k] + 1, w[k] * da[2 * lv + 1]);
+                        const uint64_t slot = (s * (uint64_t)p.grid.levels + (uint64_t)lv) * 8u + (uint64_t)k;
+                        p.scatter.keys[slot] = base[k];
+                        p.scatter.vals[slot] = make_float2(w[k] * da[2 * lv], w[k] * da[2 * lv + 1]);
                     }
                 }
             }
@@ -508,8 +511,9 @@ __global__ void __launch_bounds__(256) rrs_fwd_bwd_kernel(RrsStepParams p) {
                     grid_corners(p.grid, lv, t.position, base, w);
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
-                        atomicAdd(p.g_grid + base[k], w[k] * da[2 * lv]);
-                        atomicAdd(p.g_grid + base[k] + 1, w[k] * da[2 * lv + 1]);
+                        const uint64_t slot = (s * (uint64_t)p.grid.levels + (uint64_t)lv) * 8u + (uint64_t)k;
+                        p.scatter.keys[slot] = base[k];
+                        p.scatter.vals[slot] = make_float2(w[k] * da[2 * lv], w[k] * da[2 * lv + 1]);
                     }
                 }
             }
@@ -580,6 +584,54 @@ uint32_t train_dw_ctas(uint64_t n) {
     return (uint32_t)(c < 1 ? 1 : (c > 256 ? 256 : c));
 }
 
+// Sums each entry's run of sorted contributions in slot order (sample, level, corner), like the
+// reference's sequential encode_backward loop; one thread per run start.
+__global__ void __launch_bounds__(256) grid_scatter_fold_kernel(GridScatter sc, uint64_t m, float *g_grid) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m)
+        return;
+    const uint32_t key = sc.keys_sorted[i];
+    if (key == 0xFFFFFFFFu || (i > 0 && sc.keys_sorted[i - 1] == key))
+        return;
+    float a0 = 0.0f, a1 = 0.0f;
+    for (uint64_t j = i; j < m && sc.keys_sorted[j] == key; ++j) {
+        const float2 v = sc.vals[sc.slots_sorted[j]];
+        a0 = __fadd_rn(a0, v.x);
+        a1 = __fadd_rn(a1, v.y);
+    }
+    g_grid[key] = a0;
+    g_grid[key + 1] = a1;
+}
+
+__global__ void iota_kernel(uint32_t *out, uint64_t m) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = (uint32_t)i;
+}
+
+size_t grid_scatter_sort_bytes(uint64_t contributions) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                    (const uint32_t *)nullptr, (uint32_t *)nullptr, (int64_t)contributions, 0, 32);
+    return bytes;
+}
+
+// keys of the grid's entries span [0, 2 * levels * T): sort just those bits (the 0xFFFFFFFF
+// sentinel of non-contributing slots sorts after every entry)
+static cudaError_t grid_scatter_reduce(const GridScatter &sc, uint64_t m, uint64_t ngrid, float *g_grid,
+                                       cudaStream_t stream) {
+    int bits = 1;
+    while ((1ull << bits) <= ngrid)
+        ++bits;
+    iota_kernel<<<1024, 256, 0, stream>>>(sc.slots, m);
+    size_t tmp = sc.sort_tmp_bytes;
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(sc.sort_tmp, tmp, sc.keys, sc.keys_sorted, sc.slots,
+                                                    sc.slots_sorted, (int64_t)m, 0, bits, stream);
+    if (e != cudaSuccess)
+        return e;
+    grid_scatter_fold_kernel<<<(uint32_t)((m + 255) / 256), 256, 0, stream>>>(sc, m, g_grid);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_stat_train(const TrainStepParams &p, float *partials, uint32_t dw_ctas, float *g_mlp,
                               double *loss_out, uint32_t *nonfinite, uint64_t ngrid, cudaStream_t stream) {
     const uint32_t blocks = (uint32_t)((p.n + 255) / 256);
@@ -587,7 +639,14 @@ cudaError_t launch_stat_train(const TrainStepParams &p, float *partials, uint32_
     cudaError_t e = cudaFuncSetAttribute(stat_fwd_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
         return e;
+    const uint64_t m = p.n * (uint64_t)p.grid.levels * 8u;
+    e = cudaMemsetAsync(p.scatter.keys, 0xFF, m * sizeof(uint32_t), stream);
+    if (e != cudaSuccess)
+        return e;
     stat_fwd_bwd_kernel<<<blocks, 256, smem, stream>>>(p);
+    e = grid_scatter_reduce(p.scatter, m, ngrid, p.g_grid, stream);
+    if (e != cudaSuccess)
+        return e;
     const uint64_t per = (p.n + dw_ctas - 1) / dw_ctas;
     mlp_dw_kernel<kTOut><<<dw_ctas, 256, 0, stream>>>(p.ws, p.n, p.in, per, partials);
     stat_reduce_kernel<<<64, 256, 0, stream>>>(partials, (int)dw_ctas, stat_param_count(p.in), g_mlp, p.loss_parts,
@@ -603,7 +662,18 @@ cudaError_t launch_rrs_train(const RrsStepParams &p, float *partials, uint32_t d
     cudaError_t e = cudaFuncSetAttribute(rrs_fwd_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
         return e;
+    const uint64_t m = p.n * (uint64_t)p.grid.levels * 8u;
+    if (p.variant == 1 && p.g_grid) {
+        e = cudaMemsetAsync(p.scatter.keys, 0xFF, m * sizeof(uint32_t), stream);
+        if (e != cudaSuccess)
+            return e;
+    }
     rrs_fwd_bwd_kernel<<<blocks, 256, smem, stream>>>(p);
+    if (p.variant == 1 && p.g_grid) {
+        e = grid_scatter_reduce(p.scatter, m, ngrid, p.g_grid, stream);
+        if (e != cudaSuccess)
+            return e;
+    }
     const uint64_t per = (p.n + dw_ctas - 1) / dw_ctas;
     mlp_dw_kernel<1><<<dw_ctas, 256, 0, stream>>>(p.ws, p.n, p.in, per, partials);
     rrs_reduce_kernel<<<64, 256, 0, stream>>>(partials, (int)dw_ctas, mlp_params(p.in, 1), g_mlp, p.parts,

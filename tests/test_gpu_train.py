@@ -192,3 +192,30 @@ def test_trained_weights_stage_parity(variant):
     np.testing.assert_array_equal(out.k.cpu().numpy(), dec["k"])
     np.testing.assert_array_equal(out.slots.cpu().numpy()[:res.spawned].view(np.uint32), dec["slots"])
     st.close()
+
+
+@pytest.mark.parametrize("variant", [orc.VARIANT_NRRS, orc.VARIANT_AID], ids=["nrrs", "aid"])
+def test_training_is_bitwise_deterministic(variant):
+    """Two identical train_frame sequences (warmup then full phase) from the same nets give
+    bitwise-identical live weights, EMA snapshots and losses (the reference's neural runs are
+    bit-identical across runs, test_harness.cpp:370-403): the hash-grid gradient scatter is a
+    stable sort by entry + in-order run sums, not float atomics."""
+    from paper_2510_07868_b200 import NeuralRrs, NeuralRrsConfig, RrsVariant
+    from paper_2510_07868_b200.training import FULL, WARMUP, NeuralRrsTrainer
+    rv = RrsVariant.Aid if variant == orc.VARIANT_AID else RrsVariant.Nrrs
+    _, db = _rrs_batch(20000, seed=4)
+    errors = torch.from_numpy(orc.gen_pixel_errors(2048).view(np.float32).copy()).cuda()
+    runs = []
+    for _ in range(2):
+        nets = NeuralRrs(NeuralRrsConfig(variant=rv, seed=1)).randomize_for_benchmark()
+        tr = NeuralRrsTrainer(nets, batch=8192)
+        losses = [tr.train_frame(db, None, 0.0, WARMUP) for _ in range(3)]
+        losses += [tr.train_frame(db, errors, 0.5, FULL) for _ in range(3)]
+        pub = tr.publish()
+        runs.append(([np.asarray(x).copy() for x in (pub.stat_grid, pub.stat_mlp, pub.rrs_grid, pub.rrs_mlp)],
+                     losses))
+        tr.close()
+    (wa, la), (wb, lb) = runs
+    for x, y in zip(wa, wb):
+        assert x.tobytes() == y.tobytes()
+    assert la == lb
