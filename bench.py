@@ -69,6 +69,9 @@ def parse():
     ap.add_argument("--variant", default="aid", choices=["aid", "nrrs"])
     ap.add_argument("--vertices", type=int, default=N_LOCAL, help="vertices per rank")
     ap.add_argument("--no-extra", action="store_true", help="skip the per-strategy side measurements")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling (configs[3]): --vertices is the whole film, split into N row bands "
+                         "(default: weak scaling, --vertices per rank; N=8 is the configs[4] 16.6 M batch)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     return ap.parse_args()
 
@@ -247,15 +250,21 @@ def main():
         else:
             dist.init_process_group(backend, init_method="env://")
     dev = torch.device("cuda", local)
-    n = args.vertices
-    npx = n * world
+    if args.strong:  # one film of args.vertices pixels, rank r takes the r-th contiguous band
+        first = args.vertices * rank // world
+        n = args.vertices * (rank + 1) // world - first
+        npx = args.vertices
+    else:
+        first = rank * args.vertices
+        n = args.vertices
+        npx = n * world
     cap = queue_capacity_for(npx)
     variant = RrsVariant.Aid if args.variant == "aid" else RrsVariant.Nrrs
     strategy = Strategy(StrategyKind.AidNrrs if args.variant == "aid" else StrategyKind.Nrrs)
     nets = NeuralRrs(NeuralRrsConfig(variant=variant, seed=1)).randomize_for_benchmark()
 
     # inputs resident in HBM before timing
-    hv = synthetic.gen_vertices(n, n_pixels=npx, first=rank * n)
+    hv = synthetic.gen_vertices(n, n_pixels=npx, first=first)
     dv = {k: torch.from_numpy(a.view(np.int64) if a.dtype == np.uint64 else a).to(dev)
           for k, a in hv.items() if k != "pixel"}
     if world > 1:
@@ -382,7 +391,7 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)  # max over ranks
     total_s = float(t.item())
-    value = world * n * args.steps / total_s
+    value = (args.vertices if args.strong else world * n) * args.steps / total_s
     res = _capi.StageResultC()
     if sh is not None and pending[0] is not None:
         po = pending[0].resolve(rc)  # the last timed depth's global outcome (host read after the loop)
@@ -502,7 +511,8 @@ def main():
             d2h = 8 * n + 8 * oc_.kept
         te = torch.tensor([e_tot], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * n * e_steps / float(te.item()), "unit": "vertices/s",
+        e2e = {"value": (args.vertices if args.strong else world * n) * e_steps / float(te.item()),
+               "unit": "vertices/s",
                "h2d_bytes_per_step": 56 * n, "d2h_bytes_per_step": d2h,
                "path": "ShardedRrsStage.run per rank (pinned host buffers, per-rank bytes, max over ranks)"}
 
@@ -816,9 +826,14 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "vertices/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": 1e3 * total_s / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "fp16x3-split MMA (fp32 accumulate), fp16 AID grid, f32 encodings; f64 sum", "data": "synthetic",
-        "config": {"workload": f"configs[2] shape: {args.variant}-nrrs stage over a 1920x1080 synthetic vertex "
-                               f"batch per GPU at depth 2 (SURVEY.md 8d), + compaction (~10% invalid slots)",
+        "scaling": "strong" if args.strong else "weak", "vs_baseline": None,
+        "dtype": "fp16x3-split MMA (fp32 accumulate), fp16 AID grid, f32 encodings; f64 sum", "data": "synthetic",
+        "config": {"workload": (f"configs[3] shape: {args.variant}-nrrs stage over ONE {args.vertices}-vertex "
+                                f"synthetic film split into {world} row bands at depth 2 (SURVEY.md 8d, 8e), "
+                                f"+ compaction (~10% invalid slots)") if args.strong else
+                               (f"configs[2] shape: {args.variant}-nrrs stage over a 1920x1080 synthetic vertex "
+                                f"batch per GPU at depth 2 (SURVEY.md 8d), + compaction (~10% invalid slots)"
+                                + ("; N=8 is the configs[4] 16.6 M-vertex batch" if world > 1 else "")),
                    "vertices_per_gpu": n, "n_pixels": npx, "capacity": cap, "strategy": f"{args.variant}-nrrs",
                    "depth": 2, "gain": 0.85, "parallelism": f"tile-sharded dp{world}",
                    "l2": "flushed between timed steps (256 MiB write outside the events)",

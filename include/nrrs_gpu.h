@@ -224,6 +224,12 @@ NRRS_API uint64_t nrrs_gpu_launch_count(const nrrs_gpu_ctx *ctx);
 /* ---- weights: replaces reading NeuralRrs' snapshot (networks.hpp:147, networks.cpp:276-279) */
 NRRS_API int nrrs_gpu_set_weights(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w);
 
+/* The same with DEVICE pointers in w (e.g. the snapshot blocks just broadcast
+ * over NCCL by the tile-sharded mode): the hash-grid table copies
+ * are built on the device; only the two small MLP blocks are read back for
+ * packing.  Same validation, error-budget gate and errors as nrrs_gpu_set_weights. */
+NRRS_API int nrrs_gpu_set_weights_dev(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w);
+
 /* ---- fused stage (1 rank): replaces wavefront.cpp:363-425 for one depth:
  *   strategy_factor over ns vertices (:368-389), normalize_factors (:390),
  *   gain (:391), RrsRound uniforms (:393-402), realize_counts (:403-404),

@@ -138,6 +138,7 @@ SIGNATURES = [
     ("nrrs_gpu_tracer_vertices", C.c_int, [_P, C.c_int32, C.POINTER(VertexRecSoA), C.POINTER(C.c_uint32)]),
     ("nrrs_gpu_surface_records", C.c_int, [_P, _P, _P, _P, _P, _P, C.c_uint64, _P, _P, _P, _P, _P]),
     ("nrrs_gpu_set_weights", C.c_int, [_P, C.POINTER(NetWeights)]),
+    ("nrrs_gpu_set_weights_dev", C.c_int, [_P, C.POINTER(NetWeights)]),
     ("nrrs_gpu_rrs_stage", C.c_int, [_P, C.POINTER(VertexSoA), C.c_uint64, C.POINTER(StageParams),
                                      C.POINTER(StageOut), C.POINTER(StageResultC)]),
     ("nrrs_gpu_rrs_stage_host", C.c_int, [_P, C.POINTER(VertexSoA), C.c_uint64, C.POINTER(StageParams),

@@ -486,7 +486,9 @@ int nrrs_gpu_reserve(nrrs_gpu_ctx *ctx, uint64_t max_vertices, uint32_t max_capa
     return ensure_compact_scratch(ctx, max_capacity, 18);
 }
 
-int nrrs_gpu_set_weights(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w) {
+// dev: the four parameter blocks are device pointers (nrrs_gpu_set_weights_dev); the table copies are
+// then built on the device and only the two small MLP blocks visit the host for packing.
+static int set_weights_impl(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w, bool dev) {
     if (!ctx || !w)
         return NRRS_EINVAL;
     const nrrs_grid_spec g = w->grid;
@@ -531,9 +533,19 @@ int nrrs_gpu_set_weights(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w) {
     std::vector<int> id11(11);
     for (int c = 0; c < 11; ++c)
         id11[c] = c;
-    const PackedNet stat = pack_net(w->stat_mlp, stat_in, 6, 32, grid_map);
-    const PackedNet rrs = w->variant == NRRS_VARIANT_NRRS ? pack_net(w->rrs_mlp, 11, 1, 16, id11)
-                                                          : pack_net(w->rrs_mlp, rrs_in, 1, 32, grid_map);
+    std::vector<float> stat_mlp_h, rrs_mlp_h;
+    const float *stat_mlp = w->stat_mlp, *rrs_mlp = w->rrs_mlp;
+    if (dev) {
+        stat_mlp_h.resize(w->stat_mlp_len);
+        rrs_mlp_h.resize(w->rrs_mlp_len);
+        CK(ctx, cudaMemcpy(stat_mlp_h.data(), w->stat_mlp, w->stat_mlp_len * 4, cudaMemcpyDeviceToHost));
+        CK(ctx, cudaMemcpy(rrs_mlp_h.data(), w->rrs_mlp, w->rrs_mlp_len * 4, cudaMemcpyDeviceToHost));
+        stat_mlp = stat_mlp_h.data();
+        rrs_mlp = rrs_mlp_h.data();
+    }
+    const PackedNet stat = pack_net(stat_mlp, stat_in, 6, 32, grid_map);
+    const PackedNet rrs = w->variant == NRRS_VARIANT_NRRS ? pack_net(rrs_mlp, 11, 1, 16, id11)
+                                                          : pack_net(rrs_mlp, rrs_in, 1, 32, grid_map);
     auto upload_blob = [&](DeviceBlob &b, bool with_stat, bool with_rrs) -> int {
         std::vector<uint8_t> bytes;
         KernelNets nets{};
@@ -564,12 +576,27 @@ int nrrs_gpu_set_weights(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w) {
         const uint32_t pi = i < half ? (i << 1) : (((G - 1u - i) << 1) | 1u);
         return (e & ~(G - 1u)) | pi;
     };
+    uint32_t dense_mask = 0;
+    for (int l = 0; l < g.levels; ++l) {
+        const uint64_t res = (uint64_t)g.base_resolution << l;
+        if ((res + 1) * (res + 1) * (res + 1) <= T)
+            dense_mask |= 1u << l;
+    }
     auto upload_grid = [&](auto *&dst, const float *src, uint64_t len, bool half, uint32_t copies) -> int {
         if (dst)
             cudaFree(dst);
         dst = nullptr;
         if (!len)
             return NRRS_OK;
+        if (dev) {
+            const size_t bytes = copies * len * (half ? sizeof(__half) : sizeof(float));
+            CK(ctx, cudaMalloc(reinterpret_cast<void **>(&dst), bytes));
+            CK(ctx, cudaMemsetAsync(dst, 0, bytes, ctx->stream));
+            CK(ctx, launch_grid_copies(src, dst, (uint32_t)g.levels, (uint32_t)T, copies, dense_mask, half,
+                                       ctx->stream));
+            CK(ctx, cudaStreamSynchronize(ctx->stream));
+            return NRRS_OK;
+        }
         std::vector<float> h(copies * len, 0.0f);
         std::memcpy(h.data(), src, len * sizeof(float));
         for (int l = 0; l < g.levels; ++l) {
@@ -608,7 +635,17 @@ int nrrs_gpu_set_weights(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w) {
     // half the bytes per gather on the path's binding resource, max relative error of q
     // 1.1e-4 against the 1e-3 bar.  Tables beyond fp16 range stay fp32.
     bool half = w->variant == NRRS_VARIANT_AID && !ctx->env_fp32_tables;
-    for (uint64_t i = 0; half && i < rrs_grid_len; ++i)
+    if (half && dev) {
+        unsigned int *bits = ctx->d_misc + 15, hb = 0;
+        CK(ctx, cudaMemsetAsync(bits, 0, sizeof(unsigned int), ctx->stream));
+        CK(ctx, launch_max_abs(w->rrs_grid, rrs_grid_len, bits, ctx->stream));
+        CK(ctx, cudaMemcpyAsync(&hb, bits, sizeof hb, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(ctx, cudaStreamSynchronize(ctx->stream));
+        float mx;
+        std::memcpy(&mx, &hb, sizeof mx);
+        half = mx < 32768.0f;
+    }
+    for (uint64_t i = 0; half && !dev && i < rrs_grid_len; ++i)
         if (!(std::fabs(w->rrs_grid[i]) < 32768.0f))
             half = false;
     auto usable = [&](uint32_t want) {  // copy t needs 2^(t+1) <= T
@@ -672,6 +709,10 @@ int nrrs_gpu_set_weights(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w) {
     }
     return NRRS_OK;
 }
+
+int nrrs_gpu_set_weights(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w) { return set_weights_impl(ctx, w, false); }
+
+int nrrs_gpu_set_weights_dev(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w) { return set_weights_impl(ctx, w, true); }
 
 }  // extern "C"
 

@@ -2019,6 +2019,68 @@ cudaError_t launch_compact(uint32_t words, CompactParams p, int num_sms, cudaStr
     return cudaGetLastError();
 }
 
+// Device-side table copies for nrrs_gpu_set_weights_dev (the layout set_weights builds on the host,
+// see GridDev): copy 0 = the reference layout; for hashed levels copy t stores entry e at
+// pair_pos(e, t) (when 2^(t+1) <= T); for dense levels copy 1 is shifted by one entry.  dst is
+// zeroed by the caller; half: fp16 entries.
+__global__ void grid_copies_kernel(const float2 *src, void *dst, uint32_t levels, uint32_t T, uint32_t copies,
+                                   uint32_t dense_mask, int half) {
+    const uint64_t per_copy = (uint64_t)levels * T, total = per_copy * copies;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t t = (uint32_t)(i / per_copy);
+        const uint64_t rem = i % per_copy;
+        const uint32_t l = (uint32_t)(rem / T), e = (uint32_t)(rem % T);
+        const float2 *lv = src + (uint64_t)l * T;
+        uint64_t pos;
+        float2 v;
+        if (t == 0) {
+            pos = e;
+            v = lv[e];
+        } else if ((dense_mask >> l) & 1u) {
+            if (t != 1 || e + 1 >= T)
+                continue;
+            pos = e;
+            v = lv[e + 1];
+        } else if ((2ull << t) <= T) {
+            pos = pair_pos(e, t);
+            v = lv[e];
+        } else {
+            continue;
+        }
+        const uint64_t o = (uint64_t)t * per_copy + (uint64_t)l * T + pos;
+        if (half)
+            reinterpret_cast<__half2 *>(dst)[o] = __floats2half2_rn(v.x, v.y);
+        else
+            reinterpret_cast<float2 *>(dst)[o] = v;
+    }
+}
+
+__global__ void max_abs_kernel(const float *x, uint64_t n, unsigned int *out_bits) {
+    float m = 0.0f;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const float a = fabsf(x[i]);
+        m = (a > m || a != a) ? (a != a ? __int_as_float(0x7f800000) : a) : m;  // NaN counts as +inf
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0)
+        atomicMax(out_bits, __float_as_uint(m));  // non-negative floats order like their bits
+}
+
+cudaError_t launch_grid_copies(const float *src, void *dst, uint32_t levels, uint32_t T, uint32_t copies,
+                               uint32_t dense_mask, bool half, cudaStream_t stream) {
+    grid_copies_kernel<<<1024, 256, 0, stream>>>(reinterpret_cast<const float2 *>(src), dst, levels, T, copies,
+                                                 dense_mask, half ? 1 : 0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_max_abs(const float *x, uint64_t n, unsigned int *out_bits, cudaStream_t stream) {
+    max_abs_kernel<<<256, 256, 0, stream>>>(x, n, out_bits);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_sum_check(const float *q, uint64_t n, double *parts, uint32_t *counter, uint32_t *err,
                              double *sum_out, uint32_t grid, cudaStream_t stream) {
     sum_check_kernel<<<grid, 256, 0, stream>>>(q, n, parts, counter, err, sum_out);

@@ -179,9 +179,10 @@ def row_band(rank: int, world: int, height: int):
 
 def gather_film(band: torch.Tensor, dst: int = 0, group=None) -> Optional[torch.Tensor]:
     """Per-frame film exchange of SURVEY.md 8e: each rank's band of f64 film rows ([px_band, ...],
-    pixel order) is gathered to rank `dst` in rank order, which is pixel order for row bands;
-    bands may differ in size (padded to the largest for the collective).  Returns the full film
-    on `dst`, None elsewhere."""
+    pixel order) is gathered to rank `dst` in rank order, which is pixel order for row bands --
+    a gather (one collective, only `dst` receives), not an all-gather.  Bands may differ in size:
+    their lengths are exchanged first (8 bytes per rank) and each band is padded to the largest.
+    Returns the full film on `dst`, None elsewhere."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     host = dist.get_backend(group) == "gloo" and band.is_cuda
@@ -191,30 +192,37 @@ def gather_film(band: torch.Tensor, dst: int = 0, group=None) -> Optional[torch.
     dist.all_gather(sizes, n_local, group=group)
     sizes = [int(x.item()) for x in sizes]
     rows = max(sizes)
-    pad = torch.zeros((rows,) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
-    pad[:src.shape[0]] = src
-    parts = [torch.zeros_like(pad) for _ in range(world)]
-    dist.all_gather(parts, pad, group=group)  # gather-to-dst as an all-gather: sizes are tiny next to NVLink
+    pad = src
+    if src.shape[0] != rows:
+        pad = torch.zeros((rows,) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
+        pad[:src.shape[0]] = src
+    parts = [torch.empty_like(pad) for _ in range(world)] if rank == dst else None
+    dist.gather(pad.contiguous(), gather_list=parts, dst=dst, group=group)
     if rank != dst:
         return None
     full = torch.cat([p[:k] for p, k in zip(parts, sizes)])
     return full.to(band.device)
 
 
-def broadcast_weights(nets, src: int = 0, group=None):
+def broadcast_weights(nets, src: int = 0, group=None, device=None):
     """Per publish() exchange of SURVEY.md 8e: rank `src`'s snapshot blocks (stat grid, stat MLP,
-    rrs grid for AID, rrs MLP; networks.cpp:199-204) are broadcast to every rank in place; the
-    caller then uploads them with set_weights.  Returns nets."""
+    rrs grid for AID, rrs MLP; networks.cpp:199-204) are broadcast to every rank.  On NCCL the
+    blocks stay on the GPU (returns the four device tensors for ShardedRrsStage.set_weights ->
+    nrrs_gpu_set_weights_dev, no host round trip); on gloo they are host tensors and `nets` is
+    updated in place.  Returns the list of the four broadcast tensors."""
+    nccl = dist.get_backend(group) == "nccl"
+    out = []
     for name in ("stat_grid", "stat_mlp", "rrs_grid", "rrs_mlp"):
         a = getattr(nets, name)
-        if a.size == 0:
-            continue
         t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32))
-        if dist.get_backend(group) == "nccl":
-            t = t.cuda()
-        dist.broadcast(t, src=src, group=group)
-        setattr(nets, name, t.cpu().numpy().astype(np.float32, copy=False))
-    return nets
+        if nccl:
+            t = t.to(device if device is not None else torch.device("cuda", torch.cuda.current_device()))
+        if t.numel():
+            dist.broadcast(t, src=src, group=group)
+        if not nccl:
+            setattr(nets, name, t.numpy().astype(np.float32, copy=False))
+        out.append(t)
+    return out
 
 
 class ShardedRrsStage:
@@ -258,8 +266,13 @@ class ShardedRrsStage:
                                self.group)
 
     def set_weights(self, nets, src: int = 0) -> None:
-        """publish(): broadcast rank src's snapshot, upload on every rank."""
-        self.stage.set_weights(broadcast_weights(nets, src, self.group))
+        """Per publish(): broadcast rank `src`'s snapshot and upload it on every rank (NCCL: the
+        broadcast blocks never leave the GPU, nrrs_gpu_set_weights_dev)."""
+        blocks = broadcast_weights(nets, src, self.group, device=self.device)
+        if dist.get_backend(self.group) == "nccl":
+            self.stage.set_weights_device(nets, blocks)
+        else:
+            self.stage.set_weights(nets)
 
     def run(self, vertices, depth: int, strategy: Strategy, rc: Optional[RateControl] = None,
             eps_div: float = 0.0, out: Optional[StageOutputs] = None):

@@ -153,6 +153,22 @@ class RrsStage:
         _capi.check(self.handle, self.ctx.lib.nrrs_gpu_set_weights(self.handle, C.byref(w)))
         self.nets = nets
 
+    def set_weights_device(self, nets: NeuralRrs, blocks) -> None:
+        """Uploads snapshot blocks that already live on this GPU (stat grid, stat MLP, rrs grid,
+        rrs MLP as float32 CUDA tensors; `nets` gives the variant and grid spec): the table copies
+        are built on the device (nrrs_gpu_set_weights_dev)."""
+        c = nets.cfg
+        blocks = [b.contiguous().float() for b in blocks]
+        fp = C.POINTER(C.c_float)
+        ptr = lambda t: C.cast(C.c_void_p(t.data_ptr()), fp) if t.numel() else None  # noqa: E731
+        w = _capi.NetWeights(
+            int(c.variant),
+            _capi.GridSpec(c.grid.levels, c.grid.features, c.grid.base_resolution, c.grid.log2_table_size),
+            ptr(blocks[0]), blocks[0].numel(), ptr(blocks[1]), blocks[1].numel(),
+            ptr(blocks[2]), blocks[2].numel(), ptr(blocks[3]), blocks[3].numel())
+        _capi.check(self.handle, self.ctx.lib.nrrs_gpu_set_weights_dev(self.handle, C.byref(w)))
+        self.nets = nets
+
     def table_precision(self) -> tuple:
         """(AID grid stored in fp16?, error-budget probe max relative error of q; < 0 if not run)."""
         h, e = C.c_int32(0), C.c_double(0.0)

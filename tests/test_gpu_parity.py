@@ -608,3 +608,28 @@ def test_stage_matches_reference_compiled_networks(variant):
     ref = g[f"{name}_stats"]
     assert np.max(np.abs(stats - ref) / np.maximum(np.abs(ref), 1e-2)) <= REL_TOL
     st.close()
+
+
+@pytest.mark.parametrize("variant", [orc.VARIANT_NRRS, orc.VARIANT_AID], ids=["nrrs", "aid"])
+def test_set_weights_from_device_blocks_matches_host_upload(variant):
+    """nrrs_gpu_set_weights_dev (snapshot blocks already on the GPU, e.g. just broadcast over NCCL;
+    the table copies are built on the device) installs exactly what the host upload installs:
+    identical factors, decisions and table precision choice."""
+    on = orc.OracleNets(variant, seed=1, randomize=True)
+    n = 65_536
+    v = to_dev(orc.gen_vertices(n))
+    nets = mirror_nets(on)
+    kind = StrategyKind.AidNrrs if variant == orc.VARIANT_AID else StrategyKind.Nrrs
+    a = RrsStage(n, nets)
+    b = RrsStage(n)
+    b.set_weights_device(nets, [torch.from_numpy(np.ascontiguousarray(x)).cuda()
+                                for x in (on.stat_grid, on.stat_mlp, on.rrs_grid, on.rrs_mlp)])
+    assert a.table_precision() == b.table_precision()
+    oa, ra = a.run(v, 2, Strategy(kind), rc=RateControl(), full=True)
+    ob, rb = b.run(v, 2, Strategy(kind), rc=RateControl(), full=True)
+    torch.cuda.synchronize()
+    for key in ("q_orig", "q_norm", "k", "offset"):
+        np.testing.assert_array_equal(_np(getattr(oa, key)), _np(getattr(ob, key)), err_msg=key)
+    assert ra.spawned == rb.spawned and ra.f_norm == rb.f_norm
+    a.close()
+    b.close()
