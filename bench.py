@@ -595,37 +595,119 @@ def main():
     # replays of 1000 stage calls (K-A + K-B), same strategy and nets ----
     c1 = None
     if world == 1 and not args.no_extra:
+        # configs[0]: NRRS normalized-RRS step on 65,536 synthetic vertices, random-init RRSNet, split
+        # bound 4 (C1).  Launch-bound: per-call times from CUDA-graph replays of 100
+        # calls, plus the single-call latency; the decision-only variant feeds the split-bound-4
+        # factors q = RngStream(0xACC02, i).next_float() * 4 to the decide step alone.
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import oracle as orc_c1  # split-bound-4 factor generator + CPU port (baseline only)
         n1 = 65536
         hv1 = synthetic.gen_vertices(n1, n_pixels=n1)
         dv1 = {k: torch.from_numpy(a.view(np.int64) if a.dtype == np.uint64 else a).to(dev)
                for k, a in hv1.items() if k != "pixel"}
-        st1 = RrsStage(n1, nets, device=local)
-        o1 = st1.alloc_outputs(n1)
-        for _ in range(10):
-            st1.run(dv1, 2, strategy, rc=RateControl(), out=o1, sync=False)
-        torch.cuda.synchronize()
-        lat = []
-        for _ in range(50):
+
+        def graph_us(st, kind, nets_variant):
+            o = st.alloc_outputs(n1)
+            for _ in range(5):
+                st.run(dv1, 2, Strategy(kind), rc=RateControl(), out=o, sync=False)
+            torch.cuda.synchronize()
+            lat = []
+            for _ in range(30):
+                a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                st.run(dv1, 2, Strategy(kind), rc=RateControl(), out=o, sync=False)
+                z.record()
+                torch.cuda.synchronize()
+                lat.append(a.elapsed_time(z) * 1e3)
+            g = st.capture(dv1, 2, Strategy(kind), o, gain=RateControl().gain(), calls=100)
+            g.replay()
+            torch.cuda.synchronize()
             a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
-            st1.run(dv1, 2, strategy, rc=RateControl(), out=o1, sync=False)
+            for _ in range(10):
+                g.replay()
             z.record()
             torch.cuda.synchronize()
-            lat.append(a.elapsed_time(z) * 1e3)
-        g = st1.capture(dv1, 2, strategy, o1, gain=RateControl().gain(), calls=100)
-        for _ in range(2):
-            g.replay()
+            return statistics.median(lat), a.elapsed_time(z) * 1e3 / 1000
+
+        nrrs_nets = NeuralRrs(NeuralRrsConfig(variant=RrsVariant.Nrrs, seed=1)).randomize_for_benchmark()
+        st1 = RrsStage(n1, nrrs_nets, device=local)
+        single, per_call = graph_us(st1, StrategyKind.Nrrs, RrsVariant.Nrrs)
+        # decision-only: the split-bound-4 factors through the decide step (K-B) alone
+        q4 = torch.from_numpy(orc_c1.split_bound_factors(n1)).to(dev)
+        o1 = st1.alloc_outputs(n1)
+        o1.q_orig = torch.empty(n1, dtype=torch.float32, device=dev)
+        o1.u = torch.empty(n1, dtype=torch.float32, device=dev)
+        p1 = st1.params(2, Strategy(StrategyKind.Throughput), RateControl().gain())
+        from paper_2510_07868_b200.stage import vertex_soa as _vsoa
+        soa1, oc1 = _vsoa(dv1), o1.c()
+        ls1 = torch.zeros(1, dtype=torch.float64, device=dev)
+        tot1 = torch.zeros(1, dtype=torch.int64, device=dev)
+        st1.ctx.bind_stream()
+        _capi.check(st1.handle, lib.nrrs_gpu_stage_factors(st1.handle, ctypes.byref(soa1), n1, ctypes.byref(p1),
+                                                           ctypes.byref(oc1), ls1.data_ptr()))  # u for these keys
+        o1.q_orig.copy_(q4)
+        s4 = torch.tensor([float(q4.double().sum())], dtype=torch.float64, device=dev)
+        torch.cuda.synchronize()
+
+        def decide_only():
+            _capi.check(st1.handle, lib.nrrs_gpu_stage_decide(st1.handle, n1, ctypes.byref(p1), s4.data_ptr(), 1,
+                                                              ctypes.byref(oc1), tot1.data_ptr()))
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            st1.ctx.bind_stream()
+            decide_only()
+        torch.cuda.current_stream(dev).wait_stream(side)
+        torch.cuda.synchronize()
+        gd = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gd):
+            st1.ctx.bind_stream()
+            for _ in range(100):
+                decide_only()
+        st1.ctx.bind_stream()
+        gd.replay()
         torch.cuda.synchronize()
         a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         for _ in range(10):
-            g.replay()
+            gd.replay()
         z.record()
         torch.cuda.synchronize()
-        per_call_us = a.elapsed_time(z) * 1e3 / 1000
-        c1 = {"vertices": n1, "single_call_us": statistics.median(lat), "graph_us_per_call": per_call_us,
-              "graph_vertices_per_s": n1 / (per_call_us / 1e6), "calls_replayed": 1000}
+        dec_us = a.elapsed_time(z) * 1e3 / 1000
         st1.close()
+        # AID at C1 through the default routing and the opt-in fused single kernel
+        st2 = RrsStage(n1, nets, device=local)
+        _, aid_call = graph_us(st2, StrategyKind.AidNrrs, RrsVariant.Aid)
+        st2.close()
+        os.environ["NRRS_FUSED"] = "1"
+        try:
+            st3 = RrsStage(n1, nets, device=local)
+        finally:
+            del os.environ["NRRS_FUSED"]
+        _, aid_fused_call = graph_us(st3, StrategyKind.AidNrrs, RrsVariant.Aid)
+        st3.close()
+        # CPU port of the same NRRS step and decision-only step on this host
+        vc = orc_c1.gen_vertices(n1)
+        onn = orc_c1.OracleNets(orc_c1.VARIANT_NRRS, seed=1, randomize=True)
+        thr = orc_c1.threads_available()
+        cap1 = orc_c1.lib().orc_queue_capacity_for(n1)
+        t0 = time.perf_counter()
+        for _ in range(3):
+            orc_c1.rrs_stage(vc, 2, n1, cap1, orc_c1.NRRS, onn, gain=0.85, seed=0, threads=thr)
+        cpu_stage_s = (time.perf_counter() - t0) / 3
+        c1 = {"config": "configs[0]: NRRS normalized-RRS step, 65,536 synthetic vertices, random-init RRSNet, "
+                        "split bound 4 (SURVEY.md 8d C1)", "vertices": n1,
+              "nrrs_stage": {"graph_us_per_call": per_call, "single_call_us": single,
+                             "vertices_per_s": n1 / (per_call / 1e6),
+                             "hbm_gbs": (STAGE_READ + STAGE_WRITE + 8 * 0.85) * n1 / (per_call / 1e6) / 1e9},
+              "decision_only_split_bound4": {"graph_us_per_call": dec_us, "vertices_per_s": n1 / (dec_us / 1e6),
+                                             "kernel": "decide3 (normalize, gain, stochastic round, prefix, slots)"},
+              "aid_stage_graph_us_per_call": aid_call, "aid_fused_kernel_graph_us_per_call": aid_fused_call,
+              "cpu_port": {"nrrs_stage_vertices_per_s": n1 / cpu_stage_s, "cores": thr,
+                           "sample": "the same 65,536-vertex NRRS step (oracle port), mean of 3"},
+              "note": "launch-bound: ~2-3 kernels per call; the per-call floor of two dependent launches on "
+                      "this stream is the throughput-heuristic stage"}
 
     # ---- suffix side: reverse pass + TrainSample emission + k_i + Film update
     # over a synthetic 4-depth vertex tree in queue order, 2,073,600 depth-1 vertices ----
@@ -872,7 +954,8 @@ def main():
     if extra:
         line["strategies"] = extra
     if c1:
-        line["c1_launch_bound"] = c1
+        c1["nrrs_stage"]["hbm_frac"] = c1["nrrs_stage"]["hbm_gbs"] / hbm
+        line["configs0_c1"] = c1
     if suffix:
         line["suffix_stage"] = suffix
     if train:
