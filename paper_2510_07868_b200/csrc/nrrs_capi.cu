@@ -402,6 +402,7 @@ int nrrs_gpu_create(int device, nrrs_gpu_ctx **out) {
     ctx->env_no_level_kernel = std::getenv("NRRS_NO_LEVEL_KERNEL") != nullptr;
     ctx->env_fp32_tables = std::getenv("NRRS_FP32_TABLES") != nullptr;
     ctx->env_fused = std::getenv("NRRS_FUSED") != nullptr;
+    set_pdl(std::getenv("NRRS_NO_PDL") == nullptr);  // PDL launches of K-A / K-B / K-C by default
     if (const char *sc = std::getenv("NRRS_SYNC_CHUNKS"))
         ctx->env_sync_chunks = std::max(1, std::min(std::atoi(sc), kMaxHostChunks));
     if (const char *mc = std::getenv("NRRS_ASYNC_CHUNKS"))

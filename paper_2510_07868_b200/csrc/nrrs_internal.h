@@ -386,6 +386,7 @@ cudaError_t launch_compact(uint32_t words, CompactParams p, int num_sms, cudaStr
 cudaError_t launch_grid_copies(const float *src, void *dst, uint32_t levels, uint32_t T, uint32_t copies,
                                uint32_t dense_mask, bool half, cudaStream_t stream);
 cudaError_t launch_max_abs(const float *x, uint64_t n, unsigned int *out_bits, cudaStream_t stream);
+void set_pdl(bool on);  // programmatic dependent launches for K-A / K-B / K-C (NRRS_PDL)
 // fused AID stage (nrrs_fused.cu)
 size_t aid_stage_smem_bytes(uint32_t blob_bytes, uint32_t table_size);
 uint32_t aid_stage_ring_floats2(uint32_t levels, uint32_t ctas);
