@@ -312,6 +312,7 @@ cudaError_t launch_grid_levels(const GridLevelParams &p, int num_sms, cudaStream
 
 __global__ void __launch_bounds__(kInferThreads) infer_kernel(InferParams p) {
     __shared__ InferSmemHeader hdr_s;
+    pdl_trigger();
     InferSmemHeader *hdr = &hdr_s;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint64_t n = p.n;
@@ -506,6 +507,7 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    pdl_trigger();  // K-B (PDL launch) may start on SMs this kernel leaves
     const uint32_t tmem_base = st->tmem_base;
     const uint32_t lane_base = tmem_base + ((uint32_t)((warp & 3) * 32) << 16);
     if (kTiming && p.dbg && tid == 0)
@@ -1450,13 +1452,15 @@ __global__ void __launch_bounds__(kD3T, 1) decide3_kernel(DecideParams p) {
     __shared__ Scan3Smem sm;
     extern __shared__ uint4 kq[];  // [group i][thread]: the thread's counts, parked between scan and writes
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    pdl_trigger();
+    // the factor kernel's q / u / rank sums -- and a previous decide launch on this stream must be
+    // done before this launch claims tiles from the shared LaunchSync (back-to-back stage calls)
+    pdl_wait();
     if (tid == 0)
         sm.tile = claim_tile_epoch(p.sync, &sm.epoch);
     __syncthreads();
     const uint32_t tile = sm.tile, epoch = sm.epoch;
     stamp(p.dbg, tile, 0);
-    pdl_trigger();
-    pdl_wait();  // q / u / rank sums of the factor kernel
     // this tile's items end at min(n, (tile + 1) * tile_items): warps past a short tile idle
     const uint32_t n = min((uint32_t)p.n, (tile + 1u) * p.tile_items);
     const uint32_t wbase = tile * p.tile_items + (uint32_t)warp * kD3Warp + 4u * (uint32_t)lane;
@@ -1671,12 +1675,12 @@ __global__ void __launch_bounds__(kD3T, 1) compact3_kernel(CompactParams p) {
     __shared__ Scan3Smem sm;
     __shared__ uint2 cbuf[kD3T / 32 * 128];  // per-warp staging of one item group's kept records
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    pdl_wait();  // the records and count of the producing kernel (and any earlier compaction)
     if (tid == 0)
         sm.tile = claim_tile_epoch(p.sync, &sm.epoch);
     __syncthreads();
     const uint32_t tile = sm.tile, epoch = sm.epoch;
     stamp(p.dbg, tile, 0);
-    pdl_wait();  // the records and count of the producing kernel
     uint64_t count64 = p.count;
     if (p.count_in) {
         const uint64_t c = *p.count_in;
