@@ -633,3 +633,66 @@ def test_set_weights_from_device_blocks_matches_host_upload(variant):
     assert ra.spawned == rb.spawned and ra.f_norm == rb.f_norm
     a.close()
     b.close()
+
+
+def test_back_to_back_decide_and_compact_graph_replay():
+    """Consecutive decide (K-B) and compaction (K-C) launches share their LaunchSync; under
+    programmatic dependent launch a launch may start before the previous one ends, so tiles are
+    claimed only after griddepcontrol.wait.  100 decide-only calls and 100 compactions replayed
+    from CUDA graphs give the direct call's outputs (and finish)."""
+    import ctypes as C
+    from paper_2510_07868_b200 import _capi
+    from paper_2510_07868_b200.stage import vertex_soa
+    n = 65_536
+    v = to_dev(orc.gen_vertices(n))
+    st = _stage(n)
+    lib = _capi.lib()
+    out = st.alloc_outputs(n, full=True)
+    p = st.params(2, Strategy(StrategyKind.Throughput), 0.85)
+    soa, oc = vertex_soa(v), out.c()
+    ls = torch.zeros(1, dtype=torch.float64, device="cuda")
+    tot = torch.zeros(1, dtype=torch.int64, device="cuda")
+    st.ctx.bind_stream()
+    _capi.check(st.handle, lib.nrrs_gpu_stage_factors(st.handle, C.byref(soa), n, C.byref(p), C.byref(oc),
+                                                      ls.data_ptr()))
+    out.q_orig.copy_(torch.from_numpy(orc.split_bound_factors(n)).cuda())
+    s4 = torch.tensor([float(out.q_orig.double().sum())], dtype=torch.float64, device="cuda")
+    used = (torch.arange(st.capacity, device="cuda") % 7 != 0).to(torch.uint8)
+    comp = torch.empty((st.capacity, 2), dtype=torch.int32, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+
+    def decide():
+        _capi.check(st.handle, lib.nrrs_gpu_stage_decide(st.handle, n, C.byref(p), s4.data_ptr(), 1, C.byref(oc),
+                                                         tot.data_ptr()))
+
+    def compact():
+        _capi.check(st.handle, lib.nrrs_gpu_compact_dev(st.handle, out.slots.data_ptr(), used.data_ptr(),
+                                                        tot.data_ptr(), st.capacity, 2, comp.data_ptr(),
+                                                        cnt.data_ptr()))
+    decide()
+    compact()
+    torch.cuda.synchronize()
+    ref_slots, ref_comp, ref_cnt = _np(out.slots).copy(), _np(comp).copy(), int(cnt.item())
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        st.ctx.bind_stream()
+        decide()
+        compact()
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        st.ctx.bind_stream()
+        for _ in range(100):
+            decide()
+        for _ in range(100):
+            compact()
+    st.ctx.bind_stream()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(_np(out.slots), ref_slots)
+    np.testing.assert_array_equal(_np(comp)[:ref_cnt], ref_comp[:ref_cnt])
+    assert int(cnt.item()) == ref_cnt
+    st.close()
