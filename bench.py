@@ -949,6 +949,19 @@ def main():
             "achieved": gu * n / infer_avg, "peak": GATHER_CEILING_PER_S,
             "frac": gu * n / infer_avg / GATHER_CEILING_PER_S, "units_per_vertex": gu,
             "peak_source": "measured, profiles/r01_microbench_gather_bw.txt"}
+    ipv = prof.get("instructions_per_vertex") if args.variant == "aid" else None
+    if ipv:
+        # HBM does not bind this stage: every kernel is issue-bound (profiles/r02_stage_kernels.txt);
+        # the instruction-issue ceiling = 4 warp-instructions per clock per SM at the max SM clock
+        wi = sum(v for k, v in ipv.items() if not k.startswith("_"))
+        sm_hz = peaks.get("sm_max_mhz", 1965.0) * 1e6
+        issue_peak = 4.0 * 148 * sm_hz / wi
+        line["issue_roofline"] = {
+            "bound": "instruction issue", "unit": "vertices/s", "achieved": value, "peak": issue_peak,
+            "frac": value / issue_peak, "warp_instructions_per_vertex": wi,
+            "per_kernel": {k: v for k, v in ipv.items() if not k.startswith("_")},
+            "peak_source": "4 warp-instructions/clk/SM x 148 SMs x MEASURED_PEAKS sm_max_mhz; instruction counts: "
+                           "smsp__inst_executed.sum of the ncu capture (profiles/ncu_summary.json)"}
     if e2e:
         line["e2e"] = e2e
     if extra:
