@@ -1094,7 +1094,11 @@ __global__ void __launch_bounds__(GM * 128, 1) infer_aid_fused_kernel(InferParam
         // ---- 4-layer chain ----
 #pragma unroll 1
         for (int l = 0; l < 4; ++l) {
+#if NRRS_AID_MMA_HINT
+            mbar_wait_sleep(&st->mma_bar[g], phase, NRRS_AID_MMA_HINT);
+#else
             mbar_wait(&st->mma_bar[g], phase);
+#endif
             phase ^= 1u;
             tc_fence_after();
             const uint32_t boff = st->bias[1][l];
@@ -1925,6 +1929,9 @@ size_t infer_smem_bytes(int kind, const InferParams &p) {
 #endif
 #ifndef NRRS_AID_FUSED
 #define NRRS_AID_FUSED 8  // K-A over level planes as NRRS_AID_FUSED self-contained groups
+#endif
+#ifndef NRRS_AID_MMA_HINT
+#define NRRS_AID_MMA_HINT 0  // ns suspend hint of the AID K-A MMA-completion wait (0: plain try_wait loop)
 #endif
 template <int KIND>
 static cudaError_t launch_ws_cfg(const InferParams &p, int num_sms, cudaStream_t stream, uint32_t *grid_out) {
