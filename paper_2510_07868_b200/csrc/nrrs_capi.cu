@@ -173,6 +173,7 @@ struct nrrs_gpu_ctx {
     nrrs_grid_spec spec{};
     GridDev grid{}, grid_rrs{};  // StatNet / AID RRSNet grids (same spec, own pair-copy counts)
     float *d_stat_grid = nullptr;
+    float *d_stat_fm = nullptr;  // feature-major copy [level][feature][T] of the StatNet grid (K-A0, fp32 kinds)
     void *d_rrs_grid = nullptr;
     bool rrs_half = false;  // AID grid stored as fp16 (precision)
     double rrs_half_probe_err = -1.0;  // error-budget probe of the fp16 AID tables (< 0: not run)
@@ -430,7 +431,7 @@ int nrrs_gpu_destroy(nrrs_gpu_ctx *ctx) {
     cudaStreamSynchronize(ctx->stream);
     void *ptrs[] = {ctx->d_stat_grid, ctx->d_rrs_grid, ctx->blob_stat.ptr, ctx->blob_rrs.ptr, ctx->blob_both.ptr,
                     ctx->d_q, ctx->d_u, ctx->d_parts, ctx->d_part_counts, ctx->d_tile_state, ctx->d_ctile_state,
-                    ctx->d_misc, ctx->d_res, ctx->d_sum, ctx->d_total, ctx->d_sync, ctx->d_etile_state, ctx->d_hist, ctx->d_tws, ctx->d_tloss, ctx->d_tpart, ctx->d_gsc, ctx->d_gsc_tmp, ctx->d_feat, ctx->d_ring, ctx->d_fsync, ctx->d_fstate, ctx->st.p01, ctx->st.wo01, ctx->st.rough,
+                    ctx->d_misc, ctx->d_res, ctx->d_sum, ctx->d_total, ctx->d_sync, ctx->d_etile_state, ctx->d_hist, ctx->d_tws, ctx->d_tloss, ctx->d_tpart, ctx->d_gsc, ctx->d_gsc_tmp, ctx->d_stat_fm, ctx->d_feat, ctx->d_ring, ctx->d_fsync, ctx->d_fstate, ctx->st.p01, ctx->st.wo01, ctx->st.rough,
                     ctx->st.weight, ctx->st.ipix, ctx->st.key, ctx->st.q_norm, ctx->st.q_real, ctx->st.q_orig,
                     ctx->st.u, ctx->st.k, ctx->st.offset, ctx->st.slots, ctx->st.decided};
     for (void *p : ptrs)
@@ -657,6 +658,14 @@ static int set_weights_impl(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w, bool d
     };
     const uint32_t stat_copies = usable(kPairCopiesF32), rrs_copies = usable(half ? kPairCopies : kPairCopiesF32);
     rc = upload_grid(ctx->d_stat_grid, w->stat_grid, grid_len, false, stat_copies);
+    if (!rc) {
+        if (ctx->d_stat_fm)
+            cudaFree(ctx->d_stat_fm);
+        ctx->d_stat_fm = nullptr;
+        CK(ctx, cudaMalloc(&ctx->d_stat_fm, grid_len * sizeof(float)));
+        CK(ctx, launch_feature_major(ctx->d_stat_grid, ctx->d_stat_fm, (uint32_t)g.levels, (uint32_t)T, ctx->stream));
+        CK(ctx, cudaStreamSynchronize(ctx->stream));
+    }
     if (!rc)
         rc = upload_grid(ctx->d_rrs_grid, w->rrs_grid, rrs_grid_len, half, rrs_copies);
     ctx->rrs_half = half;
@@ -762,8 +771,21 @@ static int prepare_level_planes(nrrs_gpu_ctx *ctx, int kind, InferParams &ip, ui
     *n_kernels = 1;
     ip.feat = nullptr;
     ip.feat_stride = 0;
-    if (kind != kKindAid || !ctx->rrs_half || ctx->env_no_level_kernel ||
-        (uint64_t)ctx->grid_rrs.table_size * 4u > kLevelSmemMax || ip.n == 0)
+    ip.stat_fm = nullptr;
+    if (ctx->env_no_level_kernel || ip.n == 0)
+        return NRRS_OK;
+    if ((kind == kKindAdrrs || kind == kKindStats || kind == kKindNrrs) && ctx->d_stat_fm &&
+        (uint64_t)ctx->grid.table_size * 4u <= kLevelSmemMax && ctx->grid.levels <= 8) {
+        // fp32 StatNet grid: one (level, feature) table per K-A0 CTA, 2 * levels float planes
+        const uint64_t stride = (ip.n + 31) & ~31ull;
+        CK(ctx, grow(ctx->d_feat, ctx->cap_feat, stride * (uint64_t)ctx->grid.levels));
+        ip.feat = ctx->d_feat;
+        ip.feat_stride = stride;
+        ip.stat_fm = ctx->d_stat_fm;
+        *n_kernels = 2;
+        return NRRS_OK;
+    }
+    if (kind != kKindAid || !ctx->rrs_half || (uint64_t)ctx->grid_rrs.table_size * 4u > kLevelSmemMax)
         return NRRS_OK;
     const uint64_t stride = (ip.n + 31) & ~31ull;
     CK(ctx, grow(ctx->d_feat, ctx->cap_feat, stride * (uint64_t)ctx->grid_rrs.levels));

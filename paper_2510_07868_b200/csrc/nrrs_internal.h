@@ -106,8 +106,9 @@ struct InferParams {
     uint32_t rrs_half;
     GridDev grid;        // StatNet grid (fp32)
     GridDev grid_rrs;    // AID RRSNet grid (same spec; its own number of pair copies)
-    float2 *feat;          // AID with fp16 tables in smem reach: K-A0 level planes [levels][feat_stride]
+    float2 *feat;          // K-A0 planes: AID [levels][feat_stride] float2; StatNet kinds [levels*2][feat_stride] float
     uint64_t feat_stride;
+    const float *stat_fm;  // feature-major copy of the fp32 StatNet grid (K-A0 for ADRRS-NN / stats / NRRS)
     const uint8_t *blob;
     uint32_t blob_bytes;
     KernelNets nets;
@@ -366,10 +367,12 @@ size_t infer_smem_bytes(int kind, const InferParams &p);
 struct GridLevelParams {
     const float *p01;
     uint64_t n;
-    const void *table;  // fp16 reference layout [level][T] half2 (copy 0 of the AID grid)
+    const void *table;  // fp16 reference layout [level][T] half2 (copy 0 of the AID grid), or with f32:
+                        // the fp32 StatNet grid feature-major [level][feature][T]
     GridDev g;
-    float2 *feat;
+    float2 *feat;       // planes: [level][stride] float2, or with f32 [level * 2 + feature][stride] float
     uint64_t feat_stride;
+    uint32_t f32;
 };
 constexpr uint32_t kLevelSmemMax = 150u * 1024u;  // table bytes; + 72 KB of staged p01 blocks <= 227 KB
 cudaError_t launch_grid_levels(const GridLevelParams &p, int num_sms, cudaStream_t stream);
@@ -386,6 +389,7 @@ cudaError_t launch_compact(uint32_t words, CompactParams p, int num_sms, cudaStr
 cudaError_t launch_grid_copies(const float *src, void *dst, uint32_t levels, uint32_t T, uint32_t copies,
                                uint32_t dense_mask, bool half, cudaStream_t stream);
 cudaError_t launch_max_abs(const float *x, uint64_t n, unsigned int *out_bits, cudaStream_t stream);
+cudaError_t launch_feature_major(const float *src, float *dst, uint32_t levels, uint32_t T, cudaStream_t stream);
 void set_pdl(bool on);  // programmatic dependent launches for K-A / K-B / K-C (NRRS_PDL)
 // fused AID stage (nrrs_fused.cu)
 size_t aid_stage_smem_bytes(uint32_t blob_bytes, uint32_t table_size);

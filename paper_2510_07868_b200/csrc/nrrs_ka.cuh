@@ -105,6 +105,48 @@ __device__ __forceinline__ float2 level_encode(const uint8_t *tab, const LevelCo
     return upk2(fadd2(acc[0], acc[1]));
 }
 
+// One feature of one level from a shared-memory fp32 table (the StatNet grid's feature-major copy):
+// the same cell, weights and corner indices as level_encode, 8 scalar loads and FMAs.
+__device__ __forceinline__ float level_encode_f32(const uint8_t *tab, const LevelConsts &c, float px, float py,
+                                                  float pz) {
+    const float fx = __saturatef(px) * c.resf, fy = __saturatef(py) * c.resf, fz = __saturatef(pz) * c.resf;
+    const uint32_t cx = min((uint32_t)fx, c.res - 1u);
+    const uint32_t cy = min((uint32_t)fy, c.res - 1u);
+    const uint32_t cz = min((uint32_t)fz, c.res - 1u);
+    const float tx = fx - (float)cx, ty = fy - (float)cy, tz = fz - (float)cz;
+    const float wx[2] = {1.0f - tx, tx}, wy[2] = {1.0f - ty, ty}, wz[2] = {1.0f - tz, tz};
+    uint32_t idx4[8];
+    if (c.dense) {
+        const uint32_t b4 = ((cx * c.nn + cy) * c.nn + cz) * 4u;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            idx4[k] = b4 + c.doff4[k];
+    } else {
+        const uint32_t hx0 = cx * 4u, hx1 = hx0 + 4u;
+        const uint32_t hy0 = cy * (2654435761u * 4u), hy1 = hy0 + 2654435761u * 4u;
+        const uint32_t hz0 = cz * (805459861u * 4u), hz1 = hz0 + 805459861u * 4u;
+        const uint32_t hyz[4] = {hy0 ^ hz0, hy1 ^ hz0, hy0 ^ hz1, hy1 ^ hz1};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            idx4[2 * q] = lop3_xor_and(hx0, hyz[q], c.m4);
+            idx4[2 * q + 1] = lop3_xor_and(hx1, hyz[q], c.m4);
+        }
+    }
+    float v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        v[k] = *reinterpret_cast<const float *>(tab + idx4[k]);
+    float a0 = 0.0f, a1 = 0.0f;  // oz = 0 / 1 (two short FMA chains)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {  // corners (0, oy, oz), (1, oy, oz); q = oy + 2 oz
+        const float wyz = wy[q & 1] * wz[q >> 1];
+        float &acc = (q >> 1) ? a1 : a0;
+        acc = fmaf(wx[0] * wyz, v[2 * q], acc);
+        acc = fmaf(wx[1] * wyz, v[2 * q + 1], acc);
+    }
+    return a0 + a1;
+}
+
 
 namespace ws {
 

@@ -164,14 +164,19 @@ constexpr int kLevelThreads = 1024;
 constexpr uint32_t kLevelPer = NRRS_LEVEL_PER_THREAD;             // vertices per thread per block
 constexpr uint32_t kLevelBlock = kLevelPer * kLevelThreads;  // staged p01 block (12 B per vertex), double-buffered
 
+// kF32: the fp32 StatNet grid, one (level, feature) table per CTA role (128 KB of fp32 at the default
+// 2^15 entries, from the feature-major copy [level][feature][entry]); planes are then one float per
+// (level, feature) and vertex.  Otherwise the fp16 AID grid, one level (both features) per role.
+template <bool kF32>
 __global__ void __launch_bounds__(kLevelThreads, 1) grid_level_kernel(GridLevelParams p) {
     extern __shared__ __align__(128) uint8_t lvl_smem[];
     __shared__ uint64_t bar[1];  // table landed
     pdl_trigger();  // K-A may start its prologue on SMs this kernel leaves
     const GridDev &g = p.g;
-    const uint32_t L = (uint32_t)g.levels;
-    const uint32_t l = blockIdx.x % L, q = blockIdx.x / L;
-    const uint32_t nq = (gridDim.x - l + L - 1) / L;  // CTAs serving level l
+    const uint32_t L = (uint32_t)g.levels, R = kF32 ? 2u * L : L;  // CTA roles
+    const uint32_t role = blockIdx.x % R, q = blockIdx.x / R;
+    const uint32_t l = kF32 ? role >> 1 : role;
+    const uint32_t nq = (gridDim.x - role + R - 1) / R;  // CTAs serving this role
     const uint32_t res = (uint32_t)g.base_resolution << l;
     const uint32_t nn = res + 1u;
     const bool dense = (g.dense_mask >> l) & 1u;
@@ -184,7 +189,7 @@ __global__ void __launch_bounds__(kLevelThreads, 1) grid_level_kernel(GridLevelP
         mbar_init(&bar[0], 1);
         fence_barrier_init();
         mbar_arrive_expect_tx(&bar[0], bytes);
-        const uint8_t *src = reinterpret_cast<const uint8_t *>(p.table) + (uint64_t)l * tab_bytes;
+        const uint8_t *src = reinterpret_cast<const uint8_t *>(p.table) + (uint64_t)role * tab_bytes;
         for (uint32_t off = 0; off < bytes; off += 32768u)
             bulk_g2s(lvl_smem + off, src + off, bytes - off < 32768u ? bytes - off : 32768u, &bar[0]);
     }
@@ -198,7 +203,8 @@ __global__ void __launch_bounds__(kLevelThreads, 1) grid_level_kernel(GridLevelP
 #pragma unroll
     for (int k = 0; k < 8; ++k)
         c.doff4[k] = (((k & 1) * nn + ((k >> 1) & 1)) * nn + (k >> 2)) * 4u;
-    float2 *out = p.feat + (uint64_t)l * p.feat_stride;
+    float2 *out = p.feat + (uint64_t)role * p.feat_stride;
+    float *out1 = reinterpret_cast<float *>(p.feat) + (uint64_t)role * p.feat_stride;
     // kLevelPer vertices per thread per block (t, t + 1024, ...); the next block's p01 is loaded
     // into registers before this block's gathers, so its L2 round trip hides behind them (no
     // shared-memory staging and no barrier in the loop: every thread owns its own vertices).
@@ -229,15 +235,28 @@ __global__ void __launch_bounds__(kLevelThreads, 1) grid_level_kernel(GridLevelP
         }
         if (s + kLevelBlock < j1)
             load_block(s + kLevelBlock);
-        float2 r[kLevelPer];
+        if constexpr (kF32) {
+            float r[kLevelPer];
 #pragma unroll
-        for (int u = 0; u < (int)kLevelPer; ++u)
-            r[u] = level_encode(lvl_smem, c, cur[u][0], cur[u][1], cur[u][2]);
+            for (int u = 0; u < (int)kLevelPer; ++u)
+                r[u] = level_encode_f32(lvl_smem, c, cur[u][0], cur[u][1], cur[u][2]);
 #pragma unroll
-        for (int u = 0; u < (int)kLevelPer; ++u) {
-            const uint64_t j = s + threadIdx.x + (uint64_t)u * kLevelThreads;
-            if (j < j1)
-                __stcs(out + j, r[u]);
+            for (int u = 0; u < (int)kLevelPer; ++u) {
+                const uint64_t j = s + threadIdx.x + (uint64_t)u * kLevelThreads;
+                if (j < j1)
+                    __stcs(out1 + j, r[u]);
+            }
+        } else {
+            float2 r[kLevelPer];
+#pragma unroll
+            for (int u = 0; u < (int)kLevelPer; ++u)
+                r[u] = level_encode(lvl_smem, c, cur[u][0], cur[u][1], cur[u][2]);
+#pragma unroll
+            for (int u = 0; u < (int)kLevelPer; ++u) {
+                const uint64_t j = s + threadIdx.x + (uint64_t)u * kLevelThreads;
+                if (j < j1)
+                    __stcs(out + j, r[u]);
+            }
         }
     }
 }
@@ -295,19 +314,25 @@ cudaError_t launch_sharded_clip(const unsigned long long *totals, int nranks, in
     return cudaGetLastError();
 }
 
-cudaError_t launch_grid_levels(const GridLevelParams &p, int num_sms, cudaStream_t stream) {
-    const uint32_t L = (uint32_t)p.g.levels;
+template <bool kF32>
+static cudaError_t launch_grid_levels_t(const GridLevelParams &p, int num_sms, cudaStream_t stream) {
+    const uint32_t R = (kF32 ? 2u : 1u) * (uint32_t)p.g.levels;
     const size_t smem = (size_t)p.g.table_size * 4u;
-    cudaError_t e = cudaFuncSetAttribute(grid_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(grid_level_kernel<kF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
         return e;
-    // one CTA per SM; every level gets floor or ceil of num_sms / L CTAs
-    uint64_t grid = (uint64_t)num_sms < L ? L : (uint64_t)num_sms;
-    const uint64_t max_useful = L * ((p.n + kLevelThreads - 1) / kLevelThreads);
+    // one CTA per SM; every role (level, or level x feature) gets floor or ceil of num_sms / R CTAs
+    uint64_t grid = (uint64_t)num_sms < R ? R : (uint64_t)num_sms;
+    const uint64_t max_useful = R * ((p.n + kLevelThreads - 1) / kLevelThreads);
     if (grid > max_useful)
-        grid = max_useful < L ? L : max_useful;
-    grid_level_kernel<<<(uint32_t)grid, kLevelThreads, smem, stream>>>(p);
+        grid = max_useful < R ? R : max_useful;
+    grid_level_kernel<kF32><<<(uint32_t)grid, kLevelThreads, smem, stream>>>(p);
     return cudaGetLastError();
+}
+
+cudaError_t launch_grid_levels(const GridLevelParams &p, int num_sms, cudaStream_t stream) {
+    return p.f32 ? launch_grid_levels_t<true>(p, num_sms, stream) : launch_grid_levels_t<false>(p, num_sms, stream);
 }
 
 __global__ void __launch_bounds__(kInferThreads) infer_kernel(InferParams p) {
@@ -1219,6 +1244,357 @@ __global__ void __launch_bounds__(GM * 128, 1) infer_aid_fused_kernel(InferParam
     }
 }
 
+// ===========================================================================
+// K-A over fp32 feature planes for the StatNet-grid kinds (ADRRS-NN, stats, NRRS): the same
+// self-contained-group shape as infer_aid_fused_kernel, fed by grid_level_kernel<true> (one
+// (level, feature) table of the fp32 StatNet grid per CTA from shared memory) instead of L2 gathers.
+// Layer-0 input: the 16 StatNet grid features + build_stat_tail (networks.cpp:131-135).  ADRRS-NN /
+// stats end at the StatNet head (networks.cpp:252-264, rrs.hpp:56-61); NRRS continues with
+// build_nrrs_input (networks.cpp:137-147) and the RRSNet chain (8 MMA layers per tile).
+// ===========================================================================
+template <int KIND>
+__global__ void __launch_bounds__(8 * 128, 1) infer_stat_planes_kernel(InferParams p) {
+    constexpr int GM = 8;
+    constexpr int kNL = KIND == kKindNrrs ? 8 : 4;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem_w = smem_raw;
+    ws::SmemTail *st = reinterpret_cast<ws::SmemTail *>(smem_raw + ((p.blob_bytes + 127u) & ~127u));
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int kThreads = GM * 128;
+    {
+        const uint4 *src = reinterpret_cast<const uint4 *>(p.blob);
+        uint4 *dst = reinterpret_cast<uint4 *>(smem_w);
+        for (uint32_t i = tid; i < p.blob_bytes / 16u; i += kThreads)
+            dst[i] = __ldg(src + i);
+    }
+    if (tid == 0) {
+        for (int net = 0; net < (KIND == kKindNrrs ? 2 : 1); ++net) {
+            const NetDesc &nd = net == 0 ? p.nets.stat : p.nets.rrs;
+            for (int l = 0; l < 4; ++l) {
+                const LayerDesc &Ld = nd.layer[l];
+                st->idesc_n[net][l] = make_idesc_f16(Ld.N);
+                st->idesc_2n[net][l] = make_idesc_f16(2u * Ld.N);
+                st->nslices[net][l] = (uint32_t)Ld.K / 16u;
+                st->bias[net][l] = Ld.bias;
+                const uint32_t sbo = (uint32_t)Ld.K * 16u;
+                for (int kk = 0; kk < 2; ++kk) {
+                    st->wdesc[net][l][kk] = make_smem_desc(smem_u32(smem_w + Ld.w_hi) + 256u * kk, 128u, sbo);
+                    st->wdesc_lo[net][l][kk] = make_smem_desc(
+                        smem_u32(smem_w + Ld.w_hi) + 256u * kk + ((uint32_t)Ld.N / 8u) * sbo, 128u, sbo);
+                }
+            }
+        }
+        for (int q = 0; q < GM; ++q) {
+            mbar_init(&st->mma_bar[q], 1);
+            mbar_init(&st->full[q], 1);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 0)
+        tmem_alloc(&st->tmem_base, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    pdl_trigger();
+    pdl_wait();  // the feature planes of grid_level_kernel<true>
+    const uint32_t tmem_base = st->tmem_base;
+    const uint32_t lane_base = tmem_base + ((uint32_t)((warp & 3) * 32) << 16);
+    const int g = tid >> 7, r = tid & 127;
+    const bool issuer = r == 0;
+    const uint32_t bar_id = 1u + (uint32_t)g;
+    const uint32_t col_d = 64u * (uint32_t)g, col_a = col_d + 32u;
+
+    const uint64_t n = p.n;
+    const uint64_t num_tiles = (n + kTileM - 1) / kTileM;
+    const uint64_t t_begin = num_tiles * blockIdx.x / gridDim.x;
+    const uint64_t t_end = num_tiles * (blockIdx.x + 1) / gridDim.x;
+    const uint32_t T = (uint32_t)(t_end - t_begin);
+    double my_sum = 0.0;
+    uint32_t my_nonfinite = 0, my_bc = 0;
+    const bool depth1 = p.depth == 1u;
+    const int nfeat = 2 * p.grid.levels;  // fp32 planes: one per (level, feature)
+    constexpr bool kNeedIpx = KIND != kKindStats;
+    uint32_t phase = 0;
+    uint8_t *in_s = smem_raw + aid_in_offset(p.blob_bytes) + (uint32_t)g * kAidInBytes;
+    const bool in_bulk = p.in_bulk != 0u;
+    const uint64_t full_tiles = n / kTileM;
+    uint32_t in_phase = 0;
+    const float *planes = reinterpret_cast<const float *>(p.feat);
+    auto issue_in = [&](uint64_t tile) {
+        const uint64_t j0 = tile * kTileM;
+        const uint32_t ipx_bytes = !kNeedIpx ? 0u : (p.i_pixel ? 12u * kTileM : 4u * kTileM);
+        mbar_arrive_expect_tx(&st->full[g], (uint32_t)nfeat * 4u * kTileM + 12u * kTileM + 8u * kTileM + ipx_bytes +
+                                                4u * kTileM + 8u * kTileM);
+        for (int q = 0; q < nfeat; ++q)
+            bulk_g2s(in_s + 4u * kTileM * q, planes + (uint64_t)q * p.feat_stride + j0, 4u * kTileM, &st->full[g]);
+        bulk_g2s(in_s + kAidInWeight, p.weight + 3 * j0, 12u * kTileM, &st->full[g]);
+        bulk_g2s(in_s + kAidInWo, p.wo01 + 2 * j0, 8u * kTileM, &st->full[g]);
+        if (kNeedIpx) {
+            if (p.i_pixel)
+                bulk_g2s(in_s + kAidInIpx, p.i_pixel + 3 * j0, ipx_bytes, &st->full[g]);
+            else
+                bulk_g2s(in_s + kAidInIpx, p.pixel + j0, ipx_bytes, &st->full[g]);
+        }
+        bulk_g2s(in_s + kAidInRough, p.roughness + j0, 4u * kTileM, &st->full[g]);
+        bulk_g2s(in_s + kAidInKey, p.path_key + j0, 8u * kTileM, &st->full[g]);
+    };
+    if (in_bulk && r == 32 && (uint32_t)g < T && t_begin + (uint32_t)g < full_tiles)
+        issue_in(t_begin + (uint32_t)g);
+
+    for (uint32_t i = (uint32_t)g; i < T; i += GM) {
+        const uint64_t j = (t_begin + i) * kTileM + r;
+        const bool valid = j < n;
+        const bool staged = in_bulk && t_begin + i < full_tiles;
+        float f[16];
+        float wx = 0, wy = 0, wz = 0, wox = 0, woy = 0, ia = 0, ib = 0, ic = 0, rough = 0;
+        uint64_t key = 0;
+        if (staged) {
+            mbar_wait(&st->full[g], in_phase);
+            in_phase ^= 1u;
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                f[q] = q < nfeat ? reinterpret_cast<const float *>(in_s + 4u * kTileM * q)[r] : 0.0f;
+            const float *w3 = reinterpret_cast<const float *>(in_s + kAidInWeight) + 3 * r;
+            wx = w3[0]; wy = w3[1]; wz = w3[2];
+            const float2 wo = reinterpret_cast<const float2 *>(in_s + kAidInWo)[r];
+            wox = wo.x; woy = wo.y;
+            if (kNeedIpx) {
+                if (p.i_pixel) {
+                    const float *i3 = reinterpret_cast<const float *>(in_s + kAidInIpx) + 3 * r;
+                    ia = i3[0]; ib = i3[1]; ic = i3[2];
+                } else {
+                    const uint64_t px_idx = reinterpret_cast<const uint32_t *>(in_s + kAidInIpx)[r];
+                    ia = __ldg(p.i_acc + 3 * px_idx); ib = __ldg(p.i_acc + 3 * px_idx + 1); ic = __ldg(p.i_acc + 3 * px_idx + 2);
+                }
+            }
+            rough = reinterpret_cast<const float *>(in_s + kAidInRough)[r];
+            key = reinterpret_cast<const uint64_t *>(in_s + kAidInKey)[r];
+        } else {
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                f[q] = valid && q < nfeat ? __ldcs(planes + (uint64_t)q * p.feat_stride + j) : 0.0f;
+            if (valid) {
+                wx = __ldg(p.weight + 3 * j); wy = __ldg(p.weight + 3 * j + 1); wz = __ldg(p.weight + 3 * j + 2);
+                wox = __ldg(p.wo01 + 2 * j); woy = __ldg(p.wo01 + 2 * j + 1);
+                if (kNeedIpx) {
+                    if (p.i_pixel) {
+                        ia = __ldg(p.i_pixel + 3 * j); ib = __ldg(p.i_pixel + 3 * j + 1); ic = __ldg(p.i_pixel + 3 * j + 2);
+                    } else {
+                        const uint64_t px_idx = __ldg(p.pixel + j);
+                        ia = __ldg(p.i_acc + 3 * px_idx); ib = __ldg(p.i_acc + 3 * px_idx + 1); ic = __ldg(p.i_acc + 3 * px_idx + 2);
+                    }
+                }
+                rough = __ldg(p.roughness + j);
+                key = KIND != kKindStats ? __ldg(p.path_key + j) : 0ull;
+            }
+        }
+        const bool active = valid && (p.gate ? (!depth1 && luminance(wx, wy, wz) > 0.0f) : true);
+        // ---- layer-0 input: encode_stat_inputs (networks.cpp:206-217) in the packed K order ----
+        float x0[16], x1[16];  // [0,16): grid 0-7 | ob4(wo.x), ob4(wo.y); [16,32): grid 8-15 | ob8(remap(r))
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            x0[q] = f[q];
+            x1[q] = f[8 + q];
+        }
+        one_blob_fast<4>(wox, x0 + 8);
+        one_blob_fast<4>(woy, x0 + 12);
+        one_blob_fast<8>(remap_fast(rough), x1 + 8);
+        if (!valid) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                x0[q] = x1[q] = 0.0f;
+        }
+        ws::ws_store_a16(lane_base, col_a, 0, x0);
+        ws::ws_store_a16(lane_base, col_a, 1, x1);
+        tmem_wait_st();
+        tc_fence_before();
+        named_bar_sync(bar_id, 128);
+        if (issuer)
+            ws::ws_issue(st, 0, 0, tmem_base, col_a, col_d, &st->mma_bar[g]);
+        if (r == 32 && in_bulk && i + GM < T && t_begin + i + GM < full_tiles) {
+            fence_proxy_async_smem();
+            issue_in(t_begin + i + GM);
+        }
+        // ---- MMA chain: StatNet (layers 0-3), then for NRRS the RRSNet (4-7) ----
+#pragma unroll 1
+        for (int l = 0; l < kNL; ++l) {
+            mbar_wait(&st->mma_bar[g], phase);
+            phase ^= 1u;
+            tc_fence_after();
+            const int lyr = l & 3;
+            const int net = l >= 4 ? 1 : 0;
+            const uint32_t boff = st->bias[net][lyr];
+            const float *bias = boff == kNoBias ? nullptr : reinterpret_cast<const float *>(smem_w + boff);
+            if (lyr < 3) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    float z[16];
+                    ws::ws_load_sum16(lane_base, col_d, 32u, 16u * (uint32_t)h, bias, z);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {  // leaky ReLU = cwiseMax(z, slope z)
+                        const float2 t = upk2(fmul2(pk2(z[2 * q], z[2 * q + 1]), pk2(0.01f, 0.01f)));
+                        z[2 * q] = fmaxf(z[2 * q], t.x);
+                        z[2 * q + 1] = fmaxf(z[2 * q + 1], t.y);
+                    }
+                    ws::ws_store_a16(lane_base, col_a, h, z);
+                }
+                tmem_wait_st();
+                tc_fence_before();
+                named_bar_sync(bar_id, 128);
+                if (issuer)
+                    ws::ws_issue(st, net, lyr + 1, tmem_base, col_a, col_d, &st->mma_bar[g]);
+            } else if (KIND == kKindNrrs && l == 3) {
+                // stats -> build_nrrs_input (networks.cpp:137-147) -> RRSNet layer 0
+                float y[16];
+                ws::ws_load_sum16(lane_base, col_d, 16u, 0u, bias, y);
+                uint32_t bc = 0;
+                float xin[16];
+#pragma unroll
+                for (int q = 0; q < 6; ++q)
+                    xin[q] = box_cox_fast(y[q], bc);
+                xin[6] = box_cox_fast(wx, bc);
+                xin[7] = box_cox_fast(wy, bc);
+                xin[8] = box_cox_fast(wz, bc);
+                xin[9] = box_cox_fast(mean3_fast(ia, ib, ic), bc);
+                xin[10] = remap_fast(rough);
+                xin[11] = 1.0f;  // bias column of the RRSNet first layer
+#pragma unroll
+                for (int q = 12; q < 16; ++q)
+                    xin[q] = 0.0f;
+                if (!valid) {
+#pragma unroll
+                    for (int q = 0; q < 11; ++q)
+                        xin[q] = 0.0f;
+                }
+                if (active)
+                    my_bc += bc;
+                uint32_t hw[8], lw[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    split2(xin[2 * q], xin[2 * q + 1], hw[q], lw[q]);
+                tmem_st8(lane_base + col_a, hw);
+                tmem_st8(lane_base + col_a + 16u, lw);
+                tmem_wait_st();
+                tc_fence_before();
+                named_bar_sync(bar_id, 128);
+                if (issuer)
+                    ws::ws_issue(st, 1, 0, tmem_base, col_a, col_d, &st->mma_bar[g]);
+            } else {
+                float qv = 0.0f;
+                if (KIND == kKindStats) {
+                    float y[16];
+                    ws::ws_load_sum16(lane_base, col_d, 16u, 0u, bias, y);
+                    tc_fence_before();
+                    if (valid) {
+#pragma unroll
+                        for (int q = 0; q < 6; ++q)
+                            p.stats_out[6 * j + q] = y[q];
+                    }
+                    continue;
+                } else if (KIND == kKindAdrrs) {
+                    float y[16];
+                    ws::ws_load_sum16(lane_base, col_d, 16u, 0u, bias, y);
+                    const float num = luminance(wx * y[0], wy * y[1], wz * y[2]);
+                    const float qq = num / (luminance(ia, ib, ic) + p.eps);
+                    qv = qq < 0.05f ? 0.05f : (20.0f < qq ? 20.0f : qq);
+                } else {
+                    qv = softplus_mod(ws::ws_load_head1(lane_base, col_d, bias));
+                }
+                tc_fence_before();
+                uint32_t decided = active ? 1u : 0u;
+                if (p.gate) {
+                    if (valid && depth1)
+                        qv = 1.0f;
+                    if (!active && !depth1)
+                        qv = 0.0f;
+                    decided = valid && (depth1 || active) ? 1u : 0u;
+                    if (valid && (!isfinite(qv) || qv < 0.0f)) {  // sanitize (wavefront.cpp:381-385)
+                        qv = 0.0f;
+                        decided = 0;
+                        ++my_nonfinite;
+                    }
+                }
+                if (valid) {
+                    p.q_out[j] = qv;
+                    if (p.u_out)
+                        p.u_out[j] = rrs_uniform(p.mixed_seed, key, p.depth);
+                    if (p.decided_out)
+                        p.decided_out[j] = (uint8_t)decided;
+                    my_sum += (double)qv;
+                }
+            }
+        }
+    }
+
+    // ---- teardown + deterministic CTA reduction, then last-CTA-done ----
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0)
+        tmem_dealloc(tmem_base, 512);
+    if (KIND == kKindStats || p.parts == nullptr)
+        return;
+    {
+        double sv = my_sum;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+            sv += __shfl_xor_sync(0xffffffffu, sv, o);
+        const uint32_t nf = __reduce_add_sync(0xffffffffu, my_nonfinite);
+        const uint32_t bcs = __reduce_add_sync(0xffffffffu, my_bc);
+        if (lane == 0) {
+            st->red_sum[warp] = sv;
+            st->red_nf[warp] = nf;
+            st->red_bc[warp] = bcs;
+        }
+        __syncthreads();
+    }
+    constexpr int kWarps = kThreads / 32;
+    if (tid == 0) {
+        double cs = 0.0;
+        uint32_t cn = 0, cb = 0;
+        for (int w = 0; w < kWarps; ++w) {
+            cs += st->red_sum[w];
+            cn += st->red_nf[w];
+            cb += st->red_bc[w];
+        }
+        p.parts[blockIdx.x] = cs;
+        p.part_counts[2 * blockIdx.x] = cn;
+        p.part_counts[2 * blockIdx.x + 1] = cb;
+        __threadfence();
+        st->is_last = atomicAdd(p.counter, 1u) == gridDim.x - 1 ? 1u : 0u;
+    }
+    __syncthreads();
+    if (!st->is_last)
+        return;
+    __threadfence();
+    if (warp == 0) {
+        double sv = 0.0;
+        uint32_t nf = 0, bcs = 0;
+        for (uint32_t b = lane; b < gridDim.x; b += 32) {
+            sv += __ldcg(p.parts + b);
+            nf += __ldcg(p.part_counts + 2 * b);
+            bcs += __ldcg(p.part_counts + 2 * b + 1);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+            sv += __shfl_xor_sync(0xffffffffu, sv, o);
+        nf = __reduce_add_sync(0xffffffffu, nf);
+        bcs = __reduce_add_sync(0xffffffffu, bcs);
+        if (lane == 0) {
+            *p.sum_out = sv;
+            if (p.accumulate) {
+                p.res->sum_q += sv;
+                p.res->nonfinite += nf;
+                p.res->box_cox_clamps += bcs;
+            } else {
+                p.res->sum_q = sv;
+                p.res->nonfinite = nf;
+                p.res->box_cox_clamps = bcs;
+            }
+            *p.counter = 0;  // self-cleaning for the next launch
+        }
+    }
+}
+
 static bool aligned16(const void *q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; }
 
 template <int GM>
@@ -1248,6 +1624,31 @@ static cudaError_t launch_aid_fused(const InferParams &p_in, int num_sms, cudaSt
         grid = 1;
     *grid_out = (uint32_t)grid;
     return launch_maybe_pdl(infer_aid_fused_kernel<GM>, (uint32_t)grid, GM * 128, smem, stream, p);
+}
+
+template <int KIND>
+static cudaError_t launch_stat_planes(const InferParams &p_in, int num_sms, cudaStream_t stream, uint32_t *grid_out) {
+    InferParams p = p_in;
+    const size_t smem_direct = ((p.blob_bytes + 127u) & ~127u) + sizeof(ws::SmemTail) + 64;
+    const size_t smem_staged = (size_t)aid_in_offset(p.blob_bytes) + (size_t)8 * kAidInBytes;
+    p.in_bulk = 0;
+    const bool ipx_ok = KIND == kKindStats || (p.i_pixel ? aligned16(p.i_pixel) : (p.pixel != nullptr && aligned16(p.pixel)));
+    if (smem_staged <= 227u * 1024u && p.grid.levels <= 8 && (p.feat_stride & 3u) == 0 && aligned16(p.feat) &&
+        aligned16(p.weight) && aligned16(p.wo01) && aligned16(p.roughness) && aligned16(p.path_key) && ipx_ok)
+        p.in_bulk = 1;
+    const size_t smem = p.in_bulk ? smem_staged : smem_direct;
+    cudaError_t e = cudaFuncSetAttribute(infer_stat_planes_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess)
+        return e;
+    const uint64_t tiles = (p.n + kTileM - 1) / kTileM;
+    uint64_t grid = (uint64_t)num_sms;
+    if (grid > tiles)
+        grid = tiles;
+    if (grid < 1)
+        grid = 1;
+    *grid_out = (uint32_t)grid;
+    return launch_maybe_pdl(infer_stat_planes_kernel<KIND>, (uint32_t)grid, 8 * 128, smem, stream, p);
 }
 
 template <int KIND, int GE, int GM, int P, int TPR, bool HALF>
@@ -1953,6 +2354,24 @@ static cudaError_t launch_ws_cfg(const InferParams &p, int num_sms, cudaStream_t
         if (p.rrs_half)
             return launch_ws<KIND, NRRS_WS4_GE, NRRS_WS4_GM, 1, 1, true>(p, num_sms, stream, grid_out);
     }
+    if constexpr (KIND == kKindAdrrs || KIND == kKindStats || KIND == kKindNrrs) {
+        if (p.feat && p.stat_fm) {
+            // fp32 StatNet grid from shared memory, one (level, feature) table per CTA, then K-A over
+            // the feature planes
+            GridLevelParams gp{};
+            gp.p01 = p.p01;
+            gp.n = p.n;
+            gp.table = p.stat_fm;
+            gp.g = p.grid;
+            gp.feat = p.feat;
+            gp.feat_stride = p.feat_stride;
+            gp.f32 = 1;
+            cudaError_t e = launch_grid_levels(gp, num_sms, stream);
+            if (e != cudaSuccess)
+                return e;
+            return launch_stat_planes<KIND>(p, num_sms, stream, grid_out);
+        }
+    }
     // NRRS chains 8 MMA layers per tile (StatNet then RRSNet): 2 encoder + 3 MLP groups; the 4-layer
     // kinds are gather-bound and run 3 encoder + 2 MLP groups (ADRRS-NN 0.397 -> 0.377 ms)
     if constexpr (KIND == kKindNrrs)
@@ -2110,6 +2529,23 @@ __global__ void max_abs_kernel(const float *x, uint64_t n, unsigned int *out_bit
         m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     if ((threadIdx.x & 31) == 0)
         atomicMax(out_bits, __float_as_uint(m));  // non-negative floats order like their bits
+}
+
+// Feature-major copy [level][feature][T] of a [level][T][feature] fp32 grid (grid_level_kernel<true>).
+__global__ void feature_major_kernel(const float2 *src, float *dst, uint32_t levels, uint32_t T) {
+    const uint64_t total = (uint64_t)levels * T;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t l = i / T, e = i % T;
+        const float2 v = src[i];
+        dst[(2 * l) * T + e] = v.x;
+        dst[(2 * l + 1) * T + e] = v.y;
+    }
+}
+
+cudaError_t launch_feature_major(const float *src, float *dst, uint32_t levels, uint32_t T, cudaStream_t stream) {
+    feature_major_kernel<<<512, 256, 0, stream>>>(reinterpret_cast<const float2 *>(src), dst, levels, T);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_grid_copies(const float *src, void *dst, uint32_t levels, uint32_t T, uint32_t copies,
