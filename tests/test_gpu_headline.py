@@ -98,3 +98,29 @@ def test_fused_aid_stage_headline_oracle_parity(monkeypatch):
     """The opt-in fused stage at the configs[2] size against the oracle directly."""
     monkeypatch.setenv("NRRS_FUSED", "1")
     test_headline_size_parity(orc.VARIANT_AID, orc.AID_NRRS, 1920 * 1080)
+
+
+def test_adrrs_nn_headline_size_parity():
+    """ADRRS-NN at 1,228,800 vertices: the level-sliced fp32 StatNet planes (grid_level_kernel<true>
+    + infer_stat_planes_kernel) over many tiles per group against the oracle (adrrs.cpp restated)."""
+    n = 1_228_800
+    v = orc.gen_vertices(n)
+    on = orc.OracleNets(orc.VARIANT_NRRS, seed=1, randomize=True)
+    cap = queue_capacity_for(n)
+    eps_div = 1e-4
+    ref = orc.rrs_stage(v, 2, n, cap, orc.ADRRS_NN, on, gain=0.85, eps_div=eps_div, seed=0,
+                        threads=orc.threads_available())
+    st = RrsStage(n, mirror_nets(on))
+    out, res = st.run(to_dev(v), 2, Strategy(StrategyKind(orc.ADRRS_NN)), rc=RateControl(), eps_div=eps_div,
+                      full=True)
+    torch.cuda.synchronize()
+    err = rel_err(_np(out.q_orig), ref["q_orig"], 1e-6)
+    assert err.max() <= REL_TOL, f"q_orig max rel err {err.max():.3e} at vertex {int(err.argmax())}"
+    assert rel_err(_np(out.q_norm), ref["q_norm"], 1e-6).max() <= REL_TOL
+    np.testing.assert_array_equal(_np(out.u), ref["u"])
+    np.testing.assert_array_equal(_np(out.decided), ref["decided"])
+    assert abs(res.f_norm - ref["f_norm"]) <= REL_TOL * ref["f_norm"]
+    assert res.nonfinite == ref["nonfinite"]
+    flips = np.count_nonzero(_np(out.k) != ref["k"])
+    assert flips <= max(3, n // 2000), f"{flips} count flips"
+    st.close()
