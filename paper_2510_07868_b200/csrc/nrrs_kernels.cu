@@ -203,29 +203,32 @@ __global__ void __launch_bounds__(kLevelThreads, 1) grid_level_kernel(GridLevelP
 #pragma unroll
     for (int k = 0; k < 8; ++k)
         c.doff4[k] = (((k & 1) * nn + ((k >> 1) & 1)) * nn + (k >> 2)) * 4u;
-    float2 *out = p.feat + (uint64_t)role * p.feat_stride;
-    float *out1 = reinterpret_cast<float *>(p.feat) + (uint64_t)role * p.feat_stride;
+    // 32-bit offsets inside the CTA's range (a CTA serves < 2^32 vertices): the pointers advance once
+    // per block and the bounds are one 32-bit compare per vertex
+    const float *src3 = p.p01 + 3 * j0 + threadIdx.x * 3u;
+    float2 *out = p.feat + (uint64_t)role * p.feat_stride + j0 + threadIdx.x;
+    float *out1 = reinterpret_cast<float *>(p.feat) + (uint64_t)role * p.feat_stride + j0 + threadIdx.x;
+    const uint32_t span = (uint32_t)(j1 - j0);
     // kLevelPer vertices per thread per block (t, t + 1024, ...); the next block's p01 is loaded
     // into registers before this block's gathers, so its L2 round trip hides behind them (no
     // shared-memory staging and no barrier in the loop: every thread owns its own vertices).
     float pv[kLevelPer][3];
-    auto load_block = [&](uint64_t s) {
+    auto load_block = [&](uint32_t s) {  // s: block start relative to j0
+        const float *g = src3 + 3u * s;
 #pragma unroll
         for (int u = 0; u < (int)kLevelPer; ++u) {
-            const uint64_t j = s + threadIdx.x + (uint64_t)u * kLevelThreads;
-            if (j < j1) {
-                const float *g3 = p.p01 + 3 * j;
-                pv[u][0] = __ldg(g3);
-                pv[u][1] = __ldg(g3 + 1);
-                pv[u][2] = __ldg(g3 + 2);
+            if (s + threadIdx.x + (uint32_t)u * kLevelThreads < span) {
+                pv[u][0] = __ldg(g + 3u * u * kLevelThreads);
+                pv[u][1] = __ldg(g + 3u * u * kLevelThreads + 1);
+                pv[u][2] = __ldg(g + 3u * u * kLevelThreads + 2);
             } else {
                 pv[u][0] = pv[u][1] = pv[u][2] = 0.0f;
             }
         }
     };
-    load_block(j0);
+    load_block(0);
     mbar_wait(&bar[0], 0);
-    for (uint64_t s = j0; s < j1; s += kLevelBlock) {
+    for (uint32_t s = 0; s < span; s += kLevelBlock) {
         float cur[kLevelPer][3];
 #pragma unroll
         for (int u = 0; u < (int)kLevelPer; ++u) {
@@ -233,7 +236,7 @@ __global__ void __launch_bounds__(kLevelThreads, 1) grid_level_kernel(GridLevelP
             cur[u][1] = pv[u][1];
             cur[u][2] = pv[u][2];
         }
-        if (s + kLevelBlock < j1)
+        if (s + kLevelBlock < span)
             load_block(s + kLevelBlock);
         if constexpr (kF32) {
             float r[kLevelPer];
@@ -241,22 +244,18 @@ __global__ void __launch_bounds__(kLevelThreads, 1) grid_level_kernel(GridLevelP
             for (int u = 0; u < (int)kLevelPer; ++u)
                 r[u] = level_encode_f32(lvl_smem, c, cur[u][0], cur[u][1], cur[u][2]);
 #pragma unroll
-            for (int u = 0; u < (int)kLevelPer; ++u) {
-                const uint64_t j = s + threadIdx.x + (uint64_t)u * kLevelThreads;
-                if (j < j1)
-                    __stcs(out1 + j, r[u]);
-            }
+            for (int u = 0; u < (int)kLevelPer; ++u)
+                if (s + threadIdx.x + (uint32_t)u * kLevelThreads < span)
+                    __stcs(out1 + s + (uint32_t)u * kLevelThreads, r[u]);
         } else {
             float2 r[kLevelPer];
 #pragma unroll
             for (int u = 0; u < (int)kLevelPer; ++u)
                 r[u] = level_encode(lvl_smem, c, cur[u][0], cur[u][1], cur[u][2]);
 #pragma unroll
-            for (int u = 0; u < (int)kLevelPer; ++u) {
-                const uint64_t j = s + threadIdx.x + (uint64_t)u * kLevelThreads;
-                if (j < j1)
-                    __stcs(out + j, r[u]);
-            }
+            for (int u = 0; u < (int)kLevelPer; ++u)
+                if (s + threadIdx.x + (uint32_t)u * kLevelThreads < span)
+                    __stcs(out + s + (uint32_t)u * kLevelThreads, r[u]);
         }
     }
 }
@@ -2406,11 +2405,19 @@ cudaError_t launch_infer(int kind, const InferParams &p, int num_sms, cudaStream
 uint32_t infer_max_grid(int num_sms) { return (uint32_t)num_sms * 16u; }
 
 // Tile shape of decide3 / compact3: batches up to num_sms full tiles run as one wave with the
-// items spread evenly over the SMs (512-item warp granularity); larger ones use full tiles.
+// items spread evenly over the SMs (512-item warp granularity); larger ones use full tiles.  Small
+// batches keep at least kD3MinItems per tile: the warps of a CTA run side by side, while every
+// extra tile lengthens the look-back and adds a CTA launch (C1: 8 tiles of 16 warps, not 128 of 1).
+#ifndef NRRS_D3_MIN_ITEMS
+#define NRRS_D3_MIN_ITEMS 8192
+#endif
+constexpr uint64_t kD3MinItems = NRRS_D3_MIN_ITEMS;
 static void scan_tile_shape(uint64_t n, int num_sms, uint32_t *items, uint32_t *tiles, uint32_t *single) {
     const uint64_t sms = num_sms < 1 ? 1 : (uint64_t)num_sms;
     if (n <= sms * (uint64_t)kD3Tile && sms <= 256) {
         uint64_t per = (n + sms - 1) / sms;
+        if (per < kD3MinItems)
+            per = kD3MinItems;
         per = (per + kD3Warp - 1) / kD3Warp * kD3Warp;
         if (per == 0)
             per = kD3Warp;

@@ -46,5 +46,7 @@ probe("aid (default routing)", RrsVariant.Aid, StrategyKind.AidNrrs)
 probe("aid (fused-gather K-A, no K-A0)", RrsVariant.Aid, StrategyKind.AidNrrs, "NRRS_NO_LEVEL_KERNEL")
 probe("aid (fused single kernel)", RrsVariant.Aid, StrategyKind.AidNrrs, "NRRS_FUSED")
 probe("nrrs", RrsVariant.Nrrs, StrategyKind.Nrrs)
+probe("nrrs (L2-gather K-A, no K-A0)", RrsVariant.Nrrs, StrategyKind.Nrrs, "NRRS_NO_LEVEL_KERNEL")
+probe("adrrs-nn (L2-gather K-A, no K-A0)", RrsVariant.Nrrs, StrategyKind.AdrrsNn, "NRRS_NO_LEVEL_KERNEL")
 probe("adrrs-nn", RrsVariant.Nrrs, StrategyKind.AdrrsNn)
 probe("throughput", RrsVariant.Nrrs, StrategyKind.Throughput)
