@@ -241,6 +241,11 @@ def main():
     world, rank, local = dist_env()
     # test-only knobs: run N ranks on one device with gloo exchanges (functional check of the N>1 path)
     backend = os.environ.get("NRRS_BENCH_BACKEND", "nccl")
+    # N > 1 exchange: "collective" (torch.distributed all-gathers, default) or "mailbox" (in-kernel
+    # over NVLink peer memory, CUDA IPC; one GPU per rank -- never with NRRS_BENCH_SAME_DEVICE)
+    exchange = os.environ.get("NRRS_BENCH_EXCHANGE", "collective")
+    if exchange == "mailbox" and os.environ.get("NRRS_BENCH_SAME_DEVICE") and world > 1:
+        raise SystemExit("NRRS_BENCH_EXCHANGE=mailbox needs one GPU per rank (its kernels wait on the other ranks)")
     if os.environ.get("NRRS_BENCH_SAME_DEVICE"):
         local = 0
     torch.cuda.set_device(local)
@@ -268,7 +273,7 @@ def main():
     dv = {k: torch.from_numpy(a.view(np.int64) if a.dtype == np.uint64 else a).to(dev)
           for k, a in hv.items() if k != "pixel"}
     if world > 1:
-        sh = ShardedRrsStage(npx, nets, device=local)
+        sh = ShardedRrsStage(npx, nets, device=local, exchange=exchange)
         stage = sh.stage
     else:
         sh = None
@@ -331,8 +336,11 @@ def main():
             from paper_2510_07868_b200.sharded import sharded_depth_async
             # no host wait inside the depth: the global clip runs on the device (NCCL path) and this rank's
             # compaction needs only its own queue; the scalars are read after the timed loop
-            pending[0] = sharded_depth_async(local_sum, lambda rs: sh.decide(n, 2, strategy, out, rs, gain, 0.0), cap,
-                                             npx, sh.stage, None, after_exchange=lambda clip: compact(sh._total))
+            if sh.exchange == "mailbox":
+                pending[0] = sh.depth_async(n, 2, strategy, out, gain, 0.0, after_exchange=lambda clip: compact(sh._total))
+            else:
+                pending[0] = sharded_depth_async(local_sum, lambda rs: sh.decide(n, 2, strategy, out, rs, gain, 0.0),
+                                                 cap, npx, sh.stage, None, after_exchange=lambda clip: compact(sh._total))
         ev[-1].record(stream)
 
     def events(k=2):
@@ -918,6 +926,7 @@ def main():
                                 + ("; N=8 is the configs[4] 16.6 M-vertex batch" if world > 1 else "")),
                    "vertices_per_gpu": n, "n_pixels": npx, "capacity": cap, "strategy": f"{args.variant}-nrrs",
                    "depth": 2, "gain": 0.85, "parallelism": f"tile-sharded dp{world}",
+                   "exchange": (exchange if world > 1 else "none"),
                    "l2": "flushed between timed steps (256 MiB write outside the events)",
                    "aid_tables": aid_tables},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
@@ -925,7 +934,8 @@ def main():
                      "kernel": ("K-A0 grid_level_kernel + K-A infer_aid_fused_kernel<8> (level planes, 8 self-contained "
                                 "MLP groups): the strategy-factor step of the stage, timed as one unit"
                                 if args.variant == "aid" else
-                                "infer_ws_kernel<Nrrs> (warp-specialized, 2 encoder + 3 MLP groups, L2 gathers)"),
+                                "K-A0 grid_level_kernel<true> + K-A infer_stat_planes_kernel<Nrrs> (fp32 StatNet "
+                                "grid one (level, feature) table per CTA; StatNet + RRSNet chains)"),
                      "alg_bytes_per_vertex": ALG_BYTES_INFER, "peak_source": peak_src,
                      "stage_frac": (stage_bytes / (statistics.mean(step_ms) / 1e3) / 1e9) / hbm},
         "kernels_ms": {"infer": statistics.mean(infer_ms), "decide": statistics.mean(decide_ms),

@@ -444,6 +444,35 @@ NRRS_API int nrrs_gpu_sharded_clip(const uint64_t *h_rank_totals, int32_t nranks
 NRRS_API int nrrs_gpu_sharded_clip_dev(nrrs_gpu_ctx *ctx, const uint64_t *d_rank_totals, int32_t nranks,
                                        int32_t rank, uint32_t capacity, uint64_t *d_out);
 
+/* ---- in-kernel rank exchange over NVLink / NVSwitch peer memory (mailbox mode; DESIGN.md
+ * section 7).  Replaces the caller's two all-gathers per depth (wavefront.cpp:141-154 and
+ * rrs.cpp:8-24 across ranks): with a connected mailbox, nrrs_gpu_stage_factors' last CTA writes
+ * the rank's sum of q into every rank's mailbox, nrrs_gpu_stage_decide_mbox waits for all N
+ * sums in its own mailbox (summed in rank order, so F is identical on every rank) and its last
+ * tile publishes the realized total, and nrrs_gpu_sharded_clip_mbox waits for the N totals and
+ * applies the global clip -- no host round trip and no collective launch per depth.
+ * Generations are device counters, so CUDA graph replays stay valid; every rank must run the
+ * same sequence of depths.  A wait that sees no peer for 10 s raises the timeout flag
+ * (nrrs_gpu_mailbox_status) instead of hanging. */
+#define NRRS_IPC_HANDLE_BYTES 64
+/* Allocates this rank's mailbox (zeroed): returns its CUDA IPC handle (NRRS_IPC_HANDLE_BYTES)
+ * and, optionally, its device address (for ranks that share this process). nranks <= 8. */
+NRRS_API int nrrs_gpu_mailbox_init(nrrs_gpu_ctx *ctx, int32_t nranks, int32_t rank, void *ipc_handle_out,
+                                   uint64_t *d_addr_out);
+/* Maps every rank's mailbox: ipc_handles = nranks x NRRS_IPC_HANDLE_BYTES in rank order (the
+ * caller exchanges them, e.g. over the torch.distributed store); same_process_addrs (optional,
+ * nranks entries): a nonzero entry is that rank's device address in this process, used directly. */
+NRRS_API int nrrs_gpu_mailbox_connect(nrrs_gpu_ctx *ctx, const void *ipc_handles, const uint64_t *same_process_addrs);
+/* Phase 2 of the mailbox mode (nrrs_gpu_stage_decide with the rank sums taken from the mailbox). */
+NRRS_API int nrrs_gpu_stage_decide_mbox(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_stage_params *p,
+                                        const nrrs_stage_out *d_out, uint64_t *d_local_total);
+/* The global clip of the mailbox mode: d_out[4] as nrrs_gpu_sharded_clip_dev; optionally the
+ * rank sums (f64) and totals (u64) this depth used, nranks entries each, rank order. */
+NRRS_API int nrrs_gpu_sharded_clip_mbox(nrrs_gpu_ctx *ctx, uint32_t capacity, uint64_t *d_out,
+                                        double *d_rank_sums_out, uint64_t *d_rank_totals_out);
+/* Synchronizes the context stream; *timed_out = 1 if a mailbox wait gave up on a peer. */
+NRRS_API int nrrs_gpu_mailbox_status(nrrs_gpu_ctx *ctx, int32_t *timed_out);
+
 /* ---- order-preserving compaction of filled slots (wavefront.cpp:488-497):
  * keeps record s iff d_used[s] != 0, in slot order.  Records are
  * record_words x 32-bit (2 for slot records, 18 for a 72-byte PathState).

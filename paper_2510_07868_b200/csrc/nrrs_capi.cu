@@ -244,6 +244,15 @@ struct nrrs_gpu_ctx {
     uint64_t next_ticket = 0;
     bool in_flight[2] = {false, false};
     uint64_t set_ticket[2] = {0, 0};
+
+    // sharded mailbox mode (nrrs_gpu_mailbox_init / _connect): the rank's IPC-exported mailbox,
+    // its device descriptor and the peer mappings opened here (closed at destroy)
+    unsigned long long *d_mbox = nullptr;
+    MboxDev *d_mbox_dev = nullptr;
+    uint8_t *d_mbox_aux = nullptr;  // gen[kMboxKinds] u32, err u32, sums_seen f64[8], totals_seen u64[8]
+    void *mbox_opened[kMboxMaxRanks] = {};
+    int32_t mbox_nranks = 0, mbox_rank = 0;
+    bool mbox_ready = false;
 };
 
 static int fail(nrrs_gpu_ctx *ctx, int code, const char *fmt, ...) {
@@ -289,7 +298,8 @@ static int ensure_compact_scratch(nrrs_gpu_ctx *ctx, uint64_t count, uint32_t wo
 }
 
 static int run_factors(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, const nrrs_stage_params *p,
-                       float *q_out, float *u_out, uint8_t *decided_out, double *sum_out, bool accumulate = false);
+                       float *q_out, float *u_out, uint8_t *decided_out, double *sum_out, bool accumulate = false,
+                       const MboxDev *mbox = nullptr);
 
 // Error-budget gate of the fp16 AID tables: the RRSNet factors of a fixed probe
 // batch (16,384 vertices, U[0,1)^3 positions, the SURVEY 8d tail ranges) through the fp16 tables and
@@ -461,6 +471,12 @@ int nrrs_gpu_destroy(nrrs_gpu_ctx *ctx) {
         for (cudaEvent_t e : ctx->ev_chunk)
             cudaEventDestroy(e);
     }
+    for (void *m : ctx->mbox_opened)
+        if (m)
+            cudaIpcCloseMemHandle(m);
+    for (void *m : {(void *)ctx->d_mbox, (void *)ctx->d_mbox_dev, (void *)ctx->d_mbox_aux})
+        if (m)
+            cudaFree(m);
     delete ctx;
     return NRRS_OK;
 }
@@ -828,7 +844,8 @@ static int check_soa(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, int kind) {
 }
 
 static int run_factors(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, const nrrs_stage_params *p,
-                       float *q_out, float *u_out, uint8_t *decided_out, double *sum_out, bool accumulate) {
+                       float *q_out, float *u_out, uint8_t *decided_out, double *sum_out, bool accumulate,
+                       const MboxDev *mbox) {
     int kind = 0, heur = 0;
     int rc = select_kind(ctx, p->depth, p->strategy, &kind, &heur);
     if (rc)
@@ -862,6 +879,7 @@ static int run_factors(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, 
     ip.sum_out = sum_out;
     ip.res = ctx->d_res;
     ip.accumulate = accumulate ? 1u : 0u;
+    ip.mbox = mbox;
 #ifdef NRRS_KERNEL_TIMING
     if (const char *ab = std::getenv("NRRS_DEBUG_ABLATE"))  // diagnostics build only; results invalid
         ip.ablate = (uint32_t)std::atoi(ab);
@@ -957,7 +975,8 @@ static void phase_dump(nrrs_gpu_ctx *ctx, const char *what, unsigned long long *
 
 static int run_decide(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_stage_params *p, const float *q, const float *u,
                       const double *rank_sums, int nranks, uint64_t n_pixels, uint32_t capacity,
-                      const nrrs_stage_out *o, unsigned long long *total_out, DevResult *res) {
+                      const nrrs_stage_out *o, unsigned long long *total_out, DevResult *res,
+                      const MboxDev *mbox = nullptr) {
     if (!std::isfinite(p->gain) || p->gain < 0.0f)
         return fail(ctx, NRRS_EINVAL, "stage: gain must be finite and >= 0 (got %g)", (double)p->gain);
     const bool adaptive = p->strategy.kind != NRRS_FIXED;
@@ -982,6 +1001,7 @@ static int run_decide(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_stage_params *p,
     dp.err_flag = ctx->d_misc + 3;
     dp.total_out = total_out;
     dp.res = res;
+    dp.mbox = mbox;
 #ifdef NRRS_KERNEL_TIMING
     dp.dbg = phase_dbg(ctx);
 #endif
@@ -2131,6 +2151,10 @@ int nrrs_gpu_stage_factors(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t
         return rc;
     if (n == 0) {
         CK(ctx, cudaMemsetAsync(d_local_sum, 0, sizeof(double), ctx->stream));
+        if (ctx->mbox_ready) {  // an empty rank still takes part in the depth's exchange
+            CK(ctx, launch_mbox_publish(ctx->d_mbox_dev, 0, 0ull, ctx->stream));
+            ctx->launches += 1;
+        }
         return NRRS_OK;
     }
     rc = ensure_scratch(ctx, n);
@@ -2141,7 +2165,9 @@ int nrrs_gpu_stage_factors(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t
     // nrrs_gpu_stage_decide reads q_orig / u as 16-byte vectors
     if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(u)) & 15u)
         return fail(ctx, NRRS_EINVAL, "stage out: q_orig / u must be 16-byte aligned");
-    return run_factors(ctx, v, n, p, q, u, o ? o->decided : nullptr, d_local_sum);
+    // mailbox mode: K-A's last CTA also publishes the rank's sum to every rank
+    return run_factors(ctx, v, n, p, q, u, o ? o->decided : nullptr, d_local_sum, false,
+                       ctx->mbox_ready ? ctx->d_mbox_dev : nullptr);
 }
 
 int nrrs_gpu_stage_decide(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_stage_params *p, const double *d_rank_sums,
@@ -2170,6 +2196,126 @@ int nrrs_gpu_stage_decide(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_stage_params
     // rank-local records, the global clip is applied by the caller.
     return run_decide(ctx, n, p, q, u, d_rank_sums, nranks, p->n_pixels, cap, o,
                       reinterpret_cast<unsigned long long *>(d_local_total), ctx->d_res);
+}
+
+int nrrs_gpu_mailbox_init(nrrs_gpu_ctx *ctx, int32_t nranks, int32_t rank, void *ipc_handle_out,
+                          uint64_t *d_addr_out) {
+    if (!ctx || nranks < 1 || nranks > kMboxMaxRanks || rank < 0 || rank >= nranks || !ipc_handle_out)
+        return ctx ? fail(ctx, NRRS_EINVAL, "mailbox_init: nranks must be 1..%d and 0 <= rank < nranks",
+                          kMboxMaxRanks)
+                   : NRRS_EINVAL;
+    if (ctx->d_mbox)
+        return fail(ctx, NRRS_ESTATE, "mailbox_init: the context already has a mailbox");
+    CK(ctx, cudaSetDevice(ctx->device));
+    CK(ctx, cudaMalloc(&ctx->d_mbox, kMboxBytes));
+    CK(ctx, cudaMemset(ctx->d_mbox, 0, kMboxBytes));
+    constexpr size_t aux = 64 + 8 * kMboxMaxRanks * 2;
+    CK(ctx, cudaMalloc(&ctx->d_mbox_aux, aux));
+    CK(ctx, cudaMemset(ctx->d_mbox_aux, 0, aux));
+    CK(ctx, cudaMalloc(&ctx->d_mbox_dev, sizeof(MboxDev)));
+    cudaIpcMemHandle_t h;
+    CK(ctx, cudaIpcGetMemHandle(&h, ctx->d_mbox));
+    std::memcpy(ipc_handle_out, &h, sizeof h);
+    static_assert(sizeof(cudaIpcMemHandle_t) == NRRS_IPC_HANDLE_BYTES, "IPC handle size");
+    if (d_addr_out)
+        *d_addr_out = reinterpret_cast<uint64_t>(ctx->d_mbox);
+    ctx->mbox_nranks = nranks;
+    ctx->mbox_rank = rank;
+    return NRRS_OK;
+}
+
+int nrrs_gpu_mailbox_connect(nrrs_gpu_ctx *ctx, const void *ipc_handles, const uint64_t *same_process_addrs) {
+    if (!ctx || !ipc_handles)
+        return NRRS_EINVAL;
+    if (!ctx->d_mbox || ctx->mbox_ready)
+        return fail(ctx, NRRS_ESTATE, "mailbox_connect: needs mailbox_init first (and connects once)");
+    CK(ctx, cudaSetDevice(ctx->device));
+    MboxDev m{};
+    for (int r = 0; r < ctx->mbox_nranks; ++r) {
+        if (r == ctx->mbox_rank) {
+            m.peer[r] = ctx->d_mbox;
+        } else if (same_process_addrs && same_process_addrs[r]) {
+            m.peer[r] = reinterpret_cast<unsigned long long *>(same_process_addrs[r]);
+        } else {
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, static_cast<const uint8_t *>(ipc_handles) + (size_t)r * NRRS_IPC_HANDLE_BYTES, sizeof h);
+            void *ptr = nullptr;
+            CK(ctx, cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+            ctx->mbox_opened[r] = ptr;
+            m.peer[r] = static_cast<unsigned long long *>(ptr);
+        }
+    }
+    m.gen = reinterpret_cast<uint32_t *>(ctx->d_mbox_aux);
+    m.err = reinterpret_cast<uint32_t *>(ctx->d_mbox_aux) + kMboxKinds;
+    m.sums_seen = reinterpret_cast<double *>(ctx->d_mbox_aux + 64);
+    m.totals_seen = reinterpret_cast<unsigned long long *>(ctx->d_mbox_aux + 64 + 8 * kMboxMaxRanks);
+    m.nranks = ctx->mbox_nranks;
+    m.rank = ctx->mbox_rank;
+    CK(ctx, cudaMemcpy(ctx->d_mbox_dev, &m, sizeof m, cudaMemcpyHostToDevice));
+    ctx->mbox_ready = true;
+    return NRRS_OK;
+}
+
+int nrrs_gpu_stage_decide_mbox(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_stage_params *p, const nrrs_stage_out *o,
+                               uint64_t *d_local_total) {
+    if (!ctx || !d_local_total)
+        return NRRS_EINVAL;
+    if (!ctx->mbox_ready)
+        return fail(ctx, NRRS_ESTATE, "stage_decide_mbox: the context has no connected mailbox");
+    uint32_t cap = 0;
+    int rc = resolve_capacity(ctx, p, &cap);
+    if (rc)
+        return rc;
+    rc = check_out(ctx, o, n);
+    if (rc)
+        return rc;
+    if (n == 0) {  // nothing to decide, but the rank's (zero) total still goes to every rank
+        CK(ctx, cudaMemsetAsync(d_local_total, 0, sizeof(uint64_t), ctx->stream));
+        CK(ctx, launch_mbox_publish(ctx->d_mbox_dev, 1, 0ull, ctx->stream));
+        ctx->launches += 1;
+        return NRRS_OK;
+    }
+    rc = ensure_scratch(ctx, n);
+    if (rc)
+        return rc;
+    const float *q = o->q_orig ? o->q_orig : ctx->d_q;
+    const float *u = o->u ? o->u : ctx->d_u;
+    if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(u)) & 15u)
+        return fail(ctx, NRRS_EINVAL, "stage out: q_orig / u must be 16-byte aligned");
+    return run_decide(ctx, n, p, q, u, nullptr, 0, p->n_pixels, cap, o,
+                      reinterpret_cast<unsigned long long *>(d_local_total), ctx->d_res, ctx->d_mbox_dev);
+}
+
+int nrrs_gpu_sharded_clip_mbox(nrrs_gpu_ctx *ctx, uint32_t capacity, uint64_t *d_out, double *d_rank_sums_out,
+                               uint64_t *d_rank_totals_out) {
+    if (!ctx || !d_out)
+        return NRRS_EINVAL;
+    if (!ctx->mbox_ready)
+        return fail(ctx, NRRS_ESTATE, "sharded_clip_mbox: the context has no connected mailbox");
+    CK(ctx, cudaSetDevice(ctx->device));
+    CK(ctx, launch_mbox_clip(ctx->d_mbox_dev, capacity, reinterpret_cast<unsigned long long *>(d_out), ctx->stream));
+    ctx->launches += 1;
+    const size_t b = 8 * (size_t)ctx->mbox_nranks;
+    if (d_rank_sums_out)
+        CK(ctx, cudaMemcpyAsync(d_rank_sums_out, ctx->d_mbox_aux + 64, b, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (d_rank_totals_out)
+        CK(ctx, cudaMemcpyAsync(d_rank_totals_out, ctx->d_mbox_aux + 64 + 8 * kMboxMaxRanks, b,
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+    return NRRS_OK;
+}
+
+int nrrs_gpu_mailbox_status(nrrs_gpu_ctx *ctx, int32_t *timed_out) {
+    if (!ctx || !timed_out)
+        return NRRS_EINVAL;
+    if (!ctx->d_mbox_aux) {
+        *timed_out = 0;
+        return NRRS_OK;
+    }
+    uint32_t e = 0;
+    CK(ctx, cudaStreamSynchronize(ctx->stream));
+    CK(ctx, cudaMemcpy(&e, ctx->d_mbox_aux + 4 * kMboxKinds, sizeof e, cudaMemcpyDeviceToHost));
+    *timed_out = e ? 1 : 0;
+    return NRRS_OK;
 }
 
 int nrrs_gpu_sharded_clip(const uint64_t *totals, int32_t nranks, int32_t rank, uint32_t capacity,

@@ -411,6 +411,58 @@ __device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t *p) {
     return v;
 }
 
+// ---- peer mailbox (MboxDev): system-scope stores into peer memory, polls of the own mailbox ----
+constexpr unsigned long long kMboxTimeoutNs = 10ull * 1000 * 1000 * 1000;  // a missing rank: error, not a hang
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// One thread: the rank's value of `kind` into its line of every rank's mailbox, value before the
+// generation (st.release.sys orders it), generation = the rank's next counter value.
+__device__ __forceinline__ void mbox_publish(const MboxDev *m, int kind, unsigned long long value) {
+    const uint32_t g = m->gen[kind] + 1u;
+    m->gen[kind] = g;
+    for (int r = 0; r < m->nranks; ++r) {
+        unsigned long long *line = m->peer[r] + ((size_t)kind * kMboxMaxRanks + m->rank) * kMboxLineWords;
+        asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(line + 1), "l"(value) : "memory");
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(line), "l"((unsigned long long)g) : "memory");
+    }
+}
+
+// One thread: waits until every rank's line of `kind` in this rank's mailbox carries this rank's
+// current generation of `kind` (its own publish of the same step already advanced it), then hands
+// the values to f(rank, value) in rank order.  Returns false (and raises m->err) after
+// kMboxTimeoutNs.
+template <typename F>
+__device__ __forceinline__ bool mbox_wait(const MboxDev *m, int kind, F &&f) {
+    const uint32_t g = m->gen[kind];
+    const unsigned long long *mine = m->peer[m->rank] + (size_t)kind * kMboxMaxRanks * kMboxLineWords;
+    const unsigned long long t0 = globaltimer_ns();
+    bool ok = true;
+    for (int r = 0; r < m->nranks; ++r) {
+        const unsigned long long *line = mine + (size_t)r * kMboxLineWords;
+        for (;;) {
+            unsigned long long w;
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(w) : "l"(line) : "memory");
+            if ((int32_t)((uint32_t)w - g) >= 0)
+                break;
+            if (globaltimer_ns() - t0 > kMboxTimeoutNs) {
+                atomicExch(m->err, 1u);
+                ok = false;
+                break;
+            }
+            __nanosleep(100);
+        }
+        unsigned long long v;
+        asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(line + 1) : "memory");
+        f(r, v);
+    }
+    return ok;
+}
+
 __device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t *p) {
     uint64_t v;
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");

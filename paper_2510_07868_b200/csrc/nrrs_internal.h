@@ -77,6 +77,27 @@ struct GridDev {
     uint32_t pair_copies; // usable copies: t < pair_copies needs 2^(t+1) <= table_size
 };
 
+// Peer mailbox of the in-kernel rank exchange (replaces the two 8-byte
+// all-gathers per depth of wavefront.cpp:141-154 / rrs.cpp:8-24 across ranks).  Each rank's
+// mailbox holds, per kind (0: the rank's sum of q as f64 bits, 1: its realized total) and per
+// SOURCE rank, one 64-byte line {generation, value}.  A rank writes its value into its line of
+// EVERY rank's mailbox (peer mappings over NVLink / NVSwitch, CUDA IPC), value first, then the
+// generation with release semantics at system scope; a waiter polls only its own mailbox.
+// Generations are device counters advanced by the publishing kernel itself, so the protocol
+// needs no host round trip and stays valid under CUDA graph replay.
+constexpr int kMboxMaxRanks = 8;
+constexpr int kMboxLineWords = 8;  // u64 words per line
+constexpr int kMboxKinds = 2;
+constexpr size_t kMboxBytes = (size_t)kMboxKinds * kMboxMaxRanks * kMboxLineWords * 8;
+struct MboxDev {
+    unsigned long long *peer[kMboxMaxRanks];  // every rank's mailbox (own included), mapped here
+    uint32_t *gen;                            // this rank's generation per kind [kMboxKinds]
+    uint32_t *err;                            // set to 1 when a wait times out
+    double *sums_seen;                        // [nranks] rank sums the last decide used (rank order)
+    unsigned long long *totals_seen;          // [nranks] rank totals the last clip used
+    int32_t nranks, rank;
+};
+
 // Device-side scalar results of one stage call (mirrors nrrs_stage_result).
 struct DevResult {
     double f_norm;
@@ -124,6 +145,7 @@ struct InferParams {
     uint32_t in_bulk;  // set by launch_aid_fused: K-A stages row inputs by TMA (aligned inputs)
     uint32_t ablate;   // debug only (env NRRS_DEBUG_ABLATE): bit0 skip grid gathers, bit1 skip MLP
     unsigned long long *dbg;  // debug only (env NRRS_DEBUG_TIMING): per-CTA clock64 phase counters [grid][16]
+    const MboxDev *mbox;      // sharded mailbox mode: the last CTA publishes the rank's sum of q
 };
 
 // The fused AID-NRRS stage (nrrs_fused.cu): factor inputs + decision outputs.
@@ -170,6 +192,7 @@ struct DecideParams {
     uint32_t tile_items;      // items per tile (multiple of 512; set by launch_decide / launch_compact)
     uint32_t single_wave;     // every tile resident at once: prefix = sum of predecessor aggregates
     unsigned long long *dbg;  // NRRS_KERNEL_TIMING builds only: per-tile %globaltimer phase stamps [tile][8]
+    const MboxDev *mbox;      // sharded mailbox mode: rank sums from the mailbox, total published to peers
 };
 
 struct CompactParams {
@@ -406,5 +429,11 @@ cudaError_t launch_scale(float *q, uint64_t n, const double *sum, uint64_t n_pix
                          double *f_out, int num_sms, cudaStream_t stream);
 cudaError_t launch_realize(const float *q, const float *u, int32_t *counts, uint64_t n, uint32_t *err,
                            unsigned long long *total, int num_sms, cudaStream_t stream);
+
+// Mailbox mode: waits for every rank's realized total of this depth and applies the global clip
+// (base, kept, spawned, dropped -> out[0..3], as sharded_clip_kernel); one thread.
+cudaError_t launch_mbox_clip(const MboxDev *m, uint32_t capacity, unsigned long long *out, cudaStream_t stream);
+// Mailbox mode, empty rank: publishes `value` for `kind` (one thread).
+cudaError_t launch_mbox_publish(const MboxDev *m, int kind, unsigned long long value, cudaStream_t stream);
 
 }  // namespace nrrs

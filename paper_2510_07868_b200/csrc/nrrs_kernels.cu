@@ -307,6 +307,44 @@ static cudaError_t launch_maybe_pdl(K kernel, uint32_t grid, uint32_t block, siz
     return cudaLaunchKernelEx(&cfg, kernel, p);
 }
 
+// Mailbox mode of sharded_clip_kernel: the rank totals come from the own mailbox (kind 1).
+__global__ void mbox_clip_kernel(const MboxDev *m, uint32_t capacity, unsigned long long *out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0)
+        return;
+    unsigned long long base = 0, all = 0, mine = 0;
+    mbox_wait(m, 1, [&](int r, unsigned long long t) {
+        if (r < m->rank)
+            base += t;
+        if (r == m->rank)
+            mine = t;
+        all += t;
+        m->totals_seen[r] = t;
+    });
+    const unsigned long long cap = capacity;
+    const unsigned long long room = cap - (base < cap ? base : cap);
+    const unsigned long long kept = mine < room ? mine : room;
+    const unsigned long long spawned = all < cap ? all : cap;
+    out[0] = base;
+    out[1] = kept;
+    out[2] = spawned;
+    out[3] = all - spawned;
+}
+
+__global__ void mbox_publish_kernel(const MboxDev *m, int kind, unsigned long long value) {
+    if (threadIdx.x == 0 && blockIdx.x == 0)
+        mbox_publish(m, kind, value);
+}
+
+cudaError_t launch_mbox_publish(const MboxDev *m, int kind, unsigned long long value, cudaStream_t stream) {
+    mbox_publish_kernel<<<1, 32, 0, stream>>>(m, kind, value);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_mbox_clip(const MboxDev *m, uint32_t capacity, unsigned long long *out, cudaStream_t stream) {
+    mbox_clip_kernel<<<1, 32, 0, stream>>>(m, capacity, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_sharded_clip(const unsigned long long *totals, int nranks, int rank, uint32_t capacity,
                                 unsigned long long *out, cudaStream_t stream) {
     sharded_clip_kernel<<<1, 32, 0, stream>>>(totals, nranks, rank, capacity, out);
@@ -440,6 +478,8 @@ __global__ void __launch_bounds__(kInferThreads) infer_kernel(InferParams p) {
             tb += hdr->warp_bc[w];
         }
         *p.sum_out = total;
+        if (p.mbox)  // sharded mailbox mode: this rank's sum to every rank
+            mbox_publish(p.mbox, 0, (unsigned long long)__double_as_longlong(total));
         if (p.accumulate) {
             p.res->sum_q += total;
             p.res->nonfinite += tn;
@@ -917,6 +957,8 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
         bcs = __reduce_add_sync(0xffffffffu, bcs);
         if (lane == 0) {
             *p.sum_out = sv;
+            if (p.mbox)  // sharded mailbox mode: this rank's sum to every rank
+                mbox_publish(p.mbox, 0, (unsigned long long)__double_as_longlong(sv));
             if (p.accumulate) {
                 p.res->sum_q += sv;
                 p.res->nonfinite += nf;
@@ -1229,6 +1271,8 @@ __global__ void __launch_bounds__(GM * 128, 1) infer_aid_fused_kernel(InferParam
         bcs = __reduce_add_sync(0xffffffffu, bcs);
         if (lane == 0) {
             *p.sum_out = sv;
+            if (p.mbox)  // sharded mailbox mode: this rank's sum to every rank
+                mbox_publish(p.mbox, 0, (unsigned long long)__double_as_longlong(sv));
             if (p.accumulate) {
                 p.res->sum_q += sv;
                 p.res->nonfinite += nf;
@@ -1580,6 +1624,8 @@ __global__ void __launch_bounds__(8 * 128, 1) infer_stat_planes_kernel(InferPara
         bcs = __reduce_add_sync(0xffffffffu, bcs);
         if (lane == 0) {
             *p.sum_out = sv;
+            if (p.mbox)  // sharded mailbox mode: this rank's sum to every rank
+                mbox_publish(p.mbox, 0, (unsigned long long)__double_as_longlong(sv));
             if (p.accumulate) {
                 p.res->sum_q += sv;
                 p.res->nonfinite += nf;
@@ -1873,8 +1919,24 @@ __global__ void __launch_bounds__(kD3T, 1) decide3_kernel(DecideParams p) {
     float scale = 1.0f;
     if (SRC == 0) {
         double sum = 0.0;
-        for (int r = 0; r < p.nranks; ++r)
-            sum += p.rank_sums[r];
+        if (p.mbox) {  // sharded mailbox mode: every rank's sum of this depth from the own mailbox
+            __shared__ double s_sum;
+            if (tid == 0) {
+                double t = 0.0;
+                mbox_wait(p.mbox, 0, [&](int r, unsigned long long v) {  // rank order, as the all-gather path
+                    const double x = __longlong_as_double((long long)v);
+                    t += x;
+                    if (tile == 0)
+                        p.mbox->sums_seen[r] = x;
+                });
+                s_sum = t;
+            }
+            __syncthreads();
+            sum = s_sum;
+        } else {
+            for (int r = 0; r < p.nranks; ++r)
+                sum += p.rank_sums[r];
+        }
         if (sum > 0.0) {
             const double f = __ddiv_rn((double)p.n_pixels, sum);  // F = Npx / sum (rrs.cpp:17)
             if (f < 1.0) {
@@ -2056,6 +2118,8 @@ __global__ void __launch_bounds__(kD3T, 1) decide3_kernel(DecideParams p) {
         const uint64_t total = P + agg;
         if (p.total_out)
             *p.total_out = total;
+        if (p.mbox)  // this rank's realized total to every rank (the clip kernel waits on all of them)
+            mbox_publish(p.mbox, 1, total);
         if (p.res) {
             const uint64_t spawned = total < cap ? total : cap;
             p.res->total = total;

@@ -21,7 +21,8 @@ from __future__ import annotations
 
 import ctypes as C
 import dataclasses
-from typing import Callable, List, Optional
+import os
+from typing import Callable, List, Optional, Sequence, Tuple
 
 import numpy as np
 import torch
@@ -100,9 +101,12 @@ class PendingDepth:
     n_pixels_total: int
     capacity: int
     rank: int
+    check: Optional[Callable[[], None]] = None  # mailbox mode: raises if a peer wait timed out
 
     def resolve(self, rc: Optional[RateControl] = None) -> ShardOutcome:
         """Reads the depth's scalars (one host wait) and applies the overflow to RateControl."""
+        if self.check is not None:
+            self.check()
         tot = [int(x) for x in self.rank_totals.tolist()]
         sums_h = [float(x) for x in self.rank_sums.tolist()]
         if self.clip is not None:
@@ -150,6 +154,66 @@ def sharded_depth_async(local_sum: torch.Tensor, decide: Callable[[torch.Tensor]
     if after_exchange is not None:
         after_exchange(clip)
     return PendingDepth(rank_sums_t, totals_t, clip, n_pixels_total, capacity, rank)
+
+
+# ---- mailbox mode: the two per-depth exchanges inside the kernels, over peer memory ----------
+IPC_HANDLE_BYTES = 64  # NRRS_IPC_HANDLE_BYTES
+
+
+def mailbox_init(stage: RrsStage, world: int, rank: int) -> Tuple[bytes, int]:
+    """nrrs_gpu_mailbox_init: allocates the rank's mailbox; returns (CUDA IPC handle, device address)."""
+    h = (C.c_uint8 * IPC_HANDLE_BYTES)()
+    addr = C.c_uint64(0)
+    _capi.check(stage.handle, stage.ctx.lib.nrrs_gpu_mailbox_init(stage.handle, world, rank, h, C.byref(addr)))
+    return bytes(h), addr.value
+
+
+def mailbox_connect(stage: RrsStage, handles: Sequence[bytes], same_process_addrs: Sequence[int]) -> None:
+    """nrrs_gpu_mailbox_connect: maps every rank's mailbox (IPC handles in rank order; a nonzero
+    same-process address is used directly)."""
+    world = len(handles)
+    buf = (C.c_uint8 * (IPC_HANDLE_BYTES * world)).from_buffer_copy(b"".join(handles))
+    addrs = (C.c_uint64 * world)(*same_process_addrs)
+    _capi.check(stage.handle, stage.ctx.lib.nrrs_gpu_mailbox_connect(stage.handle, buf, addrs))
+
+
+def mailbox_check(stage: RrsStage) -> None:
+    """Raises if a mailbox wait of this context gave up on a peer (nrrs_gpu_mailbox_status)."""
+    t = C.c_int32(0)
+    _capi.check(stage.handle, stage.ctx.lib.nrrs_gpu_mailbox_status(stage.handle, C.byref(t)))
+    if t.value:
+        raise RuntimeError("mailbox exchange timed out: a rank did not publish this depth (all ranks must run "
+                           "the same sequence of depths)")
+
+
+def connect_mailboxes_in_process(stages: Sequence[RrsStage]) -> None:
+    """All ranks in ONE process (one RrsStage per rank, e.g. a functional check): mailboxes are
+    connected through their device addresses, no IPC."""
+    world = len(stages)
+    infos = [mailbox_init(st, world, r) for r, st in enumerate(stages)]
+    for st in stages:
+        mailbox_connect(st, [h for h, _ in infos], [a for _, a in infos])
+
+
+def mailbox_depth(stage: RrsStage, n: int, p, out: StageOutputs, local_total: torch.Tensor, world: int, rank: int,
+                  capacity: int, n_pixels_total: int,
+                  after_exchange: Optional[Callable[[torch.Tensor], None]] = None) -> PendingDepth:
+    """Phase 2 of a depth in mailbox mode (phase 1, nrrs_gpu_stage_factors, already published the
+    rank's sum): decide with the rank sums from the mailbox, then the global clip from the
+    mailboxed totals, both on the device with no collective and no host wait."""
+    lib = stage.ctx.lib
+    oc = out.c()
+    _capi.check(stage.handle, lib.nrrs_gpu_stage_decide_mbox(stage.handle, n, C.byref(p), C.byref(oc),
+                                                             local_total.data_ptr()))
+    dev = local_total.device
+    clip = torch.empty(4, dtype=torch.int64, device=dev)
+    sums = torch.empty(world, dtype=torch.float64, device=dev)
+    tots = torch.empty(world, dtype=torch.int64, device=dev)
+    _capi.check(stage.handle, lib.nrrs_gpu_sharded_clip_mbox(stage.handle, int(capacity), clip.data_ptr(),
+                                                             sums.data_ptr(), tots.data_ptr()))
+    if after_exchange is not None:
+        after_exchange(clip)
+    return PendingDepth(sums, tots, clip, n_pixels_total, capacity, rank, check=lambda: mailbox_check(stage))
 
 
 def _gather_in_rank_order(local: torch.Tensor, group=None) -> torch.Tensor:
@@ -226,17 +290,44 @@ def broadcast_weights(nets, src: int = 0, group=None, device=None):
 
 
 class ShardedRrsStage:
-    """One rank of the tile-sharded stage (one GPU per process, NCCL over NVLink)."""
+    """One rank of the tile-sharded stage (one GPU per process, NCCL over NVLink).
+
+    exchange="collective" (default): the two per-depth exchanges are torch.distributed
+    all-gathers.  exchange="mailbox": they run inside the stage kernels over peer memory
+    (CUDA IPC mappings of every rank's mailbox, NVLink / NVSwitch); the handles are exchanged
+    once here over the process group."""
 
     def __init__(self, n_pixels_total: int, nets=None, capacity: int = 0, seed: int = 0, device: int = 0,
-                 group=None):
+                 group=None, exchange: str = "collective"):
+        if exchange not in ("collective", "mailbox"):
+            raise ValueError(f"exchange must be 'collective' or 'mailbox', got {exchange!r}")
         self.stage = RrsStage(n_pixels_total, nets, capacity=capacity, seed=seed, device=device)
         self.n_pixels_total = int(n_pixels_total)
         self.capacity = self.stage.capacity
         self.group = group
         self.device = self.stage.device
+        self.exchange = exchange
         self._sum = torch.zeros(1, dtype=torch.float64, device=self.device)
         self._total = torch.zeros(1, dtype=torch.int64, device=self.device)
+        if exchange == "mailbox":
+            world, rank = dist.get_world_size(group), dist.get_rank(group)
+            h, addr = mailbox_init(self.stage, world, rank)
+            infos = [None] * world
+            dist.all_gather_object(infos, (h, addr, os.getpid()), group=group)
+            mailbox_connect(self.stage, [i[0] for i in infos],
+                            [i[1] if i[2] == os.getpid() else 0 for i in infos])
+
+    def depth_async(self, n: int, depth: int, strategy: Strategy, out: StageOutputs, gain: float = 1.0,
+                    eps_div: float = 0.0,
+                    after_exchange: Optional[Callable[[torch.Tensor], None]] = None) -> PendingDepth:
+        """Phase 2 of a depth after factors(): the exchanges (collective or mailbox), the decision
+        and the device-side global clip, without a host wait."""
+        if self.exchange == "mailbox":
+            p = self.stage.params(depth, strategy, gain, eps_div, n_pixels=self.n_pixels_total)
+            return mailbox_depth(self.stage, n, p, out, self._total, dist.get_world_size(self.group),
+                                 dist.get_rank(self.group), self.capacity, self.n_pixels_total, after_exchange)
+        return sharded_depth_async(self._sum, lambda rs: self.decide(n, depth, strategy, out, rs, gain, eps_div),
+                                   self.capacity, self.n_pixels_total, self.stage, self.group, after_exchange)
 
     def factors(self, vertices, depth: int, strategy: Strategy, out: StageOutputs, eps_div: float = 0.0,
                 gain: float = 1.0) -> torch.Tensor:
@@ -283,6 +374,8 @@ class ShardedRrsStage:
             out.q_orig = torch.empty(n, dtype=torch.float32, device=self.device)
             out.u = torch.empty(n, dtype=torch.float32, device=self.device)
         local = self.factors(vertices, depth, strategy, out, eps_div, gain)
+        if self.exchange == "mailbox":
+            return out, self.depth_async(n, depth, strategy, out, gain, eps_div).resolve(rc)
         outcome = sharded_depth(local, lambda rs: self.decide(n, depth, strategy, out, rs, gain, eps_div),
                                 self.capacity, self.n_pixels_total, self.group, rc)
         return out, outcome

@@ -268,3 +268,9 @@ def test_sharded_depth_async_matches_sync():
         assert p.exitcode == 0
     for r in res:
         assert r[1] and r[2] and r[3], r
+
+
+def test_sharded_stage_rejects_unknown_exchange():
+    from paper_2510_07868_b200.sharded import ShardedRrsStage
+    with pytest.raises(ValueError, match="exchange"):
+        ShardedRrsStage(16, None, exchange="carrier-pigeon")
