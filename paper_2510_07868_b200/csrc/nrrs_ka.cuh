@@ -11,14 +11,32 @@ namespace nrrs {
 
 constexpr int kTileM = 128;           // vertices per MMA tile (UMMA M)
 
-// fp32 -> fp16 hi/lo split of two values with packed conversions
-// (x = hi + lo to ~22 bits).
+// fp32 -> fp16 hi/lo split of two values (x = hi + lo to ~22 bits).  The
+// residual is produced NEGATED, l = f16(hi - x): sm_100's mixed-precision subtract (f16 operand
+// minus f32, one FHADD per element) replaces unpacking hi to fp32 plus an fp32x2 subtract, and
+// hi - x is exact in fp32 either way.  Every MMA that consumes the lo operand sets the
+// instruction descriptor's negate-A bit (kIdescNegA), so the products are bit-identical.
+#ifndef NRRS_NEG_LO
+#define NRRS_NEG_LO 1
+#endif
+constexpr bool kNegLo = NRRS_NEG_LO != 0;
+constexpr uint32_t kIdescNegA = kNegLo ? (1u << 13) : 0u;  // tcgen05 instruction descriptor: negate A
 __device__ __forceinline__ void split2(float v0, float v1, uint32_t &h, uint32_t &l) {
     const __half2 hh = __float22half2_rn(make_float2(v0, v1));
-    const float2 b = __half22float2(hh);
-    const __half2 ll = __float22half2_rn(upk2(fsub2(pk2(v0, v1), pk2(b.x, b.y))));
     h = *reinterpret_cast<const uint32_t *>(&hh);
-    l = *reinterpret_cast<const uint32_t *>(&ll);
+    if (kNegLo) {
+        float r0, r1;
+        asm("{\n\t.reg .f16 a, b;\n\tmov.b32 {a, b}, %2;\n\t"
+            "sub.rn.f32.f16 %0, a, %3;\n\tsub.rn.f32.f16 %1, b, %4;\n\t}"
+            : "=f"(r0), "=f"(r1)
+            : "r"(h), "f"(v0), "f"(v1));
+        const __half2 ll = __float22half2_rn(make_float2(r0, r1));
+        l = *reinterpret_cast<const uint32_t *>(&ll);
+    } else {
+        const float2 b = __half22float2(hh);
+        const __half2 ll = __float22half2_rn(upk2(fsub2(pk2(v0, v1), pk2(b.x, b.y))));
+        l = *reinterpret_cast<const uint32_t *>(&ll);
+    }
 }
 
 
@@ -223,11 +241,11 @@ __device__ __forceinline__ void ws_issue(const SmemTail *st, int net, int layer,
         const uint32_t ah = tmem_base + col_a + 8u * k, al = ah + 16u;
         if (kMma3) {
             mma_f16_ts(d, ah, w, i1, k > 0 ? 1u : 0u);
-            mma_f16_ts(d, al, w, i1, 1u);
+            mma_f16_ts(d, al, w, i1 | kIdescNegA, 1u);  // A_lo holds -lo (split2)
             mma_f16_ts(d, ah, st->wdesc_lo[net][layer][k], i1, 1u);
         } else {
             mma_f16_ts(d, ah, w, i2, k > 0 ? 1u : 0u);
-            mma_f16_ts(d, al, w, i1, 1u);
+            mma_f16_ts(d, al, w, i1 | kIdescNegA, 1u);
         }
     }
     mma_commit(bar);
