@@ -158,3 +158,46 @@ def test_mailbox_single_rank_depths_and_graph_replay():
     np.testing.assert_array_equal(_np(out.k), _np(ref.k))
     st.close()
     ref_st.close()
+
+
+def test_mailbox_empty_rank_still_exchanges():
+    """A rank with no vertices this depth publishes a zero sum and a zero total (one-thread
+    kernels), so the other rank's waits complete and its clip sees the right base."""
+    n = npx = 20000
+    nets = orc.OracleNets(orc.VARIANT_NRRS, seed=1, randomize=True)
+    v = orc.gen_vertices(n, n_pixels=npx)
+    stages = [RrsStage(npx, mirror_nets(nets), seed=0) for _ in range(2)]
+    connect_mailboxes_in_process(stages)
+    sums = [torch.zeros(1, dtype=torch.float64, device="cuda") for _ in range(2)]
+    tots = [torch.zeros(1, dtype=torch.int64, device="cuda") for _ in range(2)]
+    outs = [stages[0].alloc_outputs(1, full=True), stages[1].alloc_outputs(n, full=True)]
+    bands = [(0, 0), (0, n)]  # rank 0 empty, rank 1 the whole film
+    for rk, st in enumerate(stages):
+        lo, hi = bands[rk]
+        p = st.params(2, Strategy(StrategyKind.Nrrs), RateControl().gain(), 0.0, n_pixels=npx)
+        _factors(st, to_dev(_band(v, lo, max(hi, lo))), hi - lo, p, outs[rk], sums[rk])
+    torch.cuda.synchronize()
+    for rk, st in enumerate(stages):
+        lo, hi = bands[rk]
+        p = st.params(2, Strategy(StrategyKind.Nrrs), RateControl().gain(), 0.0, n_pixels=npx)
+        _capi.check(st.handle, st.ctx.lib.nrrs_gpu_stage_decide_mbox(st.handle, hi - lo, C.byref(p),
+                                                                     C.byref(outs[rk].c()), tots[rk].data_ptr()))
+    torch.cuda.synchronize()
+    clips = []
+    for st in stages:
+        clip = torch.zeros(4, dtype=torch.int64, device="cuda")
+        _capi.check(st.handle, st.ctx.lib.nrrs_gpu_sharded_clip_mbox(st.handle, st.capacity, clip.data_ptr(),
+                                                                     None, None))
+        clips.append(clip)
+    torch.cuda.synchronize()
+    for st in stages:
+        mailbox_check(st)
+    ref_st = RrsStage(npx, mirror_nets(nets), seed=0)
+    ref, r = ref_st.run(to_dev(v), 2, Strategy(StrategyKind.Nrrs), rc=RateControl(), full=True)
+    torch.cuda.synchronize()
+    assert float(sums[0].item()) == 0.0 and int(tots[0].item()) == 0
+    assert [int(x) for x in _np(clips[0])] == [0, 0, r.spawned, r.dropped]
+    assert [int(x) for x in _np(clips[1])] == [0, r.spawned, r.spawned, r.dropped]
+    np.testing.assert_array_equal(_np(outs[1].k), _np(ref.k))
+    for st in stages + [ref_st]:
+        st.close()
