@@ -1330,14 +1330,13 @@ int nrrs_gpu_film_roll_acc(nrrs_gpu_ctx *ctx, float *d_i_acc, const float *d_i_c
 // Scratch of the deterministic grid-gradient scatter for n samples of `levels` levels.
 static int ensure_scatter(nrrs_gpu_ctx *ctx, uint64_t n, int levels, GridScatter *sc) {
     const uint64_t m = n * (uint64_t)levels * 8u;
-    CK(ctx, grow(ctx->d_gsc, ctx->cap_gsc, 6 * m));  // keys, keys_sorted, slots, slots_sorted, vals (2 words)
+    CK(ctx, grow(ctx->d_gsc, ctx->cap_gsc, 6 * m));  // keys, keys_sorted, vals, vals_sorted (2 words each)
     const uint64_t tb = grid_scatter_sort_bytes(m);
     CK(ctx, grow(ctx->d_gsc_tmp, ctx->cap_gsc_tmp, tb));
     sc->keys = ctx->d_gsc;
     sc->keys_sorted = ctx->d_gsc + m;
-    sc->slots = ctx->d_gsc + 2 * m;
-    sc->slots_sorted = ctx->d_gsc + 3 * m;
-    sc->vals = reinterpret_cast<float2 *>(ctx->d_gsc + 4 * m);
+    sc->vals = reinterpret_cast<float2 *>(ctx->d_gsc + 2 * m);
+    sc->vals_sorted = reinterpret_cast<float2 *>(ctx->d_gsc + 4 * m);
     sc->sort_tmp = ctx->d_gsc_tmp;
     sc->sort_tmp_bytes = tb;
     return NRRS_OK;

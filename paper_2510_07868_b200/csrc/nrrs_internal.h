@@ -253,8 +253,8 @@ struct TrainGrid {
 // entry then sums each entry's run sequentially in slot order -- the reference's own loop order
 // (hashgrid.cpp:84-103), so the gradient is bit-identical from run to run.
 struct GridScatter {
-    uint32_t *keys, *keys_sorted, *slots, *slots_sorted;  // [n * levels * 8]; keys pre-set to 0xFFFFFFFF
-    float2 *vals;                                          // [n * levels * 8]
+    uint32_t *keys, *keys_sorted;  // [n * levels * 8]; keys pre-set to 0xFFFFFFFF
+    float2 *vals, *vals_sorted;    // [n * levels * 8]; sorted along with the keys (stable)
     void *sort_tmp;
     size_t sort_tmp_bytes;
 };

@@ -215,59 +215,151 @@ __global__ void __launch_bounds__(256) stat_fwd_bwd_kernel(TrainStepParams p) {
     }
 }
 
-// weight / bias gradients from the workspace: CTA b sums samples [b*per, (b+1)*per)
+// weight / bias gradients from the workspace: CTA b sums samples [b*per, (b+1)*per).  Each thread
+// owns a 4 (output row) x 4 (input column) block of one layer's [W | b] (the bias is input column
+// `li`, whose value is 1) and accumulates it over the CTA's samples in sample order with one FMA
+// per entry and sample -- the order and arithmetic of a per-parameter loop, so the partials are
+// bit-identical to it -- reading two 16-byte vectors (4 deltas, 4 inputs) per sample from the
+// staged chunk instead of two scalars per entry.  Blocks: 3 x (8 x ceil((li + 1) / 4)) for the
+// three 32-wide layers plus ceil(OUT / 4) x 9 for the head: <= 234 of the 256 threads.
 template <int OUT>
 __global__ void __launch_bounds__(256) mlp_dw_kernel(const float *ws, uint64_t n, int in, uint64_t per,
                                                      float *partials) {
-    __shared__ float st[kDwChunk][kWs];
+    static_assert(OUT <= 8, "head deltas: 8 workspace slots");
+    __shared__ __align__(16) float st[kDwChunk][kWs];
     const int tid = threadIdx.x, P = mlp_params(in, OUT);
-    constexpr int kMaxOwn = 14;  // ceil(3366 / 256)
-    float acc[kMaxOwn];
-    int doff[kMaxOwn], ioff[kMaxOwn];
-#pragma unroll
-    for (int k = 0; k < kMaxOwn; ++k) {
-        acc[k] = 0.0f;
-        doff[k] = -1;
-        ioff[k] = -1;
-        const int q = tid + 256 * k;
-        if (q >= P)
-            continue;
-        int l = 3;
-        while (l > 0 && q < stat_layer_offset(in, l))
-            --l;
-        const int li = l == 0 ? in : kTH, lo = l == 3 ? OUT : kTH;
-        const int e = q - stat_layer_offset(in, l);
-        if (e < lo * li) {  // column-major W: e = c * lo + r
-            doff[k] = 4 * kTH + kTH * l + e % lo;
-            ioff[k] = kTH * l + e / lo;
-        } else {            // bias r
-            doff[k] = 4 * kTH + kTH * l + (e - lo * li);
-            ioff[k] = -1;
+    // this thread's block: layer l, rows [r0, r0 + 4), columns [c0, c0 + 4)
+    int l = -1, r0 = 0, c0 = 0, t = tid;
+    for (int L = 0; L < 4 && l < 0; ++L) {
+        const int li = L == 0 ? in : kTH, lo = L == 3 ? OUT : kTH;
+        const int ct = (li + 1 + 3) / 4, nb = ((lo + 3) / 4) * ct;
+        if (t < nb) {
+            l = L;
+            r0 = 4 * (t / ct);
+            c0 = 4 * (t % ct);
+        } else {
+            t -= nb;
         }
     }
+    const int li = l == 0 ? in : kTH, lo = l == 3 ? OUT : kTH;
+    const int doff = 4 * kTH + kTH * (l < 0 ? 0 : l) + r0, ioff = kTH * (l < 0 ? 0 : l) + c0;
+    // column kinds: 0 input, 1 the bias column (value 1), 2 beyond
+    int kind[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+        kind[b] = c0 + b < li ? 0 : (c0 + b == li ? 1 : 2);
+    const bool edge = c0 + 3 >= li;
+    float acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+            acc[a][b] = 0.0f;
     const uint64_t s0 = (uint64_t)blockIdx.x * per, s1 = s0 + per < n ? s0 + per : n;
-    for (uint64_t c0 = s0; c0 < s1; c0 += kDwChunk) {
-        const int cnt = (int)(s1 - c0 < (uint64_t)kDwChunk ? s1 - c0 : (uint64_t)kDwChunk);
-        for (int i = tid; i < cnt * kWs; i += 256)
-            st[i / kWs][i % kWs] = ws[c0 * kWs + i];
-        __syncthreads();
+    // chunks of kDwChunk records (kWs floats each, contiguous) move as 16-byte vectors; the next
+    // chunk's vectors are loaded into registers before this chunk's FMAs, stored after them
+    constexpr int kV = kDwChunk * kWs / 4, kPerThread = (kV + 255) / 256;
+    static_assert(kWs % 4 == 0, "16-byte workspace records");
+    float4 *st4 = reinterpret_cast<float4 *>(&st[0][0]);
+    float4 nxt[kPerThread];
+    auto fetch = [&](uint64_t c) {
+        const int cnt = (int)(s1 - c < (uint64_t)kDwChunk ? s1 - c : (uint64_t)kDwChunk);
+        const float4 *src = reinterpret_cast<const float4 *>(ws + c * kWs);
 #pragma unroll
-        for (int k = 0; k < kMaxOwn; ++k) {
-            if (doff[k] < 0)
-                continue;
-            float a = acc[k];
-            for (int j = 0; j < cnt; ++j)
-                a += st[j][doff[k]] * (ioff[k] >= 0 ? st[j][ioff[k]] : 1.0f);
-            acc[k] = a;
+        for (int u = 0; u < kPerThread; ++u) {
+            const int v = tid + 256 * u;
+            nxt[u] = v < cnt * (kWs / 4) ? __ldcs(src + v) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        }
+    };
+    if (s0 < s1)
+        fetch(s0);
+    for (uint64_t c = s0; c < s1; c += kDwChunk) {
+        const int cnt = (int)(s1 - c < (uint64_t)kDwChunk ? s1 - c : (uint64_t)kDwChunk);
+#pragma unroll
+        for (int u = 0; u < kPerThread; ++u) {
+            const int v = tid + 256 * u;
+            if (v < kV)
+                st4[v] = nxt[u];
+        }
+        __syncthreads();
+        if (c + kDwChunk < s1)
+            fetch(c + kDwChunk);
+        if (l >= 0) {
+            for (int j = 0; j < cnt; ++j) {
+                const float4 d4 = *reinterpret_cast<const float4 *>(&st[j][doff]);
+                float4 x4 = *reinterpret_cast<const float4 *>(&st[j][ioff]);
+                if (edge) {
+                    x4.x = kind[0] == 0 ? x4.x : (kind[0] == 1 ? 1.0f : 0.0f);
+                    x4.y = kind[1] == 0 ? x4.y : (kind[1] == 1 ? 1.0f : 0.0f);
+                    x4.z = kind[2] == 0 ? x4.z : (kind[2] == 1 ? 1.0f : 0.0f);
+                    x4.w = kind[3] == 0 ? x4.w : (kind[3] == 1 ? 1.0f : 0.0f);
+                }
+                const float d[4] = {d4.x, d4.y, d4.z, d4.w}, x[4] = {x4.x, x4.y, x4.z, x4.w};
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b)
+                        acc[a][b] = fmaf(d[a], x[b], acc[a][b]);
+            }
         }
         __syncthreads();
     }
+    if (l < 0)
+        return;
+    const int base = stat_layer_offset(in, l);
 #pragma unroll
-    for (int k = 0; k < kMaxOwn; ++k) {
-        const int q = tid + 256 * k;
-        if (q < P)
-            partials[(uint64_t)blockIdx.x * P + q] = acc[k];
+    for (int a = 0; a < 4; ++a) {
+        const int r = r0 + a;
+        if (r >= lo)
+            continue;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int col = c0 + b;
+            if (kind[b] == 2)
+                continue;
+            const int q = base + (col < li ? col * lo + r : lo * li + r);  // column-major W, then bias
+            partials[(uint64_t)blockIdx.x * P + q] = acc[a][b];
+        }
     }
+}
+
+// Sequential sum of n values p[0], p[stride], ... in index order, with kB loads in flight per round
+// trip (the adds keep the order, so the result equals the plain loop's).
+template <typename T>
+__device__ __forceinline__ T ordered_sum(const T *p, int n, uint64_t stride) {
+    constexpr int kB = 16;
+    T s = T(0);
+    for (int b0 = 0; b0 < n; b0 += kB) {
+        T v[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u)
+            v[u] = b0 + u < n ? p[(uint64_t)(b0 + u) * stride] : T(0);
+#pragma unroll
+        for (int u = 0; u < kB; ++u)
+            if (b0 + u < n)
+                s += v[u];
+    }
+    return s;
+}
+
+// any non-finite entry of g[0, n) -> *flag (16-byte loads where aligned)
+__device__ __forceinline__ void flag_nonfinite(const float *g, uint64_t n, uint32_t *flag) {
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
+    bool bad = false;
+    if ((reinterpret_cast<uintptr_t>(g) & 15u) == 0) {
+        const float4 *g4 = reinterpret_cast<const float4 *>(g);
+        for (uint64_t i = tid; i < n / 4; i += nt) {
+            const float4 v = g4[i];
+            bad |= !isfinite(v.x) || !isfinite(v.y) || !isfinite(v.z) || !isfinite(v.w);
+        }
+        for (uint64_t i = n / 4 * 4 + tid; i < n; i += nt)
+            bad |= !isfinite(g[i]);
+    } else {
+        for (uint64_t i = tid; i < n; i += nt)
+            bad |= !isfinite(g[i]);
+    }
+    if (bad)
+        atomicOr(flag, 1u);
 }
 
 // g_mlp[q] = sum over CTAs (fixed order); loss = sum of block parts * inv_n; finite flags
@@ -276,22 +368,14 @@ __global__ void stat_reduce_kernel(const float *partials, int nparts, int P, flo
                                    uint32_t *nonfinite) {
     const int tid = threadIdx.x + blockIdx.x * blockDim.x;
     for (int q = tid; q < P; q += gridDim.x * blockDim.x) {
-        float s = 0.0f;
-        for (int b = 0; b < nparts; ++b)
-            s += partials[(uint64_t)b * P + q];
+        const float s = ordered_sum(partials + q, nparts, (uint64_t)P);
         g_mlp[q] = s;
         if (!isfinite(s))
             atomicOr(nonfinite, 1u);
     }
-    for (uint64_t i = tid; i < ngrid; i += (uint64_t)gridDim.x * blockDim.x)
-        if (!isfinite(g_grid[i]))
-            atomicOr(nonfinite, 1u);
-    if (tid == 0) {
-        double l = 0.0;
-        for (int b = 0; b < nloss; ++b)
-            l += loss_parts[b];
-        *loss_out = l * (double)inv_n;
-    }
+    flag_nonfinite(g_grid, ngrid, nonfinite);
+    if (tid == 0)
+        *loss_out = ordered_sum(loss_parts, nloss, 1) * (double)inv_n;
 }
 
 // grad *= inv_scale; Adam::step (optimizer.hpp:21-32); EmaTracker::update (:54-61)
@@ -555,24 +639,15 @@ __global__ void rrs_reduce_kernel(const float *partials, int nparts, int P, floa
                                   uint32_t *nonfinite) {
     const int tid = threadIdx.x + blockIdx.x * blockDim.x;
     for (int q = tid; q < P; q += gridDim.x * blockDim.x) {
-        float s = 0.0f;
-        for (int b = 0; b < nparts; ++b)
-            s += partials[(uint64_t)b * P + q];
+        const float s = ordered_sum(partials + q, nparts, (uint64_t)P);
         g_mlp[q] = s;
         if (!isfinite(s))
             atomicOr(nonfinite, 1u);
     }
-    for (uint64_t i = tid; i < ngrid; i += (uint64_t)gridDim.x * blockDim.x)
-        if (!isfinite(g_grid[i]))
-            atomicOr(nonfinite, 1u);
-    if (tid == 0) {
-        double t[3] = {0.0, 0.0, 0.0};
-        for (int b = 0; b < nblocks; ++b)
-            for (int j = 0; j < 3; ++j)
-                t[j] += parts[3 * b + j];
-        for (int j = 0; j < 3; ++j)
-            parts_out[j] = t[j];
-    }
+    if (g_grid)
+        flag_nonfinite(g_grid, ngrid, nonfinite);
+    if (tid < 3)  // the three loss-part columns, each summed over the blocks in order
+        parts_out[tid] = ordered_sum(parts + tid, nblocks, 3);
 }
 
 // ---- launchers ----
@@ -585,33 +660,58 @@ uint32_t train_dw_ctas(uint64_t n) {
 }
 
 // Sums each entry's run of sorted contributions in slot order (sample, level, corner), like the
-// reference's sequential encode_backward loop; one thread per run start.
+// reference's sequential encode_backward loop.  The contributions were sorted together with their
+// keys, so a run is contiguous in memory.  Each thread owns kFoldPer consecutive positions and sums
+// the runs that START there (16 keys / values in flight per round trip; the adds stay sequential).
+constexpr int kFoldPer = 8;
 __global__ void __launch_bounds__(256) grid_scatter_fold_kernel(GridScatter sc, uint64_t m, float *g_grid) {
-    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= m)
+    const uint64_t i0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kFoldPer;
+    if (i0 >= m)
         return;
-    const uint32_t key = sc.keys_sorted[i];
-    if (key == 0xFFFFFFFFu || (i > 0 && sc.keys_sorted[i - 1] == key))
-        return;
-    float a0 = 0.0f, a1 = 0.0f;
-    for (uint64_t j = i; j < m && sc.keys_sorted[j] == key; ++j) {
-        const float2 v = sc.vals[sc.slots_sorted[j]];
-        a0 = __fadd_rn(a0, v.x);
-        a1 = __fadd_rn(a1, v.y);
+    uint32_t prev = i0 > 0 ? sc.keys_sorted[i0 - 1] : 0xFFFFFFFEu;
+    uint32_t kk[kFoldPer];
+#pragma unroll
+    for (int e = 0; e < kFoldPer; ++e)
+        kk[e] = i0 + e < m ? sc.keys_sorted[i0 + e] : 0xFFFFFFFFu;
+#pragma unroll 1
+    for (int e = 0; e < kFoldPer; ++e) {
+        const uint32_t key = kk[e];
+        const bool start = key != 0xFFFFFFFFu && key != prev;
+        prev = key;
+        if (!start)
+            continue;
+        constexpr int kU = 16;
+        float a0 = 0.0f, a1 = 0.0f;
+        for (uint64_t j = i0 + e;; j += kU) {
+            uint32_t k[kU];
+            float2 v[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                k[u] = j + u < m ? sc.keys_sorted[j + u] : 0xFFFFFFFFu;
+                v[u] = j + u < m ? sc.vals_sorted[j + u] : make_float2(0.0f, 0.0f);
+            }
+            bool more = true;
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                more = more && k[u] == key;
+                if (more) {
+                    a0 = __fadd_rn(a0, v[u].x);
+                    a1 = __fadd_rn(a1, v[u].y);
+                }
+            }
+            if (!more)
+                break;
+        }
+        g_grid[key] = a0;
+        g_grid[key + 1] = a1;
     }
-    g_grid[key] = a0;
-    g_grid[key + 1] = a1;
-}
-
-__global__ void iota_kernel(uint32_t *out, uint64_t m) {
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
-        out[i] = (uint32_t)i;
 }
 
 size_t grid_scatter_sort_bytes(uint64_t contributions) {
     size_t bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t *)nullptr, (uint32_t *)nullptr,
-                                    (const uint32_t *)nullptr, (uint32_t *)nullptr, (int64_t)contributions, 0, 32);
+                                    (const unsigned long long *)nullptr, (unsigned long long *)nullptr,
+                                    (int64_t)contributions, 0, 32);
     return bytes;
 }
 
@@ -622,13 +722,14 @@ static cudaError_t grid_scatter_reduce(const GridScatter &sc, uint64_t m, uint64
     int bits = 1;
     while ((1ull << bits) <= ngrid)
         ++bits;
-    iota_kernel<<<1024, 256, 0, stream>>>(sc.slots, m);
     size_t tmp = sc.sort_tmp_bytes;
-    cudaError_t e = cub::DeviceRadixSort::SortPairs(sc.sort_tmp, tmp, sc.keys, sc.keys_sorted, sc.slots,
-                                                    sc.slots_sorted, (int64_t)m, 0, bits, stream);
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(
+        sc.sort_tmp, tmp, sc.keys, sc.keys_sorted, reinterpret_cast<const unsigned long long *>(sc.vals),
+        reinterpret_cast<unsigned long long *>(sc.vals_sorted), (int64_t)m, 0, bits, stream);
     if (e != cudaSuccess)
         return e;
-    grid_scatter_fold_kernel<<<(uint32_t)((m + 255) / 256), 256, 0, stream>>>(sc, m, g_grid);
+    const uint64_t threads = (m + kFoldPer - 1) / kFoldPer;
+    grid_scatter_fold_kernel<<<(uint32_t)((threads + 255) / 256), 256, 0, stream>>>(sc, m, g_grid);
     return cudaGetLastError();
 }
 
