@@ -78,7 +78,79 @@ __device__ __forceinline__ void grid_corners(const TrainGrid &g, int l, const fl
     }
 }
 
-__global__ void __launch_bounds__(256) stat_fwd_bwd_kernel(TrainStepParams p) {
+// One 32-wide layer z = W a + b (W column-major [c][r] in smem, mlp.cpp:63-66): per output r the
+// sum over c runs in order with one FMA per term -- the plain loop's arithmetic.  LI > 0: the input
+// width is a compile-time constant, the loops unroll (a, z stay in registers) and W is read as
+// 16-byte vectors of four outputs; LI == 0: the runtime width `li`.
+template <int LI>
+__device__ __forceinline__ void dense_fwd(const float *W, const float *b, int li, const float (&a)[kTH],
+                                          float (&z)[kTH]) {
+    if constexpr (LI > 0) {
+#pragma unroll
+        for (int r = 0; r < kTH; ++r)
+            z[r] = 0.0f;
+#pragma unroll
+        for (int c = 0; c < LI; ++c) {
+            asm volatile("" ::: "memory");  // one column's W in flight at a time (no hoisting into spills)
+            const float ac = a[c];
+#pragma unroll
+            for (int r4 = 0; r4 < kTH / 4; ++r4) {
+                const float4 w4 = *reinterpret_cast<const float4 *>(W + c * kTH + 4 * r4);
+                z[4 * r4] = fmaf(w4.x, ac, z[4 * r4]);
+                z[4 * r4 + 1] = fmaf(w4.y, ac, z[4 * r4 + 1]);
+                z[4 * r4 + 2] = fmaf(w4.z, ac, z[4 * r4 + 2]);
+                z[4 * r4 + 3] = fmaf(w4.w, ac, z[4 * r4 + 3]);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < kTH; ++r)
+            z[r] = z[r] + b[r];
+    } else {
+        for (int r = 0; r < kTH; ++r) {
+            float acc = 0.0f;
+            for (int c = 0; c < li; ++c)
+                acc += W[c * kTH + r] * a[c];
+            z[r] = acc + b[r];
+        }
+    }
+}
+
+// da = W^T delta for one 32-wide layer (mlp.cpp:74-111): per input c the sum over r in order.
+template <int LI>
+__device__ __forceinline__ void dense_bwd(const float *W, int li, const float (&delta)[kTH], float (&da)[kTH]) {
+    if constexpr (LI > 0) {
+#pragma unroll
+        for (int c = 0; c < LI; ++c) {
+            asm volatile("" ::: "memory");
+            float acc = 0.0f;
+#pragma unroll
+            for (int r4 = 0; r4 < kTH / 4; ++r4) {
+                const float4 w4 = *reinterpret_cast<const float4 *>(W + c * kTH + 4 * r4);
+                acc = fmaf(w4.x, delta[4 * r4], acc);
+                acc = fmaf(w4.y, delta[4 * r4 + 1], acc);
+                acc = fmaf(w4.z, delta[4 * r4 + 2], acc);
+                acc = fmaf(w4.w, delta[4 * r4 + 3], acc);
+            }
+            da[c] = acc;
+        }
+    } else {
+        for (int c = 0; c < li; ++c) {
+            float acc = 0.0f;
+            for (int r = 0; r < kTH; ++r)
+                acc += W[c * kTH + r] * delta[r];
+            da[c] = acc;
+        }
+    }
+}
+
+// 32 floats to a 16-byte-aligned workspace row slice
+__device__ __forceinline__ void store32(float *dst, const float (&v)[kTH]) {
+#pragma unroll
+    for (int i = 0; i < kTH / 4; ++i)
+        reinterpret_cast<float4 *>(dst)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+}
+
+__global__ void __launch_bounds__(256) stat_fwd_bwd_kernel(TrainStepParams p) {  // any grid / input width
     extern __shared__ float w_s[];
     const int tid = threadIdx.x;
     const int in = p.in, P = stat_param_count(in);
@@ -191,6 +263,167 @@ __global__ void __launch_bounds__(256) stat_fwd_bwd_kernel(TrainStepParams p) {
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
                         const uint64_t slot = (s * (uint64_t)p.grid.levels + (uint64_t)lv) * 8u + (uint64_t)k;
+                        p.scatter.keys[slot] = base[k];
+                        p.scatter.vals[slot] = make_float2(w[k] * da[2 * lv], w[k] * da[2 * lv + 1]);
+                    }
+                }
+            }
+        }
+    }
+    // block sum of the per-sample loss terms (fixed order) -> loss_parts[block]
+    __shared__ double red[8];
+    double v = my_loss;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((tid & 31) == 0)
+        red[tid >> 5] = v;
+    __syncthreads();
+    if (tid == 0) {
+        double b = 0.0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i)
+            b += red[i];
+        p.loss_parts[blockIdx.x] = b;
+    }
+}
+
+// The default grid (8 levels, StatNet input 32) with compile-time widths: the same arithmetic in
+// the same order as stat_fwd_bwd_kernel, with the arrays in registers and W read as 16-byte vectors.
+#ifndef NRRS_TRAIN_MINB
+#define NRRS_TRAIN_MINB 1
+#endif
+template <int LV, int IN>
+__global__ void __launch_bounds__(256, NRRS_TRAIN_MINB) stat_fwd_bwd_fast_kernel(TrainStepParams p) {
+    extern __shared__ __align__(16) float w_s[];
+    const int tid = threadIdx.x;
+    const int in = IN ? IN : p.in, levels = LV ? LV : p.grid.levels, P = stat_param_count(in);
+    for (int i = tid; i < P; i += blockDim.x)
+        w_s[i] = p.mlp[i];
+    __syncthreads();
+    const float slope = 0.01f;
+    const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + tid;
+    double my_loss = 0.0;
+    if (s < p.n) {
+        const nrrs_train_sample &t = p.batch[s];
+        float *ws = p.ws + s * kWs;
+        const int gd = 2 * levels;
+        float a[kTH];
+        // ---- encode_stat_inputs (networks.cpp:206-217): grid features, then the stat tail ----
+#pragma unroll
+        for (int l = 0; l < (LV ? LV : 8); ++l) {
+            if (!LV && l >= levels)
+                break;
+            uint32_t base[8];
+            float w[8];
+            grid_corners(p.grid, l, t.position, base, w);
+            float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                a0 += w[k] * __ldg(p.theta_grid + base[k]);
+                a1 += w[k] * __ldg(p.theta_grid + base[k] + 1);
+            }
+            a[2 * l] = a0;
+            a[2 * l + 1] = a1;
+            asm volatile("" ::: "memory");  // one level's 16 gathers in flight at a time (registers)
+        }
+        one_blob_exact(t.omega_o[0], 4, a + gd);
+        one_blob_exact(t.omega_o[1], 4, a + gd + 4);
+        one_blob_exact(1.0f - expf(-t.roughness), 8, a + gd + 8);  // roughness_remap (encodings.hpp:65-67)
+#pragma unroll
+        for (int i = 0; i < kTH; ++i)
+            if (i >= in)
+                a[i] = 0.0f;
+        store32(ws, a);
+        // ---- Mlp::forward (mlp.cpp:52-72), keeping post-activations ----
+#pragma unroll 1
+        for (int l = 0; l < 3; ++l) {
+            const int li = l == 0 ? in : kTH;
+            const float *W = w_s + stat_layer_offset(in, l), *b = W + kTH * li;
+            float z[kTH];
+            if (l == 0)
+                dense_fwd<IN>(W, b, li, a, z);
+            else
+                dense_fwd<(IN ? kTH : 0)>(W, b, li, a, z);
+#pragma unroll
+            for (int r = 0; r < kTH; ++r) {
+                const float zs = z[r] * slope;
+                a[r] = z[r] < zs ? zs : z[r];  // cwiseMax(z, slope z)
+            }
+            store32(ws + kTH * (l + 1), a);
+        }
+        float y[kTOut];
+        {
+            const float *W = w_s + stat_layer_offset(in, 3), *b = W + kTOut * kTH;
+#pragma unroll
+            for (int r = 0; r < kTOut; ++r) {
+                float acc = 0.0f;
+#pragma unroll
+                for (int c = 0; c < kTH; ++c)
+                    acc += W[c * kTOut + r] * a[c];
+                y[r] = acc + b[r];
+            }
+        }
+        // ---- relative L2 against (lo, lo^2) (networks.cpp:370-381) ----
+        float dy[kTOut];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const float lo = t.lo_sample[c];
+            const float t2 = lo * lo;
+            const float d1 = y[c] - lo, inv1 = 1.0f / (lo * lo + p.eps);
+            const float d2 = y[3 + c] - t2, inv2 = 1.0f / (t2 * t2 + p.eps);
+            my_loss += (double)(d1 * d1 * inv1) + (double)(d2 * d2 * inv2);
+            dy[c] = 2.0f * d1 * inv1 * p.inv_n * p.d_scale;
+            dy[3 + c] = 2.0f * d2 * inv2 * p.inv_n * p.d_scale;
+        }
+        // ---- Mlp::backward (mlp.cpp:74-111) ----
+        float *dws = ws + 4 * kTH;  // delta0 [32], delta1 [32], delta2 [32], delta3 [8]
+#pragma unroll
+        for (int r = 0; r < kTOut; ++r)
+            dws[3 * kTH + r] = dy[r];
+        float delta[kTH];
+        {
+            const float *W = w_s + stat_layer_offset(in, 3);
+#pragma unroll
+            for (int c = 0; c < kTH; ++c) {
+                float acc = 0.0f;
+#pragma unroll
+                for (int r = 0; r < kTOut; ++r)
+                    acc += W[c * kTOut + r] * dy[r];
+                delta[c] = a[c] <= 0.0f ? acc * slope : acc;  // post2 <= 0 <=> pre2 <= 0
+            }
+        }
+#pragma unroll 1
+        for (int l = 2; l >= 0; --l) {
+            store32(dws + kTH * l, delta);
+            const int li = l == 0 ? in : kTH;
+            const float *W = w_s + stat_layer_offset(in, l);
+            float da[kTH];
+            if (l == 0)
+                dense_bwd<IN>(W, li, delta, da);
+            else
+                dense_bwd<(IN ? kTH : 0)>(W, li, delta, da);
+            if (l > 0) {
+                const float4 *post = reinterpret_cast<const float4 *>(ws + kTH * l);  // post_{l-1}
+#pragma unroll
+                for (int c4 = 0; c4 < kTH / 4; ++c4) {
+                    const float4 q = post[c4];
+                    delta[4 * c4] = q.x <= 0.0f ? da[4 * c4] * slope : da[4 * c4];
+                    delta[4 * c4 + 1] = q.y <= 0.0f ? da[4 * c4 + 1] * slope : da[4 * c4 + 1];
+                    delta[4 * c4 + 2] = q.z <= 0.0f ? da[4 * c4 + 2] * slope : da[4 * c4 + 2];
+                    delta[4 * c4 + 3] = q.w <= 0.0f ? da[4 * c4 + 3] * slope : da[4 * c4 + 3];
+                }
+            } else {
+                // ---- HashGrid::encode_backward: grad[base + f] += w * d_x ----
+#pragma unroll
+                for (int lv = 0; lv < (LV ? LV : 8); ++lv) {
+                    if (!LV && lv >= levels)
+                        break;
+                    uint32_t base[8];
+                    float w[8];
+                    grid_corners(p.grid, lv, t.position, base, w);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const uint64_t slot = (s * (uint64_t)levels + (uint64_t)lv) * 8u + (uint64_t)k;
                         p.scatter.keys[slot] = base[k];
                         p.scatter.vals[slot] = make_float2(w[k] * da[2 * lv], w[k] * da[2 * lv + 1]);
                     }
@@ -633,6 +866,252 @@ __global__ void __launch_bounds__(256) rrs_fwd_bwd_kernel(RrsStepParams p) {
     }
 }
 
+// snapshot_stats for the default grid (8 levels, StatNet input 32), compile-time widths
+__device__ __forceinline__ void snapshot_stats_fast(const RrsStepParams &p, const float *w_stat,
+                                                    const nrrs_train_sample &t, float st[6]) {
+    constexpr int kLv = 8, gd = 2 * kLv, in = gd + 16;
+    float a[kTH];
+#pragma unroll
+    for (int l = 0; l < kLv; ++l) {
+        uint32_t base[8];
+        float w[8];
+        grid_corners(p.grid, l, t.position, base, w);
+        float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            a0 += w[k] * __ldg(p.snap_grid + base[k]);
+            a1 += w[k] * __ldg(p.snap_grid + base[k] + 1);
+        }
+        a[2 * l] = a0;
+        a[2 * l + 1] = a1;
+        asm volatile("" ::: "memory");
+    }
+    one_blob_exact(t.omega_o[0], 4, a + gd);
+    one_blob_exact(t.omega_o[1], 4, a + gd + 4);
+    one_blob_exact(1.0f - expf(-t.roughness), 8, a + gd + 8);
+#pragma unroll 1
+    for (int l = 0; l < 3; ++l) {
+        const float *W = w_stat + stat_layer_offset(in, l), *b = W + kTH * kTH;
+        float z[kTH];
+        dense_fwd<kTH>(W, b, kTH, a, z);
+#pragma unroll
+        for (int r = 0; r < kTH; ++r) {
+            const float zs = z[r] * 0.01f;
+            a[r] = z[r] < zs ? zs : z[r];
+        }
+    }
+    const float *W = w_stat + stat_layer_offset(in, 3), *b = W + kTOut * kTH;
+#pragma unroll
+    for (int r = 0; r < kTOut; ++r) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int c = 0; c < kTH; ++c)
+            acc += W[c * kTOut + r] * a[c];
+        st[r] = acc + b[r];
+    }
+}
+
+// rrs_fwd_bwd_kernel for the default grid with compile-time widths (VAR 0: NRRS, 11 inputs; 1: AID,
+// own grid + tail, 32 inputs): the same arithmetic in the same order, arrays in registers, W read as
+// 16-byte vectors.  The RRSNet weights start at a 16-byte boundary after the StatNet's (w_rrs_off).
+__host__ __device__ constexpr int rrs_w_offset(int ps) { return (ps + 3) & ~3; }
+template <int VAR>
+__global__ void __launch_bounds__(256, NRRS_TRAIN_MINB) rrs_fwd_bwd_fast_kernel(RrsStepParams p) {
+    extern __shared__ __align__(16) float w_s[];
+    constexpr int kLv = 8, gd = 2 * kLv, kIn = VAR ? gd + 16 : 11;
+    const int tid = threadIdx.x;
+    const int Ps = stat_param_count(gd + 16), Pr = mlp_params(kIn, 1);
+    float *w_stat = w_s, *w_rrs = w_s + rrs_w_offset(Ps);
+    for (int i = tid; i < Ps; i += blockDim.x)
+        w_stat[i] = p.snap_mlp[i];
+    for (int i = tid; i < Pr; i += blockDim.x)
+        w_rrs[i] = p.rrs_mlp[i];
+    __syncthreads();
+    const float slope = 0.01f;
+    const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + tid;
+    double pmin = 0.0, pavg = 0.0, prrs = 0.0;
+    uint32_t skipped = 0;
+    if (s < p.n) {
+        const nrrs_train_sample &t = p.batch[s];
+        float *ws = p.ws + s * kWs;
+        float st[6];
+        snapshot_stats_fast(p, w_stat, t, st);
+        float a[kTH];
+        const float imean = (t.i_pixel[0] + (t.i_pixel[1] + t.i_pixel[2])) / 3.0f;
+        if (VAR == 0) {  // build_nrrs_input (networks.cpp:137-147)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                a[c] = box_cox_exact(st[c]);
+                a[3 + c] = box_cox_exact(st[3 + c]);
+                a[6 + c] = box_cox_exact(t.t_x[c]);
+            }
+            a[9] = box_cox_exact(imean);
+            a[10] = 1.0f - expf(-t.roughness);
+        } else {         // AID: own grid + build_aid_tail (networks.cpp:149-157)
+#pragma unroll
+            for (int l = 0; l < kLv; ++l) {
+                uint32_t base[8];
+                float w[8];
+                grid_corners(p.grid, l, t.position, base, w);
+                float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    a0 += w[k] * __ldg(p.rrs_grid + base[k]);
+                    a1 += w[k] * __ldg(p.rrs_grid + base[k] + 1);
+                }
+                a[2 * l] = a0;
+                a[2 * l + 1] = a1;
+                asm volatile("" ::: "memory");
+            }
+            one_blob_exact(t.omega_o[0], 4, a + gd);
+            one_blob_exact(t.omega_o[1], 4, a + gd + 4);
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                a[gd + 8 + c] = box_cox_exact(t.t_x[c]);
+            a[gd + 11] = box_cox_exact(imean);
+            one_blob_exact(1.0f - expf(-t.roughness), 4, a + gd + 12);
+        }
+#pragma unroll
+        for (int i = kIn; i < kTH; ++i)
+            a[i] = 0.0f;
+        store32(ws, a);
+#pragma unroll 1
+        for (int l = 0; l < 3; ++l) {
+            const int li = l == 0 ? kIn : kTH;
+            const float *W = w_rrs + stat_layer_offset(kIn, l), *b = W + kTH * li;
+            float z[kTH];
+            if (l == 0)
+                dense_fwd<kIn>(W, b, li, a, z);
+            else
+                dense_fwd<kTH>(W, b, li, a, z);
+#pragma unroll
+            for (int r = 0; r < kTH; ++r) {
+                const float zs = z[r] * slope;
+                a[r] = z[r] < zs ? zs : z[r];
+            }
+            store32(ws + kTH * (l + 1), a);
+        }
+        const float *Wh = w_rrs + stat_layer_offset(kIn, 3);
+        float zacc = 0.0f;
+#pragma unroll
+        for (int c = 0; c < kTH; ++c)
+            zacc += Wh[c] * a[c];
+        const float z = zacc + Wh[kTH];
+        const float q = z < 0.0f ? log1pf(expf(z)) : 0.5f * z + 0.6931471805599453f;  // softplus_mod
+        float d_q = 0.0f;
+        if (p.phase == 0) {
+            const float d = q - 1.0f, inv = 1.0f / (1.0f + p.eps);
+            prrs += (double)(d * d * inv);
+            d_q = 2.0f * d * inv * p.inv_n;
+        } else {
+            const uint32_t px = t.pixel;
+            const float inv_k = t.k_i > 0.0f ? 1.0f / t.k_i : 1.0f;
+            if (px < p.n_errors) {
+                const float pe_e = p.errors[2 * px], pe_inv = p.errors[2 * px + 1];
+                float gvar = 0.0f;
+                const float wl = luminance(t.t_x[0], t.t_x[1], t.t_x[2]);
+                if (t.q_real < 1.0f) {
+                    if (t.q_real > 0.0f) {
+                        const float hl = luminance(t.lo_sample[0], t.lo_sample[1], t.lo_sample[2]);
+                        gvar = -(wl * wl) * (hl * hl) / (t.q_real * t.q_real);
+                    }
+                } else {
+                    float var[3];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const float v = st[3 + c] - st[c] * st[c];
+                        var[c] = v < 0.0f ? 0.0f : v;
+                    }
+                    gvar = -(wl * wl) * luminance(var[0], var[1], var[2]) / (t.q_real * t.q_real);
+                }
+                const float de_dq = pe_inv * gvar * inv_k;
+                pmin += (double)(pe_e * inv_k);
+                const float dev = pe_e - p.e_avg;
+                pavg += (double)(dev * dev * inv_k);
+                d_q += (p.gamma_min * de_dq + p.gamma_avg * 2.0f * dev * de_dq) * p.inv_n;
+            } else {
+                skipped = 1;
+            }
+            const float gap = q - t.q_norm;
+            prrs += (double)(gap * gap);
+            d_q += p.gamma_rrs * 2.0f * gap * p.inv_n;
+        }
+        const float sg = z < 0.0f ? expf(z) / (1.0f + expf(z)) : 0.5f;  // softplus_mod_grad
+        const float dy = d_q * sg * p.d_scale;
+        float *dws = ws + 4 * kTH;
+        dws[3 * kTH] = dy;
+        float delta[kTH];
+#pragma unroll
+        for (int c = 0; c < kTH; ++c) {
+            const float acc = Wh[c] * dy;
+            delta[c] = a[c] <= 0.0f ? acc * slope : acc;
+        }
+#pragma unroll 1
+        for (int l = 2; l >= 0; --l) {
+            store32(dws + kTH * l, delta);
+            const int li = l == 0 ? kIn : kTH;
+            const float *W = w_rrs + stat_layer_offset(kIn, l);
+            float da[kTH];
+            if (l == 0)
+                dense_bwd<kIn>(W, li, delta, da);
+            else
+                dense_bwd<kTH>(W, li, delta, da);
+            if (l > 0) {
+                const float4 *post = reinterpret_cast<const float4 *>(ws + kTH * l);
+#pragma unroll
+                for (int c4 = 0; c4 < kTH / 4; ++c4) {
+                    const float4 q4 = post[c4];
+                    delta[4 * c4] = q4.x <= 0.0f ? da[4 * c4] * slope : da[4 * c4];
+                    delta[4 * c4 + 1] = q4.y <= 0.0f ? da[4 * c4 + 1] * slope : da[4 * c4 + 1];
+                    delta[4 * c4 + 2] = q4.z <= 0.0f ? da[4 * c4 + 2] * slope : da[4 * c4 + 2];
+                    delta[4 * c4 + 3] = q4.w <= 0.0f ? da[4 * c4 + 3] * slope : da[4 * c4 + 3];
+                }
+            } else if (VAR == 1 && p.g_grid) {
+#pragma unroll
+                for (int lv = 0; lv < kLv; ++lv) {
+                    uint32_t base[8];
+                    float w[8];
+                    grid_corners(p.grid, lv, t.position, base, w);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const uint64_t slot = (s * (uint64_t)kLv + (uint64_t)lv) * 8u + (uint64_t)k;
+                        p.scatter.keys[slot] = base[k];
+                        p.scatter.vals[slot] = make_float2(w[k] * da[2 * lv], w[k] * da[2 * lv + 1]);
+                    }
+                }
+            }
+        }
+    }
+    __shared__ double red[3][8];
+    __shared__ uint32_t reds[8];
+    double v[3] = {pmin, pavg, prrs};
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+            v[j] += __shfl_xor_sync(0xffffffffu, v[j], o);
+    const uint32_t sk = __reduce_add_sync(0xffffffffu, skipped);
+    if ((tid & 31) == 0) {
+        for (int j = 0; j < 3; ++j)
+            red[j][tid >> 5] = v[j];
+        reds[tid >> 5] = sk;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double b[3] = {0.0, 0.0, 0.0};
+        uint32_t bs = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+            for (int j = 0; j < 3; ++j)
+                b[j] += red[j][i];
+            bs += reds[i];
+        }
+        for (int j = 0; j < 3; ++j)
+            p.parts[3 * blockIdx.x + j] = b[j];
+        if (bs)
+            atomicAdd(p.skipped, bs);
+    }
+}
+
 // g_mlp = sum of CTA partials (fixed order), loss parts summed over blocks, finite flags
 __global__ void rrs_reduce_kernel(const float *partials, int nparts, int P, float *g_mlp, const double *parts,
                                   int nblocks, double *parts_out, const float *g_grid, uint64_t ngrid,
@@ -737,14 +1216,20 @@ cudaError_t launch_stat_train(const TrainStepParams &p, float *partials, uint32_
                               double *loss_out, uint32_t *nonfinite, uint64_t ngrid, cudaStream_t stream) {
     const uint32_t blocks = (uint32_t)((p.n + 255) / 256);
     const size_t smem = (size_t)stat_param_count(p.in) * sizeof(float);
-    cudaError_t e = cudaFuncSetAttribute(stat_fwd_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(stat_fwd_bwd_fast_kernel<8, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(stat_fwd_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
         return e;
     const uint64_t m = p.n * (uint64_t)p.grid.levels * 8u;
     e = cudaMemsetAsync(p.scatter.keys, 0xFF, m * sizeof(uint32_t), stream);
     if (e != cudaSuccess)
         return e;
-    stat_fwd_bwd_kernel<<<blocks, 256, smem, stream>>>(p);
+    if (p.grid.levels == 8 && p.in == 32)  // the default grid: compile-time widths
+        stat_fwd_bwd_fast_kernel<8, 32><<<blocks, 256, smem, stream>>>(p);
+    else
+        stat_fwd_bwd_kernel<<<blocks, 256, smem, stream>>>(p);
     e = grid_scatter_reduce(p.scatter, m, ngrid, p.g_grid, stream);
     if (e != cudaSuccess)
         return e;
@@ -759,8 +1244,13 @@ cudaError_t launch_rrs_train(const RrsStepParams &p, float *partials, uint32_t d
                              double *parts_out, uint32_t *nonfinite, uint64_t ngrid, cudaStream_t stream) {
     const uint32_t blocks = (uint32_t)((p.n + 255) / 256);
     const int gd = 2 * p.grid.levels;
-    const size_t smem = (size_t)(stat_param_count(gd + 16) + mlp_params(p.in, 1)) * sizeof(float);
+    const size_t smem = (size_t)(rrs_w_offset(stat_param_count(gd + 16)) + mlp_params(p.in, 1)) * sizeof(float);
+    const int fast = p.grid.levels != 8 ? -1 : (p.variant == 0 && p.in == 11 ? 0 : (p.variant == 1 && p.in == 32 ? 1 : -1));
     cudaError_t e = cudaFuncSetAttribute(rrs_fwd_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(rrs_fwd_bwd_fast_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(rrs_fwd_bwd_fast_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
         return e;
     const uint64_t m = p.n * (uint64_t)p.grid.levels * 8u;
@@ -769,7 +1259,12 @@ cudaError_t launch_rrs_train(const RrsStepParams &p, float *partials, uint32_t d
         if (e != cudaSuccess)
             return e;
     }
-    rrs_fwd_bwd_kernel<<<blocks, 256, smem, stream>>>(p);
+    if (fast == 0)
+        rrs_fwd_bwd_fast_kernel<0><<<blocks, 256, smem, stream>>>(p);
+    else if (fast == 1)
+        rrs_fwd_bwd_fast_kernel<1><<<blocks, 256, smem, stream>>>(p);
+    else
+        rrs_fwd_bwd_kernel<<<blocks, 256, smem, stream>>>(p);
     if (p.variant == 1 && p.g_grid) {
         e = grid_scatter_reduce(p.scatter, m, ngrid, p.g_grid, stream);
         if (e != cudaSuccess)
