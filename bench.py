@@ -684,16 +684,17 @@ def main():
         torch.cuda.synchronize()
         dec_us = a.elapsed_time(z) * 1e3 / 1000
         st1.close()
-        # AID at C1 through the default routing and the opt-in fused single kernel
+        # AID at C1 through the default routing (the fused single-kernel stage up to 196,608
+        # vertices) and through K-A0 + K-A + K-B (NRRS_FUSED=0)
         st2 = RrsStage(n1, nets, device=local)
         _, aid_call = graph_us(st2, StrategyKind.AidNrrs, RrsVariant.Aid)
         st2.close()
-        os.environ["NRRS_FUSED"] = "1"
+        os.environ["NRRS_FUSED"] = "0"
         try:
             st3 = RrsStage(n1, nets, device=local)
         finally:
             del os.environ["NRRS_FUSED"]
-        _, aid_fused_call = graph_us(st3, StrategyKind.AidNrrs, RrsVariant.Aid)
+        _, aid_3k_call = graph_us(st3, StrategyKind.AidNrrs, RrsVariant.Aid)
         st3.close()
         # CPU port of the same NRRS step and decision-only step on this host
         vc = orc_c1.gen_vertices(n1)
@@ -711,7 +712,7 @@ def main():
                              "hbm_gbs": (STAGE_READ + STAGE_WRITE + 8 * 0.85) * n1 / (per_call / 1e6) / 1e9},
               "decision_only_split_bound4": {"graph_us_per_call": dec_us, "vertices_per_s": n1 / (dec_us / 1e6),
                                              "kernel": "decide3 (normalize, gain, stochastic round, prefix, slots)"},
-              "aid_stage_graph_us_per_call": aid_call, "aid_fused_kernel_graph_us_per_call": aid_fused_call,
+              "aid_stage_graph_us_per_call": aid_call, "aid_three_kernel_graph_us_per_call": aid_3k_call,
               "cpu_port": {"nrrs_stage_vertices_per_s": n1 / cpu_stage_s, "cores": thr,
                            "sample": "the same 65,536-vertex NRRS step (oracle port), mean of 3"},
               "note": "launch-bound: ~2-3 kernels per call; the per-call floor of two dependent launches on "

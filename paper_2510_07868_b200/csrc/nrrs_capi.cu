@@ -163,7 +163,8 @@ struct nrrs_gpu_ctx {
     // tuning / test switches, read once at nrrs_gpu_create (never on the per-call path)
     bool env_no_level_kernel = false;  // NRRS_NO_LEVEL_KERNEL: AID through the fused-gather K-A
     bool env_fp32_tables = false;      // NRRS_FP32_TABLES: keep the AID grid in fp32
-    bool env_fused = false;            // NRRS_FUSED: AID through the fused single-kernel stage (nrrs_fused.cu)
+    int env_fused = -1;                // NRRS_FUSED: AID through the fused single-kernel stage (nrrs_fused.cu):
+                                       // 1 always, 0 never, unset: batches up to kFusedAutoMaxN
     int env_sync_chunks = 0;           // NRRS_SYNC_CHUNKS / NRRS_ASYNC_CHUNKS: host-path H2D pieces (0: default)
     int env_async_chunks = 0;
 
@@ -412,7 +413,8 @@ int nrrs_gpu_create(int device, nrrs_gpu_ctx **out) {
     cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
     ctx->env_no_level_kernel = std::getenv("NRRS_NO_LEVEL_KERNEL") != nullptr;
     ctx->env_fp32_tables = std::getenv("NRRS_FP32_TABLES") != nullptr;
-    ctx->env_fused = std::getenv("NRRS_FUSED") != nullptr;
+    if (const char *f = std::getenv("NRRS_FUSED"))
+        ctx->env_fused = std::atoi(f) != 0 ? 1 : 0;
     set_pdl(std::getenv("NRRS_NO_PDL") == nullptr);  // PDL launches of K-A / K-B / K-C by default
     if (const char *sc = std::getenv("NRRS_SYNC_CHUNKS"))
         ctx->env_sync_chunks = std::max(1, std::min(std::atoi(sc), kMaxHostChunks));
@@ -1018,9 +1020,14 @@ static int run_decide(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_stage_params *p,
 // K-A0 + K-A + K-B on B200 (both halves are issue-bound, so sharing the SMs
 // adds their instruction streams), hence not the default.  Returns 1 (not applicable:
 // the caller runs K-A0 + K-A + K-B), 0 (launched) or an error status.
+// Default routing: up to this many vertices the one-launch fused stage is faster than K-A0 + K-A +
+// K-B (graph-replayed calls: 21.2 vs 24.3 us at 32,768, 23.7 vs 27.5 at 65,536, 29.7 vs 31.6 at
+// 131,072; 44.7 vs 43.2 at 262,144 and slower beyond), the batch being too small to fill the SMs
+// with K-A's eight chains, so one launch and no level-plane round trip decide it.
+constexpr uint64_t kFusedAutoMaxN = 196608;
 static int run_fused_stage(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, const nrrs_stage_params *p,
                            const nrrs_stage_out *o, uint32_t cap) {
-    if (!ctx->env_fused || ctx->env_no_level_kernel)
+    if (ctx->env_fused == 0 || (ctx->env_fused < 0 && n > kFusedAutoMaxN) || ctx->env_no_level_kernel)
         return 1;
     int kind = 0, heur = 0;
     int rc = select_kind(ctx, p->depth, p->strategy, &kind, &heur);

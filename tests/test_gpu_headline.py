@@ -62,7 +62,7 @@ def test_headline_size_parity(variant, kind, n):
 
 
 @pytest.mark.parametrize("n", [1920 * 1080, 65_536, 8 * 128 * 3 + 77])
-def test_fused_aid_stage_matches_three_kernel_path(n, monkeypatch):  # NRRS_FUSED=1 (opt-in path)
+def test_fused_aid_stage_matches_three_kernel_path(n, monkeypatch):  # NRRS_FUSED=1 vs =0
     """The fused AID stage (one persistent kernel: level-sliced encode over an L2 ring, tcgen05 MLP,
     in-kernel normalization / rounding / slot emission) against K-A0 + K-A + K-B on the same batch:
     identical q_orig and u (same per-row arithmetic), and identical decisions whenever float(F)
@@ -71,10 +71,7 @@ def test_fused_aid_stage_matches_three_kernel_path(n, monkeypatch):  # NRRS_FUSE
     on = orc.OracleNets(orc.VARIANT_AID, seed=1, randomize=True)
     outs = []
     for fused in (True, False):
-        if fused:
-            monkeypatch.setenv("NRRS_FUSED", "1")
-        else:
-            monkeypatch.delenv("NRRS_FUSED", raising=False)
+        monkeypatch.setenv("NRRS_FUSED", "1" if fused else "0")
         st = RrsStage(n, mirror_nets(on))
         out, res = st.run(to_dev(v), 2, Strategy(StrategyKind.AidNrrs), rc=RateControl(), full=True)
         torch.cuda.synchronize()

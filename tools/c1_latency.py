@@ -17,9 +17,9 @@ dv = {k: torch.from_numpy(a.view(np.int64) if a.dtype == np.uint64 else a).cuda(
       if k != "pixel"}
 
 
-def probe(name, variant, kind, env=None):
+def probe(name, variant, kind, env=None, val="1"):
     if env:
-        os.environ[env] = "1"
+        os.environ[env] = val
     try:
         nets = NeuralRrs(NeuralRrsConfig(variant=variant, seed=1)).randomize_for_benchmark()
         st = RrsStage(n, nets)
@@ -45,6 +45,7 @@ def probe(name, variant, kind, env=None):
 probe("aid (default routing)", RrsVariant.Aid, StrategyKind.AidNrrs)
 probe("aid (fused-gather K-A, no K-A0)", RrsVariant.Aid, StrategyKind.AidNrrs, "NRRS_NO_LEVEL_KERNEL")
 probe("aid (fused single kernel)", RrsVariant.Aid, StrategyKind.AidNrrs, "NRRS_FUSED")
+probe("aid (K-A0 + K-A + K-B)", RrsVariant.Aid, StrategyKind.AidNrrs, "NRRS_FUSED", "0")
 probe("nrrs", RrsVariant.Nrrs, StrategyKind.Nrrs)
 probe("nrrs (L2-gather K-A, no K-A0)", RrsVariant.Nrrs, StrategyKind.Nrrs, "NRRS_NO_LEVEL_KERNEL")
 probe("adrrs-nn (L2-gather K-A, no K-A0)", RrsVariant.Nrrs, StrategyKind.AdrrsNn, "NRRS_NO_LEVEL_KERNEL")
