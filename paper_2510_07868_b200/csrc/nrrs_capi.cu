@@ -219,6 +219,9 @@ struct nrrs_gpu_ctx {
     uint64_t cap_gsc = 0;
     uint8_t *d_gsc_tmp = nullptr;
     uint64_t cap_gsc_tmp = 0;
+    // per-level side streams of the scatter's segment sorts (created on first use)
+    cudaStream_t gsc_side[kScatterMaxLevels] = {};
+    cudaEvent_t gsc_fork = nullptr, gsc_join[kScatterMaxLevels] = {};
 
     // host-path pipeline: chunked H2D on copy_stream overlapped with K-A on `stream`
     cudaStream_t copy_stream = nullptr;
@@ -476,6 +479,16 @@ int nrrs_gpu_destroy(nrrs_gpu_ctx *ctx) {
     for (void *m : ctx->mbox_opened)
         if (m)
             cudaIpcCloseMemHandle(m);
+    for (int l = 0; l < kScatterMaxLevels; ++l) {
+        if (ctx->gsc_side[l]) {
+            cudaStreamSynchronize(ctx->gsc_side[l]);
+            cudaStreamDestroy(ctx->gsc_side[l]);
+        }
+        if (ctx->gsc_join[l])
+            cudaEventDestroy(ctx->gsc_join[l]);
+    }
+    if (ctx->gsc_fork)
+        cudaEventDestroy(ctx->gsc_fork);
     for (void *m : {(void *)ctx->d_mbox, (void *)ctx->d_mbox_dev, (void *)ctx->d_mbox_aux})
         if (m)
             cudaFree(m);
@@ -1335,17 +1348,36 @@ int nrrs_gpu_film_roll_acc(nrrs_gpu_ctx *ctx, float *d_i_acc, const float *d_i_c
 
 
 // Scratch of the deterministic grid-gradient scatter for n samples of `levels` levels.
-static int ensure_scatter(nrrs_gpu_ctx *ctx, uint64_t n, int levels, GridScatter *sc) {
-    const uint64_t m = n * (uint64_t)levels * 8u;
+static int ensure_scatter(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_grid_spec *spec, GridScatter *sc) {
+    const int levels = spec->levels;
+    if (levels < 1 || levels > kScatterMaxLevels)
+        return fail(ctx, NRRS_EINVAL, "training: 1..%d grid levels", kScatterMaxLevels);
+    const uint64_t seg = n * 8u, m = seg * (uint64_t)levels;
     CK(ctx, grow(ctx->d_gsc, ctx->cap_gsc, 6 * m));  // keys, keys_sorted, vals, vals_sorted (2 words each)
-    const uint64_t tb = grid_scatter_sort_bytes(m);
-    CK(ctx, grow(ctx->d_gsc_tmp, ctx->cap_gsc_tmp, tb));
+    const int end_bit = 1 + spec->log2_table_size;  // keys (level * T + entry) * 2: entry bits [1, end_bit)
+    const uint64_t tb = grid_scatter_sort_bytes(seg, end_bit);
+    CK(ctx, grow(ctx->d_gsc_tmp, ctx->cap_gsc_tmp, tb * (uint64_t)levels));
+    if (!ctx->gsc_fork) {
+        CK(ctx, cudaEventCreateWithFlags(&ctx->gsc_fork, cudaEventDisableTiming));
+        for (int l = 0; l < kScatterMaxLevels; ++l) {
+            CK(ctx, cudaStreamCreateWithFlags(&ctx->gsc_side[l], cudaStreamNonBlocking));
+            CK(ctx, cudaEventCreateWithFlags(&ctx->gsc_join[l], cudaEventDisableTiming));
+        }
+    }
     sc->keys = ctx->d_gsc;
     sc->keys_sorted = ctx->d_gsc + m;
     sc->vals = reinterpret_cast<float2 *>(ctx->d_gsc + 2 * m);
     sc->vals_sorted = reinterpret_cast<float2 *>(ctx->d_gsc + 4 * m);
     sc->sort_tmp = ctx->d_gsc_tmp;
-    sc->sort_tmp_bytes = tb;
+    sc->seg_tmp_bytes = tb;
+    sc->seg = seg;
+    sc->levels = levels;
+    sc->key_end_bit = end_bit;
+    sc->fork = ctx->gsc_fork;
+    for (int l = 0; l < kScatterMaxLevels; ++l) {
+        sc->side[l] = ctx->gsc_side[l];
+        sc->join[l] = ctx->gsc_join[l];
+    }
     return NRRS_OK;
 }
 
@@ -1397,7 +1429,7 @@ int nrrs_gpu_stat_loss_grad(nrrs_gpu_ctx *ctx, const nrrs_grid_spec *spec, const
     p.g_grid = d_g_grid;
     p.loss_parts = ctx->d_tloss;
     {
-        const int rc = ensure_scatter(ctx, n, spec->levels, &p.scatter);
+        const int rc = ensure_scatter(ctx, n, spec, &p.scatter);
         if (rc)
             return rc;
     }
@@ -1477,7 +1509,7 @@ int nrrs_gpu_rrs_loss_grad(nrrs_gpu_ctx *ctx, int32_t variant, const nrrs_grid_s
     p.ws = ctx->d_tws;
     p.g_grid = variant == 1 ? d_g_grid : nullptr;
     if (variant == 1) {
-        const int rc = ensure_scatter(ctx, n, spec->levels, &p.scatter);
+        const int rc = ensure_scatter(ctx, n, spec, &p.scatter);
         if (rc)
             return rc;
     }

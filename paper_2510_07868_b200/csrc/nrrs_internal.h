@@ -252,13 +252,23 @@ struct TrainGrid {
 // w * d_out goes to slot (s * levels + l) * 8 + c with its entry as key; a stable radix sort by
 // entry then sums each entry's run sequentially in slot order -- the reference's own loop order
 // (hashgrid.cpp:84-103), so the gradient is bit-identical from run to run.
+// Grid-gradient contributions, level-major: slot (level * n + sample) * 8 + corner, so each level's
+// contributions are one segment in (sample, corner) order and the per-entry order is the reference's
+// loop order (sample, level, corner).  Each segment is sorted by its own entry bits on its own
+// stream (levels run concurrently), the fold then walks the concatenation.
+constexpr int kScatterMaxLevels = 8;
 struct GridScatter {
     uint32_t *keys, *keys_sorted;  // [n * levels * 8]; keys pre-set to 0xFFFFFFFF
     float2 *vals, *vals_sorted;    // [n * levels * 8]; sorted along with the keys (stable)
-    void *sort_tmp;
-    size_t sort_tmp_bytes;
+    void *sort_tmp;                // levels x seg_tmp_bytes
+    size_t seg_tmp_bytes;
+    uint64_t seg;                  // contributions per level (n * 8)
+    int levels;
+    int key_end_bit;               // entry bits of a key within a level: [1, key_end_bit)
+    cudaStream_t side[kScatterMaxLevels];
+    cudaEvent_t fork, join[kScatterMaxLevels];
 };
-size_t grid_scatter_sort_bytes(uint64_t contributions);
+size_t grid_scatter_sort_bytes(uint64_t contributions, int end_bit);
 
 struct TrainStepParams {
     const nrrs_train_sample *batch;

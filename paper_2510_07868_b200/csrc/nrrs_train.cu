@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(256) stat_fwd_bwd_kernel(TrainStepParams p) { 
                     grid_corners(p.grid, lv, t.position, base, w);
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
-                        const uint64_t slot = (s * (uint64_t)p.grid.levels + (uint64_t)lv) * 8u + (uint64_t)k;
+                        const uint64_t slot = ((uint64_t)lv * p.n + s) * 8u + (uint64_t)k;  // level-major
                         p.scatter.keys[slot] = base[k];
                         p.scatter.vals[slot] = make_float2(w[k] * da[2 * lv], w[k] * da[2 * lv + 1]);
                     }
@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(256, NRRS_TRAIN_MINB) stat_fwd_bwd_fast_kernel
                     grid_corners(p.grid, lv, t.position, base, w);
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
-                        const uint64_t slot = (s * (uint64_t)levels + (uint64_t)lv) * 8u + (uint64_t)k;
+                        const uint64_t slot = ((uint64_t)lv * p.n + s) * 8u + (uint64_t)k;  // level-major
                         p.scatter.keys[slot] = base[k];
                         p.scatter.vals[slot] = make_float2(w[k] * da[2 * lv], w[k] * da[2 * lv + 1]);
                     }
@@ -828,7 +828,7 @@ __global__ void __launch_bounds__(256) rrs_fwd_bwd_kernel(RrsStepParams p) {
                     grid_corners(p.grid, lv, t.position, base, w);
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
-                        const uint64_t slot = (s * (uint64_t)p.grid.levels + (uint64_t)lv) * 8u + (uint64_t)k;
+                        const uint64_t slot = ((uint64_t)lv * p.n + s) * 8u + (uint64_t)k;  // level-major
                         p.scatter.keys[slot] = base[k];
                         p.scatter.vals[slot] = make_float2(w[k] * da[2 * lv], w[k] * da[2 * lv + 1]);
                     }
@@ -1074,7 +1074,7 @@ __global__ void __launch_bounds__(256, NRRS_TRAIN_MINB) rrs_fwd_bwd_fast_kernel(
                     grid_corners(p.grid, lv, t.position, base, w);
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
-                        const uint64_t slot = (s * (uint64_t)kLv + (uint64_t)lv) * 8u + (uint64_t)k;
+                        const uint64_t slot = ((uint64_t)lv * p.n + s) * 8u + (uint64_t)k;  // level-major
                         p.scatter.keys[slot] = base[k];
                         p.scatter.vals[slot] = make_float2(w[k] * da[2 * lv], w[k] * da[2 * lv + 1]);
                     }
@@ -1186,25 +1186,36 @@ __global__ void __launch_bounds__(256) grid_scatter_fold_kernel(GridScatter sc, 
     }
 }
 
-size_t grid_scatter_sort_bytes(uint64_t contributions) {
+size_t grid_scatter_sort_bytes(uint64_t contributions, int end_bit) {
     size_t bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t *)nullptr, (uint32_t *)nullptr,
                                     (const unsigned long long *)nullptr, (unsigned long long *)nullptr,
-                                    (int64_t)contributions, 0, 32);
-    return bytes;
+                                    (int64_t)contributions, 1, end_bit);
+    return (bytes + 255) & ~(size_t)255;
 }
 
-// keys of the grid's entries span [0, 2 * levels * T): sort just those bits (the 0xFFFFFFFF
-// sentinel of non-contributing slots sorts after every entry)
+// per level: stable sort of its segment by the entry bits [1, end_bit) of the keys (a level's keys
+// share their higher bits; the 0xFFFFFFFF sentinel of non-contributing slots sorts last) on the
+// level's side stream, all levels concurrently; then one fold over the whole array
 static cudaError_t grid_scatter_reduce(const GridScatter &sc, uint64_t m, uint64_t ngrid, float *g_grid,
                                        cudaStream_t stream) {
-    int bits = 1;
-    while ((1ull << bits) <= ngrid)
-        ++bits;
-    size_t tmp = sc.sort_tmp_bytes;
-    cudaError_t e = cub::DeviceRadixSort::SortPairs(
-        sc.sort_tmp, tmp, sc.keys, sc.keys_sorted, reinterpret_cast<const unsigned long long *>(sc.vals),
-        reinterpret_cast<unsigned long long *>(sc.vals_sorted), (int64_t)m, 0, bits, stream);
+    (void)ngrid;
+    cudaError_t e = cudaEventRecord(sc.fork, stream);
+    for (int l = 0; l < sc.levels && e == cudaSuccess; ++l) {
+        const uint64_t o = (uint64_t)l * sc.seg;
+        e = cudaStreamWaitEvent(sc.side[l], sc.fork, 0);
+        size_t tmp = sc.seg_tmp_bytes;
+        if (e == cudaSuccess)
+            e = cub::DeviceRadixSort::SortPairs(
+                static_cast<uint8_t *>(sc.sort_tmp) + (size_t)l * sc.seg_tmp_bytes, tmp, sc.keys + o,
+                sc.keys_sorted + o, reinterpret_cast<const unsigned long long *>(sc.vals + o),
+                reinterpret_cast<unsigned long long *>(sc.vals_sorted + o), (int64_t)sc.seg, 1, sc.key_end_bit,
+                sc.side[l]);
+        if (e == cudaSuccess)
+            e = cudaEventRecord(sc.join[l], sc.side[l]);
+        if (e == cudaSuccess)
+            e = cudaStreamWaitEvent(stream, sc.join[l], 0);
+    }
     if (e != cudaSuccess)
         return e;
     const uint64_t threads = (m + kFoldPer - 1) / kFoldPer;
