@@ -219,3 +219,32 @@ def test_training_is_bitwise_deterministic(variant):
     for x, y in zip(wa, wb):
         assert x.tobytes() == y.tobytes()
     assert la == lb
+
+
+@pytest.mark.parametrize("variant", [orc.VARIANT_NRRS, orc.VARIANT_AID], ids=["nrrs", "aid"])
+def test_non_default_grid_runs_the_generic_training_kernels(variant):
+    """3 levels, base 4, 2^10 entries: StatNet input 22, so the steps take the generic (runtime-width)
+    kernels and the scatter sorts 11-bit entry segments; gradients still match the oracle."""
+    from paper_2510_07868_b200.training import RrsNetTrainer, StatNetTrainer
+    nets = orc.OracleNets(variant, levels=3, base=4, log2t=10, seed=9, randomize=True)
+    hb, db = _batch(2049, seed=4)
+    loss, gm, gg = orc.stat_loss(nets, hb)
+    tr = StatNetTrainer(mirror_nets(nets))
+    gl, fin = tr.loss_and_grad(db)
+    assert fin and abs(gl - loss) <= 1e-6 * abs(loss)
+    assert _rel(tr.g_mlp.cpu().numpy(), gm) < 1e-4
+    assert _rel(tr.g_grid.cpu().numpy(), gg) < 1e-4
+    tr.close()
+    hb2, db2 = _rrs_batch(2049)
+    errors = orc.gen_pixel_errors(2048)
+    parts, gm2, gg2 = orc.rrs_loss(nets, nets.stat_grid, nets.stat_mlp, hb2, errors, 0.4, 1, d_scale=0.5)
+    rt = RrsNetTrainer(mirror_nets(nets))
+    gp, sk, fin = rt.loss_and_grad(db2, torch.from_numpy(nets.stat_grid).cuda(),
+                                   torch.from_numpy(nets.stat_mlp).cuda(),
+                                   torch.from_numpy(errors.view(np.float32).copy()).cuda(), 0.4, 1, d_scale=0.5)
+    assert fin and sk == parts.skipped
+    assert abs(gp["total"] - parts.total) <= 1e-5 * max(abs(parts.total), 1e-12)
+    assert _rel(rt.g_mlp.cpu().numpy(), gm2) < 2e-4
+    if variant == orc.VARIANT_AID:
+        assert _rel(rt.g_grid.cpu().numpy(), gg2) < 2e-4
+    rt.close()
