@@ -121,3 +121,29 @@ def test_adrrs_nn_headline_size_parity():
     flips = np.count_nonzero(_np(out.k) != ref["k"])
     assert flips <= max(3, n // 2000), f"{flips} count flips"
     st.close()
+
+
+@pytest.mark.parametrize("n", [1, 127, 129, 1000, 20_000, 196_608, 196_609])
+def test_aid_default_routing_small_and_ragged_batches(n):
+    """AID through the default routing around the fused-stage threshold (kFusedAutoMaxN = 196,608):
+    ragged and tiny batches (fewer tiles than MLP groups, or than producer CTAs) against the
+    oracle -- q_orig within 1e-3, u and gates exact, decisions bit-exact on the GPU's own factors."""
+    v = orc.gen_vertices(n, n_pixels=max(n, 64))
+    v["weight"][::9] = 0.0  # zero throughput: undecided, q = 0
+    on = orc.OracleNets(orc.VARIANT_AID, seed=1, randomize=True)
+    npx = max(n, 64)
+    cap = queue_capacity_for(npx)
+    ref = orc.rrs_stage(v, 2, npx, cap, orc.AID_NRRS, on, gain=0.85, seed=0, threads=orc.threads_available())
+    st = RrsStage(npx, mirror_nets(on))
+    out, res = st.run(to_dev(v), 2, Strategy(StrategyKind.AidNrrs), rc=RateControl(), full=True)
+    torch.cuda.synchronize()
+    q = _np(out.q_orig)
+    assert rel_err(q, ref["q_orig"], 1e-6).max() <= REL_TOL
+    np.testing.assert_array_equal(_np(out.u), ref["u"])
+    np.testing.assert_array_equal(_np(out.decided), ref["decided"])
+    dec = oracle_decide(q, _np(out.u), npx, cap, 0.85)
+    np.testing.assert_array_equal(_np(out.q_norm), dec["q_norm"])
+    np.testing.assert_array_equal(_np(out.k), dec["k"])
+    assert res.spawned == dec["spawned"] and res.dropped == dec["dropped"]
+    np.testing.assert_array_equal(_np(out.slots)[:res.spawned].view(np.uint32), dec["slots"])
+    st.close()
