@@ -199,3 +199,23 @@ def test_trace_frame_errors():
     big = film_m.GpuFilm(32, 32, film_m.SuffixStage(ctx=ctx))
     with pytest.raises(_capi.NrrsError):
         tracer.trace_frame(pt, render.TraceConfig(max_depth=4), rc, big)
+
+
+@pytest.mark.parametrize("kind,size", [(orc.AID_NRRS, (48, 40)), (orc.AID_NRRS, (512, 512)), (orc.NRRS, (96, 80))],
+                         ids=["aid-fused-small", "aid-three-kernel", "nrrs"])
+def test_neural_trace_is_bitwise_reproducible(kind, size):
+    """The reference's renders are bit-identical across runs (test_engine.cpp:461-502); the GPU
+    trace_frame with neural RRS (the fused small-batch AID stage, the three-kernel path at 512 x 512,
+    NRRS) gives bit-identical films, normals and depth counts on two fresh contexts."""
+    _, render, _, _ = _mods()
+    desc = render.make_cornell_scene()
+    on = orc.OracleNets(orc.VARIANT_AID if kind == orc.AID_NRRS else orc.VARIANT_NRRS, seed=1, randomize=True)
+    B = 6
+    assignment = [(0, 1.0)] + [(kind, 1.0)] * (B - 1)
+    w, h = size
+    a = _gpu_trace(desc, w, h, assignment, B, seed=7, frames=2, nets=on)
+    b = _gpu_trace(desc, w, h, assignment, B, seed=7, frames=2, nets=on)
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x["sum"], y["sum"])
+        np.testing.assert_array_equal(x["normals"], y["normals"])
+        assert list(x["report"].depth_counts) == list(y["report"].depth_counts)
