@@ -1724,13 +1724,11 @@ static cudaError_t launch_ws(const InferParams &p, int num_sms, cudaStream_t str
 }
 
 // ===========================================================================
-// K-B / K-C, two-pass large-tile versions (used by the launchers below).
-// A tile is NRRS_BSUBS (default 4) sub-tiles of 512 threads x 4 items = 8,192 elements.  Pass 1
-// computes and writes the per-element results and keeps the counts in shared
-// memory; one warp-parallel look-back over <= n/kBTile tiles gives the tile's
-// exclusive prefix; pass 2 re-scans the counts sub-tile by sub-tile and emits
-// offsets / slot records with coalesced stores.  Few, large tiles keep the
-// look-back chain short (the small-tile version spent most of its time there).
+// Two-pass large-tile compaction (round 1's K-C form), kept for the 72-byte PathState records of
+// trace_frame (compact2_kernel<18, 1>; the stage's slot records use compact3_kernel).  A tile is
+// NRRS_BSUBS (default 4) sub-tiles of 512 threads x 4 items = 8,192 records.  Pass 1 keeps the
+// flags in shared memory; one warp-parallel look-back gives the tile's exclusive prefix; pass 2
+// re-scans sub-tile by sub-tile and writes the kept records with coalesced stores.
 // ===========================================================================
 constexpr int kBT = 512;            // threads
 constexpr int kBItems = 4;          // items per thread per sub-tile
@@ -1739,7 +1737,6 @@ constexpr int kBSub = kBT * kBItems;  // 2048
 #define NRRS_BSUBS 4
 #endif
 constexpr int kBSubs = NRRS_BSUBS;  // sub-tiles per CTA tile (sweep 8/4/2/1: DESIGN.md section 6)
-constexpr int kBTile = kBSub * kBSubs;  // 8192 at the default 4 sub-tiles
 
 template <int NT>
 __device__ __forceinline__ uint32_t block_scan_excl(uint32_t v, uint32_t *warp_tot, uint32_t &total) {
