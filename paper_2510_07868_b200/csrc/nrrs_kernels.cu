@@ -1732,7 +1732,6 @@ static cudaError_t launch_ws(const InferParams &p, int num_sms, cudaStream_t str
 // ===========================================================================
 constexpr int kBT = 512;            // threads
 constexpr int kBItems = 4;          // items per thread per sub-tile
-constexpr int kBSub = kBT * kBItems;  // 2048
 #ifndef NRRS_BSUBS
 #define NRRS_BSUBS 4
 #endif
