@@ -1731,7 +1731,6 @@ static cudaError_t launch_ws(const InferParams &p, int num_sms, cudaStream_t str
 // re-scans sub-tile by sub-tile and writes the kept records with coalesced stores.
 // ===========================================================================
 constexpr int kBT = 512;            // threads
-constexpr int kBItems = 4;          // items per thread per sub-tile
 #ifndef NRRS_BSUBS
 #define NRRS_BSUBS 4
 #endif
