@@ -1373,6 +1373,7 @@ static int ensure_scatter(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_grid_spec *s
     sc->seg = seg;
     sc->levels = levels;
     sc->key_end_bit = end_bit;
+    sc->ngrid = (uint64_t)levels * (1ull << spec->log2_table_size) * 2u;
     sc->fork = ctx->gsc_fork;
     for (int l = 0; l < kScatterMaxLevels; ++l) {
         sc->side[l] = ctx->gsc_side[l];

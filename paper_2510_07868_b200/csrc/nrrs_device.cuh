@@ -7,11 +7,31 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda_fp16.h>
 
 #include "nrrs_internal.h"
 
 namespace nrrs {
+
+// Bounds-checked diagnostics build (NRRS_BOUNDS_CHECK; compute-sanitizer is not available on the
+// GPU pool): every checked index is tested on the device and a violation prints and traps, so the
+// GPU suite run against this build fails loudly on an out-of-range access.  Compiles to nothing
+// otherwise.
+#ifdef NRRS_BOUNDS_CHECK
+#define NRRS_CHECK(cond, what, a, b)                                                                        \
+    do {                                                                                                    \
+        if (!(cond)) {                                                                                      \
+            printf("NRRS_CHECK failed: %s (%llu vs %llu) block %d thread %d\n", what, (unsigned long long)(a), \
+                   (unsigned long long)(b), (int)blockIdx.x, (int)threadIdx.x);                             \
+            __trap();                                                                                       \
+        }                                                                                                   \
+    } while (0)
+#else
+#define NRRS_CHECK(cond, what, a, b) \
+    do {                             \
+    } while (0)
+#endif
 
 // ---------------------------------------------------------------------------
 // Counter-based RNG: SplitMix64 keyed PCG32 (reference rng.hpp:8-82).

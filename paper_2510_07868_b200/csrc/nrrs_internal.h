@@ -265,6 +265,7 @@ struct GridScatter {
     uint64_t seg;                  // contributions per level (n * 8)
     int levels;
     int key_end_bit;               // entry bits of a key within a level: [1, key_end_bit)
+    uint64_t ngrid;                // floats of the gradient grid (bounds-checked builds)
     cudaStream_t side[kScatterMaxLevels];
     cudaEvent_t fork, join[kScatterMaxLevels];
 };

@@ -109,8 +109,10 @@ __device__ __forceinline__ float2 level_encode(const uint8_t *tab, const LevelCo
     }
     uint32_t raw[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
+    for (int k = 0; k < 8; ++k) {
+        NRRS_CHECK(idx4[k] <= c.m4 || (c.dense && idx4[k] < c.nn * c.nn * c.nn * 4u), "level table index", idx4[k], c.m4);
         raw[k] = *reinterpret_cast<const uint32_t *>(tab + idx4[k]);
+    }
     uint64_t acc[2] = {pk2(0.0f, 0.0f), pk2(0.0f, 0.0f)};  // oz = 0 / 1 (two short FMA chains)
 #pragma unroll
     for (int q = 0; q < 4; ++q) {  // corners (0, oy, oz), (1, oy, oz); q = oy + 2 oz
@@ -152,8 +154,10 @@ __device__ __forceinline__ float level_encode_f32(const uint8_t *tab, const Leve
     }
     float v[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
+    for (int k = 0; k < 8; ++k) {
+        NRRS_CHECK(idx4[k] <= c.m4 || (c.dense && idx4[k] < c.nn * c.nn * c.nn * 4u), "f32 level table index", idx4[k], c.m4);
         v[k] = *reinterpret_cast<const float *>(tab + idx4[k]);
+    }
     float a0 = 0.0f, a1 = 0.0f;  // oz = 0 / 1 (two short FMA chains)
 #pragma unroll
     for (int q = 0; q < 4; ++q) {  // corners (0, oy, oz), (1, oy, oz); q = oy + 2 oz
@@ -376,6 +380,7 @@ __device__ __forceinline__ void scan4_positions(const uint32_t (&s)[4], Scan3Sme
 constexpr uint32_t kStatePad = 16;
 __device__ __forceinline__ uint64_t tile_prefix(uint64_t *state, uint32_t tile, uint64_t agg, uint32_t epoch,
                                                 bool single_wave, unsigned long long *dbg = nullptr) {
+    NRRS_CHECK(!single_wave || tile < 256u, "single-wave tile", tile, 256u);
     if (!single_wave)
         return lookback_warp(state, tile, agg, epoch);
     const uint32_t lane = threadIdx.x & 31u;

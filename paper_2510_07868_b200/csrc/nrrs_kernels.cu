@@ -2067,10 +2067,12 @@ __global__ void __launch_bounds__(kD3T, 1) decide3_kernel(DecideParams p) {
                     const uint32_t pos = excl[i] + (rel - (excl[i] - gbase));  // tile-relative
                     const uint32_t kept = pos < room ? min(kk[e], room - pos) : 0u;
                     for (uint32_t c = 0; c < kept; ++c) {
-                        if (rel + c < (uint32_t)kD3Stage)
+                        if (rel + c < (uint32_t)kD3Stage) {
                             wbuf[rel + c] = make_uint2(j, c);
-                        else
+                        } else {
+                            NRRS_CHECK(P + pos + c < cap, "slot record (direct)", P + pos + c, cap);
                             __stcs(slots + pos + c, make_uint2(j, c));
+                        }
                     }
                     rel += kk[e];
                 }
@@ -2079,8 +2081,10 @@ __global__ void __launch_bounds__(kD3T, 1) decide3_kernel(DecideParams p) {
             const uint32_t groom = gbase < room ? room - gbase : 0u;
             uint32_t nw = gtot < groom ? gtot : groom;
             nw = nw < (uint32_t)kD3Stage ? nw : (uint32_t)kD3Stage;
-            for (uint32_t r = (uint32_t)lane; r < nw; r += 32u)
+            for (uint32_t r = (uint32_t)lane; r < nw; r += 32u) {
+                NRRS_CHECK(P + gbase + r < cap, "slot record (staged)", P + gbase + r, cap);
                 __stcs(slots + gbase + r, wbuf[r]);
+            }
             __syncwarp();
         }
         if (p.offset || p.k_out) {
@@ -2091,6 +2095,7 @@ __global__ void __launch_bounds__(kD3T, 1) decide3_kernel(DecideParams p) {
                 off[e] = (uint32_t)(cum < cap ? cum : cap);  // min(cum, capacity)
                 cum += kk[e];
             }
+            NRRS_CHECK(nv[i] == 0u || first + nv[i] <= n, "offset / k index", first + nv[i], n);
             if (nv[i] == 4u && vec_out) {
                 if (p.offset)
                     *reinterpret_cast<uint4 *>(p.offset + first) = make_uint4(off[0], off[1], off[2], off[3]);
@@ -2210,8 +2215,10 @@ __global__ void __launch_bounds__(kD3T, 1) compact3_kernel(CompactParams p) {
             if (m[i] & (1u << e))
                 wbuf[pos++] = rec[4 * i + e];
         __syncwarp();
-        for (uint32_t r = (uint32_t)lane; r < gtot; r += 32u)
+        for (uint32_t r = (uint32_t)lane; r < gtot; r += 32u) {
+            NRRS_CHECK(sm.prefix + gbase + r < p.count, "compacted record", sm.prefix + gbase + r, p.count);
             __stcs(out + gbase + r, wbuf[r]);
+        }
         __syncwarp();
     }
     if (tile == p.num_tiles - 1 && tid == 0)

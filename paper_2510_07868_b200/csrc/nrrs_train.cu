@@ -263,6 +263,7 @@ __global__ void __launch_bounds__(256) stat_fwd_bwd_kernel(TrainStepParams p) { 
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
                         const uint64_t slot = ((uint64_t)lv * p.n + s) * 8u + (uint64_t)k;  // level-major
+                        NRRS_CHECK(slot < p.n * (uint64_t)p.grid.levels * 8u, "scatter slot", slot, p.n * (uint64_t)p.grid.levels * 8u);
                         p.scatter.keys[slot] = base[k];
                         p.scatter.vals[slot] = make_float2(w[k] * da[2 * lv], w[k] * da[2 * lv + 1]);
                     }
@@ -424,6 +425,7 @@ __global__ void __launch_bounds__(256, NRRS_TRAIN_MINB) stat_fwd_bwd_fast_kernel
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
                         const uint64_t slot = ((uint64_t)lv * p.n + s) * 8u + (uint64_t)k;  // level-major
+                        NRRS_CHECK(slot < p.n * (uint64_t)p.grid.levels * 8u, "scatter slot", slot, p.n * (uint64_t)p.grid.levels * 8u);
                         p.scatter.keys[slot] = base[k];
                         p.scatter.vals[slot] = make_float2(w[k] * da[2 * lv], w[k] * da[2 * lv + 1]);
                     }
@@ -551,6 +553,7 @@ __global__ void __launch_bounds__(256) mlp_dw_kernel(const float *ws, uint64_t n
             if (kind[b] == 2)
                 continue;
             const int q = base + (col < li ? col * lo + r : lo * li + r);  // column-major W, then bias
+            NRRS_CHECK(q < P, "mlp gradient index", q, P);
             partials[(uint64_t)blockIdx.x * P + q] = acc[a][b];
         }
     }
@@ -829,6 +832,7 @@ __global__ void __launch_bounds__(256) rrs_fwd_bwd_kernel(RrsStepParams p) {
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
                         const uint64_t slot = ((uint64_t)lv * p.n + s) * 8u + (uint64_t)k;  // level-major
+                        NRRS_CHECK(slot < p.n * (uint64_t)p.grid.levels * 8u, "scatter slot", slot, p.n * (uint64_t)p.grid.levels * 8u);
                         p.scatter.keys[slot] = base[k];
                         p.scatter.vals[slot] = make_float2(w[k] * da[2 * lv], w[k] * da[2 * lv + 1]);
                     }
@@ -1075,6 +1079,7 @@ __global__ void __launch_bounds__(256, NRRS_TRAIN_MINB) rrs_fwd_bwd_fast_kernel(
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
                         const uint64_t slot = ((uint64_t)lv * p.n + s) * 8u + (uint64_t)k;  // level-major
+                        NRRS_CHECK(slot < p.n * (uint64_t)p.grid.levels * 8u, "scatter slot", slot, p.n * (uint64_t)p.grid.levels * 8u);
                         p.scatter.keys[slot] = base[k];
                         p.scatter.vals[slot] = make_float2(w[k] * da[2 * lv], w[k] * da[2 * lv + 1]);
                     }
@@ -1181,6 +1186,7 @@ __global__ void __launch_bounds__(256) grid_scatter_fold_kernel(GridScatter sc, 
             if (!more)
                 break;
         }
+        NRRS_CHECK(key + 1u < sc.ngrid, "grid gradient entry", key + 1u, sc.ngrid);
         g_grid[key] = a0;
         g_grid[key + 1] = a1;
     }
