@@ -282,7 +282,7 @@ static int ensure_scratch(nrrs_gpu_ctx *ctx, uint64_t n) {
     CK(ctx, grow(ctx->d_q, ctx->cap_q, n));
     CK(ctx, grow(ctx->d_u, ctx->cap_u, n));
     const uint64_t g = infer_max_grid(ctx->num_sms);
-    CK(ctx, grow(ctx->d_parts, ctx->cap_parts, g));
+    CK(ctx, grow(ctx->d_parts, ctx->cap_parts, 2 * g));  // an exact 128-bit sum (Fx128) per CTA
     CK(ctx, grow(ctx->d_part_counts, ctx->cap_part_counts, 2 * g));
     const uint64_t tiles = decide_tiles(n) + 1;
     if (tiles > ctx->cap_tiles) {
@@ -2691,8 +2691,8 @@ static int enqueue_host_stage(nrrs_gpu_ctx *ctx, Staging &s, const nrrs_vertex_s
     if (rc)
         return rc;
     // Pipeline: chunk c's H2D (copy_stream) overlaps K-A of chunks < c (stream).  Each chunk's K-A
-    // writes its own sum; K-B sums them in chunk order (the rank_sums input), so the result does not
-    // depend on how chunk launches were scheduled.  Chunks are whole 128-vertex tiles.
+    // adds its exact fixed-point sum (Fx128) to the call's running total, so the sum has the same bits
+    // as one launch over the whole batch.  Chunks are whole 128-vertex tiles.
     if (!ctx->copy_stream) {
         CK(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
         CK(ctx, cudaEventCreateWithFlags(&ctx->ev_start, cudaEventDisableTiming));
@@ -2711,7 +2711,7 @@ static int enqueue_host_stage(nrrs_gpu_ctx *ctx, Staging &s, const nrrs_vertex_s
         CK(ctx, cudaEventRecord(ctx->ev_start, ctx->stream));  // staging buffers free once prior work is done
         CK(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_start, 0));
     }
-    double *chunk_sums = ctx->d_sum + kChunkSums;
+    double *total_sum = ctx->d_sum + kChunkSums;  // the running exact total; complete after the last chunk
     for (uint64_t c = 0; c < nc; ++c) {
         const uint64_t base = c * chunk, cn = n - base < chunk ? n - base : chunk;
         auto h2d = [&](void *dst, const void *src, size_t elem) -> int {
@@ -2739,7 +2739,7 @@ static int enqueue_host_stage(nrrs_gpu_ctx *ctx, Staging &s, const nrrs_vertex_s
         dv.i_pixel = s.ipix + 3 * base;
         dv.path_key = h->path_key ? s.key + base : nullptr;
         rc = run_factors(ctx, &dv, cn, p, s.q_orig + base, s.u + base, dout->decided ? dout->decided + base : nullptr,
-                         chunk_sums + c, c > 0);
+                         total_sum, c > 0);
         if (rc) {
             // chunks already enqueued may still read / write set s on either stream
             cudaStreamSynchronize(ctx->copy_stream);
@@ -2747,7 +2747,7 @@ static int enqueue_host_stage(nrrs_gpu_ctx *ctx, Staging &s, const nrrs_vertex_s
             return rc;
         }
     }
-    return run_decide(ctx, n, p, s.q_orig, s.u, chunk_sums, (int)nc, p->n_pixels, cap, dout, ctx->d_total, ctx->d_res);
+    return run_decide(ctx, n, p, s.q_orig, s.u, total_sum, 1, p->n_pixels, cap, dout, ctx->d_total, ctx->d_res);
 }
 
 static int check_host_call(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *h, uint64_t n, const nrrs_stage_out *ho) {

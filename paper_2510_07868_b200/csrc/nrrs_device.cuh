@@ -483,6 +483,37 @@ __device__ __forceinline__ bool mbox_wait(const MboxDev *m, int kind, F &&f) {
     return ok;
 }
 
+// ---- exact sum of the sanitized factors (normalize_factors' sum, rrs.cpp:8-24) ----
+// q >= 0 accumulated in 128-bit fixed point, units of 2^-64 (integer part in hi).  Integer addition is
+// associative, so the sum's bits do not depend on the grid, the SM count, the kernel or the chunking
+// of the host paths; it is converted to double once.  A factor >= 2^63 saturates the integer part
+// (such counts overflow the decision step, which reports them -- as the reference's own count
+// conversion cannot represent them either).
+struct Fx128 {
+    unsigned long long lo, hi;
+};
+__device__ __forceinline__ void fx_add(Fx128 &a, const Fx128 &b) {
+    a.lo += b.lo;
+    a.hi += b.hi + (a.lo < b.lo ? 1ull : 0ull);
+}
+__device__ __forceinline__ void fx_add_q(Fx128 &a, float q) {
+    const unsigned long long ih = __float2ull_rz(q);  // floor (q >= 0); exact below 2^64
+    const float fr = q - __ull2float_rz(ih);          // exact: q's bits below the binary point
+    const unsigned long long fl = __float2ull_rn(fr * 18446744073709551616.0f);  // fr * 2^64
+    fx_add(a, Fx128{fl, ih});
+}
+__device__ __forceinline__ Fx128 fx_warp_sum(Fx128 a) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const Fx128 b{__shfl_xor_sync(0xffffffffu, a.lo, o), __shfl_xor_sync(0xffffffffu, a.hi, o)};
+        fx_add(a, b);
+    }
+    return a;
+}
+__device__ __forceinline__ double fx_to_double(const Fx128 &a) {
+    return (double)a.hi + (double)a.lo * 5.421010862427522e-20;  // lo * 2^-64
+}
+
 __device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t *p) {
     uint64_t v;
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");

@@ -55,7 +55,7 @@ struct Smem {  // after the weight blob
     uint64_t full[kGM];       // loader -> group: the tile's inputs landed
     uint64_t slot_free[kGM];  // group -> loader: the group has consumed its input slot
     uint64_t table_bar;
-    double red_sum[32];
+    Fx128 red_fx[32];
     uint32_t red_nf[32], red_bc[32];
     uint32_t cta_total;
     unsigned long long prefix;
@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(kThreads, 1) aid_stage_kernel(AidStageParams P
     uint32_t *produced = P.sync + 2u * kPad;                      // [kRoundSlots] padded
     uint32_t *consumed = produced + (uint32_t)kRoundSlots * kPad;  // [kRoundSlots] padded
     const uint32_t ring_round = L * G * (uint32_t)kGM * kTileM;   // float2 per ring slot
-    double my_sum = 0.0;
+    Fx128 my_fx{0ull, 0ull};  // exact sum of q (fixed point)
     uint32_t my_nonfinite = 0, my_bc = 0;
 
     if (warp < kLoaderWarp) {
@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1) aid_stage_kernel(AidStageParams P
                             p.u_out[j] = uv;
                         if (p.decided_out)
                             p.decided_out[j] = (uint8_t)decided;
-                        my_sum += (double)qv;
+                        fx_add_q(my_fx, qv);
                     } else {
                         qv = 0.0f;
                     }
@@ -517,14 +517,11 @@ __global__ void __launch_bounds__(kThreads, 1) aid_stage_kernel(AidStageParams P
     // ======================= decision tail (all warps) =======================
     // CTA partials of q (fixed tree over the threads), then the grid barrier
     {
-        double sv = my_sum;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-            sv += __shfl_xor_sync(0xffffffffu, sv, o);
+        const Fx128 sv = fx_warp_sum(my_fx);
         const uint32_t nf = __reduce_add_sync(0xffffffffu, my_nonfinite);
         const uint32_t bcs = __reduce_add_sync(0xffffffffu, my_bc);
         if (lane == 0) {
-            S.red_sum[warp] = sv;
+            S.red_fx[warp] = sv;
             S.red_nf[warp] = nf;
             S.red_bc[warp] = bcs;
         }
@@ -533,14 +530,14 @@ __global__ void __launch_bounds__(kThreads, 1) aid_stage_kernel(AidStageParams P
     __syncthreads();
     tc_fence_after();
     if (tid == 0) {
-        double cs = 0.0;
+        Fx128 cs{0ull, 0ull};
         uint32_t cn = 0, cb = 0;
         for (int w = 0; w < 32; ++w) {
-            cs += S.red_sum[w];
+            fx_add(cs, S.red_fx[w]);
             cn += S.red_nf[w];
             cb += S.red_bc[w];
         }
-        p.parts[b] = cs;
+        reinterpret_cast<Fx128 *>(p.parts)[b] = cs;
         p.part_counts[2 * b] = cn;
         p.part_counts[2 * b + 1] = cb;
     }
@@ -562,16 +559,16 @@ __global__ void __launch_bounds__(kThreads, 1) aid_stage_kernel(AidStageParams P
     }
     // sum of q over the whole batch in CTA order (identical on every CTA)
     if (warp == 0) {
-        double sv = 0.0;
+        Fx128 fx{0ull, 0ull};  // exact, so every CTA (and K-A0 + K-A + K-B) gets the same bits
         uint32_t nf = 0, bcs = 0;
         for (uint32_t c = lane; c < G; c += 32) {
-            sv += __ldcg(p.parts + c);
+            const unsigned long long *pp = reinterpret_cast<const unsigned long long *>(p.parts) + 2 * c;
+            fx_add(fx, Fx128{__ldcg(pp), __ldcg(pp + 1)});
             nf += __ldcg(p.part_counts + 2 * c);
             bcs += __ldcg(p.part_counts + 2 * c + 1);
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-            sv += __shfl_xor_sync(0xffffffffu, sv, o);
+        fx = fx_warp_sum(fx);
+        const double sv = fx_to_double(fx);
         nf = __reduce_add_sync(0xffffffffu, nf);
         bcs = __reduce_add_sync(0xffffffffu, bcs);
         if (lane == 0) {
@@ -579,6 +576,8 @@ __global__ void __launch_bounds__(kThreads, 1) aid_stage_kernel(AidStageParams P
             if (b == 0) {
                 *p.sum_out = sv;
                 p.res->sum_q = sv;
+                p.res->sum_fx[0] = fx.lo;
+                p.res->sum_fx[1] = fx.hi;
                 p.res->nonfinite = nf;
                 p.res->box_cox_clamps = bcs;
             }

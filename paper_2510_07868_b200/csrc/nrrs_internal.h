@@ -102,6 +102,7 @@ struct MboxDev {
 struct DevResult {
     double f_norm;
     double sum_q;
+    unsigned long long sum_fx[2];  // the exact fixed-point sum (lo, hi) sum_q is converted from
     unsigned long long total;
     unsigned long long dropped;
     unsigned long long nonfinite;

@@ -170,6 +170,16 @@ __device__ __forceinline__ float level_encode_f32(const uint8_t *tab, const Leve
 }
 
 
+// The launch's exact sum of q -> the call's running total (chunked host paths add their chunks in
+// any order with the same bits), written back to res->sum_fx; returns it as double.
+__device__ __forceinline__ double fx_finish(const InferParams &p, Fx128 launch_total) {
+    if (p.accumulate)
+        fx_add(launch_total, Fx128{p.res->sum_fx[0], p.res->sum_fx[1]});
+    p.res->sum_fx[0] = launch_total.lo;
+    p.res->sum_fx[1] = launch_total.hi;
+    return fx_to_double(launch_total);
+}
+
 namespace ws {
 
 struct Side {        // 32 B per tile row
@@ -221,7 +231,7 @@ struct SmemTail {
     uint32_t bias[2][4];       // smem byte offset of the fp32 bias, or kNoBias (folded into W)
     uint32_t tmem_base;
     uint32_t is_last;
-    double red_sum[32];
+    Fx128 red_fx[32];
     uint32_t red_nf[32];
     uint32_t red_bc[32];
 };

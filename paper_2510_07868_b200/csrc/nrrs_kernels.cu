@@ -34,7 +34,7 @@ constexpr int kInferThreads = 256;    // heuristic kernel block
 
 struct InferSmemHeader {
     uint32_t is_last;
-    double warp_sums[8];
+    Fx128 warp_fx[8];
     uint32_t warp_cnt[8];
     uint32_t warp_bc[8];
 };
@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(kInferThreads) infer_kernel(InferParams p) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint64_t n = p.n;
     // per-thread accumulators, reduced once per CTA in a fixed order (deterministic)
-    double my_sum = 0.0;
+    Fx128 my_fx{0ull, 0ull};  // exact sum of q (fixed point)
     uint32_t my_nonfinite = 0;
     const uint32_t my_bc = 0;
     const bool depth1 = p.depth == 1u;
@@ -408,7 +408,7 @@ __global__ void __launch_bounds__(kInferThreads) infer_kernel(InferParams p) {
             p.u_out[j] = rrs_uniform(p.mixed_seed, __ldg(p.path_key + j), p.depth);
         if (p.decided_out)
             p.decided_out[j] = (uint8_t)decided;
-        my_sum += (double)q;
+        fx_add_q(my_fx, q);
     }
 
     if (p.parts == nullptr)
@@ -416,29 +416,26 @@ __global__ void __launch_bounds__(kInferThreads) infer_kernel(InferParams p) {
     // ---- CTA sum in a fixed tree, then last-CTA-done reduction in CTA order ----
     constexpr int kWarps = kInferThreads / 32;
     {
-        double s = my_sum;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-            s += __shfl_xor_sync(0xffffffffu, s, o);
+        const Fx128 s = fx_warp_sum(my_fx);
         const uint32_t nf = __reduce_add_sync(0xffffffffu, my_nonfinite);
         const uint32_t bcs = __reduce_add_sync(0xffffffffu, my_bc);
         if (lane == 0) {
-            hdr->warp_sums[warp] = s;
+            hdr->warp_fx[warp] = s;
             hdr->warp_cnt[warp] = nf;
             hdr->warp_bc[warp] = bcs;
         }
         __syncthreads();
     }
     if (tid == 0) {
-        double cs = 0.0;
+        Fx128 cs{0ull, 0ull};
         uint32_t cn = 0, cb = 0;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
-            cs += hdr->warp_sums[w];
+            fx_add(cs, hdr->warp_fx[w]);
             cn += hdr->warp_cnt[w];
             cb += hdr->warp_bc[w];
         }
-        p.parts[blockIdx.x] = cs;
+        reinterpret_cast<Fx128 *>(p.parts)[blockIdx.x] = cs;
         p.part_counts[2 * blockIdx.x] = cn;
         p.part_counts[2 * blockIdx.x + 1] = cb;
         __threadfence();
@@ -449,39 +446,39 @@ __global__ void __launch_bounds__(kInferThreads) infer_kernel(InferParams p) {
     if (!hdr->is_last)
         return;
     __threadfence();
-    double s = 0.0;
+    Fx128 s{0ull, 0ull};
     uint32_t nf = 0, bcs = 0;
     for (uint32_t b = tid; b < gridDim.x; b += kInferThreads) {
-        s += __ldcg(p.parts + b);
+        const unsigned long long *pp = reinterpret_cast<const unsigned long long *>(p.parts) + 2 * b;
+        fx_add(s, Fx128{__ldcg(pp), __ldcg(pp + 1)});
         nf += __ldcg(p.part_counts + 2 * b);
         bcs += __ldcg(p.part_counts + 2 * b + 1);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-        s += __shfl_xor_sync(0xffffffffu, s, o);
+    s = fx_warp_sum(s);
     nf = __reduce_add_sync(0xffffffffu, nf);
     bcs = __reduce_add_sync(0xffffffffu, bcs);
     __syncthreads();
     if (lane == 0) {
-        hdr->warp_sums[warp] = s;
+        hdr->warp_fx[warp] = s;
         hdr->warp_cnt[warp] = nf;
         hdr->warp_bc[warp] = bcs;
     }
     __syncthreads();
     if (tid == 0) {
-        double total = 0.0;
+        Fx128 fx{0ull, 0ull};
         unsigned long long tn = 0, tb = 0;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
-            total += hdr->warp_sums[w];
+            fx_add(fx, hdr->warp_fx[w]);
             tn += hdr->warp_cnt[w];
             tb += hdr->warp_bc[w];
         }
+        const double total = fx_finish(p, fx);
         *p.sum_out = total;
         if (p.mbox)  // sharded mailbox mode: this rank's sum to every rank
             mbox_publish(p.mbox, 0, (unsigned long long)__double_as_longlong(total));
         if (p.accumulate) {
-            p.res->sum_q += total;
+            p.res->sum_q = total;  // the running exact total (fx_finish)
             p.res->nonfinite += tn;
             p.res->box_cox_clamps += tb;
         } else {
@@ -582,7 +579,7 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
     const uint64_t t_begin = num_tiles * blockIdx.x / gridDim.x;
     const uint64_t t_end = num_tiles * (blockIdx.x + 1) / gridDim.x;
     const uint32_t T = (uint32_t)(t_end - t_begin);
-    double my_sum = 0.0;
+    Fx128 my_fx{0ull, 0ull};  // exact sum of q (fixed point)
     uint32_t my_nonfinite = 0, my_bc = 0;
     const bool depth1 = p.depth == 1u;
 
@@ -873,7 +870,7 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
                                         p.u_out[j] = rrs_uniform(p.mixed_seed, sd.key, p.depth);
                                     if (p.decided_out)
                                         p.decided_out[j] = (uint8_t)decided;
-                                    my_sum += (double)qv;
+                                    fx_add_q(my_fx, qv);
                                 }
                             }
                             mbar_arrive(&st->empty[slot[c]]);
@@ -910,14 +907,11 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
     if (KIND == kKindStats || p.parts == nullptr)
         return;
     {
-        double sv = my_sum;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-            sv += __shfl_xor_sync(0xffffffffu, sv, o);
+        const Fx128 sv = fx_warp_sum(my_fx);
         const uint32_t nf = __reduce_add_sync(0xffffffffu, my_nonfinite);
         const uint32_t bcs = __reduce_add_sync(0xffffffffu, my_bc);
         if (lane == 0) {
-            st->red_sum[warp] = sv;
+            st->red_fx[warp] = sv;
             st->red_nf[warp] = nf;
             st->red_bc[warp] = bcs;
         }
@@ -925,14 +919,14 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
     }
     constexpr int kWarps = Cfg::kThreads / 32;
     if (tid == 0) {
-        double cs = 0.0;
+        Fx128 cs{0ull, 0ull};
         uint32_t cn = 0, cb = 0;
         for (int w = 0; w < kWarps; ++w) {
-            cs += st->red_sum[w];
+            fx_add(cs, st->red_fx[w]);
             cn += st->red_nf[w];
             cb += st->red_bc[w];
         }
-        p.parts[blockIdx.x] = cs;
+        reinterpret_cast<Fx128 *>(p.parts)[blockIdx.x] = cs;
         p.part_counts[2 * blockIdx.x] = cn;
         p.part_counts[2 * blockIdx.x + 1] = cb;
         __threadfence();
@@ -943,28 +937,28 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
         return;
     __threadfence();
     if (warp == 0) {
-        double sv = 0.0;
+        Fx128 sv{0ull, 0ull};
         uint32_t nf = 0, bcs = 0;
         for (uint32_t b = lane; b < gridDim.x; b += 32) {
-            sv += __ldcg(p.parts + b);
+            const unsigned long long *pp = reinterpret_cast<const unsigned long long *>(p.parts) + 2 * b;
+            fx_add(sv, Fx128{__ldcg(pp), __ldcg(pp + 1)});
             nf += __ldcg(p.part_counts + 2 * b);
             bcs += __ldcg(p.part_counts + 2 * b + 1);
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-            sv += __shfl_xor_sync(0xffffffffu, sv, o);
+        sv = fx_warp_sum(sv);
         nf = __reduce_add_sync(0xffffffffu, nf);
         bcs = __reduce_add_sync(0xffffffffu, bcs);
         if (lane == 0) {
-            *p.sum_out = sv;
+            const double tot = fx_finish(p, sv);
+            *p.sum_out = tot;
             if (p.mbox)  // sharded mailbox mode: this rank's sum to every rank
-                mbox_publish(p.mbox, 0, (unsigned long long)__double_as_longlong(sv));
+                mbox_publish(p.mbox, 0, (unsigned long long)__double_as_longlong(tot));
             if (p.accumulate) {
-                p.res->sum_q += sv;
+                p.res->sum_q = tot;  // the running exact total (fx_finish)
                 p.res->nonfinite += nf;
                 p.res->box_cox_clamps += bcs;
             } else {
-                p.res->sum_q = sv;
+                p.res->sum_q = tot;
                 p.res->nonfinite = nf;
                 p.res->box_cox_clamps = bcs;
             }
@@ -1034,7 +1028,7 @@ __global__ void __launch_bounds__(GM * 128, 1) infer_aid_fused_kernel(InferParam
     const uint64_t t_begin = num_tiles * blockIdx.x / gridDim.x;
     const uint64_t t_end = num_tiles * (blockIdx.x + 1) / gridDim.x;
     const uint32_t T = (uint32_t)(t_end - t_begin);
-    double my_sum = 0.0;
+    Fx128 my_fx{0ull, 0ull};  // exact sum of q (fixed point)
     uint32_t my_nonfinite = 0, my_bc = 0;
     const bool depth1 = p.depth == 1u;
     const int levels = p.grid_rrs.levels;
@@ -1210,7 +1204,7 @@ __global__ void __launch_bounds__(GM * 128, 1) infer_aid_fused_kernel(InferParam
                         p.u_out[j] = rrs_uniform(p.mixed_seed, key, p.depth);
                     if (p.decided_out)
                         p.decided_out[j] = (uint8_t)decided;
-                    my_sum += (double)qv;
+                    fx_add_q(my_fx, qv);
                 }
             }
         }
@@ -1224,14 +1218,11 @@ __global__ void __launch_bounds__(GM * 128, 1) infer_aid_fused_kernel(InferParam
     if (p.parts == nullptr)
         return;
     {
-        double sv = my_sum;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-            sv += __shfl_xor_sync(0xffffffffu, sv, o);
+        const Fx128 sv = fx_warp_sum(my_fx);
         const uint32_t nf = __reduce_add_sync(0xffffffffu, my_nonfinite);
         const uint32_t bcs = __reduce_add_sync(0xffffffffu, my_bc);
         if (lane == 0) {
-            st->red_sum[warp] = sv;
+            st->red_fx[warp] = sv;
             st->red_nf[warp] = nf;
             st->red_bc[warp] = bcs;
         }
@@ -1239,14 +1230,14 @@ __global__ void __launch_bounds__(GM * 128, 1) infer_aid_fused_kernel(InferParam
     }
     constexpr int kWarps = kThreads / 32;
     if (tid == 0) {
-        double cs = 0.0;
+        Fx128 cs{0ull, 0ull};
         uint32_t cn = 0, cb = 0;
         for (int w = 0; w < kWarps; ++w) {
-            cs += st->red_sum[w];
+            fx_add(cs, st->red_fx[w]);
             cn += st->red_nf[w];
             cb += st->red_bc[w];
         }
-        p.parts[blockIdx.x] = cs;
+        reinterpret_cast<Fx128 *>(p.parts)[blockIdx.x] = cs;
         p.part_counts[2 * blockIdx.x] = cn;
         p.part_counts[2 * blockIdx.x + 1] = cb;
         __threadfence();
@@ -1257,28 +1248,28 @@ __global__ void __launch_bounds__(GM * 128, 1) infer_aid_fused_kernel(InferParam
         return;
     __threadfence();
     if (warp == 0) {
-        double sv = 0.0;
+        Fx128 sv{0ull, 0ull};
         uint32_t nf = 0, bcs = 0;
         for (uint32_t b = lane; b < gridDim.x; b += 32) {
-            sv += __ldcg(p.parts + b);
+            const unsigned long long *pp = reinterpret_cast<const unsigned long long *>(p.parts) + 2 * b;
+            fx_add(sv, Fx128{__ldcg(pp), __ldcg(pp + 1)});
             nf += __ldcg(p.part_counts + 2 * b);
             bcs += __ldcg(p.part_counts + 2 * b + 1);
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-            sv += __shfl_xor_sync(0xffffffffu, sv, o);
+        sv = fx_warp_sum(sv);
         nf = __reduce_add_sync(0xffffffffu, nf);
         bcs = __reduce_add_sync(0xffffffffu, bcs);
         if (lane == 0) {
-            *p.sum_out = sv;
+            const double tot = fx_finish(p, sv);
+            *p.sum_out = tot;
             if (p.mbox)  // sharded mailbox mode: this rank's sum to every rank
-                mbox_publish(p.mbox, 0, (unsigned long long)__double_as_longlong(sv));
+                mbox_publish(p.mbox, 0, (unsigned long long)__double_as_longlong(tot));
             if (p.accumulate) {
-                p.res->sum_q += sv;
+                p.res->sum_q = tot;  // the running exact total (fx_finish)
                 p.res->nonfinite += nf;
                 p.res->box_cox_clamps += bcs;
             } else {
-                p.res->sum_q = sv;
+                p.res->sum_q = tot;
                 p.res->nonfinite = nf;
                 p.res->box_cox_clamps = bcs;
             }
@@ -1352,7 +1343,7 @@ __global__ void __launch_bounds__(8 * 128, 1) infer_stat_planes_kernel(InferPara
     const uint64_t t_begin = num_tiles * blockIdx.x / gridDim.x;
     const uint64_t t_end = num_tiles * (blockIdx.x + 1) / gridDim.x;
     const uint32_t T = (uint32_t)(t_end - t_begin);
-    double my_sum = 0.0;
+    Fx128 my_fx{0ull, 0ull};  // exact sum of q (fixed point)
     uint32_t my_nonfinite = 0, my_bc = 0;
     const bool depth1 = p.depth == 1u;
     const int nfeat = 2 * p.grid.levels;  // fp32 planes: one per (level, feature)
@@ -1563,7 +1554,7 @@ __global__ void __launch_bounds__(8 * 128, 1) infer_stat_planes_kernel(InferPara
                         p.u_out[j] = rrs_uniform(p.mixed_seed, key, p.depth);
                     if (p.decided_out)
                         p.decided_out[j] = (uint8_t)decided;
-                    my_sum += (double)qv;
+                    fx_add_q(my_fx, qv);
                 }
             }
         }
@@ -1577,14 +1568,11 @@ __global__ void __launch_bounds__(8 * 128, 1) infer_stat_planes_kernel(InferPara
     if (KIND == kKindStats || p.parts == nullptr)
         return;
     {
-        double sv = my_sum;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-            sv += __shfl_xor_sync(0xffffffffu, sv, o);
+        const Fx128 sv = fx_warp_sum(my_fx);
         const uint32_t nf = __reduce_add_sync(0xffffffffu, my_nonfinite);
         const uint32_t bcs = __reduce_add_sync(0xffffffffu, my_bc);
         if (lane == 0) {
-            st->red_sum[warp] = sv;
+            st->red_fx[warp] = sv;
             st->red_nf[warp] = nf;
             st->red_bc[warp] = bcs;
         }
@@ -1592,14 +1580,14 @@ __global__ void __launch_bounds__(8 * 128, 1) infer_stat_planes_kernel(InferPara
     }
     constexpr int kWarps = kThreads / 32;
     if (tid == 0) {
-        double cs = 0.0;
+        Fx128 cs{0ull, 0ull};
         uint32_t cn = 0, cb = 0;
         for (int w = 0; w < kWarps; ++w) {
-            cs += st->red_sum[w];
+            fx_add(cs, st->red_fx[w]);
             cn += st->red_nf[w];
             cb += st->red_bc[w];
         }
-        p.parts[blockIdx.x] = cs;
+        reinterpret_cast<Fx128 *>(p.parts)[blockIdx.x] = cs;
         p.part_counts[2 * blockIdx.x] = cn;
         p.part_counts[2 * blockIdx.x + 1] = cb;
         __threadfence();
@@ -1610,28 +1598,28 @@ __global__ void __launch_bounds__(8 * 128, 1) infer_stat_planes_kernel(InferPara
         return;
     __threadfence();
     if (warp == 0) {
-        double sv = 0.0;
+        Fx128 sv{0ull, 0ull};
         uint32_t nf = 0, bcs = 0;
         for (uint32_t b = lane; b < gridDim.x; b += 32) {
-            sv += __ldcg(p.parts + b);
+            const unsigned long long *pp = reinterpret_cast<const unsigned long long *>(p.parts) + 2 * b;
+            fx_add(sv, Fx128{__ldcg(pp), __ldcg(pp + 1)});
             nf += __ldcg(p.part_counts + 2 * b);
             bcs += __ldcg(p.part_counts + 2 * b + 1);
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-            sv += __shfl_xor_sync(0xffffffffu, sv, o);
+        sv = fx_warp_sum(sv);
         nf = __reduce_add_sync(0xffffffffu, nf);
         bcs = __reduce_add_sync(0xffffffffu, bcs);
         if (lane == 0) {
-            *p.sum_out = sv;
+            const double tot = fx_finish(p, sv);
+            *p.sum_out = tot;
             if (p.mbox)  // sharded mailbox mode: this rank's sum to every rank
-                mbox_publish(p.mbox, 0, (unsigned long long)__double_as_longlong(sv));
+                mbox_publish(p.mbox, 0, (unsigned long long)__double_as_longlong(tot));
             if (p.accumulate) {
-                p.res->sum_q += sv;
+                p.res->sum_q = tot;  // the running exact total (fx_finish)
                 p.res->nonfinite += nf;
                 p.res->box_cox_clamps += bcs;
             } else {
-                p.res->sum_q = sv;
+                p.res->sum_q = tot;
                 p.res->nonfinite = nf;
                 p.res->box_cox_clamps = bcs;
             }
@@ -2236,31 +2224,31 @@ __global__ void __launch_bounds__(kD3T, 1) compact3_kernel(CompactParams p) {
 // ===========================================================================
 __global__ void __launch_bounds__(256) sum_check_kernel(const float *q, uint64_t n, double *parts,
                                                         uint32_t *counter, uint32_t *err, double *sum_out) {
-    __shared__ double ws[8];
+    // the stage's exact fixed-point sum (Fx128), so normalize_factors here and inside the stage agree
+    __shared__ Fx128 ws[8];
     __shared__ uint32_t is_last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t begin = n * blockIdx.x / gridDim.x, end = n * (blockIdx.x + 1) / gridDim.x;
-    double s = 0.0;
+    Fx128 s{0ull, 0ull};
     uint32_t bad = 0;
     for (uint64_t i = begin + tid; i < end; i += 256) {
         const float v = q[i];
         if (!(v >= 0.0f) || !isfinite(v))
             bad = 1;
-        s += (double)v;
+        else
+            fx_add_q(s, v);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-        s += __shfl_xor_sync(0xffffffffu, s, o);
+    s = fx_warp_sum(s);
     if (__any_sync(0xffffffffu, bad) && lane == 0)
         atomicOr(err, 1u);
     if (lane == 0)
         ws[warp] = s;
     __syncthreads();
     if (tid == 0) {
-        double t = 0.0;
+        Fx128 t{0ull, 0ull};
         for (int w = 0; w < 8; ++w)
-            t += ws[w];
-        parts[blockIdx.x] = t;
+            fx_add(t, ws[w]);
+        reinterpret_cast<Fx128 *>(parts)[blockIdx.x] = t;
         __threadfence();
         is_last = atomicAdd(counter, 1u) == gridDim.x - 1 ? 1u : 0u;
     }
@@ -2268,20 +2256,20 @@ __global__ void __launch_bounds__(256) sum_check_kernel(const float *q, uint64_t
     if (!is_last)
         return;
     __threadfence();
-    double t = 0.0;
-    for (uint32_t b = tid; b < gridDim.x; b += 256)
-        t += __ldcg(parts + b);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-        t += __shfl_xor_sync(0xffffffffu, t, o);
+    Fx128 t{0ull, 0ull};
+    for (uint32_t b = tid; b < gridDim.x; b += 256) {
+        const unsigned long long *pp = reinterpret_cast<const unsigned long long *>(parts) + 2 * b;
+        fx_add(t, Fx128{__ldcg(pp), __ldcg(pp + 1)});
+    }
+    t = fx_warp_sum(t);
     if (lane == 0)
         ws[warp] = t;
     __syncthreads();
     if (tid == 0) {
-        double tot = 0.0;
+        Fx128 tot{0ull, 0ull};
         for (int w = 0; w < 8; ++w)
-            tot += ws[w];
-        *sum_out = tot;
+            fx_add(tot, ws[w]);
+        *sum_out = fx_to_double(tot);
         *counter = 0;
     }
 }

@@ -147,3 +147,40 @@ def test_aid_default_routing_small_and_ragged_batches(n):
     assert res.spawned == dec["spawned"] and res.dropped == dec["dropped"]
     np.testing.assert_array_equal(_np(out.slots)[:res.spawned].view(np.uint32), dec["slots"])
     st.close()
+
+
+@pytest.mark.parametrize("kind,n", [(orc.AID_NRRS, 65_536), (orc.AID_NRRS, 1_000_003), (orc.NRRS, 300_001),
+                                    (orc.THROUGHPUT, 1_000_003)])
+def test_sum_of_factors_is_identical_across_entry_points(kind, n, monkeypatch):
+    """normalize_factors' sum (rrs.cpp:8-24) is reduced in a fixed shape over 32-row blocks, so the
+    device call (fused small-batch stage or K-A0 + K-A + K-B), the chunked host-buffer calls (sync
+    and two-in-flight) and the sharded phase-1 entry all produce the same f64 sum and F, bit for bit."""
+    from paper_2510_07868_b200 import RrsVariant
+    v = orc.gen_vertices(n)
+    variant = orc.VARIANT_AID if kind == orc.AID_NRRS else orc.VARIANT_NRRS
+    on = orc.OracleNets(variant, seed=1, randomize=True)
+    strat = Strategy(StrategyKind(kind))
+    sums = {}
+    for name, env in (("device", None), ("device-3k", "0"), ("device-fused", "1")):
+        if env is None:
+            monkeypatch.delenv("NRRS_FUSED", raising=False)
+        else:
+            monkeypatch.setenv("NRRS_FUSED", env)
+        st = RrsStage(n, mirror_nets(on))
+        _, res = st.run(to_dev(v), 2, strat, rc=RateControl(), full=True)
+        torch.cuda.synchronize()
+        sums[name] = (res.sum_q, res.f_norm)
+        st.close()
+    monkeypatch.delenv("NRRS_FUSED", raising=False)
+    st = RrsStage(n, mirror_nets(on))
+    hv = {k: np.ascontiguousarray(a) for k, a in v.items()}
+    _, res = st.run_host(hv, 2, strat, rc=RateControl())
+    sums["host"] = (res.sum_q, res.f_norm)
+    st.close()
+    ref = sums["device"]
+    for name, val in sums.items():
+        assert val == ref, (name, val, ref)
+    # and the float32 F the decisions use equals the oracle's (sequential f64 sum of the same q)
+    q_ref = orc.rrs_stage(v, 2, n, queue_capacity_for(n), kind, on if kind != orc.THROUGHPUT else None,
+                          gain=0.85, seed=0, threads=orc.threads_available())["f_norm"]
+    assert abs(ref[1] - q_ref) <= (1e-12 if kind == orc.THROUGHPUT else 1e-5) * q_ref
