@@ -442,19 +442,21 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 
 // One thread: the rank's value of `kind` into its line of every rank's mailbox, value before the
 // generation (st.release.sys orders it), generation = the rank's next counter value.
-__device__ __forceinline__ void mbox_publish(const MboxDev *m, int kind, unsigned long long value) {
+__device__ __forceinline__ void mbox_publish(const MboxDev *m, int kind, unsigned long long value,
+                                             unsigned long long value2 = 0ull) {
     const uint32_t g = m->gen[kind] + 1u;
     m->gen[kind] = g;
     for (int r = 0; r < m->nranks; ++r) {
         unsigned long long *line = m->peer[r] + ((size_t)kind * kMboxMaxRanks + m->rank) * kMboxLineWords;
         asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(line + 1), "l"(value) : "memory");
+        asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(line + 2), "l"(value2) : "memory");
         asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(line), "l"((unsigned long long)g) : "memory");
     }
 }
 
 // One thread: waits until every rank's line of `kind` in this rank's mailbox carries this rank's
 // current generation of `kind` (its own publish of the same step already advanced it), then hands
-// the values to f(rank, value) in rank order.  Returns false (and raises m->err) after
+// the values to f(rank, value, value2) in rank order.  Returns false (and raises m->err) after
 // kMboxTimeoutNs.
 template <typename F>
 __device__ __forceinline__ bool mbox_wait(const MboxDev *m, int kind, F &&f) {
@@ -476,9 +478,10 @@ __device__ __forceinline__ bool mbox_wait(const MboxDev *m, int kind, F &&f) {
             }
             __nanosleep(100);
         }
-        unsigned long long v;
+        unsigned long long v, v2;
         asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(line + 1) : "memory");
-        f(r, v);
+        asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v2) : "l"(line + 2) : "memory");
+        f(r, v, v2);
     }
     return ok;
 }

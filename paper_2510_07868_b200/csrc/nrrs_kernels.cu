@@ -312,7 +312,7 @@ __global__ void mbox_clip_kernel(const MboxDev *m, uint32_t capacity, unsigned l
     if (threadIdx.x != 0 || blockIdx.x != 0)
         return;
     unsigned long long base = 0, all = 0, mine = 0;
-    mbox_wait(m, 1, [&](int r, unsigned long long t) {
+    mbox_wait(m, 1, [&](int r, unsigned long long t, unsigned long long) {
         if (r < m->rank)
             base += t;
         if (r == m->rank)
@@ -332,7 +332,7 @@ __global__ void mbox_clip_kernel(const MboxDev *m, uint32_t capacity, unsigned l
 
 __global__ void mbox_publish_kernel(const MboxDev *m, int kind, unsigned long long value) {
     if (threadIdx.x == 0 && blockIdx.x == 0)
-        mbox_publish(m, kind, value);
+        mbox_publish(m, kind, value, 0ull);  // an empty rank: total 0 / exact sum 0
 }
 
 cudaError_t launch_mbox_publish(const MboxDev *m, int kind, unsigned long long value, cudaStream_t stream) {
@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(kInferThreads) infer_kernel(InferParams p) {
         const double total = fx_finish(p, fx);
         *p.sum_out = total;
         if (p.mbox)  // sharded mailbox mode: this rank's sum to every rank
-            mbox_publish(p.mbox, 0, (unsigned long long)__double_as_longlong(total));
+            mbox_publish(p.mbox, 0, p.res->sum_fx[0], p.res->sum_fx[1]);  // the exact 128-bit sum
         if (p.accumulate) {
             p.res->sum_q = total;  // the running exact total (fx_finish)
             p.res->nonfinite += tn;
@@ -952,7 +952,7 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
             const double tot = fx_finish(p, sv);
             *p.sum_out = tot;
             if (p.mbox)  // sharded mailbox mode: this rank's sum to every rank
-                mbox_publish(p.mbox, 0, (unsigned long long)__double_as_longlong(tot));
+                mbox_publish(p.mbox, 0, p.res->sum_fx[0], p.res->sum_fx[1]);  // the exact 128-bit sum
             if (p.accumulate) {
                 p.res->sum_q = tot;  // the running exact total (fx_finish)
                 p.res->nonfinite += nf;
@@ -1263,7 +1263,7 @@ __global__ void __launch_bounds__(GM * 128, 1) infer_aid_fused_kernel(InferParam
             const double tot = fx_finish(p, sv);
             *p.sum_out = tot;
             if (p.mbox)  // sharded mailbox mode: this rank's sum to every rank
-                mbox_publish(p.mbox, 0, (unsigned long long)__double_as_longlong(tot));
+                mbox_publish(p.mbox, 0, p.res->sum_fx[0], p.res->sum_fx[1]);  // the exact 128-bit sum
             if (p.accumulate) {
                 p.res->sum_q = tot;  // the running exact total (fx_finish)
                 p.res->nonfinite += nf;
@@ -1613,7 +1613,7 @@ __global__ void __launch_bounds__(8 * 128, 1) infer_stat_planes_kernel(InferPara
             const double tot = fx_finish(p, sv);
             *p.sum_out = tot;
             if (p.mbox)  // sharded mailbox mode: this rank's sum to every rank
-                mbox_publish(p.mbox, 0, (unsigned long long)__double_as_longlong(tot));
+                mbox_publish(p.mbox, 0, p.res->sum_fx[0], p.res->sum_fx[1]);  // the exact 128-bit sum
             if (p.accumulate) {
                 p.res->sum_q = tot;  // the running exact total (fx_finish)
                 p.res->nonfinite += nf;
@@ -1905,14 +1905,13 @@ __global__ void __launch_bounds__(kD3T, 1) decide3_kernel(DecideParams p) {
         if (p.mbox) {  // sharded mailbox mode: every rank's sum of this depth from the own mailbox
             __shared__ double s_sum;
             if (tid == 0) {
-                double t = 0.0;
-                mbox_wait(p.mbox, 0, [&](int r, unsigned long long v) {  // rank order, as the all-gather path
-                    const double x = __longlong_as_double((long long)v);
-                    t += x;
+                Fx128 t{0ull, 0ull};  // the ranks' exact sums add exactly: F equals the one-rank F bit for bit
+                mbox_wait(p.mbox, 0, [&](int r, unsigned long long lo, unsigned long long hi) {
+                    fx_add(t, Fx128{lo, hi});
                     if (tile == 0)
-                        p.mbox->sums_seen[r] = x;
+                        p.mbox->sums_seen[r] = fx_to_double(Fx128{lo, hi});
                 });
-                s_sum = t;
+                s_sum = fx_to_double(t);
             }
             __syncthreads();
             sum = s_sum;

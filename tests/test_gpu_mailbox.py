@@ -93,6 +93,11 @@ def test_mailbox_two_ranks_match_single_rank(variant):
     for rk in range(world):
         np.testing.assert_array_equal(_np(seen_s[rk]), np.array([float(x.item()) for x in sums]))
         np.testing.assert_array_equal(_np(seen_t[rk]), np.array([int(x.item()) for x in tots]))
+    # the ranks exchanged their exact 128-bit sums: F equals the one-rank F bit for bit
+    for st in stages:
+        fr = _capi.StageResultC()
+        _capi.check(st.handle, st.ctx.lib.nrrs_gpu_fetch_result(st.handle, C.byref(fr)))
+        assert fr.f_norm == r.f_norm
     base0, kept0, sp0, dr0 = (int(x) for x in _np(clips[0]))
     base1, kept1, sp1, dr1 = (int(x) for x in _np(clips[1]))
     assert (sp0, dr0) == (sp1, dr1) == (r.spawned, r.dropped)
