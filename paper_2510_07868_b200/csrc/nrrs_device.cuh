@@ -487,11 +487,11 @@ __device__ __forceinline__ bool mbox_wait(const MboxDev *m, int kind, F &&f) {
 }
 
 // ---- exact sum of the sanitized factors (normalize_factors' sum, rrs.cpp:8-24) ----
-// q >= 0 accumulated in 128-bit fixed point, units of 2^-64 (integer part in hi).  Integer addition is
-// associative, so the sum's bits do not depend on the grid, the SM count, the kernel or the chunking
-// of the host paths; it is converted to double once.  A factor >= 2^63 saturates the integer part
-// (such counts overflow the decision step, which reports them -- as the reference's own count
-// conversion cannot represent them either).
+// q >= 0 accumulated as a 128-bit integer in units of 2^-40 (the high word counts 2^24).  Integer
+// addition is associative, so the sum's bits do not depend on the grid, the SM count, the kernel or
+// the chunking of the host paths; it is converted to double once.  A factor below 2^24 costs one
+// rounded conversion (q * 2^40 < 2^64); larger ones are split at 2^24.  Terms are rounded to the
+// 2^-40 grid (|error| <= 2^-41 each, ~1e-12 relative at the sums where F < 1 applies).
 struct Fx128 {
     unsigned long long lo, hi;
 };
@@ -500,10 +500,13 @@ __device__ __forceinline__ void fx_add(Fx128 &a, const Fx128 &b) {
     a.hi += b.hi + (a.lo < b.lo ? 1ull : 0ull);
 }
 __device__ __forceinline__ void fx_add_q(Fx128 &a, float q) {
-    const unsigned long long ih = __float2ull_rz(q);  // floor (q >= 0); exact below 2^64
-    const float fr = q - __ull2float_rz(ih);          // exact: q's bits below the binary point
-    const unsigned long long fl = __float2ull_rn(fr * 18446744073709551616.0f);  // fr * 2^64
-    fx_add(a, Fx128{fl, ih});
+    if (q < 16777216.0f) {
+        fx_add(a, Fx128{__float2ull_rn(q * 1099511627776.0f), 0ull});  // q * 2^40 (exact scaling)
+    } else {
+        const float qh = truncf(q * 5.9604644775390625e-08f);  // floor(q / 2^24), exact
+        const float ql = fmaf(qh, -16777216.0f, q);           // q - qh * 2^24, exact
+        fx_add(a, Fx128{__float2ull_rn(ql * 1099511627776.0f), __float2ull_rz(qh)});
+    }
 }
 __device__ __forceinline__ Fx128 fx_warp_sum(Fx128 a) {
 #pragma unroll
@@ -514,7 +517,7 @@ __device__ __forceinline__ Fx128 fx_warp_sum(Fx128 a) {
     return a;
 }
 __device__ __forceinline__ double fx_to_double(const Fx128 &a) {
-    return (double)a.hi + (double)a.lo * 5.421010862427522e-20;  // lo * 2^-64
+    return (double)a.hi * 16777216.0 + (double)a.lo * 9.094947017729282e-13;  // hi * 2^24 + lo * 2^-40
 }
 
 __device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t *p) {

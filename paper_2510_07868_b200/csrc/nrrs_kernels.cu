@@ -372,7 +372,7 @@ cudaError_t launch_grid_levels(const GridLevelParams &p, int num_sms, cudaStream
     return p.f32 ? launch_grid_levels_t<true>(p, num_sms, stream) : launch_grid_levels_t<false>(p, num_sms, stream);
 }
 
-__global__ void __launch_bounds__(kInferThreads) infer_kernel(InferParams p) {
+__global__ void __launch_bounds__(kInferThreads, 8) infer_kernel(InferParams p) {
     __shared__ InferSmemHeader hdr_s;
     pdl_trigger();
     InferSmemHeader *hdr = &hdr_s;
