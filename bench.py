@@ -296,6 +296,7 @@ def main():
     import ctypes as C
     rc = RateControl()
     local_sum = torch.zeros(1, dtype=torch.float64, device=dev)
+    local_fx = torch.zeros(2, dtype=torch.int64, device=dev)  # the exact sum the ranks exchange
     local_total = torch.zeros(1, dtype=torch.int64, device=dev)
 
     pending = [None]  # N > 1: the last depth's device-side scalars (sharded_depth_async)
@@ -339,7 +340,8 @@ def main():
             if sh.exchange == "mailbox":
                 pending[0] = sh.depth_async(n, 2, strategy, out, gain, 0.0, after_exchange=lambda clip: compact(sh._total))
             else:
-                pending[0] = sharded_depth_async(local_sum, lambda rs: sh.decide(n, 2, strategy, out, rs, gain, 0.0),
+                _capi.check(stage.handle, lib.nrrs_gpu_stage_local_sum_exact(stage.handle, local_fx.data_ptr()))
+                pending[0] = sharded_depth_async(local_fx, lambda rs: sh.decide(n, 2, strategy, out, rs, gain, 0.0),
                                                  cap, npx, sh.stage, None, after_exchange=lambda clip: compact(sh._total))
         ev[-1].record(stream)
 

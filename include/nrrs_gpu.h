@@ -444,6 +444,15 @@ NRRS_API int nrrs_gpu_sharded_clip(const uint64_t *h_rank_totals, int32_t nranks
 NRRS_API int nrrs_gpu_sharded_clip_dev(nrrs_gpu_ctx *ctx, const uint64_t *d_rank_totals, int32_t nranks,
                                        int32_t rank, uint32_t capacity, uint64_t *d_out);
 
+/* Exact form of the two phases: the rank's sum of factors as the 128-bit fixed-point integer the
+ * stage accumulates (2 x u64 lo, hi, bit-exactness), written to d_out after
+ * nrrs_gpu_stage_factors; and phase 2 taking the all-gathered exact sums (2 x nranks words, rank
+ * order), added exactly -- so the sharded F equals the one-rank F bit for bit. */
+NRRS_API int nrrs_gpu_stage_local_sum_exact(nrrs_gpu_ctx *ctx, uint64_t *d_out);
+NRRS_API int nrrs_gpu_stage_decide_exact(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_stage_params *p,
+                                         const uint64_t *d_rank_sums_exact, int32_t nranks,
+                                         const nrrs_stage_out *d_out, uint64_t *d_local_total);
+
 /* ---- in-kernel rank exchange over NVLink / NVSwitch peer memory (mailbox mode; DESIGN.md
  * section 7).  Replaces the caller's two all-gathers per depth (wavefront.cpp:141-154 and
  * rrs.cpp:8-24 across ranks): with a connected mailbox, nrrs_gpu_stage_factors' last CTA writes

@@ -991,7 +991,7 @@ static void phase_dump(nrrs_gpu_ctx *ctx, const char *what, unsigned long long *
 static int run_decide(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_stage_params *p, const float *q, const float *u,
                       const double *rank_sums, int nranks, uint64_t n_pixels, uint32_t capacity,
                       const nrrs_stage_out *o, unsigned long long *total_out, DevResult *res,
-                      const MboxDev *mbox = nullptr) {
+                      const MboxDev *mbox = nullptr, const unsigned long long *rank_sums_fx = nullptr) {
     if (!std::isfinite(p->gain) || p->gain < 0.0f)
         return fail(ctx, NRRS_EINVAL, "stage: gain must be finite and >= 0 (got %g)", (double)p->gain);
     const bool adaptive = p->strategy.kind != NRRS_FIXED;
@@ -1000,6 +1000,7 @@ static int run_decide(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_stage_params *p,
     dp.u = u;
     dp.n = n;
     dp.rank_sums = rank_sums;
+    dp.rank_sums_fx = rank_sums_fx;
     dp.nranks = nranks;
     dp.n_pixels = n_pixels;
     dp.gain = (p->depth >= 2 && adaptive) ? p->gain : 1.0f;  // wavefront.cpp:391
@@ -2190,6 +2191,7 @@ int nrrs_gpu_stage_factors(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t
         return rc;
     if (n == 0) {
         CK(ctx, cudaMemsetAsync(d_local_sum, 0, sizeof(double), ctx->stream));
+        CK(ctx, cudaMemsetAsync(&ctx->d_res->sum_fx[0], 0, 2 * sizeof(uint64_t), ctx->stream));
         if (ctx->mbox_ready) {  // an empty rank still takes part in the depth's exchange
             CK(ctx, launch_mbox_publish(ctx->d_mbox_dev, 0, 0ull, ctx->stream));
             ctx->launches += 1;
@@ -2235,6 +2237,43 @@ int nrrs_gpu_stage_decide(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_stage_params
     // rank-local records, the global clip is applied by the caller.
     return run_decide(ctx, n, p, q, u, d_rank_sums, nranks, p->n_pixels, cap, o,
                       reinterpret_cast<unsigned long long *>(d_local_total), ctx->d_res);
+}
+
+int nrrs_gpu_stage_local_sum_exact(nrrs_gpu_ctx *ctx, uint64_t *d_out) {
+    if (!ctx || !d_out)
+        return NRRS_EINVAL;
+    CK(ctx, cudaSetDevice(ctx->device));
+    CK(ctx, cudaMemcpyAsync(d_out, &ctx->d_res->sum_fx[0], 2 * sizeof(uint64_t), cudaMemcpyDeviceToDevice,
+                            ctx->stream));
+    return NRRS_OK;
+}
+
+int nrrs_gpu_stage_decide_exact(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_stage_params *p,
+                                const uint64_t *d_rank_sums_exact, int32_t nranks, const nrrs_stage_out *o,
+                                uint64_t *d_local_total) {
+    if (!ctx || !d_rank_sums_exact || nranks < 1 || !d_local_total)
+        return NRRS_EINVAL;
+    uint32_t cap = 0;
+    int rc = resolve_capacity(ctx, p, &cap);
+    if (rc)
+        return rc;
+    rc = check_out(ctx, o, n);
+    if (rc)
+        return rc;
+    if (n == 0) {
+        CK(ctx, cudaMemsetAsync(d_local_total, 0, sizeof(uint64_t), ctx->stream));
+        return NRRS_OK;
+    }
+    rc = ensure_scratch(ctx, n);
+    if (rc)
+        return rc;
+    const float *q = o->q_orig ? o->q_orig : ctx->d_q;
+    const float *u = o->u ? o->u : ctx->d_u;
+    if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(u)) & 15u)
+        return fail(ctx, NRRS_EINVAL, "stage out: q_orig / u must be 16-byte aligned");
+    return run_decide(ctx, n, p, q, u, nullptr, nranks, p->n_pixels, cap, o,
+                      reinterpret_cast<unsigned long long *>(d_local_total), ctx->d_res, nullptr,
+                      reinterpret_cast<const unsigned long long *>(d_rank_sums_exact));
 }
 
 int nrrs_gpu_mailbox_init(nrrs_gpu_ctx *ctx, int32_t nranks, int32_t rank, void *ipc_handle_out,

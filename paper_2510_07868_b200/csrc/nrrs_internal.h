@@ -174,6 +174,7 @@ struct DecideParams {
     const int32_t *counts_in;
     uint64_t n;
     const double *rank_sums;
+    const unsigned long long *rank_sums_fx;  // optional: the ranks' exact sums (lo, hi) x nranks, added exactly
     int32_t nranks;
     uint64_t n_pixels;
     float gain;

@@ -1915,6 +1915,11 @@ __global__ void __launch_bounds__(kD3T, 1) decide3_kernel(DecideParams p) {
             }
             __syncthreads();
             sum = s_sum;
+        } else if (p.rank_sums_fx) {  // exact rank sums: F equals the one-rank F bit for bit
+            Fx128 t{0ull, 0ull};
+            for (int r = 0; r < p.nranks; ++r)
+                fx_add(t, Fx128{p.rank_sums_fx[2 * r], p.rank_sums_fx[2 * r + 1]});
+            sum = fx_to_double(t);
         } else {
             for (int r = 0; r < p.nranks; ++r)
                 sum += p.rank_sums[r];

@@ -62,11 +62,42 @@ def f_norm_from_sums(rank_sums: List[float], n_pixels_total: int) -> float:
     return 1.0 if s <= 0.0 else float(n_pixels_total) / s
 
 
+# ---- exact rank sums (nrrs_gpu_stage_local_sum_exact): the stage's 128-bit fixed-point sum as two
+# int64 words (lo, hi), value = hi * 2^24 + lo * 2^-40 (bit-exactness) ----
+_U64 = (1 << 64) - 1
+
+
+def fx_to_float(lo: int, hi: int) -> float:
+    """The device's fx_to_double: float(hi) * 2^24 + float(lo) * 2^-40 (the same two roundings)."""
+    return float(hi & _U64) * 16777216.0 + float(lo & _U64) * 9.094947017729282e-13
+
+
+def exact_rank_floats(t: torch.Tensor) -> List[float]:
+    w = [int(x) for x in t.reshape(-1).tolist()]
+    return [fx_to_float(w[2 * r], w[2 * r + 1]) for r in range(len(w) // 2)]
+
+
+def f_norm_from_exact(t: torch.Tensor, n_pixels_total: int) -> float:
+    """F from the all-gathered exact rank sums, added exactly (decide3's rank_sums_fx path)."""
+    w = [int(x) & _U64 for x in t.reshape(-1).tolist()]
+    total = sum((w[2 * r + 1] << 64) | w[2 * r] for r in range(len(w) // 2)) & ((1 << 128) - 1)
+    s = fx_to_float(total & _U64, total >> 64)
+    return 1.0 if s <= 0.0 else float(n_pixels_total) / s
+
+
+def _outcome_sums(rank_sums_t: torch.Tensor, n_pixels_total: int):
+    """(per-rank floats, F) for f64 rank sums or exact (int64 word pair) rank sums."""
+    if rank_sums_t.dtype == torch.int64:
+        return exact_rank_floats(rank_sums_t), f_norm_from_exact(rank_sums_t, n_pixels_total)
+    sums_h = [float(x) for x in rank_sums_t.tolist()]
+    return sums_h, f_norm_from_sums(sums_h, n_pixels_total)
+
+
 def sharded_depth(local_sum: torch.Tensor, decide: Callable[[torch.Tensor], torch.Tensor], capacity: int,
                   n_pixels_total: int, group=None, rc: Optional[RateControl] = None,
                   after_exchange: Optional[Callable[[], None]] = None) -> ShardOutcome:
-    """Runs the two exchanges of one depth.  local_sum: [1] float64 on the
-    collective's device; decide(rank_sums) launches phase 2 and returns the
+    """Runs the two exchanges of one depth.  local_sum: [1] float64, or the exact sum as [2] int64
+    words (nrrs_gpu_stage_local_sum_exact), on the collective's device; decide(rank_sums) launches phase 2 and returns the
     rank's [1] int64 realized total.  after_exchange() (optional) is called once
     the second exchange is issued and before the host reads its result: device
     work that needs only this rank's queue (e.g. its compaction) is queued
@@ -85,11 +116,11 @@ def sharded_depth(local_sum: torch.Tensor, decide: Callable[[torch.Tensor], torc
     if after_exchange is not None:
         after_exchange()
     tot = [int(x) for x in torch.cat(totals).tolist()]  # the one host wait of the depth
-    sums_h = [float(x) for x in rank_sums_t.tolist()]
+    sums_h, f_norm = _outcome_sums(rank_sums_t, n_pixels_total)
     base, kept, spawned, dropped = global_clip(tot, rank, capacity)
     if rc is not None and dropped > 0:
         rc.note_overflow()
-    return ShardOutcome(sums_h, tot, base, kept, spawned, dropped, f_norm_from_sums(sums_h, n_pixels_total))
+    return ShardOutcome(sums_h, tot, base, kept, spawned, dropped, f_norm)
 
 
 @dataclasses.dataclass
@@ -108,14 +139,14 @@ class PendingDepth:
         if self.check is not None:
             self.check()
         tot = [int(x) for x in self.rank_totals.tolist()]
-        sums_h = [float(x) for x in self.rank_sums.tolist()]
+        sums_h, f_norm = _outcome_sums(self.rank_sums, self.n_pixels_total)
         if self.clip is not None:
             base, kept, spawned, dropped = (int(x) for x in self.clip.tolist())
         else:
             base, kept, spawned, dropped = global_clip(tot, self.rank, self.capacity)
         if rc is not None and dropped > 0:
             rc.note_overflow()
-        return ShardOutcome(sums_h, tot, base, kept, spawned, dropped, f_norm_from_sums(sums_h, self.n_pixels_total))
+        return ShardOutcome(sums_h, tot, base, kept, spawned, dropped, f_norm)
 
 
 def _all_gather_flat(x: torch.Tensor, host: bool, group=None) -> torch.Tensor:
@@ -308,6 +339,7 @@ class ShardedRrsStage:
         self.device = self.stage.device
         self.exchange = exchange
         self._sum = torch.zeros(1, dtype=torch.float64, device=self.device)
+        self._sum_fx = torch.zeros(2, dtype=torch.int64, device=self.device)  # the exact sum (lo, hi)
         self._total = torch.zeros(1, dtype=torch.int64, device=self.device)
         if exchange == "mailbox":
             world, rank = dist.get_world_size(group), dist.get_rank(group)
@@ -326,7 +358,7 @@ class ShardedRrsStage:
             p = self.stage.params(depth, strategy, gain, eps_div, n_pixels=self.n_pixels_total)
             return mailbox_depth(self.stage, n, p, out, self._total, dist.get_world_size(self.group),
                                  dist.get_rank(self.group), self.capacity, self.n_pixels_total, after_exchange)
-        return sharded_depth_async(self._sum, lambda rs: self.decide(n, depth, strategy, out, rs, gain, eps_div),
+        return sharded_depth_async(self._sum_fx, lambda rs: self.decide(n, depth, strategy, out, rs, gain, eps_div),
                                    self.capacity, self.n_pixels_total, self.stage, self.group, after_exchange)
 
     def factors(self, vertices, depth: int, strategy: Strategy, out: StageOutputs, eps_div: float = 0.0,
@@ -339,7 +371,9 @@ class ShardedRrsStage:
         oc = out.c()
         _capi.check(st.handle, st.ctx.lib.nrrs_gpu_stage_factors(st.handle, C.byref(soa), n, C.byref(p),
                                                                  C.byref(oc), self._sum.data_ptr()))
-        return self._sum
+        # the exact 128-bit sum is what the ranks exchange: F is then the one-rank F bit for bit
+        _capi.check(st.handle, st.ctx.lib.nrrs_gpu_stage_local_sum_exact(st.handle, self._sum_fx.data_ptr()))
+        return self._sum_fx
 
     def decide(self, n: int, depth: int, strategy: Strategy, out: StageOutputs, rank_sums: torch.Tensor,
                gain: float = 1.0, eps_div: float = 0.0) -> torch.Tensor:
@@ -347,8 +381,13 @@ class ShardedRrsStage:
         p = st.params(depth, strategy, gain, eps_div, n_pixels=self.n_pixels_total)
         oc = out.c()
         rs = rank_sums.contiguous()
-        _capi.check(st.handle, st.ctx.lib.nrrs_gpu_stage_decide(st.handle, n, C.byref(p), rs.data_ptr(),
-                                                                rs.numel(), C.byref(oc), self._total.data_ptr()))
+        if rs.dtype == torch.int64:  # exact rank sums (2 words per rank), added exactly
+            _capi.check(st.handle, st.ctx.lib.nrrs_gpu_stage_decide_exact(st.handle, n, C.byref(p), rs.data_ptr(),
+                                                                          rs.numel() // 2, C.byref(oc),
+                                                                          self._total.data_ptr()))
+        else:
+            _capi.check(st.handle, st.ctx.lib.nrrs_gpu_stage_decide(st.handle, n, C.byref(p), rs.data_ptr(),
+                                                                    rs.numel(), C.byref(oc), self._total.data_ptr()))
         return self._total
 
     def eps_div(self, i_acc_band: torch.Tensor, eps_scale: float = ADRRS_EPS_SCALE) -> float:

@@ -52,7 +52,7 @@ def _rank(rank, port, n, npx, cap, variant, q):
     out = st.stage.alloc_outputs(hi - lo, full=True)
     kind = StrategyKind.AidNrrs if variant == orc.VARIANT_AID else StrategyKind.Nrrs
     local = st.factors(dv, 2, Strategy(kind), out, 0.0, rc.gain())
-    sums = [torch.zeros(1, dtype=torch.float64) for _ in range(WORLD)]
+    sums = [torch.zeros_like(local.cpu()) for _ in range(WORLD)]  # the exact sums: [2] int64 words
     dist.all_gather(sums, local.cpu())
     rank_sums = torch.cat(sums).cuda()
     total = st.decide(hi - lo, 2, Strategy(kind), out, rank_sums, rc.gain(), 0.0)
@@ -62,8 +62,9 @@ def _rank(rank, port, n, npx, cap, variant, q):
     totals = [int(t.item()) for t in tots]
     base, kept, spawned, dropped = global_clip(totals, rank, st.capacity)
     torch.cuda.synchronize()
+    fr = st.stage.fetch_result()
     q.put((rank, base, kept, spawned, dropped, out.k.cpu().numpy(), out.q_norm.cpu().numpy(),
-           out.slots.cpu().numpy()[:kept].view(np.uint32)))
+           out.slots.cpu().numpy()[:kept].view(np.uint32), fr.f_norm))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -96,6 +97,7 @@ def test_two_rank_sharded_stage_matches_single_rank(variant):
     np.testing.assert_array_equal(k, out.k.cpu().numpy())
     np.testing.assert_array_equal(np.concatenate([x[6] for x in res]), out.q_norm.cpu().numpy())
     assert res[0][3] == res[1][3] == r.spawned and res[0][4] == r.dropped
+    assert res[0][8] == res[1][8] == r.f_norm  # exact rank sums: the one-rank F, bit for bit
     # rank queues concatenate to the global queue: rank 1's parents are offset by rank 0's band
     slots = out.slots.cpu().numpy()[: r.spawned].view(np.uint32)
     r0 = res[0][7]
