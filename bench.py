@@ -249,7 +249,15 @@ def main():
     if os.environ.get("NRRS_BENCH_SAME_DEVICE"):
         local = 0
     torch.cuda.set_device(local)
-    if world > 1:
+    # test-only: the sharded path with one rank (a 1-rank NCCL group), to see its host and collective
+    # overhead on one GPU
+    force_sharded = bool(os.environ.get("NRRS_BENCH_FORCE_SHARDED")) and world == 1
+    if force_sharded:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29561")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
+    if world > 1 or force_sharded:
         if backend == "nccl":
             dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
         else:
@@ -272,7 +280,7 @@ def main():
     hv = synthetic.gen_vertices(n, n_pixels=npx, first=first)
     dv = {k: torch.from_numpy(a.view(np.int64) if a.dtype == np.uint64 else a).to(dev)
           for k, a in hv.items() if k != "pixel"}
-    if world > 1:
+    if world > 1 or force_sharded:
         sh = ShardedRrsStage(npx, nets, device=local, exchange=exchange)
         stage = sh.stage
     else:
@@ -337,12 +345,14 @@ def main():
             from paper_2510_07868_b200.sharded import sharded_depth_async
             # no host wait inside the depth: the global clip runs on the device (NCCL path) and this rank's
             # compaction needs only its own queue; the scalars are read after the timed loop
+            # this rank's compaction needs only its own total: queued right behind K-B (programmatic
+            # dependent launch), ahead of the totals exchange and the clip
             if sh.exchange == "mailbox":
-                pending[0] = sh.depth_async(n, 2, strategy, out, gain, 0.0, after_exchange=lambda clip: compact(sh._total))
+                pending[0] = sh.depth_async(n, 2, strategy, out, gain, 0.0, after_decide=lambda: compact(sh._total))
             else:
                 _capi.check(stage.handle, lib.nrrs_gpu_stage_local_sum_exact(stage.handle, local_fx.data_ptr()))
                 pending[0] = sharded_depth_async(local_fx, lambda rs: sh.decide(n, 2, strategy, out, rs, gain, 0.0),
-                                                 cap, npx, sh.stage, None, after_exchange=lambda clip: compact(sh._total))
+                                                 cap, npx, sh.stage, None, after_decide=lambda: compact(sh._total))
         ev[-1].record(stream)
 
     def events(k=2):
@@ -359,11 +369,13 @@ def main():
     evs = []
     launches0 = stage.ctx.launch_count()
     with ClockSampler(local) as clk:
+        t_host = time.perf_counter()
         for _ in range(args.steps):
             flush.zero_()  # L2 flush between timed steps (outside the events)
             ev = events()
             step(ev)
             evs.append(ev)
+        host_enqueue_ms = (time.perf_counter() - t_host) * 1e3 / max(args.steps, 1)  # host time per step
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -945,6 +957,7 @@ def main():
                        "compact": statistics.mean(compact_ms)},
         "clocks": clk.summary(),
         "gpu_launches": launches,
+        "host_enqueue_ms_per_step": host_enqueue_ms,
         "spawned": spawned,
     }
     if levels_ms:

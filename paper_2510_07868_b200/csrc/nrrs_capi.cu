@@ -2371,14 +2371,9 @@ int nrrs_gpu_sharded_clip_mbox(nrrs_gpu_ctx *ctx, uint32_t capacity, uint64_t *d
     if (!ctx->mbox_ready)
         return fail(ctx, NRRS_ESTATE, "sharded_clip_mbox: the context has no connected mailbox");
     CK(ctx, cudaSetDevice(ctx->device));
-    CK(ctx, launch_mbox_clip(ctx->d_mbox_dev, capacity, reinterpret_cast<unsigned long long *>(d_out), ctx->stream));
+    CK(ctx, launch_mbox_clip(ctx->d_mbox_dev, capacity, reinterpret_cast<unsigned long long *>(d_out),
+                             d_rank_sums_out, reinterpret_cast<unsigned long long *>(d_rank_totals_out), ctx->stream));
     ctx->launches += 1;
-    const size_t b = 8 * (size_t)ctx->mbox_nranks;
-    if (d_rank_sums_out)
-        CK(ctx, cudaMemcpyAsync(d_rank_sums_out, ctx->d_mbox_aux + 64, b, cudaMemcpyDeviceToDevice, ctx->stream));
-    if (d_rank_totals_out)
-        CK(ctx, cudaMemcpyAsync(d_rank_totals_out, ctx->d_mbox_aux + 64 + 8 * kMboxMaxRanks, b,
-                                cudaMemcpyDeviceToDevice, ctx->stream));
     return NRRS_OK;
 }
 

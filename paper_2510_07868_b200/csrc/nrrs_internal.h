@@ -445,7 +445,8 @@ cudaError_t launch_realize(const float *q, const float *u, int32_t *counts, uint
 
 // Mailbox mode: waits for every rank's realized total of this depth and applies the global clip
 // (base, kept, spawned, dropped -> out[0..3], as sharded_clip_kernel); one thread.
-cudaError_t launch_mbox_clip(const MboxDev *m, uint32_t capacity, unsigned long long *out, cudaStream_t stream);
+cudaError_t launch_mbox_clip(const MboxDev *m, uint32_t capacity, unsigned long long *out, double *sums_out,
+                             unsigned long long *totals_out, cudaStream_t stream);
 // Mailbox mode, empty rank: publishes `value` for `kind` (one thread).
 cudaError_t launch_mbox_publish(const MboxDev *m, int kind, unsigned long long value, cudaStream_t stream);
 

@@ -308,7 +308,8 @@ static cudaError_t launch_maybe_pdl(K kernel, uint32_t grid, uint32_t block, siz
 }
 
 // Mailbox mode of sharded_clip_kernel: the rank totals come from the own mailbox (kind 1).
-__global__ void mbox_clip_kernel(const MboxDev *m, uint32_t capacity, unsigned long long *out) {
+__global__ void mbox_clip_kernel(const MboxDev *m, uint32_t capacity, unsigned long long *out, double *sums_out,
+                                 unsigned long long *totals_out) {
     if (threadIdx.x != 0 || blockIdx.x != 0)
         return;
     unsigned long long base = 0, all = 0, mine = 0;
@@ -328,6 +329,12 @@ __global__ void mbox_clip_kernel(const MboxDev *m, uint32_t capacity, unsigned l
     out[1] = kept;
     out[2] = spawned;
     out[3] = all - spawned;
+    for (int r = 0; r < m->nranks; ++r) {  // the depth's rank sums (decide3 kept them) and totals
+        if (sums_out)
+            sums_out[r] = m->sums_seen[r];
+        if (totals_out)
+            totals_out[r] = m->totals_seen[r];
+    }
 }
 
 __global__ void mbox_publish_kernel(const MboxDev *m, int kind, unsigned long long value) {
@@ -340,8 +347,9 @@ cudaError_t launch_mbox_publish(const MboxDev *m, int kind, unsigned long long v
     return cudaGetLastError();
 }
 
-cudaError_t launch_mbox_clip(const MboxDev *m, uint32_t capacity, unsigned long long *out, cudaStream_t stream) {
-    mbox_clip_kernel<<<1, 32, 0, stream>>>(m, capacity, out);
+cudaError_t launch_mbox_clip(const MboxDev *m, uint32_t capacity, unsigned long long *out, double *sums_out,
+                             unsigned long long *totals_out, cudaStream_t stream) {
+    mbox_clip_kernel<<<1, 32, 0, stream>>>(m, capacity, out, sums_out, totals_out);
     return cudaGetLastError();
 }
 

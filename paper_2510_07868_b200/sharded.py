@@ -165,7 +165,8 @@ def _all_gather_flat(x: torch.Tensor, host: bool, group=None) -> torch.Tensor:
 
 def sharded_depth_async(local_sum: torch.Tensor, decide: Callable[[torch.Tensor], torch.Tensor], capacity: int,
                         n_pixels_total: int, stage: Optional[RrsStage] = None, group=None,
-                        after_exchange: Optional[Callable[[torch.Tensor], None]] = None) -> PendingDepth:
+                        after_exchange: Optional[Callable[[torch.Tensor], None]] = None,
+                        after_decide: Optional[Callable[[], None]] = None) -> PendingDepth:
     """sharded_depth without the host wait: the global clip runs on the device
     (nrrs_gpu_sharded_clip_dev on `stage`'s context stream) when the collective's tensors live on
     the GPU, so consecutive depths queue back to back.  after_exchange(clip) receives the [4]
@@ -176,6 +177,8 @@ def sharded_depth_async(local_sum: torch.Tensor, decide: Callable[[torch.Tensor]
     host = dist.get_backend(group) == "gloo" and local_sum.is_cuda
     rank_sums_t = _all_gather_flat(local_sum, host, group).to(local_sum.device)
     local_total = decide(rank_sums_t)
+    if after_decide is not None:  # work on this rank's queue only (its compaction) goes ahead of the exchange
+        after_decide()
     totals_t = _all_gather_flat(local_total, host, group)
     clip = None
     if not host and stage is not None and totals_t.is_cuda:
@@ -228,14 +231,19 @@ def connect_mailboxes_in_process(stages: Sequence[RrsStage]) -> None:
 
 def mailbox_depth(stage: RrsStage, n: int, p, out: StageOutputs, local_total: torch.Tensor, world: int, rank: int,
                   capacity: int, n_pixels_total: int,
-                  after_exchange: Optional[Callable[[torch.Tensor], None]] = None) -> PendingDepth:
+                  after_exchange: Optional[Callable[[torch.Tensor], None]] = None,
+                  after_decide: Optional[Callable[[], None]] = None) -> PendingDepth:
     """Phase 2 of a depth in mailbox mode (phase 1, nrrs_gpu_stage_factors, already published the
     rank's sum): decide with the rank sums from the mailbox, then the global clip from the
-    mailboxed totals, both on the device with no collective and no host wait."""
+    mailboxed totals, both on the device with no collective and no host wait.  after_decide()
+    (optional) queues work that needs only this rank's queue (its compaction) right behind the
+    decision kernel, ahead of the clip's wait for the other ranks."""
     lib = stage.ctx.lib
     oc = out.c()
     _capi.check(stage.handle, lib.nrrs_gpu_stage_decide_mbox(stage.handle, n, C.byref(p), C.byref(oc),
                                                              local_total.data_ptr()))
+    if after_decide is not None:
+        after_decide()
     dev = local_total.device
     clip = torch.empty(4, dtype=torch.int64, device=dev)
     sums = torch.empty(world, dtype=torch.float64, device=dev)
@@ -351,15 +359,18 @@ class ShardedRrsStage:
 
     def depth_async(self, n: int, depth: int, strategy: Strategy, out: StageOutputs, gain: float = 1.0,
                     eps_div: float = 0.0,
-                    after_exchange: Optional[Callable[[torch.Tensor], None]] = None) -> PendingDepth:
+                    after_exchange: Optional[Callable[[torch.Tensor], None]] = None,
+                    after_decide: Optional[Callable[[], None]] = None) -> PendingDepth:
         """Phase 2 of a depth after factors(): the exchanges (collective or mailbox), the decision
         and the device-side global clip, without a host wait."""
         if self.exchange == "mailbox":
             p = self.stage.params(depth, strategy, gain, eps_div, n_pixels=self.n_pixels_total)
             return mailbox_depth(self.stage, n, p, out, self._total, dist.get_world_size(self.group),
-                                 dist.get_rank(self.group), self.capacity, self.n_pixels_total, after_exchange)
+                                 dist.get_rank(self.group), self.capacity, self.n_pixels_total, after_exchange,
+                                 after_decide)
         return sharded_depth_async(self._sum_fx, lambda rs: self.decide(n, depth, strategy, out, rs, gain, eps_div),
-                                   self.capacity, self.n_pixels_total, self.stage, self.group, after_exchange)
+                                   self.capacity, self.n_pixels_total, self.stage, self.group, after_exchange,
+                                   after_decide)
 
     def factors(self, vertices, depth: int, strategy: Strategy, out: StageOutputs, eps_div: float = 0.0,
                 gain: float = 1.0) -> torch.Tensor:
