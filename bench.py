@@ -304,7 +304,6 @@ def main():
     import ctypes as C
     rc = RateControl()
     local_sum = torch.zeros(1, dtype=torch.float64, device=dev)
-    local_fx = torch.zeros(2, dtype=torch.int64, device=dev)  # the exact sum the ranks exchange
     local_total = torch.zeros(1, dtype=torch.int64, device=dev)
 
     pending = [None]  # N > 1: the last depth's device-side scalars (sharded_depth_async)
@@ -350,8 +349,7 @@ def main():
             if sh.exchange == "mailbox":
                 pending[0] = sh.depth_async(n, 2, strategy, out, gain, 0.0, after_decide=lambda: compact(sh._total))
             else:
-                _capi.check(stage.handle, lib.nrrs_gpu_stage_local_sum_exact(stage.handle, local_fx.data_ptr()))
-                pending[0] = sharded_depth_async(local_fx, lambda rs: sh.decide(n, 2, strategy, out, rs, gain, 0.0),
+                pending[0] = sharded_depth_async(sh._sum_fx, lambda rs: sh.decide(n, 2, strategy, out, rs, gain, 0.0),
                                                  cap, npx, sh.stage, None, after_decide=lambda: compact(sh._total))
         ev[-1].record(stream)
 
@@ -359,6 +357,8 @@ def main():
         return [torch.cuda.Event(enable_timing=True) for _ in range(k)]
 
     stage.ctx.bind_stream()
+    if world > 1:
+        dist.barrier()  # every rank set up before the first exchange (mailbox waits are bounded)
     for _ in range(max(args.warmup, 3)):
         flush.zero_()
         step(events())

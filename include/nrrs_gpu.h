@@ -449,6 +449,9 @@ NRRS_API int nrrs_gpu_sharded_clip_dev(nrrs_gpu_ctx *ctx, const uint64_t *d_rank
  * nrrs_gpu_stage_factors; and phase 2 taking the all-gathered exact sums (2 x nranks words, rank
  * order), added exactly -- so the sharded F equals the one-rank F bit for bit. */
 NRRS_API int nrrs_gpu_stage_local_sum_exact(nrrs_gpu_ctx *ctx, uint64_t *d_out);
+/* The device address of the same two words inside the context (valid until the next stage call on
+ * it), for exchanging them without a copy, e.g. as the send buffer of the all-gather. */
+NRRS_API int nrrs_gpu_stage_sum_exact_dev(nrrs_gpu_ctx *ctx, const uint64_t **d_sum);
 NRRS_API int nrrs_gpu_stage_decide_exact(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_stage_params *p,
                                          const uint64_t *d_rank_sums_exact, int32_t nranks,
                                          const nrrs_stage_out *d_out, uint64_t *d_local_total);

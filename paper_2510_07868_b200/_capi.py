@@ -152,6 +152,7 @@ SIGNATURES = [
                                         C.POINTER(StageOut), _P]),
     ("nrrs_gpu_sharded_clip_dev", C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_uint32, _P]),
     ("nrrs_gpu_stage_local_sum_exact", C.c_int, [_P, _P]),
+    ("nrrs_gpu_stage_sum_exact_dev", C.c_int, [_P, C.POINTER(C.c_void_p)]),
     ("nrrs_gpu_stage_decide_exact", C.c_int, [_P, C.c_uint64, C.POINTER(StageParams), _P, C.c_int32,
                                               C.POINTER(StageOut), _P]),
     ("nrrs_gpu_mailbox_init", C.c_int, [_P, C.c_int32, C.c_int32, _P, C.POINTER(C.c_uint64)]),

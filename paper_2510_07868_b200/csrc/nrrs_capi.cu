@@ -2239,6 +2239,13 @@ int nrrs_gpu_stage_decide(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_stage_params
                       reinterpret_cast<unsigned long long *>(d_local_total), ctx->d_res);
 }
 
+int nrrs_gpu_stage_sum_exact_dev(nrrs_gpu_ctx *ctx, const uint64_t **d_sum) {
+    if (!ctx || !d_sum)
+        return NRRS_EINVAL;
+    *d_sum = reinterpret_cast<const uint64_t *>(&ctx->d_res->sum_fx[0]);
+    return NRRS_OK;
+}
+
 int nrrs_gpu_stage_local_sum_exact(nrrs_gpu_ctx *ctx, uint64_t *d_out) {
     if (!ctx || !d_out)
         return NRRS_EINVAL;

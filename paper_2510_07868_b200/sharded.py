@@ -85,6 +85,21 @@ def f_norm_from_exact(t: torch.Tensor, n_pixels_total: int) -> float:
     return 1.0 if s <= 0.0 else float(n_pixels_total) / s
 
 
+class _CudaWords:
+    """__cuda_array_interface__ of a device address (zero-copy torch view)."""
+
+    def __init__(self, addr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i8", "data": (addr, False), "version": 3}
+
+
+def exact_sum_view(stage: RrsStage) -> torch.Tensor:
+    """[2] int64 view of the context's exact sum of q (nrrs_gpu_stage_sum_exact_dev), current after
+    every nrrs_gpu_stage_factors on that context's stream."""
+    ptr = C.c_void_p()
+    _capi.check(stage.handle, stage.ctx.lib.nrrs_gpu_stage_sum_exact_dev(stage.handle, C.byref(ptr)))
+    return torch.as_tensor(_CudaWords(ptr.value, 2), device=stage.device)
+
+
 def _outcome_sums(rank_sums_t: torch.Tensor, n_pixels_total: int):
     """(per-rank floats, F) for f64 rank sums or exact (int64 word pair) rank sums."""
     if rank_sums_t.dtype == torch.int64:
@@ -347,7 +362,7 @@ class ShardedRrsStage:
         self.device = self.stage.device
         self.exchange = exchange
         self._sum = torch.zeros(1, dtype=torch.float64, device=self.device)
-        self._sum_fx = torch.zeros(2, dtype=torch.int64, device=self.device)  # the exact sum (lo, hi)
+        self._sum_fx = exact_sum_view(self.stage)  # the context's exact sum (lo, hi): exchanged without a copy
         self._total = torch.zeros(1, dtype=torch.int64, device=self.device)
         if exchange == "mailbox":
             world, rank = dist.get_world_size(group), dist.get_rank(group)
@@ -382,8 +397,8 @@ class ShardedRrsStage:
         oc = out.c()
         _capi.check(st.handle, st.ctx.lib.nrrs_gpu_stage_factors(st.handle, C.byref(soa), n, C.byref(p),
                                                                  C.byref(oc), self._sum.data_ptr()))
-        # the exact 128-bit sum is what the ranks exchange: F is then the one-rank F bit for bit
-        _capi.check(st.handle, st.ctx.lib.nrrs_gpu_stage_local_sum_exact(st.handle, self._sum_fx.data_ptr()))
+        # the exact 128-bit sum (a view of the context's words) is what the ranks exchange: F is then
+        # the one-rank F bit for bit
         return self._sum_fx
 
     def decide(self, n: int, depth: int, strategy: Strategy, out: StageOutputs, rank_sums: torch.Tensor,
