@@ -498,6 +498,74 @@ __global__ void __launch_bounds__(kInferThreads, 8) infer_kernel(InferParams p) 
     }
 }
 
+// Teardown shared by the persistent K-A kernels: the CTA's exact sum of q (Fx128) and its
+// non-finite / Box-Cox-clamp counts as one partial per CTA, then the last CTA to finish reduces the
+// partials (exact, so order-free), converts the call's running total (fx_finish) and writes sum_out,
+// the result counters and, in sharded mailbox mode, the rank's exact sum to every rank.  Called by
+// every thread of the CTA after its last tile.
+template <int kWarps>
+__device__ __forceinline__ void ka_reduce_finish(const InferParams &p, ws::SmemTail *st, const Fx128 &my_fx,
+                                                 uint32_t my_nonfinite, uint32_t my_bc) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    {
+        const Fx128 sv = fx_warp_sum(my_fx);
+        const uint32_t nf = __reduce_add_sync(0xffffffffu, my_nonfinite);
+        const uint32_t bcs = __reduce_add_sync(0xffffffffu, my_bc);
+        if (lane == 0) {
+            st->red_fx[warp] = sv;
+            st->red_nf[warp] = nf;
+            st->red_bc[warp] = bcs;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        Fx128 cs{0ull, 0ull};
+        uint32_t cn = 0, cb = 0;
+        for (int w = 0; w < kWarps; ++w) {
+            fx_add(cs, st->red_fx[w]);
+            cn += st->red_nf[w];
+            cb += st->red_bc[w];
+        }
+        reinterpret_cast<Fx128 *>(p.parts)[blockIdx.x] = cs;
+        p.part_counts[2 * blockIdx.x] = cn;
+        p.part_counts[2 * blockIdx.x + 1] = cb;
+        __threadfence();
+        st->is_last = atomicAdd(p.counter, 1u) == gridDim.x - 1 ? 1u : 0u;
+    }
+    __syncthreads();
+    if (!st->is_last)
+        return;
+    __threadfence();
+    if (warp == 0) {
+        Fx128 sv{0ull, 0ull};
+        uint32_t nf = 0, bcs = 0;
+        for (uint32_t b = lane; b < gridDim.x; b += 32) {
+            const unsigned long long *pp = reinterpret_cast<const unsigned long long *>(p.parts) + 2 * b;
+            fx_add(sv, Fx128{__ldcg(pp), __ldcg(pp + 1)});
+            nf += __ldcg(p.part_counts + 2 * b);
+            bcs += __ldcg(p.part_counts + 2 * b + 1);
+        }
+        sv = fx_warp_sum(sv);
+        nf = __reduce_add_sync(0xffffffffu, nf);
+        bcs = __reduce_add_sync(0xffffffffu, bcs);
+        if (lane == 0) {
+            const double tot = fx_finish(p, sv);
+            *p.sum_out = tot;
+            if (p.mbox)  // sharded mailbox mode: this rank's exact 128-bit sum to every rank
+                mbox_publish(p.mbox, 0, p.res->sum_fx[0], p.res->sum_fx[1]);
+            p.res->sum_q = tot;  // the running exact total (fx_finish)
+            if (p.accumulate) {
+                p.res->nonfinite += nf;
+                p.res->box_cox_clamps += bcs;
+            } else {
+                p.res->nonfinite = nf;
+                p.res->box_cox_clamps = bcs;
+            }
+            *p.counter = 0;  // self-cleaning for the next launch
+        }
+    }
+}
+
 // ===========================================================================
 // K-A (neural kinds): warp-specialized persistent pipeline, 1 CTA per SM.
 //
@@ -537,7 +605,7 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
     uint8_t *smem_w = smem_raw;
     ws::Side *side = reinterpret_cast<ws::Side *>(smem_raw + ((p.blob_bytes + 127u) & ~127u));
     ws::SmemTail *st = reinterpret_cast<ws::SmemTail *>(reinterpret_cast<uint8_t *>(side) + S * 128 * sizeof(ws::Side));
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, warp = tid >> 5;
 
     // ---- setup: weights -> smem, UMMA descriptors, barriers, TMEM (all 512 columns) ----
     {
@@ -914,65 +982,7 @@ __global__ void __launch_bounds__(ws::Cfg<GE, GM, P, TPR>::kThreads, 1) infer_ws
         tmem_dealloc(tmem_base, 512);
     if (KIND == kKindStats || p.parts == nullptr)
         return;
-    {
-        const Fx128 sv = fx_warp_sum(my_fx);
-        const uint32_t nf = __reduce_add_sync(0xffffffffu, my_nonfinite);
-        const uint32_t bcs = __reduce_add_sync(0xffffffffu, my_bc);
-        if (lane == 0) {
-            st->red_fx[warp] = sv;
-            st->red_nf[warp] = nf;
-            st->red_bc[warp] = bcs;
-        }
-        __syncthreads();
-    }
-    constexpr int kWarps = Cfg::kThreads / 32;
-    if (tid == 0) {
-        Fx128 cs{0ull, 0ull};
-        uint32_t cn = 0, cb = 0;
-        for (int w = 0; w < kWarps; ++w) {
-            fx_add(cs, st->red_fx[w]);
-            cn += st->red_nf[w];
-            cb += st->red_bc[w];
-        }
-        reinterpret_cast<Fx128 *>(p.parts)[blockIdx.x] = cs;
-        p.part_counts[2 * blockIdx.x] = cn;
-        p.part_counts[2 * blockIdx.x + 1] = cb;
-        __threadfence();
-        st->is_last = atomicAdd(p.counter, 1u) == gridDim.x - 1 ? 1u : 0u;
-    }
-    __syncthreads();
-    if (!st->is_last)
-        return;
-    __threadfence();
-    if (warp == 0) {
-        Fx128 sv{0ull, 0ull};
-        uint32_t nf = 0, bcs = 0;
-        for (uint32_t b = lane; b < gridDim.x; b += 32) {
-            const unsigned long long *pp = reinterpret_cast<const unsigned long long *>(p.parts) + 2 * b;
-            fx_add(sv, Fx128{__ldcg(pp), __ldcg(pp + 1)});
-            nf += __ldcg(p.part_counts + 2 * b);
-            bcs += __ldcg(p.part_counts + 2 * b + 1);
-        }
-        sv = fx_warp_sum(sv);
-        nf = __reduce_add_sync(0xffffffffu, nf);
-        bcs = __reduce_add_sync(0xffffffffu, bcs);
-        if (lane == 0) {
-            const double tot = fx_finish(p, sv);
-            *p.sum_out = tot;
-            if (p.mbox)  // sharded mailbox mode: this rank's sum to every rank
-                mbox_publish(p.mbox, 0, p.res->sum_fx[0], p.res->sum_fx[1]);  // the exact 128-bit sum
-            if (p.accumulate) {
-                p.res->sum_q = tot;  // the running exact total (fx_finish)
-                p.res->nonfinite += nf;
-                p.res->box_cox_clamps += bcs;
-            } else {
-                p.res->sum_q = tot;
-                p.res->nonfinite = nf;
-                p.res->box_cox_clamps = bcs;
-            }
-            *p.counter = 0;  // self-cleaning for the next launch
-        }
-    }
+    ka_reduce_finish<Cfg::kThreads / 32>(p, st, my_fx, my_nonfinite, my_bc);
 }
 
 // ===========================================================================
@@ -987,7 +997,7 @@ __global__ void __launch_bounds__(GM * 128, 1) infer_aid_fused_kernel(InferParam
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem_w = smem_raw;
     ws::SmemTail *st = reinterpret_cast<ws::SmemTail *>(smem_raw + ((p.blob_bytes + 127u) & ~127u));
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, warp = tid >> 5;
     constexpr int kThreads = GM * 128;
     static_assert(GM * 64 <= 512 && GM <= 8, "TMEM: 64 columns per group");
     {
@@ -1225,65 +1235,7 @@ __global__ void __launch_bounds__(GM * 128, 1) infer_aid_fused_kernel(InferParam
         tmem_dealloc(tmem_base, 512);
     if (p.parts == nullptr)
         return;
-    {
-        const Fx128 sv = fx_warp_sum(my_fx);
-        const uint32_t nf = __reduce_add_sync(0xffffffffu, my_nonfinite);
-        const uint32_t bcs = __reduce_add_sync(0xffffffffu, my_bc);
-        if (lane == 0) {
-            st->red_fx[warp] = sv;
-            st->red_nf[warp] = nf;
-            st->red_bc[warp] = bcs;
-        }
-        __syncthreads();
-    }
-    constexpr int kWarps = kThreads / 32;
-    if (tid == 0) {
-        Fx128 cs{0ull, 0ull};
-        uint32_t cn = 0, cb = 0;
-        for (int w = 0; w < kWarps; ++w) {
-            fx_add(cs, st->red_fx[w]);
-            cn += st->red_nf[w];
-            cb += st->red_bc[w];
-        }
-        reinterpret_cast<Fx128 *>(p.parts)[blockIdx.x] = cs;
-        p.part_counts[2 * blockIdx.x] = cn;
-        p.part_counts[2 * blockIdx.x + 1] = cb;
-        __threadfence();
-        st->is_last = atomicAdd(p.counter, 1u) == gridDim.x - 1 ? 1u : 0u;
-    }
-    __syncthreads();
-    if (!st->is_last)
-        return;
-    __threadfence();
-    if (warp == 0) {
-        Fx128 sv{0ull, 0ull};
-        uint32_t nf = 0, bcs = 0;
-        for (uint32_t b = lane; b < gridDim.x; b += 32) {
-            const unsigned long long *pp = reinterpret_cast<const unsigned long long *>(p.parts) + 2 * b;
-            fx_add(sv, Fx128{__ldcg(pp), __ldcg(pp + 1)});
-            nf += __ldcg(p.part_counts + 2 * b);
-            bcs += __ldcg(p.part_counts + 2 * b + 1);
-        }
-        sv = fx_warp_sum(sv);
-        nf = __reduce_add_sync(0xffffffffu, nf);
-        bcs = __reduce_add_sync(0xffffffffu, bcs);
-        if (lane == 0) {
-            const double tot = fx_finish(p, sv);
-            *p.sum_out = tot;
-            if (p.mbox)  // sharded mailbox mode: this rank's sum to every rank
-                mbox_publish(p.mbox, 0, p.res->sum_fx[0], p.res->sum_fx[1]);  // the exact 128-bit sum
-            if (p.accumulate) {
-                p.res->sum_q = tot;  // the running exact total (fx_finish)
-                p.res->nonfinite += nf;
-                p.res->box_cox_clamps += bcs;
-            } else {
-                p.res->sum_q = tot;
-                p.res->nonfinite = nf;
-                p.res->box_cox_clamps = bcs;
-            }
-            *p.counter = 0;  // self-cleaning for the next launch
-        }
-    }
+    ka_reduce_finish<kThreads / 32>(p, st, my_fx, my_nonfinite, my_bc);
 }
 
 // ===========================================================================
@@ -1301,7 +1253,7 @@ __global__ void __launch_bounds__(8 * 128, 1) infer_stat_planes_kernel(InferPara
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem_w = smem_raw;
     ws::SmemTail *st = reinterpret_cast<ws::SmemTail *>(smem_raw + ((p.blob_bytes + 127u) & ~127u));
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, warp = tid >> 5;
     constexpr int kThreads = GM * 128;
     {
         const uint4 *src = reinterpret_cast<const uint4 *>(p.blob);
@@ -1575,65 +1527,7 @@ __global__ void __launch_bounds__(8 * 128, 1) infer_stat_planes_kernel(InferPara
         tmem_dealloc(tmem_base, 512);
     if (KIND == kKindStats || p.parts == nullptr)
         return;
-    {
-        const Fx128 sv = fx_warp_sum(my_fx);
-        const uint32_t nf = __reduce_add_sync(0xffffffffu, my_nonfinite);
-        const uint32_t bcs = __reduce_add_sync(0xffffffffu, my_bc);
-        if (lane == 0) {
-            st->red_fx[warp] = sv;
-            st->red_nf[warp] = nf;
-            st->red_bc[warp] = bcs;
-        }
-        __syncthreads();
-    }
-    constexpr int kWarps = kThreads / 32;
-    if (tid == 0) {
-        Fx128 cs{0ull, 0ull};
-        uint32_t cn = 0, cb = 0;
-        for (int w = 0; w < kWarps; ++w) {
-            fx_add(cs, st->red_fx[w]);
-            cn += st->red_nf[w];
-            cb += st->red_bc[w];
-        }
-        reinterpret_cast<Fx128 *>(p.parts)[blockIdx.x] = cs;
-        p.part_counts[2 * blockIdx.x] = cn;
-        p.part_counts[2 * blockIdx.x + 1] = cb;
-        __threadfence();
-        st->is_last = atomicAdd(p.counter, 1u) == gridDim.x - 1 ? 1u : 0u;
-    }
-    __syncthreads();
-    if (!st->is_last)
-        return;
-    __threadfence();
-    if (warp == 0) {
-        Fx128 sv{0ull, 0ull};
-        uint32_t nf = 0, bcs = 0;
-        for (uint32_t b = lane; b < gridDim.x; b += 32) {
-            const unsigned long long *pp = reinterpret_cast<const unsigned long long *>(p.parts) + 2 * b;
-            fx_add(sv, Fx128{__ldcg(pp), __ldcg(pp + 1)});
-            nf += __ldcg(p.part_counts + 2 * b);
-            bcs += __ldcg(p.part_counts + 2 * b + 1);
-        }
-        sv = fx_warp_sum(sv);
-        nf = __reduce_add_sync(0xffffffffu, nf);
-        bcs = __reduce_add_sync(0xffffffffu, bcs);
-        if (lane == 0) {
-            const double tot = fx_finish(p, sv);
-            *p.sum_out = tot;
-            if (p.mbox)  // sharded mailbox mode: this rank's sum to every rank
-                mbox_publish(p.mbox, 0, p.res->sum_fx[0], p.res->sum_fx[1]);  // the exact 128-bit sum
-            if (p.accumulate) {
-                p.res->sum_q = tot;  // the running exact total (fx_finish)
-                p.res->nonfinite += nf;
-                p.res->box_cox_clamps += bcs;
-            } else {
-                p.res->sum_q = tot;
-                p.res->nonfinite = nf;
-                p.res->box_cox_clamps = bcs;
-            }
-            *p.counter = 0;  // self-cleaning for the next launch
-        }
-    }
+    ka_reduce_finish<kThreads / 32>(p, st, my_fx, my_nonfinite, my_bc);
 }
 
 static bool aligned16(const void *q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; }
