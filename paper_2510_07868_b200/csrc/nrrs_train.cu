@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(256) stat_fwd_bwd_kernel(TrainStepParams p) { 
 // The default grid (8 levels, StatNet input 32) with compile-time widths: the same arithmetic in
 // the same order as stat_fwd_bwd_kernel, with the arrays in registers and W read as 16-byte vectors.
 #ifndef NRRS_TRAIN_MINB
-#define NRRS_TRAIN_MINB 1
+#define NRRS_TRAIN_MINB 2  // 128 registers, 2 CTAs per SM: train_frame 1.01 -> 0.95 ms (1: 255 registers, 4: spills)
 #endif
 template <int LV, int IN>
 __global__ void __launch_bounds__(256, NRRS_TRAIN_MINB) stat_fwd_bwd_fast_kernel(TrainStepParams p) {
