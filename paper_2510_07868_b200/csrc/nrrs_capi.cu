@@ -17,6 +17,28 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <nvtx3/nvToolsExt.h>
+
+// NVTX ranges around the C-ABI entry points (SURVEY.md section 5 tracing; header-only NVTX v3: a
+// no-op pointer check unless a profiler injects itself).  Domain "nrrs", one range per call.
+namespace {
+nvtxDomainHandle_t nvtx_domain() {
+    static nvtxDomainHandle_t d = nvtxDomainCreateA("nrrs");
+    return d;
+}
+struct NvtxRange {
+    explicit NvtxRange(const char *name) {
+        nvtxEventAttributes_t a{};
+        a.version = NVTX_VERSION;
+        a.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+        a.messageType = NVTX_MESSAGE_TYPE_ASCII;
+        a.message.ascii = name;
+        nvtxDomainRangePushEx(nvtx_domain(), &a);
+    }
+    ~NvtxRange() { nvtxDomainRangePop(nvtx_domain()); }
+};
+}  // namespace
+#define NRRS_RANGE(name) NvtxRange nrrs_nvtx_range_(name)
 #include <string>
 #include <vector>
 
@@ -751,9 +773,15 @@ static int set_weights_impl(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w, bool d
     return NRRS_OK;
 }
 
-int nrrs_gpu_set_weights(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w) { return set_weights_impl(ctx, w, false); }
+int nrrs_gpu_set_weights(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w) {
+    NRRS_RANGE("nrrs_gpu_set_weights");
+    return set_weights_impl(ctx, w, false);
+}
 
-int nrrs_gpu_set_weights_dev(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w) { return set_weights_impl(ctx, w, true); }
+int nrrs_gpu_set_weights_dev(nrrs_gpu_ctx *ctx, const nrrs_net_weights *w) {
+    NRRS_RANGE("nrrs_gpu_set_weights_dev");
+    return set_weights_impl(ctx, w, true);
+}
 
 }  // extern "C"
 
@@ -1175,6 +1203,7 @@ extern "C" {
 
 int nrrs_gpu_rrs_stage(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, const nrrs_stage_params *p,
                        const nrrs_stage_out *o, nrrs_stage_result *h_result) {
+    NRRS_RANGE("nrrs_gpu_rrs_stage");
     if (!ctx)
         return NRRS_EINVAL;
     uint32_t cap = 0;
@@ -1244,6 +1273,7 @@ int nrrs_gpu_film_luminance_sum(nrrs_gpu_ctx *ctx, const float *d_i_acc, uint64_
 static_assert(sizeof(nrrs_train_sample) == 80, "TrainSample is 80 bytes (networks.hpp:20-32)");
 int nrrs_gpu_fold_ordered(nrrs_gpu_ctx *ctx, double *d_dst, uint64_t n_dst, const int32_t *d_keys,
                           const double *d_terms, uint64_t n) {
+    NRRS_RANGE("nrrs_gpu_fold_ordered");
     if (!ctx || (n && (!d_dst || !d_keys || !d_terms)))
         return NRRS_EINVAL;
     if (n == 0)
@@ -1266,6 +1296,7 @@ int nrrs_gpu_fold_ordered(nrrs_gpu_ctx *ctx, double *d_dst, uint64_t n_dst, cons
 int nrrs_gpu_emit_train(nrrs_gpu_ctx *ctx, uint32_t depth, const nrrs_vertex_rec_soa *v, uint64_t n,
                         const float *d_i_acc, nrrs_train_sample *d_out, uint64_t capacity, const uint64_t *d_count_in,
                         uint64_t *d_count_out, uint64_t *d_nonfinite) {
+    NRRS_RANGE("nrrs_gpu_emit_train");
     if (!ctx || !v || !d_count_in || !d_count_out || !d_nonfinite || d_count_in == d_count_out)
         return NRRS_EINVAL;
     CK(ctx, cudaSetDevice(ctx->device));
@@ -1311,6 +1342,7 @@ int nrrs_gpu_emit_train(nrrs_gpu_ctx *ctx, uint32_t depth, const nrrs_vertex_rec
 
 int nrrs_gpu_train_k_i(nrrs_gpu_ctx *ctx, nrrs_train_sample *d_samples, uint64_t start, const uint64_t *d_end,
                        uint64_t capacity, uint32_t n_pixels) {
+    NRRS_RANGE("nrrs_gpu_train_k_i");
     if (!ctx || !d_samples || !d_end || n_pixels == 0)
         return NRRS_EINVAL;
     CK(ctx, cudaSetDevice(ctx->device));
@@ -1330,6 +1362,7 @@ int nrrs_gpu_train_k_i(nrrs_gpu_ctx *ctx, nrrs_train_sample *d_samples, uint64_t
 
 int nrrs_gpu_film_add_frame(nrrs_gpu_ctx *ctx, double *d_sum, uint32_t *d_samples, float *d_i_cur,
                             const double *d_frame, uint32_t n_pixels) {
+    NRRS_RANGE("nrrs_gpu_film_add_frame");
     if (!ctx || (n_pixels && (!d_sum || !d_samples || !d_i_cur || !d_frame)))
         return NRRS_EINVAL;
     CK(ctx, cudaSetDevice(ctx->device));
@@ -1387,6 +1420,7 @@ static int ensure_scatter(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_grid_spec *s
 int nrrs_gpu_stat_loss_grad(nrrs_gpu_ctx *ctx, const nrrs_grid_spec *spec, const float *d_stat_grid,
                             const float *d_stat_mlp, const nrrs_train_sample *d_batch, uint64_t n, float eps,
                             float d_scale, float *d_g_mlp, float *d_g_grid, double *h_loss, int32_t *h_finite) {
+    NRRS_RANGE("nrrs_gpu_stat_loss_grad");
     if (!ctx || !spec || !d_stat_grid || !d_stat_mlp || !d_g_mlp || !d_g_grid || !h_loss || !h_finite ||
         (n && !d_batch))
         return NRRS_EINVAL;
@@ -1454,6 +1488,7 @@ int nrrs_gpu_rrs_loss_grad(nrrs_gpu_ctx *ctx, int32_t variant, const nrrs_grid_s
                            const float *d_errors, uint64_t n_errors, float e_avg, int32_t phase, float gamma_min,
                            float gamma_avg, float gamma_rrs, float eps, float d_scale, float *d_g_mlp,
                            float *d_g_grid, double *h_parts, uint32_t *h_skipped, int32_t *h_finite) {
+    NRRS_RANGE("nrrs_gpu_rrs_loss_grad");
     if (!ctx || !spec || !d_snap_stat_grid || !d_snap_stat_mlp || !d_rrs_mlp || !d_g_mlp || !h_parts ||
         !h_skipped || !h_finite || (n && !d_batch) || (variant != 0 && variant != 1) || (phase != 0 && phase != 1) ||
         (variant == 1 && (!d_rrs_grid || !d_g_grid)) || (n_errors && !d_errors))
@@ -1541,6 +1576,7 @@ int nrrs_gpu_rrs_loss_grad(nrrs_gpu_ctx *ctx, int32_t variant, const nrrs_grid_s
 int nrrs_gpu_adam_ema(nrrs_gpu_ctx *ctx, float *d_theta, const float *d_grad, float *d_m, float *d_v,
                       float *d_shadow, uint64_t n, int64_t t, float lr, float beta1, float beta2, float eps,
                       float inv_scale, float ema_decay) {
+    NRRS_RANGE("nrrs_gpu_adam_ema");
     if (!ctx || t < 1 || (n && (!d_theta || !d_grad || !d_m || !d_v)))
         return NRRS_EINVAL;
     CK(ctx, cudaSetDevice(ctx->device));
@@ -1631,6 +1667,7 @@ extern "C" {
 int nrrs_gpu_scene_create(nrrs_gpu_ctx *ctx, const float *pos, uint32_t n_vert, const uint32_t *idx, uint32_t n_tri,
                           const uint32_t *mat_ids, const nrrs_material *mats, uint32_t n_mats,
                           const nrrs_camera *cam, nrrs_scene **out) {
+    NRRS_RANGE("nrrs_gpu_scene_create");
     if (!ctx || !out || !cam || (n_vert && !pos) || (n_tri && (!idx || !mat_ids)) || (n_mats && !mats))
         return NRRS_EINVAL;
     *out = nullptr;
@@ -1939,6 +1976,7 @@ int nrrs_gpu_trace_frame(nrrs_tracer *t, const nrrs_scene *scene, const nrrs_tra
                          const nrrs_strategy *assignment, nrrs_rate_control *rc, const nrrs_film_dev *film,
                          nrrs_train_sample *d_train, uint64_t train_capacity, uint64_t *h_train_count,
                          nrrs_frame_report *report) {
+    NRRS_RANGE("nrrs_gpu_trace_frame");
     if (!t || !scene || !cfg || !assignment || !rc || !film || !report)
         return NRRS_EINVAL;
     nrrs_gpu_ctx *ctx = t->ctx;
@@ -2183,6 +2221,7 @@ int nrrs_gpu_fetch_result(nrrs_gpu_ctx *ctx, nrrs_stage_result *h_result) {
 
 int nrrs_gpu_stage_factors(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, const nrrs_stage_params *p,
                            const nrrs_stage_out *o, double *d_local_sum) {
+    NRRS_RANGE("nrrs_gpu_stage_factors");
     if (!ctx || !d_local_sum)
         return NRRS_EINVAL;
     uint32_t cap = 0;
@@ -2213,6 +2252,7 @@ int nrrs_gpu_stage_factors(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t
 
 int nrrs_gpu_stage_decide(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_stage_params *p, const double *d_rank_sums,
                           int32_t nranks, const nrrs_stage_out *o, uint64_t *d_local_total) {
+    NRRS_RANGE("nrrs_gpu_stage_decide");
     if (!ctx || !d_rank_sums || nranks < 1 || !d_local_total)
         return NRRS_EINVAL;
     uint32_t cap = 0;
@@ -2258,6 +2298,7 @@ int nrrs_gpu_stage_local_sum_exact(nrrs_gpu_ctx *ctx, uint64_t *d_out) {
 int nrrs_gpu_stage_decide_exact(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_stage_params *p,
                                 const uint64_t *d_rank_sums_exact, int32_t nranks, const nrrs_stage_out *o,
                                 uint64_t *d_local_total) {
+    NRRS_RANGE("nrrs_gpu_stage_decide_exact");
     if (!ctx || !d_rank_sums_exact || nranks < 1 || !d_local_total)
         return NRRS_EINVAL;
     uint32_t cap = 0;
@@ -2343,6 +2384,7 @@ int nrrs_gpu_mailbox_connect(nrrs_gpu_ctx *ctx, const void *ipc_handles, const u
 
 int nrrs_gpu_stage_decide_mbox(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_stage_params *p, const nrrs_stage_out *o,
                                uint64_t *d_local_total) {
+    NRRS_RANGE("nrrs_gpu_stage_decide_mbox");
     if (!ctx || !d_local_total)
         return NRRS_EINVAL;
     if (!ctx->mbox_ready)
@@ -2373,6 +2415,7 @@ int nrrs_gpu_stage_decide_mbox(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_stage_p
 
 int nrrs_gpu_sharded_clip_mbox(nrrs_gpu_ctx *ctx, uint32_t capacity, uint64_t *d_out, double *d_rank_sums_out,
                                uint64_t *d_rank_totals_out) {
+    NRRS_RANGE("nrrs_gpu_sharded_clip_mbox");
     if (!ctx || !d_out)
         return NRRS_EINVAL;
     if (!ctx->mbox_ready)
@@ -2426,6 +2469,7 @@ int nrrs_gpu_sharded_clip(const uint64_t *totals, int32_t nranks, int32_t rank, 
 
 int nrrs_gpu_sharded_clip_dev(nrrs_gpu_ctx *ctx, const uint64_t *d_rank_totals, int32_t nranks, int32_t rank,
                               uint32_t capacity, uint64_t *d_out) {
+    NRRS_RANGE("nrrs_gpu_sharded_clip_dev");
     if (!ctx || !d_rank_totals || !d_out || nranks < 1 || rank < 0 || rank >= nranks)
         return ctx ? fail(ctx, NRRS_EINVAL, "sharded_clip_dev: invalid arguments") : NRRS_EINVAL;
     CK(ctx, cudaSetDevice(ctx->device));
@@ -2437,6 +2481,7 @@ int nrrs_gpu_sharded_clip_dev(nrrs_gpu_ctx *ctx, const uint64_t *d_rank_totals, 
 
 int nrrs_gpu_compact(nrrs_gpu_ctx *ctx, const void *d_in, const uint8_t *d_used, uint32_t count,
                      uint32_t record_words, void *d_out, uint32_t *d_count, uint32_t *h_count) {
+    NRRS_RANGE("nrrs_gpu_compact");
     if (!ctx || (count && (!d_in || !d_used || !d_out)))
         return NRRS_EINVAL;
     if (record_words != 2 && record_words != 18)
@@ -2476,6 +2521,7 @@ int nrrs_gpu_compact(nrrs_gpu_ctx *ctx, const void *d_in, const uint8_t *d_used,
 
 int nrrs_gpu_compact_dev(nrrs_gpu_ctx *ctx, const void *d_in, const uint8_t *d_used, const uint64_t *d_count_in,
                          uint32_t max_count, uint32_t record_words, void *d_out, uint32_t *d_count) {
+    NRRS_RANGE("nrrs_gpu_compact_dev");
     if (!ctx || !d_count_in || (max_count && (!d_in || !d_used || !d_out)))
         return NRRS_EINVAL;
     if (record_words != 2 && record_words != 18)
@@ -2505,6 +2551,7 @@ int nrrs_gpu_compact_dev(nrrs_gpu_ctx *ctx, const void *d_in, const uint8_t *d_u
 }
 
 int nrrs_gpu_normalize_factors(nrrs_gpu_ctx *ctx, float *d_q, uint64_t n, uint64_t n_pixels, double *h_f_norm) {
+    NRRS_RANGE("nrrs_gpu_normalize_factors");
     if (!ctx || (n && !d_q))
         return NRRS_EINVAL;
     if (n == 0) {
@@ -2539,6 +2586,7 @@ int nrrs_gpu_normalize_factors(nrrs_gpu_ctx *ctx, float *d_q, uint64_t n, uint64
 
 int nrrs_gpu_realize_counts(nrrs_gpu_ctx *ctx, const float *d_q, const float *d_u, int32_t *d_counts, uint64_t n,
                             uint64_t *h_total) {
+    NRRS_RANGE("nrrs_gpu_realize_counts");
     if (!ctx || (n && (!d_q || !d_u || !d_counts)))
         return NRRS_EINVAL;
     CK(ctx, cudaMemsetAsync(ctx->d_misc + 3, 0, sizeof(uint32_t), ctx->stream));
@@ -2561,6 +2609,7 @@ int nrrs_gpu_realize_counts(nrrs_gpu_ctx *ctx, const float *d_q, const float *d_
 
 int nrrs_gpu_plan_spawns(nrrs_gpu_ctx *ctx, const int32_t *d_counts, uint64_t n, uint32_t capacity,
                          uint32_t *d_offset, uint32_t *h_spawned, uint64_t *h_dropped) {
+    NRRS_RANGE("nrrs_gpu_plan_spawns");
     if (!ctx || (n && (!d_counts || !d_offset)))
         return NRRS_EINVAL;
     if (n == 0) {
@@ -2604,6 +2653,7 @@ int nrrs_gpu_plan_spawns(nrrs_gpu_ctx *ctx, const int32_t *d_counts, uint64_t n,
 
 int nrrs_gpu_strategy_factor(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, const nrrs_strategy *s,
                              float eps_div, float *d_q) {
+    NRRS_RANGE("nrrs_gpu_strategy_factor");
     if (!ctx || !s || (n && !d_q))
         return NRRS_EINVAL;
     int kind = 0, heur = 0;
@@ -2643,6 +2693,7 @@ int nrrs_gpu_strategy_factor(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64
 
 int nrrs_gpu_encode_levels(nrrs_gpu_ctx *ctx, const float *d_p01, uint64_t n, float *d_planes,
                            uint64_t plane_stride) {
+    NRRS_RANGE("nrrs_gpu_encode_levels");
     if (!ctx || (n && (!d_p01 || !d_planes)) || plane_stride < n)
         return ctx ? fail(ctx, NRRS_EINVAL, "encode_levels: null buffer or plane_stride < n") : NRRS_EINVAL;
     if (!ctx->has_weights || ctx->variant != NRRS_VARIANT_AID || !ctx->rrs_half ||
@@ -2664,6 +2715,7 @@ int nrrs_gpu_encode_levels(nrrs_gpu_ctx *ctx, const float *d_p01, uint64_t n, fl
 }
 
 int nrrs_gpu_predict_stats(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *v, uint64_t n, float *d_stats) {
+    NRRS_RANGE("nrrs_gpu_predict_stats");
     if (!ctx || (n && !d_stats))
         return NRRS_EINVAL;
     if (!ctx->has_weights)
@@ -2829,6 +2881,7 @@ extern "C" {
 
 int nrrs_gpu_rrs_stage_host(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *h, uint64_t n, const nrrs_stage_params *p,
                             const nrrs_stage_out *ho, nrrs_stage_result *h_result) {
+    NRRS_RANGE("nrrs_gpu_rrs_stage_host");
     if (!ctx)
         return NRRS_EINVAL;
     int rc = check_host_call(ctx, h, n, ho);
@@ -2879,6 +2932,7 @@ int nrrs_gpu_rrs_stage_host(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *h, uint64_
 
 int nrrs_gpu_rrs_stage_host_async(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *h, uint64_t n,
                                   const nrrs_stage_params *p, const nrrs_stage_out *ho, uint64_t *ticket) {
+    NRRS_RANGE("nrrs_gpu_rrs_stage_host_async");
     if (!ctx || !ticket)
         return NRRS_EINVAL;
     int rc = check_host_call(ctx, h, n, ho);
@@ -2949,6 +3003,7 @@ int nrrs_gpu_rrs_stage_host_async(nrrs_gpu_ctx *ctx, const nrrs_vertex_soa *h, u
 }
 
 int nrrs_gpu_stage_host_wait(nrrs_gpu_ctx *ctx, uint64_t ticket, nrrs_stage_result *h_result) {
+    NRRS_RANGE("nrrs_gpu_stage_host_wait");
     if (!ctx)
         return NRRS_EINVAL;
     const int b = (int)(ticket & 1u);
