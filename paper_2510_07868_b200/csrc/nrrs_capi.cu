@@ -1388,7 +1388,9 @@ static int ensure_scatter(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_grid_spec *s
         return fail(ctx, NRRS_EINVAL, "training: 1..%d grid levels", kScatterMaxLevels);
     const uint64_t seg = n * 8u, m = seg * (uint64_t)levels;
     CK(ctx, grow(ctx->d_gsc, ctx->cap_gsc, 6 * m));  // keys, keys_sorted, vals, vals_sorted (2 words each)
-    const int end_bit = 1 + spec->log2_table_size;  // keys (level * T + entry) * 2: entry bits [1, end_bit)
+    // level-local keys 2 * entry: entry bits [1, 1 + log2 T); bit 1 + log2 T is set only by the
+    // 0xFFFFFFFF sentinel of slots that contributed nothing, which so sorts after the last entry
+    const int end_bit = 2 + spec->log2_table_size;
     const uint64_t tb = grid_scatter_sort_bytes(seg, end_bit);
     CK(ctx, grow(ctx->d_gsc_tmp, ctx->cap_gsc_tmp, tb * (uint64_t)levels));
     if (!ctx->gsc_fork) {
@@ -1407,6 +1409,7 @@ static int ensure_scatter(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_grid_spec *s
     sc->seg = seg;
     sc->levels = levels;
     sc->key_end_bit = end_bit;
+    sc->level_stride = (1u << spec->log2_table_size) * 2u;
     sc->ngrid = (uint64_t)levels * (1ull << spec->log2_table_size) * 2u;
     sc->fork = ctx->gsc_fork;
     for (int l = 0; l < kScatterMaxLevels; ++l) {

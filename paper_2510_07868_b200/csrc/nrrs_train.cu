@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(256) stat_fwd_bwd_kernel(TrainStepParams p) { 
                     for (int k = 0; k < 8; ++k) {
                         const uint64_t slot = ((uint64_t)lv * p.n + s) * 8u + (uint64_t)k;  // level-major
                         NRRS_CHECK(slot < p.n * (uint64_t)p.grid.levels * 8u, "scatter slot", slot, p.n * (uint64_t)p.grid.levels * 8u);
-                        p.scatter.keys[slot] = base[k];
+                        p.scatter.keys[slot] = base[k] - 2u * (uint32_t)lv * p.grid.table_size;  // level-local
                         p.scatter.vals[slot] = make_float2(w[k] * da[2 * lv], w[k] * da[2 * lv + 1]);
                     }
                 }
@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(256, NRRS_TRAIN_MINB) stat_fwd_bwd_fast_kernel
                     for (int k = 0; k < 8; ++k) {
                         const uint64_t slot = ((uint64_t)lv * p.n + s) * 8u + (uint64_t)k;  // level-major
                         NRRS_CHECK(slot < p.n * (uint64_t)p.grid.levels * 8u, "scatter slot", slot, p.n * (uint64_t)p.grid.levels * 8u);
-                        p.scatter.keys[slot] = base[k];
+                        p.scatter.keys[slot] = base[k] - 2u * (uint32_t)lv * p.grid.table_size;  // level-local
                         p.scatter.vals[slot] = make_float2(w[k] * da[2 * lv], w[k] * da[2 * lv + 1]);
                     }
                 }
@@ -833,7 +833,7 @@ __global__ void __launch_bounds__(256) rrs_fwd_bwd_kernel(RrsStepParams p) {
                     for (int k = 0; k < 8; ++k) {
                         const uint64_t slot = ((uint64_t)lv * p.n + s) * 8u + (uint64_t)k;  // level-major
                         NRRS_CHECK(slot < p.n * (uint64_t)p.grid.levels * 8u, "scatter slot", slot, p.n * (uint64_t)p.grid.levels * 8u);
-                        p.scatter.keys[slot] = base[k];
+                        p.scatter.keys[slot] = base[k] - 2u * (uint32_t)lv * p.grid.table_size;  // level-local
                         p.scatter.vals[slot] = make_float2(w[k] * da[2 * lv], w[k] * da[2 * lv + 1]);
                     }
                 }
@@ -1080,7 +1080,7 @@ __global__ void __launch_bounds__(256, NRRS_TRAIN_MINB) rrs_fwd_bwd_fast_kernel(
                     for (int k = 0; k < 8; ++k) {
                         const uint64_t slot = ((uint64_t)lv * p.n + s) * 8u + (uint64_t)k;  // level-major
                         NRRS_CHECK(slot < p.n * (uint64_t)p.grid.levels * 8u, "scatter slot", slot, p.n * (uint64_t)p.grid.levels * 8u);
-                        p.scatter.keys[slot] = base[k];
+                        p.scatter.keys[slot] = base[k] - 2u * (uint32_t)lv * p.grid.table_size;  // level-local
                         p.scatter.vals[slot] = make_float2(w[k] * da[2 * lv], w[k] * da[2 * lv + 1]);
                     }
                 }
@@ -1196,9 +1196,20 @@ __global__ void __launch_bounds__(256) grid_scatter_fold_kernel(GridScatter sc, 
             v[e] = i0 + e < m ? sc.vals_sorted[i0 + e] : make_float2(0.0f, 0.0f);
         }
     }
+    // level-local keys -> gradient offsets (a lane's 8 elements lie in one level: seg is a multiple
+    // of 8); the sentinel stays the sentinel
+    const uint32_t lv_off = (uint32_t)(i0 / sc.seg) * sc.level_stride;
+#pragma unroll
+    for (int e = 0; e < kFoldE; ++e)
+        k[e] = k[e] == 0xFFFFFFFFu ? k[e] : k[e] + lv_off;
     uint32_t pk = __shfl_up_sync(0xffffffffu, k[kFoldE - 1], 1);
-    if (lane == 0)
-        pk = b > 0 ? sc.keys_sorted[b - 1] : 0xFFFFFFFEu;
+    if (lane == 0) {
+        pk = 0xFFFFFFFEu;
+        if (b > 0) {
+            const uint32_t kb = sc.keys_sorted[b - 1];
+            pk = kb == 0xFFFFFFFFu ? kb : kb + (uint32_t)((b - 1) / sc.seg) * sc.level_stride;
+        }
+    }
     // first run start in the lane (kFoldE: none) and the runs that start here, in order
     int fs = kFoldE;
 #pragma unroll
@@ -1257,21 +1268,23 @@ __global__ void __launch_bounds__(256) grid_scatter_fold_kernel(GridScatter sc, 
             }
         fold_flush(g_grid, sc, in.key, a0, a1);
     }
-    // the run open at the window's end continues into the next window(s)
+    // the run open at the window's end continues into the next window(s), up to its level's end
     if (lane == 31 && out.key != 0xFFFFFFFFu) {
         float a0 = out.a0, a1 = out.a1;
+        const uint64_t lv = i0 / sc.seg, lv_end = min(m, (lv + 1) * sc.seg);
+        const uint32_t local = out.key - (uint32_t)lv * sc.level_stride;
         for (uint64_t j = b + kFoldWin;; j += 4) {
             uint32_t kk[4];
             float2 vv[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                kk[u] = j + u < m ? sc.keys_sorted[j + u] : 0xFFFFFFFFu;
-                vv[u] = j + u < m ? sc.vals_sorted[j + u] : make_float2(0.0f, 0.0f);
+                kk[u] = j + u < lv_end ? sc.keys_sorted[j + u] : 0xFFFFFFFFu;
+                vv[u] = j + u < lv_end ? sc.vals_sorted[j + u] : make_float2(0.0f, 0.0f);
             }
             bool more = true;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                more = more && kk[u] == out.key;
+                more = more && kk[u] == local;
                 if (more) {
                     a0 = __fadd_rn(a0, vv[u].x);
                     a1 = __fadd_rn(a1, vv[u].y);
@@ -1284,53 +1297,6 @@ __global__ void __launch_bounds__(256) grid_scatter_fold_kernel(GridScatter sc, 
     }
 }
 
-#ifdef NRRS_FOLD_V1  // the round-2 one-thread-per-start walk (A/B reference only)
-constexpr int kFoldPer = 8;
-__global__ void __launch_bounds__(256) grid_scatter_fold_v1_kernel(GridScatter sc, uint64_t m, float *g_grid) {
-    const uint64_t i0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kFoldPer;
-    if (i0 >= m)
-        return;
-    uint32_t prev = i0 > 0 ? sc.keys_sorted[i0 - 1] : 0xFFFFFFFEu;
-    uint32_t kk[kFoldPer];
-#pragma unroll
-    for (int e = 0; e < kFoldPer; ++e)
-        kk[e] = i0 + e < m ? sc.keys_sorted[i0 + e] : 0xFFFFFFFFu;
-#pragma unroll 1
-    for (int e = 0; e < kFoldPer; ++e) {
-        const uint32_t key = kk[e];
-        const bool start = key != 0xFFFFFFFFu && key != prev;
-        prev = key;
-        if (!start)
-            continue;
-        constexpr int kU = 16;
-        float a0 = 0.0f, a1 = 0.0f;
-        for (uint64_t j = i0 + e;; j += kU) {
-            uint32_t k[kU];
-            float2 v[kU];
-#pragma unroll
-            for (int u = 0; u < kU; ++u) {
-                k[u] = j + u < m ? sc.keys_sorted[j + u] : 0xFFFFFFFFu;
-                v[u] = j + u < m ? sc.vals_sorted[j + u] : make_float2(0.0f, 0.0f);
-            }
-            bool more = true;
-#pragma unroll
-            for (int u = 0; u < kU; ++u) {
-                more = more && k[u] == key;
-                if (more) {
-                    a0 = __fadd_rn(a0, v[u].x);
-                    a1 = __fadd_rn(a1, v[u].y);
-                }
-            }
-            if (!more)
-                break;
-        }
-        NRRS_CHECK(key + 1u < sc.ngrid, "grid gradient entry", key + 1u, sc.ngrid);
-        g_grid[key] = a0;
-        g_grid[key + 1] = a1;
-    }
-}
-#endif
-
 size_t grid_scatter_sort_bytes(uint64_t contributions, int end_bit) {
     size_t bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t *)nullptr, (uint32_t *)nullptr,
@@ -1339,9 +1305,9 @@ size_t grid_scatter_sort_bytes(uint64_t contributions, int end_bit) {
     return (bytes + 255) & ~(size_t)255;
 }
 
-// per level: stable sort of its segment by the entry bits [1, end_bit) of the keys (a level's keys
-// share their higher bits; the 0xFFFFFFFF sentinel of non-contributing slots sorts last) on the
-// level's side stream, all levels concurrently; then one fold over the whole array
+// per level: stable sort of its segment by the bits [1, end_bit) of the level-local keys (the
+// 0xFFFFFFFF sentinel of non-contributing slots sorts after the last entry) on the level's side
+// stream, all levels concurrently; then one fold over the whole array
 static cudaError_t grid_scatter_reduce(const GridScatter &sc, uint64_t m, uint64_t ngrid, float *g_grid,
                                        cudaStream_t stream) {
     (void)ngrid;
@@ -1363,13 +1329,8 @@ static cudaError_t grid_scatter_reduce(const GridScatter &sc, uint64_t m, uint64
     }
     if (e != cudaSuccess)
         return e;
-#ifdef NRRS_FOLD_V1
-    const uint64_t threads = (m + kFoldPer - 1) / kFoldPer;
-    grid_scatter_fold_v1_kernel<<<(uint32_t)((threads + 255) / 256), 256, 0, stream>>>(sc, m, g_grid);
-#else
     const uint64_t warps = (m + kFoldWin - 1) / kFoldWin;
     grid_scatter_fold_kernel<<<(uint32_t)((warps + 7) / 8), 256, 0, stream>>>(sc, m, g_grid);
-#endif
     return cudaGetLastError();
 }
 

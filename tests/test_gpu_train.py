@@ -128,6 +128,35 @@ def test_rrs_loss_and_gradients_match_oracle(variant, phase):
     tr.close()
 
 
+def test_grid_gradient_last_entry_with_skipped_samples():
+    """The grid-gradient fold at the edges of its sorted segments: each level's LAST table entry is
+    the last run of the level's segment (next to the following level's first run; keys are
+    level-local, and the 0xFFFFFFFF sentinel of a slot that contributed nothing sorts after it).
+    65,536 samples, so every hashed level's last entry is hit ~16 times, half of them without a
+    pixel error (their pixel-error terms are skipped, hashgrid.cpp:84-103 still scatters their
+    other terms): the AID grid gradient matches the oracle on those entries and overall."""
+    from paper_2510_07868_b200.training import RrsNetTrainer
+    nets = orc.OracleNets(orc.VARIANT_AID, seed=5, randomize=True)
+    n = 1 << 16
+    hb, _ = _rrs_batch(n, seed=41)
+    hb["pixel"][1::2] = 4096  # no error record: skipped
+    db = torch.from_numpy(hb.view(np.uint8).reshape(n, 80).copy()).cuda()
+    errors = orc.gen_pixel_errors(2048)
+    parts, gm, gg = orc.rrs_loss(nets, nets.stat_grid, nets.stat_mlp, hb, errors, 0.4, 1, d_scale=0.5)
+    tr = RrsNetTrainer(mirror_nets(nets))
+    de = torch.from_numpy(errors.view(np.float32).copy()).cuda()
+    gp, sk, fin = tr.loss_and_grad(db, torch.from_numpy(nets.stat_grid).cuda(), torch.from_numpy(nets.stat_mlp).cuda(),
+                                   de, 0.4, 1, d_scale=0.5)
+    assert fin and sk == parts.skipped >= n // 2
+    g = tr.g_grid.cpu().numpy()
+    T = 1 << nets.spec.log2_table_size
+    last = np.array([(lv * T + T - 1) * 2 + f for lv in range(nets.spec.levels) for f in range(2)])
+    assert np.count_nonzero(gg[last]) > 0
+    np.testing.assert_allclose(g[last], gg[last], rtol=1e-3, atol=1e-5 * np.abs(gg[last]).max())
+    assert _rel(g, gg) < 2e-4
+    tr.close()
+
+
 def test_train_frame_warmup_drives_q_to_one_and_publishes():
     """NeuralRrs::train_frame in the warmup phase (q regressed to 1) + publish: the RRSNet loss
     falls and the published snapshot loads into the inference stage."""
