@@ -1388,8 +1388,8 @@ static int ensure_scatter(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_grid_spec *s
         return fail(ctx, NRRS_EINVAL, "training: 1..%d grid levels", kScatterMaxLevels);
     const uint64_t seg = n * 8u, m = seg * (uint64_t)levels;
     CK(ctx, grow(ctx->d_gsc, ctx->cap_gsc, 6 * m));  // keys, keys_sorted, vals, vals_sorted (2 words each)
-    // level-local keys 2 * entry: entry bits [1, 1 + log2 T); bit 1 + log2 T is set only by the
-    // 0xFFFFFFFF sentinel of slots that contributed nothing, which so sorts after the last entry
+    // keys (level << end_bit) | 2 * entry: entry bits [1, 1 + log2 T); bit 1 + log2 T is set only by
+    // the 0xFFFFFFFF sentinel of slots that contributed nothing, which so sorts after the last entry
     const int end_bit = 2 + spec->log2_table_size;
     const uint64_t tb = grid_scatter_sort_bytes(seg, end_bit);
     CK(ctx, grow(ctx->d_gsc_tmp, ctx->cap_gsc_tmp, tb * (uint64_t)levels));
@@ -1410,6 +1410,7 @@ static int ensure_scatter(nrrs_gpu_ctx *ctx, uint64_t n, const nrrs_grid_spec *s
     sc->levels = levels;
     sc->key_end_bit = end_bit;
     sc->level_stride = (1u << spec->log2_table_size) * 2u;
+    sc->key_shift = (uint32_t)end_bit;
     sc->ngrid = (uint64_t)levels * (1ull << spec->log2_table_size) * 2u;
     sc->fork = ctx->gsc_fork;
     for (int l = 0; l < kScatterMaxLevels; ++l) {

@@ -260,15 +260,16 @@ struct TrainGrid {
 // stream (levels run concurrently), the fold then walks the concatenation.
 constexpr int kScatterMaxLevels = 8;
 struct GridScatter {
-    uint32_t *keys, *keys_sorted;  // [n * levels * 8]; level-local keys 2 * entry; pre-set to 0xFFFFFFFF
+    uint32_t *keys, *keys_sorted;  // [n * levels * 8]; keys (level << key_shift) | 2 * entry; pre-set to 0xFFFFFFFF
     float2 *vals, *vals_sorted;    // [n * levels * 8]; sorted along with the keys (stable)
     void *sort_tmp;                // levels x seg_tmp_bytes
     size_t seg_tmp_bytes;
     uint64_t seg;                  // contributions per level (n * 8)
     int levels;
-    int key_end_bit;               // sorted key bits [1, key_end_bit): the entry, plus one bit that
-                                   // only the sentinel sets, so it sorts after the level's last entry
-    uint32_t level_stride;         // gradient floats per level (2 * table size): global = key + lv * stride
+    int key_end_bit;               // sorted key bits [1, key_end_bit) of one level's segment: the entry, plus
+                                   // one bit only the sentinel sets, so it sorts after the level's last entry
+    uint32_t key_shift;            // 2 + log2 T: the level field of a key
+    uint32_t level_stride;         // gradient floats per level (2 * table size)
     uint64_t ngrid;                // floats of the gradient grid (bounds-checked builds)
     cudaStream_t side[kScatterMaxLevels];
     cudaEvent_t fork, join[kScatterMaxLevels];

@@ -54,6 +54,14 @@ __device__ __forceinline__ void one_blob_exact(float x, int bins, float *out) {
 }
 
 // the 8 corners of level l: table offsets (floats) and trilinear weights (hashgrid.cpp:38-82)
+// Scatter key of a grid-gradient contribution: (level << (2 + log2 T)) | 2 * entry.  Bit 1 + log2 T
+// is never set by a real entry, only by the 0xFFFFFFFF sentinel of a slot that contributed nothing,
+// so a sort over bits [1, 2 + log2 T) (one level) or [1, 2 + log2 T + level bits) (all levels)
+// puts the sentinel after every real entry.  base = (level * T + entry) * 2 (the gradient offset).
+__device__ __forceinline__ uint32_t scatter_key(uint32_t base, int lv, uint32_t table_size) {
+    const uint32_t e2 = base - 2u * (uint32_t)lv * table_size;
+    return ((uint32_t)lv << (__ffs((int)table_size) + 1)) | e2;
+}
 __device__ __forceinline__ void grid_corners(const TrainGrid &g, int l, const float p[3], uint32_t base[8],
                                              float w[8]) {
     const uint32_t res = (uint32_t)g.base_resolution << l;
@@ -264,7 +272,7 @@ __global__ void __launch_bounds__(256) stat_fwd_bwd_kernel(TrainStepParams p) { 
                     for (int k = 0; k < 8; ++k) {
                         const uint64_t slot = ((uint64_t)lv * p.n + s) * 8u + (uint64_t)k;  // level-major
                         NRRS_CHECK(slot < p.n * (uint64_t)p.grid.levels * 8u, "scatter slot", slot, p.n * (uint64_t)p.grid.levels * 8u);
-                        p.scatter.keys[slot] = base[k] - 2u * (uint32_t)lv * p.grid.table_size;  // level-local
+                        p.scatter.keys[slot] = scatter_key(base[k], lv, p.grid.table_size);
                         p.scatter.vals[slot] = make_float2(w[k] * da[2 * lv], w[k] * da[2 * lv + 1]);
                     }
                 }
@@ -426,7 +434,7 @@ __global__ void __launch_bounds__(256, NRRS_TRAIN_MINB) stat_fwd_bwd_fast_kernel
                     for (int k = 0; k < 8; ++k) {
                         const uint64_t slot = ((uint64_t)lv * p.n + s) * 8u + (uint64_t)k;  // level-major
                         NRRS_CHECK(slot < p.n * (uint64_t)p.grid.levels * 8u, "scatter slot", slot, p.n * (uint64_t)p.grid.levels * 8u);
-                        p.scatter.keys[slot] = base[k] - 2u * (uint32_t)lv * p.grid.table_size;  // level-local
+                        p.scatter.keys[slot] = scatter_key(base[k], lv, p.grid.table_size);
                         p.scatter.vals[slot] = make_float2(w[k] * da[2 * lv], w[k] * da[2 * lv + 1]);
                     }
                 }
@@ -833,7 +841,7 @@ __global__ void __launch_bounds__(256) rrs_fwd_bwd_kernel(RrsStepParams p) {
                     for (int k = 0; k < 8; ++k) {
                         const uint64_t slot = ((uint64_t)lv * p.n + s) * 8u + (uint64_t)k;  // level-major
                         NRRS_CHECK(slot < p.n * (uint64_t)p.grid.levels * 8u, "scatter slot", slot, p.n * (uint64_t)p.grid.levels * 8u);
-                        p.scatter.keys[slot] = base[k] - 2u * (uint32_t)lv * p.grid.table_size;  // level-local
+                        p.scatter.keys[slot] = scatter_key(base[k], lv, p.grid.table_size);
                         p.scatter.vals[slot] = make_float2(w[k] * da[2 * lv], w[k] * da[2 * lv + 1]);
                     }
                 }
@@ -1080,7 +1088,7 @@ __global__ void __launch_bounds__(256, NRRS_TRAIN_MINB) rrs_fwd_bwd_fast_kernel(
                     for (int k = 0; k < 8; ++k) {
                         const uint64_t slot = ((uint64_t)lv * p.n + s) * 8u + (uint64_t)k;  // level-major
                         NRRS_CHECK(slot < p.n * (uint64_t)p.grid.levels * 8u, "scatter slot", slot, p.n * (uint64_t)p.grid.levels * 8u);
-                        p.scatter.keys[slot] = base[k] - 2u * (uint32_t)lv * p.grid.table_size;  // level-local
+                        p.scatter.keys[slot] = scatter_key(base[k], lv, p.grid.table_size);
                         p.scatter.vals[slot] = make_float2(w[k] * da[2 * lv], w[k] * da[2 * lv + 1]);
                     }
                 }
@@ -1162,6 +1170,11 @@ struct FoldRun {
     uint32_t key;  // 0xFFFFFFFF: none
     float a0, a1;
 };
+__device__ __forceinline__ uint32_t fold_offset(const GridScatter &sc, uint32_t key) {
+    if (key == 0xFFFFFFFFu)
+        return key;
+    return (key >> sc.key_shift) * sc.level_stride + (key & ((1u << sc.key_shift) - 1u));
+}
 __device__ __forceinline__ void fold_flush(float *g_grid, const GridScatter &sc, uint32_t key, float a0, float a1) {
     if (key == 0xFFFFFFFFu)
         return;  // slots that contributed nothing sort last under the sentinel key
@@ -1196,20 +1209,13 @@ __global__ void __launch_bounds__(256) grid_scatter_fold_kernel(GridScatter sc, 
             v[e] = i0 + e < m ? sc.vals_sorted[i0 + e] : make_float2(0.0f, 0.0f);
         }
     }
-    // level-local keys -> gradient offsets (a lane's 8 elements lie in one level: seg is a multiple
-    // of 8); the sentinel stays the sentinel
-    const uint32_t lv_off = (uint32_t)(i0 / sc.seg) * sc.level_stride;
+    // scatter keys -> gradient offsets; the sentinel stays the sentinel
 #pragma unroll
     for (int e = 0; e < kFoldE; ++e)
-        k[e] = k[e] == 0xFFFFFFFFu ? k[e] : k[e] + lv_off;
+        k[e] = fold_offset(sc, k[e]);
     uint32_t pk = __shfl_up_sync(0xffffffffu, k[kFoldE - 1], 1);
-    if (lane == 0) {
-        pk = 0xFFFFFFFEu;
-        if (b > 0) {
-            const uint32_t kb = sc.keys_sorted[b - 1];
-            pk = kb == 0xFFFFFFFFu ? kb : kb + (uint32_t)((b - 1) / sc.seg) * sc.level_stride;
-        }
-    }
+    if (lane == 0)
+        pk = b > 0 ? fold_offset(sc, sc.keys_sorted[b - 1]) : 0xFFFFFFFEu;
     // first run start in the lane (kFoldE: none) and the runs that start here, in order
     int fs = kFoldE;
 #pragma unroll
@@ -1271,20 +1277,18 @@ __global__ void __launch_bounds__(256) grid_scatter_fold_kernel(GridScatter sc, 
     // the run open at the window's end continues into the next window(s), up to its level's end
     if (lane == 31 && out.key != 0xFFFFFFFFu) {
         float a0 = out.a0, a1 = out.a1;
-        const uint64_t lv = i0 / sc.seg, lv_end = min(m, (lv + 1) * sc.seg);
-        const uint32_t local = out.key - (uint32_t)lv * sc.level_stride;
         for (uint64_t j = b + kFoldWin;; j += 4) {
             uint32_t kk[4];
             float2 vv[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                kk[u] = j + u < lv_end ? sc.keys_sorted[j + u] : 0xFFFFFFFFu;
-                vv[u] = j + u < lv_end ? sc.vals_sorted[j + u] : make_float2(0.0f, 0.0f);
+                kk[u] = j + u < m ? fold_offset(sc, sc.keys_sorted[j + u]) : 0xFFFFFFFFu;
+                vv[u] = j + u < m ? sc.vals_sorted[j + u] : make_float2(0.0f, 0.0f);
             }
             bool more = true;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                more = more && kk[u] == local;
+                more = more && kk[u] == out.key;
                 if (more) {
                     a0 = __fadd_rn(a0, vv[u].x);
                     a1 = __fadd_rn(a1, vv[u].y);
