@@ -214,8 +214,10 @@ def run_reference(args):
                                    f"(full batch each step)",
                        "n_pixels": args.vertices, "strategy": f"{args.variant}-nrrs", "depth": 2},
             "cpu_baseline": {"value": value, "unit": "vertices/s", "cores": threads, "kind": "port", "host": host_cpu(),
-                             "sample": f"the full {sample}-vertex batch per step; the reference does not build here "
-                                       "(Eigen absent): C restatement of the reference path"},
+                             "sample": f"the full {sample}-vertex batch per step; C restatement of the reference "
+                                       "path (the reference's network code builds here only against this repo's "
+                                       "Eigen-subset shim -- a correctness pin, not a performance-representative "
+                                       "build of the reference)"},
             "e2e": {"value": value, "unit": "vertices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     if world > 1:
