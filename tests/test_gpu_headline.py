@@ -119,6 +119,13 @@ def test_adrrs_nn_headline_size_parity():
     assert res.nonfinite == ref["nonfinite"]
     flips = np.count_nonzero(_np(out.k) != ref["k"])
     assert flips <= max(3, n // 2000), f"{flips} count flips"
+    # the decision chain on the GPU's own factors: bit-exact against the oracle's chain
+    dec = oracle_decide(_np(out.q_orig), _np(out.u), n, cap, 0.85)
+    assert np.float32(res.f_norm) == np.float32(dec["f_norm"])
+    np.testing.assert_array_equal(_np(out.q_norm), dec["q_norm"])
+    np.testing.assert_array_equal(_np(out.k), dec["k"])
+    assert res.spawned == dec["spawned"] and res.dropped == dec["dropped"]
+    np.testing.assert_array_equal(_np(out.slots)[:res.spawned].view(np.uint32), dec["slots"])
     st.close()
 
 
