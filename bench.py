@@ -943,7 +943,7 @@ def main():
                                 + ("; N=8 is the configs[4] 16.6 M-vertex batch" if world > 1 else "")),
                    "vertices_per_gpu": n, "n_pixels": npx, "capacity": cap, "strategy": f"{args.variant}-nrrs",
                    "depth": 2, "gain": 0.85, "parallelism": f"tile-sharded dp{world}",
-                   "exchange": (exchange if world > 1 else "none"),
+                   "exchange": (exchange if world > 1 or force_sharded else "none"),
                    "l2": "flushed between timed steps (256 MiB write outside the events)",
                    "aid_tables": aid_tables},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
