@@ -1009,6 +1009,7 @@ def main():
         print(json.dumps(line))
     if world > 1:
         dist.barrier()
+    if world > 1 or force_sharded:
         dist.destroy_process_group()
 
 
